@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark: particle current deposits/s on B200 (BASELINE.json metric).
+
+Workload (N=1): BASELINE configs[1] ("C2"): 128^3 cells, 16 particles/cell,
+order 3 (QSP), Maxwellian u_th = 0.01c, dt = 0.5, seeded synthetic plasma
+(SURVEY 8(d) generator, generated in HBM).  One STEP = the reference's step
+(simulation.hpp:753-829): bit-exact push -> incremental cell sort (bins with
+slack, migration) -> current deposition J.  Inputs stay resident in HBM.
+
+value  = particles * steps * n_gpus / (max over ranks of the device time of K steps)
+e2e    = the same metric through the stateless C-ABI drop-in for
+         pic::deposit_scalar (picgpu_deposit_current) on pinned HOST buffers:
+         H2D of the 7 particle arrays + sort + deposit + D2H of J every step.
+roofline: the J kernel (dominant), timed with CUDA events on the session's
+         stream inside the timed region.  Order 3 is FP64-bound: achieved =
+         particles * 534 flops (reference tally, deposit.hpp:336-345) / launch
+         time, against the FP64 peak measured in-run by a DFMA microbenchmark
+         (MEASURED_PEAKS.json has no FP64 figure); the HBM view (56 + 24/ppc
+         bytes per deposit vs MEASURED_PEAKS hbm_gbs) is reported beside it.
+cpu_baseline: the reference's own step (oracle/_ref: advance + detect_moves +
+         apply_pending_moves + deposit_scalar), all host threads, each thread
+         an independent 32^3 x 16 ppc sub-box (bounded sample).
+
+--impl reference runs only that CPU arm and prints its line.
+Multi-GPU (torchrun, N>1): each rank runs an independent C2 box (replicas,
+weak scaling); slab decomposition with guard exchange is not implemented yet.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n, ppc, order, u_th, dt, default steps, description)
+    "c1": (64, 8, 1, 0.01, 0.5, 10, "C1: 64^3 cells, 8 ppc, order 1 (CIC), u_th 0.01, dt 0.5"),
+    "c2": (128, 16, 3, 0.01, 0.5, 20, "C2: 128^3 cells, 16 ppc, order 3 (QSP), u_th 0.01, dt 0.5"),
+    "c3o1": (256, 32, 1, 0.1, 0.5, 5, "C3: 256^3 cells, 32 ppc, order 1, u_th 0.1, dt 0.5"),
+    "c3o2": (256, 32, 2, 0.1, 0.5, 5, "C3: 256^3 cells, 32 ppc, order 2 (TSC), u_th 0.1, dt 0.5"),
+    "c3o3": (256, 32, 3, 0.1, 0.5, 5, "C3: 256^3 cells, 32 ppc, order 3, u_th 0.1, dt 0.5"),
+}
+METRIC = "particle current deposits/sec"
+UNIT = "deposits/s"
+FLOPS = {1: 76, 2: 238, 3: 534}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference(order, ppc, u_th, dt, steps, threads, nx=32, seed=1):
+    """The reference's own step on `threads` independent sub-boxes (oracle/_ref)."""
+    import oracle
+
+    if not oracle.reference_available():
+        return None
+    L = oracle.Reference().L
+    L.ref_bench_steps.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_double, C.c_int, C.c_int,
+                                  C.c_void_p, C.c_void_p]
+    sec, n = C.c_double(), C.c_uint64()
+    if order not in (1, 3):  # the reference has no order 2: time its QSP kernel as the stand-in
+        order = 3
+    rc = L.ref_bench_steps(nx, ppc, u_th, seed, order, dt, steps, threads, C.byref(sec), C.byref(n))
+    if rc:
+        raise RuntimeError(L.ref_last_error().decode())
+    return n.value * threads * steps / sec.value, n.value, sec.value
+
+
+def run_reference_arm(args, cfgname):
+    nx, ppc, order, u_th, dt, _, desc = CONFIGS[cfgname]
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    W, K = args.warmup, args.steps
+    if W:
+        cpu_reference(order, ppc, u_th, dt, W, threads)
+    r = cpu_reference(order, ppc, u_th, dt, K, threads)
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpicref.so not built"}))
+        return 0
+    value, nsub, sec = r
+    sample = (f"{threads} threads x independent 32^3 x {ppc} ppc periodic sub-boxes ({nsub} particles each), "
+              f"reference baseline-incrsort step (advance + detect_moves + apply_pending_moves + deposit_scalar "
+              f"order {order if order != 2 else 3})")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": K, "warmup": W,
+        "ms_per_step": sec / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (SURVEY 8(d) generator, reference counter RNG)",
+        "config": {"workload": desc, "grid": [nx] * 3, "ppc": ppc, "order": order},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def load_traffic(order):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"order{order}")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    nx, ppc, order, u_th, dt, default_steps, desc = CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = default_steps
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args, args.config)
+
+    import numpy as np
+    import torch
+
+    import paper_2601_08277_b200 as pg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    grid = pg.Grid.make(nx)
+    S = pg.Session(grid, order=order, device=local, timing=True)
+    S.generate_plasma(ppc, u_th, seed=1 + rank)
+    n = S.num_particles
+    stream = torch.cuda.ExternalStream(S.stream)
+    for _ in range(args.warmup):
+        S.step(dt)
+    S.reset_phase_times()
+    barrier()
+    launches0 = pg.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    moved = 0
+    rebuilds = 0
+    with Clocks(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            st = S.step(dt)
+            moved += st["moved"]
+            rebuilds += st["rebuilt"]
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+    launches = pg.kernel_launches() - launches0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = n * args.steps * world / (ms_max * 1e-3)
+    phases = S.phase_times()
+    j_ms, j_launches = phases["deposit_current"]
+    j_avg_s = j_ms / max(j_launches, 1) * 1e-3
+
+    # roofline of the dominant kernel (J deposition)
+    hbm_peak, hbm_src = peaks()
+    bytes_per = 56 + 24 / ppc
+    hbm_achieved = n * bytes_per / j_avg_s / 1e9
+    fp64_peak = pg.fp64_peak_tflops(local)
+    fp64_achieved = n * FLOPS[order] / j_avg_s / 1e12
+    frac_hbm = hbm_achieved / hbm_peak
+    frac_fp64 = fp64_achieved / fp64_peak
+    traffic = load_traffic(order)
+    if frac_fp64 >= frac_hbm:
+        roof = {"bound": "fp64", "achieved": fp64_achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": frac_fp64, "traffic": traffic,
+                "peak_source": "measured in-run (DFMA microbenchmark, picgpu_fp64_peak)",
+                "flops_per_deposit": FLOPS[order]}
+    else:
+        roof = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s", "frac": frac_hbm,
+                "traffic": traffic, "peak_source": hbm_src, "bytes_per_deposit": bytes_per}
+    roof.update({"kernel": "deposit_current_kernel", "launch_ms": j_avg_s * 1e3,
+                 "hbm_view": {"achieved_gbs": hbm_achieved, "peak_gbs": hbm_peak, "frac": frac_hbm},
+                 "fp64_view": {"achieved_tflops": fp64_achieved, "peak_tflops": fp64_peak, "frac": frac_fp64},
+                 "deposits_per_s_kernel_only": n / j_avg_s})
+
+    # e2e through the stateless C-ABI drop-in, pinned host buffers
+    e2e = None
+    if rank == 0 or True:
+        p = S.particles()
+        host = {}
+        for k in ("x", "y", "z", "vx", "vy", "vz", "w"):
+            tt = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            tt.numpy()[:] = getattr(p, k)
+            host[k] = tt
+        outs = [torch.empty(grid.ncells, dtype=torch.float64, pin_memory=True) for _ in range(3)]
+        L = pg.lib()
+        ptr = lambda tt: C.c_void_p(tt.data_ptr())  # noqa: E731
+        q = -1.0
+
+        def call():
+            rc = L.picgpu_deposit_current(C.byref(grid), order, *(ptr(host[k]) for k in
+                                                                  ("x", "y", "z", "vx", "vy", "vz", "w")),
+                                          q, n, ptr(outs[0]), ptr(outs[1]), ptr(outs[2]))
+            if rc:
+                raise RuntimeError(L.picgpu_last_error().decode())
+
+        call()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            call()
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        tt = torch.tensor([e2e_s], device="cuda")
+        if dist is not None:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": n * args.e2e_steps * world / float(tt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": 7 * 8 * n, "d2h_bytes_per_step": 3 * 8 * grid.ncells,
+               "steps": args.e2e_steps, "api": "picgpu_deposit_current (drop-in for pic::deposit_scalar)",
+               "timer": "host wall clock around synchronous C-ABI calls (copies inside)"}
+    S.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        r = cpu_reference(order, ppc, u_th, dt, 3, threads)
+        if r is not None:
+            v, nsub, sec = r
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{threads} threads x independent 32^3 x {ppc} ppc sub-boxes ({nsub} particles each), "
+                             f"3 reference steps (advance + detect_moves + apply_pending_moves + deposit_scalar), "
+                             f"{sec:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY 8(d) seeded plasma generated in HBM; no dataset)",
+            "config": {"workload": desc + "; step = push + incremental sort + J deposit",
+                       "grid": [nx] * 3, "ppc": ppc, "order": order, "particles_per_gpu": n,
+                       "l2": f"inputs larger than L2 ({n * 64 / 1e9:.1f} GB particle store)",
+                       "parallelism": "single" if world == 1 else f"replicas x{world} (independent boxes)"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "phases_ms_total": {k: v[0] for k, v in phases.items()},
+            "moved_fraction": moved / (n * args.steps), "rebuilds": rebuilds,
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

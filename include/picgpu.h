@@ -1,0 +1,208 @@
+/*
+ * picgpu.h -- C ABI of the B200-native (sm_100a) MatrixPIC deposition + cell-sort path.
+ *
+ * Every entry point takes plain pointers and sizes; no torch or C++ types cross
+ * this boundary.  The C++ shim include/picgpu.hpp restores the reference's
+ * value-semantics API (namespace picgpu mirrors namespace pic) on top of it,
+ * and INTEGRATION.md shows the binding a maintainer adds to the reference.
+ *
+ * Reference interface each export replaces (paths under the reference tree
+ * proj/include/pic/):
+ *   picgpu_deposit_current   <- pic::deposit_scalar          deposit.hpp:62-73
+ *   picgpu_deposit_density   <- pic::deposit_density         deposit.hpp:76-83
+ *   picgpu_counting_sort     <- pic::gpma_build's counting sort (perm/starts/counts) gpma.hpp:379-394
+ *   picgpu_advance           <- pic::advance                 workload.hpp:139-155
+ *   picgpu_cell_of           <- pic::cell_of                 grid.hpp:106-113
+ *   picgpu_session_*         <- the run_simulation step loop simulation.hpp:753-829 with a
+ *                               device-resident pic::Gpma (gpma.hpp:52-371): gpma_build,
+ *                               detect_moves + apply_pending_moves, rebuild, global_sort
+ *                               (sort_policy.hpp:83), deposit_scalar / deposit_density.
+ *   picgpu_should_global_sort <- pic::should_global_sort     sort_policy.hpp:62-73
+ *
+ * Errors: every call returns a status.  The codes map one-to-one onto the
+ * exception types the reference throws; picgpu_last_error()
+ * returns a thread-local message for the last failing call on this thread.
+ */
+#ifndef PICGPU_H
+#define PICGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PICGPU_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PICGPU_API __attribute__((visibility("default")))
+#else
+#define PICGPU_API
+#endif
+
+enum picgpu_status {
+    PICGPU_OK = 0,
+    PICGPU_EINVAL = 1,  /* std::invalid_argument (non-finite position, bad order, grid < stencil) */
+    PICGPU_ERANGE = 2,  /* std::out_of_range */
+    PICGPU_ELENGTH = 3, /* std::length_error (slot capacity >= 2^32, gpma.hpp:279) */
+    PICGPU_ELOGIC = 4,  /* std::logic_error */
+    PICGPU_EDOMAIN = 5, /* std::domain_error (advance: displacement above the cap, workload.hpp:147) */
+    PICGPU_ECUDA = 6,   /* CUDA runtime failure (std::runtime_error in the shim) */
+    PICGPU_ENCCL = 7,   /* NCCL failure */
+    PICGPU_ENOMEM = 8   /* device allocation failure (std::bad_alloc in the shim) */
+};
+
+/* Periodic box (pic::GridSpec, grid.hpp:26-72).  Node arrays use the cell
+ * layout id = i + nx*(j + ny*k) (grid.hpp:50-54). */
+typedef struct picgpu_grid {
+    int32_t nx, ny, nz, pad_;
+    double dx, dy, dz;
+    double ox, oy, oz;
+} picgpu_grid;
+
+/* ---- library ----------------------------------------------------------- */
+PICGPU_API int picgpu_abi_version(void);
+PICGPU_API const char* picgpu_last_error(void);
+/* Number of this library's kernels launched since load (all entry points). */
+PICGPU_API uint64_t picgpu_kernel_launches(void);
+/* Reference flop tally per deposit (deposit.hpp:336-345): 76 / 238 / 534. */
+PICGPU_API int picgpu_flop_count(int order);
+
+/* ---- stateless, host buffers (synchronous, like the reference) --------- */
+/* J = sum_p q*W_p*v_p*S(x_i - x_p) at shape order 1, 2 or 3; jx/jy/jz hold
+ * ncells doubles each and are overwritten.  Order 2 is this project's TSC. */
+PICGPU_API int picgpu_deposit_current(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
+                           const double* vx, const double* vy, const double* vz, const double* w, double q,
+                           uint64_t n, double* jx, double* jy, double* jz);
+/* rho = one-component scatter of quantity[p] in STORAGE ORDER, bit-identical
+ * to pic::deposit_density on the same arrays. */
+PICGPU_API int picgpu_deposit_density(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
+                           const double* quantity, uint64_t n, double* rho);
+/* Stable counting sort by linear cell id: perm bit-identical to gpma_build's. */
+PICGPU_API int picgpu_counting_sort(const picgpu_grid* g, const double* x, const double* y, const double* z, uint64_t n,
+                         uint32_t* perm, uint32_t* bin_start, uint32_t* bin_count);
+/* Ballistic push x = wrap(x + v*dt), bit-identical to pic::advance. */
+PICGPU_API int picgpu_advance(const picgpu_grid* g, double dt, double* x, double* y, double* z, const double* vx,
+                   const double* vy, const double* vz, uint64_t n, uint64_t* moved);
+PICGPU_API int picgpu_cell_of(const picgpu_grid* g, const double* x, const double* y, const double* z, uint64_t n,
+                   uint32_t* cell);
+
+/* ---- stateless, device buffers (asynchronous on `stream`) -------------- */
+/* Inputs and outputs are device pointers; scratch is allocated internally.
+ * These are the hot-path entry points when particles already live in HBM. */
+PICGPU_API int picgpu_deposit_current_dev(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
+                               const double* vx, const double* vy, const double* vz, const double* w, double q,
+                               uint64_t n, double* jx, double* jy, double* jz, void* stream);
+
+/* ---- resort policy (host logic, sort_policy.hpp:12-79) ------------------ */
+typedef struct picgpu_sort_policy {
+    uint32_t sort_interval;         /* 50 */
+    uint32_t min_sort_interval;     /* 10 */
+    uint32_t trigger_rebuild_count; /* 100 */
+    uint32_t perf_enable;           /* 1 */
+    double trigger_empty_ratio;     /* 0.15 */
+    double trigger_full_ratio;      /* 0.85 */
+    double perf_degrad;             /* 0.80 */
+} picgpu_sort_policy;
+
+typedef struct picgpu_rank_sort_stats {
+    uint32_t steps_since_sort;
+    uint32_t pad_;
+    uint64_t cumulative_local_rebuilds;
+    double empty_slot_ratio;
+    double perf_metric;
+    double baseline_perf;
+    uint64_t total_inserts;
+    uint64_t total_shifts;
+} picgpu_rank_sort_stats;
+
+enum picgpu_sort_reason {
+    PICGPU_SORT_NONE = 0,
+    PICGPU_SORT_INTERVAL = 1,
+    PICGPU_SORT_REBUILDS = 2,
+    PICGPU_SORT_SLOT_RATIO = 3,
+    PICGPU_SORT_PERF = 4
+};
+
+PICGPU_API void picgpu_sort_policy_defaults(picgpu_sort_policy* p);
+PICGPU_API int picgpu_should_global_sort(const picgpu_rank_sort_stats* s, const picgpu_sort_policy* p);
+
+/* ---- device-resident session: bins-with-slack sorter + deposition ------ */
+typedef struct picgpu_session picgpu_session;
+
+typedef struct picgpu_session_config {
+    int32_t order;        /* 1, 2, 3 */
+    int32_t device;       /* CUDA device ordinal */
+    double gap_ratio;     /* GpmaConfig::gap_ratio (0.25) */
+    uint32_t min_gap;     /* GpmaConfig::min_gap (2) */
+    uint32_t flags;       /* PICGPU_SESSION_* */
+} picgpu_session_config;
+
+#define PICGPU_SESSION_TIMING 1u        /* record CUDA events around each phase */
+#define PICGPU_SESSION_DETERMINISTIC 2u /* canonical in-bin order of arrivals (sorted by id) */
+
+/* per-step flags */
+#define PICGPU_STEP_PUSH 1u       /* advance (bit-exact pic::advance) */
+#define PICGPU_STEP_SORT 2u       /* incremental sort (detect + migrate) */
+#define PICGPU_STEP_CURRENT 4u    /* deposit J */
+#define PICGPU_STEP_DENSITY 8u    /* deposit rho = q*W (bit-exact ordered gather) */
+#define PICGPU_STEP_GLOBAL_SORT 16u /* force a full re-sort (global_sort) after the deposit */
+#define PICGPU_STEP_NO_SYNC 32u   /* do not read back step stats (counts stay on device) */
+#define PICGPU_STEP_DEFAULT (PICGPU_STEP_PUSH | PICGPU_STEP_SORT | PICGPU_STEP_CURRENT)
+
+typedef struct picgpu_step_stats {
+    uint64_t moved;        /* particles whose cell changed (advance's moved count) */
+    uint64_t inserts;      /* migrated particles placed into bins */
+    uint64_t overflowed;   /* arrivals that found no slack -> rebuild */
+    uint32_t rebuilt;      /* 1 if this step rebuilt the bins */
+    uint32_t global_sorted;
+    double empty_slot_ratio;
+    uint64_t capacity;
+    uint64_t num_particles;
+} picgpu_step_stats;
+
+PICGPU_API int picgpu_session_create(const picgpu_grid* g, const picgpu_session_config* cfg, picgpu_session** out);
+PICGPU_API int picgpu_session_destroy(picgpu_session* s);
+/* Upload a particle store (host pointers) and build the bins: stable counting
+ * sort by cell + layout with slack = ceil(count*(1+gap_ratio)) + min_gap per
+ * bin (gpma_build, gpma.hpp:379-402, layout :269-302).  id may be NULL (ids =
+ * storage index).  Replaces any previous content. */
+PICGPU_API int picgpu_session_upload(picgpu_session* s, uint64_t n, const double* x, const double* y, const double* z,
+                          const double* vx, const double* vy, const double* vz, const double* w,
+                          const uint64_t* id, double q);
+/* Generate the SURVEY 8(d) seeded plasma directly in HBM (device-side
+ * generator on the reference counter RNG; inputs for benchmarks). */
+PICGPU_API int picgpu_session_generate_plasma(picgpu_session* s, int ppc, double u_th, uint64_t seed);
+/* One step: [push] -> [incremental sort] -> [deposit J] -> [deposit rho] -> [global sort]. */
+PICGPU_API int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_step_stats* out);
+PICGPU_API int picgpu_session_global_sort(picgpu_session* s);
+PICGPU_API int picgpu_session_synchronize(picgpu_session* s);
+PICGPU_API uint64_t picgpu_session_num_particles(picgpu_session* s);
+PICGPU_API uint64_t picgpu_session_capacity(picgpu_session* s);
+PICGPU_API void* picgpu_session_stream(picgpu_session* s);
+/* Downloads (synchronous).  Particles come out in storage order: bins
+ * ascending by cell, slot order within a bin (valid slots only, compacted). */
+PICGPU_API int picgpu_session_download_particles(picgpu_session* s, double* x, double* y, double* z, double* vx, double* vy,
+                                      double* vz, double* w, uint64_t* id);
+PICGPU_API int picgpu_session_download_bins(picgpu_session* s, uint32_t* bin_offset, uint32_t* bin_count);
+PICGPU_API int picgpu_session_download_current(picgpu_session* s, double* jx, double* jy, double* jz);
+PICGPU_API int picgpu_session_download_density(picgpu_session* s, double* rho);
+/* Device pointers of J (3*ncells doubles, jx|jy|jz) and rho (ncells). */
+PICGPU_API int picgpu_session_device_fields(picgpu_session* s, double** j, double** rho);
+/* Accumulated per-phase device times (ms) and launch counts since the last
+ * reset, recorded only with PICGPU_SESSION_TIMING.  Phases:
+ * 0 push+detect, 1 migrate (compact+insert), 2 rebuild/global sort, 3 deposit J,
+ * 4 deposit rho, 5 zero fields. */
+#define PICGPU_NPHASES 6
+PICGPU_API int picgpu_session_phase_times(picgpu_session* s, double* ms, uint64_t* launches, int nphases);
+PICGPU_API int picgpu_session_reset_phase_times(picgpu_session* s);
+
+/* ---- microbenchmarks (roofline denominators measured in-run) ------------ */
+/* Runs a dependent-free DFMA loop on all SMs; returns measured FP64 TFLOP/s. */
+PICGPU_API int picgpu_fp64_peak(int device, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PICGPU_H */

@@ -1,0 +1,457 @@
+"""picgpu -- B200-native (sm_100a) MatrixPIC deposition + cell sorter.
+
+Python mirror of the reference's `pic::` interface for the hot path, over the
+C ABI in include/picgpu.h (ctypes; no torch types cross the boundary).  Names
+and argument meaning follow the reference headers under proj/include/pic/:
+
+    deposit_scalar(soa, grid, order)            deposit.hpp:62-73
+    deposit_density(soa, grid, order, quantity) deposit.hpp:76-83
+    counting_sort(soa, grid)                    gpma.hpp:379-394 (perm, starts, counts)
+    gpma_build(soa, grid, cfg)                  gpma.hpp:379-402 (permutes soa in place)
+    advance(soa, dt, grid)                      workload.hpp:139-155
+    cell_of(pos, grid)                          grid.hpp:106-113
+    should_global_sort(stats, policy)           sort_policy.hpp:62-73
+    Session                                     run_simulation's step loop on a device-resident Gpma
+
+Errors raise the Python analogue of the reference's exception type.  The
+product path has no CPU fallback: importing works anywhere, but every compute
+call goes through libpicgpu.so and fails loudly without a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpicgpu.so")
+
+CIC, TSC, QSP = 1, 2, 3
+
+OK, EINVAL, ERANGE, ELENGTH, ELOGIC, EDOMAIN, ECUDA, ENCCL, ENOMEM = range(9)
+
+STEP_PUSH, STEP_SORT, STEP_CURRENT, STEP_DENSITY, STEP_GLOBAL_SORT, STEP_NO_SYNC = 1, 2, 4, 8, 16, 32
+STEP_DEFAULT = STEP_PUSH | STEP_SORT | STEP_CURRENT
+SESSION_TIMING = 1
+PHASES = ("push_detect", "migrate", "rebuild_or_global_sort", "deposit_current", "deposit_density", "zero_fields")
+
+
+class PicError(RuntimeError):
+    code = -1
+
+
+class InvalidArgument(PicError, ValueError):  # std::invalid_argument
+    code = EINVAL
+
+
+class OutOfRange(PicError, IndexError):  # std::out_of_range
+    code = ERANGE
+
+
+class LengthError(PicError, ValueError):  # std::length_error
+    code = ELENGTH
+
+
+class LogicError(PicError):  # std::logic_error
+    code = ELOGIC
+
+
+class DomainError(PicError, ArithmeticError):  # std::domain_error
+    code = EDOMAIN
+
+
+class CudaError(PicError):
+    code = ECUDA
+
+
+class NcclError(PicError):
+    code = ENCCL
+
+
+class DeviceOutOfMemory(PicError, MemoryError):
+    code = ENOMEM
+
+
+_ERRORS = {c.code: c for c in (InvalidArgument, OutOfRange, LengthError, LogicError, DomainError, CudaError,
+                                NcclError, DeviceOutOfMemory)}
+
+
+class Grid(C.Structure):
+    """picgpu_grid == pic::GridSpec (grid.hpp:26-72), periodic on every axis."""
+
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("pad_", C.c_int32),
+                ("dx", C.c_double), ("dy", C.c_double), ("dz", C.c_double),
+                ("ox", C.c_double), ("oy", C.c_double), ("oz", C.c_double)]
+
+    @classmethod
+    def make(cls, nx, ny=None, nz=None, dx=1.0, dy=1.0, dz=1.0, origin=(0.0, 0.0, 0.0)):
+        ny = nx if ny is None else ny
+        nz = nx if nz is None else nz
+        return cls(nx, ny, nz, 0, dx, dy, dz, *origin)
+
+    @property
+    def ncells(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def linear_id(self, i, j, k):  # grid.hpp:50-54
+        return i + self.nx * (j + self.ny * k)
+
+
+GridSpec = Grid
+
+
+class StepStats(C.Structure):
+    _fields_ = [("moved", C.c_uint64), ("inserts", C.c_uint64), ("overflowed", C.c_uint64),
+                ("rebuilt", C.c_uint32), ("global_sorted", C.c_uint32), ("empty_slot_ratio", C.c_double),
+                ("capacity", C.c_uint64), ("num_particles", C.c_uint64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class SessionConfig(C.Structure):
+    _fields_ = [("order", C.c_int32), ("device", C.c_int32), ("gap_ratio", C.c_double), ("min_gap", C.c_uint32),
+                ("flags", C.c_uint32)]
+
+
+class SortPolicy(C.Structure):
+    """pic::SortPolicy (sort_policy.hpp:12-30); defaults are Table 4's."""
+
+    _fields_ = [("sort_interval", C.c_uint32), ("min_sort_interval", C.c_uint32),
+                ("trigger_rebuild_count", C.c_uint32), ("perf_enable", C.c_uint32),
+                ("trigger_empty_ratio", C.c_double), ("trigger_full_ratio", C.c_double),
+                ("perf_degrad", C.c_double)]
+
+    @classmethod
+    def defaults(cls, **kw):
+        p = cls()
+        lib().picgpu_sort_policy_defaults(C.byref(p))
+        for k, v in kw.items():
+            setattr(p, k, v)
+        return p
+
+
+class RankSortStats(C.Structure):
+    """pic::RankSortStats (sort_policy.hpp:35-44)."""
+
+    _fields_ = [("steps_since_sort", C.c_uint32), ("pad_", C.c_uint32), ("cumulative_local_rebuilds", C.c_uint64),
+                ("empty_slot_ratio", C.c_double), ("perf_metric", C.c_double), ("baseline_perf", C.c_double),
+                ("total_inserts", C.c_uint64), ("total_shifts", C.c_uint64)]
+
+
+SORT_REASONS = ("none", "interval", "rebuilds", "slot_ratio", "perf_degradation")
+
+_lib = None
+_P = C.c_void_p
+_D = C.c_double
+_U64 = C.c_uint64
+
+
+def lib():
+    """Load libpicgpu.so (the sm_100a build); there is no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    G = C.POINTER(Grid)
+    L.picgpu_last_error.restype = C.c_char_p
+    L.picgpu_kernel_launches.restype = _U64
+    L.picgpu_deposit_current.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, _P, _P, _P]
+    L.picgpu_deposit_current_dev.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, _P, _P, _P, _P]
+    L.picgpu_deposit_density.argtypes = [G, C.c_int, _P, _P, _P, _P, _U64, _P]
+    L.picgpu_counting_sort.argtypes = [G, _P, _P, _P, _U64, _P, _P, _P]
+    L.picgpu_advance.argtypes = [G, _D, _P, _P, _P, _P, _P, _P, _U64, _P]
+    L.picgpu_cell_of.argtypes = [G, _P, _P, _P, _U64, _P]
+    L.picgpu_sort_policy_defaults.argtypes = [C.POINTER(SortPolicy)]
+    L.picgpu_sort_policy_defaults.restype = None
+    L.picgpu_should_global_sort.argtypes = [C.POINTER(RankSortStats), C.POINTER(SortPolicy)]
+    L.picgpu_session_create.argtypes = [G, C.POINTER(SessionConfig), C.POINTER(_P)]
+    L.picgpu_session_destroy.argtypes = [_P]
+    L.picgpu_session_upload.argtypes = [_P, _U64] + [_P] * 8 + [_D]
+    L.picgpu_session_generate_plasma.argtypes = [_P, C.c_int, _D, _U64]
+    L.picgpu_session_step.argtypes = [_P, _D, C.c_uint32, C.POINTER(StepStats)]
+    L.picgpu_session_global_sort.argtypes = [_P]
+    L.picgpu_session_synchronize.argtypes = [_P]
+    L.picgpu_session_num_particles.argtypes = [_P]
+    L.picgpu_session_num_particles.restype = _U64
+    L.picgpu_session_capacity.argtypes = [_P]
+    L.picgpu_session_capacity.restype = _U64
+    L.picgpu_session_stream.argtypes = [_P]
+    L.picgpu_session_stream.restype = _P
+    L.picgpu_session_download_particles.argtypes = [_P] * 9
+    L.picgpu_session_download_bins.argtypes = [_P, _P, _P]
+    L.picgpu_session_download_current.argtypes = [_P, _P, _P, _P]
+    L.picgpu_session_download_density.argtypes = [_P, _P]
+    L.picgpu_session_device_fields.argtypes = [_P, C.POINTER(_P), C.POINTER(_P)]
+    L.picgpu_session_phase_times.argtypes = [_P, _P, _P, C.c_int]
+    L.picgpu_session_reset_phase_times.argtypes = [_P]
+    L.picgpu_fp64_peak.argtypes = [C.c_int, C.POINTER(_D)]
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc:
+        msg = lib().picgpu_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, PicError)(msg)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_P)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def kernel_launches() -> int:
+    return int(lib().picgpu_kernel_launches())
+
+
+def flop_count(order: int) -> int:
+    """deposit.hpp:336-345 tally (76 / 534), 238 for this project's TSC."""
+    return lib().picgpu_flop_count(order)
+
+
+@dataclass
+class ParticleSoA:
+    """pic::ParticleSoA (particles.hpp:14-19)."""
+
+    x: np.ndarray
+    y: np.ndarray
+    z: np.ndarray
+    vx: np.ndarray
+    vy: np.ndarray
+    vz: np.ndarray
+    w: np.ndarray
+    id: np.ndarray = None
+    q: float = 1.0
+
+    def __post_init__(self):
+        for k in ("x", "y", "z", "vx", "vy", "vz", "w"):
+            setattr(self, k, _f64(getattr(self, k)))
+        if self.id is None:
+            self.id = np.arange(len(self.x), dtype=np.uint64)
+        self.id = np.ascontiguousarray(self.id, dtype=np.uint64)
+
+    @classmethod
+    def from_dict(cls, d, q=None):
+        return cls(d["x"], d["y"], d["z"], d["vx"], d["vy"], d["vz"], d["w"], d.get("id"),
+                   d.get("q", 1.0) if q is None else q)
+
+    def size(self):
+        return len(self.x)
+
+    def apply_permutation(self, perm):  # particles.hpp:34-47
+        for k in ("x", "y", "z", "vx", "vy", "vz", "w", "id"):
+            setattr(self, k, np.ascontiguousarray(getattr(self, k)[perm]))
+
+
+@dataclass
+class CurrentGrid:
+    """pic::CurrentGrid (grid.hpp:127-150)."""
+
+    spec: Grid
+    jx: np.ndarray
+    jy: np.ndarray
+    jz: np.ndarray
+
+    def component(self, c):
+        return (self.jx, self.jy, self.jz)[c]
+
+    def component_sums(self):
+        return [float(np.sum(a)) for a in (self.jx, self.jy, self.jz)]
+
+
+def _soa(soa, q=None):
+    if isinstance(soa, ParticleSoA):
+        return soa
+    return ParticleSoA.from_dict(soa, q)
+
+
+def deposit_scalar(soa, grid: Grid, order: int, q: float | None = None) -> CurrentGrid:
+    """Current deposition at order 1/2/3 (deposit_scalar, deposit.hpp:62-73)."""
+    s = _soa(soa, q)
+    qq = s.q if q is None else q
+    nc = grid.ncells
+    jx, jy, jz = np.empty(nc), np.empty(nc), np.empty(nc)
+    _check(lib().picgpu_deposit_current(C.byref(grid), order, _ptr(s.x), _ptr(s.y), _ptr(s.z), _ptr(s.vx),
+                                        _ptr(s.vy), _ptr(s.vz), _ptr(s.w), qq, s.size(), _ptr(jx), _ptr(jy),
+                                        _ptr(jz)))
+    return CurrentGrid(grid, jx, jy, jz)
+
+
+def deposit_density(soa, grid: Grid, order: int, quantity) -> np.ndarray:
+    """One-component deposition in storage order, bit-identical (deposit.hpp:76-83)."""
+    s = _soa(soa)
+    qv = _f64(quantity)
+    if len(qv) != s.size():
+        raise InvalidArgument("deposit_density: quantity length mismatch")
+    rho = np.empty(grid.ncells)
+    _check(lib().picgpu_deposit_density(C.byref(grid), order, _ptr(s.x), _ptr(s.y), _ptr(s.z), _ptr(qv),
+                                        s.size(), _ptr(rho)))
+    return rho
+
+
+def counting_sort(soa, grid: Grid):
+    """Stable counting sort by cell: (perm, starts, counts), perm == gpma_build's."""
+    s = _soa(soa)
+    n = s.size()
+    perm = np.empty(n, np.uint32)
+    starts = np.empty(grid.ncells, np.uint32)
+    counts = np.empty(grid.ncells, np.uint32)
+    _check(lib().picgpu_counting_sort(C.byref(grid), _ptr(s.x), _ptr(s.y), _ptr(s.z), n, _ptr(perm),
+                                      _ptr(starts), _ptr(counts)))
+    return perm, starts, counts
+
+
+def gpma_build(soa: ParticleSoA, grid: Grid):
+    """gpma_build's physical stable sort of the store (gpma.hpp:379-395).
+    Returns (starts, counts) of the packed bins; the store is permuted in place."""
+    perm, starts, counts = counting_sort(soa, grid)
+    soa.apply_permutation(perm)
+    return starts, counts
+
+
+def advance(soa: ParticleSoA, dt: float, grid: Grid) -> float:
+    """Ballistic push with periodic wrap, in place; returns the moved fraction."""
+    n = soa.size()
+    moved = np.zeros(1, np.uint64)
+    _check(lib().picgpu_advance(C.byref(grid), dt, _ptr(soa.x), _ptr(soa.y), _ptr(soa.z), _ptr(soa.vx),
+                                _ptr(soa.vy), _ptr(soa.vz), n, _ptr(moved)))
+    return float(moved[0]) / n if n else 0.0
+
+
+def cells(soa, grid: Grid) -> np.ndarray:
+    s = _soa(soa)
+    out = np.empty(s.size(), np.uint32)
+    _check(lib().picgpu_cell_of(C.byref(grid), _ptr(s.x), _ptr(s.y), _ptr(s.z), s.size(), _ptr(out)))
+    return out
+
+
+def cell_of(pos, grid: Grid) -> int:
+    x, y, z = (np.array([v], np.float64) for v in pos)
+    out = np.empty(1, np.uint32)
+    _check(lib().picgpu_cell_of(C.byref(grid), _ptr(x), _ptr(y), _ptr(z), 1, _ptr(out)))
+    return int(out[0])
+
+
+def should_global_sort(stats: RankSortStats, policy: SortPolicy | None = None) -> str:
+    policy = policy or SortPolicy.defaults()
+    return SORT_REASONS[lib().picgpu_should_global_sort(C.byref(stats), C.byref(policy))]
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    out = C.c_double(0.0)
+    _check(lib().picgpu_fp64_peak(device, C.byref(out)))
+    return out.value
+
+
+class Session:
+    """Device-resident particles in cell bins with slack + deposition fields.
+
+    One step = [advance] -> [incremental sort] -> [deposit J] -> [deposit rho]
+    -> [global sort], the reference's run_simulation order (simulation.hpp:753-829).
+    """
+
+    def __init__(self, grid: Grid, order: int = QSP, gap_ratio: float = 0.25, min_gap: int = 2, device: int = 0,
+                 timing: bool = False):
+        self.grid = grid
+        self.order = order
+        cfg = SessionConfig(order, device, gap_ratio, min_gap, SESSION_TIMING if timing else 0)
+        h = _P()
+        _check(lib().picgpu_session_create(C.byref(grid), C.byref(cfg), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().picgpu_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def upload(self, soa, q=None):
+        s = _soa(soa, q)
+        _check(lib().picgpu_session_upload(self._h, s.size(), _ptr(s.x), _ptr(s.y), _ptr(s.z), _ptr(s.vx),
+                                           _ptr(s.vy), _ptr(s.vz), _ptr(s.w), _ptr(s.id),
+                                           s.q if q is None else q))
+
+    def generate_plasma(self, ppc: int, u_th: float, seed: int = 1):
+        _check(lib().picgpu_session_generate_plasma(self._h, ppc, u_th, seed))
+
+    def step(self, dt: float = 0.5, flags: int = STEP_DEFAULT) -> dict:
+        st = StepStats()
+        _check(lib().picgpu_session_step(self._h, dt, flags, C.byref(st)))
+        return st.as_dict()
+
+    def global_sort(self):
+        _check(lib().picgpu_session_global_sort(self._h))
+
+    def synchronize(self):
+        _check(lib().picgpu_session_synchronize(self._h))
+
+    @property
+    def num_particles(self) -> int:
+        return int(lib().picgpu_session_num_particles(self._h))
+
+    @property
+    def capacity(self) -> int:
+        return int(lib().picgpu_session_capacity(self._h))
+
+    @property
+    def stream(self) -> int:
+        return int(lib().picgpu_session_stream(self._h) or 0)
+
+    def particles(self) -> ParticleSoA:
+        n = self.num_particles
+        a = {k: np.empty(n) for k in ("x", "y", "z", "vx", "vy", "vz", "w")}
+        ids = np.empty(n, np.uint64)
+        _check(lib().picgpu_session_download_particles(self._h, *(_ptr(a[k]) for k in
+                                                                  ("x", "y", "z", "vx", "vy", "vz", "w")),
+                                                       _ptr(ids)))
+        return ParticleSoA(id=ids, **a)
+
+    def bins(self):
+        off = np.empty(self.grid.ncells + 1, np.uint32)
+        cnt = np.empty(self.grid.ncells, np.uint32)
+        _check(lib().picgpu_session_download_bins(self._h, _ptr(off), _ptr(cnt)))
+        return off, cnt
+
+    def current(self) -> CurrentGrid:
+        nc = self.grid.ncells
+        jx, jy, jz = np.empty(nc), np.empty(nc), np.empty(nc)
+        _check(lib().picgpu_session_download_current(self._h, _ptr(jx), _ptr(jy), _ptr(jz)))
+        return CurrentGrid(self.grid, jx, jy, jz)
+
+    def density(self) -> np.ndarray:
+        rho = np.empty(self.grid.ncells)
+        _check(lib().picgpu_session_download_density(self._h, _ptr(rho)))
+        return rho
+
+    def device_fields(self):
+        j, r = _P(), _P()
+        lib().picgpu_session_device_fields(self._h, C.byref(j), C.byref(r))
+        return j.value, r.value
+
+    def phase_times(self):
+        ms = np.zeros(len(PHASES))
+        launches = np.zeros(len(PHASES), np.uint64)
+        lib().picgpu_session_phase_times(self._h, _ptr(ms), _ptr(launches), len(PHASES))
+        return {p: (float(m), int(l)) for p, m, l in zip(PHASES, ms, launches)}
+
+    def reset_phase_times(self):
+        lib().picgpu_session_reset_phase_times(self._h)

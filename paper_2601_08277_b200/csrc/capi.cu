@@ -1,0 +1,681 @@
+// capi.cu -- the C ABI (include/picgpu.h): stateless drop-ins for the
+// reference's deposition / sort / push functions and the device-resident
+// session that runs the reference's step loop (simulation.hpp:753-829) on HBM.
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "kernels.hpp"
+#include "store.hpp"
+
+namespace picgpu {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static thread_local std::string g_error;
+
+static int set_error(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+template <class F>
+static int guard(F&& f) {
+    try {
+        f();
+        return PICGPU_OK;
+    } catch (const Status& s) {
+        return set_error(s.code, s.msg ? s.msg : "error");
+    } catch (const CudaError& e) {
+        return set_error(PICGPU_ECUDA, std::string(e.what) + ": " + cudaGetErrorString(e.code));
+    } catch (const std::bad_alloc&) {
+        return set_error(PICGPU_ENOMEM, "host allocation failed");
+    } catch (...) {
+        return set_error(PICGPU_ELOGIC, "unexpected exception");
+    }
+}
+
+static bool is_pow2(double h) {
+    int e = 0;
+    return std::frexp(h, &e) == 0.5;
+}
+
+// GridSpec::validate (grid.hpp:32-36) + the derived constants.
+GridD make_grid(const picgpu_grid& h) {
+    if (h.nx < 1 || h.ny < 1 || h.nz < 1) throw Status{PICGPU_EINVAL, "grid: cell counts must be >= 1"};
+    if (!(h.dx > 0.0) || !(h.dy > 0.0) || !(h.dz > 0.0))
+        throw Status{PICGPU_EINVAL, "grid: cell sizes must be positive"};
+    const uint64_t nc = (uint64_t)h.nx * (uint64_t)h.ny * (uint64_t)h.nz;
+    if (nc >= 0xffffffffull) throw Status{PICGPU_ELENGTH, "grid: more than 2^32-1 cells"};
+    GridD g{};
+    g.nx = h.nx; g.ny = h.ny; g.nz = h.nz;
+    g.dx = h.dx; g.dy = h.dy; g.dz = h.dz;
+    g.ox = h.ox; g.oy = h.oy; g.oz = h.oz;
+    g.Lx = h.nx * h.dx;  // GridSpec::length: cells(axis) * spacing(axis)
+    g.Ly = h.ny * h.dy;
+    g.Lz = h.nz * h.dz;
+    g.pow2x = is_pow2(h.dx); g.pow2y = is_pow2(h.dy); g.pow2z = is_pow2(h.dz);
+    g.inv_dx = 1.0 / h.dx; g.inv_dy = 1.0 / h.dy; g.inv_dz = 1.0 / h.dz;
+    g.ncells = (uint32_t)nc;
+    return g;
+}
+
+static void check_order(int order) {
+    if (order < 1 || order > 3) throw Status{PICGPU_EINVAL, "shape order must be 1, 2 or 3"};
+}
+
+static int window(int order) { return order == 1 ? 2 : 4; }
+
+static void check_density_grid(const picgpu_grid& g, int order) {
+    const int W = window(order);
+    if (g.nx < W || g.ny < W || g.nz < W)
+        throw Status{PICGPU_EINVAL, "deposit_density: grid smaller than the shape window"};
+}
+
+// advance's displacement cap (workload.hpp:141): (min_spacing/dt)^2.
+static double cap2_of(const picgpu_grid& g, double dt) {
+    if (!(dt > 0.0)) throw Status{PICGPU_EINVAL, "advance: dt must be positive"};
+    const double ms = std::min(g.dx, std::min(g.dy, g.dz));
+    return (ms / dt) * (ms / dt);
+}
+
+__global__ void k_fill_ids(uint64_t* id, uint64_t n) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) id[p] = p;
+}
+
+__global__ void k_not_identity(const uint32_t* perm, uint64_t n, int* flag) {
+    const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n && perm[r] != (uint32_t)r) *flag = 1;
+}
+
+static void h2d(void* d, const void* h, size_t bytes, cudaStream_t st) {
+    if (bytes) PICGPU_CUDA_TRY(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+}
+static void d2h(void* h, const void* d, size_t bytes, cudaStream_t st) {
+    if (bytes && h) PICGPU_CUDA_TRY(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st));
+}
+
+static int current_sms() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+// Workspace of the stateless entry points (packed bins, gap 0 / min_gap 0).
+struct Stateless {
+    std::mutex mu;
+    cudaStream_t st = nullptr;
+    BinStore store;
+    DevBuf J, aux, flag;
+    picgpu_grid grid{};
+    bool ready = false;
+
+    void prepare(const picgpu_grid& g) {
+        if (!st) PICGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        if (!ready || std::memcmp(&g, &grid, sizeof g) != 0) {
+            store.init(g, 0.0, 0, st);
+            grid = g;
+            ready = true;
+        }
+        flag.ensure(16);
+    }
+};
+
+static Stateless& stateless() {
+    static Stateless* s = new Stateless;  // never destroyed (driver may be gone at exit)
+    return *s;
+}
+
+}  // namespace picgpu
+
+using namespace picgpu;
+
+// ===========================================================================
+// session
+
+struct picgpu_session {
+    int device = 0;
+    int order = 3;
+    uint32_t flags = 0;
+    double q = 1.0;
+    cudaStream_t st = nullptr;
+    BinStore store;
+    DevBuf J, rho, dscratch;
+    bool timing = false;
+    cudaEvent_t ev[8] = {};
+    double phase_ms[PICGPU_NPHASES] = {};
+    uint64_t phase_launches[PICGPU_NPHASES] = {};
+};
+
+static void set_device(const picgpu_session* s) { PICGPU_CUDA_TRY(cudaSetDevice(s->device)); }
+
+extern "C" {
+
+int picgpu_abi_version(void) { return PICGPU_ABI_VERSION; }
+const char* picgpu_last_error(void) { return g_error.c_str(); }
+uint64_t picgpu_kernel_launches(void) { return g_launches.load(); }
+
+int picgpu_flop_count(int order) {
+    if (order == 1) return 9 + 3 + 4 + 60;   // deposit.hpp:343-344
+    if (order == 3) return 9 + 57 + 4 + 464;
+    if (order == 2) return 9 + 27 + 4 + 9 + 7 * 27;  // this project's TSC tally (f_shape = 9)
+    return -1;
+}
+
+void picgpu_sort_policy_defaults(picgpu_sort_policy* p) {
+    p->sort_interval = 50;  // sort_policy.hpp:17-23
+    p->min_sort_interval = 10;
+    p->trigger_rebuild_count = 100;
+    p->perf_enable = 1;
+    p->trigger_empty_ratio = 0.15;
+    p->trigger_full_ratio = 0.85;
+    p->perf_degrad = 0.80;
+}
+
+// sort_policy.hpp:62-73, same priority order.
+int picgpu_should_global_sort(const picgpu_rank_sort_stats* s, const picgpu_sort_policy* p) {
+    if (s->steps_since_sort < p->min_sort_interval) return PICGPU_SORT_NONE;
+    if (s->steps_since_sort >= p->sort_interval) return PICGPU_SORT_INTERVAL;
+    if (s->cumulative_local_rebuilds > p->trigger_rebuild_count) return PICGPU_SORT_REBUILDS;
+    if (s->empty_slot_ratio < p->trigger_empty_ratio || s->empty_slot_ratio > p->trigger_full_ratio)
+        return PICGPU_SORT_SLOT_RATIO;
+    if (p->perf_enable && s->baseline_perf > 0.0 && s->perf_metric < p->perf_degrad * s->baseline_perf)
+        return PICGPU_SORT_PERF;
+    return PICGPU_SORT_NONE;
+}
+
+// ---- stateless -------------------------------------------------------------
+
+int picgpu_deposit_current(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
+                           const double* vx, const double* vy, const double* vz, const double* w, double q,
+                           uint64_t n, double* jx, double* jy, double* jz) {
+    return guard([&] {
+        check_order(order);
+        const GridD gd = make_grid(*g);
+        Stateless& S = stateless();
+        std::lock_guard<std::mutex> lk(S.mu);
+        S.prepare(*g);
+        BinStore& bs = S.store;
+        const cudaStream_t st = S.st;
+        bs.B.ensure(n);
+        const Soa b = bs.B.soa();
+        h2d(b.x, x, n * 8, st); h2d(b.y, y, n * 8, st); h2d(b.z, z, n * 8, st);
+        h2d(b.vx, vx, n * 8, st); h2d(b.vy, vy, n * 8, st); h2d(b.vz, vz, n * 8, st);
+        h2d(b.w, w, n * 8, st);
+        bs.full_sort_from_B(n);
+        S.J.ensure((size_t)gd.ncells * 24);
+        double* J = S.J.as<double>();
+        PICGPU_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)gd.ncells * 24, st));
+        if (n) launch_deposit_current(order, gd, bs.A.soa(), bs.d_off(), bs.d_cnt(), q, J, bs.num_sms, st);
+        d2h(jx, J, (size_t)gd.ncells * 8, st);
+        d2h(jy, J + gd.ncells, (size_t)gd.ncells * 8, st);
+        d2h(jz, J + 2 * (size_t)gd.ncells, (size_t)gd.ncells * 8, st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
+int picgpu_deposit_current_dev(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
+                               const double* vx, const double* vy, const double* vz, const double* w, double q,
+                               uint64_t n, double* jx, double* jy, double* jz, void* stream) {
+    return guard([&] {
+        check_order(order);
+        const GridD gd = make_grid(*g);
+        Stateless& S = stateless();
+        std::lock_guard<std::mutex> lk(S.mu);
+        S.prepare(*g);
+        BinStore& bs = S.store;
+        const cudaStream_t st = S.st;
+        cudaEvent_t ev;
+        PICGPU_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        PICGPU_CUDA_TRY(cudaEventRecord(ev, (cudaStream_t)stream));
+        PICGPU_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+        bs.B.ensure(n);
+        const Soa b = bs.B.soa();
+        const double* src[7] = {x, y, z, vx, vy, vz, w};
+        double* dst[7] = {b.x, b.y, b.z, b.vx, b.vy, b.vz, b.w};
+        for (int a = 0; a < 7; ++a)
+            if (n) PICGPU_CUDA_TRY(cudaMemcpyAsync(dst[a], src[a], n * 8, cudaMemcpyDeviceToDevice, st));
+        bs.full_sort_from_B(n);
+        S.J.ensure((size_t)gd.ncells * 24);
+        double* J = S.J.as<double>();
+        PICGPU_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)gd.ncells * 24, st));
+        if (n) launch_deposit_current(order, gd, bs.A.soa(), bs.d_off(), bs.d_cnt(), q, J, bs.num_sms, st);
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(jx, J, (size_t)gd.ncells * 8, cudaMemcpyDeviceToDevice, st));
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(jy, J + gd.ncells, (size_t)gd.ncells * 8, cudaMemcpyDeviceToDevice, st));
+        PICGPU_CUDA_TRY(
+            cudaMemcpyAsync(jz, J + 2 * (size_t)gd.ncells, (size_t)gd.ncells * 8, cudaMemcpyDeviceToDevice, st));
+        PICGPU_CUDA_TRY(cudaEventRecord(ev, st));
+        PICGPU_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, ev, 0));
+        PICGPU_CUDA_TRY(cudaEventDestroy(ev));
+    });
+}
+
+int picgpu_deposit_density(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
+                           const double* quantity, uint64_t n, double* rho) {
+    return guard([&] {
+        check_order(order);
+        const GridD gd = make_grid(*g);
+        check_density_grid(*g, order);
+        Stateless& S = stateless();
+        std::lock_guard<std::mutex> lk(S.mu);
+        S.prepare(*g);
+        BinStore& bs = S.store;
+        const cudaStream_t st = S.st;
+        bs.B.ensure(n);
+        const Soa b = bs.B.soa();
+        h2d(b.x, x, n * 8, st); h2d(b.y, y, n * 8, st); h2d(b.z, z, n * 8, st);
+        h2d(b.w, quantity, n * 8, st);  // quantity rides in the w slot through the sort
+        bs.full_sort_from_B(n);
+        S.J.ensure((size_t)gd.ncells * 8);
+        double* R = S.J.as<double>();
+        if (n == 0) {
+            PICGPU_CUDA_TRY(cudaMemsetAsync(R, 0, (size_t)gd.ncells * 8, st));
+        } else {
+            int* flag = S.flag.as<int>();
+            PICGPU_CUDA_TRY(cudaMemsetAsync(flag, 0, 4, st));
+            k_not_identity<<<div_up((long long)n, 256), 256, 0, st>>>(bs.vals2.as<uint32_t>(), n, flag);
+            note_launch();
+            int h = 0;
+            PICGPU_CUDA_TRY(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, st));
+            PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+            S.aux.ensure(density_scratch_bytes(order, n));
+            const Soa a = bs.A.soa();
+            if (!h)  // storage already cell-sorted: source-cell order == storage order
+                launch_deposit_density(order, gd, a, a.w, 0.0, bs.d_off(), bs.d_cnt(), n, S.aux.p, R, st);
+            else
+                launch_deposit_density_merge(order, gd, a, a.w, 0.0, bs.vals2.as<uint32_t>(), bs.d_off(), bs.d_cnt(),
+                                             n, S.aux.p, R, st);
+        }
+        d2h(rho, R, (size_t)gd.ncells * 8, st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
+int picgpu_counting_sort(const picgpu_grid* g, const double* x, const double* y, const double* z, uint64_t n,
+                         uint32_t* perm, uint32_t* bin_start, uint32_t* bin_count) {
+    return guard([&] {
+        const GridD gd = make_grid(*g);
+        Stateless& S = stateless();
+        std::lock_guard<std::mutex> lk(S.mu);
+        S.prepare(*g);
+        BinStore& bs = S.store;
+        const cudaStream_t st = S.st;
+        bs.B.ensure(n);
+        const Soa b = bs.B.soa();
+        h2d(b.x, x, n * 8, st); h2d(b.y, y, n * 8, st); h2d(b.z, z, n * 8, st);
+        bs.full_sort_from_B(n);
+        d2h(perm, bs.vals2.p, n * 4, st);
+        d2h(bin_start, bs.off.p, (size_t)gd.ncells * 4, st);  // packed layout: off == exclusive scan of counts
+        d2h(bin_count, bs.cnt.p, (size_t)gd.ncells * 4, st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
+int picgpu_advance(const picgpu_grid* g, double dt, double* x, double* y, double* z, const double* vx,
+                   const double* vy, const double* vz, uint64_t n, uint64_t* moved) {
+    return guard([&] {
+        const GridD gd = make_grid(*g);
+        const double cap2 = cap2_of(*g, dt);
+        Stateless& S = stateless();
+        std::lock_guard<std::mutex> lk(S.mu);
+        S.prepare(*g);
+        BinStore& bs = S.store;
+        const cudaStream_t st = S.st;
+        bs.B.ensure(n);
+        const Soa b = bs.B.soa();
+        h2d(b.x, x, n * 8, st); h2d(b.y, y, n * 8, st); h2d(b.z, z, n * 8, st);
+        h2d(b.vx, vx, n * 8, st); h2d(b.vy, vy, n * 8, st); h2d(b.vz, vz, n * 8, st);
+        S.flag.ensure(16);
+        unsigned long long* dm = S.flag.as<unsigned long long>();
+        int* err = reinterpret_cast<int*>(dm + 1);
+        PICGPU_CUDA_TRY(cudaMemsetAsync(dm, 0, 16, st));
+        launch_advance(gd, dt, cap2, b.x, b.y, b.z, b.vx, b.vy, b.vz, n, dm, err, st);
+        unsigned long long hm[2] = {0, 0};
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(hm, dm, 16, cudaMemcpyDeviceToHost, st));
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+        const int e = (int)(hm[1] & 0xffffffffu);
+        if (e == PICGPU_EDOMAIN) throw Status{e, "advance: particle displacement exceeds the single-cell cap"};
+        if (e) throw Status{e, "cell_of: non-finite particle position"};
+        d2h(x, b.x, n * 8, st); d2h(y, b.y, n * 8, st); d2h(z, b.z, n * 8, st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+        if (moved) *moved = hm[0];
+    });
+}
+
+int picgpu_cell_of(const picgpu_grid* g, const double* x, const double* y, const double* z, uint64_t n,
+                   uint32_t* cell) {
+    return guard([&] {
+        const GridD gd = make_grid(*g);
+        Stateless& S = stateless();
+        std::lock_guard<std::mutex> lk(S.mu);
+        S.prepare(*g);
+        BinStore& bs = S.store;
+        const cudaStream_t st = S.st;
+        bs.B.ensure(n);
+        bs.keys.ensure(n * 4 + 4);
+        const Soa b = bs.B.soa();
+        h2d(b.x, x, n * 8, st); h2d(b.y, y, n * 8, st); h2d(b.z, z, n * 8, st);
+        int* err = S.flag.as<int>();
+        PICGPU_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+        launch_cells(gd, b.x, b.y, b.z, n, bs.keys.as<uint32_t>(), err, st);
+        int h = 0;
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st));
+        d2h(cell, bs.keys.p, n * 4, st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h) throw Status{h, "cell_of: non-finite particle position"};
+    });
+}
+
+// ---- session ---------------------------------------------------------------
+
+int picgpu_session_create(const picgpu_grid* g, const picgpu_session_config* cfg, picgpu_session** out) {
+    *out = nullptr;
+    picgpu_session* s = nullptr;
+    const int rc = guard([&] {
+        check_order(cfg->order);
+        make_grid(*g);
+        if (!(cfg->gap_ratio >= 0.0)) throw Status{PICGPU_EINVAL, "gpma: gap_ratio must be >= 0"};
+        s = new picgpu_session;
+        s->device = cfg->device;
+        s->order = cfg->order;
+        s->flags = cfg->flags;
+        set_device(s);
+        PICGPU_CUDA_TRY(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+        s->store.init(*g, cfg->gap_ratio, cfg->min_gap, s->st);
+        s->J.ensure((size_t)s->store.g.ncells * 24);
+        PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)s->store.g.ncells * 24, s->st));
+        s->timing = (cfg->flags & PICGPU_SESSION_TIMING) != 0;
+        for (auto& e : s->ev) PICGPU_CUDA_TRY(cudaEventCreate(&e));
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
+    if (rc) {
+        delete s;
+        return rc;
+    }
+    *out = s;
+    return PICGPU_OK;
+}
+
+int picgpu_session_destroy(picgpu_session* s) {
+    if (!s) return PICGPU_OK;
+    return guard([&] {
+        set_device(s);
+        cudaStreamSynchronize(s->st);
+        for (auto& e : s->ev)
+            if (e) cudaEventDestroy(e);
+        cudaStream_t st = s->st;
+        delete s;
+        if (st) cudaStreamDestroy(st);
+    });
+}
+
+int picgpu_session_upload(picgpu_session* s, uint64_t n, const double* x, const double* y, const double* z,
+                          const double* vx, const double* vy, const double* vz, const double* w, const uint64_t* id,
+                          double q) {
+    return guard([&] {
+        set_device(s);
+        BinStore& bs = s->store;
+        const cudaStream_t st = s->st;
+        bs.B.ensure(n);
+        const Soa b = bs.B.soa();
+        h2d(b.x, x, n * 8, st); h2d(b.y, y, n * 8, st); h2d(b.z, z, n * 8, st);
+        h2d(b.vx, vx, n * 8, st); h2d(b.vy, vy, n * 8, st); h2d(b.vz, vz, n * 8, st);
+        h2d(b.w, w, n * 8, st);
+        if (id)
+            h2d(b.id, id, n * 8, st);
+        else if (n) {
+            k_fill_ids<<<div_up((long long)n, 256), 256, 0, st>>>(b.id, n);
+            note_launch();
+        }
+        bs.full_sort_from_B(n);
+        s->q = q;
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
+int picgpu_session_generate_plasma(picgpu_session* s, int ppc, double u_th, uint64_t seed) {
+    return guard([&] {
+        set_device(s);
+        if (ppc < 1) throw Status{PICGPU_EINVAL, "workload: ppc must be >= 1"};
+        BinStore& bs = s->store;
+        const uint64_t n = (uint64_t)bs.g.ncells * (uint64_t)ppc;
+        bs.B.ensure(n);
+        launch_generate_plasma(bs.g, ppc, u_th, seed, bs.B.soa(), s->st);
+        bs.full_sort_from_B(n);
+        s->q = -1.0;  // electrons
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
+}
+
+static void accumulate_phase(picgpu_session* s, int phase, int e0, int e1, uint64_t launches) {
+    float ms = 0.f;
+    PICGPU_CUDA_TRY(cudaEventElapsedTime(&ms, s->ev[e0], s->ev[e1]));
+    s->phase_ms[phase] += ms;
+    s->phase_launches[phase] += launches;
+}
+
+int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_step_stats* out) {
+    return guard([&] {
+        set_device(s);
+        BinStore& bs = s->store;
+        const cudaStream_t st = s->st;
+        const GridD& g = bs.g;
+        if ((flags & PICGPU_STEP_PUSH) && !(flags & PICGPU_STEP_SORT))
+            throw Status{PICGPU_EINVAL, "session_step: PUSH requires SORT (push and move detection are fused)"};
+        picgpu_step_stats stats{};
+        const uint64_t rebuilds0 = bs.rebuilds;
+        const bool T = s->timing;
+        if (flags & PICGPU_STEP_SORT) {
+            const double cap2 = (flags & PICGPU_STEP_PUSH) ? cap2_of(bs.hg, dt) : 0.0;
+            const uint64_t l0 = g_launches.load();
+            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
+            const StepCounters c = bs.incremental_step((flags & PICGPU_STEP_PUSH) != 0, dt, cap2);
+            if (T) {
+                PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
+                PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[1]));
+                accumulate_phase(s, bs.rebuilds != rebuilds0 ? 2 : 0, 0, 1, g_launches.load() - l0);
+            }
+            if (c.err == PICGPU_EDOMAIN)
+                throw Status{c.err, "advance: particle displacement exceeds the single-cell cap"};
+            if (c.err) throw Status{c.err, "cell_of: non-finite particle position"};
+            stats.moved = c.moved;
+            stats.inserts = std::min<uint64_t>(c.nmovers, bs.mcap) ;
+            stats.overflowed = c.noverflow;
+        }
+        if (flags & PICGPU_STEP_CURRENT) {
+            const uint64_t l0 = g_launches.load();
+            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[2], st));
+            PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)g.ncells * 24, st));
+            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[3], st));
+            if (bs.n)
+                launch_deposit_current(s->order, g, bs.A.soa(), bs.d_off(), bs.d_cnt(), s->q, s->J.as<double>(),
+                                       bs.num_sms, st);
+            if (T) {
+                PICGPU_CUDA_TRY(cudaEventRecord(s->ev[4], st));
+                PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[4]));
+                accumulate_phase(s, 5, 2, 3, 0);
+                accumulate_phase(s, 3, 3, 4, g_launches.load() - l0);
+            }
+        }
+        if (flags & PICGPU_STEP_DENSITY) {
+            check_density_grid(bs.hg, s->order);
+            const uint64_t l0 = g_launches.load();
+            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[5], st));
+            s->rho.ensure((size_t)g.ncells * 8);
+            s->dscratch.ensure(density_scratch_bytes(s->order, bs.capacity));
+            launch_deposit_density(s->order, g, bs.A.soa(), nullptr, s->q, bs.d_off(), bs.d_cnt(), bs.capacity,
+                                   s->dscratch.p, s->rho.as<double>(), st);
+            if (T) {
+                PICGPU_CUDA_TRY(cudaEventRecord(s->ev[6], st));
+                PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[6]));
+                accumulate_phase(s, 4, 5, 6, g_launches.load() - l0);
+            }
+        }
+        if (flags & PICGPU_STEP_GLOBAL_SORT) {
+            const uint64_t l0 = g_launches.load();
+            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
+            bs.relayout();
+            stats.global_sorted = 1;
+            if (T) {
+                PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
+                PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[1]));
+                accumulate_phase(s, 2, 0, 1, g_launches.load() - l0);
+            }
+        }
+        if (!(flags & PICGPU_STEP_NO_SYNC)) PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+        stats.rebuilt = bs.rebuilds != rebuilds0;
+        stats.capacity = bs.capacity;
+        stats.num_particles = bs.n;
+        stats.empty_slot_ratio = bs.capacity ? (double)(bs.capacity - bs.n) / (double)bs.capacity : 1.0;
+        if (out) *out = stats;
+    });
+}
+
+int picgpu_session_global_sort(picgpu_session* s) {
+    return guard([&] {
+        set_device(s);
+        s->store.relayout();
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
+}
+
+int picgpu_session_synchronize(picgpu_session* s) {
+    return guard([&] {
+        set_device(s);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
+}
+
+uint64_t picgpu_session_num_particles(picgpu_session* s) { return s->store.n; }
+uint64_t picgpu_session_capacity(picgpu_session* s) { return s->store.capacity; }
+void* picgpu_session_stream(picgpu_session* s) { return (void*)s->st; }
+
+int picgpu_session_download_particles(picgpu_session* s, double* x, double* y, double* z, double* vx, double* vy,
+                                      double* vz, double* w, uint64_t* id) {
+    return guard([&] {
+        set_device(s);
+        BinStore& bs = s->store;
+        const cudaStream_t st = s->st;
+        bs.compact_to_B();
+        const Soa b = bs.B.soa();
+        const size_t n = bs.n;
+        d2h(x, b.x, n * 8, st); d2h(y, b.y, n * 8, st); d2h(z, b.z, n * 8, st);
+        d2h(vx, b.vx, n * 8, st); d2h(vy, b.vy, n * 8, st); d2h(vz, b.vz, n * 8, st);
+        d2h(w, b.w, n * 8, st); d2h(id, b.id, n * 8, st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
+int picgpu_session_download_bins(picgpu_session* s, uint32_t* bin_offset, uint32_t* bin_count) {
+    return guard([&] {
+        set_device(s);
+        const size_t nc = s->store.g.ncells;
+        d2h(bin_offset, s->store.off.p, (nc + 1) * 4, s->st);
+        d2h(bin_count, s->store.cnt.p, nc * 4, s->st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
+}
+
+int picgpu_session_download_current(picgpu_session* s, double* jx, double* jy, double* jz) {
+    return guard([&] {
+        set_device(s);
+        const size_t nc = s->store.g.ncells;
+        const double* J = s->J.as<double>();
+        d2h(jx, J, nc * 8, s->st);
+        d2h(jy, J + nc, nc * 8, s->st);
+        d2h(jz, J + 2 * nc, nc * 8, s->st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
+}
+
+int picgpu_session_download_density(picgpu_session* s, double* rho) {
+    return guard([&] {
+        set_device(s);
+        if (!s->rho.p) throw Status{PICGPU_ELOGIC, "session: no density deposited yet"};
+        d2h(rho, s->rho.p, (size_t)s->store.g.ncells * 8, s->st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
+}
+
+int picgpu_session_device_fields(picgpu_session* s, double** j, double** rho) {
+    if (j) *j = s->J.as<double>();
+    if (rho) *rho = s->rho.as<double>();
+    return PICGPU_OK;
+}
+
+int picgpu_session_phase_times(picgpu_session* s, double* ms, uint64_t* launches, int nphases) {
+    for (int i = 0; i < nphases && i < PICGPU_NPHASES; ++i) {
+        if (ms) ms[i] = s->phase_ms[i];
+        if (launches) launches[i] = s->phase_launches[i];
+    }
+    return PICGPU_OK;
+}
+
+int picgpu_session_reset_phase_times(picgpu_session* s) {
+    for (int i = 0; i < PICGPU_NPHASES; ++i) {
+        s->phase_ms[i] = 0.0;
+        s->phase_launches[i] = 0;
+    }
+    return PICGPU_OK;
+}
+
+}  // extern "C"
+
+// ---- FP64 peak microbenchmark (roofline denominator, measured in-run) -------
+
+namespace picgpu {
+__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+    double r0 = threadIdx.x, r1 = r0 + 1, r2 = r0 + 2, r3 = r0 + 3, r4 = r0 + 4, r5 = r0 + 5, r6 = r0 + 6,
+           r7 = r0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            r0 = fma(r0, a, b); r1 = fma(r1, a, b); r2 = fma(r2, a, b); r3 = fma(r3, a, b);
+            r4 = fma(r4, a, b); r5 = fma(r5, a, b); r6 = fma(r6, a, b); r7 = fma(r7, a, b);
+        }
+    }
+    const double s = r0 + r1 + r2 + r3 + r4 + r5 + r6 + r7;
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+}  // namespace picgpu
+
+extern "C" int picgpu_fp64_peak(int device, double* tflops) {
+    return guard([&] {
+        PICGPU_CUDA_TRY(cudaSetDevice(device));
+        const int sms = current_sms();
+        DevBuf out;
+        out.ensure(64);
+        cudaStream_t st;
+        PICGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        cudaEvent_t e0, e1;
+        PICGPU_CUDA_TRY(cudaEventCreate(&e0));
+        PICGPU_CUDA_TRY(cudaEventCreate(&e1));
+        const int blocks = sms * 4, threads = 256, iters = 4096;
+        k_dfma_peak<<<blocks, threads, 0, st>>>(out.as<double>(), 64, 0.999, 1e-3);  // warm-up
+        note_launch();
+        float best = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+            PICGPU_CUDA_TRY(cudaEventRecord(e0, st));
+            k_dfma_peak<<<blocks, threads, 0, st>>>(out.as<double>(), iters, 0.999, 1e-3);
+            note_launch();
+            PICGPU_CUDA_TRY(cudaEventRecord(e1, st));
+            PICGPU_CUDA_TRY(cudaEventSynchronize(e1));
+            float ms = 0;
+            PICGPU_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+            best = std::min(best, ms);
+        }
+        PICGPU_CUDA_TRY(cudaGetLastError());
+        const double flops = 2.0 * 64.0 * iters * (double)blocks * threads;
+        *tflops = flops / (best * 1e-3) / 1e12;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(st);
+    });
+}

@@ -1,0 +1,179 @@
+// common.cuh -- device primitives shared by the sm_100a kernels.
+//
+// Everything on the parity-critical path (cell location, shape weights, push,
+// rho accumulation) uses explicit round-to-nearest intrinsics (__dmul_rn,
+// __dadd_rn, __dsub_rn, __ddiv_rn) so nvcc can never contract them into FMAs:
+// the reference build has no FMA.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "picgpu.h"
+
+namespace picgpu {
+
+// Device view of the periodic box (pic::GridSpec, grid.hpp:26-72) plus values
+// precomputed on the host exactly as the reference computes them.
+struct GridD {
+    int nx, ny, nz;
+    double dx, dy, dz;
+    double ox, oy, oz;
+    double Lx, Ly, Lz;        // GridSpec::length(axis) = cells * spacing (grid.hpp:46)
+    double inv_dx, inv_dy, inv_dz;
+    int pow2x, pow2y, pow2z;  // spacing is a power of two: (x-o)*inv == (x-o)/h exactly
+    uint32_t ncells;
+};
+
+GridD make_grid(const picgpu_grid& g);
+
+// Particle store, structure of arrays (pic::ParticleSoA, particles.hpp:14-19).
+struct Soa {
+    double *x, *y, *z, *vx, *vy, *vz, *w;
+    uint64_t* id;
+};
+
+struct CSoa {
+    const double *x, *y, *z, *vx, *vy, *vz, *w;
+    const uint64_t* id;
+    CSoa() = default;
+    CSoa(const Soa& s) : x(s.x), y(s.y), z(s.z), vx(s.vx), vy(s.vy), vz(s.vz), w(s.w), id(s.id) {}
+};
+
+// Device error word: first error code wins (host reads it back once per call).
+__device__ __forceinline__ void raise_error(int* err, int code) {
+    if (err) atomicCAS(err, 0, code);
+}
+
+// grid.hpp:64-67
+__host__ __device__ __forceinline__ int wrap_index(int i, int n) {
+    int r = i % n;
+    return r < 0 ? r + n : r;
+}
+
+// detail::locate_axis, grid.hpp:81-100.  Bit-identical to the reference:
+// u = (x - origin) / spacing (a multiply by the exact reciprocal when the
+// spacing is a power of two, which yields the same correctly rounded value).
+__device__ __forceinline__ int locate_axis(double x, double origin, double spacing, double inv, int pow2, int n,
+                                           double& frac) {
+    const double t = __dsub_rn(x, origin);
+    const double u = pow2 ? __dmul_rn(t, inv) : __ddiv_rn(t, spacing);
+    double fu = floor(u);
+    double fr = __dsub_rn(u, fu);
+    if (fr >= 1.0) {
+        fr = 0.0;
+        fu = __dadd_rn(fu, 1.0);
+    }
+    frac = fr;
+    if (fu >= 0.0 && fu < (double)n) return (int)fu;
+    double c = fmod(fu, (double)n);
+    if (c < 0.0) c = __dadd_rn(c, (double)n);
+    int ci = (int)c;
+    if (ci == n) ci = 0;
+    return ci;
+}
+
+__device__ __forceinline__ bool finite3(double x, double y, double z) {
+    return isfinite(x) && isfinite(y) && isfinite(z);
+}
+
+// cell_of, grid.hpp:106-113 (caller checks finiteness).
+__device__ __forceinline__ uint32_t cell_linear(const GridD& g, double x, double y, double z, int& i, int& j,
+                                                int& k, double& fx, double& fy, double& fz) {
+    i = locate_axis(x, g.ox, g.dx, g.inv_dx, g.pow2x, g.nx, fx);
+    j = locate_axis(y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, fy);
+    k = locate_axis(z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, fz);
+    return (uint32_t)i + (uint32_t)g.nx * ((uint32_t)j + (uint32_t)g.ny * (uint32_t)k);
+}
+
+__device__ __forceinline__ uint32_t cell_linear(const GridD& g, double x, double y, double z) {
+    int i, j, k;
+    double fx, fy, fz;
+    return cell_linear(g, x, y, z, i, j, k, fx, fy, fz);
+}
+
+// Shape weights in a fixed window of W taps starting at node cell + OFF.
+//   order 1: CIC, cic_shape_1d (shape.hpp:26-29), W = 2, OFF = 0.
+//   order 3: QSP, qsp_shape_1d (shape.hpp:33-43), W = 4, OFF = -1.
+//   order 2: TSC (this project's restatement, oracle/picoracle.c po_shape_1d):
+//            3 taps from base cell-1+up, padded into a W = 4 window at OFF = -1;
+//            `up` (d >= 0.5) says which end of the window holds the zero.
+// Expression order matches the reference exactly (bit-identical weights).
+template <int ORDER>
+struct Shape;
+
+template <>
+struct Shape<1> {
+    static constexpr int W = 2, OFF = 0, TAPS = 2;
+    __device__ __forceinline__ static void weights(double d, double (&s)[W], int& up) {
+        s[0] = __dsub_rn(1.0, d);
+        s[1] = d;
+        up = 0;
+    }
+};
+
+template <>
+struct Shape<3> {
+    static constexpr int W = 4, OFF = -1, TAPS = 4;
+    __device__ __forceinline__ static void weights(double d, double (&s)[W], int& up) {
+        const double t = d;
+        const double t2 = __dmul_rn(t, t);
+        const double t3 = __dmul_rn(t2, t);
+        const double u = __dsub_rn(1.0, t);
+        const double k6 = 1.0 / 6.0;
+        s[0] = __dmul_rn(__dmul_rn(__dmul_rn(u, u), u), k6);
+        s[1] = __dmul_rn(__dadd_rn(__dsub_rn(__dmul_rn(3.0, t3), __dmul_rn(6.0, t2)), 4.0), k6);
+        s[2] = __dmul_rn(
+            __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(-3.0, t3), __dmul_rn(3.0, t2)), __dmul_rn(3.0, t)), 1.0), k6);
+        s[3] = __dmul_rn(t3, k6);
+        up = 0;
+    }
+};
+
+template <>
+struct Shape<2> {
+    static constexpr int W = 4, OFF = -1, TAPS = 3;
+    // Unpadded 3 taps (base = cell - 1 + up).
+    __device__ __forceinline__ static void taps(double d, double (&w)[3], int& up) {
+        up = d >= 0.5;
+        const double dl = up ? __dsub_rn(d, 1.0) : d;
+        const double a = __dsub_rn(0.5, dl);
+        const double b = __dadd_rn(0.5, dl);
+        w[0] = __dmul_rn(0.5, __dmul_rn(a, a));
+        w[1] = __dsub_rn(0.75, __dmul_rn(dl, dl));
+        w[2] = __dmul_rn(0.5, __dmul_rn(b, b));
+    }
+    __device__ __forceinline__ static void weights(double d, double (&s)[W], int& up) {
+        double w[3];
+        taps(d, w, up);
+        s[0] = up ? 0.0 : w[0];
+        s[1] = up ? w[0] : w[1];
+        s[2] = up ? w[1] : w[2];
+        s[3] = up ? w[2] : 0.0;
+    }
+};
+
+// Launch bookkeeping: every kernel launch of this library bumps the counter
+// reported by picgpu_kernel_launches() (evidence that the native path ran).
+void note_launch(uint64_t n = 1);
+
+#define PICGPU_CUDA_TRY(expr)                                              \
+    do {                                                                   \
+        cudaError_t e__ = (expr);                                          \
+        if (e__ != cudaSuccess) throw ::picgpu::CudaError(e__, #expr);     \
+    } while (0)
+
+struct CudaError {
+    cudaError_t code;
+    const char* what;
+    CudaError(cudaError_t c, const char* w) : code(c), what(w) {}
+};
+
+struct Status {  // thrown inside the library, converted to a return code at the C boundary
+    int code;
+    const char* msg;
+};
+
+inline int div_up(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace picgpu

@@ -1,0 +1,41 @@
+// kernels.hpp -- host-side launchers shared between the translation units.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace picgpu {
+
+// deposit_current.cu ---------------------------------------------------------
+// J (3*ncells doubles: jx|jy|jz, pre-zeroed) += deposit of the binned store.
+void launch_deposit_current(int order, const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt,
+                            double q, double* j, int num_sms, cudaStream_t st);
+
+// deposit_density.cu ---------------------------------------------------------
+// rho[node] = ordered sum (storage order) of quantity[s] * S (quantity NULL: qscale*w[s]), over binned,
+// cell-sorted storage (bins ascending by cell, slot order within a bin).
+// `scratch` holds (3*W + 1) doubles per slot (+1 byte per slot for TSC).
+size_t density_scratch_bytes(int order, uint64_t slots);
+void launch_deposit_density(int order, const GridD& g, const CSoa& p, const double* quantity, double qscale,
+                            const uint32_t* off,
+                            const uint32_t* cnt, uint64_t slots, void* scratch, double* rho, cudaStream_t st);
+// Unsorted storage: contributions to a node are merged by storage index across
+// its source cells (k-way merge).  `rank[s]` is the storage index of slot s.
+void launch_deposit_density_merge(int order, const GridD& g, const CSoa& p, const double* quantity, double qscale,
+                                  const uint32_t* rank, const uint32_t* off, const uint32_t* cnt, uint64_t slots,
+                                  void* scratch, double* rho, cudaStream_t st);
+
+// sorter.cu ------------------------------------------------------------------
+// cell[p] = linear cell id (bit-identical cell_of); raises EINVAL on non-finite.
+void launch_cells(const GridD& g, const double* x, const double* y, const double* z, uint64_t n, uint32_t* cell,
+                  int* err, cudaStream_t st);
+// Ballistic push, bit-identical to pic::advance; counts movers.
+void launch_advance(const GridD& g, double dt, double cap2, double* x, double* y, double* z, const double* vx,
+                    const double* vy, const double* vz, uint64_t n, unsigned long long* moved, int* err,
+                    cudaStream_t st);
+// Device-side SURVEY 8(d) plasma generator (cell-major, counter RNG).
+void launch_generate_plasma(const GridD& g, int ppc, double u_th, uint64_t seed, Soa out, cudaStream_t st);
+
+}  // namespace picgpu

@@ -1,0 +1,686 @@
+// sorter.cu -- the GPU cell sorter (bins with slack, incremental migration,
+// full stable re-sort), the bit-exact push and the device plasma generator.
+//
+// Reference anchors (proj/include/pic/):
+//   gpma_build          gpma.hpp:379-402  -> BinStore::full_sort_from_B (stable radix sort by cell)
+//   Gpma::layout        gpma.hpp:269-302  -> k_counts_caps + scan (same capacity rule)
+//   detect_moves        gpma.hpp:162-177  -> k_push_detect (fused with the push, warp-ballot append)
+//   apply_moves/insert  gpma.hpp:110-125, :248-262 -> k_insert (per-bin atomic tail cursor into slack)
+//   borrow/overflow     gpma.hpp:337-370  -> overflow list -> rebuild (relayout with fresh slack)
+//   rebuild             gpma.hpp:130-143  -> BinStore::rebuild_overflow
+//   global_sort         sort_policy.hpp:83-85 -> BinStore::relayout
+//   advance             workload.hpp:128-155 -> push_one (round-to-nearest intrinsics, bit-identical)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <utility>
+
+#include "kernels.hpp"
+#include "store.hpp"
+
+namespace picgpu {
+
+// ---------------------------------------------------------------------------
+// buffers
+
+DevBuf::~DevBuf() { release(); }
+
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+void DevBuf::ensure(size_t b) {
+    if (b <= bytes) return;
+    release();
+    const size_t nb = std::max<size_t>(b, 256);
+    if (cudaMalloc(&p, nb) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        throw Status{PICGPU_ENOMEM, "device allocation failed"};
+    }
+    bytes = nb;
+}
+
+void SoaBuf::ensure(size_t n) {
+    for (auto& b : a) b.ensure(std::max<size_t>(n, 1) * 8);
+    cap = std::max(cap, n);
+}
+
+Soa SoaBuf::soa() const {
+    return Soa{a[0].as<double>(), a[1].as<double>(), a[2].as<double>(), a[3].as<double>(),
+               a[4].as<double>(), a[5].as<double>(), a[6].as<double>(), a[7].as<uint64_t>()};
+}
+
+static void swap_soa(SoaBuf& x, SoaBuf& y) {
+    for (int i = 0; i < 8; ++i) {
+        std::swap(x.a[i].p, y.a[i].p);
+        std::swap(x.a[i].bytes, y.a[i].bytes);
+    }
+    std::swap(x.cap, y.cap);
+}
+
+static void swap_buf(DevBuf& x, DevBuf& y) {
+    std::swap(x.p, y.p);
+    std::swap(x.bytes, y.bytes);
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+__device__ __forceinline__ void copy_particle(const Soa& src, uint64_t s, const Soa& dst, uint64_t d) {
+    dst.x[d] = src.x[s];
+    dst.y[d] = src.y[s];
+    dst.z[d] = src.z[s];
+    dst.vx[d] = src.vx[s];
+    dst.vy[d] = src.vy[s];
+    dst.vz[d] = src.vz[s];
+    dst.w[d] = src.w[s];
+    dst.id[d] = src.id[s];
+}
+
+// detail::wrap_position, workload.hpp:128-132
+__device__ __forceinline__ double wrap_position(double x, double origin, double length) {
+    double r = __dsub_rn(x, __dmul_rn(length, floor(__ddiv_rn(__dsub_rn(x, origin), length))));
+    if (__dsub_rn(r, origin) >= length) r = origin;
+    return r;
+}
+
+// One particle of pic::advance (workload.hpp:144-153); returns false on a cap
+// violation (the reference throws std::domain_error).
+__device__ __forceinline__ bool push_one(const GridD& g, double dt, double cap2, double& x, double& y, double& z,
+                                         double vx, double vy, double vz) {
+    const double v2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+    if (v2 > cap2) return false;
+    x = wrap_position(__dadd_rn(x, __dmul_rn(vx, dt)), g.ox, g.Lx);
+    y = wrap_position(__dadd_rn(y, __dmul_rn(vy, dt)), g.oy, g.Ly);
+    z = wrap_position(__dadd_rn(z, __dmul_rn(vz, dt)), g.oz, g.Lz);
+    return true;
+}
+
+// Largest b in [0, nb) with so[b] <= s (bins of one CTA, offsets in smem).
+__device__ __forceinline__ int find_bin(const uint32_t* so, int nb, uint32_t s) {
+    int lo = 0, hi = nb - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (so[mid] <= s)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+
+__global__ void k_cells(const GridD g, const double* __restrict__ x, const double* __restrict__ y,
+                        const double* __restrict__ z, uint64_t n, uint32_t* __restrict__ cell, int* err) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const double px = x[p], py = y[p], pz = z[p];
+    if (!finite3(px, py, pz)) {
+        raise_error(err, PICGPU_EINVAL);
+        cell[p] = 0;
+        return;
+    }
+    cell[p] = cell_linear(g, px, py, pz);
+}
+
+__global__ void k_iota(uint32_t* v, uint64_t n) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) v[p] = (uint32_t)p;
+}
+
+// Run boundaries of the sorted keys: start[c] = first rank, endp[c] = last rank + 1.
+__global__ void k_boundaries(const uint32_t* __restrict__ key, uint64_t n, uint32_t* start, uint32_t* endp) {
+    const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t k = key[r];
+    if (r == 0 || key[r - 1] != k) start[k] = (uint32_t)r;
+    if (r == n - 1 || key[r + 1] != k) endp[k] = (uint32_t)(r + 1);
+}
+
+// Capacity rule of Gpma::layout (gpma.hpp:275-278): ceil(count*(1+gap)) + min_gap.
+__device__ __forceinline__ uint32_t bin_capacity(uint32_t count, double onepg, uint32_t min_gap) {
+    return (uint32_t)ceil(__dmul_rn((double)count, onepg)) + min_gap;
+}
+
+__global__ void k_counts_caps(const uint32_t* start, const uint32_t* endp, uint32_t ncells, uint32_t* cnt,
+                              uint32_t* caps, double onepg, uint32_t min_gap) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > ncells) return;
+    if (c == ncells) {
+        caps[c] = 0;
+        return;
+    }
+    const uint32_t k = endp[c] - start[c];
+    cnt[c] = k;
+    caps[c] = bin_capacity(k, onepg, min_gap);
+}
+
+__global__ void k_caps_from_cnt(const uint32_t* cnt, uint32_t ncells, uint32_t* caps, double onepg,
+                                uint32_t min_gap) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > ncells) return;
+    caps[c] = c == ncells ? 0 : bin_capacity(cnt[c], onepg, min_gap);
+}
+
+// min(cnt, bin capacity): what a bin physically holds (after an overflow cnt
+// counts the overflowed arrivals too).
+__global__ void k_held(const uint32_t* cnt, const uint32_t* off, uint32_t ncells, uint32_t* held) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > ncells) return;
+    held[c] = c == ncells ? 0 : min(cnt[c], off[c + 1] - off[c]);
+}
+
+__global__ void k_u64_to_u32(const unsigned long long* in, uint32_t* out, uint64_t n) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (uint32_t)in[i];
+}
+
+__global__ void k_gather_sorted(const Soa src, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ key,
+                                const uint32_t* __restrict__ start, const uint32_t* __restrict__ off, const Soa dst,
+                                uint64_t n) {
+    const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t c = key[r];
+    copy_particle(src, perm[r], dst, (uint64_t)off[c] + (r - start[c]));
+}
+
+constexpr int BPB = 64;  // bins per CTA for the slot-range kernels
+
+// Copy every bin's held particles (slot order kept) from src to dst offsets.
+__global__ void __launch_bounds__(256) k_relayout(const Soa src, const uint32_t* __restrict__ soff,
+                                                  const uint32_t* __restrict__ cnt, const Soa dst,
+                                                  const uint32_t* __restrict__ doff, uint32_t ncells) {
+    __shared__ uint32_t so[BPB + 1], sc[BPB], dof[BPB];
+    const uint32_t c0 = blockIdx.x * BPB;
+    const int nb = (int)umin((uint32_t)BPB, ncells - c0);
+    for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+        so[b] = soff[c0 + b];
+        if (b < nb) {
+            sc[b] = min(cnt[c0 + b], soff[c0 + b + 1] - soff[c0 + b]);
+            dof[b] = doff[c0 + b];
+        }
+    }
+    __syncthreads();
+    for (uint32_t s = so[0] + threadIdx.x; s < so[nb]; s += blockDim.x) {
+        const int b = find_bin(so, nb, s);
+        const uint32_t r = s - so[b];
+        if (r < sc[b]) copy_particle(src, s, dst, (uint64_t)dof[b] + r);
+    }
+}
+
+// Push (optional) + move detection + in-bin compaction, one CTA per BPB bins.
+//  - pushes every valid slot (bit-exact pic::advance), recomputes its cell;
+//  - a particle whose cell changed is appended to the mover list
+//    (warp-ballot aggregated append) and flagged;
+//  - after a barrier, one thread per bin compacts the stayers in slot order
+//    (stable) and writes the bin's new count.
+// Movers that do not fit the mover buffer stay in their (now stale) bin and
+// are flagged 2; the host then falls back to a full re-sort.
+template <bool PUSH>
+__global__ void __launch_bounds__(256) k_push_detect(const GridD g, const Soa A, const uint32_t* __restrict__ off,
+                                                     uint32_t* __restrict__ cnt, uint8_t* __restrict__ mflag,
+                                                     double dt, double cap2, const Soa M,
+                                                     uint32_t* __restrict__ mcell, uint32_t mcap,
+                                                     StepCounters* ctr) {
+    __shared__ uint32_t so[BPB + 1], sc[BPB], sdep[BPB];
+    __shared__ unsigned long long smoved;
+    const uint32_t c0 = blockIdx.x * BPB;
+    const int nb = (int)umin((uint32_t)BPB, g.ncells - c0);
+    for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+        so[b] = off[c0 + b];
+        if (b < nb) {
+            sc[b] = cnt[c0 + b];
+            sdep[b] = 0;
+        }
+    }
+    if (threadIdx.x == 0) smoved = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    unsigned local_moved = 0;
+    for (uint32_t s = so[0] + threadIdx.x; s < so[nb]; s += blockDim.x) {
+        const int b = find_bin(so, nb, s);
+        const bool valid = s - so[b] < sc[b];
+        bool moved = false;
+        uint32_t nc = 0;
+        double x = 0, y = 0, z = 0, vx = 0, vy = 0, vz = 0;
+        if (valid) {
+            x = A.x[s];
+            y = A.y[s];
+            z = A.z[s];
+            vx = A.vx[s];
+            vy = A.vy[s];
+            vz = A.vz[s];
+            bool ok = true;
+            if (PUSH) {
+                if (!push_one(g, dt, cap2, x, y, z, vx, vy, vz)) {
+                    raise_error(&ctr->err, PICGPU_EDOMAIN);
+                    ok = false;
+                } else {
+                    A.x[s] = x;
+                    A.y[s] = y;
+                    A.z[s] = z;
+                }
+            }
+            if (ok && !finite3(x, y, z)) {
+                raise_error(&ctr->err, PICGPU_EINVAL);
+                ok = false;
+            }
+            if (ok) {
+                nc = cell_linear(g, x, y, z);
+                moved = nc != c0 + (uint32_t)b;
+            }
+            mflag[s] = moved ? 1 : 0;
+        }
+        const unsigned act = __activemask();
+        const unsigned mv = __ballot_sync(act, moved);
+        if (mv) {
+            const int leader = __ffs(mv) - 1;
+            unsigned base = 0;
+            if (lane == leader) base = atomicAdd(&ctr->nmovers, (unsigned)__popc(mv));
+            base = __shfl_sync(act, base, leader);
+            if (moved) {
+                const unsigned idx = base + __popc(mv & ((1u << lane) - 1u));
+                ++local_moved;
+                if (idx < mcap) {
+                    atomicAdd(&sdep[b], 1u);
+                    M.x[idx] = x;
+                    M.y[idx] = y;
+                    M.z[idx] = z;
+                    M.vx[idx] = vx;
+                    M.vy[idx] = vy;
+                    M.vz[idx] = vz;
+                    M.w[idx] = A.w[s];
+                    M.id[idx] = A.id[s];
+                    mcell[idx] = nc;
+                } else {
+                    mflag[s] = 2;  // stays in its stale bin; host re-sorts fully
+                }
+            }
+        }
+    }
+    if (local_moved) atomicAdd(&smoved, (unsigned long long)local_moved);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        if (sdep[b] == 0) continue;
+        const uint32_t lo = so[b], hi = so[b] + sc[b];
+        uint32_t wpos = lo;
+        for (uint32_t r = lo; r < hi; ++r) {
+            if (mflag[r] == 1) continue;
+            if (wpos != r) copy_particle(A, r, A, wpos);
+            ++wpos;
+        }
+        cnt[c0 + b] = wpos - lo;
+    }
+    if (threadIdx.x == 0 && smoved) atomicAdd(&ctr->moved, smoved);
+}
+
+// Migration: every recorded mover takes the next slot of its target bin's
+// slack (atomic tail cursor); arrivals beyond the slack go to the overflow list.
+__global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32_t* __restrict__ mpos, uint32_t mcap,
+                         StepCounters* ctr, const Soa A, const uint32_t* __restrict__ off, uint32_t* cnt,
+                         uint32_t* __restrict__ ovf) {
+    const uint32_t nm = min(ctr->nmovers, mcap);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
+        const uint32_t d = mcell[i];
+        const uint32_t pos = atomicAdd(&cnt[d], 1u);
+        const uint32_t lo = off[d], cap = off[d + 1] - lo;
+        if (pos < cap) {
+            copy_particle(M, i, A, (uint64_t)lo + pos);
+        } else {
+            mpos[i] = pos;
+            ovf[atomicAdd(&ctr->noverflow, 1u)] = i;
+        }
+    }
+}
+
+// Overflowed arrivals land after their bin's held particles in the new layout.
+__global__ void k_place_overflow(const Soa M, const uint32_t* __restrict__ mcell, const uint32_t* __restrict__ mpos,
+                                 const uint32_t* __restrict__ ovf, uint32_t novf, const Soa dst,
+                                 const uint32_t* __restrict__ doff) {
+    const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= novf) return;
+    const uint32_t i = ovf[o];
+    copy_particle(M, i, dst, (uint64_t)doff[mcell[i]] + mpos[i]);
+}
+
+// Overflowed movers appended after a packed store (mover-buffer fallback).
+__global__ void k_append_overflow(const Soa M, const uint32_t* __restrict__ ovf, uint32_t novf, const Soa dst,
+                                  uint64_t base) {
+    const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o < novf) copy_particle(M, ovf[o], dst, base + o);
+}
+
+__global__ void k_advance(const GridD g, double dt, double cap2, double* __restrict__ x, double* __restrict__ y,
+                          double* __restrict__ z, const double* __restrict__ vx, const double* __restrict__ vy,
+                          const double* __restrict__ vz, uint64_t n, unsigned long long* moved, int* err) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool m = false;
+    if (p < n) {
+        double px = x[p], py = y[p], pz = z[p];
+        if (!finite3(px, py, pz)) {
+            raise_error(err, PICGPU_EINVAL);
+        } else {
+            const uint32_t before = cell_linear(g, px, py, pz);
+            if (!push_one(g, dt, cap2, px, py, pz, vx[p], vy[p], vz[p])) {
+                raise_error(err, PICGPU_EDOMAIN);
+            } else {
+                x[p] = px;
+                y[p] = py;
+                z[p] = pz;
+                if (!finite3(px, py, pz))
+                    raise_error(err, PICGPU_EINVAL);
+                else
+                    m = cell_linear(g, px, py, pz) != before;
+            }
+        }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(moved, (unsigned long long)__popc(b));
+}
+
+// rng.hpp:12-27 (bit-identical), rng.hpp:30-34 (device libm: last-ulp
+// differences from glibc are possible; benchmark inputs only).
+__device__ __forceinline__ uint64_t hash_mix(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ double uniform01(uint64_t seed, uint64_t stream, uint64_t counter) {
+    const uint64_t bits = hash_mix(hash_mix(hash_mix(seed) ^ stream) ^ counter);
+    return __dmul_rn(__dadd_rn((double)(bits >> 11), 0.5), 0x1.0p-53);
+}
+__device__ __forceinline__ double gaussian(uint64_t seed, uint64_t stream, uint64_t counter) {
+    const double u1 = uniform01(seed, stream, 2 * counter);
+    const double u2 = uniform01(seed, stream, 2 * counter + 1);
+    return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
+}
+
+__global__ void k_generate(const GridD g, int ppc, double u_th, uint64_t seed, const Soa out, uint64_t n) {
+    const uint64_t pid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pid >= n) return;
+    const uint64_t lin = pid / (uint64_t)ppc;
+    const int i = (int)(lin % (uint64_t)g.nx);
+    const int j = (int)((lin / (uint64_t)g.nx) % (uint64_t)g.ny);
+    const int k = (int)(lin / ((uint64_t)g.nx * (uint64_t)g.ny));
+    out.x[pid] = __dadd_rn(g.ox, __dmul_rn(__dadd_rn((double)i, uniform01(seed, pid, 6)), g.dx));
+    out.y[pid] = __dadd_rn(g.oy, __dmul_rn(__dadd_rn((double)j, uniform01(seed, pid, 7)), g.dy));
+    out.z[pid] = __dadd_rn(g.oz, __dmul_rn(__dadd_rn((double)k, uniform01(seed, pid, 8)), g.dz));
+    const double ux = u_th * gaussian(seed, pid, 0);
+    const double uy = u_th * gaussian(seed, pid, 1);
+    const double uz = u_th * gaussian(seed, pid, 2);
+    const double gam = sqrt(1.0 + ux * ux + uy * uy + uz * uz);
+    out.vx[pid] = ux / gam;
+    out.vy[pid] = uy / gam;
+    out.vz[pid] = uz / gam;
+    out.w[pid] = 1.0 / (double)ppc;
+    out.id[pid] = pid;
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+
+void launch_cells(const GridD& g, const double* x, const double* y, const double* z, uint64_t n, uint32_t* cell,
+                  int* err, cudaStream_t st) {
+    if (!n) return;
+    k_cells<<<div_up((long long)n, 256), 256, 0, st>>>(g, x, y, z, n, cell, err);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_advance(const GridD& g, double dt, double cap2, double* x, double* y, double* z, const double* vx,
+                    const double* vy, const double* vz, uint64_t n, unsigned long long* moved, int* err,
+                    cudaStream_t st) {
+    if (!n) return;
+    k_advance<<<div_up((long long)n, 256), 256, 0, st>>>(g, dt, cap2, x, y, z, vx, vy, vz, n, moved, err);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_generate_plasma(const GridD& g, int ppc, double u_th, uint64_t seed, Soa out, cudaStream_t st) {
+    const uint64_t n = (uint64_t)g.ncells * (uint64_t)ppc;
+    if (!n) return;
+    k_generate<<<div_up((long long)n, 256), 256, 0, st>>>(g, ppc, u_th, seed, out, n);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+void cub_exclusive_sum_u32_to_u64(const uint32_t* in, unsigned long long* out, size_t n, DevBuf& tmp,
+                                  cudaStream_t st) {
+    size_t bytes = 0;
+    PICGPU_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)n, st));
+    tmp.ensure(bytes);
+    PICGPU_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, (int64_t)n, st));
+    note_launch();
+}
+
+// ---------------------------------------------------------------------------
+// BinStore
+
+BinStore::~BinStore() {
+    if (hcounters) cudaFreeHost(hcounters);
+}
+
+void BinStore::init(const picgpu_grid& grid, double gap_ratio, uint32_t mg, cudaStream_t stream) {
+    hg = grid;
+    g = make_grid(grid);
+    onepg = 1.0 + gap_ratio;
+    min_gap = mg;
+    st = stream;
+    int dev = 0;
+    PICGPU_CUDA_TRY(cudaGetDevice(&dev));
+    PICGPU_CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t nc = g.ncells;
+    off.ensure((nc + 1) * 4);
+    off2.ensure((nc + 1) * 4);
+    cnt.ensure(nc * 4);
+    start.ensure(nc * 4);
+    endp.ensure(nc * 4);
+    caps.ensure((nc + 1) * 8);
+    counters.ensure(sizeof(StepCounters));
+    if (!hcounters) PICGPU_CUDA_TRY(cudaMallocHost((void**)&hcounters, sizeof(StepCounters)));
+    PICGPU_CUDA_TRY(cudaMemsetAsync(off.p, 0, (nc + 1) * 4, st));
+    PICGPU_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, nc * 4, st));
+    capacity = 0;
+    n = 0;
+}
+
+// caps (u32, ncells+1 entries, last 0) -> off2 (u32 offsets) ; capacity_next.
+void BinStore::layout_from_counts(uint64_t) {
+    const size_t nc = g.ncells;
+    DevBuf& off64 = keys2;  // scratch: (nc+1) u64
+    off64.ensure((nc + 1) * 8);
+    cub_exclusive_sum_u32_to_u64(caps.as<uint32_t>(), off64.as<unsigned long long>(), nc + 1, cub_tmp, st);
+    unsigned long long total = 0;
+    PICGPU_CUDA_TRY(cudaMemcpyAsync(&total, off64.as<unsigned long long>() + nc, 8, cudaMemcpyDeviceToHost, st));
+    PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    if (total >= 0xffffffffull) throw Status{PICGPU_ELENGTH, "gpma: capacity overflow"};
+    k_u64_to_u32<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(off64.as<unsigned long long>(),
+                                                                 off2.as<uint32_t>(), nc + 1);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+    capacity_next = total;
+}
+
+void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev) {
+    const size_t nc = g.ncells;
+    if (np >= 0xffffffffull) throw Status{PICGPU_ELENGTH, "gpma: particle count exceeds 32-bit slots"};
+    keys.ensure(np * 4 + 4);
+    vals.ensure(np * 4 + 4);
+    vals2.ensure(np * 4 + 4);
+    skeys.ensure(np * 4 + 4);
+    const Soa b = B.soa();
+    StepCounters* ctr = counters.as<StepCounters>();
+    PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
+    PICGPU_CUDA_TRY(cudaMemsetAsync(start.p, 0, nc * 4, st));
+    PICGPU_CUDA_TRY(cudaMemsetAsync(endp.p, 0, nc * 4, st));
+    if (np) {
+        launch_cells(g, b.x, b.y, b.z, np, keys.as<uint32_t>(), &ctr->err, st);
+        k_iota<<<div_up((long long)np, 256), 256, 0, st>>>(vals.as<uint32_t>(), np);
+        note_launch();
+        int bits = 1;
+        while (bits < 32 && (1ull << bits) < nc) ++bits;
+        size_t bytes = 0;
+        PICGPU_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.as<uint32_t>(), skeys.as<uint32_t>(),
+                                                        vals.as<uint32_t>(), vals2.as<uint32_t>(), (int64_t)np, 0,
+                                                        bits, st));
+        cub_tmp.ensure(bytes);
+        PICGPU_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, keys.as<uint32_t>(), skeys.as<uint32_t>(),
+                                                        vals.as<uint32_t>(), vals2.as<uint32_t>(), (int64_t)np, 0,
+                                                        bits, st));
+        note_launch();
+        k_boundaries<<<div_up((long long)np, 256), 256, 0, st>>>(skeys.as<uint32_t>(), np, start.as<uint32_t>(),
+                                                                 endp.as<uint32_t>());
+        note_launch();
+    }
+    k_counts_caps<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(start.as<uint32_t>(), endp.as<uint32_t>(),
+                                                                  (uint32_t)nc, cnt.as<uint32_t>(),
+                                                                  caps.as<uint32_t>(), onepg, min_gap);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+    PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, ctr, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
+    layout_from_counts(np);  // synchronises
+    if (hcounters->err) throw Status{hcounters->err, "cell_of: non-finite particle position"};
+    A.ensure(capacity_next);
+    mflag.ensure(capacity_next + 1);
+    swap_buf(off, off2);
+    if (np) {
+        k_gather_sorted<<<div_up((long long)np, 256), 256, 0, st>>>(b, vals2.as<uint32_t>(), skeys.as<uint32_t>(),
+                                                                    start.as<uint32_t>(), off.as<uint32_t>(),
+                                                                    A.soa(), np);
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+        if (perm_out_dev)
+            PICGPU_CUDA_TRY(cudaMemcpyAsync(perm_out_dev, vals2.p, np * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    capacity = capacity_next;
+    n = np;
+}
+
+void BinStore::relayout() {
+    const size_t nc = g.ncells;
+    k_caps_from_cnt<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt.as<uint32_t>(), (uint32_t)nc,
+                                                                    caps.as<uint32_t>(), onepg, min_gap);
+    note_launch();
+    layout_from_counts(n);
+    B.ensure(capacity_next);
+    mflag.ensure(capacity_next + 1);
+    if (nc) {
+        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                               B.soa(), off2.as<uint32_t>(), (uint32_t)nc);
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+    }
+    swap_soa(A, B);
+    swap_buf(off, off2);
+    capacity = capacity_next;
+}
+
+void BinStore::compact_to_B() {
+    const size_t nc = g.ncells;
+    DevBuf& held = start;  // u32 scratch (nc) -- holds min(cnt, cap); needs nc+1
+    held.ensure((nc + 1) * 4);
+    k_held<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt.as<uint32_t>(), off.as<uint32_t>(), (uint32_t)nc,
+                                                           held.as<uint32_t>());
+    note_launch();
+    DevBuf& off64 = keys2;
+    off64.ensure((nc + 1) * 8);
+    cub_exclusive_sum_u32_to_u64(held.as<uint32_t>(), off64.as<unsigned long long>(), nc + 1, cub_tmp, st);
+    k_u64_to_u32<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(off64.as<unsigned long long>(),
+                                                                 off2.as<uint32_t>(), nc + 1);
+    note_launch();
+    B.ensure(n + mcap + 1);
+    if (nc) {
+        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                               B.soa(), off2.as<uint32_t>(), (uint32_t)nc);
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+    }
+}
+
+void BinStore::ensure_movers(size_t m) {
+    if (m <= mcap) return;
+    M.ensure(m);
+    mcell.ensure(m * 4);
+    mpos.ensure(std::max<size_t>(m, n + 1) * 4);
+    ovf.ensure(m * 4);
+    mcap = m;
+}
+
+StepCounters BinStore::incremental_step(bool push, double dt, double cap2) {
+    const size_t nc = g.ncells;
+    ensure_movers(std::max<size_t>(size_t(1) << 16, n / 4));
+    StepCounters* ctr = counters.as<StepCounters>();
+    PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
+    if (nc && n) {
+        const int blocks = div_up((long long)nc, BPB);
+        if (push)
+            k_push_detect<true><<<blocks, 256, 0, st>>>(g, A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                        mflag.as<uint8_t>(), dt, cap2, M.soa(), mcell.as<uint32_t>(),
+                                                        (uint32_t)mcap, ctr);
+        else
+            k_push_detect<false><<<blocks, 256, 0, st>>>(g, A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                         mflag.as<uint8_t>(), dt, cap2, M.soa(),
+                                                         mcell.as<uint32_t>(), (uint32_t)mcap, ctr);
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+        k_insert<<<num_sms * 4, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), mpos.as<uint32_t>(), (uint32_t)mcap, ctr,
+                                              A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>());
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+    }
+    PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, ctr, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
+    PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    StepCounters out = *hcounters;
+    if (out.err) return out;
+    if (out.nmovers > mcap) {
+        // Mover buffer overflow: stale movers still sit in their old bins.
+        // Compact everything (bins + overflowed arrivals) and re-sort fully.
+        compact_to_B();
+        uint64_t held = 0;
+        {
+            unsigned int h32 = 0;
+            PICGPU_CUDA_TRY(cudaMemcpyAsync(&h32, off2.as<uint32_t>() + nc, 4, cudaMemcpyDeviceToHost, st));
+            PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+            held = h32;
+        }
+        if (out.noverflow) {
+            k_append_overflow<<<div_up(out.noverflow, 256), 256, 0, st>>>(M.soa(), ovf.as<uint32_t>(), out.noverflow,
+                                                                         B.soa(), held);
+            note_launch();
+        }
+        full_sort_from_B(held + out.noverflow);
+        ++rebuilds;
+        ensure_movers(out.nmovers + out.nmovers / 2);
+    } else if (out.noverflow) {
+        // Gpma::rebuild (gpma.hpp:130-143): fresh slack from the true counts,
+        // held particles keep their slot order, overflowed arrivals follow.
+        k_caps_from_cnt<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt.as<uint32_t>(), (uint32_t)nc,
+                                                                        caps.as<uint32_t>(), onepg, min_gap);
+        note_launch();
+        layout_from_counts(n);
+        B.ensure(capacity_next);
+        mflag.ensure(capacity_next + 1);
+        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                               B.soa(), off2.as<uint32_t>(), (uint32_t)nc);
+        note_launch();
+        k_place_overflow<<<div_up(out.noverflow, 256), 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(),
+                                                                    mpos.as<uint32_t>(), ovf.as<uint32_t>(),
+                                                                    out.noverflow, B.soa(), off2.as<uint32_t>());
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+        swap_soa(A, B);
+        swap_buf(off, off2);
+        capacity = capacity_next;
+        ++rebuilds;
+    }
+    return out;
+}
+
+}  // namespace picgpu

@@ -1,0 +1,100 @@
+// store.hpp -- device-resident particle store in cell bins with slack (the GPU
+// analogue of pic::Gpma, proj/include/pic/gpma.hpp:52-371).
+//
+// Unlike the reference GPMA, whose slots hold REFERENCES into an unsorted
+// store, the bins here hold the particle data itself (7 FP64 arrays + id): the
+// deposition kernels then read particles cell-locally and coalesced straight
+// from HBM.  Bin c owns slots [off[c], off[c+1]); its cnt[c] particles are
+// packed at the head, the slack at the tail.  Capacities follow the
+// reference's layout rule exactly, ceil(count*(1+gap_ratio)) + min_gap
+// (gpma.hpp:274-281), so capacity and empty_slot_ratio match the reference.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace picgpu {
+
+// Grow-only device allocation.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf();
+    void ensure(size_t b);
+    void release();
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct SoaBuf {
+    DevBuf a[8];  // x y z vx vy vz w (double), id (uint64)
+    size_t cap = 0;
+    void ensure(size_t n);
+    Soa soa() const;
+};
+
+// Device counters of one step (read back once per step).
+struct StepCounters {
+    unsigned long long moved;
+    unsigned int nmovers;     // movers detected (may exceed mover capacity)
+    unsigned int noverflow;   // arrivals that found no slack
+    int err;                  // picgpu_status of the first device-side error
+    int pad;
+};
+
+struct BinStore {
+    GridD g{};
+    picgpu_grid hg{};
+    double onepg = 1.25;  // 1 + gap_ratio
+    uint32_t min_gap = 2;
+    int num_sms = 148;
+    cudaStream_t st = nullptr;
+
+    SoaBuf A, B;              // A: binned store; B: spare (re-layout target, packed staging)
+    DevBuf off, cnt, off2;    // off: ncells+1 (u32), cnt: ncells (u32)
+    DevBuf keys, keys2, skeys, vals, vals2, start, endp, caps, cub_tmp;
+    DevBuf mflag;             // per-slot mover flag (u8)
+    SoaBuf M;                 // mover records
+    DevBuf mcell, mpos, ovf;  // mover target cell, insert position, overflow list
+    DevBuf counters;          // StepCounters
+    StepCounters* hcounters = nullptr;  // pinned mirror
+
+    uint64_t n = 0;           // particles
+    uint64_t capacity = 0;    // slots in use (off[ncells])
+    size_t mcap = 0;          // mover record capacity
+    uint64_t rebuilds = 0;
+
+    void init(const picgpu_grid& grid, double gap_ratio, uint32_t min_gap, cudaStream_t stream);
+    ~BinStore();
+
+    // B holds n packed particles: stable sort by cell into A with fresh slack
+    // (gpma_build, gpma.hpp:379-402).  perm/starts/counts optionally exported.
+    void full_sort_from_B(uint64_t n_particles, uint32_t* perm_out_dev = nullptr);
+    // Re-layout A's bins with fresh slack from the current counts (global_sort
+    // on an already-binned store == identity permutation inside bins).
+    void relayout();
+    // A's valid particles compacted into B in storage order (bins ascending);
+    // returns the packed offsets in `off2` (exclusive scan of cnt).
+    void compact_to_B();
+    // One incremental step: push (optional) + detect + in-bin compaction +
+    // migration; rebuilds on overflow.  Returns counters (synchronises).
+    StepCounters incremental_step(bool push, double dt, double cap2);
+
+    uint32_t* d_off() const { return off.as<uint32_t>(); }
+    uint32_t* d_cnt() const { return cnt.as<uint32_t>(); }
+
+   private:
+    void ensure_movers(size_t m);
+    void layout_from_counts(uint64_t total_particles);  // caps + scan -> off2; returns via capacity_next
+    uint64_t capacity_next = 0;
+};
+
+void cub_exclusive_sum_u32_to_u64(const uint32_t* in, unsigned long long* out, size_t n, DevBuf& tmp, cudaStream_t st);
+
+}  // namespace picgpu

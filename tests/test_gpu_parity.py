@@ -1,0 +1,301 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle and the
+reference's golden fixtures.
+
+Bars (north_star / SURVEY 8(c)):
+  rho, sort permutation, push, cell ids, bin sets:  bit-exact
+  J:  <= 1e-12 peak-normalised per component (reference metric,
+      proj/tests/test_pipeline.cpp:27-40; the reference's own kernels agree to 1e-13)
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_golden, peak_rel_err, to_pg_grid
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+J_TOL = 1e-12
+
+
+def scramble(s, seed):
+    p = np.random.default_rng(seed).permutation(len(s["x"]))
+    return {k: np.ascontiguousarray(v[p]) for k, v in s.items()}
+
+
+GRIDS = [
+    dict(nx=8),
+    dict(nx=13, ny=6, nz=9, dx=0.5, dy=1.0, dz=0.25, origin=(-1.0, 2.0, 0.5)),
+    dict(nx=5, ny=4, nz=7, dx=0.3, dy=1.7, dz=0.05, origin=(-1.0, 2.0, 0.25)),
+    dict(nx=37, ny=11, nz=20),
+    dict(nx=4, ny=4, nz=4),
+]
+
+
+# ------------------------------------------------------------- golden fixtures
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_golden_current_density_perm(pg, case):
+    d, g, s = load_golden(case)
+    G = to_pg_grid(g)
+    q = float(d["q"])
+    for order in (1, 3):
+        J = pg.deposit_scalar(s, G, order, q=q)
+        assert peak_rel_err((J.jx, J.jy, J.jz), d[f"J_o{order}"]) <= J_TOL
+        rho = pg.deposit_density(s, G, order, q * s["w"])
+        assert np.array_equal(rho, d[f"rho_o{order}"]), f"rho order {order} not bit-exact"
+    perm, starts, counts = pg.counting_sort(s, G)
+    assert np.array_equal(perm, d["perm"])
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_golden_session_lockstep(pg, case):
+    """Session (device-resident bins): push + incremental sort each step must
+    reproduce the reference's positions bit-for-bit and its bin sets."""
+    d, g, s = load_golden(case)
+    G = to_pg_grid(g)
+    q = float(d["q"])
+    with pg.Session(G, order=3) as S:
+        S.upload(s, q=q)
+        assert S.capacity == int(d["cap_gpma"])  # same layout rule as Gpma::layout
+        k = 1
+        while f"adv{k}_x" in d:
+            st = S.step(float(d["dt"]), pg.STEP_PUSH | pg.STEP_SORT)
+            assert st["moved"] / len(s["x"]) == float(d[f"adv{k}_frac"])
+            p = S.particles()
+            mine = np.argsort(p.id)
+            want = np.argsort(d[f"adv{k}_id"])
+            for a in ("x", "y", "z"):
+                assert np.array_equal(getattr(p, a)[mine], d[f"adv{k}_{a}"][want])
+            off, cnt = S.bins()
+            bin_of = np.repeat(np.arange(G.ncells, dtype=np.uint32), cnt.astype(np.int64))
+            assert np.array_equal(bin_of[mine], d[f"bins{k}"][want])
+            k += 1
+        S.step(0.5, pg.STEP_CURRENT | pg.STEP_DENSITY)
+        J = S.current()
+        assert peak_rel_err((J.jx, J.jy, J.jz), d["final_J_o3_bin_order"]) <= J_TOL
+
+
+# ---------------------------------------------------------- oracle, many cases
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+@pytest.mark.parametrize("gi", range(len(GRIDS)))
+def test_current_vs_oracle(pg, orc, order, gi):
+    g = O.Grid.make(**GRIDS[gi])
+    s = scramble(orc.make_plasma(g, 7, 0.3 * min(g.dx, g.dy, g.dz), 100 + gi), gi)
+    s["x"][:3] += np.array([1.0, -2.0, 5.0]) * g.nx * g.dx  # out-of-box positions wrap
+    q = -0.75
+    want = orc.deposit_current(g, order, s, q)
+    J = pg.deposit_scalar(s, to_pg_grid(g), order, q=q)
+    assert peak_rel_err((J.jx, J.jy, J.jz), want) <= J_TOL
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+@pytest.mark.parametrize("sorted_input", [True, False])
+@pytest.mark.parametrize("gi", [0, 1, 2, 3])
+def test_density_bit_exact(pg, orc, order, sorted_input, gi):
+    g = O.Grid.make(**GRIDS[gi])
+    s = orc.make_plasma(g, 5, 0.2 * min(g.dx, g.dy, g.dz), 200 + gi)
+    for _ in range(2):
+        orc.advance(g, 0.5, s)
+    if sorted_input:
+        perm, _, _ = orc.counting_sort(g, s)
+        s = {k: np.ascontiguousarray(v[perm]) for k, v in s.items()}
+    else:
+        s = scramble(s, gi)
+    quantity = np.random.default_rng(gi).standard_normal(len(s["x"]))
+    want = orc.deposit_density(g, order, s, quantity)
+    got = pg.deposit_density(s, to_pg_grid(g), order, quantity)
+    assert np.array_equal(got, want), f"{np.count_nonzero(got != want)} nodes differ"
+
+
+@pytest.mark.parametrize("gi", range(len(GRIDS)))
+def test_counting_sort_and_cells_exact(pg, orc, gi):
+    g = O.Grid.make(**GRIDS[gi])
+    s = scramble(orc.make_plasma(g, 6, 0.1, 300 + gi), gi)
+    s["y"][:4] = [-1e-18, 1e30, -1e30, np.nextafter(g.oy + g.ny * g.dy, 0)]
+    perm, starts, counts = orc.counting_sort(g, s)
+    gp, gs, gc = pg.counting_sort(s, to_pg_grid(g))
+    assert np.array_equal(gp, perm) and np.array_equal(gs, starts) and np.array_equal(gc, counts)
+    assert np.array_equal(pg.cells(s, to_pg_grid(g)), orc.cells(g, s))
+
+
+@pytest.mark.parametrize("gi", range(len(GRIDS)))
+def test_advance_bit_exact(pg, orc, gi):
+    g = O.Grid.make(**GRIDS[gi])
+    ms = min(g.dx, g.dy, g.dz)
+    s = orc.make_plasma(g, 4, 0.9 * ms, 400 + gi)  # hot: many crossings and wraps
+    sp = pg.ParticleSoA.from_dict(s)
+    G = to_pg_grid(g)
+    for _ in range(5):
+        m = orc.advance(g, 0.5, s)
+        f = pg.advance(sp, 0.5, G)
+        assert f == m / len(s["x"])
+        for a in ("x", "y", "z"):
+            assert np.array_equal(getattr(sp, a), s[a])
+
+
+def test_single_particle_kats(pg):
+    G = pg.Grid.make(4)
+    one = dict(x=[1.0], y=[2.0], z=[3.0], vx=[0.5], vy=[-1.0], vz=[0.25], w=[3.0])  # test_pipeline.cpp:76-90
+    J = pg.deposit_scalar(one, G, pg.CIC, q=2.0)
+    node = G.linear_id(1, 2, 3)
+    assert J.jx[node] == pytest.approx(3.0, rel=1e-15) and J.jy[node] == pytest.approx(-6.0, rel=1e-15)
+    assert np.count_nonzero(J.jx) == 1
+    one.update(x=[1.3], y=[2.3], z=[3.3])
+    J = pg.deposit_scalar(one, G, pg.QSP, q=2.0)
+    assert np.count_nonzero(J.jx) == 64
+    assert sum(J.component_sums()) == pytest.approx(3.0 - 6.0 + 1.5, rel=1e-13)
+    J2 = pg.deposit_scalar(one, G, pg.TSC, q=2.0)
+    assert np.count_nonzero(J2.jx) == 27
+    G6 = pg.Grid.make(6)  # test_acceptance.cpp:322-341
+    one = dict(x=[2.3], y=[3.45], z=[1.7], vx=[0.4], vy=[-0.2], vz=[0.1], w=[1.5])
+    J = pg.deposit_scalar(one, G6, pg.QSP, q=-2.0)
+    for c in range(3):
+        assert np.count_nonzero(J.component(c)) == 64
+
+
+def test_empty_inputs(pg):
+    G = pg.Grid.make(4)
+    empty = {k: np.zeros(0) for k in ("x", "y", "z", "vx", "vy", "vz", "w")}
+    for order in (1, 2, 3):
+        J = pg.deposit_scalar(empty, G, order)
+        assert not np.any(J.jx) and not np.any(J.jy) and not np.any(J.jz)
+        assert not np.any(pg.deposit_density(empty, G, order, np.zeros(0)))
+    perm, starts, counts = pg.counting_sort(empty, G)
+    assert len(perm) == 0 and not np.any(counts)
+
+
+def test_errors_map_to_reference_exceptions(pg):
+    G = pg.Grid.make(4)
+    bad = dict(x=[np.nan], y=[1.0], z=[1.0], vx=[0.0], vy=[0.0], vz=[0.0], w=[1.0])
+    with pytest.raises(pg.InvalidArgument):
+        pg.deposit_scalar(bad, G, 1)
+    with pytest.raises(pg.InvalidArgument):
+        pg.counting_sort(bad, G)
+    ok = dict(x=[1.0], y=[1.0], z=[1.0], vx=[0.0], vy=[0.0], vz=[0.0], w=[1.0])
+    with pytest.raises(pg.InvalidArgument):
+        pg.deposit_scalar(ok, G, 4)
+    fast = pg.ParticleSoA.from_dict(dict(ok, vx=[2.5]))
+    with pytest.raises(pg.DomainError):
+        pg.advance(fast, 0.5, G)
+    with pytest.raises(pg.InvalidArgument):
+        pg.deposit_scalar(ok, pg.Grid.make(0, 4, 4), 1)
+
+
+def test_current_on_tiny_grids_aliasing(pg, orc):
+    """Grids smaller than the stencil window: the periodic footprint aliases
+    onto itself; every halo node is reduced, never overwritten."""
+    for dims in [(1, 1, 1), (2, 3, 1), (3, 3, 3), (2, 2, 9)]:
+        g = O.Grid.make(*dims)
+        s = orc.make_plasma(g, 9, 0.1, 9)
+        for order in (1, 2, 3):
+            want = orc.deposit_current(g, order, s, 1.0)
+            J = pg.deposit_scalar(s, to_pg_grid(g), order, q=1.0)
+            assert peak_rel_err((J.jx, J.jy, J.jz), want) <= J_TOL, (dims, order)
+
+
+# ------------------------------------------------------------------- sessions
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_session_lockstep_vs_oracle(pg, orc, order):
+    g = O.Grid.make(12, 10, 9)
+    s = orc.make_plasma(g, 6, 0.35, 31)
+    q = -1.0
+    G = to_pg_grid(g)
+    with pg.Session(G, order=order) as S:
+        S.upload(s, q=q)
+        perm, _, _ = orc.counting_sort(g, s)
+        cur = {k: np.ascontiguousarray(v[perm]) for k, v in s.items()}
+        for step in range(6):
+            moved = orc.advance(g, 0.5, cur)
+            st = S.step(0.5, pg.STEP_PUSH | pg.STEP_SORT | pg.STEP_CURRENT | pg.STEP_DENSITY)
+            assert st["moved"] == moved
+            p = S.particles()
+            mine, want = np.argsort(p.id), np.argsort(cur["id"])
+            for a in ("x", "y", "z", "vx", "vy", "vz", "w"):
+                assert np.array_equal(getattr(p, a)[mine], cur[a][want])
+            # bins: every particle sits in the bin of its cell; storage is cell-sorted
+            off, cnt = S.bins()
+            bin_of = np.repeat(np.arange(G.ncells, dtype=np.uint32), cnt.astype(np.int64))
+            assert np.array_equal(bin_of, orc.cells(g, {"x": p.x, "y": p.y, "z": p.z}))
+            # J against the oracle; rho bit-exact against the oracle on the GPU's storage order
+            pd = {"x": p.x, "y": p.y, "z": p.z, "vx": p.vx, "vy": p.vy, "vz": p.vz, "w": p.w}
+            J = S.current()
+            assert peak_rel_err((J.jx, J.jy, J.jz), orc.deposit_current(g, order, pd, q)) <= J_TOL
+            assert np.array_equal(S.density(), orc.deposit_density(g, order, pd, q * p.w))
+
+
+def test_session_overflow_rebuild(pg, orc):
+    """No slack at all: every arrival overflows, so every step with movers
+    rebuilds (Gpma::rebuild, gpma.hpp:119-122, :130-143); results unchanged."""
+    g = O.Grid.make(8)
+    s = orc.make_plasma(g, 4, 0.6, 5)
+    G = to_pg_grid(g)
+    with pg.Session(G, order=3, gap_ratio=0.0, min_gap=0) as S:
+        S.upload(s, q=1.0)
+        assert S.capacity == len(s["x"])
+        perm, _, _ = orc.counting_sort(g, s)
+        cur = {k: np.ascontiguousarray(v[perm]) for k, v in s.items()}
+        rebuilt = 0
+        for _ in range(4):
+            orc.advance(g, 0.5, cur)
+            st = S.step(0.5, pg.STEP_DEFAULT)
+            rebuilt += st["rebuilt"]
+            assert st["overflowed"] > 0
+            p = S.particles()
+            off, cnt = S.bins()
+            assert int(cnt.sum()) == len(s["x"])
+            bin_of = np.repeat(np.arange(G.ncells, dtype=np.uint32), cnt.astype(np.int64))
+            assert np.array_equal(bin_of, orc.cells(g, {"x": p.x, "y": p.y, "z": p.z}))
+            assert np.array_equal(np.sort(p.id), np.sort(cur["id"]))
+            J = S.current()
+            pd = {"x": p.x, "y": p.y, "z": p.z, "vx": p.vx, "vy": p.vy, "vz": p.vz, "w": p.w}
+            assert peak_rel_err((J.jx, J.jy, J.jz), orc.deposit_current(g, 3, pd, 1.0)) <= J_TOL
+        assert rebuilt == 4
+
+
+def test_session_global_sort_and_stats(pg, orc):
+    g = O.Grid.make(10)
+    s = orc.make_plasma(g, 8, 0.3, 8)
+    G = to_pg_grid(g)
+    with pg.Session(G, order=1) as S:
+        S.upload(s, q=-1.0)
+        cap0 = S.capacity
+        for _ in range(3):
+            st = S.step(0.5)
+        assert st["capacity"] == cap0 and st["num_particles"] == len(s["x"])
+        assert st["empty_slot_ratio"] == pytest.approx((cap0 - len(s["x"])) / cap0)
+        J0 = S.current()
+        st = S.step(0.5, pg.STEP_CURRENT | pg.STEP_GLOBAL_SORT)
+        assert st["global_sorted"] == 1
+        off, cnt = S.bins()
+        caps = np.diff(off.astype(np.int64))
+        assert np.array_equal(caps, np.ceil(cnt * 1.25).astype(np.int64) + 2)
+        S.step(0.5, pg.STEP_CURRENT)
+        J1 = S.current()
+        assert peak_rel_err((J1.jx, J1.jy, J1.jz), (J0.jx, J0.jy, J0.jz)) <= J_TOL
+
+
+def test_session_generator_matches_cpu_generator(pg, orc):
+    g = O.Grid.make(6, 5, 4)
+    with pg.Session(to_pg_grid(g), order=3) as S:
+        S.generate_plasma(4, 0.05, seed=3)
+        p = S.particles()
+    s = orc.make_plasma(g, 4, 0.05, 3)
+    mine, want = np.argsort(p.id), np.argsort(s["id"])
+    for a in ("x", "y", "z", "w"):
+        assert np.array_equal(getattr(p, a)[mine], s[a][want])  # integer-hash uniforms: exact
+    for a in ("vx", "vy", "vz"):
+        assert np.allclose(getattr(p, a)[mine], s[a][want], rtol=1e-14, atol=1e-17)  # libm last ulp
+
+
+def test_launch_counter_moves(pg, orc):
+    before = pg.kernel_launches()
+    g = O.Grid.make(4)
+    s = orc.make_plasma(g, 2, 0.1, 1)
+    pg.deposit_scalar(s, to_pg_grid(g), 3)
+    assert pg.kernel_launches() > before
