@@ -192,7 +192,7 @@ PICGPU_API int picgpu_session_download_density(picgpu_session* s, double* rho);
 PICGPU_API int picgpu_session_device_fields(picgpu_session* s, double** j, double** rho);
 /* Accumulated per-phase device times (ms) and launch counts since the last
  * reset, recorded only with PICGPU_SESSION_TIMING.  Phases:
- * 0 push+detect, 1 migrate (compact+insert), 2 rebuild/global sort, 3 deposit J,
+ * 0 push + detect + migrate + borrow, 1 reserved, 2 rebuild/global sort, 3 deposit J,
  * 4 deposit rho, 5 zero fields. */
 #define PICGPU_NPHASES 6
 PICGPU_API int picgpu_session_phase_times(picgpu_session* s, double* ms, uint64_t* launches, int nphases);

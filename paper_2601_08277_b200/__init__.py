@@ -35,7 +35,7 @@ OK, EINVAL, ERANGE, ELENGTH, ELOGIC, EDOMAIN, ECUDA, ENCCL, ENOMEM = range(9)
 STEP_PUSH, STEP_SORT, STEP_CURRENT, STEP_DENSITY, STEP_GLOBAL_SORT, STEP_NO_SYNC = 1, 2, 4, 8, 16, 32
 STEP_DEFAULT = STEP_PUSH | STEP_SORT | STEP_CURRENT
 SESSION_TIMING = 1
-PHASES = ("push_detect", "migrate", "rebuild_or_global_sort", "deposit_current", "deposit_density", "zero_fields")
+PHASES = ("push_sort", "reserved", "rebuild_or_global_sort", "deposit_current", "deposit_density", "zero_fields")
 
 
 class PicError(RuntimeError):
@@ -233,10 +233,10 @@ class ParticleSoA:
 
     def __post_init__(self):
         for k in ("x", "y", "z", "vx", "vy", "vz", "w"):
-            setattr(self, k, _f64(getattr(self, k)))
+            setattr(self, k, np.array(getattr(self, k), dtype=np.float64, copy=True))
         if self.id is None:
             self.id = np.arange(len(self.x), dtype=np.uint64)
-        self.id = np.ascontiguousarray(self.id, dtype=np.uint64)
+        self.id = np.array(self.id, dtype=np.uint64, copy=True)
 
     @classmethod
     def from_dict(cls, d, q=None):

@@ -61,6 +61,8 @@ GridD make_grid(const picgpu_grid& h) {
     g.Lz = h.nz * h.dz;
     g.pow2x = is_pow2(h.dx); g.pow2y = is_pow2(h.dy); g.pow2z = is_pow2(h.dz);
     g.inv_dx = 1.0 / h.dx; g.inv_dy = 1.0 / h.dy; g.inv_dz = 1.0 / h.dz;
+    g.pow2Lx = is_pow2(g.Lx); g.pow2Ly = is_pow2(g.Ly); g.pow2Lz = is_pow2(g.Lz);
+    g.inv_Lx = 1.0 / g.Lx; g.inv_Ly = 1.0 / g.Ly; g.inv_Lz = 1.0 / g.Lz;
     g.ncells = (uint32_t)nc;
     return g;
 }
@@ -461,62 +463,97 @@ static void accumulate_phase(picgpu_session* s, int phase, int e0, int e1, uint6
     s->phase_launches[phase] += launches;
 }
 
+// Deposits requested by `flags`, enqueued on the session stream; events
+// ev[2..6] bracket them when timing is on.
+static void enqueue_deposits(picgpu_session* s, uint32_t flags, uint64_t* lj, uint64_t* lr) {
+    BinStore& bs = s->store;
+    const cudaStream_t st = s->st;
+    const GridD& g = bs.g;
+    const bool T = s->timing;
+    if (flags & PICGPU_STEP_CURRENT) {
+        const uint64_t l0 = g_launches.load();
+        if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[2], st));
+        PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)g.ncells * 24, st));
+        if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[3], st));
+        if (bs.n)
+            launch_deposit_current(s->order, g, bs.A.soa(), bs.d_off(), bs.d_cnt(), s->q, s->J.as<double>(),
+                                   bs.num_sms, st);
+        if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[4], st));
+        *lj = g_launches.load() - l0;
+    }
+    if (flags & PICGPU_STEP_DENSITY) {
+        check_density_grid(bs.hg, s->order);
+        const uint64_t l0 = g_launches.load();
+        if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[5], st));
+        s->rho.ensure((size_t)g.ncells * 8);
+        s->dscratch.ensure(density_scratch_bytes(s->order, bs.capacity));
+        launch_deposit_density(s->order, g, bs.A.soa(), nullptr, s->q, bs.d_off(), bs.d_cnt(), bs.capacity,
+                               s->dscratch.p, s->rho.as<double>(), st);
+        if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[6], st));
+        *lr = g_launches.load() - l0;
+    }
+}
+
+// One step of the reference loop (simulation.hpp:753-829), device-resident:
+// [push + incremental sort] -> [J] -> [rho] -> [global sort].  Everything is
+// enqueued back to back; the host waits once, at the end, for the sorter's
+// counters.  In the rare step whose arrivals found no slack even after
+// borrowing, the bins are rebuilt and the deposits re-run on them.
 int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_step_stats* out) {
     return guard([&] {
         set_device(s);
         BinStore& bs = s->store;
         const cudaStream_t st = s->st;
-        const GridD& g = bs.g;
         if ((flags & PICGPU_STEP_PUSH) && !(flags & PICGPU_STEP_SORT))
             throw Status{PICGPU_EINVAL, "session_step: PUSH requires SORT (push and move detection are fused)"};
+        if ((flags & PICGPU_STEP_DENSITY)) check_density_grid(bs.hg, s->order);
         picgpu_step_stats stats{};
         const uint64_t rebuilds0 = bs.rebuilds;
         const bool T = s->timing;
-        if (flags & PICGPU_STEP_SORT) {
+        const bool sort = (flags & PICGPU_STEP_SORT) != 0;
+        uint64_t ls = 0, lj = 0, lr = 0;
+        if (sort) {
             const double cap2 = (flags & PICGPU_STEP_PUSH) ? cap2_of(bs.hg, dt) : 0.0;
             const uint64_t l0 = g_launches.load();
             if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
-            const StepCounters c = bs.incremental_step((flags & PICGPU_STEP_PUSH) != 0, dt, cap2);
-            if (T) {
-                PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
-                PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[1]));
-                accumulate_phase(s, bs.rebuilds != rebuilds0 ? 2 : 0, 0, 1, g_launches.load() - l0);
-            }
+            bs.enqueue_incremental((flags & PICGPU_STEP_PUSH) != 0, dt, cap2);
+            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
+            ls = g_launches.load() - l0;
+        }
+        enqueue_deposits(s, flags, &lj, &lr);
+        if (sort) {
+            StepCounters c{};
+            const bool rebuilt = bs.finish_incremental(c);
             if (c.err == PICGPU_EDOMAIN)
                 throw Status{c.err, "advance: particle displacement exceeds the single-cell cap"};
             if (c.err) throw Status{c.err, "cell_of: non-finite particle position"};
             stats.moved = c.moved;
-            stats.inserts = std::min<uint64_t>(c.nmovers, bs.mcap) ;
-            stats.overflowed = c.noverflow;
-        }
-        if (flags & PICGPU_STEP_CURRENT) {
-            const uint64_t l0 = g_launches.load();
-            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[2], st));
-            PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)g.ncells * 24, st));
-            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[3], st));
-            if (bs.n)
-                launch_deposit_current(s->order, g, bs.A.soa(), bs.d_off(), bs.d_cnt(), s->q, s->J.as<double>(),
-                                       bs.num_sms, st);
+            stats.inserts = std::min<uint64_t>(c.nmovers, bs.mcap);
+            stats.overflowed = c.nborrowed + c.noverflow;
             if (T) {
-                PICGPU_CUDA_TRY(cudaEventRecord(s->ev[4], st));
-                PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[4]));
+                accumulate_phase(s, 0, 0, 1, ls);
+                if (flags & PICGPU_STEP_CURRENT) {
+                    accumulate_phase(s, 5, 2, 3, 0);
+                    accumulate_phase(s, 3, 3, 4, lj);
+                }
+                if (flags & PICGPU_STEP_DENSITY) accumulate_phase(s, 4, 5, 6, lr);
+            }
+            if (rebuilt) {
+                if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
+                enqueue_deposits(s, flags, &lj, &lr);  // the bins changed: deposit again
+                if (T) {
+                    PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
+                    PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[1]));
+                    accumulate_phase(s, 2, 0, 1, lj + lr);
+                }
+            }
+        } else if (T && (flags & (PICGPU_STEP_CURRENT | PICGPU_STEP_DENSITY))) {
+            PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+            if (flags & PICGPU_STEP_CURRENT) {
                 accumulate_phase(s, 5, 2, 3, 0);
-                accumulate_phase(s, 3, 3, 4, g_launches.load() - l0);
+                accumulate_phase(s, 3, 3, 4, lj);
             }
-        }
-        if (flags & PICGPU_STEP_DENSITY) {
-            check_density_grid(bs.hg, s->order);
-            const uint64_t l0 = g_launches.load();
-            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[5], st));
-            s->rho.ensure((size_t)g.ncells * 8);
-            s->dscratch.ensure(density_scratch_bytes(s->order, bs.capacity));
-            launch_deposit_density(s->order, g, bs.A.soa(), nullptr, s->q, bs.d_off(), bs.d_cnt(), bs.capacity,
-                                   s->dscratch.p, s->rho.as<double>(), st);
-            if (T) {
-                PICGPU_CUDA_TRY(cudaEventRecord(s->ev[6], st));
-                PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[6]));
-                accumulate_phase(s, 4, 5, 6, g_launches.load() - l0);
-            }
+            if (flags & PICGPU_STEP_DENSITY) accumulate_phase(s, 4, 5, 6, lr);
         }
         if (flags & PICGPU_STEP_GLOBAL_SORT) {
             const uint64_t l0 = g_launches.load();

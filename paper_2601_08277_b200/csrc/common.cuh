@@ -22,6 +22,8 @@ struct GridD {
     double Lx, Ly, Lz;        // GridSpec::length(axis) = cells * spacing (grid.hpp:46)
     double inv_dx, inv_dy, inv_dz;
     int pow2x, pow2y, pow2z;  // spacing is a power of two: (x-o)*inv == (x-o)/h exactly
+    double inv_Lx, inv_Ly, inv_Lz;
+    int pow2Lx, pow2Ly, pow2Lz;  // same for the box lengths (wrap_position)
     uint32_t ncells;
 };
 

@@ -81,9 +81,11 @@ __device__ __forceinline__ void copy_particle(const Soa& src, uint64_t s, const 
     dst.id[d] = src.id[s];
 }
 
-// detail::wrap_position, workload.hpp:128-132
-__device__ __forceinline__ double wrap_position(double x, double origin, double length) {
-    double r = __dsub_rn(x, __dmul_rn(length, floor(__ddiv_rn(__dsub_rn(x, origin), length))));
+// detail::wrap_position, workload.hpp:128-132 (a power-of-two length divides
+// exactly as a multiply by its reciprocal).
+__device__ __forceinline__ double wrap_position(double x, double origin, double length, double inv, int pow2) {
+    const double t = __dsub_rn(x, origin);
+    double r = __dsub_rn(x, __dmul_rn(length, floor(pow2 ? __dmul_rn(t, inv) : __ddiv_rn(t, length))));
     if (__dsub_rn(r, origin) >= length) r = origin;
     return r;
 }
@@ -94,9 +96,9 @@ __device__ __forceinline__ bool push_one(const GridD& g, double dt, double cap2,
                                          double vx, double vy, double vz) {
     const double v2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
     if (v2 > cap2) return false;
-    x = wrap_position(__dadd_rn(x, __dmul_rn(vx, dt)), g.ox, g.Lx);
-    y = wrap_position(__dadd_rn(y, __dmul_rn(vy, dt)), g.oy, g.Ly);
-    z = wrap_position(__dadd_rn(z, __dmul_rn(vz, dt)), g.oz, g.Lz);
+    x = wrap_position(__dadd_rn(x, __dmul_rn(vx, dt)), g.ox, g.Lx, g.inv_Lx, g.pow2Lx);
+    y = wrap_position(__dadd_rn(y, __dmul_rn(vy, dt)), g.oy, g.Ly, g.inv_Ly, g.pow2Ly);
+    z = wrap_position(__dadd_rn(z, __dmul_rn(vz, dt)), g.oz, g.Lz, g.inv_Lz, g.pow2Lz);
     return true;
 }
 
@@ -306,23 +308,45 @@ __global__ void __launch_bounds__(256) k_push_detect(const GridD g, const Soa A,
     }
     if (local_moved) atomicAdd(&smoved, (unsigned long long)local_moved);
     __syncthreads();
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    // Stable in-bin compaction of the stayers, one warp per bin with
+    // departures: ballot the keep-mask 32 slots at a time, every kept lane
+    // loads its particle, then stores it at its rank (reads of a chunk all
+    // precede its writes, and writes never reach a later chunk's slots).
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int b = warp; b < nb; b += nwarps) {
         if (sdep[b] == 0) continue;
         const uint32_t lo = so[b], hi = so[b] + sc[b];
         uint32_t wpos = lo;
-        for (uint32_t r = lo; r < hi; ++r) {
-            if (mflag[r] == 1) continue;
-            if (wpos != r) copy_particle(A, r, A, wpos);
-            ++wpos;
+        for (uint32_t base = lo; base < hi; base += 32) {
+            const uint32_t r = base + lane;
+            const bool keep = r < hi && mflag[r] != 1;
+            const unsigned km = __ballot_sync(0xffffffffu, keep);
+            const uint32_t dst = wpos + __popc(km & ((1u << lane) - 1u));
+            double px = 0, py = 0, pz = 0, pvx = 0, pvy = 0, pvz = 0, pw = 0;
+            uint64_t pid = 0;
+            const bool mv = keep && dst != r;
+            if (mv) {
+                px = A.x[r]; py = A.y[r]; pz = A.z[r];
+                pvx = A.vx[r]; pvy = A.vy[r]; pvz = A.vz[r];
+                pw = A.w[r]; pid = A.id[r];
+            }
+            __syncwarp();
+            if (mv) {
+                A.x[dst] = px; A.y[dst] = py; A.z[dst] = pz;
+                A.vx[dst] = pvx; A.vy[dst] = pvy; A.vz[dst] = pvz;
+                A.w[dst] = pw; A.id[dst] = pid;
+            }
+            __syncwarp();
+            wpos += __popc(km);
         }
-        cnt[c0 + b] = wpos - lo;
+        if (lane == 0) cnt[c0 + b] = wpos - lo;
     }
     if (threadIdx.x == 0 && smoved) atomicAdd(&ctr->moved, smoved);
 }
 
 // Migration: every recorded mover takes the next slot of its target bin's
 // slack (atomic tail cursor); arrivals beyond the slack go to the overflow list.
-__global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32_t* __restrict__ mpos, uint32_t mcap,
+__global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32_t mcap,
                          StepCounters* ctr, const Soa A, const uint32_t* __restrict__ off, uint32_t* cnt,
                          uint32_t* __restrict__ ovf) {
     const uint32_t nm = min(ctr->nmovers, mcap);
@@ -333,20 +357,53 @@ __global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32
         if (pos < cap) {
             copy_particle(M, i, A, (uint64_t)lo + pos);
         } else {
-            mpos[i] = pos;
             ovf[atomicAdd(&ctr->noverflow, 1u)] = i;
         }
     }
 }
 
-// Overflowed arrivals land after their bin's held particles in the new layout.
-__global__ void k_place_overflow(const Soa M, const uint32_t* __restrict__ mcell, const uint32_t* __restrict__ mpos,
-                                 const uint32_t* __restrict__ ovf, uint32_t novf, const Soa dst,
-                                 const uint32_t* __restrict__ doff) {
-    const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
-    if (o >= novf) return;
-    const uint32_t i = ovf[o];
-    copy_particle(M, i, dst, (uint64_t)doff[mcell[i]] + mpos[i]);
+// borrow_insert (gpma.hpp:337-370) for the few arrivals that found their bin
+// full: the nearest of the next `scan` bins with slack lends one slot; every
+// boundary in (d, donor] moves up by one and each bin in between hands its
+// first particle to its own tail (the slot just vacated above it), so bins
+// stay contiguous and cell-exact.  One thread walks the overflow list in order
+// (there are a handful per step); entries with no donor are compacted to the
+// front of `ovf` and left for the full re-sort.
+__global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restrict__ mcell, uint32_t* ovf,
+                         const Soa A, uint32_t* off, const uint32_t* __restrict__ cnt, uint32_t ncells, int scan) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint32_t n = ctr->noverflow;
+    if (n == 0) return;
+    uint32_t left = 0;
+    for (uint32_t o = 0; o < n; ++o) {
+        const uint32_t i = ovf[o];
+        const uint32_t d = mcell[i];
+        int64_t donor = -1;
+        const uint64_t lim = (uint64_t)d + (uint64_t)scan;
+        const uint32_t last = (uint32_t)(lim < (uint64_t)ncells - 1 ? lim : (uint64_t)ncells - 1);
+        for (uint32_t b = d + 1; b <= last && d + 1 < ncells; ++b)
+            if (cnt[b] < off[b + 1] - off[b]) {
+                donor = b;
+                break;
+            }
+        if (donor < 0) {
+            ovf[left++] = i;
+            continue;
+        }
+        const uint32_t slot = off[d + 1];  // becomes bin d's new last slot
+        uint32_t above = off[(uint32_t)donor + 1];  // old lower boundary of the bin above j
+        for (uint32_t j = (uint32_t)donor; j > d; --j) {
+            const uint32_t oj = off[j];
+            const uint32_t held = min(cnt[j], above - oj);  // capacity before this borrow
+            // donor: its free tail slot; a full bin: `above`, just vacated by bin j+1
+            if (held > 0) copy_particle(A, oj, A, (uint64_t)oj + held);
+            off[j] = oj + 1;
+            above = oj;
+        }
+        copy_particle(M, i, A, slot);
+    }
+    ctr->noverflow = left;
+    ctr->nborrowed = n - left;
 }
 
 // Overflowed movers appended after a packed store (mover-buffer fallback).
@@ -608,79 +665,65 @@ void BinStore::ensure_movers(size_t m) {
     if (m <= mcap) return;
     M.ensure(m);
     mcell.ensure(m * 4);
-    mpos.ensure(std::max<size_t>(m, n + 1) * 4);
     ovf.ensure(m * 4);
     mcap = m;
 }
 
-StepCounters BinStore::incremental_step(bool push, double dt, double cap2) {
+void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
     const size_t nc = g.ncells;
     ensure_movers(std::max<size_t>(size_t(1) << 16, n / 4));
     StepCounters* ctr = counters.as<StepCounters>();
     PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
-    if (nc && n) {
-        const int blocks = div_up((long long)nc, BPB);
-        if (push)
-            k_push_detect<true><<<blocks, 256, 0, st>>>(g, A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                        mflag.as<uint8_t>(), dt, cap2, M.soa(), mcell.as<uint32_t>(),
-                                                        (uint32_t)mcap, ctr);
-        else
-            k_push_detect<false><<<blocks, 256, 0, st>>>(g, A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                         mflag.as<uint8_t>(), dt, cap2, M.soa(),
-                                                         mcell.as<uint32_t>(), (uint32_t)mcap, ctr);
-        note_launch();
-        PICGPU_CUDA_TRY(cudaGetLastError());
-        k_insert<<<num_sms * 4, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), mpos.as<uint32_t>(), (uint32_t)mcap, ctr,
-                                              A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>());
-        note_launch();
-        PICGPU_CUDA_TRY(cudaGetLastError());
-    }
+    if (!nc || !n) return;
+    const int blocks = div_up((long long)nc, BPB);
+    if (push)
+        k_push_detect<true><<<blocks, 256, 0, st>>>(g, A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                    mflag.as<uint8_t>(), dt, cap2, M.soa(), mcell.as<uint32_t>(),
+                                                    (uint32_t)mcap, ctr);
+    else
+        k_push_detect<false><<<blocks, 256, 0, st>>>(g, A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                     mflag.as<uint8_t>(), dt, cap2, M.soa(), mcell.as<uint32_t>(),
+                                                     (uint32_t)mcap, ctr);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+    k_insert<<<num_sms * 4, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap, ctr, A.soa(),
+                                          off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>());
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+    // borrow_insert for the few full-bin arrivals; exits at once when there are none
+    k_borrow<<<1, 32, 0, st>>>(ctr, M.soa(), mcell.as<uint32_t>(), ovf.as<uint32_t>(), A.soa(), off.as<uint32_t>(),
+                               cnt.as<uint32_t>(), (uint32_t)nc, kBorrowScanBins);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
     PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, ctr, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
+}
+
+bool BinStore::finish_incremental(StepCounters& out) {
+    const size_t nc = g.ncells;
     PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
-    StepCounters out = *hcounters;
-    if (out.err) return out;
-    if (out.nmovers > mcap) {
-        // Mover buffer overflow: stale movers still sit in their old bins.
-        // Compact everything (bins + overflowed arrivals) and re-sort fully.
-        compact_to_B();
-        uint64_t held = 0;
-        {
-            unsigned int h32 = 0;
-            PICGPU_CUDA_TRY(cudaMemcpyAsync(&h32, off2.as<uint32_t>() + nc, 4, cudaMemcpyDeviceToHost, st));
-            PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
-            held = h32;
-        }
-        if (out.noverflow) {
-            k_append_overflow<<<div_up(out.noverflow, 256), 256, 0, st>>>(M.soa(), ovf.as<uint32_t>(), out.noverflow,
-                                                                         B.soa(), held);
-            note_launch();
-        }
-        full_sort_from_B(held + out.noverflow);
-        ++rebuilds;
-        ensure_movers(out.nmovers + out.nmovers / 2);
-    } else if (out.noverflow) {
-        // Gpma::rebuild (gpma.hpp:130-143): fresh slack from the true counts,
-        // held particles keep their slot order, overflowed arrivals follow.
-        k_caps_from_cnt<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt.as<uint32_t>(), (uint32_t)nc,
-                                                                        caps.as<uint32_t>(), onepg, min_gap);
-        note_launch();
-        layout_from_counts(n);
-        B.ensure(capacity_next);
-        mflag.ensure(capacity_next + 1);
-        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                               B.soa(), off2.as<uint32_t>(), (uint32_t)nc);
-        note_launch();
-        k_place_overflow<<<div_up(out.noverflow, 256), 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(),
-                                                                    mpos.as<uint32_t>(), ovf.as<uint32_t>(),
-                                                                    out.noverflow, B.soa(), off2.as<uint32_t>());
+    out = *hcounters;
+    if (out.err) return false;
+    const bool mover_overflow = out.nmovers > mcap;
+    const uint32_t left = out.noverflow;  // unplaced: no donor, or everything after a mover overflow
+    borrowed += out.nborrowed;
+    if (!mover_overflow && !left) return false;
+    // Gpma::rebuild (gpma.hpp:119-122, :130-143) generalised: either the
+    // mover buffer overflowed (stale movers still sit in their old bins) or an
+    // arrival found no donor within the scan window.  Compact every held
+    // particle plus the unplaced arrivals and re-sort fully.
+    compact_to_B();
+    unsigned int h32 = 0;
+    PICGPU_CUDA_TRY(cudaMemcpyAsync(&h32, off2.as<uint32_t>() + nc, 4, cudaMemcpyDeviceToHost, st));
+    PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    if (left) {
+        k_append_overflow<<<div_up(left, 256), 256, 0, st>>>(M.soa(), ovf.as<uint32_t>(), left, B.soa(), h32);
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
-        swap_soa(A, B);
-        swap_buf(off, off2);
-        capacity = capacity_next;
-        ++rebuilds;
     }
-    return out;
+    full_sort_from_B((uint64_t)h32 + left);
+    ++rebuilds;
+    if (mover_overflow) ensure_movers(out.nmovers + out.nmovers / 2);
+    return true;
 }
 
 }  // namespace picgpu

@@ -43,10 +43,12 @@ struct SoaBuf {
 struct StepCounters {
     unsigned long long moved;
     unsigned int nmovers;     // movers detected (may exceed mover capacity)
-    unsigned int noverflow;   // arrivals that found no slack
+    unsigned int noverflow;   // arrivals that found no slack (after k_borrow: those still unplaced)
     int err;                  // picgpu_status of the first device-side error
-    int pad;
+    unsigned int nborrowed;   // arrivals placed by borrowing a following bin's slack
 };
+
+constexpr int kBorrowScanBins = 4;  // GpmaConfig::borrow_scan_bins (gpma.hpp:25)
 
 struct BinStore {
     GridD g{};
@@ -61,7 +63,7 @@ struct BinStore {
     DevBuf keys, keys2, skeys, vals, vals2, start, endp, caps, cub_tmp;
     DevBuf mflag;             // per-slot mover flag (u8)
     SoaBuf M;                 // mover records
-    DevBuf mcell, mpos, ovf;  // mover target cell, insert position, overflow list
+    DevBuf mcell, ovf;        // mover target cell, overflow list
     DevBuf counters;          // StepCounters
     StepCounters* hcounters = nullptr;  // pinned mirror
 
@@ -69,6 +71,7 @@ struct BinStore {
     uint64_t capacity = 0;    // slots in use (off[ncells])
     size_t mcap = 0;          // mover record capacity
     uint64_t rebuilds = 0;
+    uint64_t borrowed = 0;    // arrivals placed by borrowing a neighbour's slack
 
     void init(const picgpu_grid& grid, double gap_ratio, uint32_t min_gap, cudaStream_t stream);
     ~BinStore();
@@ -82,9 +85,15 @@ struct BinStore {
     // A's valid particles compacted into B in storage order (bins ascending);
     // returns the packed offsets in `off2` (exclusive scan of cnt).
     void compact_to_B();
-    // One incremental step: push (optional) + detect + in-bin compaction +
-    // migration; rebuilds on overflow.  Returns counters (synchronises).
-    StepCounters incremental_step(bool push, double dt, double cap2);
+    // One incremental step, enqueued without host synchronisation: push
+    // (optional) + detect + in-bin compaction, migration into slack, borrow
+    // from the following bins for full bins; counters copied to the host.
+    void enqueue_incremental(bool push, double dt, double cap2);
+    // Synchronises, reads the counters and, if an arrival found no slack even
+    // after borrowing (or the mover buffer overflowed), rebuilds by a full
+    // re-sort.  Returns true when it rebuilt (fields deposited since the
+    // enqueue must then be recomputed).
+    bool finish_incremental(StepCounters& out);
 
     uint32_t* d_off() const { return off.as<uint32_t>(); }
     uint32_t* d_cnt() const { return cnt.as<uint32_t>(); }
