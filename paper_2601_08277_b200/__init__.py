@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpicgpu.so")
+LIB_PATH = os.environ.get("PICGPU_LIB", os.path.join(_HERE, "libpicgpu.so"))
 
 CIC, TSC, QSP = 1, 2, 3
 

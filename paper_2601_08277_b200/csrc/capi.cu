@@ -529,7 +529,7 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
             if (c.err) throw Status{c.err, "cell_of: non-finite particle position"};
             stats.moved = c.moved;
             stats.inserts = std::min<uint64_t>(c.nmovers, bs.mcap);
-            stats.overflowed = c.nborrowed + c.noverflow;
+            stats.overflowed = c.noverflow;
             if (T) {
                 accumulate_phase(s, 0, 0, 1, ls);
                 if (flags & PICGPU_STEP_CURRENT) {

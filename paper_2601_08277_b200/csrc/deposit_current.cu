@@ -9,12 +9,16 @@
 //  * A CTA owns a PX x PY tile of cell "pencils" (x-y) and walks a z-chunk of
 //    cells.  Particles are read from the cell bins maintained by the sorter
 //    (sorter.cu), i.e. cell-local and coalesced.
-//  * A group of G lanes owns one pencil.  Each lane owns a fixed sub-block of
-//    the per-cell outer product (its ix/jy subset x 3 components) for a
-//    sliding window of W z-planes held in REGISTERS: after the pencil's cell k
-//    is done, plane k+OFF can receive nothing more from this pencil, so it is
-//    emitted and the window slides.  The contraction over the cell's particles
-//    therefore never touches shared or global memory (FP64 FMA in registers).
+//  * G lanes own one pencil.  Lane l owns the jy-slice(s) of the per-cell outer
+//    product for ALL ix, all 3 components and a sliding window of W z-planes,
+//    held in REGISTERS (QSP: 4 ix x 3 c x 4 kz = 48 accumulators).  After the
+//    pencil's cell k is done, plane k+OFF can receive nothing more from it, so
+//    it is emitted and the window slides.  The contraction over a cell's
+//    particles never touches shared or global memory: per particle a lane
+//    reads 12+1+4 staged weights (conflict-free LDS.128) and issues 4 DMUL +
+//    48 DFMA.  (FP64 DMMA was measured at the same 64 MAC/clk/SM as DFMA on
+//    B200 -- tools/fp64_pipes.cu -- and would pad the 12x16 block to 16x16,
+//    so the register-blocked DFMA form is the faster one.)
 //  * Emitted planes of all pencils meet in a shared-memory patch buffer
 //    (double-buffered, one __syncthreads per z-step); a gather pass sums the
 //    overlapping W x W patches per node (no shared-memory atomics -- FP64
@@ -26,6 +30,9 @@
 // uses FMA and its own summation order.  Cell location and shape weights are
 // bit-identical to the reference so the particle always belongs to its bin.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -36,49 +43,60 @@ namespace {
 
 template <int ORDER>
 struct JCfg;
-// CIC: one lane per pencil owns the whole 2x2x2x3 block (24 accumulators); no staging.
+// CIC: one lane per pencil owns the whole 2x2x2x3 block (24 accumulators) and
+// reads its own particles (no staging; the order is HBM-bound).
 template <>
 struct JCfg<1> {
-    static constexpr int G = 1, NJ = 2, NI = 2, PX = 32, PY = 4, MINB = 4;
+    static constexpr int G = 1, PX = 32, PY = 4, MINB = 4, CH = 1;
 };
-// TSC / QSP: 8 lanes per pencil, lane = (jy, ix-half): 1 jy x 2 ix x 3 comps x 4 planes = 24 acc.
-template <>
-struct JCfg<2> {
-    static constexpr int G = 8, NJ = 1, NI = 2, PX = 8, PY = 4, MINB = 2;
-};
-template <>
-struct JCfg<3> {
-    static constexpr int G = 8, NJ = 1, NI = 2, PX = 8, PY = 4, MINB = 2;
-};
+// (TSC / QSP use the warp-per-pencil kernel below.)
 
 template <int ORDER>
 struct JLayout {
     using C = JCfg<ORDER>;
     static constexpr int W = Shape<ORDER>::W;
-    static constexpr int NP = C::PX * C::PY;
-    static constexpr int NT = NP * C::G;
-    static constexpr int REC = 5 * W;                         // a[3][W] | sy[W] | sz[W]
-    static constexpr int GSTRIDE = C::G * REC + 4;            // +32 B: de-alias groups across banks
-    static constexpr int PATCH = NP * 3 * W * W;              // one buffer
-    static constexpr int STAGE = C::G > 1 ? NP * GSTRIDE : 0;
+    static constexpr int NJ = W / C::G;                 // jy values per lane
+    static constexpr int NP = C::PX * C::PY;            // pencils per CTA
+    static constexpr int NT = NP * C::G;                // threads per CTA
+    static constexpr int REC = 5 * W + 2;               // a[3][W] | sy[W] | sz[W] | pad: 22 doubles (176 B)
+    static constexpr int PLANE = NP * REC + 2;          // one chunk slot for all pencils (+16 B skew)
+    static constexpr int STAGE = C::G > 1 ? C::CH * PLANE : 0;
+    // One emitted plane of every pencil, offset-major: [jy][ix][c][PY][PX] with
+    // a 2-double skew per (jy,ix,c) row so the 4 jy-lanes of a pencil write
+    // to distinct banks and the gather reads consecutive pencils contiguously.
+    static constexpr int PSTRIDE = NP + 2;
+    static constexpr int PATCH = W * W * 3 * PSTRIDE;
     static constexpr size_t SMEM = (size_t)(2 * PATCH + STAGE) * sizeof(double);
 };
+
+struct PData {  // one particle as read from the bins
+    double x, y, z, vx, vy, vz, w;
+};
+
+__device__ __forceinline__ void load_particle(const CSoa& p, uint32_t s, PData& d) {
+    d.x = __ldg(p.x + s);
+    d.y = __ldg(p.y + s);
+    d.z = __ldg(p.z + s);
+    d.vx = __ldg(p.vx + s);
+    d.vy = __ldg(p.vy + s);
+    d.vz = __ldg(p.vz + s);
+    d.w = __ldg(p.w + s);
+}
 
 // Per-particle prologue (shape.hpp:64-85 + particle_weights :46-50): the
 // window weights and the x-weights pre-multiplied by wq_c = (q*W)*v_c.
 template <int ORDER>
-__device__ __forceinline__ void particle_window(const GridD& g, const CSoa& p, uint32_t s, double q,
+__device__ __forceinline__ void particle_window(const GridD& g, const PData& d, double q,
                                                 double (&a)[3][Shape<ORDER>::W], double (&sy)[Shape<ORDER>::W],
                                                 double (&sz)[Shape<ORDER>::W]) {
     constexpr int W = Shape<ORDER>::W;
-    const double x = p.x[s], y = p.y[s], z = p.z[s];
-    const double qw = q * p.w[s];
-    const double wq0 = qw * p.vx[s], wq1 = qw * p.vy[s], wq2 = qw * p.vz[s];
+    const double qw = q * d.w;
+    const double wq0 = qw * d.vx, wq1 = qw * d.vy, wq2 = qw * d.vz;
     double fx, fy, fz;
     int up;
-    locate_axis(x, g.ox, g.dx, g.inv_dx, g.pow2x, g.nx, fx);
-    locate_axis(y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, fy);
-    locate_axis(z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, fz);
+    locate_axis(d.x, g.ox, g.dx, g.inv_dx, g.pow2x, g.nx, fx);
+    locate_axis(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, fy);
+    locate_axis(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, fz);
     double sx[W];
     Shape<ORDER>::weights(fx, sx, up);
     Shape<ORDER>::weights(fy, sy, up);
@@ -91,6 +109,21 @@ __device__ __forceinline__ void particle_window(const GridD& g, const CSoa& p, u
     }
 }
 
+template <int W, int NJ>
+__device__ __forceinline__ void accumulate(double (&acc)[W][NJ][W][3], const double (&a)[3][W], const double (&syv)[NJ],
+                                           const double (&sz)[W]) {
+#pragma unroll
+    for (int kz = 0; kz < W; ++kz)
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) {
+            const double b = syv[jj] * sz[kz];
+#pragma unroll
+            for (int ix = 0; ix < W; ++ix)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[kz][jj][ix][c] = fma(a[c][ix], b, acc[kz][jj][ix][c]);
+        }
+}
+
 template <int ORDER>
 __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
     deposit_current_kernel(const GridD g, const CSoa p, const uint32_t* __restrict__ off,
@@ -98,14 +131,13 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                            double* __restrict__ jy, double* __restrict__ jz, const int zlen) {
     using C = JCfg<ORDER>;
     using L = JLayout<ORDER>;
-    constexpr int W = L::W, OFF = Shape<ORDER>::OFF;
-    constexpr int G = C::G, NJ = C::NJ, NI = C::NI, PX = C::PX, PY = C::PY;
-    constexpr int JS = W / NJ;  // lanes splitting jy
+    constexpr int W = L::W, OFF = Shape<ORDER>::OFF, NJ = L::NJ;
+    constexpr int G = C::G, PX = C::PX, PY = C::PY, CH = C::CH;
     constexpr int FX = PX + W - 1, FY = PY + W - 1;
 
     extern __shared__ __align__(16) double smem[];
-    double* patch = smem;                 // [2][NP][3][W(jy)][W(ix)]
-    double* stage = smem + 2 * L::PATCH;  // [NP][GSTRIDE]
+    double* patch = smem;                 // [2][W(jy)][W(ix)][3][PSTRIDE]
+    double* stage = smem + 2 * L::PATCH;  // [CH][NP][REC] (+skew per chunk slot)
 
     const int tid = threadIdx.x;
     const int grp = tid / G, lg = tid % G;
@@ -115,146 +147,149 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
     const int k1 = min(k0 + zlen, g.nz);
     const int i = i0 + px, j = j0 + py;
     const bool pv = (i < g.nx) && (j < g.ny);
-    const int jsub = lg % JS, isub = lg / JS;
     const int pxv = min(PX, g.nx - i0), pyv = min(PY, g.ny - j0);
     const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
+    const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
+    const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
 
-    double acc[W][NJ][NI][3];
+    double acc[W][NJ][W][3];
 #pragma unroll
     for (int kz = 0; kz < W; ++kz)
 #pragma unroll
         for (int jj = 0; jj < NJ; ++jj)
 #pragma unroll
-            for (int ii = 0; ii < NI; ++ii)
+            for (int ix = 0; ix < W; ++ix)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) acc[kz][jj][ii][c] = 0.0;
+                for (int c = 0; c < 3; ++c) acc[kz][jj][ix][c] = 0.0;
+
+    // bin of this pencil's current cell, and a prefetched particle for the
+    // next chunk (loads of chunk n+1 are in flight while chunk n is consumed)
+    uint32_t c_off = 0;
+    int n_c = 0;
+    if (pv && k0 < k1) {
+        c_off = off[col + plane_cells * k0];
+        n_c = (int)cnt[col + plane_cells * k0];
+    }
+    PData nxt{};
+    if constexpr (G > 1) {
+        if (lg < n_c) load_particle(p, c_off + lg, nxt);
+    }
 
     int buf = 0;
     for (int k = k0; k < k1 + W - 1; ++k) {
         if (k < k1) {
-            uint32_t c_off = 0;
-            int n_c = 0;
-            if (pv) {
-                const uint32_t c = (uint32_t)i + (uint32_t)g.nx * ((uint32_t)j + (uint32_t)g.ny * (uint32_t)k);
-                c_off = off[c];
-                n_c = (int)cnt[c];
+            // bin of the next cell (for the cross-cell prefetch)
+            uint32_t n_off = 0;
+            int n_n = 0;
+            if (pv && k + 1 < k1) {
+                n_off = off[col + plane_cells * (k + 1)];
+                n_n = (int)cnt[col + plane_cells * (k + 1)];
             }
             if constexpr (G == 1) {
                 for (int t = 0; t < n_c; ++t) {
+                    PData d;
+                    load_particle(p, c_off + t, d);
                     double a[3][W], sy[W], sz[W];
-                    particle_window<ORDER>(g, p, c_off + t, q, a, sy, sz);
+                    particle_window<ORDER>(g, d, q, a, sy, sz);
+                    double syv[NJ];
 #pragma unroll
-                    for (int kz = 0; kz < W; ++kz)
-#pragma unroll
-                        for (int jj = 0; jj < NJ; ++jj) {
-                            const double b = sy[jsub * NJ + jj] * sz[kz];
-#pragma unroll
-                            for (int ii = 0; ii < NI; ++ii)
-#pragma unroll
-                                for (int c = 0; c < 3; ++c)
-                                    acc[kz][jj][ii][c] = fma(a[c][isub * NI + ii], b, acc[kz][jj][ii][c]);
-                        }
+                    for (int jj = 0; jj < NJ; ++jj) syv[jj] = sy[jj];
+                    accumulate<W, NJ>(acc, a, syv, sz);
                 }
             } else {
                 const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
-                double* gstage = stage + grp * L::GSTRIDE;
-                for (int base = 0; base < m; base += G) {
+                if (m == 0 && lg < n_n) load_particle(p, n_off + lg, nxt);  // empty cells: still prefetch
+                for (int base = 0; base < m; base += CH) {
+                    // prologue of this lane's particle -> staging slot (lg, grp)
                     {
-                        double* rec = gstage + lg * L::REC;
-                        const int idx = base + lg;
+                        const PData cur = nxt;
+                        const bool valid = base + lg < n_c;
+                        // prefetch the next chunk: same cell, or the next cell's first chunk
+                        if (base + CH < m) {
+                            if (base + CH + lg < n_c) load_particle(p, c_off + base + CH + lg, nxt);
+                        } else if (lg < n_n) {
+                            load_particle(p, n_off + lg, nxt);
+                        }
                         double a[3][W], sy[W], sz[W];
-                        if (idx < n_c) {
-                            particle_window<ORDER>(g, p, c_off + idx, q, a, sy, sz);
+                        if (valid) {
+                            particle_window<ORDER>(g, cur, q, a, sy, sz);
                         } else {
 #pragma unroll
-                            for (int t = 0; t < W; ++t) {
-                                a[0][t] = a[1][t] = a[2][t] = 0.0;
-                                sy[t] = sz[t] = 0.0;
-                            }
+                            for (int t = 0; t < W; ++t) a[0][t] = a[1][t] = a[2][t] = sy[t] = sz[t] = 0.0;
                         }
-                        // a grouped by ix-subset so a lane reads its 3*NI values contiguously
+                        double2* rec = reinterpret_cast<double2*>(stage + lg * L::PLANE + grp * L::REC);
 #pragma unroll
-                        for (int is = 0; is < W / NI; ++is)
+                        for (int c = 0; c < 3; ++c)
 #pragma unroll
-                            for (int c = 0; c < 3; ++c)
+                            for (int t = 0; t < W; t += 2) rec[(c * W + t) / 2] = make_double2(a[c][t], a[c][t + 1]);
 #pragma unroll
-                                for (int ii = 0; ii < NI; ++ii) rec[is * 3 * NI + c * NI + ii] = a[c][is * NI + ii];
-#pragma unroll
-                        for (int t = 0; t < W; ++t) {
-                            rec[3 * W + t] = sy[t];
-                            rec[4 * W + t] = sz[t];
+                        for (int t = 0; t < W; t += 2) {
+                            rec[(3 * W + t) / 2] = make_double2(sy[t], sy[t + 1]);
+                            rec[(4 * W + t) / 2] = make_double2(sz[t], sz[t + 1]);
                         }
                     }
                     __syncwarp();
-                    const int nn = min(G, m - base);
+                    const int nn = min(CH, m - base);
+#pragma unroll 1
                     for (int jj0 = 0; jj0 < nn; ++jj0) {
-                        const double* r = gstage + jj0 * L::REC;
-                        double av[3 * NI];
-                        const double2* ap = reinterpret_cast<const double2*>(r + isub * 3 * NI);
+                        const double2* r = reinterpret_cast<const double2*>(stage + jj0 * L::PLANE + grp * L::REC);
+                        double a[3][W], syv[NJ], sz[W];
 #pragma unroll
-                        for (int u = 0; u < 3 * NI / 2; ++u) {
-                            const double2 v = ap[u];
-                            av[2 * u] = v.x;
-                            av[2 * u + 1] = v.y;
-                        }
-                        double syv[NJ];
+                        for (int c = 0; c < 3; ++c)
 #pragma unroll
-                        for (int jj = 0; jj < NJ; ++jj) syv[jj] = r[3 * W + jsub * NJ + jj];
-                        double szv[W];
-                        const double2* zp = reinterpret_cast<const double2*>(r + 4 * W);
-#pragma unroll
-                        for (int u = 0; u < W / 2; ++u) {
-                            const double2 v = zp[u];
-                            szv[2 * u] = v.x;
-                            szv[2 * u + 1] = v.y;
-                        }
-#pragma unroll
-                        for (int kz = 0; kz < W; ++kz)
-#pragma unroll
-                            for (int jj = 0; jj < NJ; ++jj) {
-                                const double b = syv[jj] * szv[kz];
-#pragma unroll
-                                for (int ii = 0; ii < NI; ++ii)
-#pragma unroll
-                                    for (int c = 0; c < 3; ++c)
-                                        acc[kz][jj][ii][c] = fma(av[c * NI + ii], b, acc[kz][jj][ii][c]);
+                            for (int t = 0; t < W; t += 2) {
+                                const double2 v = r[(c * W + t) / 2];
+                                a[c][t] = v.x;
+                                a[c][t + 1] = v.y;
                             }
+#pragma unroll
+                        for (int jj = 0; jj < NJ; ++jj)
+                            syv[jj] = reinterpret_cast<const double*>(r)[3 * W + lg * NJ + jj];
+#pragma unroll
+                        for (int t = 0; t < W; t += 2) {
+                            const double2 v = r[(4 * W + t) / 2];
+                            sz[t] = v.x;
+                            sz[t + 1] = v.y;
+                        }
+                        accumulate<W, NJ>(acc, a, syv, sz);
                     }
                     __syncwarp();
                 }
             }
+            c_off = n_off;
+            n_c = n_n;
         }
 
         // Plane k+OFF is final for this pencil: emit it, slide the window.
         {
-            double* pp = patch + (buf * L::NP + grp) * (3 * W * W);
+            double* pp = patch + buf * L::PATCH + grp;
 #pragma unroll
             for (int c = 0; c < 3; ++c)
 #pragma unroll
                 for (int jj = 0; jj < NJ; ++jj)
 #pragma unroll
-                    for (int ii = 0; ii < NI; ++ii)
-                        pp[(c * W + jsub * NJ + jj) * W + isub * NI + ii] = acc[0][jj][ii][c];
+                    for (int ix = 0; ix < W; ++ix)
+                        pp[(((lg * NJ + jj) * W + ix) * 3 + c) * L::PSTRIDE] = acc[0][jj][ix][c];
 #pragma unroll
             for (int kz = 0; kz < W - 1; ++kz)
 #pragma unroll
                 for (int jj = 0; jj < NJ; ++jj)
 #pragma unroll
-                    for (int ii = 0; ii < NI; ++ii)
+                    for (int ix = 0; ix < W; ++ix)
 #pragma unroll
-                        for (int c = 0; c < 3; ++c) acc[kz][jj][ii][c] = acc[kz + 1][jj][ii][c];
+                        for (int c = 0; c < 3; ++c) acc[kz][jj][ix][c] = acc[kz + 1][jj][ix][c];
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj)
 #pragma unroll
-                for (int ii = 0; ii < NI; ++ii)
+                for (int ix = 0; ix < W; ++ix)
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) acc[W - 1][jj][ii][c] = 0.0;
+                    for (int c = 0; c < 3; ++c) acc[W - 1][jj][ix][c] = 0.0;
         }
         __syncthreads();
 
         // Gather the overlapping pencil patches of plane Z and flush each node once.
         {
-            const double* pb = patch + buf * L::NP * (3 * W * W);
+            const double* pb = patch + buf * L::PATCH;
             const int Z = wrap_index(k + OFF, g.nz);
             const bool zc = (k >= k0 + W - 1) && (k < k1);  // every contributing cell is in [k0, k1)
             const size_t zrow = (size_t)g.ny * (size_t)Z;
@@ -272,7 +307,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                     for (int dx = 0; dx < W; ++dx) {
                         const int qx = ux - dx;
                         if (qx < 0 || qx >= pxv) continue;
-                        s += pb[((qy * PX + qx) * 3 + c) * W * W + dy * W + dx];
+                        s += pb[((dy * W + dx) * 3 + c) * L::PSTRIDE + qy * PX + qx];
                     }
                 }
                 const int X = wrap_index(i0 + OFF + ux, g.nx);
@@ -288,6 +323,561 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
         }
         buf ^= 1;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Orders 2 and 3 (4-tap window): ONE WARP PER PENCIL.
+//
+// The warp streams its pencil's particles (cells k0..k1-1 concatenated) in
+// chunks of 32: lane l loads and pre-processes the l-th particle of the chunk
+// (all lanes busy whatever the cell counts), writes a 30-double record
+// {a[ix][c] = wq_c*sx[ix] (12), b[jy][kz] = sy[jy]*sz[kz] (16)} to the warp's
+// staging area, and the next chunk's loads are already in flight.  Then the
+// two half-warps consume the staged particles two at a time (even/odd, same
+// cell): lane = (half, jy, ix) owns 4 kz x 3 comps = 12 accumulators, reads
+// 7 operands with broadcast LDS.64 (1 wavefront each; LDS.128 costs 4) and
+// issues 12 DFMA.  The z window slides inside the registers; the halves'
+// partial sums meet with one shuffle when a plane is emitted.
+#ifndef PICGPU_WARP_MINB
+#define PICGPU_WARP_MINB 2
+#endif
+struct WCfg {
+    static constexpr int PX = 4, PY = 2, NW = PX * PY, NT = NW * 32, MINB = PICGPU_WARP_MINB;
+    // Staging is field-major: field f of chunk particle l at [f*FS + l].  The
+    // 34-double field stride makes the staging writes conflict-free and puts
+    // the two half-warps' operands (particles l, l+1) in disjoint banks; the
+    // operands of one lane sit 34 doubles apart, so ptxas cannot fuse them
+    // into LDS.128 (4 wavefronts) -- every operand load is a 1-wavefront LDS.64.
+    static constexpr int NF = 28, FS = 34, REC = NF * FS;  // per-warp staging block (doubles)
+    static constexpr int R = 2;                         // planes emitted per CTA barrier
+    static constexpr int PS = 49;                       // per-pencil patch stride (3*16 + 1 skew)
+    static constexpr int PATCH = NW * PS;               // one plane slot: [pencil][c][jy][ix]
+    static constexpr int STAGE = NW * REC;
+    static constexpr size_t SMEM = (size_t)(2 * R * PATCH + STAGE) * sizeof(double);
+};
+
+__device__ __forceinline__ double lds64(const double* p) {
+    // explicit 64-bit shared load: a broadcast LDS.64 costs one wavefront,
+    // whereas the LDS.128 nvcc would merge neighbouring doubles into costs four
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(WCfg::NT, WCfg::MINB)
+    deposit_current_warp_kernel(const GridD g, const CSoa p, const uint32_t* __restrict__ off,
+                                const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
+                                double* __restrict__ jy, double* __restrict__ jz, const int zlen) {
+    constexpr int W = 4, OFF = Shape<ORDER>::OFF;
+    static_assert(Shape<ORDER>::W == 4, "warp kernel is for the 4-tap window");
+    constexpr int PX = WCfg::PX, PY = WCfg::PY, FS = WCfg::FS, PS = WCfg::PS;
+    constexpr int FX = PX + W - 1, FY = PY + W - 1, NITEM = 3 * FX * FY;
+    static_assert(NITEM <= WCfg::NT, "one gather item per thread");
+    constexpr int SY = W - PX * PS, SX = 1 - PS;  // patch offset of tap (dy, dx) from tap (0, 0)
+    constexpr unsigned FULL = 0xffffffffu;
+
+    extern __shared__ __align__(16) double smem[];
+    double* patch = smem;  // [2 phases][R planes][pencil][c][jy][ix]
+    double* stage = smem + 2 * WCfg::R * WCfg::PATCH;
+
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int px = wid % PX, py = wid / PX;
+    const int jyl = lane & 3, ixl = (lane >> 2) & 3, hh = lane >> 4;
+    const int i0 = blockIdx.x * PX, j0 = blockIdx.y * PY;
+    const int k0 = blockIdx.z * zlen;
+    const int k1 = min(k0 + zlen, g.nz);
+    const int i = i0 + px, j = j0 + py;
+    const bool pv = (i < g.nx) && (j < g.ny);
+    const int pxv = min(PX, g.nx - i0), pyv = min(PY, g.ny - j0);
+    const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
+    const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
+    const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
+    double* recs = stage + wid * WCfg::REC;
+
+    // ---- this thread's gather item (fixed for all planes) ----
+    bool g_active = false, g_inxy = false;
+    uint32_t g_taps = 0;
+    int g_base = 0;
+    double* g_field = jx;
+    size_t g_xy = 0;
+    {
+        const int it = threadIdx.x;
+        if (it < NITEM) {
+            const int c = it / (FX * FY);
+            const int r = it - c * (FX * FY);
+            const int uy = r / FX, ux = r - uy * FX;
+            if (ux < pxv + W - 1 && uy < pyv + W - 1) {
+                g_active = true;
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const int qy = uy - (t >> 2), qx = ux - (t & 3);
+                    if (qy >= 0 && qy < pyv && qx >= 0 && qx < pxv) g_taps |= 1u << t;
+                }
+                g_base = (uy * PX + ux) * PS + c * 16;  // pencil (ux, uy), tap (0, 0)
+                g_field = c == 0 ? jx : (c == 1 ? jy : jz);
+                g_xy = (size_t)wrap_index(i0 + OFF + ux, g.nx) +
+                       (size_t)g.nx * (size_t)wrap_index(j0 + OFF + uy, g.ny);
+                g_inxy = !alias_xy && ux >= W - 1 && ux <= pxv - 1 && uy >= W - 1 && uy <= pyv - 1;
+            }
+        }
+    }
+
+    // ---- stream planner: lane l gets the l-th particle from (sk, spos) ----
+    int sk = k0;
+    uint32_t spos = 0;
+    auto plan = [&](uint32_t& slot, int& cz, bool& valid) {
+        uint32_t wcnt = 0, woff = 0;
+        const int kk = sk + lane;
+        if (pv && kk < k1) {
+            const uint32_t c = col + plane_cells * (uint32_t)kk;
+            woff = off[c];
+            wcnt = cnt[c];
+        }
+        uint32_t incl = wcnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t v = __shfl_up_sync(FULL, incl, d);
+            if (lane >= d) incl += v;
+        }
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        const uint32_t t = spos + (uint32_t)lane;
+        valid = t < total;
+        int pos = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t v = __shfl_sync(FULL, incl, pos + step - 1);
+            if (v <= t) pos += step;
+        }
+        const int jw = pos < 31 ? pos : 31;
+        const uint32_t excl_j = __shfl_sync(FULL, incl - wcnt, jw);
+        const uint32_t off_j = __shfl_sync(FULL, woff, jw);
+        slot = off_j + (t - excl_j);
+        cz = sk + jw;
+        const uint32_t tend = total > spos ? min(spos + 32u, total) : spos;
+        if (tend >= total) {
+            sk = min(sk + 32, k1);
+            spos = 0;
+        } else {
+            const int pe = __popc(__ballot_sync(FULL, incl <= tend));
+            spos = tend - __shfl_sync(FULL, incl - wcnt, pe);
+            sk = sk + pe;
+        }
+    };
+
+    PData nxt{};
+    uint32_t nslot = 0;
+    int ncz = 0;
+    bool nvalid = false;
+    plan(nslot, ncz, nvalid);
+    if (nvalid) load_particle(p, nslot, nxt);
+    bool pending = __any_sync(FULL, nvalid);
+
+    double acc[W][3];
+#pragma unroll
+    for (int kz = 0; kz < W; ++kz) acc[kz][0] = acc[kz][1] = acc[kz][2] = 0.0;
+    int navail = 0, nidx = 0, cz_reg = 0x7fffffff;
+    const int T = k1 + W - 1 - k0;  // planes emitted by every warp (CTA-uniform)
+
+    // One z-step at register rotation RT (slot (kz+RT)&3 holds local plane kz),
+    // unrolled 4x so the sliding window never moves registers.
+    auto step = [&](auto rot, int kb) {
+        constexpr int RT = decltype(rot)::value;
+        const int k = k0 + kb + RT;
+        if (kb + RT >= T) return;
+        if (k < k1) {
+            for (;;) {
+                if (nidx == navail) {
+                    if (!pending) break;
+                    __syncwarp();  // the previous chunk's records are no longer read
+                    if (nvalid) {  // prologue: shape.hpp:64-85 + particle_weights :46-50
+                        double a[3][W], sy[W], sz[W];
+                        particle_window<ORDER>(g, nxt, q, a, sy, sz);
+                        // fields: a[c][ix] at f = c*4 + ix; b[kz][jy] = sy*sz at f = 12 + kz*4 + jy
+                        double* rr = recs + lane;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+#pragma unroll
+                            for (int xx = 0; xx < W; ++xx) rr[(c * 4 + xx) * FS] = a[c][xx];
+#pragma unroll
+                        for (int zz = 0; zz < W; ++zz)
+#pragma unroll
+                            for (int yy = 0; yy < W; ++yy) rr[(12 + zz * 4 + yy) * FS] = sy[yy] * sz[zz];
+                    }
+                    cz_reg = nvalid ? ncz : 0x7fffffff;
+                    navail = __popc(__ballot_sync(FULL, nvalid));
+                    nidx = 0;
+                    __syncwarp();
+                    plan(nslot, ncz, nvalid);  // prefetch the following chunk
+                    if (nvalid) load_particle(p, nslot, nxt);
+                    pending = __any_sync(FULL, nvalid);
+                    continue;
+                }
+                // staged particles nidx.. of cell k (contiguous): the two
+                // half-warps take them two at a time
+                const unsigned mk = __ballot_sync(FULL, cz_reg == k) & (FULL << nidx);
+                const int cntk = __popc(mk);
+                const double* ra = recs + ixl * FS + nidx + hh;
+                const double* rb = recs + (12 + jyl) * FS + nidx + hh;
+                int t = 0;
+#pragma unroll 2
+                for (; t + 1 < cntk; t += 2) {
+                    const double a0 = ra[0], a1 = ra[4 * FS], a2 = ra[8 * FS];
+#pragma unroll
+                    for (int kz = 0; kz < W; ++kz) {
+                        const double b = rb[kz * 4 * FS];
+                        double* A = acc[(kz + RT) & 3];
+                        A[0] = fma(a0, b, A[0]);
+                        A[1] = fma(a1, b, A[1]);
+                        A[2] = fma(a2, b, A[2]);
+                    }
+                    ra += 2;
+                    rb += 2;
+                }
+                if (t < cntk && hh == 0) {  // odd count: the last one goes to half 0
+                    const double a0 = ra[0], a1 = ra[4 * FS], a2 = ra[8 * FS];
+#pragma unroll
+                    for (int kz = 0; kz < W; ++kz) {
+                        const double b = rb[kz * 4 * FS];
+                        double* A = acc[(kz + RT) & 3];
+                        A[0] = fma(a0, b, A[0]);
+                        A[1] = fma(a1, b, A[1]);
+                        A[2] = fma(a2, b, A[2]);
+                    }
+                }
+                nidx += cntk;
+                if (nidx < navail || cntk == 0) break;  // the rest of the chunk is in later cells
+            }
+        }
+        // Plane k+OFF is final for this pencil: add the halves, emit, recycle the slot.
+        constexpr int SL = RT & 1, PH = (RT >> 1) & 1;  // ring slot and phase (R = 2 planes per barrier)
+        {
+            double* pp = patch + (PH * WCfg::R + SL) * WCfg::PATCH + wid * PS + jyl * W + ixl;
+            double* A = acc[RT & 3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double v = A[c] + __shfl_xor_sync(FULL, A[c], 16);
+                if (hh == 0) pp[c * 16] = v;
+                A[c] = 0.0;
+            }
+        }
+        if (SL == 0 && kb + RT + 1 < T) return;  // flush every 2 planes (and after the last)
+        __syncthreads();
+        if (g_active) {
+#pragma unroll
+            for (int sl = 0; sl <= SL; ++sl) {
+                const int kk = k - SL + sl;
+                const double* pb = patch + (PH * WCfg::R + sl) * WCfg::PATCH + g_base;
+                double s = 0.0;
+#pragma unroll
+                for (int tp = 0; tp < 16; ++tp)
+                    if (g_taps & (1u << tp)) s += pb[(tp >> 2) * SY + (tp & 3) * SX];
+                const int Z = wrap_index(kk + OFF, g.nz);
+                const size_t node = g_xy + (size_t)plane_cells * (size_t)Z;
+                const bool zc = (kk >= k0 + W - 1) && (kk < k1);
+                if (g_inxy && zc)
+                    g_field[node] = s;
+                else if (s != 0.0)
+                    atomicAdd(g_field + node, s);
+            }
+        }
+    };
+
+    for (int kb = 0; kb < T; kb += 4) {
+        step(std::integral_constant<int, 0>{}, kb);
+        step(std::integral_constant<int, 1>{}, kb);
+        step(std::integral_constant<int, 2>{}, kb);
+        step(std::integral_constant<int, 3>{}, kb);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Orders 2 and 3, FP64 tensor-core variant: ONE WARP PER PENCIL, the per-cell
+// outer-product contraction J_cell[(c,ix)][(kz,jy)] = sum_p a_p (x) b_p issued
+// as DMMA m8n8k4 (mma.sync ... f64): K = 4 particles per MMA, M = 12 (c,ix)
+// rows padded to 16, N = 16 (kz,jy) columns.  Each lane holds only the 8
+// accumulator doubles of the 2x2 fragment tiles; per 4 particles it issues 4
+// LDS.64 (2 wavefronts each) and 4 DMMA.  This is the paper's MPU
+// outer-product form (tile.hpp:23-29, pack_qsp :83-92) on Blackwell's FP64
+// matrix pipe.  The pipe's rate equals DFMA's (64 MAC/clk/SM, measured by
+// tools/fp64_pipes.cu) and the row padding costs 25%, but the instruction
+// count per particle drops ~4x, which is what bounded the DFMA kernels.
+struct MCfg {
+    static constexpr int PX = 4, PY = 2, NW = PX * PY, NT = NW * 32, MINB = 3;
+    static constexpr int NF = 28, FS = 36;               // staging fields: a[(c,ix)] 12 | b[(kz,jy)] 16
+    static constexpr int REC = NF * FS;                  // per-warp staging block (doubles)
+    static constexpr int R = 2;                          // planes emitted per CTA barrier
+    static constexpr int PS = 49;                        // per-pencil patch stride
+    static constexpr int PATCH = NW * PS;
+    static constexpr int STAGE = NW * REC;
+    static constexpr size_t SMEM = (size_t)(2 * R * PATCH + STAGE) * sizeof(double);
+};
+
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(MCfg::NT, MCfg::MINB)
+    deposit_current_dmma_kernel(const GridD g, const CSoa p, const uint32_t* __restrict__ off,
+                                const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
+                                double* __restrict__ jy, double* __restrict__ jz, const int zlen) {
+    constexpr int W = 4, OFF = Shape<ORDER>::OFF;
+    static_assert(Shape<ORDER>::W == 4, "DMMA kernel is for the 4-tap window");
+    constexpr int PX = MCfg::PX, PY = MCfg::PY, FS = MCfg::FS, PS = MCfg::PS;
+    constexpr int FX = PX + W - 1, FY = PY + W - 1, NITEM = 3 * FX * FY;
+    static_assert(NITEM <= MCfg::NT, "one gather item per thread");
+    constexpr int SY = W - PX * PS, SX = 1 - PS;
+    constexpr unsigned FULL = 0xffffffffu;
+
+    extern __shared__ __align__(16) double smem[];
+    double* patch = smem;  // [2 phases][R planes][pencil][c][jy][ix]
+    double* stage = smem + 2 * MCfg::R * MCfg::PATCH;
+
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;  // mma fragment coordinates
+    const int px = wid % PX, py = wid / PX;
+    const int i0 = blockIdx.x * PX, j0 = blockIdx.y * PY;
+    const int k0 = blockIdx.z * zlen;
+    const int k1 = min(k0 + zlen, g.nz);
+    const int i = i0 + px, j = j0 + py;
+    const bool pv = (i < g.nx) && (j < g.ny);
+    const int pxv = min(PX, g.nx - i0), pyv = min(PY, g.ny - j0);
+    const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
+    const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
+    const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
+    double* recs = stage + wid * MCfg::REC;
+
+    // ---- this thread's gather item ----
+    bool g_active = false, g_inxy = false;
+    uint32_t g_taps = 0;
+    int g_base = 0;
+    double* g_field = jx;
+    size_t g_xy = 0;
+    {
+        const int it = threadIdx.x;
+        if (it < NITEM) {
+            const int c = it / (FX * FY);
+            const int r = it - c * (FX * FY);
+            const int uy = r / FX, ux = r - uy * FX;
+            if (ux < pxv + W - 1 && uy < pyv + W - 1) {
+                g_active = true;
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const int qy = uy - (t >> 2), qx = ux - (t & 3);
+                    if (qy >= 0 && qy < pyv && qx >= 0 && qx < pxv) g_taps |= 1u << t;
+                }
+                g_base = (uy * PX + ux) * PS + c * 16;
+                g_field = c == 0 ? jx : (c == 1 ? jy : jz);
+                g_xy = (size_t)wrap_index(i0 + OFF + ux, g.nx) +
+                       (size_t)g.nx * (size_t)wrap_index(j0 + OFF + uy, g.ny);
+                g_inxy = !alias_xy && ux >= W - 1 && ux <= pxv - 1 && uy >= W - 1 && uy <= pyv - 1;
+            }
+        }
+    }
+
+    // ---- stream planner (as in the DFMA warp kernel) ----
+    int sk = k0;
+    uint32_t spos = 0;
+    auto plan = [&](uint32_t& slot, int& cz, bool& valid) {
+        uint32_t wcnt = 0, woff = 0;
+        const int kk = sk + lane;
+        if (pv && kk < k1) {
+            const uint32_t c = col + plane_cells * (uint32_t)kk;
+            woff = off[c];
+            wcnt = cnt[c];
+        }
+        uint32_t incl = wcnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t v = __shfl_up_sync(FULL, incl, d);
+            if (lane >= d) incl += v;
+        }
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        const uint32_t t = spos + (uint32_t)lane;
+        valid = t < total;
+        int pos = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t v = __shfl_sync(FULL, incl, pos + step - 1);
+            if (v <= t) pos += step;
+        }
+        const int jw = pos < 31 ? pos : 31;
+        const uint32_t excl_j = __shfl_sync(FULL, incl - wcnt, jw);
+        const uint32_t off_j = __shfl_sync(FULL, woff, jw);
+        slot = off_j + (t - excl_j);
+        cz = sk + jw;
+        const uint32_t tend = total > spos ? min(spos + 32u, total) : spos;
+        if (tend >= total) {
+            sk = min(sk + 32, k1);
+            spos = 0;
+        } else {
+            const int pe = __popc(__ballot_sync(FULL, incl <= tend));
+            spos = tend - __shfl_sync(FULL, incl - wcnt, pe);
+            sk = sk + pe;
+        }
+    };
+
+    PData nxt{};
+    uint32_t nslot = 0;
+    int ncz = 0;
+    bool nvalid = false;
+    plan(nslot, ncz, nvalid);
+    if (nvalid) load_particle(p, nslot, nxt);
+    bool pending = __any_sync(FULL, nvalid);
+
+    // D[mt][nt][2]: rows m = mt*8 + gq = (c, ix) = (m/4, m%4); cols n = nt*8 + 2tq + e = (kz, jy) = (n/4, n%4)
+    double D[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+    int navail = 0, nidx = 0, cz_reg = 0x7fffffff;
+    int phase = 0;
+    const int T = k1 + W - 1 - k0;
+    const bool a_hi = gq < 4;  // rows 8..11 of the second m-tile are c = 2; 12..15 are padding
+    for (int st = 0; st < T; ++st) {
+        const int k = k0 + st;
+        if (k < k1) {
+            for (;;) {
+                if (nidx == navail) {
+                    if (!pending) break;
+                    __syncwarp();
+                    if (nvalid) {  // prologue: shape.hpp:64-85 + particle_weights :46-50
+                        double a[3][W], sy[W], sz[W];
+                        particle_window<ORDER>(g, nxt, q, a, sy, sz);
+                        double* rr = recs + lane;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+#pragma unroll
+                            for (int xx = 0; xx < W; ++xx) rr[(c * 4 + xx) * FS] = a[c][xx];
+#pragma unroll
+                        for (int zz = 0; zz < W; ++zz)
+#pragma unroll
+                            for (int yy = 0; yy < W; ++yy) rr[(12 + zz * 4 + yy) * FS] = sy[yy] * sz[zz];
+                    }
+                    cz_reg = nvalid ? ncz : 0x7fffffff;
+                    navail = __popc(__ballot_sync(FULL, nvalid));
+                    nidx = 0;
+                    __syncwarp();
+                    plan(nslot, ncz, nvalid);
+                    if (nvalid) load_particle(p, nslot, nxt);
+                    pending = __any_sync(FULL, nvalid);
+                    continue;
+                }
+                const unsigned mk = __ballot_sync(FULL, cz_reg == k) & (FULL << nidx);
+                const int cntk = __popc(mk);
+                for (int kb = 0; kb < cntk; kb += 4) {
+                    const bool v = kb + tq < cntk;
+                    const int pidx = nidx + kb + tq;
+                    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+                    if (v) {
+                        const double* r = recs + pidx;
+                        a0 = r[gq * FS];                       // a row m = gq
+                        if (a_hi) a1 = r[(8 + gq) * FS];       // a row m = 8 + gq (c = 2)
+                        b0 = r[(12 + gq) * FS];                // b col n = gq
+                        b1 = r[(20 + gq) * FS];                // b col n = 8 + gq
+                    }
+                    dmma_8x8x4(D[0][0], a0, b0);
+                    dmma_8x8x4(D[0][1], a0, b1);
+                    dmma_8x8x4(D[1][0], a1, b0);
+                    dmma_8x8x4(D[1][1], a1, b1);
+                }
+                nidx += cntk;
+                if (nidx < navail || cntk == 0) break;
+            }
+        }
+        // Emit local plane kz = 0 (tile nt = 0, lanes tq < 2), then slide:
+        // kz <- kz + 1 is a swap between lanes tq and tq ^ 2 and tiles.
+        const int SL = st % MCfg::R, PH = phase;
+        {
+            double* pp = patch + (PH * MCfg::R + SL) * MCfg::PATCH + wid * PS;
+            if (tq < 2) {
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const int m = mt * 8 + gq;
+                    if (m < 12) {
+                        const int c = m >> 2, ix = m & 3;
+                        pp[c * 16 + (2 * tq) * W + ix] = D[mt][0][0];
+                        pp[c * 16 + (2 * tq + 1) * W + ix] = D[mt][0][1];
+                    }
+                }
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double x0 = __shfl_xor_sync(FULL, D[mt][0][e], 2);
+                    const double x1 = __shfl_xor_sync(FULL, D[mt][1][e], 2);
+                    D[mt][0][e] = (tq & 2) ? x1 : x0;
+                    D[mt][1][e] = (tq & 2) ? 0.0 : x1;
+                }
+        }
+        if (SL != MCfg::R - 1 && st + 1 < T) continue;
+        __syncthreads();
+        if (g_active) {
+            for (int sl = 0; sl <= SL; ++sl) {
+                const int kk = k - SL + sl;
+                const double* pb = patch + (PH * MCfg::R + sl) * MCfg::PATCH + g_base;
+                double s = 0.0;
+#pragma unroll
+                for (int tp = 0; tp < 16; ++tp)
+                    if (g_taps & (1u << tp)) s += pb[(tp >> 2) * SY + (tp & 3) * SX];
+                const int Z = wrap_index(kk + OFF, g.nz);
+                const size_t node = g_xy + (size_t)plane_cells * (size_t)Z;
+                const bool zc = (kk >= k0 + W - 1) && (kk < k1);
+                if (g_inxy && zc)
+                    g_field[node] = s;
+                else if (s != 0.0)
+                    atomicAdd(g_field + node, s);
+            }
+        }
+        phase ^= 1;
+    }
+}
+
+template <int ORDER>
+void launch_dmma(const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+                 int num_sms, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_dmma_kernel<ORDER>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MCfg::SMEM));
+        configured = true;
+    }
+    const int tx = div_up(g.nx, MCfg::PX), ty = div_up(g.ny, MCfg::PY);
+    const long long tiles = (long long)tx * ty;
+    const long long target = (long long)num_sms * MCfg::MINB * 8;
+    int zch = (int)std::max<long long>(1, (target + tiles - 1) / tiles);
+    zch = std::min(zch, std::max(1, g.nz / 16));
+    const int zlen = div_up(g.nz, zch);
+    zch = div_up(g.nz, zlen);
+    dim3 grid(tx, ty, zch);
+    deposit_current_dmma_kernel<ORDER><<<grid, MCfg::NT, MCfg::SMEM, st>>>(g, p, off, cnt, q, j, j + g.ncells,
+                                                                          j + 2 * (size_t)g.ncells, zlen);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+template <int ORDER>
+void launch_warp(const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+                 int num_sms, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_warp_kernel<ORDER>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WCfg::SMEM));
+        configured = true;
+    }
+    const int tx = div_up(g.nx, WCfg::PX), ty = div_up(g.ny, WCfg::PY);
+    const long long tiles = (long long)tx * ty;
+    const long long target = (long long)num_sms * WCfg::MINB * 8;
+    int zch = (int)std::max<long long>(1, (target + tiles - 1) / tiles);
+    zch = std::min(zch, std::max(1, g.nz / 16));
+    const int zlen = div_up(g.nz, zch);
+    zch = div_up(g.nz, zlen);
+    dim3 grid(tx, ty, zch);
+    deposit_current_warp_kernel<ORDER><<<grid, WCfg::NT, WCfg::SMEM, st>>>(g, p, off, cnt, q, j, j + g.ncells,
+                                                                          j + 2 * (size_t)g.ncells, zlen);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
 template <int ORDER>
@@ -320,13 +910,29 @@ void launch_order(const GridD& g, const CSoa& p, const uint32_t* off, const uint
 
 }  // namespace
 
+// Order-2/3 contraction: 0 = FP64 DMMA (default), 1 = DFMA register blocking.
+// PICGPU_J_VARIANT=dfma selects the latter (ablation / profiling).
+static int j_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("PICGPU_J_VARIANT");
+        return (e && std::string(e) == "dfma") ? 1 : 0;
+    }();
+    return v;
+}
+
 // J must be zeroed by the caller (halo nodes are reduced into it).
 void launch_deposit_current(int order, const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt,
                             double q, double* j, int num_sms, cudaStream_t st) {
     switch (order) {
         case 1: launch_order<1>(g, p, off, cnt, q, j, num_sms, st); break;
-        case 2: launch_order<2>(g, p, off, cnt, q, j, num_sms, st); break;
-        case 3: launch_order<3>(g, p, off, cnt, q, j, num_sms, st); break;
+        case 2:
+            if (j_variant() == 1) launch_warp<2>(g, p, off, cnt, q, j, num_sms, st);
+            else launch_dmma<2>(g, p, off, cnt, q, j, num_sms, st);
+            break;
+        case 3:
+            if (j_variant() == 1) launch_warp<3>(g, p, off, cnt, q, j, num_sms, st);
+            else launch_dmma<3>(g, p, off, cnt, q, j, num_sms, st);
+            break;
         default: throw Status{PICGPU_EINVAL, "deposit: shape order must be 1, 2 or 3"};
     }
 }

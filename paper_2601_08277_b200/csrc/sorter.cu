@@ -245,63 +245,85 @@ __global__ void __launch_bounds__(256) k_push_detect(const GridD g, const Soa A,
     __syncthreads();
     const int lane = threadIdx.x & 31;
     unsigned local_moved = 0;
-    for (uint32_t s = so[0] + threadIdx.x; s < so[nb]; s += blockDim.x) {
-        const int b = find_bin(so, nb, s);
-        const bool valid = s - so[b] < sc[b];
-        bool moved = false;
-        uint32_t nc = 0;
-        double x = 0, y = 0, z = 0, vx = 0, vy = 0, vz = 0;
-        if (valid) {
-            x = A.x[s];
-            y = A.y[s];
-            z = A.z[s];
-            vx = A.vx[s];
-            vy = A.vy[s];
-            vz = A.vz[s];
-            bool ok = true;
-            if (PUSH) {
-                if (!push_one(g, dt, cap2, x, y, z, vx, vy, vz)) {
-                    raise_error(&ctr->err, PICGPU_EDOMAIN);
-                    ok = false;
-                } else {
-                    A.x[s] = x;
-                    A.y[s] = y;
-                    A.z[s] = z;
-                }
+    // Two slots per thread per pass: both slots' loads are issued before either
+    // is processed (more bytes in flight per thread).
+    constexpr int UNR = 2;
+    const uint32_t S1 = so[nb];
+    for (uint32_t s0 = so[0] + threadIdx.x; s0 < S1; s0 += UNR * blockDim.x) {
+        double x[UNR], y[UNR], z[UNR], vx[UNR], vy[UNR], vz[UNR];
+        int bb[UNR];
+        bool valid[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t s = s0 + u * blockDim.x;
+            bb[u] = 0;
+            valid[u] = false;
+            x[u] = y[u] = z[u] = vx[u] = vy[u] = vz[u] = 0.0;
+            if (s < S1) {
+                bb[u] = find_bin(so, nb, s);
+                valid[u] = s - so[bb[u]] < sc[bb[u]];
             }
-            if (ok && !finite3(x, y, z)) {
-                raise_error(&ctr->err, PICGPU_EINVAL);
-                ok = false;
+            if (valid[u]) {
+                x[u] = A.x[s];
+                y[u] = A.y[s];
+                z[u] = A.z[s];
+                vx[u] = A.vx[s];
+                vy[u] = A.vy[s];
+                vz[u] = A.vz[s];
             }
-            if (ok) {
-                nc = cell_linear(g, x, y, z);
-                moved = nc != c0 + (uint32_t)b;
-            }
-            mflag[s] = moved ? 1 : 0;
         }
-        const unsigned act = __activemask();
-        const unsigned mv = __ballot_sync(act, moved);
-        if (mv) {
-            const int leader = __ffs(mv) - 1;
-            unsigned base = 0;
-            if (lane == leader) base = atomicAdd(&ctr->nmovers, (unsigned)__popc(mv));
-            base = __shfl_sync(act, base, leader);
-            if (moved) {
-                const unsigned idx = base + __popc(mv & ((1u << lane) - 1u));
-                ++local_moved;
-                if (idx < mcap) {
-                    atomicAdd(&sdep[b], 1u);
-                    M.x[idx] = x;
-                    M.y[idx] = y;
-                    M.z[idx] = z;
-                    M.vx[idx] = vx;
-                    M.vy[idx] = vy;
-                    M.vz[idx] = vz;
-                    M.w[idx] = A.w[s];
-                    M.id[idx] = A.id[s];
-                    mcell[idx] = nc;
-                } else {
-                    mflag[s] = 2;  // stays in its stale bin; host re-sorts fully
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t s = s0 + u * blockDim.x;
+            const int b = bb[u];
+            bool moved = false;
+            uint32_t nc = 0;
+            if (valid[u]) {
+                bool ok = true;
+                if (PUSH) {
+                    if (!push_one(g, dt, cap2, x[u], y[u], z[u], vx[u], vy[u], vz[u])) {
+                        raise_error(&ctr->err, PICGPU_EDOMAIN);
+                        ok = false;
+                    } else {
+                        A.x[s] = x[u];
+                        A.y[s] = y[u];
+                        A.z[s] = z[u];
+                    }
+                }
+                if (ok && !finite3(x[u], y[u], z[u])) {
+                    raise_error(&ctr->err, PICGPU_EINVAL);
+                    ok = false;
+                }
+                if (ok) {
+                    nc = cell_linear(g, x[u], y[u], z[u]);
+                    moved = nc != c0 + (uint32_t)b;
+                }
+                mflag[s] = moved ? 1 : 0;
+            }
+            const unsigned act = __activemask();
+            const unsigned mv = __ballot_sync(act, moved);
+            if (mv) {
+                const int leader = __ffs(mv) - 1;
+                unsigned base = 0;
+                if (lane == leader) base = atomicAdd(&ctr->nmovers, (unsigned)__popc(mv));
+                base = __shfl_sync(act, base, leader);
+                if (moved) {
+                    const unsigned idx = base + __popc(mv & ((1u << lane) - 1u));
+                    ++local_moved;
+                    if (idx < mcap) {
+                        atomicAdd(&sdep[b], 1u);
+                        M.x[idx] = x[u];
+                        M.y[idx] = y[u];
+                        M.z[idx] = z[u];
+                        M.vx[idx] = vx[u];
+                        M.vy[idx] = vy[u];
+                        M.vz[idx] = vz[u];
+                        M.w[idx] = A.w[s];
+                        M.id[idx] = A.id[s];
+                        mcell[idx] = nc;
+                    } else {
+                        mflag[s] = 2;  // stays in its stale bin; host re-sorts fully
+                    }
                 }
             }
         }
@@ -362,48 +384,69 @@ __global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32
     }
 }
 
-// borrow_insert (gpma.hpp:337-370) for the few arrivals that found their bin
+// borrow_insert (gpma.hpp:337-370) for the arrivals that found their bin
 // full: the nearest of the next `scan` bins with slack lends one slot; every
 // boundary in (d, donor] moves up by one and each bin in between hands its
 // first particle to its own tail (the slot just vacated above it), so bins
-// stay contiguous and cell-exact.  One thread walks the overflow list in order
-// (there are a handful per step); entries with no donor are compacted to the
-// front of `ovf` and left for the full re-sort.
-__global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restrict__ mcell, uint32_t* ovf,
-                         const Soa A, uint32_t* off, const uint32_t* __restrict__ cnt, uint32_t ncells, int scan) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const uint32_t n = ctr->noverflow;
-    if (n == 0) return;
-    uint32_t left = 0;
-    for (uint32_t o = 0; o < n; ++o) {
+// stay contiguous and cell-exact.  One thread per overflowed arrival; a thread
+// works only while it holds try-locks on its whole window [d, d+scan] (taken
+// in ascending order, released on any failure, so no thread ever waits while
+// holding a lock).  Arrivals with no donor go to `left` for the re-sort.
+__global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restrict__ mcell,
+                         const uint32_t* __restrict__ ovf, uint32_t* __restrict__ left, const Soa A, uint32_t* off,
+                         const uint32_t* __restrict__ cnt, unsigned int* lock, uint32_t ncells, int scan) {
+    const uint32_t n = *(volatile unsigned int*)&ctr->noverflow;
+    for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) {
         const uint32_t i = ovf[o];
         const uint32_t d = mcell[i];
-        int64_t donor = -1;
         const uint64_t lim = (uint64_t)d + (uint64_t)scan;
         const uint32_t last = (uint32_t)(lim < (uint64_t)ncells - 1 ? lim : (uint64_t)ncells - 1);
-        for (uint32_t b = d + 1; b <= last && d + 1 < ncells; ++b)
-            if (cnt[b] < off[b + 1] - off[b]) {
-                donor = b;
-                break;
-            }
-        if (donor < 0) {
-            ovf[left++] = i;
+        if (last <= d) {  // last bin: nothing follows it
+            left[atomicAdd(&ctr->nleft, 1u)] = i;
             continue;
         }
-        const uint32_t slot = off[d + 1];  // becomes bin d's new last slot
-        uint32_t above = off[(uint32_t)donor + 1];  // old lower boundary of the bin above j
-        for (uint32_t j = (uint32_t)donor; j > d; --j) {
-            const uint32_t oj = off[j];
-            const uint32_t held = min(cnt[j], above - oj);  // capacity before this borrow
-            // donor: its free tail slot; a full bin: `above`, just vacated by bin j+1
-            if (held > 0) copy_particle(A, oj, A, (uint64_t)oj + held);
-            off[j] = oj + 1;
-            above = oj;
+        for (int attempt = 0;; ++attempt) {
+            uint32_t got = d;
+            while (got <= last && atomicCAS(&lock[got], 0u, 1u) == 0u) ++got;
+            if (got <= last) {
+                for (uint32_t b = d; b < got; ++b) atomicExch(&lock[b], 0u);
+                __nanosleep(64u << (attempt < 6 ? attempt : 6));
+                continue;
+            }
+            __threadfence();
+            volatile uint32_t* voff = off;
+            int64_t donor = -1;
+            for (uint32_t b = d + 1; b <= last; ++b)
+                if (cnt[b] < voff[b + 1] - voff[b]) {
+                    donor = b;
+                    break;
+                }
+            if (donor < 0) {
+                left[atomicAdd(&ctr->nleft, 1u)] = i;
+            } else {
+                const uint32_t slot = voff[d + 1];  // becomes bin d's new last slot
+                uint32_t above = voff[(uint32_t)donor + 1];
+                for (uint32_t j = (uint32_t)donor; j > d; --j) {
+                    const uint32_t oj = voff[j];
+                    const uint32_t held = min(cnt[j], above - oj);  // capacity before this borrow
+                    if (held > 0) {  // donor: its free tail slot; a full bin: `above`, vacated by bin j+1
+                        const uint64_t dst = (uint64_t)oj + held;
+                        A.x[dst] = __ldcg(A.x + oj); A.y[dst] = __ldcg(A.y + oj); A.z[dst] = __ldcg(A.z + oj);
+                        A.vx[dst] = __ldcg(A.vx + oj); A.vy[dst] = __ldcg(A.vy + oj);
+                        A.vz[dst] = __ldcg(A.vz + oj); A.w[dst] = __ldcg(A.w + oj);
+                        A.id[dst] = __ldcg((const unsigned long long*)A.id + oj);
+                    }
+                    voff[j] = oj + 1;
+                    above = oj;
+                }
+                copy_particle(M, i, A, slot);
+                atomicAdd(&ctr->nborrowed, 1u);
+            }
+            __threadfence();
+            for (uint32_t b = d; b <= last; ++b) atomicExch(&lock[b], 0u);
+            break;
         }
-        copy_particle(M, i, A, slot);
     }
-    ctr->noverflow = left;
-    ctr->nborrowed = n - left;
 }
 
 // Overflowed movers appended after a packed store (mover-buffer fallback).
@@ -544,6 +587,8 @@ void BinStore::init(const picgpu_grid& grid, double gap_ratio, uint32_t mg, cuda
     if (!hcounters) PICGPU_CUDA_TRY(cudaMallocHost((void**)&hcounters, sizeof(StepCounters)));
     PICGPU_CUDA_TRY(cudaMemsetAsync(off.p, 0, (nc + 1) * 4, st));
     PICGPU_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, nc * 4, st));
+    locks.ensure(nc * 4 + 4);
+    PICGPU_CUDA_TRY(cudaMemsetAsync(locks.p, 0, nc * 4 + 4, st));
     capacity = 0;
     n = 0;
 }
@@ -666,6 +711,7 @@ void BinStore::ensure_movers(size_t m) {
     M.ensure(m);
     mcell.ensure(m * 4);
     ovf.ensure(m * 4);
+    ovf_left.ensure(m * 4);
     mcap = m;
 }
 
@@ -690,9 +736,10 @@ void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
                                           off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>());
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
-    // borrow_insert for the few full-bin arrivals; exits at once when there are none
-    k_borrow<<<1, 32, 0, st>>>(ctr, M.soa(), mcell.as<uint32_t>(), ovf.as<uint32_t>(), A.soa(), off.as<uint32_t>(),
-                               cnt.as<uint32_t>(), (uint32_t)nc, kBorrowScanBins);
+    // borrow_insert for the full-bin arrivals; no work when there are none
+    k_borrow<<<num_sms, 128, 0, st>>>(ctr, M.soa(), mcell.as<uint32_t>(), ovf.as<uint32_t>(), ovf_left.as<uint32_t>(),
+                                      A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(), locks.as<unsigned int>(),
+                                      (uint32_t)nc, kBorrowScanBins);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
     PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, ctr, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
@@ -704,7 +751,9 @@ bool BinStore::finish_incremental(StepCounters& out) {
     out = *hcounters;
     if (out.err) return false;
     const bool mover_overflow = out.nmovers > mcap;
-    const uint32_t left = out.noverflow;  // unplaced: no donor, or everything after a mover overflow
+    // unplaced arrivals (no donor found); borrowed ones already sit in their bins
+    const uint32_t left = out.nleft;
+    const uint32_t* left_list = ovf_left.as<uint32_t>();
     borrowed += out.nborrowed;
     if (!mover_overflow && !left) return false;
     // Gpma::rebuild (gpma.hpp:119-122, :130-143) generalised: either the
@@ -716,7 +765,7 @@ bool BinStore::finish_incremental(StepCounters& out) {
     PICGPU_CUDA_TRY(cudaMemcpyAsync(&h32, off2.as<uint32_t>() + nc, 4, cudaMemcpyDeviceToHost, st));
     PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
     if (left) {
-        k_append_overflow<<<div_up(left, 256), 256, 0, st>>>(M.soa(), ovf.as<uint32_t>(), left, B.soa(), h32);
+        k_append_overflow<<<div_up(left, 256), 256, 0, st>>>(M.soa(), left_list, left, B.soa(), h32);
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
     }

@@ -43,9 +43,11 @@ struct SoaBuf {
 struct StepCounters {
     unsigned long long moved;
     unsigned int nmovers;     // movers detected (may exceed mover capacity)
-    unsigned int noverflow;   // arrivals that found no slack (after k_borrow: those still unplaced)
+    unsigned int noverflow;   // arrivals that found no slack in their own bin
     int err;                  // picgpu_status of the first device-side error
-    unsigned int nborrowed;   // arrivals placed by borrowing a following bin's slack
+    unsigned int nborrowed;   // ... placed by borrowing a following bin's slack
+    unsigned int nleft;       // ... with no donor (-> full re-sort)
+    unsigned int pad;
 };
 
 constexpr int kBorrowScanBins = 4;  // GpmaConfig::borrow_scan_bins (gpma.hpp:25)
@@ -63,7 +65,8 @@ struct BinStore {
     DevBuf keys, keys2, skeys, vals, vals2, start, endp, caps, cub_tmp;
     DevBuf mflag;             // per-slot mover flag (u8)
     SoaBuf M;                 // mover records
-    DevBuf mcell, ovf;        // mover target cell, overflow list
+    DevBuf mcell, ovf, ovf_left;  // mover target cell, overflow list, unplaced overflow
+    DevBuf locks;             // per-bin try-locks of the borrow kernel (always released)
     DevBuf counters;          // StepCounters
     StepCounters* hcounters = nullptr;  // pinned mirror
 
