@@ -495,10 +495,10 @@ static void enqueue_deposits(picgpu_session* s, uint32_t flags, uint64_t* lj, ui
 }
 
 // One step of the reference loop (simulation.hpp:753-829), device-resident:
-// [push + incremental sort] -> [J] -> [rho] -> [global sort].  Everything is
-// enqueued back to back; the host waits once, at the end, for the sorter's
-// counters.  In the rare step whose arrivals found no slack even after
-// borrowing, the bins are rebuilt and the deposits re-run on them.
+// [push + incremental sort] -> [J] -> [rho] -> [global sort].  The sorter's
+// counters are read once after the sort kernels (one host wait per step):
+// when an arrival found no slack even after borrowing, the bins are rebuilt
+// before anything is deposited on them.
 int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_step_stats* out) {
     return guard([&] {
         set_device(s);
@@ -510,20 +510,16 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
         picgpu_step_stats stats{};
         const uint64_t rebuilds0 = bs.rebuilds;
         const bool T = s->timing;
-        const bool sort = (flags & PICGPU_STEP_SORT) != 0;
-        uint64_t ls = 0, lj = 0, lr = 0;
-        if (sort) {
+        uint64_t lj = 0, lr = 0;
+        if (flags & PICGPU_STEP_SORT) {
             const double cap2 = (flags & PICGPU_STEP_PUSH) ? cap2_of(bs.hg, dt) : 0.0;
             const uint64_t l0 = g_launches.load();
             if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
             bs.enqueue_incremental((flags & PICGPU_STEP_PUSH) != 0, dt, cap2);
             if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
-            ls = g_launches.load() - l0;
-        }
-        enqueue_deposits(s, flags, &lj, &lr);
-        if (sort) {
+            const uint64_t ls = g_launches.load() - l0;
             StepCounters c{};
-            const bool rebuilt = bs.finish_incremental(c);
+            const bool rebuilt = bs.finish_incremental(c);  // host waits here
             if (c.err == PICGPU_EDOMAIN)
                 throw Status{c.err, "advance: particle displacement exceeds the single-cell cap"};
             if (c.err) throw Status{c.err, "cell_of: non-finite particle position"};
@@ -532,29 +528,14 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
             stats.overflowed = c.noverflow;
             if (T) {
                 accumulate_phase(s, 0, 0, 1, ls);
-                if (flags & PICGPU_STEP_CURRENT) {
-                    accumulate_phase(s, 5, 2, 3, 0);
-                    accumulate_phase(s, 3, 3, 4, lj);
-                }
-                if (flags & PICGPU_STEP_DENSITY) accumulate_phase(s, 4, 5, 6, lr);
-            }
-            if (rebuilt) {
-                if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
-                enqueue_deposits(s, flags, &lj, &lr);  // the bins changed: deposit again
-                if (T) {
-                    PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
-                    PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[1]));
-                    accumulate_phase(s, 2, 0, 1, lj + lr);
+                if (rebuilt) {
+                    PICGPU_CUDA_TRY(cudaEventRecord(s->ev[7], st));
+                    PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[7]));
+                    accumulate_phase(s, 2, 1, 7, g_launches.load() - l0 - ls);
                 }
             }
-        } else if (T && (flags & (PICGPU_STEP_CURRENT | PICGPU_STEP_DENSITY))) {
-            PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
-            if (flags & PICGPU_STEP_CURRENT) {
-                accumulate_phase(s, 5, 2, 3, 0);
-                accumulate_phase(s, 3, 3, 4, lj);
-            }
-            if (flags & PICGPU_STEP_DENSITY) accumulate_phase(s, 4, 5, 6, lr);
         }
+        enqueue_deposits(s, flags, &lj, &lr);
         if (flags & PICGPU_STEP_GLOBAL_SORT) {
             const uint64_t l0 = g_launches.load();
             if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
@@ -566,7 +547,14 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
                 accumulate_phase(s, 2, 0, 1, g_launches.load() - l0);
             }
         }
-        if (!(flags & PICGPU_STEP_NO_SYNC)) PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+        if (!(flags & PICGPU_STEP_NO_SYNC) || T) PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+        if (T) {
+            if (flags & PICGPU_STEP_CURRENT) {
+                accumulate_phase(s, 5, 2, 3, 0);
+                accumulate_phase(s, 3, 3, 4, lj);
+            }
+            if (flags & PICGPU_STEP_DENSITY) accumulate_phase(s, 4, 5, 6, lr);
+        }
         stats.rebuilt = bs.rebuilds != rebuilds0;
         stats.capacity = bs.capacity;
         stats.num_particles = bs.n;

@@ -49,7 +49,19 @@ template <>
 struct JCfg<1> {
     static constexpr int G = 1, PX = 32, PY = 4, MINB = 4, CH = 1;
 };
-// (TSC / QSP use the warp-per-pencil kernel below.)
+// TSC / QSP, "lane" variant: 4 lanes per pencil (lane = jy), 8 pencils per
+// warp, 48 accumulators per lane (4 ix x 3 c x 4 kz).
+#ifndef PICGPU_LANE_MINB
+#define PICGPU_LANE_MINB 3
+#endif
+template <>
+struct JCfg<2> {
+    static constexpr int G = 4, PX = 8, PY = 4, MINB = PICGPU_LANE_MINB, CH = 4;
+};
+template <>
+struct JCfg<3> {
+    static constexpr int G = 4, PX = 8, PY = 4, MINB = PICGPU_LANE_MINB, CH = 4;
+};
 
 template <int ORDER>
 struct JLayout {
@@ -58,9 +70,14 @@ struct JLayout {
     static constexpr int NJ = W / C::G;                 // jy values per lane
     static constexpr int NP = C::PX * C::PY;            // pencils per CTA
     static constexpr int NT = NP * C::G;                // threads per CTA
-    static constexpr int REC = 5 * W + 2;               // a[3][W] | sy[W] | sz[W] | pad: 22 doubles (176 B)
-    static constexpr int PLANE = NP * REC + 2;          // one chunk slot for all pencils (+16 B skew)
-    static constexpr int STAGE = C::G > 1 ? C::CH * PLANE : 0;
+    // Field-major staging: field f (a[c][ix] = c*W+ix, sy[t] = 3W+t, sz[t] =
+    // 4W+t) of chunk position l of pencil grp at [f*FSS + l*SS + grp].  SS =
+    // NP + 4 makes the writes of a half-warp (4 pencils x 4 positions) hit 16
+    // distinct banks and the reads (8 pencils, same position) contiguous.
+    static constexpr int NF = 5 * W;
+    static constexpr int SS = NP + 4;
+    static constexpr int FSS = C::CH * SS;
+    static constexpr int STAGE = C::G > 1 ? NF * FSS : 0;
     // One emitted plane of every pencil, offset-major: [jy][ix][c][PY][PX] with
     // a 2-double skew per (jy,ix,c) row so the 4 jy-lanes of a pencil write
     // to distinct banks and the gather reads consecutive pencils contiguously.
@@ -109,6 +126,50 @@ __device__ __forceinline__ void particle_window(const GridD& g, const PData& d, 
     }
 }
 
+// J-only prologue: same cell location (bit-identical locate_axis, so the
+// particle is in its bin's cell), weights evaluated with FMA-contracted
+// polynomials (J is compared at 1e-12; rho keeps the exact forms).
+template <int ORDER>
+__device__ __forceinline__ void weights_fast(double d, double (&s)[4]) {
+    if constexpr (ORDER == 3) {
+        const double t2 = d * d, t3 = t2 * d, u = 1.0 - d;
+        s[0] = u * u * u * (1.0 / 6.0);
+        s[1] = fma(0.5, t3, fma(-1.0, t2, 2.0 / 3.0));
+        s[2] = fma(-0.5, t3, fma(0.5, t2, fma(0.5, d, 1.0 / 6.0)));
+        s[3] = t3 * (1.0 / 6.0);
+    } else {
+        const bool up = d >= 0.5;
+        const double dl = up ? d - 1.0 : d;
+        const double a = 0.5 - dl, b = 0.5 + dl;
+        const double w0 = 0.5 * a * a, w1 = fma(-dl, dl, 0.75), w2 = 0.5 * b * b;
+        s[0] = up ? 0.0 : w0;
+        s[1] = up ? w0 : w1;
+        s[2] = up ? w1 : w2;
+        s[3] = up ? w2 : 0.0;
+    }
+}
+
+template <int ORDER>
+__device__ __forceinline__ void particle_window_fast(const GridD& g, const PData& d, double q, double (&a)[3][4],
+                                                     double (&sy)[4], double (&sz)[4]) {
+    const double qw = q * d.w;
+    const double wq0 = qw * d.vx, wq1 = qw * d.vy, wq2 = qw * d.vz;
+    double fx, fy, fz;
+    locate_axis(d.x, g.ox, g.dx, g.inv_dx, g.pow2x, g.nx, fx);
+    locate_axis(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, fy);
+    locate_axis(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, fz);
+    double sx[4];
+    weights_fast<ORDER>(fx, sx);
+    weights_fast<ORDER>(fy, sy);
+    weights_fast<ORDER>(fz, sz);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        a[0][t] = wq0 * sx[t];
+        a[1][t] = wq1 * sx[t];
+        a[2][t] = wq2 * sx[t];
+    }
+}
+
 template <int W, int NJ>
 __device__ __forceinline__ void accumulate(double (&acc)[W][NJ][W][3], const double (&a)[3][W], const double (&syv)[NJ],
                                            const double (&sz)[W]) {
@@ -137,7 +198,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
 
     extern __shared__ __align__(16) double smem[];
     double* patch = smem;                 // [2][W(jy)][W(ix)][3][PSTRIDE]
-    double* stage = smem + 2 * L::PATCH;  // [CH][NP][REC] (+skew per chunk slot)
+    double* stage = smem + 2 * L::PATCH;  // [NF][CH][SS]
 
     const int tid = threadIdx.x;
     const int grp = tid / G, lg = tid % G;
@@ -217,41 +278,40 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
 #pragma unroll
                             for (int t = 0; t < W; ++t) a[0][t] = a[1][t] = a[2][t] = sy[t] = sz[t] = 0.0;
                         }
-                        double2* rec = reinterpret_cast<double2*>(stage + lg * L::PLANE + grp * L::REC);
+                        double* rec = stage + lg * L::SS + grp;
 #pragma unroll
                         for (int c = 0; c < 3; ++c)
 #pragma unroll
-                            for (int t = 0; t < W; t += 2) rec[(c * W + t) / 2] = make_double2(a[c][t], a[c][t + 1]);
+                            for (int t = 0; t < W; ++t) rec[(c * W + t) * L::FSS] = a[c][t];
 #pragma unroll
-                        for (int t = 0; t < W; t += 2) {
-                            rec[(3 * W + t) / 2] = make_double2(sy[t], sy[t + 1]);
-                            rec[(4 * W + t) / 2] = make_double2(sz[t], sz[t + 1]);
+                        for (int t = 0; t < W; ++t) {
+                            rec[(3 * W + t) * L::FSS] = sy[t];
+                            rec[(4 * W + t) * L::FSS] = sz[t];
                         }
                     }
                     __syncwarp();
                     const int nn = min(CH, m - base);
 #pragma unroll 1
                     for (int jj0 = 0; jj0 < nn; ++jj0) {
-                        const double2* r = reinterpret_cast<const double2*>(stage + jj0 * L::PLANE + grp * L::REC);
-                        double a[3][W], syv[NJ], sz[W];
+                        const double* r = stage + jj0 * L::SS + grp;
+                        double b[W][NJ];
+#pragma unroll
+                        for (int kz = 0; kz < W; ++kz) {
+                            const double z = r[(4 * W + kz) * L::FSS];
+#pragma unroll
+                            for (int jj = 0; jj < NJ; ++jj) b[kz][jj] = r[(3 * W + lg * NJ + jj) * L::FSS] * z;
+                        }
 #pragma unroll
                         for (int c = 0; c < 3; ++c)
 #pragma unroll
-                            for (int t = 0; t < W; t += 2) {
-                                const double2 v = r[(c * W + t) / 2];
-                                a[c][t] = v.x;
-                                a[c][t + 1] = v.y;
+                            for (int ix = 0; ix < W; ++ix) {
+                                const double av = r[(c * W + ix) * L::FSS];
+#pragma unroll
+                                for (int kz = 0; kz < W; ++kz)
+#pragma unroll
+                                    for (int jj = 0; jj < NJ; ++jj)
+                                        acc[kz][jj][ix][c] = fma(av, b[kz][jj], acc[kz][jj][ix][c]);
                             }
-#pragma unroll
-                        for (int jj = 0; jj < NJ; ++jj)
-                            syv[jj] = reinterpret_cast<const double*>(r)[3 * W + lg * NJ + jj];
-#pragma unroll
-                        for (int t = 0; t < W; t += 2) {
-                            const double2 v = r[(4 * W + t) / 2];
-                            sz[t] = v.x;
-                            sz[t + 1] = v.y;
-                        }
-                        accumulate<W, NJ>(acc, a, syv, sz);
                     }
                     __syncwarp();
                 }
@@ -333,22 +393,23 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
 // (all lanes busy whatever the cell counts), writes a 30-double record
 // {a[ix][c] = wq_c*sx[ix] (12), b[jy][kz] = sy[jy]*sz[kz] (16)} to the warp's
 // staging area, and the next chunk's loads are already in flight.  Then the
-// two half-warps consume the staged particles two at a time (even/odd, same
-// cell): lane = (half, jy, ix) owns 4 kz x 3 comps = 12 accumulators, reads
-// 7 operands with broadcast LDS.64 (1 wavefront each; LDS.128 costs 4) and
-// issues 12 DFMA.  The z window slides inside the registers; the halves'
-// partial sums meet with one shuffle when a plane is emitted.
+// four quarter-warps consume the staged particles four at a time (same
+// cell): lane = (quarter, jy, ix pair) owns 4 kz x 2 ix x 3 comps = 24
+// accumulators, reads 10 operands with LDS.64 (1 wavefront each; LDS.128
+// costs 4) and issues 24 DFMA.  The z window slides by register rotation
+// (the z loop is unrolled 4x); the quarters' partial sums meet with two
+// shuffles when a plane is emitted.
 #ifndef PICGPU_WARP_MINB
 #define PICGPU_WARP_MINB 2
 #endif
 struct WCfg {
     static constexpr int PX = 4, PY = 2, NW = PX * PY, NT = NW * 32, MINB = PICGPU_WARP_MINB;
     // Staging is field-major: field f of chunk particle l at [f*FS + l].  The
-    // 34-double field stride makes the staging writes conflict-free and puts
-    // the two half-warps' operands (particles l, l+1) in disjoint banks; the
-    // operands of one lane sit 34 doubles apart, so ptxas cannot fuse them
+    // 36-double field stride makes the staging writes conflict-free and puts
+    // the four quarter-warps' operands (particles l..l+3) in disjoint banks;
+    // the operands of one lane sit FS doubles apart, so ptxas cannot fuse them
     // into LDS.128 (4 wavefronts) -- every operand load is a 1-wavefront LDS.64.
-    static constexpr int NF = 28, FS = 34, REC = NF * FS;  // per-warp staging block (doubles)
+    static constexpr int NF = 28, FS = 36, REC = NF * FS;  // per-warp staging block (doubles)
     static constexpr int R = 2;                         // planes emitted per CTA barrier
     static constexpr int PS = 49;                       // per-pencil patch stride (3*16 + 1 skew)
     static constexpr int PATCH = NW * PS;               // one plane slot: [pencil][c][jy][ix]
@@ -383,7 +444,7 @@ __global__ void __launch_bounds__(WCfg::NT, WCfg::MINB)
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int px = wid % PX, py = wid / PX;
-    const int jyl = lane & 3, ixl = (lane >> 2) & 3, hh = lane >> 4;
+    const int jyl = lane & 3, ixp = (lane >> 2) & 1, qq = lane >> 3;  // (jy, ix pair, quarter)
     const int i0 = blockIdx.x * PX, j0 = blockIdx.y * PY;
     const int k0 = blockIdx.z * zlen;
     const int k1 = min(k0 + zlen, g.nz);
@@ -473,9 +534,11 @@ __global__ void __launch_bounds__(WCfg::NT, WCfg::MINB)
     if (nvalid) load_particle(p, nslot, nxt);
     bool pending = __any_sync(FULL, nvalid);
 
-    double acc[W][3];
+    double acc[W][2][3];  // [kz slot][ix in pair][c]
 #pragma unroll
-    for (int kz = 0; kz < W; ++kz) acc[kz][0] = acc[kz][1] = acc[kz][2] = 0.0;
+    for (int kz = 0; kz < W; ++kz)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[kz][e][0] = acc[kz][e][1] = acc[kz][e][2] = 0.0;
     int navail = 0, nidx = 0, cz_reg = 0x7fffffff;
     const int T = k1 + W - 1 - k0;  // planes emitted by every warp (CTA-uniform)
 
@@ -492,7 +555,7 @@ __global__ void __launch_bounds__(WCfg::NT, WCfg::MINB)
                     __syncwarp();  // the previous chunk's records are no longer read
                     if (nvalid) {  // prologue: shape.hpp:64-85 + particle_weights :46-50
                         double a[3][W], sy[W], sz[W];
-                        particle_window<ORDER>(g, nxt, q, a, sy, sz);
+                        particle_window_fast<ORDER>(g, nxt, q, a, sy, sz);
                         // fields: a[c][ix] at f = c*4 + ix; b[kz][jy] = sy*sz at f = 12 + kz*4 + jy
                         double* rr = recs + lane;
 #pragma unroll
@@ -513,37 +576,32 @@ __global__ void __launch_bounds__(WCfg::NT, WCfg::MINB)
                     pending = __any_sync(FULL, nvalid);
                     continue;
                 }
-                // staged particles nidx.. of cell k (contiguous): the two
-                // half-warps take them two at a time
+                // staged particles nidx.. of cell k (contiguous): the four
+                // quarter-warps take them four at a time
                 const unsigned mk = __ballot_sync(FULL, cz_reg == k) & (FULL << nidx);
                 const int cntk = __popc(mk);
-                const double* ra = recs + ixl * FS + nidx + hh;
-                const double* rb = recs + (12 + jyl) * FS + nidx + hh;
-                int t = 0;
-#pragma unroll 2
-                for (; t + 1 < cntk; t += 2) {
-                    const double a0 = ra[0], a1 = ra[4 * FS], a2 = ra[8 * FS];
+                const double* ra = recs + (2 * ixp) * FS + nidx + qq;
+                const double* rb = recs + (12 + jyl) * FS + nidx + qq;
+                for (int t = 0; t < cntk; t += 4) {
+                    if (t + qq < cntk) {
+                        double av[3][2], bv[W];
 #pragma unroll
-                    for (int kz = 0; kz < W; ++kz) {
-                        const double b = rb[kz * 4 * FS];
-                        double* A = acc[(kz + RT) & 3];
-                        A[0] = fma(a0, b, A[0]);
-                        A[1] = fma(a1, b, A[1]);
-                        A[2] = fma(a2, b, A[2]);
-                    }
-                    ra += 2;
-                    rb += 2;
-                }
-                if (t < cntk && hh == 0) {  // odd count: the last one goes to half 0
-                    const double a0 = ra[0], a1 = ra[4 * FS], a2 = ra[8 * FS];
+                        for (int c = 0; c < 3; ++c) {
+                            av[c][0] = ra[(c * 4) * FS];
+                            av[c][1] = ra[(c * 4 + 1) * FS];
+                        }
 #pragma unroll
-                    for (int kz = 0; kz < W; ++kz) {
-                        const double b = rb[kz * 4 * FS];
-                        double* A = acc[(kz + RT) & 3];
-                        A[0] = fma(a0, b, A[0]);
-                        A[1] = fma(a1, b, A[1]);
-                        A[2] = fma(a2, b, A[2]);
+                        for (int kz = 0; kz < W; ++kz) bv[kz] = rb[kz * 4 * FS];
+#pragma unroll
+                        for (int kz = 0; kz < W; ++kz)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e)
+#pragma unroll
+                                for (int c = 0; c < 3; ++c)
+                                    acc[(kz + RT) & 3][e][c] = fma(av[c][e], bv[kz], acc[(kz + RT) & 3][e][c]);
                     }
+                    ra += 4;
+                    rb += 4;
                 }
                 nidx += cntk;
                 if (nidx < navail || cntk == 0) break;  // the rest of the chunk is in later cells
@@ -552,14 +610,17 @@ __global__ void __launch_bounds__(WCfg::NT, WCfg::MINB)
         // Plane k+OFF is final for this pencil: add the halves, emit, recycle the slot.
         constexpr int SL = RT & 1, PH = (RT >> 1) & 1;  // ring slot and phase (R = 2 planes per barrier)
         {
-            double* pp = patch + (PH * WCfg::R + SL) * WCfg::PATCH + wid * PS + jyl * W + ixl;
-            double* A = acc[RT & 3];
+            double* pp = patch + (PH * WCfg::R + SL) * WCfg::PATCH + wid * PS + jyl * W + 2 * ixp;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const double v = A[c] + __shfl_xor_sync(FULL, A[c], 16);
-                if (hh == 0) pp[c * 16] = v;
-                A[c] = 0.0;
-            }
+            for (int e = 0; e < 2; ++e)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double v = acc[RT & 3][e][c];
+                    v += __shfl_xor_sync(FULL, v, 8);
+                    v += __shfl_xor_sync(FULL, v, 16);
+                    if (qq == 0) pp[c * 16 + e] = v;
+                    acc[RT & 3][e][c] = 0.0;
+                }
         }
         if (SL == 0 && kb + RT + 1 < T) return;  // flush every 2 planes (and after the last)
         __syncthreads();
@@ -910,12 +971,16 @@ void launch_order(const GridD& g, const CSoa& p, const uint32_t* off, const uint
 
 }  // namespace
 
-// Order-2/3 contraction: 0 = FP64 DMMA (default), 1 = DFMA register blocking.
-// PICGPU_J_VARIANT=dfma selects the latter (ablation / profiling).
+// Order-2/3 kernel variant (ablation / profiling; PICGPU_J_VARIANT):
+//   lane (default) -- 8 pencils per warp, 48 DFMA accumulators per lane
+//   dfma           -- one warp per pencil, streamed chunks, 24 accumulators per lane
+//   dmma           -- one warp per pencil, FP64 tensor-core contraction
 static int j_variant() {
     static const int v = [] {
         const char* e = std::getenv("PICGPU_J_VARIANT");
-        return (e && std::string(e) == "dfma") ? 1 : 0;
+        if (!e) return 0;
+        const std::string s(e);
+        return s == "dfma" ? 1 : s == "dmma" ? 2 : 0;
     }();
     return v;
 }
@@ -927,11 +992,13 @@ void launch_deposit_current(int order, const GridD& g, const CSoa& p, const uint
         case 1: launch_order<1>(g, p, off, cnt, q, j, num_sms, st); break;
         case 2:
             if (j_variant() == 1) launch_warp<2>(g, p, off, cnt, q, j, num_sms, st);
-            else launch_dmma<2>(g, p, off, cnt, q, j, num_sms, st);
+            else if (j_variant() == 2) launch_dmma<2>(g, p, off, cnt, q, j, num_sms, st);
+            else launch_order<2>(g, p, off, cnt, q, j, num_sms, st);
             break;
         case 3:
             if (j_variant() == 1) launch_warp<3>(g, p, off, cnt, q, j, num_sms, st);
-            else launch_dmma<3>(g, p, off, cnt, q, j, num_sms, st);
+            else if (j_variant() == 2) launch_dmma<3>(g, p, off, cnt, q, j, num_sms, st);
+            else launch_order<3>(g, p, off, cnt, q, j, num_sms, st);
             break;
         default: throw Status{PICGPU_EINVAL, "deposit: shape order must be 1, 2 or 3"};
     }

@@ -4,7 +4,7 @@
 // Reference anchors (proj/include/pic/):
 //   gpma_build          gpma.hpp:379-402  -> BinStore::full_sort_from_B (stable radix sort by cell)
 //   Gpma::layout        gpma.hpp:269-302  -> k_counts_caps + scan (same capacity rule)
-//   detect_moves        gpma.hpp:162-177  -> k_push_detect (fused with the push, warp-ballot append)
+//   detect_moves        gpma.hpp:162-177  -> k_push (fused with the push, warp-ballot append) + k_compact
 //   apply_moves/insert  gpma.hpp:110-125, :248-262 -> k_insert (per-bin atomic tail cursor into slack)
 //   borrow/overflow     gpma.hpp:337-370  -> overflow list -> rebuild (relayout with fresh slack)
 //   rebuild             gpma.hpp:130-143  -> BinStore::rebuild_overflow
@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <utility>
 
 #include "kernels.hpp"
@@ -34,8 +35,11 @@ void DevBuf::release() {
 
 void DevBuf::ensure(size_t b) {
     if (b <= bytes) return;
+    // regrowth keeps 12.5% headroom: a store whose capacity creeps up after
+    // rebuilds must not pay cudaFree/cudaMalloc (device-synchronising) each time
+    const size_t grown = bytes ? b + b / 8 : b;
     release();
-    const size_t nb = std::max<size_t>(b, 256);
+    const size_t nb = std::max<size_t>(grown, 256);
     if (cudaMalloc(&p, nb) != cudaSuccess) {
         cudaGetLastError();
         p = nullptr;
@@ -216,132 +220,136 @@ __global__ void __launch_bounds__(256) k_relayout(const Soa src, const uint32_t*
     }
 }
 
-// Push (optional) + move detection + in-bin compaction, one CTA per BPB bins.
-//  - pushes every valid slot (bit-exact pic::advance), recomputes its cell;
-//  - a particle whose cell changed is appended to the mover list
-//    (warp-ballot aggregated append) and flagged;
-//  - after a barrier, one thread per bin compacts the stayers in slot order
-//    (stable) and writes the bin's new count.
-// Movers that do not fit the mover buffer stay in their (now stale) bin and
-// are flagged 2; the host then falls back to a full re-sort.
-template <bool PUSH>
-__global__ void __launch_bounds__(256) k_push_detect(const GridD g, const Soa A, const uint32_t* __restrict__ off,
-                                                     uint32_t* __restrict__ cnt, uint8_t* __restrict__ mflag,
-                                                     double dt, double cap2, const Soa M,
-                                                     uint32_t* __restrict__ mcell, uint32_t mcap,
-                                                     StepCounters* ctr) {
-    __shared__ uint32_t so[BPB + 1], sc[BPB], sdep[BPB];
-    __shared__ unsigned long long smoved;
-    const uint32_t c0 = blockIdx.x * BPB;
-    const int nb = (int)umin((uint32_t)BPB, g.ncells - c0);
-    for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
-        so[b] = off[c0 + b];
-        if (b < nb) {
-            sc[b] = cnt[c0 + b];
-            sdep[b] = 0;
+// Every slack slot holds a sentinel x (all-ones bit pattern, a NaN no valid
+// particle can carry: non-finite positions are rejected), so the push can
+// stream over raw slots without knowing the bin layout.
+__device__ __forceinline__ bool is_gap(double x) { return __double_as_longlong(x) == -1LL; }
+
+// Push (optional) + move detection (pic::advance + Gpma::detect_moves,
+// workload.hpp:139-155, gpma.hpp:162-177).  Each CTA streams one contiguous
+// chunk of UNR*256 slots; a thread issues all loads of its UNR slots up front.
+// A particle whose cell changed is flagged and appended to the mover list:
+// slots are numbered with a shared-memory atomic and the CTA reserves its
+// range with ONE global atomic (no per-warp atomic round trips on the hot
+// path); departures are counted per bin with fire-and-forget reductions.
+// Movers that do not fit the mover buffer stay in their (now stale) bin with
+// flag 2; the host then re-sorts fully.
+template <bool PUSH, int UNR>
+__global__ void __launch_bounds__(256) k_push(const GridD g, const Soa A, uint64_t slots, uint8_t* __restrict__ mflag,
+                                              double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
+                                              uint32_t mcap, uint32_t* __restrict__ dep, StepCounters* ctr) {
+    __shared__ unsigned s_cnt, s_base;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const uint64_t cbeg = (uint64_t)blockIdx.x * (UNR * blockDim.x);
+    const uint64_t cend = min(cbeg + UNR * blockDim.x, slots);
+    double x[UNR], y[UNR], z[UNR], vx[UNR], vy[UNR], vz[UNR];
+    uint32_t nc[UNR], before[UNR];
+    int lidx[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+        const uint64_t s = cbeg + threadIdx.x + u * blockDim.x;
+        x[u] = __longlong_as_double(-1LL);
+        y[u] = z[u] = vx[u] = vy[u] = vz[u] = 0.0;
+        if (s < cend) {
+            x[u] = A.x[s];
+            y[u] = A.y[s];
+            z[u] = A.z[s];
+            vx[u] = A.vx[s];
+            vy[u] = A.vy[s];
+            vz[u] = A.vz[s];
         }
     }
-    if (threadIdx.x == 0) smoved = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
     unsigned local_moved = 0;
-    // Two slots per thread per pass: both slots' loads are issued before either
-    // is processed (more bytes in flight per thread).
-    constexpr int UNR = 2;
-    const uint32_t S1 = so[nb];
-    for (uint32_t s0 = so[0] + threadIdx.x; s0 < S1; s0 += UNR * blockDim.x) {
-        double x[UNR], y[UNR], z[UNR], vx[UNR], vy[UNR], vz[UNR];
-        int bb[UNR];
-        bool valid[UNR];
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const uint32_t s = s0 + u * blockDim.x;
-            bb[u] = 0;
-            valid[u] = false;
-            x[u] = y[u] = z[u] = vx[u] = vy[u] = vz[u] = 0.0;
-            if (s < S1) {
-                bb[u] = find_bin(so, nb, s);
-                valid[u] = s - so[bb[u]] < sc[bb[u]];
+    for (int u = 0; u < UNR; ++u) {
+        const uint64_t s = cbeg + threadIdx.x + u * blockDim.x;
+        lidx[u] = -1;
+        nc[u] = before[u] = 0;
+        if (is_gap(x[u])) continue;
+        bool ok = finite3(x[u], y[u], z[u]);
+        bool moved = false;
+        if (!ok) {
+            raise_error(&ctr->err, PICGPU_EINVAL);
+        } else {
+            before[u] = cell_linear(g, x[u], y[u], z[u]);
+            if (PUSH) {
+                if (!push_one(g, dt, cap2, x[u], y[u], z[u], vx[u], vy[u], vz[u])) {
+                    raise_error(&ctr->err, PICGPU_EDOMAIN);
+                    ok = false;
+                } else {
+                    A.x[s] = x[u];
+                    A.y[s] = y[u];
+                    A.z[s] = z[u];
+                    if (!finite3(x[u], y[u], z[u])) {
+                        raise_error(&ctr->err, PICGPU_EINVAL);
+                        ok = false;
+                    }
+                }
             }
-            if (valid[u]) {
-                x[u] = A.x[s];
-                y[u] = A.y[s];
-                z[u] = A.z[s];
-                vx[u] = A.vx[s];
-                vy[u] = A.vy[s];
-                vz[u] = A.vz[s];
+            if (ok) {
+                nc[u] = cell_linear(g, x[u], y[u], z[u]);
+                moved = nc[u] != before[u];
             }
         }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const uint32_t s = s0 + u * blockDim.x;
-            const int b = bb[u];
-            bool moved = false;
-            uint32_t nc = 0;
-            if (valid[u]) {
-                bool ok = true;
-                if (PUSH) {
-                    if (!push_one(g, dt, cap2, x[u], y[u], z[u], vx[u], vy[u], vz[u])) {
-                        raise_error(&ctr->err, PICGPU_EDOMAIN);
-                        ok = false;
-                    } else {
-                        A.x[s] = x[u];
-                        A.y[s] = y[u];
-                        A.z[s] = z[u];
-                    }
-                }
-                if (ok && !finite3(x[u], y[u], z[u])) {
-                    raise_error(&ctr->err, PICGPU_EINVAL);
-                    ok = false;
-                }
-                if (ok) {
-                    nc = cell_linear(g, x[u], y[u], z[u]);
-                    moved = nc != c0 + (uint32_t)b;
-                }
-                mflag[s] = moved ? 1 : 0;
-            }
-            const unsigned act = __activemask();
-            const unsigned mv = __ballot_sync(act, moved);
-            if (mv) {
-                const int leader = __ffs(mv) - 1;
-                unsigned base = 0;
-                if (lane == leader) base = atomicAdd(&ctr->nmovers, (unsigned)__popc(mv));
-                base = __shfl_sync(act, base, leader);
-                if (moved) {
-                    const unsigned idx = base + __popc(mv & ((1u << lane) - 1u));
-                    ++local_moved;
-                    if (idx < mcap) {
-                        atomicAdd(&sdep[b], 1u);
-                        M.x[idx] = x[u];
-                        M.y[idx] = y[u];
-                        M.z[idx] = z[u];
-                        M.vx[idx] = vx[u];
-                        M.vy[idx] = vy[u];
-                        M.vz[idx] = vz[u];
-                        M.w[idx] = A.w[s];
-                        M.id[idx] = A.id[s];
-                        mcell[idx] = nc;
-                    } else {
-                        mflag[s] = 2;  // stays in its stale bin; host re-sorts fully
-                    }
-                }
-            }
+        mflag[s] = moved ? 1 : 0;
+        if (moved) {
+            lidx[u] = (int)atomicAdd(&s_cnt, 1u);
+            ++local_moved;
         }
     }
-    if (local_moved) atomicAdd(&smoved, (unsigned long long)local_moved);
     __syncthreads();
-    // Stable in-bin compaction of the stayers, one warp per bin with
-    // departures: ballot the keep-mask 32 slots at a time, every kept lane
-    // loads its particle, then stores it at its rank (reads of a chunk all
-    // precede its writes, and writes never reach a later chunk's slots).
-    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    for (int b = warp; b < nb; b += nwarps) {
-        if (sdep[b] == 0) continue;
-        const uint32_t lo = so[b], hi = so[b] + sc[b];
+    if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(&ctr->nmovers, s_cnt) : 0u;
+    __syncthreads();
+    const unsigned base = s_base;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+        if (lidx[u] < 0) continue;
+        const uint64_t s = cbeg + threadIdx.x + u * blockDim.x;
+        const unsigned idx = base + (unsigned)lidx[u];
+        if (idx < mcap) {
+            M.x[idx] = x[u];
+            M.y[idx] = y[u];
+            M.z[idx] = z[u];
+            M.vx[idx] = vx[u];
+            M.vy[idx] = vy[u];
+            M.vz[idx] = vz[u];
+            M.w[idx] = A.w[s];
+            M.id[idx] = A.id[s];
+            mcell[idx] = nc[u];
+            atomicAdd(&dep[before[u]], 1u);  // result unused: RED
+        } else {
+            mflag[s] = 2;  // stays in its stale bin; host re-sorts fully
+        }
+    }
+    const unsigned wm = __reduce_add_sync(0xffffffffu, local_moved);
+    if ((threadIdx.x & 31) == 0 && wm) atomicAdd(&ctr->moved, (unsigned long long)wm);
+}
+
+// Stable in-bin compaction of every bin that lost particles (the GPU side of
+// Gpma::delete_slot, gpma.hpp:90-95).  A warp watches 32 bins' departure
+// counts with one ballot and compacts the dirty ones in turn: it ballots the
+// keep-mask 32 slots at a time, every kept lane loads its particle, then
+// stores it at its rank (reads of a chunk all precede its writes, and writes
+// never reach a later chunk's slots); the vacated tail becomes slack
+// (sentinel) again and the count is reset.  (Filling each hole from the tail
+// instead moves fewer particles but measured slower: 0.42 vs 0.24 ms at C2.)
+__global__ void __launch_bounds__(256) k_compact(const Soa A, const uint32_t* __restrict__ off, uint32_t* cnt,
+                                                 const uint8_t* __restrict__ mflag, uint32_t* dep, uint32_t ncells) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t cl = wid * 32 + lane;
+    const bool dirty_lane = cl < ncells && dep[cl] != 0;
+    unsigned todo = __ballot_sync(0xffffffffu, dirty_lane);
+    while (todo) {
+        const int bl = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint32_t c = wid * 32 + bl;
+        const uint32_t lo = off[c], hi = lo + cnt[c];
         uint32_t wpos = lo;
         for (uint32_t base = lo; base < hi; base += 32) {
             const uint32_t r = base + lane;
-            const bool keep = r < hi && mflag[r] != 1;
+            const bool keep = r < hi && mflag[r] != 1;  // flag 2 (unrecorded mover) stays
             const unsigned km = __ballot_sync(0xffffffffu, keep);
             const uint32_t dst = wpos + __popc(km & ((1u << lane) - 1u));
             double px = 0, py = 0, pz = 0, pvx = 0, pvy = 0, pvz = 0, pw = 0;
@@ -361,9 +369,10 @@ __global__ void __launch_bounds__(256) k_push_detect(const GridD g, const Soa A,
             __syncwarp();
             wpos += __popc(km);
         }
-        if (lane == 0) cnt[c0 + b] = wpos - lo;
+        for (uint32_t r = wpos + lane; r < hi; r += 32) A.x[r] = __longlong_as_double(-1LL);
+        if (lane == 0) cnt[c] = wpos - lo;
     }
-    if (threadIdx.x == 0 && smoved) atomicAdd(&ctr->moved, smoved);
+    if (dirty_lane) dep[cl] = 0;
 }
 
 // Migration: every recorded mover takes the next slot of its target bin's
@@ -447,6 +456,17 @@ __global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restr
             break;
         }
     }
+}
+
+// Gpma::rebuild tail (gpma.hpp:137): arrivals that found no slack even after
+// borrowing go after their bin's held particles in the fresh layout.
+__global__ void k_place_left(const Soa M, const uint32_t* __restrict__ mcell, const uint32_t* __restrict__ left,
+                             uint32_t nleft, const Soa dst, const uint32_t* __restrict__ doff, uint32_t* held) {
+    const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= nleft) return;
+    const uint32_t i = left[o];
+    const uint32_t d = mcell[i];
+    copy_particle(M, i, dst, (uint64_t)doff[d] + atomicAdd(&held[d], 1u));
 }
 
 // Overflowed movers appended after a packed store (mover-buffer fallback).
@@ -589,6 +609,8 @@ void BinStore::init(const picgpu_grid& grid, double gap_ratio, uint32_t mg, cuda
     PICGPU_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, nc * 4, st));
     locks.ensure(nc * 4 + 4);
     PICGPU_CUDA_TRY(cudaMemsetAsync(locks.p, 0, nc * 4 + 4, st));
+    dep.ensure(nc * 4 + 4);
+    PICGPU_CUDA_TRY(cudaMemsetAsync(dep.p, 0, nc * 4 + 4, st));
     capacity = 0;
     n = 0;
 }
@@ -651,6 +673,7 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev) {
     if (hcounters->err) throw Status{hcounters->err, "cell_of: non-finite particle position"};
     A.ensure(capacity_next);
     mflag.ensure(capacity_next + 1);
+    PICGPU_CUDA_TRY(cudaMemsetAsync(A.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
     swap_buf(off, off2);
     if (np) {
         k_gather_sorted<<<div_up((long long)np, 256), 256, 0, st>>>(b, vals2.as<uint32_t>(), skeys.as<uint32_t>(),
@@ -663,6 +686,10 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev) {
     }
     capacity = capacity_next;
     n = np;
+    // the spare store (relayout / rebuild target) gets the same capacity + headroom
+    // now, outside any timed step, instead of at the first rebuild
+    B.ensure(capacity + capacity / 8);
+    mflag.ensure(capacity + capacity / 8 + 1);
 }
 
 void BinStore::relayout() {
@@ -673,6 +700,7 @@ void BinStore::relayout() {
     layout_from_counts(n);
     B.ensure(capacity_next);
     mflag.ensure(capacity_next + 1);
+    PICGPU_CUDA_TRY(cudaMemsetAsync(B.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
     if (nc) {
         k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
                                                                B.soa(), off2.as<uint32_t>(), (uint32_t)nc);
@@ -721,15 +749,18 @@ void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
     StepCounters* ctr = counters.as<StepCounters>();
     PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
     if (!nc || !n) return;
-    const int blocks = div_up((long long)nc, BPB);
+    constexpr int UNR = 2;
+    const int blocks = (int)((capacity + 256 * UNR - 1) / (256 * UNR));
     if (push)
-        k_push_detect<true><<<blocks, 256, 0, st>>>(g, A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                    mflag.as<uint8_t>(), dt, cap2, M.soa(), mcell.as<uint32_t>(),
-                                                    (uint32_t)mcap, ctr);
+        k_push<true, UNR><<<blocks, 256, 0, st>>>(g, A.soa(), capacity, mflag.as<uint8_t>(), dt, cap2, M.soa(),
+                                                  mcell.as<uint32_t>(), (uint32_t)mcap, dep.as<uint32_t>(), ctr);
     else
-        k_push_detect<false><<<blocks, 256, 0, st>>>(g, A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                     mflag.as<uint8_t>(), dt, cap2, M.soa(), mcell.as<uint32_t>(),
-                                                     (uint32_t)mcap, ctr);
+        k_push<false, UNR><<<blocks, 256, 0, st>>>(g, A.soa(), capacity, mflag.as<uint8_t>(), dt, cap2, M.soa(),
+                                                   mcell.as<uint32_t>(), (uint32_t)mcap, dep.as<uint32_t>(), ctr);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+    k_compact<<<div_up((long long)nc, 256), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                          mflag.as<uint8_t>(), dep.as<uint32_t>(), (uint32_t)nc);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
     k_insert<<<num_sms * 4, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap, ctr, A.soa(),
@@ -756,10 +787,37 @@ bool BinStore::finish_incremental(StepCounters& out) {
     const uint32_t* left_list = ovf_left.as<uint32_t>();
     borrowed += out.nborrowed;
     if (!mover_overflow && !left) return false;
-    // Gpma::rebuild (gpma.hpp:119-122, :130-143) generalised: either the
-    // mover buffer overflowed (stale movers still sit in their old bins) or an
-    // arrival found no donor within the scan window.  Compact every held
-    // particle plus the unplaced arrivals and re-sort fully.
+    if (!mover_overflow) {
+        // Gpma::rebuild (gpma.hpp:119-122, :130-143): fresh slack from the true
+        // counts (cnt includes the unplaced arrivals), held particles keep their
+        // slot order, the unplaced arrivals follow them.
+        DevBuf& held = start;
+        held.ensure((nc + 1) * 4);
+        k_held<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt.as<uint32_t>(), off.as<uint32_t>(), (uint32_t)nc,
+                                                               held.as<uint32_t>());
+        note_launch();
+        k_caps_from_cnt<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt.as<uint32_t>(), (uint32_t)nc,
+                                                                        caps.as<uint32_t>(), onepg, min_gap);
+        note_launch();
+        layout_from_counts(n);
+        B.ensure(capacity_next);
+        mflag.ensure(capacity_next + 1);
+        PICGPU_CUDA_TRY(cudaMemsetAsync(B.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
+        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                               B.soa(), off2.as<uint32_t>(), (uint32_t)nc);
+        note_launch();
+        k_place_left<<<div_up(left, 256), 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), ovf_left.as<uint32_t>(), left,
+                                                        B.soa(), off2.as<uint32_t>(), held.as<uint32_t>());
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+        swap_soa(A, B);
+        swap_buf(off, off2);
+        capacity = capacity_next;
+        ++rebuilds;
+        return true;
+    }
+    // Mover-buffer overflow: stale movers still sit in their old bins.
+    // Compact every held particle plus the unplaced arrivals and re-sort fully.
     compact_to_B();
     unsigned int h32 = 0;
     PICGPU_CUDA_TRY(cudaMemcpyAsync(&h32, off2.as<uint32_t>() + nc, 4, cudaMemcpyDeviceToHost, st));
@@ -771,7 +829,7 @@ bool BinStore::finish_incremental(StepCounters& out) {
     }
     full_sort_from_B((uint64_t)h32 + left);
     ++rebuilds;
-    if (mover_overflow) ensure_movers(out.nmovers + out.nmovers / 2);
+    ensure_movers(out.nmovers + out.nmovers / 2);
     return true;
 }
 

@@ -5,7 +5,8 @@
 // store, the bins here hold the particle data itself (7 FP64 arrays + id): the
 // deposition kernels then read particles cell-locally and coalesced straight
 // from HBM.  Bin c owns slots [off[c], off[c+1]); its cnt[c] particles are
-// packed at the head, the slack at the tail.  Capacities follow the
+// packed at the head, the slack at the tail; every slack slot's x holds an
+// all-ones sentinel so the push can stream over raw slots.  Capacities follow the
 // reference's layout rule exactly, ceil(count*(1+gap_ratio)) + min_gap
 // (gpma.hpp:274-281), so capacity and empty_slot_ratio match the reference.
 #pragma once
@@ -46,7 +47,7 @@ struct StepCounters {
     unsigned int noverflow;   // arrivals that found no slack in their own bin
     int err;                  // picgpu_status of the first device-side error
     unsigned int nborrowed;   // ... placed by borrowing a following bin's slack
-    unsigned int nleft;       // ... with no donor (-> full re-sort)
+    unsigned int nleft;       // ... with no donor (-> rebuild)
     unsigned int pad;
 };
 
@@ -67,6 +68,7 @@ struct BinStore {
     SoaBuf M;                 // mover records
     DevBuf mcell, ovf, ovf_left;  // mover target cell, overflow list, unplaced overflow
     DevBuf locks;             // per-bin try-locks of the borrow kernel (always released)
+    DevBuf dep;               // per-bin departure counts (reset by k_compact)
     DevBuf counters;          // StepCounters
     StepCounters* hcounters = nullptr;  // pinned mirror
 
