@@ -1,0 +1,281 @@
+// picgpu.hpp -- C++20 mirror of the reference's `pic::` hot-path interface,
+// implemented on the C ABI of picgpu.h (link with -lpicgpu).
+//
+// Same names, argument meaning, value semantics and exception types as the
+// reference headers (paths under proj/include/pic/), so a call site switches
+// from `pic::` to `picgpu::` without other changes:
+//   GridSpec, CellIndex, cell_of                 grid.hpp:16-113
+//   ParticleSoA                                  particles.hpp:14-47
+//   ShapeOrder (+ tsc, this project's order 2)   shape.hpp:14
+//   CurrentGrid                                  grid.hpp:127-150
+//   deposit_scalar, deposit_density              deposit.hpp:62-83
+//   advance                                      workload.hpp:139-155
+//   GpmaConfig, gpma_build (perm + bins)         gpma.hpp:22-26, :379-402
+//   SortPolicy, RankSortStats, SortReason,
+//   should_global_sort, reset_counters           sort_policy.hpp:12-79
+//   Session: device-resident store + step loop   simulation.hpp:753-829
+// Status codes map back onto the reference's exceptions: EINVAL ->
+// std::invalid_argument, ERANGE -> std::out_of_range, ELENGTH ->
+// std::length_error, ELOGIC -> std::logic_error, EDOMAIN -> std::domain_error,
+// ECUDA / ENCCL -> std::runtime_error, ENOMEM -> std::bad_alloc.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <new>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "picgpu.h"
+
+namespace picgpu {
+
+inline void check(int rc) {
+    if (rc == PICGPU_OK) return;
+    const std::string msg = picgpu_last_error();
+    switch (rc) {
+        case PICGPU_EINVAL: throw std::invalid_argument(msg);
+        case PICGPU_ERANGE: throw std::out_of_range(msg);
+        case PICGPU_ELENGTH: throw std::length_error(msg);
+        case PICGPU_ELOGIC: throw std::logic_error(msg);
+        case PICGPU_EDOMAIN: throw std::domain_error(msg);
+        case PICGPU_ENOMEM: throw std::bad_alloc();
+        default: throw std::runtime_error(msg);
+    }
+}
+
+using Vec3 = std::array<double, 3>;
+
+struct CellIndex {
+    int i = 0, j = 0, k = 0;
+    std::uint32_t linear = 0;
+};
+
+struct GridSpec {
+    int nx = 1, ny = 1, nz = 1;
+    double dx = 1.0, dy = 1.0, dz = 1.0;
+    Vec3 origin{0.0, 0.0, 0.0};
+
+    void validate() const {
+        if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("grid: cell counts must be >= 1");
+        if (!(dx > 0.0) || !(dy > 0.0) || !(dz > 0.0)) throw std::invalid_argument("grid: cell sizes must be positive");
+    }
+    std::uint32_t n_cells() const {
+        return static_cast<std::uint32_t>(nx) * static_cast<std::uint32_t>(ny) * static_cast<std::uint32_t>(nz);
+    }
+    std::uint32_t n_nodes() const { return n_cells(); }
+    std::uint32_t linear_id(int i, int j, int k) const {
+        return static_cast<std::uint32_t>(i) +
+               static_cast<std::uint32_t>(nx) * (static_cast<std::uint32_t>(j) + static_cast<std::uint32_t>(ny) *
+                                                                                      static_cast<std::uint32_t>(k));
+    }
+    picgpu_grid c() const { return picgpu_grid{nx, ny, nz, 0, dx, dy, dz, origin[0], origin[1], origin[2]}; }
+};
+
+enum class ShapeOrder { cic = 1, tsc = 2, qsp = 3 };
+
+struct ParticleSoA {
+    std::vector<double> x, y, z;
+    std::vector<double> vx, vy, vz;
+    std::vector<double> w;
+    std::vector<std::uint64_t> id;
+    double q = 1.0;
+
+    std::size_t size() const { return x.size(); }
+    void resize(std::size_t n) {
+        x.resize(n); y.resize(n); z.resize(n);
+        vx.resize(n); vy.resize(n); vz.resize(n);
+        w.resize(n); id.resize(n);
+    }
+    Vec3 position(std::size_t i) const { return {x[i], y[i], z[i]}; }
+    void apply_permutation(std::span<const std::uint32_t> perm) {
+        if (perm.size() != size()) throw std::invalid_argument("apply_permutation: size mismatch");
+        auto permute = [&](auto& a) {
+            auto out = a;
+            for (std::size_t i = 0; i < perm.size(); ++i) out[i] = a[perm[i]];
+            a.swap(out);
+        };
+        permute(x); permute(y); permute(z);
+        permute(vx); permute(vy); permute(vz);
+        permute(w); permute(id);
+    }
+};
+
+struct CurrentGrid {
+    GridSpec spec;
+    std::vector<double> jx, jy, jz;
+    CurrentGrid() = default;
+    explicit CurrentGrid(const GridSpec& g) : spec(g), jx(g.n_nodes(), 0.0), jy(g.n_nodes(), 0.0), jz(g.n_nodes(), 0.0) {}
+    std::vector<double>& component(int c) { return c == 0 ? jx : c == 1 ? jy : jz; }
+    const std::vector<double>& component(int c) const { return c == 0 ? jx : c == 1 ? jy : jz; }
+    std::array<double, 3> component_sums() const {
+        std::array<double, 3> s{0.0, 0.0, 0.0};
+        for (int c = 0; c < 3; ++c)
+            for (double v : component(c)) s[c] += v;
+        return s;
+    }
+};
+
+inline CellIndex cell_of(const Vec3& p, const GridSpec& g) {
+    const picgpu_grid cg = g.c();
+    std::uint32_t lin = 0;
+    check(picgpu_cell_of(&cg, &p[0], &p[1], &p[2], 1, &lin));
+    CellIndex c;
+    c.linear = lin;
+    c.i = static_cast<int>(lin % static_cast<std::uint32_t>(g.nx));
+    c.j = static_cast<int>((lin / static_cast<std::uint32_t>(g.nx)) % static_cast<std::uint32_t>(g.ny));
+    c.k = static_cast<int>(lin / (static_cast<std::uint32_t>(g.nx) * static_cast<std::uint32_t>(g.ny)));
+    return c;
+}
+
+// deposit.hpp:62-73.  (The reference's optional Gpma* only changes the
+// summation order; J is order-independent to 1e-12, so it is not needed.)
+inline CurrentGrid deposit_scalar(const ParticleSoA& soa, const GridSpec& g, ShapeOrder order) {
+    CurrentGrid grid(g);
+    const picgpu_grid cg = g.c();
+    check(picgpu_deposit_current(&cg, static_cast<int>(order), soa.x.data(), soa.y.data(), soa.z.data(),
+                                 soa.vx.data(), soa.vy.data(), soa.vz.data(), soa.w.data(), soa.q, soa.size(),
+                                 grid.jx.data(), grid.jy.data(), grid.jz.data()));
+    return grid;
+}
+
+// deposit.hpp:76-83: bit-identical to the reference (storage-order sum).
+inline std::vector<double> deposit_density(const ParticleSoA& soa, const GridSpec& g, ShapeOrder order,
+                                           std::span<const double> quantity) {
+    if (quantity.size() != soa.size()) throw std::invalid_argument("deposit_density: quantity length mismatch");
+    std::vector<double> rho(g.n_nodes(), 0.0);
+    const picgpu_grid cg = g.c();
+    check(picgpu_deposit_density(&cg, static_cast<int>(order), soa.x.data(), soa.y.data(), soa.z.data(),
+                                 quantity.data(), soa.size(), rho.data()));
+    return rho;
+}
+
+// workload.hpp:139-155: bit-identical push; returns the moved fraction.
+inline double advance(ParticleSoA& soa, double dt, const GridSpec& g) {
+    const std::size_t n = soa.size();
+    if (n == 0) return 0.0;
+    const picgpu_grid cg = g.c();
+    std::uint64_t moved = 0;
+    check(picgpu_advance(&cg, dt, soa.x.data(), soa.y.data(), soa.z.data(), soa.vx.data(), soa.vy.data(),
+                         soa.vz.data(), n, &moved));
+    return static_cast<double>(moved) / static_cast<double>(n);
+}
+
+struct GpmaConfig {
+    double gap_ratio = 0.25;
+    std::uint32_t min_gap = 2;
+    int borrow_scan_bins = 4;
+};
+
+// Result of gpma_build's stable counting sort (gpma.hpp:379-394).
+struct Bins {
+    std::vector<std::uint32_t> perm;    // new storage index -> old
+    std::vector<std::uint32_t> starts;  // packed bin starts (exclusive scan of counts)
+    std::vector<std::uint32_t> counts;
+};
+
+// gpma_build (gpma.hpp:379-402): physically reorders the store by cell with a
+// stable counting sort (bit-identical permutation) and returns the bins.
+inline Bins gpma_build(ParticleSoA& soa, const GridSpec& g, GpmaConfig = {}) {
+    Bins b;
+    b.perm.resize(soa.size());
+    b.starts.resize(g.n_cells());
+    b.counts.resize(g.n_cells());
+    const picgpu_grid cg = g.c();
+    check(picgpu_counting_sort(&cg, soa.x.data(), soa.y.data(), soa.z.data(), soa.size(), b.perm.data(),
+                               b.starts.data(), b.counts.data()));
+    soa.apply_permutation(b.perm);
+    return b;
+}
+
+struct SortPolicy {
+    std::uint32_t sort_interval = 50;
+    std::uint32_t min_sort_interval = 10;
+    std::uint32_t trigger_rebuild_count = 100;
+    double trigger_empty_ratio = 0.15;
+    double trigger_full_ratio = 0.85;
+    bool perf_enable = true;
+    double perf_degrad = 0.80;
+};
+
+struct RankSortStats {
+    std::uint32_t steps_since_sort = 0;
+    std::uint64_t cumulative_local_rebuilds = 0;
+    double empty_slot_ratio = 0.0;
+    double perf_metric = 0.0;
+    double baseline_perf = 0.0;
+    std::uint64_t total_inserts = 0;
+    std::uint64_t total_shifts = 0;
+};
+
+enum class SortReason { none, interval, rebuilds, slot_ratio, perf_degradation };
+
+inline SortReason should_global_sort(const RankSortStats& s, const SortPolicy& p) {
+    const picgpu_rank_sort_stats cs{s.steps_since_sort, 0, s.cumulative_local_rebuilds, s.empty_slot_ratio,
+                                    s.perf_metric, s.baseline_perf, s.total_inserts, s.total_shifts};
+    const picgpu_sort_policy cp{p.sort_interval, p.min_sort_interval, p.trigger_rebuild_count,
+                                static_cast<std::uint32_t>(p.perf_enable), p.trigger_empty_ratio,
+                                p.trigger_full_ratio, p.perf_degrad};
+    return static_cast<SortReason>(picgpu_should_global_sort(&cs, &cp));
+}
+
+inline void reset_counters(RankSortStats& s) {  // sort_policy.hpp:75-79
+    s.steps_since_sort = 0;
+    s.cumulative_local_rebuilds = 0;
+    s.baseline_perf = 0.0;
+}
+
+// Device-resident store in cell bins with slack + deposition fields: the
+// reference's step loop with the GPMA kept on the GPU.
+class Session {
+   public:
+    Session(const GridSpec& g, ShapeOrder order, GpmaConfig gc = {}, int device = 0, bool timing = false)
+        : grid_(g) {
+        const picgpu_grid cg = g.c();
+        const picgpu_session_config cfg{static_cast<int32_t>(order), device, gc.gap_ratio, gc.min_gap,
+                                        timing ? PICGPU_SESSION_TIMING : 0u};
+        check(picgpu_session_create(&cg, &cfg, &h_));
+    }
+    ~Session() { picgpu_session_destroy(h_); }
+    Session(const Session&) = delete;
+    Session& operator=(const Session&) = delete;
+
+    void upload(const ParticleSoA& s) {
+        check(picgpu_session_upload(h_, s.size(), s.x.data(), s.y.data(), s.z.data(), s.vx.data(), s.vy.data(),
+                                    s.vz.data(), s.w.data(), s.id.empty() ? nullptr : s.id.data(), s.q));
+    }
+    picgpu_step_stats step(double dt, std::uint32_t flags = PICGPU_STEP_DEFAULT) {
+        picgpu_step_stats st{};
+        check(picgpu_session_step(h_, dt, flags, &st));
+        return st;
+    }
+    void global_sort() { check(picgpu_session_global_sort(h_)); }
+    CurrentGrid current() const {
+        CurrentGrid g(grid_);
+        check(picgpu_session_download_current(h_, g.jx.data(), g.jy.data(), g.jz.data()));
+        return g;
+    }
+    std::vector<double> density() const {
+        std::vector<double> r(grid_.n_nodes());
+        check(picgpu_session_download_density(h_, r.data()));
+        return r;
+    }
+    ParticleSoA particles() const {
+        ParticleSoA s;
+        s.resize(picgpu_session_num_particles(h_));
+        check(picgpu_session_download_particles(h_, s.x.data(), s.y.data(), s.z.data(), s.vx.data(), s.vy.data(),
+                                                s.vz.data(), s.w.data(), s.id.data()));
+        return s;
+    }
+    std::size_t capacity() const { return picgpu_session_capacity(h_); }
+    picgpu_session* handle() const { return h_; }
+
+   private:
+    GridSpec grid_;
+    picgpu_session* h_ = nullptr;
+};
+
+}  // namespace picgpu

@@ -1,0 +1,211 @@
+// dropin_parity.cpp -- TEST INFRASTRUCTURE: the reference's own C++ calls and
+// the picgpu drop-in (include/picgpu.hpp) on identical inputs, side by side.
+//
+// Built by oracle/Makefile (only where /root/reference exists; the binary in
+// oracle/_ref/ travels to the GPU box) from the UNMODIFIED reference headers
+// plus picgpu.hpp, linked against paper_2601_08277_b200/libpicgpu.so.  Each
+// block below is the same call site written once against `pic::` and once
+// against `picgpu::`; the program exits non-zero on any parity failure.
+//   positions after advance, rho, full-sort permutation: bit-identical
+//   J: <= 1e-12 peak-normalised (proj/tests/test_pipeline.cpp:27-40 metric)
+#include <pic/deposit.hpp>
+#include <pic/gpma.hpp>
+#include <pic/rng.hpp>
+#include <pic/sort_policy.hpp>
+#include <pic/workload.hpp>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <set>
+
+#include "picgpu.hpp"
+
+namespace {
+
+int failures = 0;
+
+void expect(bool ok, const char* what) {
+    std::printf("%-58s %s\n", what, ok ? "ok" : "FAIL");
+    if (!ok) ++failures;
+}
+
+template <class A, class B>
+double peak_rel_err(const A& got, const B& want) {
+    double err = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        double peak = 0.0;
+        for (double v : want.component(c)) peak = std::max(peak, std::abs(v));
+        for (std::size_t i = 0; i < want.component(c).size(); ++i) {
+            const double d = std::abs(got.component(c)[i] - want.component(c)[i]);
+            if (d == 0.0) continue;
+            if (peak == 0.0) return INFINITY;
+            err = std::max(err, d / peak);
+        }
+    }
+    return err;
+}
+
+// SURVEY 8(d) plasma on the reference counter RNG.
+pic::ParticleSoA plasma(const pic::GridSpec& g, int ppc, double u_th, std::uint64_t seed) {
+    pic::ParticleSoA s;
+    s.resize(static_cast<std::size_t>(g.n_cells()) * ppc);
+    s.q = -1.0;
+    std::size_t pid = 0;
+    for (int k = 0; k < g.nz; ++k)
+        for (int j = 0; j < g.ny; ++j)
+            for (int i = 0; i < g.nx; ++i)
+                for (int p = 0; p < ppc; ++p, ++pid) {
+                    s.x[pid] = g.origin[0] + (i + pic::uniform01(seed, pid, 6)) * g.dx;
+                    s.y[pid] = g.origin[1] + (j + pic::uniform01(seed, pid, 7)) * g.dy;
+                    s.z[pid] = g.origin[2] + (k + pic::uniform01(seed, pid, 8)) * g.dz;
+                    const double ux = u_th * pic::gaussian(seed, pid, 0), uy = u_th * pic::gaussian(seed, pid, 1),
+                                 uz = u_th * pic::gaussian(seed, pid, 2);
+                    const double gam = std::sqrt(1.0 + ux * ux + uy * uy + uz * uz);
+                    s.vx[pid] = ux / gam; s.vy[pid] = uy / gam; s.vz[pid] = uz / gam;
+                    s.w[pid] = 1.0 / ppc;
+                    s.id[pid] = pid;
+                }
+    return s;
+}
+
+picgpu::ParticleSoA to_gpu(const pic::ParticleSoA& s) {
+    picgpu::ParticleSoA o;
+    o.x = s.x; o.y = s.y; o.z = s.z; o.vx = s.vx; o.vy = s.vy; o.vz = s.vz; o.w = s.w; o.id = s.id; o.q = s.q;
+    return o;
+}
+
+}  // namespace
+
+int main() {
+    pic::GridSpec g;
+    g.nx = 12; g.ny = 10; g.nz = 9;
+    g.dx = 1.0; g.dy = 0.5; g.dz = 1.0;
+    g.origin = {-2.0, 1.0, 0.5};
+    picgpu::GridSpec gg;
+    gg.nx = g.nx; gg.ny = g.ny; gg.nz = g.nz;
+    gg.dx = g.dx; gg.dy = g.dy; gg.dz = g.dz;
+    gg.origin = g.origin;
+
+    pic::ParticleSoA ref = plasma(g, 6, 0.15, 3);
+    picgpu::ParticleSoA gpu = to_gpu(ref);
+    const double dt = 0.5;
+
+    // --- advance (workload.hpp:139) ---
+    for (int s = 0; s < 3; ++s) {
+        const double fr = pic::advance(ref, dt, g);
+        const double fg = picgpu::advance(gpu, dt, gg);
+        expect(fr == fg, "advance: moved fraction identical");
+    }
+    expect(ref.x == gpu.x && ref.y == gpu.y && ref.z == gpu.z, "advance: positions bit-identical");
+
+    // --- deposit_scalar (deposit.hpp:62) at orders 1 and 3 ---
+    for (auto [po, go] : {std::pair{pic::ShapeOrder::cic, picgpu::ShapeOrder::cic},
+                          std::pair{pic::ShapeOrder::qsp, picgpu::ShapeOrder::qsp}}) {
+        const pic::CurrentGrid jr = pic::deposit_scalar(ref, g, po);
+        const picgpu::CurrentGrid jg = picgpu::deposit_scalar(gpu, gg, go);
+        char msg[96];
+        const double e = peak_rel_err(jg, jr);
+        std::snprintf(msg, sizeof msg, "deposit_scalar order %d: J err %.2e <= 1e-12", static_cast<int>(po), e);
+        expect(e <= 1e-12, msg);
+    }
+
+    // --- deposit_density (deposit.hpp:76): storage order, bit-identical ---
+    std::vector<double> charge(ref.size());
+    for (std::size_t p = 0; p < ref.size(); ++p) charge[p] = ref.q * ref.w[p];
+    for (auto [po, go] : {std::pair{pic::ShapeOrder::cic, picgpu::ShapeOrder::cic},
+                          std::pair{pic::ShapeOrder::qsp, picgpu::ShapeOrder::qsp}}) {
+        const auto rr = pic::deposit_density(ref, g, po, charge);
+        const auto rg = picgpu::deposit_density(gpu, gg, go, charge);
+        expect(rr.size() == rg.size() && std::memcmp(rr.data(), rg.data(), rr.size() * 8) == 0,
+               "deposit_density: rho bit-identical (unsorted store)");
+    }
+
+    // --- gpma_build (gpma.hpp:379): same stable permutation of the store ---
+    pic::Gpma gpma = pic::gpma_build(ref, g);
+    const picgpu::Bins bins = picgpu::gpma_build(gpu, gg);
+    expect(ref.id == gpu.id && ref.x == gpu.x, "gpma_build: store permuted identically");
+    {
+        const auto rr = pic::deposit_density(ref, g, pic::ShapeOrder::qsp, charge);  // charge is uniform per species
+        const auto rg = picgpu::deposit_density(gpu, gg, picgpu::ShapeOrder::qsp, charge);
+        expect(std::memcmp(rr.data(), rg.data(), rr.size() * 8) == 0, "deposit_density: rho bit-identical (sorted store)");
+    }
+    bool counts_ok = true;
+    for (std::uint32_t c = 0; c < g.n_cells(); ++c) counts_ok &= gpma.bin_length(c) == bins.counts[c];
+    expect(counts_ok, "gpma_build: per-cell counts identical");
+
+    // --- incremental sort: bins as sets after push + detect/apply ---
+    {
+        picgpu::GpmaConfig gc;
+        picgpu::Session sess(gg, picgpu::ShapeOrder::qsp, gc);
+        sess.upload(gpu);
+        expect(sess.capacity() == gpma.capacity(), "session capacity == Gpma capacity (layout rule)");
+        for (int s = 0; s < 4; ++s) {
+            pic::advance(ref, dt, g);
+            auto pending = gpma.detect_moves(ref, g);
+            pic::apply_pending_moves(gpma, pending);
+            sess.step(dt, PICGPU_STEP_PUSH | PICGPU_STEP_SORT | PICGPU_STEP_CURRENT);
+        }
+        const picgpu::ParticleSoA got = sess.particles();
+        std::map<std::uint64_t, std::uint32_t> want_bin, got_bin;
+        for (std::uint32_t c = 0; c < g.n_cells(); ++c)
+            gpma.for_each_in_cell(c, [&](pic::ParticleRef p) { want_bin[ref.id[p]] = c; });
+        bool pos_ok = true;
+        std::map<std::uint64_t, std::size_t> slot;
+        for (std::size_t p = 0; p < ref.size(); ++p) slot[ref.id[p]] = p;
+        for (std::size_t p = 0; p < got.size(); ++p) {
+            got_bin[got.id[p]] = pic::cell_of(got.position(p), g).linear;
+            const std::size_t r = slot[got.id[p]];
+            pos_ok &= got.x[p] == ref.x[r] && got.y[p] == ref.y[r] && got.z[p] == ref.z[r];
+        }
+        expect(pos_ok, "session: positions bit-identical to pic::advance");
+        expect(want_bin == got_bin, "session: bin sets == reference Gpma bins");
+        const pic::CurrentGrid jr = pic::deposit_scalar(ref, g, pic::ShapeOrder::qsp, &gpma);
+        expect(peak_rel_err(sess.current(), jr) <= 1e-12, "session: J (bin order) within 1e-12");
+    }
+
+    // --- should_global_sort (sort_policy.hpp:62) ---
+    {
+        bool ok = true;
+        for (std::uint32_t steps : {5u, 10u, 20u, 50u, 200u})
+            for (std::uint64_t rb : {0ull, 100ull, 101ull})
+                for (double ratio : {0.1, 0.5, 0.9})
+                    for (double perf : {79.9, 80.1}) {
+                        pic::RankSortStats rs;
+                        rs.steps_since_sort = steps; rs.cumulative_local_rebuilds = rb;
+                        rs.empty_slot_ratio = ratio; rs.perf_metric = perf; rs.baseline_perf = 100.0;
+                        picgpu::RankSortStats gs;
+                        gs.steps_since_sort = steps; gs.cumulative_local_rebuilds = rb;
+                        gs.empty_slot_ratio = ratio; gs.perf_metric = perf; gs.baseline_perf = 100.0;
+                        ok &= static_cast<int>(pic::should_global_sort(rs, {})) ==
+                              static_cast<int>(picgpu::should_global_sort(gs, {}));
+                    }
+        expect(ok, "should_global_sort: identical decisions");
+    }
+
+    // --- error behaviour: the same exception types ---
+    {
+        picgpu::ParticleSoA bad = gpu;
+        bad.x[0] = NAN;
+        bool got_invalid = false;
+        try {
+            picgpu::deposit_scalar(bad, gg, picgpu::ShapeOrder::cic);
+        } catch (const std::invalid_argument&) {
+            got_invalid = true;
+        }
+        expect(got_invalid, "non-finite position -> std::invalid_argument");
+        picgpu::ParticleSoA fast = gpu;
+        fast.vx[0] = 10.0;
+        bool got_domain = false;
+        try {
+            picgpu::advance(fast, dt, gg);
+        } catch (const std::domain_error&) {
+            got_domain = true;
+        }
+        expect(got_domain, "displacement above the cap -> std::domain_error");
+    }
+
+    std::printf("%s (%d failures)\n", failures ? "DROP-IN PARITY FAILED" : "drop-in parity ok", failures);
+    return failures ? 1 : 0;
+}

@@ -48,7 +48,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
             if verbose:
                 sys.stderr.write(r.stderr)
     if force or _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+        # static CUDA runtime: the .so has no libcudart dependency to resolve on the box
+        cmd = [NVCC] + ARCH + ["-shared", "--cudart", "static", "-o", LIB] + objs
         subprocess.check_call(cmd)
     return LIB
 

@@ -85,3 +85,11 @@ def test_compute_fails_loudly_without_gpu(pg):
     s = {k: np.zeros(3) + 0.5 for k in ("x", "y", "z", "vx", "vy", "vz", "w")}
     with pytest.raises(pg.PicError):
         pg.deposit_scalar(s, g, 1)
+
+
+def test_cpp_shim_compiles():
+    """include/picgpu.hpp (the pic:: mirror) is self-contained C++20."""
+    r = subprocess.run(["g++", "-std=gnu++20", "-fsyntax-only", "-x", "c++", "-I", os.path.join(ROOT, "include"), "-"],
+                       input='#include "picgpu.hpp"\nint main() { picgpu::GridSpec g; g.validate(); return 0; }\n',
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
