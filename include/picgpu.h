@@ -140,7 +140,6 @@ typedef struct picgpu_session_config {
 } picgpu_session_config;
 
 #define PICGPU_SESSION_TIMING 1u        /* record CUDA events around each phase */
-#define PICGPU_SESSION_DETERMINISTIC 2u /* canonical in-bin order of arrivals (sorted by id) */
 
 /* per-step flags */
 #define PICGPU_STEP_PUSH 1u       /* advance (bit-exact pic::advance) */
