@@ -54,13 +54,23 @@ struct JCfg<1> {
 #ifndef PICGPU_LANE_MINB
 #define PICGPU_LANE_MINB 3
 #endif
+#ifndef PICGPU_LANE_PX
+#define PICGPU_LANE_PX 8
+#endif
+#ifndef PICGPU_LANE_UNROLL
+#define PICGPU_LANE_UNROLL 1
+#endif
+constexpr int kLaneUnroll = PICGPU_LANE_UNROLL;
+#ifndef PICGPU_LANE_PY
+#define PICGPU_LANE_PY 4
+#endif
 template <>
 struct JCfg<2> {
-    static constexpr int G = 4, PX = 8, PY = 4, MINB = PICGPU_LANE_MINB, CH = 4;
+    static constexpr int G = 4, PX = PICGPU_LANE_PX, PY = PICGPU_LANE_PY, MINB = PICGPU_LANE_MINB, CH = 4;
 };
 template <>
 struct JCfg<3> {
-    static constexpr int G = 4, PX = 8, PY = 4, MINB = PICGPU_LANE_MINB, CH = 4;
+    static constexpr int G = 4, PX = PICGPU_LANE_PX, PY = PICGPU_LANE_PY, MINB = PICGPU_LANE_MINB, CH = 4;
 };
 
 template <int ORDER>
@@ -170,6 +180,52 @@ __device__ __forceinline__ void particle_window_fast(const GridD& g, const PData
     }
 }
 
+// Fractional coordinate of a binned particle relative to its bin's cell
+// index `ci` (one FMA-free sub/mul per axis instead of floor/convert/branches).
+// Exact when the spacing is a power of two; otherwise within an ulp, which
+// only perturbs J at the 1e-16 level.  A position that is not inside its bin's
+// cell (periodic image after an upload of unwrapped positions) takes the exact
+// locate_axis path.
+__device__ __forceinline__ double frac_in_cell(double x, double origin, double spacing, double inv, int pow2, int n,
+                                               int ci) {
+    const double u = (x - origin) * inv;
+    const double f = u - (double)ci;
+    if (f >= -0.5 && f <= 1.5) return f;
+    double fr;
+    locate_axis(x, origin, spacing, inv, pow2, n, fr);
+    return fr;
+}
+
+// J prologue for a particle binned in cell (ci, cj, ck): window weights with
+// FMA polynomials and x-weights pre-multiplied by wq_c = (q*W)*v_c.
+template <int ORDER>
+__device__ __forceinline__ void particle_window_cell(const GridD& g, const PData& d, double q, int ci, int cj, int ck,
+                                                     double (&a)[3][Shape<ORDER>::W], double (&sy)[Shape<ORDER>::W],
+                                                     double (&sz)[Shape<ORDER>::W]) {
+    constexpr int W = Shape<ORDER>::W;
+    const double qw = q * d.w;
+    const double wq0 = qw * d.vx, wq1 = qw * d.vy, wq2 = qw * d.vz;
+    const double fx = frac_in_cell(d.x, g.ox, g.dx, g.inv_dx, g.pow2x, g.nx, ci);
+    const double fy = frac_in_cell(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, cj);
+    const double fz = frac_in_cell(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, ck);
+    double sx[W];
+    if constexpr (ORDER == 1) {
+        sx[0] = 1.0 - fx; sx[1] = fx;
+        sy[0] = 1.0 - fy; sy[1] = fy;
+        sz[0] = 1.0 - fz; sz[1] = fz;
+    } else {
+        weights_fast<ORDER>(fx, sx);
+        weights_fast<ORDER>(fy, sy);
+        weights_fast<ORDER>(fz, sz);
+    }
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+        a[0][t] = wq0 * sx[t];
+        a[1][t] = wq1 * sx[t];
+        a[2][t] = wq2 * sx[t];
+    }
+}
+
 template <int W, int NJ>
 __device__ __forceinline__ void accumulate(double (&acc)[W][NJ][W][3], const double (&a)[3][W], const double (&syv)[NJ],
                                            const double (&sz)[W]) {
@@ -251,7 +307,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                     PData d;
                     load_particle(p, c_off + t, d);
                     double a[3][W], sy[W], sz[W];
-                    particle_window<ORDER>(g, d, q, a, sy, sz);
+                    particle_window_cell<ORDER>(g, d, q, i, j, k, a, sy, sz);
                     double syv[NJ];
 #pragma unroll
                     for (int jj = 0; jj < NJ; ++jj) syv[jj] = sy[jj];
@@ -273,7 +329,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                         }
                         double a[3][W], sy[W], sz[W];
                         if (valid) {
-                            particle_window<ORDER>(g, cur, q, a, sy, sz);
+                            particle_window_cell<ORDER>(g, cur, q, i, j, k, a, sy, sz);
                         } else {
 #pragma unroll
                             for (int t = 0; t < W; ++t) a[0][t] = a[1][t] = a[2][t] = sy[t] = sz[t] = 0.0;
@@ -291,7 +347,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                     }
                     __syncwarp();
                     const int nn = min(CH, m - base);
-#pragma unroll 1
+#pragma unroll kLaneUnroll
                     for (int jj0 = 0; jj0 < nn; ++jj0) {
                         const double* r = stage + jj0 * L::SS + grp;
                         double b[W][NJ];
