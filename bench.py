@@ -22,8 +22,10 @@ cpu_baseline: the reference's own step (oracle/_ref: advance + detect_moves +
          an independent 32^3 x 16 ppc sub-box (bounded sample).
 
 --impl reference runs only that CPU arm and prints its line.
-Multi-GPU (torchrun, N>1): each rank runs an independent C2 box (replicas,
-weak scaling); slab decomposition with guard exchange is not implemented yet.
+Multi-GPU (torchrun, N>1): x-slab decomposition of one periodic
+box of (128*N) x 128 x 128 cells; each rank owns a C2-sized slab (weak
+scaling) and every step exchanges leaving particles and J guard planes with its
+two ring neighbours over NCCL (paper_2601_08277_b200/slab.py).
 """
 from __future__ import annotations
 
@@ -152,7 +154,7 @@ def run_reference_arm(args, cfgname):
         "dtype": "f64", "data": "synthetic (SURVEY 8(d) generator, reference counter RNG)",
         "config": {"workload": desc + "; step = push + incremental sort + J deposit",
                    "grid": [nx] * 3, "ppc": ppc, "order": order, "particles_per_gpu": nx ** 3 * ppc,
-                   "parallelism": "single" if args.gpus == 1 else f"replicas x{args.gpus} (independent boxes)"},
+                   "parallelism": "single" if args.gpus == 1 else f"x-slabs x{args.gpus} (GPU arm); CPU: rank 0 only"},
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -180,6 +182,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--slab", action="store_true", help="use the slab-decomposed path even at N=1 (loopback ring)")
     args = ap.parse_args()
     nx, ppc, order, u_th, dt, default_steps, desc = CONFIGS[args.config]
     if args.steps is None:
@@ -209,13 +212,24 @@ def main():
         torch.cuda.synchronize()
 
     grid = pg.Grid.make(nx)
-    S = pg.Session(grid, order=order, device=local, timing=True)
-    S.generate_plasma(ppc, u_th, seed=1 + rank)
+    if world == 1 and not args.slab:
+        S = pg.Session(grid, order=order, device=local, timing=True)
+        step = lambda: S.step(dt)  # noqa: E731
+    else:
+        from paper_2601_08277_b200.slab import RingExchange, SlabSession, slab_step
+
+        G = pg.Grid.make(nx * world, nx, nx)
+        S = SlabSession(G, rank * nx, (rank + 1) * nx, order=order, device=local, timing=True)
+        ring = RingExchange()
+        step = lambda: slab_step(S, ring, dt)  # noqa: E731
+    S.generate_plasma(ppc, u_th, seed=1)
     n = S.num_particles
+    n_total = n * world  # conserved by the migration
     stream = torch.cuda.ExternalStream(S.stream)
     for _ in range(args.warmup):
-        S.step(dt)
-    S.global_sort()  # also exercises the relayout kernels before the timed region
+        step()
+    if world == 1 and not args.slab:
+        S.global_sort()  # also exercises the relayout kernels before the timed region
     S.reset_phase_times()
     barrier()
     launches0 = pg.kernel_launches()
@@ -226,7 +240,7 @@ def main():
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            st = S.step(dt)
+            st = step()
             moved += st["moved"]
             rebuilds += st["rebuilt"]
         e1.record(stream)
@@ -238,7 +252,7 @@ def main():
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = n * args.steps * world / (ms_max * 1e-3)
+    value = n_total * args.steps / (ms_max * 1e-3)
     phases = S.phase_times()
     j_ms, j_launches = phases["deposit_current"]
     j_avg_s = j_ms / max(j_launches, 1) * 1e-3
@@ -269,6 +283,7 @@ def main():
     e2e = None
     if rank == 0 or True:
         p = S.particles()
+        n = p.size()
         host = {}
         for k in ("x", "y", "z", "vx", "vy", "vz", "w"):
             tt = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -294,9 +309,11 @@ def main():
         barrier()
         e2e_s = time.perf_counter() - t0
         tt = torch.tensor([e2e_s], device="cuda")
+        ne = torch.tensor([float(n)], device="cuda", dtype=torch.float64)
         if dist is not None:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": n * args.e2e_steps * world / float(tt.item()), "unit": UNIT,
+            dist.all_reduce(ne)
+        e2e = {"value": float(ne.item()) * args.e2e_steps / float(tt.item()), "unit": UNIT,
                "h2d_bytes_per_step": 7 * 8 * n, "d2h_bytes_per_step": 3 * 8 * grid.ncells,
                "steps": args.e2e_steps, "api": "picgpu_deposit_current (drop-in for pic::deposit_scalar)",
                "timer": "host wall clock around synchronous C-ABI calls (copies inside)"}
@@ -320,9 +337,10 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY 8(d) seeded plasma generated in HBM; no dataset)",
             "config": {"workload": desc + "; step = push + incremental sort + J deposit",
-                       "grid": [nx] * 3, "ppc": ppc, "order": order, "particles_per_gpu": n,
+                       "grid": [nx * world, nx, nx], "ppc": ppc, "order": order, "particles_per_gpu": n,
                        "l2": f"inputs larger than L2 ({n * 64 / 1e9:.1f} GB particle store)",
-                       "parallelism": "single" if world == 1 else f"replicas x{world} (independent boxes)"},
+                       "parallelism": "single" if world == 1 else
+                       f"x-slabs x{world} of a {nx * world}x{nx}x{nx} box, NCCL ring exchange (migration + J guards)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
             "phases_ms_total": {k: v[0] for k, v in phases.items()},

@@ -197,6 +197,45 @@ PICGPU_API int picgpu_session_device_fields(picgpu_session* s, double** j, doubl
 PICGPU_API int picgpu_session_phase_times(picgpu_session* s, double* ms, uint64_t* launches, int nphases);
 PICGPU_API int picgpu_session_reset_phase_times(picgpu_session* s);
 
+/* ---- x-slab decomposition over ranks -----------------------
+ * The reference runs one process over the whole periodic box and tiles it
+ * across OpenMP threads (simulation.hpp:753-829, TileDecomposition
+ * SPEC.md:505-513).  Here each rank (one process per GPU) owns the global
+ * x-cells [x0, x1) of `global` and runs one session on its slab grid: the
+ * owned cells plus `ghost` (>= 2, the QSP stencil reach) guard cells on each
+ * side.  Positions stay in global coordinates and wrap on the global box, so
+ * every per-particle value is bit-identical to the undecomposed run.  A step
+ * is split around two neighbour exchanges (done by the caller, e.g. NCCL
+ * send/recv between ranks r-1, r, r+1 on the periodic ring):
+ *   step_begin        push + move detection; particles that left the slab are
+ *                     packed as 8-double records (x y z vx vy vz w id-bits)
+ *   copy_leavers      -> caller's device buffers, sent to the left / right rank
+ *   step_end          arrivals (records from both neighbours) inserted like
+ *                     movers, then J / rho deposited on the slab grid
+ *   guard_planes      planes [0,ghost) -> left rank, [ghost+own, own+2*ghost) -> right
+ *   add_guard_planes  the left rank's high planes add into [ghost, 2*ghost),
+ *                     the right rank's low planes into [own, own+ghost)
+ * Device pointers passed in must be complete (synchronised) when the call is
+ * made; outputs are complete when it returns. */
+/* The slab grid of [x0, x1) with `ghost` guard cells per side. */
+PICGPU_API int picgpu_slab_grid(const picgpu_grid* global, int x0, int x1, int ghost, picgpu_grid* local);
+/* Turns an empty session created on picgpu_slab_grid(global, x0, x1, ghost)
+ * into a slab session.  Upload / generate_plasma then take only owned particles
+ * (generate_plasma produces the global generator's particles of the owned cells,
+ * global ids). */
+PICGPU_API int picgpu_session_set_slab(picgpu_session* s, const picgpu_grid* global, int x0, int x1, int ghost);
+/* flags as for picgpu_session_step (SORT required; GLOBAL_SORT / NO_SYNC ignored). */
+PICGPU_API int picgpu_session_step_begin(picgpu_session* s, double dt, uint32_t flags, uint64_t* n_to_left,
+                                         uint64_t* n_to_right);
+PICGPU_API int picgpu_session_copy_leavers(picgpu_session* s, double* to_left, double* to_right);
+PICGPU_API int picgpu_session_step_end(picgpu_session* s, const double* arrivals, uint64_t n_arrivals,
+                                       picgpu_step_stats* out);
+/* field 0: J (3 components), 1: rho.  Each buffer holds comps*ghost*nz*ny
+ * doubles laid out [comp][plane][z][y]. */
+PICGPU_API int picgpu_session_guard_planes(picgpu_session* s, int field, double* lo, double* hi);
+PICGPU_API int picgpu_session_add_guard_planes(picgpu_session* s, int field, const double* from_left,
+                                               const double* from_right);
+
 /* ---- microbenchmarks (roofline denominators measured in-run) ------------ */
 /* Runs a dependent-free DFMA loop on all SMs; returns measured FP64 TFLOP/s. */
 PICGPU_API int picgpu_fp64_peak(int device, double* tflops);

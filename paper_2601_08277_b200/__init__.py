@@ -12,6 +12,7 @@ and argument meaning follow the reference headers under proj/include/pic/:
     cell_of(pos, grid)                          grid.hpp:106-113
     should_global_sort(stats, policy)           sort_policy.hpp:62-73
     Session                                     run_simulation's step loop on a device-resident Gpma
+    slab.SlabSession                            the same loop on one x-slab per rank (multi-GPU)
 
 Errors raise the Python analogue of the reference's exception type.  The
 product path has no CPU fallback: importing works anywhere, but every compute
@@ -190,6 +191,13 @@ def lib():
     L.picgpu_session_phase_times.argtypes = [_P, _P, _P, C.c_int]
     L.picgpu_session_reset_phase_times.argtypes = [_P]
     L.picgpu_fp64_peak.argtypes = [C.c_int, C.POINTER(_D)]
+    L.picgpu_slab_grid.argtypes = [G, C.c_int, C.c_int, C.c_int, G]
+    L.picgpu_session_set_slab.argtypes = [_P, G, C.c_int, C.c_int, C.c_int]
+    L.picgpu_session_step_begin.argtypes = [_P, _D, C.c_uint32, C.POINTER(_U64), C.POINTER(_U64)]
+    L.picgpu_session_copy_leavers.argtypes = [_P, _P, _P]
+    L.picgpu_session_step_end.argtypes = [_P, _P, _U64, C.POINTER(StepStats)]
+    L.picgpu_session_guard_planes.argtypes = [_P, C.c_int, _P, _P]
+    L.picgpu_session_add_guard_planes.argtypes = [_P, C.c_int, _P, _P]
     _lib = L
     return L
 

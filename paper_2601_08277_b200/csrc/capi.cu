@@ -64,6 +64,15 @@ GridD make_grid(const picgpu_grid& h) {
     g.pow2Lx = is_pow2(g.Lx); g.pow2Ly = is_pow2(g.Ly); g.pow2Lz = is_pow2(g.Lz);
     g.inv_Lx = 1.0 / g.Lx; g.inv_Ly = 1.0 / g.Ly; g.inv_Lz = 1.0 / g.Lz;
     g.ncells = (uint32_t)nc;
+    g.slab = 0;
+    g.gnx = g.nx;
+    g.sx_shift = 0;
+    g.sx_lo = 0;
+    g.sx_hi = g.nx;
+    g.gox = g.ox;
+    g.gLx = g.Lx;
+    g.ginv_Lx = g.inv_Lx;
+    g.gpow2Lx = g.pow2Lx;
     return g;
 }
 
@@ -154,6 +163,15 @@ struct picgpu_session {
     cudaEvent_t ev[8] = {};
     double phase_ms[PICGPU_NPHASES] = {};
     uint64_t phase_launches[PICGPU_NPHASES] = {};
+    // x-slab decomposition (picgpu_session_set_slab)
+    bool slab = false;
+    int ghost = 0;
+    int own = 0;
+    bool pending = false;      // between step_begin and step_end
+    uint32_t pending_flags = 0;
+    uint64_t nleave[2] = {0, 0};
+    StepCounters cbegin{};
+    uint64_t begin_launches = 0;
 };
 
 static void set_device(const picgpu_session* s) { PICGPU_CUDA_TRY(cudaSetDevice(s->device)); }
@@ -447,7 +465,7 @@ int picgpu_session_generate_plasma(picgpu_session* s, int ppc, double u_th, uint
         set_device(s);
         if (ppc < 1) throw Status{PICGPU_EINVAL, "workload: ppc must be >= 1"};
         BinStore& bs = s->store;
-        const uint64_t n = (uint64_t)bs.g.ncells * (uint64_t)ppc;
+        const uint64_t n = (uint64_t)(bs.g.sx_hi - bs.g.sx_lo) * bs.g.ny * bs.g.nz * (uint64_t)ppc;
         bs.B.ensure(n);
         launch_generate_plasma(bs.g, ppc, u_th, seed, bs.B.soa(), s->st);
         bs.full_sort_from_B(n);
@@ -504,6 +522,7 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
         set_device(s);
         BinStore& bs = s->store;
         const cudaStream_t st = s->st;
+        if (s->slab) throw Status{PICGPU_ELOGIC, "session_step: slab sessions step with step_begin / step_end"};
         if ((flags & PICGPU_STEP_PUSH) && !(flags & PICGPU_STEP_SORT))
             throw Status{PICGPU_EINVAL, "session_step: PUSH requires SORT (push and move detection are fused)"};
         if ((flags & PICGPU_STEP_DENSITY)) check_density_grid(bs.hg, s->order);
@@ -649,6 +668,194 @@ int picgpu_session_reset_phase_times(picgpu_session* s) {
         s->phase_launches[i] = 0;
     }
     return PICGPU_OK;
+}
+
+// ---- x-slab decomposition ---------------------------------------------------
+
+static void slab_grid(const picgpu_grid* G, int x0, int x1, int ghost, picgpu_grid* L) {
+    make_grid(*G);
+    if (!(0 <= x0 && x0 < x1 && x1 <= G->nx)) throw Status{PICGPU_EINVAL, "slab: need 0 <= x0 < x1 <= nx"};
+    if (ghost < 2) throw Status{PICGPU_EINVAL, "slab: ghost must be >= 2 (QSP stencil reach)"};
+    if (x1 - x0 < ghost) throw Status{PICGPU_EINVAL, "slab: a slab must own at least `ghost` x-cells"};
+    *L = *G;
+    L->nx = x1 - x0 + 2 * ghost;
+    L->ox = G->ox + (double)(x0 - ghost) * G->dx;
+}
+
+int picgpu_slab_grid(const picgpu_grid* G, int x0, int x1, int ghost, picgpu_grid* L) {
+    return guard([&] { slab_grid(G, x0, x1, ghost, L); });
+}
+
+int picgpu_session_set_slab(picgpu_session* s, const picgpu_grid* G, int x0, int x1, int ghost) {
+    return guard([&] {
+        BinStore& bs = s->store;
+        if (bs.n || bs.capacity) throw Status{PICGPU_ELOGIC, "set_slab: the session must be empty"};
+        picgpu_grid L{};
+        slab_grid(G, x0, x1, ghost, &L);
+        const picgpu_grid& h = bs.hg;
+        if (h.nx != L.nx || h.ny != L.ny || h.nz != L.nz || h.dx != L.dx || h.dy != L.dy || h.dz != L.dz ||
+            h.ox != L.ox || h.oy != L.oy || h.oz != L.oz)
+            throw Status{PICGPU_EINVAL, "set_slab: session grid is not picgpu_slab_grid(global, x0, x1, ghost)"};
+        GridD& g = bs.g;
+        g.slab = 1;
+        g.gnx = G->nx;
+        g.sx_shift = x0 - ghost;
+        g.sx_lo = ghost;
+        g.sx_hi = ghost + (x1 - x0);
+        g.gox = G->ox;
+        g.gLx = G->nx * G->dx;
+        g.ginv_Lx = 1.0 / g.gLx;
+        g.gpow2Lx = is_pow2(g.gLx);
+        s->slab = true;
+        s->ghost = ghost;
+        s->own = x1 - x0;
+    });
+}
+
+static void throw_step_error(int err) {
+    if (err == PICGPU_EDOMAIN) throw Status{err, "advance: particle displacement exceeds the single-cell cap"};
+    if (err == PICGPU_ELENGTH) throw Status{err, "slab: leaver exchange buffer overflow"};
+    throw Status{err, "cell_of: non-finite particle position (or arrival outside the slab)"};
+}
+
+int picgpu_session_step_begin(picgpu_session* s, double dt, uint32_t flags, uint64_t* n_to_left,
+                              uint64_t* n_to_right) {
+    return guard([&] {
+        set_device(s);
+        BinStore& bs = s->store;
+        if (s->pending) throw Status{PICGPU_ELOGIC, "step_begin: previous step not ended"};
+        if (!(flags & PICGPU_STEP_SORT)) throw Status{PICGPU_EINVAL, "step_begin: SORT is required"};
+        if (flags & PICGPU_STEP_DENSITY) check_density_grid(bs.hg, s->order);
+        const double cap2 = (flags & PICGPU_STEP_PUSH) ? cap2_of(bs.hg, dt) : 0.0;
+        const uint64_t l0 = g_launches.load();
+        if (s->timing) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], s->st));
+        bs.enqueue_detect((flags & PICGPU_STEP_PUSH) != 0, dt, cap2);
+        if (s->timing) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], s->st));
+        PICGPU_CUDA_TRY(
+            cudaMemcpyAsync(bs.hcounters, bs.counters.p, sizeof(StepCounters), cudaMemcpyDeviceToHost, s->st));
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+        const StepCounters c = *bs.hcounters;
+        if (c.err) throw_step_error(c.err);
+        if (s->timing) accumulate_phase(s, 0, 0, 1, g_launches.load() - l0);
+        s->cbegin = c;
+        s->nleave[0] = c.nleave[0];
+        s->nleave[1] = c.nleave[1];
+        s->pending = true;
+        s->pending_flags = flags;
+        if (n_to_left) *n_to_left = c.nleave[0];
+        if (n_to_right) *n_to_right = c.nleave[1];
+    });
+}
+
+int picgpu_session_copy_leavers(picgpu_session* s, double* to_left, double* to_right) {
+    return guard([&] {
+        set_device(s);
+        if (!s->pending) throw Status{PICGPU_ELOGIC, "copy_leavers: no step in progress"};
+        BinStore& bs = s->store;
+        const double* L = bs.lrec.as<double>();
+        if (s->nleave[0])
+            PICGPU_CUDA_TRY(cudaMemcpyAsync(to_left, L, s->nleave[0] * 64, cudaMemcpyDeviceToDevice, s->st));
+        if (s->nleave[1])
+            PICGPU_CUDA_TRY(
+                cudaMemcpyAsync(to_right, L + bs.lcap * 8, s->nleave[1] * 64, cudaMemcpyDeviceToDevice, s->st));
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
+}
+
+int picgpu_session_step_end(picgpu_session* s, const double* arrivals, uint64_t n_arr, picgpu_step_stats* out) {
+    return guard([&] {
+        set_device(s);
+        if (!s->pending) throw Status{PICGPU_ELOGIC, "step_end: no step in progress"};
+        s->pending = false;
+        BinStore& bs = s->store;
+        const cudaStream_t st = s->st;
+        const uint32_t flags = s->pending_flags;
+        const bool T = s->timing;
+        const uint64_t rebuilds0 = bs.rebuilds;
+        const StepCounters& cb = s->cbegin;
+        const uint64_t l0 = g_launches.load();
+        if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
+        const size_t base = std::min<size_t>(cb.nmovers, bs.mcap);
+        if (cb.nmovers > bs.mcap) bs.movers_dropped = true;
+        if (n_arr) {
+            if (n_arr >= 0xffffffffull) throw Status{PICGPU_ELENGTH, "slab: too many arrivals"};
+            bs.ensure_movers_keep(base + n_arr + (base + n_arr) / 4, base);
+            bs.enqueue_import(arrivals, (uint32_t)n_arr, (uint32_t)base);
+        }
+        bs.n = bs.n - s->nleave[0] - s->nleave[1] + n_arr;
+        bs.enqueue_migrate();
+        if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
+        const uint64_t lm = g_launches.load() - l0;
+        StepCounters c{};
+        const bool rebuilt = bs.finish_incremental(c);  // host waits here
+        if (c.err) throw_step_error(c.err);
+        picgpu_step_stats stats{};
+        stats.moved = cb.moved;
+        stats.inserts = base + n_arr;
+        stats.overflowed = c.noverflow;
+        if (T) {
+            accumulate_phase(s, 0, 0, 1, lm);
+            if (rebuilt) {
+                PICGPU_CUDA_TRY(cudaEventRecord(s->ev[7], st));
+                PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[7]));
+                accumulate_phase(s, 2, 1, 7, g_launches.load() - l0 - lm);
+            }
+        }
+        uint64_t lj = 0, lr = 0;
+        enqueue_deposits(s, flags, &lj, &lr);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+        if (T) {
+            if (flags & PICGPU_STEP_CURRENT) {
+                accumulate_phase(s, 5, 2, 3, 0);
+                accumulate_phase(s, 3, 3, 4, lj);
+            }
+            if (flags & PICGPU_STEP_DENSITY) accumulate_phase(s, 4, 5, 6, lr);
+        }
+        stats.rebuilt = bs.rebuilds != rebuilds0;
+        stats.capacity = bs.capacity;
+        stats.num_particles = bs.n;
+        stats.empty_slot_ratio = bs.capacity ? (double)(bs.capacity - bs.n) / (double)bs.capacity : 1.0;
+        if (out) *out = stats;
+    });
+}
+
+static double* slab_field(picgpu_session* s, int field, int& comps) {
+    if (!s->slab) throw Status{PICGPU_ELOGIC, "guard planes: not a slab session"};
+    if (field == 0) {
+        comps = 3;
+        return s->J.as<double>();
+    }
+    if (field == 1) {
+        if (!s->rho.p) throw Status{PICGPU_ELOGIC, "guard planes: no density deposited yet"};
+        comps = 1;
+        return s->rho.as<double>();
+    }
+    throw Status{PICGPU_EINVAL, "guard planes: field must be 0 (J) or 1 (rho)"};
+}
+
+int picgpu_session_guard_planes(picgpu_session* s, int field, double* lo, double* hi) {
+    return guard([&] {
+        set_device(s);
+        int comps = 0;
+        double* F = slab_field(s, field, comps);
+        const GridD& g = s->store.g;
+        launch_pack_planes(F, comps, g.nx, g.ny, g.nz, 0, s->ghost, lo, s->st);
+        launch_pack_planes(F, comps, g.nx, g.ny, g.nz, s->ghost + s->own, s->ghost, hi, s->st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
+}
+
+int picgpu_session_add_guard_planes(picgpu_session* s, int field, const double* from_left,
+                                    const double* from_right) {
+    return guard([&] {
+        set_device(s);
+        int comps = 0;
+        double* F = slab_field(s, field, comps);
+        const GridD& g = s->store.g;
+        launch_add_planes(F, comps, g.nx, g.ny, g.nz, s->ghost, s->ghost, from_left, s->st);
+        launch_add_planes(F, comps, g.nx, g.ny, g.nz, s->own, s->ghost, from_right, s->st);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
 }
 
 }  // extern "C"

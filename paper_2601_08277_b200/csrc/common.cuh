@@ -25,7 +25,21 @@ struct GridD {
     double inv_Lx, inv_Ly, inv_Lz;
     int pow2Lx, pow2Ly, pow2Lz;  // same for the box lengths (wrap_position)
     uint32_t ncells;
+    // x-slab of a box decomposed over ranks; the identity for a
+    // whole box.  x is always located on the GLOBAL axis (origin gox, gnx
+    // cells, periodic length gLx) and shifted by sx_shift into the slab's
+    // ghost-extended local grid, so every per-particle quantity (cell,
+    // fraction, weights, wrapped position) is bit-identical to the
+    // undecomposed run.  The slab owns local x-cells [sx_lo, sx_hi).
+    int slab;
+    int gnx, sx_shift, sx_lo, sx_hi;
+    double gox, gLx, ginv_Lx;
+    int gpow2Lx;
 };
+
+// Store-cell codes of particles that left a slab (push / import routing).
+constexpr uint32_t kLeaveLeft = 0xFFFFFFFEu;
+constexpr uint32_t kLeaveRight = 0xFFFFFFFDu;
 
 GridD make_grid(const picgpu_grid& g);
 
@@ -79,10 +93,15 @@ __device__ __forceinline__ bool finite3(double x, double y, double z) {
     return isfinite(x) && isfinite(y) && isfinite(z);
 }
 
+// Local x-cell of a position (global locate, then the slab shift).
+__device__ __forceinline__ int locate_x(const GridD& g, double x, double& frac) {
+    return locate_axis(x, g.gox, g.dx, g.inv_dx, g.pow2x, g.gnx, frac) - g.sx_shift;
+}
+
 // cell_of, grid.hpp:106-113 (caller checks finiteness).
 __device__ __forceinline__ uint32_t cell_linear(const GridD& g, double x, double y, double z, int& i, int& j,
                                                 int& k, double& fx, double& fy, double& fz) {
-    i = locate_axis(x, g.ox, g.dx, g.inv_dx, g.pow2x, g.nx, fx);
+    i = locate_x(g, x, fx);
     j = locate_axis(y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, fy);
     k = locate_axis(z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, fz);
     return (uint32_t)i + (uint32_t)g.nx * ((uint32_t)j + (uint32_t)g.ny * (uint32_t)k);
@@ -92,6 +111,19 @@ __device__ __forceinline__ uint32_t cell_linear(const GridD& g, double x, double
     int i, j, k;
     double fx, fy, fz;
     return cell_linear(g, x, y, z, i, j, k, fx, fy, fz);
+}
+
+// Bin of a particle in a session store: its cell, or kLeaveLeft/kLeaveRight
+// when a slab does not own it (the nearer neighbour on the periodic x-axis).
+__device__ __forceinline__ uint32_t store_cell(const GridD& g, double x, double y, double z) {
+    int i, j, k;
+    double fx, fy, fz;
+    const uint32_t c = cell_linear(g, x, y, z, i, j, k, fx, fy, fz);
+    if (!g.slab || (i >= g.sx_lo && i < g.sx_hi)) return c;
+    const int ig = i + g.sx_shift, x0 = g.sx_lo + g.sx_shift, x1 = g.sx_hi + g.sx_shift;
+    const int dl = ((x0 - ig) % g.gnx + g.gnx) % g.gnx;
+    const int dr = ((ig - x1 + 1) % g.gnx + g.gnx) % g.gnx;
+    return dl <= dr ? kLeaveLeft : kLeaveRight;
 }
 
 // Shape weights in a fixed window of W taps starting at node cell + OFF.

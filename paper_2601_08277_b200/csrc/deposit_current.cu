@@ -121,7 +121,7 @@ __device__ __forceinline__ void particle_window(const GridD& g, const PData& d, 
     const double wq0 = qw * d.vx, wq1 = qw * d.vy, wq2 = qw * d.vz;
     double fx, fy, fz;
     int up;
-    locate_axis(d.x, g.ox, g.dx, g.inv_dx, g.pow2x, g.nx, fx);
+    locate_x(g, d.x, fx);
     locate_axis(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, fy);
     locate_axis(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, fz);
     double sx[W];
@@ -165,7 +165,7 @@ __device__ __forceinline__ void particle_window_fast(const GridD& g, const PData
     const double qw = q * d.w;
     const double wq0 = qw * d.vx, wq1 = qw * d.vy, wq2 = qw * d.vz;
     double fx, fy, fz;
-    locate_axis(d.x, g.ox, g.dx, g.inv_dx, g.pow2x, g.nx, fx);
+    locate_x(g, d.x, fx);
     locate_axis(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, fy);
     locate_axis(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, fz);
     double sx[4];
@@ -205,7 +205,7 @@ __device__ __forceinline__ void particle_window_cell(const GridD& g, const PData
     constexpr int W = Shape<ORDER>::W;
     const double qw = q * d.w;
     const double wq0 = qw * d.vx, wq1 = qw * d.vy, wq2 = qw * d.vz;
-    const double fx = frac_in_cell(d.x, g.ox, g.dx, g.inv_dx, g.pow2x, g.nx, ci);
+    const double fx = frac_in_cell(d.x, g.gox, g.dx, g.inv_dx, g.pow2x, g.gnx, ci + g.sx_shift);
     const double fy = frac_in_cell(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, cj);
     const double fz = frac_in_cell(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, ck);
     double sx[W];

@@ -33,7 +33,7 @@ __global__ void density_prologue(const GridD g, const CSoa p, const double* __re
     if (s >= slots) return;
     const double x = p.x[s], y = p.y[s], z = p.z[s];
     double f[3];
-    locate_axis(x, g.ox, g.dx, g.inv_dx, g.pow2x, g.nx, f[0]);
+    locate_x(g, x, f[0]);
     locate_axis(y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
     locate_axis(z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
     int bits = 0;

@@ -100,7 +100,7 @@ __device__ __forceinline__ bool push_one(const GridD& g, double dt, double cap2,
                                          double vx, double vy, double vz) {
     const double v2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
     if (v2 > cap2) return false;
-    x = wrap_position(__dadd_rn(x, __dmul_rn(vx, dt)), g.ox, g.Lx, g.inv_Lx, g.pow2Lx);
+    x = wrap_position(__dadd_rn(x, __dmul_rn(vx, dt)), g.gox, g.gLx, g.ginv_Lx, g.gpow2Lx);
     y = wrap_position(__dadd_rn(y, __dmul_rn(vy, dt)), g.oy, g.Ly, g.inv_Ly, g.pow2Ly);
     z = wrap_position(__dadd_rn(z, __dmul_rn(vz, dt)), g.oz, g.Lz, g.inv_Lz, g.pow2Lz);
     return true;
@@ -132,7 +132,13 @@ __global__ void k_cells(const GridD g, const double* __restrict__ x, const doubl
         cell[p] = 0;
         return;
     }
-    cell[p] = cell_linear(g, px, py, pz);
+    const uint32_t c = store_cell(g, px, py, pz);
+    if (c >= kLeaveRight) {  // not owned by this slab
+        raise_error(err, PICGPU_EINVAL);
+        cell[p] = 0;
+        return;
+    }
+    cell[p] = c;
 }
 
 __global__ void k_iota(uint32_t* v, uint64_t n) {
@@ -237,7 +243,8 @@ __device__ __forceinline__ bool is_gap(double x) { return __double_as_longlong(x
 template <bool PUSH, int UNR>
 __global__ void __launch_bounds__(256) k_push(const GridD g, const Soa A, uint64_t slots, uint8_t* __restrict__ mflag,
                                               double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
-                                              uint32_t mcap, uint32_t* __restrict__ dep, StepCounters* ctr) {
+                                              uint32_t mcap, uint32_t* __restrict__ dep, StepCounters* ctr,
+                                              double* __restrict__ L, uint32_t lcap) {
     __shared__ unsigned s_cnt, s_base;
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
@@ -272,7 +279,7 @@ __global__ void __launch_bounds__(256) k_push(const GridD g, const Soa A, uint64
         if (!ok) {
             raise_error(&ctr->err, PICGPU_EINVAL);
         } else {
-            before[u] = cell_linear(g, x[u], y[u], z[u]);
+            before[u] = store_cell(g, x[u], y[u], z[u]);
             if (PUSH) {
                 if (!push_one(g, dt, cap2, x[u], y[u], z[u], vx[u], vy[u], vz[u])) {
                     raise_error(&ctr->err, PICGPU_EDOMAIN);
@@ -288,14 +295,30 @@ __global__ void __launch_bounds__(256) k_push(const GridD g, const Soa A, uint64
                 }
             }
             if (ok) {
-                nc[u] = cell_linear(g, x[u], y[u], z[u]);
+                nc[u] = store_cell(g, x[u], y[u], z[u]);
                 moved = nc[u] != before[u];
             }
         }
         mflag[s] = moved ? 1 : 0;
         if (moved) {
-            lidx[u] = (int)atomicAdd(&s_cnt, 1u);
             ++local_moved;
+            if (nc[u] >= kLeaveRight) {  // left the slab: exchange record for the neighbour rank
+                const int dir = nc[u] == kLeaveLeft ? 0 : 1;
+                const unsigned li = atomicAdd(&ctr->nleave[dir], 1u);
+                if (li < lcap) {
+                    double* r = L + ((size_t)dir * lcap + li) * 8;
+                    r[0] = x[u]; r[1] = y[u]; r[2] = z[u];
+                    r[3] = vx[u]; r[4] = vy[u]; r[5] = vz[u];
+                    r[6] = A.w[s];
+                    r[7] = __longlong_as_double((long long)A.id[s]);
+                    atomicAdd(&dep[before[u]], 1u);
+                } else {
+                    raise_error(&ctr->err, PICGPU_ELENGTH);
+                    mflag[s] = 0;
+                }
+            } else {
+                lidx[u] = (int)atomicAdd(&s_cnt, 1u);
+            }
         }
     }
     __syncthreads();
@@ -380,7 +403,7 @@ __global__ void __launch_bounds__(256) k_compact(const Soa A, const uint32_t* __
 __global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32_t mcap,
                          StepCounters* ctr, const Soa A, const uint32_t* __restrict__ off, uint32_t* cnt,
                          uint32_t* __restrict__ ovf) {
-    const uint32_t nm = min(ctr->nmovers, mcap);
+    const uint32_t nm = min(ctr->nmovers, mcap) + ctr->nimport;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
         const uint32_t d = mcell[i];
         const uint32_t pos = atomicAdd(&cnt[d], 1u);
@@ -476,6 +499,71 @@ __global__ void k_append_overflow(const Soa M, const uint32_t* __restrict__ ovf,
     if (o < novf) copy_particle(M, ovf[o], dst, base + o);
 }
 
+// Arrivals from the neighbour slabs (8-double records: x y z vx vy vz w id)
+// appended to the mover list after this rank's own movers; k_insert and
+// k_borrow then place them like any mover.
+__global__ void k_import(const GridD g, const double* __restrict__ rec, uint32_t n, uint32_t base, const Soa M,
+                         uint32_t* __restrict__ mcell, StepCounters* ctr) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        ctr->nimport = n;
+        ctr->nmovers = base;  // own movers beyond the old capacity stay in their bins (flag 2)
+    }
+    if (i >= n) return;
+    const double* r = rec + (size_t)i * 8;
+    const double x = r[0], y = r[1], z = r[2];
+    uint32_t c = 0;
+    if (!finite3(x, y, z)) {
+        raise_error(&ctr->err, PICGPU_EINVAL);
+    } else {
+        c = store_cell(g, x, y, z);
+        if (c >= kLeaveRight) {  // routed to the wrong slab
+            raise_error(&ctr->err, PICGPU_EINVAL);
+            c = 0;
+        }
+    }
+    const uint32_t d = base + i;
+    M.x[d] = x; M.y[d] = y; M.z[d] = z;
+    M.vx[d] = r[3]; M.vy[d] = r[4]; M.vz[d] = r[5];
+    M.w[d] = r[6];
+    M.id[d] = (uint64_t)__double_as_longlong(r[7]);
+    mcell[d] = c;
+}
+
+// Guard planes of a slab's field (comps arrays of nx*ny*nz, x fastest):
+// planes [p0, p0+np) packed as [comp][plane][z][y].
+__global__ void k_pack_planes(const double* __restrict__ F, int comps, int nx, int ny, int nz, int p0, int np,
+                              double* __restrict__ out) {
+    const uint64_t total = (uint64_t)comps * np * ny * nz;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const int p = (int)(t % np);
+        uint64_t r = t / np;
+        const int j = (int)(r % ny);
+        r /= ny;
+        const int k = (int)(r % nz);
+        const int c = (int)(r / nz);
+        const size_t src = (size_t)c * nx * ny * nz + ((size_t)k * ny + j) * nx + p0 + p;
+        out[(((size_t)c * np + p) * nz + k) * ny + j] = F[src];
+    }
+}
+
+__global__ void k_add_planes(double* __restrict__ F, int comps, int nx, int ny, int nz, int p0, int np,
+                             const double* __restrict__ in) {
+    const uint64_t total = (uint64_t)comps * np * ny * nz;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const int p = (int)(t % np);
+        uint64_t r = t / np;
+        const int j = (int)(r % ny);
+        r /= ny;
+        const int k = (int)(r % nz);
+        const int c = (int)(r / nz);
+        const size_t dst = (size_t)c * nx * ny * nz + ((size_t)k * ny + j) * nx + p0 + p;
+        F[dst] += in[(((size_t)c * np + p) * nz + k) * ny + j];
+    }
+}
+
 __global__ void k_advance(const GridD g, double dt, double cap2, double* __restrict__ x, double* __restrict__ y,
                           double* __restrict__ z, const double* __restrict__ vx, const double* __restrict__ vy,
                           const double* __restrict__ vz, uint64_t n, unsigned long long* moved, int* err) {
@@ -522,25 +610,29 @@ __device__ __forceinline__ double gaussian(uint64_t seed, uint64_t stream, uint6
     return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
 }
 
+// The generator of the whole box restricted to the owned x-cells: particle
+// ids (and hence every hashed draw) are the global ones.
 __global__ void k_generate(const GridD g, int ppc, double u_th, uint64_t seed, const Soa out, uint64_t n) {
-    const uint64_t pid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pid >= n) return;
-    const uint64_t lin = pid / (uint64_t)ppc;
-    const int i = (int)(lin % (uint64_t)g.nx);
-    const int j = (int)((lin / (uint64_t)g.nx) % (uint64_t)g.ny);
-    const int k = (int)(lin / ((uint64_t)g.nx * (uint64_t)g.ny));
-    out.x[pid] = __dadd_rn(g.ox, __dmul_rn(__dadd_rn((double)i, uniform01(seed, pid, 6)), g.dx));
-    out.y[pid] = __dadd_rn(g.oy, __dmul_rn(__dadd_rn((double)j, uniform01(seed, pid, 7)), g.dy));
-    out.z[pid] = __dadd_rn(g.oz, __dmul_rn(__dadd_rn((double)k, uniform01(seed, pid, 8)), g.dz));
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const uint64_t lin = p / (uint64_t)ppc;
+    const uint64_t own = (uint64_t)(g.sx_hi - g.sx_lo);
+    const int i = (int)(lin % own) + g.sx_lo + g.sx_shift;  // global x-cell
+    const int j = (int)((lin / own) % (uint64_t)g.ny);
+    const int k = (int)(lin / (own * (uint64_t)g.ny));
+    const uint64_t pid = (((uint64_t)k * g.ny + j) * g.gnx + i) * (uint64_t)ppc + p % (uint64_t)ppc;
+    out.x[p] = __dadd_rn(g.gox, __dmul_rn(__dadd_rn((double)i, uniform01(seed, pid, 6)), g.dx));
+    out.y[p] = __dadd_rn(g.oy, __dmul_rn(__dadd_rn((double)j, uniform01(seed, pid, 7)), g.dy));
+    out.z[p] = __dadd_rn(g.oz, __dmul_rn(__dadd_rn((double)k, uniform01(seed, pid, 8)), g.dz));
     const double ux = u_th * gaussian(seed, pid, 0);
     const double uy = u_th * gaussian(seed, pid, 1);
     const double uz = u_th * gaussian(seed, pid, 2);
     const double gam = sqrt(1.0 + ux * ux + uy * uy + uz * uz);
-    out.vx[pid] = ux / gam;
-    out.vy[pid] = uy / gam;
-    out.vz[pid] = uz / gam;
-    out.w[pid] = 1.0 / (double)ppc;
-    out.id[pid] = pid;
+    out.vx[p] = ux / gam;
+    out.vy[p] = uy / gam;
+    out.vz[p] = uz / gam;
+    out.w[p] = 1.0 / (double)ppc;
+    out.id[p] = pid;
 }
 
 // ---------------------------------------------------------------------------
@@ -564,9 +656,29 @@ void launch_advance(const GridD& g, double dt, double cap2, double* x, double* y
 }
 
 void launch_generate_plasma(const GridD& g, int ppc, double u_th, uint64_t seed, Soa out, cudaStream_t st) {
-    const uint64_t n = (uint64_t)g.ncells * (uint64_t)ppc;
+    const uint64_t n = (uint64_t)(g.sx_hi - g.sx_lo) * g.ny * g.nz * (uint64_t)ppc;
     if (!n) return;
     k_generate<<<div_up((long long)n, 256), 256, 0, st>>>(g, ppc, u_th, seed, out, n);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_pack_planes(const double* F, int comps, int nx, int ny, int nz, int p0, int np, double* out,
+                        cudaStream_t st) {
+    const long long total = (long long)comps * np * ny * nz;
+    if (!total) return;
+    k_pack_planes<<<(int)std::min<long long>(div_up(total, 256), 148 * 8), 256, 0, st>>>(F, comps, nx, ny, nz, p0, np,
+                                                                                        out);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_add_planes(double* F, int comps, int nx, int ny, int nz, int p0, int np, const double* in,
+                       cudaStream_t st) {
+    const long long total = (long long)comps * np * ny * nz;
+    if (!total) return;
+    k_add_planes<<<(int)std::min<long long>(div_up(total, 256), 148 * 8), 256, 0, st>>>(F, comps, nx, ny, nz, p0, np,
+                                                                                       in);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
@@ -670,7 +782,9 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev) {
     PICGPU_CUDA_TRY(cudaGetLastError());
     PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, ctr, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
     layout_from_counts(np);  // synchronises
-    if (hcounters->err) throw Status{hcounters->err, "cell_of: non-finite particle position"};
+    if (hcounters->err)
+        throw Status{hcounters->err, g.slab ? "slab: particle outside the slab's owned cells (or non-finite)"
+                                            : "cell_of: non-finite particle position"};
     A.ensure(capacity_next);
     mflag.ensure(capacity_next + 1);
     PICGPU_CUDA_TRY(cudaMemsetAsync(A.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
@@ -743,9 +857,35 @@ void BinStore::ensure_movers(size_t m) {
     mcap = m;
 }
 
-void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
+void BinStore::ensure_movers_keep(size_t m, size_t keep) {
+    if (m <= mcap) return;
+    SoaBuf M2;
+    DevBuf mcell2;
+    M2.ensure(m);
+    mcell2.ensure(m * 4);
+    if (keep) {
+        for (int a = 0; a < 8; ++a)
+            PICGPU_CUDA_TRY(cudaMemcpyAsync(M2.a[a].p, M.a[a].p, keep * 8, cudaMemcpyDeviceToDevice, st));
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(mcell2.p, mcell.p, keep * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    swap_soa(M, M2);
+    swap_buf(mcell, mcell2);
+    ovf.ensure(m * 4);
+    ovf_left.ensure(m * 4);
+    mcap = m;
+}
+
+void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     const size_t nc = g.ncells;
     ensure_movers(std::max<size_t>(size_t(1) << 16, n / 4));
+    if (g.slab) {
+        const size_t want = std::max<size_t>(size_t(1) << 16, n / 4);
+        if (want > lcap) {
+            lrec.ensure(want * 2 * 8 * sizeof(double));
+            lcap = want;
+        }
+    }
     StepCounters* ctr = counters.as<StepCounters>();
     PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
     if (!nc || !n) return;
@@ -753,27 +893,52 @@ void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
     const int blocks = (int)((capacity + 256 * UNR - 1) / (256 * UNR));
     if (push)
         k_push<true, UNR><<<blocks, 256, 0, st>>>(g, A.soa(), capacity, mflag.as<uint8_t>(), dt, cap2, M.soa(),
-                                                  mcell.as<uint32_t>(), (uint32_t)mcap, dep.as<uint32_t>(), ctr);
+                                                  mcell.as<uint32_t>(), (uint32_t)mcap, dep.as<uint32_t>(), ctr,
+                                                  lrec.as<double>(), (uint32_t)lcap);
     else
         k_push<false, UNR><<<blocks, 256, 0, st>>>(g, A.soa(), capacity, mflag.as<uint8_t>(), dt, cap2, M.soa(),
-                                                   mcell.as<uint32_t>(), (uint32_t)mcap, dep.as<uint32_t>(), ctr);
+                                                   mcell.as<uint32_t>(), (uint32_t)mcap, dep.as<uint32_t>(), ctr,
+                                                   lrec.as<double>(), (uint32_t)lcap);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
     k_compact<<<div_up((long long)nc, 256), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
                                                           mflag.as<uint8_t>(), dep.as<uint32_t>(), (uint32_t)nc);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
-    k_insert<<<num_sms * 4, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap, ctr, A.soa(),
-                                          off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>());
+}
+
+void BinStore::enqueue_import(const double* rec_dev, uint32_t nimp, uint32_t base) {
+    k_import<<<div_up((long long)std::max<uint32_t>(nimp, 1u), 256), 256, 0, st>>>(
+        g, rec_dev, nimp, base, M.soa(), mcell.as<uint32_t>(), counters.as<StepCounters>());
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
-    // borrow_insert for the full-bin arrivals; no work when there are none
-    k_borrow<<<num_sms, 128, 0, st>>>(ctr, M.soa(), mcell.as<uint32_t>(), ovf.as<uint32_t>(), ovf_left.as<uint32_t>(),
-                                      A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(), locks.as<unsigned int>(),
-                                      (uint32_t)nc, kBorrowScanBins);
-    note_launch();
-    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+void BinStore::enqueue_migrate() {
+    const size_t nc = g.ncells;
+    StepCounters* ctr = counters.as<StepCounters>();
+    if (nc) {
+        k_insert<<<num_sms * 4, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap, ctr, A.soa(),
+                                              off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>());
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+        // borrow_insert for the full-bin arrivals; no work when there are none
+        k_borrow<<<num_sms, 128, 0, st>>>(ctr, M.soa(), mcell.as<uint32_t>(), ovf.as<uint32_t>(),
+                                          ovf_left.as<uint32_t>(), A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                          locks.as<unsigned int>(), (uint32_t)nc, kBorrowScanBins);
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+    }
     PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, ctr, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
+}
+
+void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
+    enqueue_detect(push, dt, cap2);
+    if (!g.ncells || !n) {
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, counters.p, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
+        return;
+    }
+    enqueue_migrate();
 }
 
 bool BinStore::finish_incremental(StepCounters& out) {
@@ -781,7 +946,9 @@ bool BinStore::finish_incremental(StepCounters& out) {
     PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
     out = *hcounters;
     if (out.err) return false;
-    const bool mover_overflow = out.nmovers > mcap;
+    const bool mover_overflow = out.nmovers > mcap || movers_dropped;
+    const uint32_t nmovers_seen = movers_dropped ? (uint32_t)std::max<size_t>(mcap, out.nmovers) : out.nmovers;
+    movers_dropped = false;
     // unplaced arrivals (no donor found); borrowed ones already sit in their bins
     const uint32_t left = out.nleft;
     const uint32_t* left_list = ovf_left.as<uint32_t>();
@@ -829,7 +996,7 @@ bool BinStore::finish_incremental(StepCounters& out) {
     }
     full_sort_from_B((uint64_t)h32 + left);
     ++rebuilds;
-    ensure_movers(out.nmovers + out.nmovers / 2);
+    ensure_movers(nmovers_seen + nmovers_seen / 2);
     return true;
 }
 

@@ -48,7 +48,8 @@ struct StepCounters {
     int err;                  // picgpu_status of the first device-side error
     unsigned int nborrowed;   // ... placed by borrowing a following bin's slack
     unsigned int nleft;       // ... with no donor (-> rebuild)
-    unsigned int pad;
+    unsigned int nimport;     // arrivals from neighbour slabs appended to the movers
+    unsigned int nleave[2];   // particles that left the slab to the left / right
 };
 
 constexpr int kBorrowScanBins = 4;  // GpmaConfig::borrow_scan_bins (gpma.hpp:25)
@@ -75,6 +76,9 @@ struct BinStore {
     uint64_t n = 0;           // particles
     uint64_t capacity = 0;    // slots in use (off[ncells])
     size_t mcap = 0;          // mover record capacity
+    DevBuf lrec;              // slab leavers: [2][lcap][8] doubles (x y z vx vy vz w id)
+    size_t lcap = 0;
+    bool movers_dropped = false;  // a slab step dropped unrecorded movers (-> full re-sort)
     uint64_t rebuilds = 0;
     uint64_t borrowed = 0;    // arrivals placed by borrowing a neighbour's slack
 
@@ -94,6 +98,13 @@ struct BinStore {
     // (optional) + detect + in-bin compaction, migration into slack, borrow
     // from the following bins for full bins; counters copied to the host.
     void enqueue_incremental(bool push, double dt, double cap2);
+    // The same step in two halves around a slab exchange: detect (push +
+    // move detection + in-bin compaction; leavers go to the exchange buffer
+    // `lrec`), then migrate (optional arrivals appended to the movers,
+    // insert, borrow).
+    void enqueue_detect(bool push, double dt, double cap2);
+    void enqueue_import(const double* rec_dev, uint32_t n, uint32_t base);
+    void enqueue_migrate();
     // Synchronises, reads the counters and, if an arrival found no slack even
     // after borrowing (or the mover buffer overflowed), rebuilds by a full
     // re-sort.  Returns true when it rebuilt (fields deposited since the
@@ -103,8 +114,10 @@ struct BinStore {
     uint32_t* d_off() const { return off.as<uint32_t>(); }
     uint32_t* d_cnt() const { return cnt.as<uint32_t>(); }
 
-   private:
     void ensure_movers(size_t m);
+    void ensure_movers_keep(size_t m, size_t keep);  // grow, preserving the first `keep` records
+
+   private:
     void layout_from_counts(uint64_t total_particles);  // caps + scan -> off2; returns via capacity_next
     uint64_t capacity_next = 0;
 };

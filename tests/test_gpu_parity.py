@@ -349,3 +349,65 @@ def test_launch_counter_moves(pg, orc):
     s = orc.make_plasma(g, 2, 0.1, 1)
     pg.deposit_scalar(s, to_pg_grid(g), 3)
     assert pg.kernel_launches() > before
+
+
+def _hp_deposit(p, g, order, q):
+    """80-bit longdouble deposition (exact shape forms, shape.hpp:26-43 and the
+    TSC restatement in oracle/picoracle.c po_shape_1d) -- an accuracy yardstick
+    independent of summation order."""
+    L = np.longdouble
+    W = 2 if order == 1 else 4
+    off = 0 if order == 1 else -1
+
+    def shape(d):
+        if order == 1:
+            return [1 - d, d]
+        if order == 3:
+            u = 1 - d
+            return [u ** 3 / 6, (4 - 6 * d * d + 3 * d ** 3) / 6, (1 + 3 * d + 3 * d * d - 3 * d ** 3) / 6, d ** 3 / 6]
+        up = d >= L(0.5)
+        dl = np.where(up, d - 1, d)
+        a, b, m = L(0.5) * (L(0.5) - dl) ** 2, L(0.75) - dl * dl, L(0.5) * (L(0.5) + dl) ** 2
+        z = np.zeros_like(d)
+        return [np.where(up, z, a), np.where(up, a, b), np.where(up, b, m), np.where(up, m, z)]
+
+    dims = (g.nx, g.ny, g.nz)
+    org = (g.ox, g.oy, g.oz)
+    hs = (g.dx, g.dy, g.dz)
+    J = np.zeros((3, g.nz, g.ny, g.nx), dtype=L)
+    ci, S = [], []
+    for a, k in enumerate("xyz"):
+        u = (np.asarray(getattr(p, k), dtype=L) - L(org[a])) / L(hs[a])
+        c = np.floor(u)
+        S.append(shape(u - c))
+        ci.append(c.astype(np.int64))
+    wq = [L(q) * np.asarray(p.w, dtype=L) * np.asarray(getattr(p, v), dtype=L) for v in ("vx", "vy", "vz")]
+    for kz in range(W):
+        for jy in range(W):
+            for ix in range(W):
+                X = (ci[0] + off + ix) % dims[0]
+                Y = (ci[1] + off + jy) % dims[1]
+                Z = (ci[2] + off + kz) % dims[2]
+                s = S[0][ix] * S[1][jy] * S[2][kz]
+                for c in range(3):
+                    np.add.at(J[c], (Z, Y, X), wq[c] * s)
+    return J.reshape(3, -1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_session_current_vs_extended_precision(pg, order):
+    """The session's J after several push/sort steps of a hot plasma is within
+    a few ulps (peak-normalised) of an 80-bit deposit of the same particles:
+    the FMA weight polynomials and the register accumulation cost < 1e-14."""
+    g = pg.Grid.make(16, 8, 8, dx=0.5, dy=0.5, dz=0.5, origin=(-2.0, 0.0, 1.0))
+    S = pg.Session(g, order)
+    S.generate_plasma(4, 0.6, seed=7)
+    for _ in range(4):
+        S.step(0.5)
+    p = S.particles()
+    J = S.current()
+    hp = _hp_deposit(p, g, order, -1.0)
+    got = np.stack([J.jx, J.jy, J.jz]).astype(np.longdouble)
+    err = float(np.abs(got - hp).max() / np.abs(hp).max())
+    assert err < 1e-14, err
