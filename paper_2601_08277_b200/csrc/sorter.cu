@@ -96,13 +96,16 @@ __device__ __forceinline__ double wrap_position(double x, double origin, double 
 
 // One particle of pic::advance (workload.hpp:144-153); returns false on a cap
 // violation (the reference throws std::domain_error).
+// P2: every spacing and box length is a power of two (checked on the host),
+// so the divide-or-multiply choice folds away at compile time.
+template <bool P2 = false>
 __device__ __forceinline__ bool push_one(const GridD& g, double dt, double cap2, double& x, double& y, double& z,
                                          double vx, double vy, double vz) {
     const double v2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
     if (v2 > cap2) return false;
-    x = wrap_position(__dadd_rn(x, __dmul_rn(vx, dt)), g.gox, g.gLx, g.ginv_Lx, g.gpow2Lx);
-    y = wrap_position(__dadd_rn(y, __dmul_rn(vy, dt)), g.oy, g.Ly, g.inv_Ly, g.pow2Ly);
-    z = wrap_position(__dadd_rn(z, __dmul_rn(vz, dt)), g.oz, g.Lz, g.inv_Lz, g.pow2Lz);
+    x = wrap_position(__dadd_rn(x, __dmul_rn(vx, dt)), g.gox, g.gLx, g.ginv_Lx, P2 || g.gpow2Lx);
+    y = wrap_position(__dadd_rn(y, __dmul_rn(vy, dt)), g.oy, g.Ly, g.inv_Ly, P2 || g.pow2Ly);
+    z = wrap_position(__dadd_rn(z, __dmul_rn(vz, dt)), g.oz, g.Lz, g.inv_Lz, P2 || g.pow2Lz);
     return true;
 }
 
@@ -231,17 +234,41 @@ __global__ void __launch_bounds__(256) k_relayout(const Soa src, const uint32_t*
 // stream over raw slots without knowing the bin layout.
 __device__ __forceinline__ bool is_gap(double x) { return __double_as_longlong(x) == -1LL; }
 
+// floor((x - o) / h) exactly as locate_axis computes it (before its range
+// handling).  For u >= 0 the fraction u - floor(u) is exact and < 1, so equal
+// non-negative floors on every axis mean the same cell.
+__device__ __forceinline__ double axis_floor(double x, double o, double h, double inv, int pow2) {
+    const double t = __dsub_rn(x, o);
+    return floor(pow2 ? __dmul_rn(t, inv) : __ddiv_rn(t, h));
+}
+
 // Push (optional) + move detection (pic::advance + Gpma::detect_moves,
 // workload.hpp:139-155, gpma.hpp:162-177).  Each CTA streams one contiguous
-// chunk of UNR*256 slots; a thread issues all loads of its UNR slots up front.
+// chunk of UNR*256 slots.  Measured at C2 (tools/push_sweep.sh): one slot per
+// thread at 6 CTAs/SM with unconditional loads (0.83 ms, 4.0 TB/s) beats
+// loading only the valid slots' y..vz after x (PICGPU_PUSH_CONDLOAD=1), whose
+// second round trip costs more than the slack bytes it saves.  The cell test is exact and
+// cheap: a particle moves at most one cell, so when every axis' floor is
+// unchanged (and non-negative) its cell is unchanged; only otherwise are the
+// full cell ids of both positions computed (pic::cell_of).
 // A particle whose cell changed is flagged and appended to the mover list:
 // slots are numbered with a shared-memory atomic and the CTA reserves its
 // range with ONE global atomic (no per-warp atomic round trips on the hot
 // path); departures are counted per bin with fire-and-forget reductions.
 // Movers that do not fit the mover buffer stay in their (now stale) bin with
 // flag 2; the host then re-sorts fully.
-template <bool PUSH, int UNR>
-__global__ void __launch_bounds__(256) k_push(const GridD g, const Soa A, uint64_t slots, uint8_t* __restrict__ mflag,
+#ifndef PICGPU_PUSH_UNR
+#define PICGPU_PUSH_UNR 1
+#endif
+#ifndef PICGPU_PUSH_MINB
+#define PICGPU_PUSH_MINB 6
+#endif
+#ifndef PICGPU_PUSH_CONDLOAD
+#define PICGPU_PUSH_CONDLOAD 0
+#endif
+
+template <bool PUSH, int UNR, bool P2>
+__global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, const Soa A, uint64_t slots, uint8_t* __restrict__ mflag,
                                               double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
                                               uint32_t mcap, uint32_t* __restrict__ dep, StepCounters* ctr,
                                               double* __restrict__ L, uint32_t lcap) {
@@ -256,10 +283,13 @@ __global__ void __launch_bounds__(256) k_push(const GridD g, const Soa A, uint64
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
         const uint64_t s = cbeg + threadIdx.x + u * blockDim.x;
-        x[u] = __longlong_as_double(-1LL);
+        x[u] = s < cend ? A.x[s] : __longlong_as_double(-1LL);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+        const uint64_t s = cbeg + threadIdx.x + u * blockDim.x;
         y[u] = z[u] = vx[u] = vy[u] = vz[u] = 0.0;
-        if (s < cend) {
-            x[u] = A.x[s];
+        if (!PICGPU_PUSH_CONDLOAD ? s < cend : !is_gap(x[u])) {
             y[u] = A.y[s];
             z[u] = A.z[s];
             vx[u] = A.vx[s];
@@ -274,29 +304,37 @@ __global__ void __launch_bounds__(256) k_push(const GridD g, const Soa A, uint64
         lidx[u] = -1;
         nc[u] = before[u] = 0;
         if (is_gap(x[u])) continue;
-        bool ok = finite3(x[u], y[u], z[u]);
         bool moved = false;
-        if (!ok) {
+        if (!finite3(x[u], y[u], z[u])) {
             raise_error(&ctr->err, PICGPU_EINVAL);
-        } else {
-            before[u] = store_cell(g, x[u], y[u], z[u]);
-            if (PUSH) {
-                if (!push_one(g, dt, cap2, x[u], y[u], z[u], vx[u], vy[u], vz[u])) {
-                    raise_error(&ctr->err, PICGPU_EDOMAIN);
+        } else if (PUSH) {
+            const double ox = x[u], oy = y[u], oz = z[u];
+            bool ok = push_one<P2>(g, dt, cap2, x[u], y[u], z[u], vx[u], vy[u], vz[u]);
+            if (!ok) {
+                raise_error(&ctr->err, PICGPU_EDOMAIN);
+            } else {
+                A.x[s] = x[u];
+                A.y[s] = y[u];
+                A.z[s] = z[u];
+                if (!finite3(x[u], y[u], z[u])) {
+                    raise_error(&ctr->err, PICGPU_EINVAL);
                     ok = false;
-                } else {
-                    A.x[s] = x[u];
-                    A.y[s] = y[u];
-                    A.z[s] = z[u];
-                    if (!finite3(x[u], y[u], z[u])) {
-                        raise_error(&ctr->err, PICGPU_EINVAL);
-                        ok = false;
-                    }
                 }
             }
             if (ok) {
-                nc[u] = store_cell(g, x[u], y[u], z[u]);
-                moved = nc[u] != before[u];
+                const int p2x = P2 || g.pow2x, p2y = P2 || g.pow2y, p2z = P2 || g.pow2z;
+                const double fx0 = axis_floor(ox, g.gox, g.dx, g.inv_dx, p2x);
+                const double fy0 = axis_floor(oy, g.oy, g.dy, g.inv_dy, p2y);
+                const double fz0 = axis_floor(oz, g.oz, g.dz, g.inv_dz, p2z);
+                const bool same = fx0 >= 0.0 && fy0 >= 0.0 && fz0 >= 0.0 &&
+                                  fx0 == axis_floor(x[u], g.gox, g.dx, g.inv_dx, p2x) &&
+                                  fy0 == axis_floor(y[u], g.oy, g.dy, g.inv_dy, p2y) &&
+                                  fz0 == axis_floor(z[u], g.oz, g.dz, g.inv_dz, p2z);
+                if (!same) {
+                    before[u] = store_cell(g, ox, oy, oz);
+                    nc[u] = store_cell(g, x[u], y[u], z[u]);
+                    moved = nc[u] != before[u];
+                }
             }
         }
         mflag[s] = moved ? 1 : 0;
@@ -575,7 +613,7 @@ __global__ void k_advance(const GridD g, double dt, double cap2, double* __restr
             raise_error(err, PICGPU_EINVAL);
         } else {
             const uint32_t before = cell_linear(g, px, py, pz);
-            if (!push_one(g, dt, cap2, px, py, pz, vx[p], vy[p], vz[p])) {
+            if (!push_one<false>(g, dt, cap2, px, py, pz, vx[p], vy[p], vz[p])) {
                 raise_error(err, PICGPU_EDOMAIN);
             } else {
                 x[p] = px;
@@ -889,16 +927,13 @@ void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     StepCounters* ctr = counters.as<StepCounters>();
     PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
     if (!nc || !n) return;
-    constexpr int UNR = 2;
+    constexpr int UNR = PICGPU_PUSH_UNR;
     const int blocks = (int)((capacity + 256 * UNR - 1) / (256 * UNR));
-    if (push)
-        k_push<true, UNR><<<blocks, 256, 0, st>>>(g, A.soa(), capacity, mflag.as<uint8_t>(), dt, cap2, M.soa(),
-                                                  mcell.as<uint32_t>(), (uint32_t)mcap, dep.as<uint32_t>(), ctr,
-                                                  lrec.as<double>(), (uint32_t)lcap);
-    else
-        k_push<false, UNR><<<blocks, 256, 0, st>>>(g, A.soa(), capacity, mflag.as<uint8_t>(), dt, cap2, M.soa(),
-                                                   mcell.as<uint32_t>(), (uint32_t)mcap, dep.as<uint32_t>(), ctr,
-                                                   lrec.as<double>(), (uint32_t)lcap);
+    const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
+    auto* kern = push ? (p2 ? k_push<true, UNR, true> : k_push<true, UNR, false>)
+                      : (p2 ? k_push<false, UNR, true> : k_push<false, UNR, false>);
+    kern<<<blocks, 256, 0, st>>>(g, A.soa(), capacity, mflag.as<uint8_t>(), dt, cap2, M.soa(), mcell.as<uint32_t>(),
+                                 (uint32_t)mcap, dep.as<uint32_t>(), ctr, lrec.as<double>(), (uint32_t)lcap);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
     k_compact<<<div_up((long long)nc, 256), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
