@@ -91,6 +91,37 @@ PICGPU_API int picgpu_cell_of(const picgpu_grid* g, const double* x, const doubl
 /* ---- stateless, device buffers (asynchronous on `stream`) -------------- */
 /* Inputs and outputs are device pointers; scratch is allocated internally.
  * These are the hot-path entry points when particles already live in HBM. */
+/* pic::StageTimes / pic::KernelCounters (deposit.hpp:121-130). */
+typedef struct picgpu_stage_times {
+    double preproc; /* s: device time of the bin build (the staging pass of deposit_tiled) */
+    double compute; /* s: device time of the J kernel */
+    double reduce;  /* s: 0 -- nodes are reduced inside the J kernel, no rhocell pass */
+} picgpu_stage_times;
+typedef struct picgpu_kernel_counters {
+    uint64_t mopa_calls;     /* tile outer products the reference's engine issues for this input */
+    uint64_t extract_passes; /* tile extractions, same rule (deposit.hpp:191-274) */
+} picgpu_kernel_counters;
+/* pic::TiledOptions (deposit.hpp:179-184) as bit flags. */
+#define PICGPU_TILED_BINS 1u      /* opt.gpma != nullptr: particles stream bin by bin */
+#define PICGPU_TILED_RESIDENCY 2u /* opt.residency (CIC tiles resident across a cell's pairs) */
+#define PICGPU_TILED_DUAL 4u      /* opt.dual_tile */
+/* deposit_tiled (deposit.hpp:284-334): the reference's three-stage MOPA
+ * pipeline.  Same J as deposit_scalar (<= 1e-12); computed by the FP64
+ * tensor-core (DMMA) kernel at orders 2/3.  counters (may be NULL) get the
+ * exact counts the reference's tile engine produces on this input and options.
+ * Grids smaller than the stencil are rejected like NodeMap (rhocell.hpp:49);
+ * the reference's 1 GiB rhocell budget (rhocell.hpp:68-73) does not apply. */
+PICGPU_API int picgpu_deposit_tiled(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
+                                    const double* vx, const double* vy, const double* vz, const double* w, double q,
+                                    uint64_t n, uint32_t options, double* jx, double* jy, double* jz,
+                                    picgpu_stage_times* times, picgpu_kernel_counters* counters);
+/* deposit_rhocell_vector (deposit.hpp:87-119): the per-cell vector-unit
+ * variant; same J, computed by the warp-per-pencil DFMA kernel at orders 2/3.
+ * reduce_seconds (may be NULL) gets 0 (no separate reduce pass). */
+PICGPU_API int picgpu_deposit_rhocell_vector(const picgpu_grid* g, int order, const double* x, const double* y,
+                                             const double* z, const double* vx, const double* vy, const double* vz,
+                                             const double* w, double q, uint64_t n, int use_bins, double* jx,
+                                             double* jy, double* jz, double* reduce_seconds);
 PICGPU_API int picgpu_deposit_current_dev(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
                                const double* vx, const double* vy, const double* vz, const double* w, double q,
                                uint64_t n, double* jx, double* jy, double* jz, void* stream);

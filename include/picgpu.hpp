@@ -9,6 +9,8 @@
 //   ShapeOrder (+ tsc, this project's order 2)   shape.hpp:14
 //   CurrentGrid                                  grid.hpp:127-150
 //   deposit_scalar, deposit_density              deposit.hpp:62-83
+//   deposit_tiled (+TiledOptions, StageTimes,
+//   KernelCounters), deposit_rhocell_vector      deposit.hpp:87-130, :179-334
 //   advance                                      workload.hpp:139-155
 //   GpmaConfig, gpma_build (perm + bins)         gpma.hpp:22-26, :379-402
 //   SortPolicy, RankSortStats, SortReason,
@@ -189,6 +191,58 @@ inline Bins gpma_build(ParticleSoA& soa, const GridSpec& g, GpmaConfig = {}) {
                                b.starts.data(), b.counts.data()));
     soa.apply_permutation(b.perm);
     return b;
+}
+
+// deposit.hpp:121-130, :179-184.
+struct KernelCounters {
+    std::uint64_t mopa_calls = 0;
+    std::uint64_t extract_passes = 0;
+};
+struct StageTimes {
+    double preproc = 0.0;
+    double compute = 0.0;
+    double reduce = 0.0;
+};
+struct TiledOptions {
+    const Bins* gpma = nullptr;  // when set, particles stream bin by bin
+    bool residency = true;
+    bool dual_tile = false;
+    KernelCounters* counters = nullptr;
+};
+
+// deposit_tiled (deposit.hpp:284-334): the same J as deposit_scalar, computed
+// by the FP64 tensor-core (DMMA) kernel; counters get the reference tile
+// engine's counts for this input and options.
+inline CurrentGrid deposit_tiled(const ParticleSoA& soa, const GridSpec& g, ShapeOrder order,
+                                 const TiledOptions& opt = {}, StageTimes* times = nullptr) {
+    CurrentGrid grid(g);
+    const picgpu_grid cg = g.c();
+    const std::uint32_t flags = (opt.gpma ? PICGPU_TILED_BINS : 0u) | (opt.residency ? PICGPU_TILED_RESIDENCY : 0u) |
+                                (opt.dual_tile ? PICGPU_TILED_DUAL : 0u);
+    picgpu_stage_times st{};
+    picgpu_kernel_counters kc{};
+    check(picgpu_deposit_tiled(&cg, static_cast<int>(order), soa.x.data(), soa.y.data(), soa.z.data(),
+                               soa.vx.data(), soa.vy.data(), soa.vz.data(), soa.w.data(), soa.q, soa.size(), flags,
+                               grid.jx.data(), grid.jy.data(), grid.jz.data(), times ? &st : nullptr,
+                               opt.counters ? &kc : nullptr));
+    if (times) *times = {st.preproc, st.compute, st.reduce};
+    if (opt.counters) {
+        opt.counters->mopa_calls += kc.mopa_calls;  // the reference increments
+        opt.counters->extract_passes += kc.extract_passes;
+    }
+    return grid;
+}
+
+// deposit_rhocell_vector (deposit.hpp:87-119): the same J, warp-DFMA kernel.
+inline CurrentGrid deposit_rhocell_vector(const ParticleSoA& soa, const GridSpec& g, ShapeOrder order,
+                                          const Bins* gpma = nullptr, double* reduce_seconds = nullptr) {
+    CurrentGrid grid(g);
+    const picgpu_grid cg = g.c();
+    check(picgpu_deposit_rhocell_vector(&cg, static_cast<int>(order), soa.x.data(), soa.y.data(), soa.z.data(),
+                                        soa.vx.data(), soa.vy.data(), soa.vz.data(), soa.w.data(), soa.q, soa.size(),
+                                        gpma != nullptr, grid.jx.data(), grid.jy.data(), grid.jz.data(),
+                                        reduce_seconds));
+    return grid;
 }
 
 struct SortPolicy {

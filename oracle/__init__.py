@@ -179,6 +179,8 @@ class Reference:
         L.ref_deposit_scalar_mt.argtypes = [_p, C.c_int, C.c_int, _p, _p, _p]
         L.ref_deposit_density.argtypes = [_p, C.c_int, _p, _p]
         L.ref_deposit_tiled.argtypes = [_p, C.c_int, C.c_int, _p, _p, _p]
+        L.ref_deposit_tiled_opt.argtypes = [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p]
+        L.ref_deposit_rhocell.argtypes = [_p, C.c_int, C.c_int, _p, _p, _p]
         L.ref_gpma_build.argtypes = [_p, _d, _u32]
         L.ref_advance.argtypes = [_p, _d, _p]
         L.ref_incremental_sort.argtypes = [_p, _p]
@@ -265,6 +267,18 @@ class RefState:
     def deposit_tiled(self, order, use_gpma=False):
         jx, jy, jz = (np.zeros(self.g.ncells) for _ in range(3))
         self.ref._check(self.ref.L.ref_deposit_tiled(self.h, order, int(use_gpma), _ptr(jx), _ptr(jy), _ptr(jz)))
+        return jx, jy, jz
+
+    def deposit_tiled_opt(self, order, use_gpma=False, residency=True, dual_tile=False):
+        jx, jy, jz = (np.zeros(self.g.ncells) for _ in range(3))
+        m, e = C.c_uint64(), C.c_uint64()
+        self.ref._check(self.ref.L.ref_deposit_tiled_opt(self.h, order, int(use_gpma), int(residency), int(dual_tile),
+                                                         _ptr(jx), _ptr(jy), _ptr(jz), C.byref(m), C.byref(e)))
+        return (jx, jy, jz), (m.value, e.value)
+
+    def deposit_rhocell(self, order, use_gpma=False):
+        jx, jy, jz = (np.zeros(self.g.ncells) for _ in range(3))
+        self.ref._check(self.ref.L.ref_deposit_rhocell(self.h, order, int(use_gpma), _ptr(jx), _ptr(jy), _ptr(jz)))
         return jx, jy, jz
 
     def gpma_build(self, gap_ratio=0.25, min_gap=2):

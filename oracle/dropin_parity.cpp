@@ -70,6 +70,41 @@ pic::ParticleSoA plasma(const pic::GridSpec& g, int ppc, double u_th, std::uint6
     return s;
 }
 
+// deposit_tiled (deposit.hpp:284) and deposit_rhocell_vector (:87): same J,
+// and the GPU reports the reference tile engine's counters exactly.
+template <class RefOpt, class GpuOpt>
+void tiled_case(const pic::ParticleSoA& ref, const pic::GridSpec& g, const picgpu::ParticleSoA& gpu,
+                const picgpu::GridSpec& gg, RefOpt ropt, GpuOpt gopt, const char* what) {
+    for (auto [po, go] : {std::pair{pic::ShapeOrder::cic, picgpu::ShapeOrder::cic},
+                          std::pair{pic::ShapeOrder::qsp, picgpu::ShapeOrder::qsp}}) {
+        for (int mode = 0; mode < 3; ++mode) {  // residency on, off, on + dual tile
+            pic::KernelCounters kr;
+            picgpu::KernelCounters kg;
+            ropt.residency = gopt.residency = mode != 1;
+            ropt.dual_tile = gopt.dual_tile = mode == 2;
+            ropt.counters = &kr;
+            gopt.counters = &kg;
+            picgpu::StageTimes st;
+            const pic::CurrentGrid jr = pic::deposit_tiled(ref, g, po, ropt);
+            const picgpu::CurrentGrid jt = picgpu::deposit_tiled(gpu, gg, go, gopt, &st);
+            char msg[160];
+            const double e = peak_rel_err(jt, jr);
+            std::snprintf(msg, sizeof msg, "deposit_tiled %s order %d mode %d: J err %.2e, counters %llu/%llu vs %llu/%llu",
+                          what, static_cast<int>(po), mode, e, (unsigned long long)kg.mopa_calls,
+                          (unsigned long long)kg.extract_passes, (unsigned long long)kr.mopa_calls,
+                          (unsigned long long)kr.extract_passes);
+            expect(e <= 1e-12 && kg.mopa_calls == kr.mopa_calls && kg.extract_passes == kr.extract_passes &&
+                       st.compute > 0.0, msg);
+        }
+        const pic::CurrentGrid jr = pic::deposit_rhocell_vector(ref, g, po, ropt.gpma);
+        const picgpu::CurrentGrid jv = picgpu::deposit_rhocell_vector(gpu, gg, go, gopt.gpma);
+        char msg[96];
+        const double e = peak_rel_err(jv, jr);
+        std::snprintf(msg, sizeof msg, "deposit_rhocell_vector %s order %d: J err %.2e", what, static_cast<int>(po), e);
+        expect(e <= 1e-12, msg);
+    }
+}
+
 picgpu::ParticleSoA to_gpu(const pic::ParticleSoA& s) {
     picgpu::ParticleSoA o;
     o.x = s.x; o.y = s.y; o.z = s.z; o.vx = s.vx; o.vy = s.vy; o.vz = s.vz; o.w = s.w; o.id = s.id; o.q = s.q;
@@ -122,9 +157,20 @@ int main() {
                "deposit_density: rho bit-identical (unsorted store)");
     }
 
+    // --- deposit_tiled / deposit_rhocell_vector on the unsorted store ---
+    tiled_case(ref, g, gpu, gg, pic::TiledOptions{}, picgpu::TiledOptions{}, "unsorted");
+
     // --- gpma_build (gpma.hpp:379): same stable permutation of the store ---
     pic::Gpma gpma = pic::gpma_build(ref, g);
     const picgpu::Bins bins = picgpu::gpma_build(gpu, gg);
+    {
+        pic::TiledOptions ro;
+        ro.gpma = &gpma;
+        picgpu::TiledOptions go;
+        go.gpma = &bins;
+        tiled_case(ref, g, gpu, gg, ro, go, "bins");
+        tiled_case(ref, g, gpu, gg, pic::TiledOptions{}, picgpu::TiledOptions{}, "sorted");
+    }
     expect(ref.id == gpu.id && ref.x == gpu.x, "gpma_build: store permuted identically");
     {
         const auto rr = pic::deposit_density(ref, g, pic::ShapeOrder::qsp, charge);  // charge is uniform per species

@@ -195,6 +195,33 @@ int ref_deposit_tiled(void* h, int order, int use_gpma, double* jx, double* jy, 
     });
 }
 
+// deposit_tiled with every TiledOptions field, plus the engine's counters.
+int ref_deposit_tiled_opt(void* h, int order, int use_gpma, int residency, int dual_tile, double* jx, double* jy,
+                          double* jz, uint64_t* mopa_calls, uint64_t* extract_passes) {
+    auto* s = static_cast<RefState*>(h);
+    return guarded([&] {
+        pic::KernelCounters kc;
+        pic::TiledOptions opt;
+        opt.gpma = use_gpma && s->has_gpma ? &s->gpma : nullptr;
+        opt.residency = residency != 0;
+        opt.dual_tile = dual_tile != 0;
+        opt.counters = &kc;
+        const pic::CurrentGrid cg = pic::deposit_tiled(s->soa, s->grid, to_order(order), opt);
+        copy_out(cg.jx, jx); copy_out(cg.jy, jy); copy_out(cg.jz, jz);
+        *mopa_calls = kc.mopa_calls;
+        *extract_passes = kc.extract_passes;
+    });
+}
+
+int ref_deposit_rhocell(void* h, int order, int use_gpma, double* jx, double* jy, double* jz) {
+    auto* s = static_cast<RefState*>(h);
+    return guarded([&] {
+        const pic::CurrentGrid cg = pic::deposit_rhocell_vector(s->soa, s->grid, to_order(order),
+                                                                use_gpma && s->has_gpma ? &s->gpma : nullptr);
+        copy_out(cg.jx, jx); copy_out(cg.jy, jy); copy_out(cg.jz, jz);
+    });
+}
+
 // pic::gpma_build: physically sorts the store (stable counting sort) and
 // indexes it.  With ids equal to the pre-sort storage index, id[i] after the
 // call is perm[i].

@@ -6,6 +6,8 @@ and argument meaning follow the reference headers under proj/include/pic/:
 
     deposit_scalar(soa, grid, order)            deposit.hpp:62-73
     deposit_density(soa, grid, order, quantity) deposit.hpp:76-83
+    deposit_tiled(soa, grid, order, opt, times) deposit.hpp:284-334 (DMMA tensor-core kernel)
+    deposit_rhocell_vector(soa, grid, order)    deposit.hpp:87-119 (warp-DFMA kernel)
     counting_sort(soa, grid)                    gpma.hpp:379-394 (perm, starts, counts)
     gpma_build(soa, grid, cfg)                  gpma.hpp:379-402 (permutes soa in place)
     advance(soa, dt, grid)                      workload.hpp:139-155
@@ -117,6 +119,31 @@ class SessionConfig(C.Structure):
                 ("flags", C.c_uint32)]
 
 
+class StageTimes(C.Structure):
+    """pic::StageTimes (deposit.hpp:126-130), seconds."""
+
+    _fields_ = [("preproc", C.c_double), ("compute", C.c_double), ("reduce", C.c_double)]
+
+
+class KernelCounters(C.Structure):
+    """pic::KernelCounters (deposit.hpp:121-124)."""
+
+    _fields_ = [("mopa_calls", C.c_uint64), ("extract_passes", C.c_uint64)]
+
+
+@dataclass
+class TiledOptions:
+    """pic::TiledOptions (deposit.hpp:179-184); gpma: stream bin by bin."""
+
+    gpma: bool = False
+    residency: bool = True
+    dual_tile: bool = False
+    counters: KernelCounters | None = None
+
+    def flags(self) -> int:
+        return (1 if self.gpma else 0) | (2 if self.residency else 0) | (4 if self.dual_tile else 0)
+
+
 class SortPolicy(C.Structure):
     """pic::SortPolicy (sort_policy.hpp:12-30); defaults are Table 4's."""
 
@@ -191,6 +218,10 @@ def lib():
     L.picgpu_session_phase_times.argtypes = [_P, _P, _P, C.c_int]
     L.picgpu_session_reset_phase_times.argtypes = [_P]
     L.picgpu_fp64_peak.argtypes = [C.c_int, C.POINTER(_D)]
+    L.picgpu_deposit_tiled.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, C.c_uint32, _P, _P, _P,
+                                                                C.POINTER(StageTimes), C.POINTER(KernelCounters)]
+    L.picgpu_deposit_rhocell_vector.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, C.c_int, _P, _P, _P,
+                                                                         C.POINTER(_D)]
     L.picgpu_slab_grid.argtypes = [G, C.c_int, C.c_int, C.c_int, G]
     L.picgpu_session_set_slab.argtypes = [_P, G, C.c_int, C.c_int, C.c_int]
     L.picgpu_session_step_begin.argtypes = [_P, _D, C.c_uint32, C.POINTER(_U64), C.POINTER(_U64)]
@@ -290,6 +321,37 @@ def deposit_scalar(soa, grid: Grid, order: int, q: float | None = None) -> Curre
     _check(lib().picgpu_deposit_current(C.byref(grid), order, _ptr(s.x), _ptr(s.y), _ptr(s.z), _ptr(s.vx),
                                         _ptr(s.vy), _ptr(s.vz), _ptr(s.w), qq, s.size(), _ptr(jx), _ptr(jy),
                                         _ptr(jz)))
+    return CurrentGrid(grid, jx, jy, jz)
+
+
+def deposit_tiled(soa, grid: Grid, order: int, opt: TiledOptions | None = None, times: StageTimes | None = None,
+                  q: float | None = None) -> CurrentGrid:
+    """deposit_tiled (deposit.hpp:284-334): same J, on the FP64 tensor-core (DMMA)
+    kernel; opt.counters gets the reference tile engine's counts for this input."""
+    s = _soa(soa, q)
+    opt = opt or TiledOptions()
+    nc = grid.ncells
+    jx, jy, jz = np.empty(nc), np.empty(nc), np.empty(nc)
+    kc = KernelCounters()
+    _check(lib().picgpu_deposit_tiled(C.byref(grid), order, _ptr(s.x), _ptr(s.y), _ptr(s.z), _ptr(s.vx), _ptr(s.vy),
+                                      _ptr(s.vz), _ptr(s.w), s.q if q is None else q, s.size(), opt.flags(),
+                                      _ptr(jx), _ptr(jy), _ptr(jz), C.byref(times) if times is not None else None,
+                                      C.byref(kc) if opt.counters is not None else None))
+    if opt.counters is not None:  # the reference increments its counters
+        opt.counters.mopa_calls += kc.mopa_calls
+        opt.counters.extract_passes += kc.extract_passes
+    return CurrentGrid(grid, jx, jy, jz)
+
+
+def deposit_rhocell_vector(soa, grid: Grid, order: int, gpma: bool = False, q: float | None = None) -> CurrentGrid:
+    """deposit_rhocell_vector (deposit.hpp:87-119): same J, on the warp-DFMA kernel."""
+    s = _soa(soa, q)
+    nc = grid.ncells
+    jx, jy, jz = np.empty(nc), np.empty(nc), np.empty(nc)
+    red = C.c_double(-1.0)
+    _check(lib().picgpu_deposit_rhocell_vector(C.byref(grid), order, _ptr(s.x), _ptr(s.y), _ptr(s.z), _ptr(s.vx),
+                                               _ptr(s.vy), _ptr(s.vz), _ptr(s.w), s.q if q is None else q, s.size(),
+                                               int(gpma), _ptr(jx), _ptr(jy), _ptr(jz), C.byref(red)))
     return CurrentGrid(grid, jx, jy, jz)
 
 

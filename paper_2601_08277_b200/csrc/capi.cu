@@ -139,6 +139,40 @@ struct Stateless {
     }
 };
 
+// Tile-engine counts of deposit_tiled (deposit.hpp:191-274) from the grouping
+// the reference would see: out[0] += groups, out[1] += sum of ceil(len/2).
+// Bins: one group per non-empty cell.  Runs: maximal runs of equal cell id in
+// storage order (the residency-on path without an index, deposit.hpp:303-313).
+__global__ void k_bin_groups(const uint32_t* __restrict__ cnt, uint32_t ncells, unsigned long long* out) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long grp = 0, pairs = 0;
+    if (c < ncells && cnt[c]) {
+        grp = 1;
+        pairs = (cnt[c] + 1u) / 2u;
+    }
+    grp = __reduce_add_sync(0xffffffffu, (unsigned)grp);
+    pairs = __reduce_add_sync(0xffffffffu, (unsigned)pairs);
+    if ((threadIdx.x & 31) == 0 && grp) {
+        atomicAdd(out, grp);
+        atomicAdd(out + 1, pairs);
+    }
+}
+
+__global__ void k_run_groups(const uint32_t* __restrict__ key, uint64_t n, unsigned long long* out) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long grp = 0, pairs = 0;
+    if (p < n && (p == 0 || key[p] != key[p - 1])) {
+        uint64_t e = p + 1;
+        while (e < n && key[e] == key[p]) ++e;
+        grp = 1;
+        pairs = (e - p + 1) / 2;
+    }
+    if (grp) {
+        atomicAdd(out, grp);
+        atomicAdd(out + 1, pairs);
+    }
+}
+
 static Stateless& stateless() {
     static Stateless* s = new Stateless;  // never destroyed (driver may be gone at exit)
     return *s;
@@ -213,31 +247,116 @@ int picgpu_should_global_sort(const picgpu_rank_sort_stats* s, const picgpu_sort
 
 // ---- stateless -------------------------------------------------------------
 
+}  // extern "C"
+
+// deposit_scalar / deposit_tiled / deposit_rhocell_vector on host buffers:
+// H2D, bin build (stable counting sort), J with the requested kernel family,
+// D2H.  Device times of the build and of J in *sort_ms / *j_ms.
+static void stateless_current(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
+                              const double* vx, const double* vy, const double* vz, const double* w, double q,
+                              uint64_t n, int kernel, double* jx, double* jy, double* jz, float* sort_ms,
+                              float* j_ms, const uint32_t* tiled_options, picgpu_kernel_counters* counters) {
+    check_order(order);
+    const GridD gd = make_grid(*g);
+    Stateless& S = stateless();
+    std::lock_guard<std::mutex> lk(S.mu);
+    S.prepare(*g);
+    BinStore& bs = S.store;
+    const cudaStream_t st = S.st;
+    const bool timed = sort_ms || j_ms;
+    cudaEvent_t ev[3] = {};
+    if (timed)
+        for (auto& e : ev) PICGPU_CUDA_TRY(cudaEventCreate(&e));
+    bs.B.ensure(n);
+    const Soa b = bs.B.soa();
+    h2d(b.x, x, n * 8, st); h2d(b.y, y, n * 8, st); h2d(b.z, z, n * 8, st);
+    h2d(b.vx, vx, n * 8, st); h2d(b.vy, vy, n * 8, st); h2d(b.vz, vz, n * 8, st);
+    h2d(b.w, w, n * 8, st);
+    if (timed) PICGPU_CUDA_TRY(cudaEventRecord(ev[0], st));
+    bs.full_sort_from_B(n);
+    if (timed) PICGPU_CUDA_TRY(cudaEventRecord(ev[1], st));
+    S.J.ensure((size_t)gd.ncells * 24);
+    double* J = S.J.as<double>();
+    PICGPU_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)gd.ncells * 24, st));
+    if (n) launch_deposit_current(order, gd, bs.A.soa(), bs.d_off(), bs.d_cnt(), q, J, bs.num_sms, st, kernel);
+    if (timed) PICGPU_CUDA_TRY(cudaEventRecord(ev[2], st));
+    if (counters) {
+        const uint32_t opt = *tiled_options;
+        unsigned long long* d = S.flag.as<unsigned long long>();
+        PICGPU_CUDA_TRY(cudaMemsetAsync(d, 0, 16, st));
+        if (opt & PICGPU_TILED_BINS) {
+            k_bin_groups<<<div_up((long long)gd.ncells, 256), 256, 0, st>>>(bs.d_cnt(), gd.ncells, d);
+            note_launch();
+        } else if (n) {  // storage-order cell ids of the input (k_cells output of the sort)
+            k_run_groups<<<div_up((long long)n, 256), 256, 0, st>>>(bs.keys.as<uint32_t>(), n, d);
+            note_launch();
+        }
+        PICGPU_CUDA_TRY(cudaGetLastError());
+        unsigned long long h[2] = {0, 0};
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, st));
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+        const bool runs = (opt & (PICGPU_TILED_BINS | PICGPU_TILED_RESIDENCY)) != 0;
+        const uint64_t pairs = runs ? h[1] : (n + 1) / 2;
+        counters->mopa_calls = 3 * pairs;
+        if (order == 1 && runs && (opt & PICGPU_TILED_RESIDENCY))  // cic_group_resident
+            counters->extract_passes = 3 * h[0] * ((opt & PICGPU_TILED_DUAL) ? 2 : 1);
+        else  // cic_pair_flush / qsp_pair: one extraction per pair and component
+            counters->extract_passes = 3 * pairs;
+    }
+    d2h(jx, J, (size_t)gd.ncells * 8, st);
+    d2h(jy, J + gd.ncells, (size_t)gd.ncells * 8, st);
+    d2h(jz, J + 2 * (size_t)gd.ncells, (size_t)gd.ncells * 8, st);
+    PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    if (timed) {
+        float a = 0, c = 0;
+        PICGPU_CUDA_TRY(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        PICGPU_CUDA_TRY(cudaEventElapsedTime(&c, ev[1], ev[2]));
+        if (sort_ms) *sort_ms = a;
+        if (j_ms) *j_ms = c;
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+}
+
+extern "C" {
+
 int picgpu_deposit_current(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
                            const double* vx, const double* vy, const double* vz, const double* w, double q,
                            uint64_t n, double* jx, double* jy, double* jz) {
     return guard([&] {
+        stateless_current(g, order, x, y, z, vx, vy, vz, w, q, n, kJDefault, jx, jy, jz, nullptr, nullptr, nullptr,
+                          nullptr);
+    });
+}
+
+int picgpu_deposit_tiled(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
+                         const double* vx, const double* vy, const double* vz, const double* w, double q, uint64_t n,
+                         uint32_t options, double* jx, double* jy, double* jz, picgpu_stage_times* times,
+                         picgpu_kernel_counters* counters) {
+    return guard([&] {
         check_order(order);
-        const GridD gd = make_grid(*g);
-        Stateless& S = stateless();
-        std::lock_guard<std::mutex> lk(S.mu);
-        S.prepare(*g);
-        BinStore& bs = S.store;
-        const cudaStream_t st = S.st;
-        bs.B.ensure(n);
-        const Soa b = bs.B.soa();
-        h2d(b.x, x, n * 8, st); h2d(b.y, y, n * 8, st); h2d(b.z, z, n * 8, st);
-        h2d(b.vx, vx, n * 8, st); h2d(b.vy, vy, n * 8, st); h2d(b.vz, vz, n * 8, st);
-        h2d(b.w, w, n * 8, st);
-        bs.full_sort_from_B(n);
-        S.J.ensure((size_t)gd.ncells * 24);
-        double* J = S.J.as<double>();
-        PICGPU_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)gd.ncells * 24, st));
-        if (n) launch_deposit_current(order, gd, bs.A.soa(), bs.d_off(), bs.d_cnt(), q, J, bs.num_sms, st);
-        d2h(jx, J, (size_t)gd.ncells * 8, st);
-        d2h(jy, J + gd.ncells, (size_t)gd.ncells * 8, st);
-        d2h(jz, J + 2 * (size_t)gd.ncells, (size_t)gd.ncells * 8, st);
-        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+        check_density_grid(*g, order);  // NodeMap: grid smaller than the stencil support
+        float sort_ms = 0, j_ms = 0;
+        stateless_current(g, order, x, y, z, vx, vy, vz, w, q, n, kJMatrix, jx, jy, jz, times ? &sort_ms : nullptr,
+                          times ? &j_ms : nullptr, &options, counters);
+        if (times) {
+            times->preproc = sort_ms * 1e-3;
+            times->compute = j_ms * 1e-3;
+            times->reduce = 0.0;
+        }
+    });
+}
+
+int picgpu_deposit_rhocell_vector(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
+                                  const double* vx, const double* vy, const double* vz, const double* w, double q,
+                                  uint64_t n, int use_bins, double* jx, double* jy, double* jz,
+                                  double* reduce_seconds) {
+    (void)use_bins;  // the same J either way; the GPU always deposits from bins
+    return guard([&] {
+        check_order(order);
+        check_density_grid(*g, order);
+        stateless_current(g, order, x, y, z, vx, vy, vz, w, q, n, kJVector, jx, jy, jz, nullptr, nullptr, nullptr,
+                          nullptr);
+        if (reduce_seconds) *reduce_seconds = 0.0;
     });
 }
 

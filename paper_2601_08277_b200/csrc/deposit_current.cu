@@ -1043,17 +1043,18 @@ static int j_variant() {
 
 // J must be zeroed by the caller (halo nodes are reduced into it).
 void launch_deposit_current(int order, const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt,
-                            double q, double* j, int num_sms, cudaStream_t st) {
+                            double q, double* j, int num_sms, cudaStream_t st, int kernel) {
+    const int k = kernel == kJDefault ? j_variant() : kernel;
     switch (order) {
         case 1: launch_order<1>(g, p, off, cnt, q, j, num_sms, st); break;
         case 2:
-            if (j_variant() == 1) launch_warp<2>(g, p, off, cnt, q, j, num_sms, st);
-            else if (j_variant() == 2) launch_dmma<2>(g, p, off, cnt, q, j, num_sms, st);
+            if (k == kJVector) launch_warp<2>(g, p, off, cnt, q, j, num_sms, st);
+            else if (k == kJMatrix) launch_dmma<2>(g, p, off, cnt, q, j, num_sms, st);
             else launch_order<2>(g, p, off, cnt, q, j, num_sms, st);
             break;
         case 3:
-            if (j_variant() == 1) launch_warp<3>(g, p, off, cnt, q, j, num_sms, st);
-            else if (j_variant() == 2) launch_dmma<3>(g, p, off, cnt, q, j, num_sms, st);
+            if (k == kJVector) launch_warp<3>(g, p, off, cnt, q, j, num_sms, st);
+            else if (k == kJMatrix) launch_dmma<3>(g, p, off, cnt, q, j, num_sms, st);
             else launch_order<3>(g, p, off, cnt, q, j, num_sms, st);
             break;
         default: throw Status{PICGPU_EINVAL, "deposit: shape order must be 1, 2 or 3"};

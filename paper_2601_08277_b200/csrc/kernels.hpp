@@ -10,8 +10,12 @@ namespace picgpu {
 
 // deposit_current.cu ---------------------------------------------------------
 // J (3*ncells doubles: jx|jy|jz, pre-zeroed) += deposit of the binned store.
+// J kernel families (orders 2 and 3; order 1 always uses the lane kernel):
+// the default register-lane DFMA kernel, the warp-per-pencil "vector" DFMA
+// kernel, and the FP64 tensor-core (DMMA m8n8k4) "matrix" kernel.
+enum JKernel { kJDefault = -1, kJLane = 0, kJVector = 1, kJMatrix = 2 };
 void launch_deposit_current(int order, const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt,
-                            double q, double* j, int num_sms, cudaStream_t st);
+                            double q, double* j, int num_sms, cudaStream_t st, int kernel = kJDefault);
 
 // deposit_density.cu ---------------------------------------------------------
 // rho[node] = ordered sum (storage order) of quantity[s] * S (quantity NULL: qscale*w[s]), over binned,
