@@ -18,6 +18,12 @@
  *                               detect_moves + apply_pending_moves, rebuild, global_sort
  *                               (sort_policy.hpp:83), deposit_scalar / deposit_density.
  *   picgpu_should_global_sort <- pic::should_global_sort     sort_policy.hpp:62-73
+ *   picgpu_deposit_tiled     <- pic::deposit_tiled (+ KernelCounters, StageTimes) deposit.hpp:121-334
+ *   picgpu_deposit_rhocell_vector <- pic::deposit_rhocell_vector deposit.hpp:87-119
+ *   picgpu_session_make_workload <- pic::make_workload        workload.hpp:16-125
+ *   picgpu_slab_grid, picgpu_session_set_slab / step_begin / step_end / guard planes
+ *                            <- new: x-slab decomposition over ranks (the
+ *                               reference has no domain decomposition)
  *
  * Errors: every call returns a status.  The codes map one-to-one onto the
  * exception types the reference throws; picgpu_last_error()
@@ -88,9 +94,6 @@ PICGPU_API int picgpu_advance(const picgpu_grid* g, double dt, double* x, double
 PICGPU_API int picgpu_cell_of(const picgpu_grid* g, const double* x, const double* y, const double* z, uint64_t n,
                    uint32_t* cell);
 
-/* ---- stateless, device buffers (asynchronous on `stream`) -------------- */
-/* Inputs and outputs are device pointers; scratch is allocated internally.
- * These are the hot-path entry points when particles already live in HBM. */
 /* pic::StageTimes / pic::KernelCounters (deposit.hpp:121-130). */
 typedef struct picgpu_stage_times {
     double preproc; /* s: device time of the bin build (the staging pass of deposit_tiled) */
@@ -122,6 +125,10 @@ PICGPU_API int picgpu_deposit_rhocell_vector(const picgpu_grid* g, int order, co
                                              const double* z, const double* vx, const double* vy, const double* vz,
                                              const double* w, double q, uint64_t n, int use_bins, double* jx,
                                              double* jy, double* jz, double* reduce_seconds);
+
+/* ---- stateless, device buffers (asynchronous on `stream`) -------------- */
+/* Inputs and outputs are device pointers; scratch is allocated internally.
+ * These are the hot-path entry points when particles already live in HBM. */
 PICGPU_API int picgpu_deposit_current_dev(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
                                const double* vx, const double* vy, const double* vz, const double* w, double q,
                                uint64_t n, double* jx, double* jy, double* jz, void* stream);
@@ -179,6 +186,8 @@ typedef struct picgpu_session_config {
 #define PICGPU_STEP_DENSITY 8u    /* deposit rho = q*W (bit-exact ordered gather) */
 #define PICGPU_STEP_GLOBAL_SORT 16u /* force a full re-sort (global_sort) after the deposit */
 #define PICGPU_STEP_NO_SYNC 32u   /* do not read back step stats (counts stay on device) */
+#define PICGPU_STEP_RESORT 64u    /* instead of SORT: after the push, a full stable counting sort of the
+                                     whole store (hybrid-globalsort and the modes without an index) */
 #define PICGPU_STEP_DEFAULT (PICGPU_STEP_PUSH | PICGPU_STEP_SORT | PICGPU_STEP_CURRENT)
 
 typedef struct picgpu_step_stats {
@@ -207,6 +216,32 @@ PICGPU_API int picgpu_session_generate_plasma(picgpu_session* s, int ppc, double
 /* One step: [push] -> [incremental sort] -> [deposit J] -> [deposit rho] -> [global sort]. */
 PICGPU_API int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_step_stats* out);
 PICGPU_API int picgpu_session_global_sort(picgpu_session* s);
+/* J kernel family used by this session's steps (orders 2/3): 0 register-lane
+ * DFMA (default), 1 warp-per-pencil DFMA ("vector", rhocell-vector modes),
+ * 2 FP64 tensor-core DMMA ("matrix", tile-engine modes). */
+PICGPU_API int picgpu_session_set_kernel(picgpu_session* s, int family);
+
+/* pic::WorkloadConfig (workload.hpp:16-44) and make_workload (:75-125): ppc
+ * particles per cell on a regular sub-lattice, Maxwellian velocities
+ * truncated at the displacement cap, optional shear drift, W = 1.  Generated
+ * on the device (velocities may differ from glibc's in the last ulp of log /
+ * cos); the reference's 2^28-particle limit does not apply. */
+#define PICGPU_WORKLOAD_UNIFORM 0
+#define PICGPU_WORKLOAD_DRIFT_GRADIENT 1
+typedef struct picgpu_workload {
+    picgpu_grid grid;
+    int32_t ppc;
+    int32_t kind;            /* PICGPU_WORKLOAD_* */
+    double thermal_speed;
+    double drift[3];         /* drift_gradient amplitude; all zero selects 0.5 * speed cap along x */
+    uint64_t seed;
+    int32_t steps;
+    int32_t order;           /* ShapeOrder */
+    double dt;
+    double charge;
+} picgpu_workload;
+/* Replaces the session's particles by make_workload(cfg) (grid must match). */
+PICGPU_API int picgpu_session_make_workload(picgpu_session* s, const picgpu_workload* cfg);
 PICGPU_API int picgpu_session_synchronize(picgpu_session* s);
 PICGPU_API uint64_t picgpu_session_num_particles(picgpu_session* s);
 PICGPU_API uint64_t picgpu_session_capacity(picgpu_session* s);

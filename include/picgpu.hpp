@@ -23,6 +23,8 @@
 #pragma once
 
 #include <array>
+#include <chrono>
+#include <string_view>
 #include <cstdint>
 #include <new>
 #include <span>
@@ -325,11 +327,184 @@ class Session {
         return s;
     }
     std::size_t capacity() const { return picgpu_session_capacity(h_); }
+    std::size_t size() const { return picgpu_session_num_particles(h_); }
+    void set_kernel(int family) { check(picgpu_session_set_kernel(h_, family)); }
+    void make_workload(const picgpu_workload& w) { check(picgpu_session_make_workload(h_, &w)); }
+    std::array<double, PICGPU_NPHASES> phase_ms() const {
+        std::array<double, PICGPU_NPHASES> ms{};
+        check(picgpu_session_phase_times(h_, ms.data(), nullptr, PICGPU_NPHASES));
+        return ms;
+    }
     picgpu_session* handle() const { return h_; }
 
    private:
     GridSpec grid_;
     picgpu_session* h_ = nullptr;
 };
+
+// ---- the reference's harness loop (simulation.hpp:19-176) -------------------
+
+enum class AblationMode {
+    baseline,
+    matrix_only,
+    hybrid_nosort,
+    hybrid_globalsort,
+    fullopt,
+    rhocell_vector,
+    baseline_incrsort,
+    rhocell_incrsort,
+};
+inline constexpr std::array<AblationMode, 8> kAllModes{
+    AblationMode::baseline,          AblationMode::matrix_only,      AblationMode::hybrid_nosort,
+    AblationMode::hybrid_globalsort, AblationMode::fullopt,          AblationMode::rhocell_vector,
+    AblationMode::baseline_incrsort, AblationMode::rhocell_incrsort};
+
+inline const char* to_string(AblationMode m) {
+    switch (m) {
+        case AblationMode::baseline: return "baseline";
+        case AblationMode::matrix_only: return "matrix-only";
+        case AblationMode::hybrid_nosort: return "hybrid-nosort";
+        case AblationMode::hybrid_globalsort: return "hybrid-globalsort";
+        case AblationMode::fullopt: return "fullopt";
+        case AblationMode::rhocell_vector: return "rhocell-vector";
+        case AblationMode::baseline_incrsort: return "baseline-incrsort";
+        case AblationMode::rhocell_incrsort: return "rhocell-incrsort";
+    }
+    return "?";
+}
+inline AblationMode mode_from_string(std::string_view s) {
+    for (AblationMode m : kAllModes)
+        if (s == to_string(m)) return m;
+    throw std::invalid_argument("unknown mode: " + std::string(s));
+}
+inline bool mode_uses_gpma(AblationMode m) {
+    return m == AblationMode::hybrid_globalsort || m == AblationMode::fullopt ||
+           m == AblationMode::baseline_incrsort || m == AblationMode::rhocell_incrsort;
+}
+inline bool mode_incremental_sort(AblationMode m) {
+    return m == AblationMode::fullopt || m == AblationMode::baseline_incrsort || m == AblationMode::rhocell_incrsort;
+}
+// GPU kernel family of a mode: the scalar modes run the register-lane DFMA
+// kernel, the rhocell-vector modes the warp-DFMA kernel, the tile-engine modes
+// the FP64 tensor-core (DMMA) kernel.
+inline int mode_kernel_family(AblationMode m) {
+    switch (m) {
+        case AblationMode::baseline:
+        case AblationMode::baseline_incrsort: return 0;
+        case AblationMode::rhocell_vector:
+        case AblationMode::rhocell_incrsort: return 1;
+        default: return 2;
+    }
+}
+
+enum class WorkloadKind { uniform_plasma, drift_gradient };
+struct WorkloadConfig {  // workload.hpp:16-44
+    GridSpec grid;
+    int ppc = 8;
+    WorkloadKind kind = WorkloadKind::uniform_plasma;
+    double thermal_speed = 0.01;
+    Vec3 drift_velocity{0.0, 0.0, 0.0};
+    std::uint64_t seed = 1;
+    int steps = 10;
+    double dt = 1.0;
+    double charge = 1.0;
+    ShapeOrder order = ShapeOrder::cic;
+    double speed_cap() const { return std::min(grid.dx, std::min(grid.dy, grid.dz)) / dt; }
+    picgpu_workload c() const {
+        return picgpu_workload{grid.c(), ppc, static_cast<int32_t>(kind), thermal_speed,
+                               {drift_velocity[0], drift_velocity[1], drift_velocity[2]}, seed, steps,
+                               static_cast<int32_t>(order), dt, charge};
+    }
+};
+
+struct StepMetrics {  // simulation.hpp:67-78
+    std::uint32_t step = 0;
+    double wall_s = 0.0;
+    double preproc_s = 0.0;
+    double compute_s = 0.0;
+    double sort_s = 0.0;
+    double reduce_s = 0.0;
+    double particles_per_second = 0.0;
+    double fraction_moved = 0.0;
+    std::uint32_t rebuilds = 0;
+    SortReason global_sort = SortReason::none;
+};
+
+struct RunResult {  // simulation.hpp:80-86
+    std::vector<StepMetrics> steps;
+    std::array<double, 3> checksum{0.0, 0.0, 0.0};
+    CurrentGrid final_grid;
+    ParticleSoA particles;
+    RankSortStats stats;
+};
+
+// run_simulation (simulation.hpp:92-176) on one GPU: per step, advance fused
+// with the mode's sort (incremental for the *-incrsort / fullopt modes, a full
+// stable counting sort of the store otherwise -- the GPU kernels always read
+// bins), deposition with the mode's kernel family, metrics from device event
+// times (sort_s includes the fused push; preproc_s and reduce_s are 0, the
+// staging and the node reduction live inside the kernels), then fullopt's
+// adaptive global-resort decision.  `initial` replaces make_workload (e.g. the
+// reference's own population, for bit-exact lockstep runs).
+inline RunResult run_simulation(const WorkloadConfig& cfg, AblationMode mode, const SortPolicy& policy = {},
+                                const GpmaConfig& gcfg = {}, int device = 0, const ParticleSoA* initial = nullptr) {
+    // SortPolicy::validate (sort_policy.hpp:20-28)
+    if (policy.min_sort_interval > policy.sort_interval)
+        throw std::invalid_argument("policy: min_sort_interval exceeds sort_interval");
+    if (!(policy.trigger_empty_ratio > 0.0 && policy.trigger_empty_ratio < 1.0) ||
+        !(policy.trigger_full_ratio > 0.0 && policy.trigger_full_ratio < 1.0))
+        throw std::invalid_argument("policy: slot-ratio triggers must lie in (0,1)");
+    if (!(policy.perf_degrad > 0.0 && policy.perf_degrad <= 1.0))
+        throw std::invalid_argument("policy: perf_degrad must lie in (0,1]");
+    RunResult out;
+    const GridSpec& g = cfg.grid;
+    Session sess(g, cfg.order, gcfg, device, /*timing=*/true);
+    sess.set_kernel(mode_kernel_family(mode));
+    if (initial)
+        sess.upload(*initial);
+    else
+        sess.make_workload(cfg.c());
+    const std::size_t n = sess.size();
+    const std::uint32_t flags = PICGPU_STEP_PUSH | PICGPU_STEP_CURRENT |
+                                (mode_incremental_sort(mode) ? PICGPU_STEP_SORT : PICGPU_STEP_RESORT);
+    std::array<double, PICGPU_NPHASES> prev = sess.phase_ms();
+    for (int step = 0; step < cfg.steps; ++step) {
+        StepMetrics m;
+        m.step = static_cast<std::uint32_t>(step);
+        const auto t0 = std::chrono::steady_clock::now();
+        const picgpu_step_stats st = sess.step(cfg.dt, flags);
+        const std::array<double, PICGPU_NPHASES> ph = sess.phase_ms();
+        m.sort_s = (ph[0] - prev[0] + ph[2] - prev[2]) * 1e-3;
+        m.compute_s = (ph[3] - prev[3] + ph[5] - prev[5]) * 1e-3;
+        prev = ph;
+        m.fraction_moved = n ? static_cast<double>(st.moved) / static_cast<double>(n) : 0.0;
+        m.rebuilds = st.rebuilt;
+        out.stats.total_inserts += st.inserts;
+        m.particles_per_second =
+            static_cast<double>(n) / std::max(m.preproc_s + m.compute_s + m.sort_s + m.reduce_s, 1e-12);
+        out.stats.perf_metric = m.particles_per_second;
+        out.stats.steps_since_sort += 1;
+        out.stats.cumulative_local_rebuilds += m.rebuilds;
+        if (mode_uses_gpma(mode)) out.stats.empty_slot_ratio = st.empty_slot_ratio;
+        if (mode == AblationMode::fullopt) {
+            if (out.stats.baseline_perf == 0.0) out.stats.baseline_perf = m.particles_per_second;
+            const SortReason reason = should_global_sort(out.stats, policy);
+            if (reason != SortReason::none) {
+                sess.step(cfg.dt, PICGPU_STEP_GLOBAL_SORT);  // global_sort, timed
+                const std::array<double, PICGPU_NPHASES> ph2 = sess.phase_ms();
+                m.sort_s += (ph2[2] - prev[2]) * 1e-3;
+                prev = ph2;
+                reset_counters(out.stats);
+                m.global_sort = reason;
+            }
+        }
+        m.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        out.steps.push_back(m);
+    }
+    out.final_grid = sess.current();
+    out.checksum = out.final_grid.component_sums();
+    out.particles = sess.particles();
+    return out;
+}
 
 }  // namespace picgpu

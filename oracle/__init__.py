@@ -179,6 +179,8 @@ class Reference:
         L.ref_deposit_scalar_mt.argtypes = [_p, C.c_int, C.c_int, _p, _p, _p]
         L.ref_deposit_density.argtypes = [_p, C.c_int, _p, _p]
         L.ref_deposit_tiled.argtypes = [_p, C.c_int, C.c_int, _p, _p, _p]
+        L.ref_make_workload.argtypes = [_p] * 9
+        L.ref_run_simulation.argtypes = [_p, C.c_char_p, _p, C.c_double, C.c_uint32] + [_p] * 15
         L.ref_deposit_tiled_opt.argtypes = [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p]
         L.ref_deposit_rhocell.argtypes = [_p, C.c_int, C.c_int, _p, _p, _p]
         L.ref_gpma_build.argtypes = [_p, _d, _u32]
@@ -202,6 +204,32 @@ class Reference:
             msg = self.L.ref_last_error().decode()
             raise {1: ValueError, 2: IndexError, 3: MemoryError, 4: RuntimeError,
                    5: ArithmeticError}.get(rc, RuntimeError)(msg)
+
+    def make_workload(self, wl):
+        """pic::make_workload; wl is a paper_2601_08277_b200.WorkloadConfig (same C layout)."""
+        n = wl.grid.nx * wl.grid.ny * wl.grid.nz * wl.ppc
+        out = {k: np.zeros(n) for k in ("x", "y", "z", "vx", "vy", "vz", "w")}
+        out["id"] = np.zeros(n, np.uint64)
+        self._check(self.L.ref_make_workload(C.byref(wl), *(_ptr(out[k]) for k in
+                                                            ("x", "y", "z", "vx", "vy", "vz", "w", "id"))))
+        return out
+
+    def run_simulation(self, wl, mode, policy, gap_ratio=0.25, min_gap=2):
+        """pic::run_simulation; policy is a paper_2601_08277_b200.SortPolicy (same C layout)."""
+        n = wl.grid.nx * wl.grid.ny * wl.grid.nz * wl.ppc
+        nc = wl.grid.nx * wl.grid.ny * wl.grid.nz
+        fm = np.zeros(max(wl.steps, 1))
+        rb = np.zeros(max(wl.steps, 1), np.uint32)
+        rs = np.zeros(max(wl.steps, 1), np.int32)
+        ck = np.zeros(3)
+        J = [np.zeros(nc) for _ in range(3)]
+        out = {k: np.zeros(n) for k in ("x", "y", "z", "vx", "vy", "vz", "w")}
+        out["id"] = np.zeros(n, np.uint64)
+        self._check(self.L.ref_run_simulation(C.byref(wl), mode.encode(), C.byref(policy), gap_ratio, min_gap,
+                                              _ptr(fm), _ptr(rb), _ptr(rs), _ptr(ck), *(_ptr(j) for j in J),
+                                              *(_ptr(out[k]) for k in ("x", "y", "z", "vx", "vy", "vz", "w", "id"))))
+        return dict(fraction_moved=fm[:wl.steps], rebuilds=rb[:wl.steps], reasons=rs[:wl.steps], checksum=ck,
+                    J=J, particles=out)
 
     def state(self, g, s, q):
         return RefState(self, g, s, q)

@@ -11,6 +11,7 @@
 #include <pic/deposit.hpp>
 #include <pic/gpma.hpp>
 #include <pic/rng.hpp>
+#include <pic/simulation.hpp>
 #include <pic/sort_policy.hpp>
 #include <pic/workload.hpp>
 
@@ -250,6 +251,63 @@ int main() {
             got_domain = true;
         }
         expect(got_domain, "displacement above the cap -> std::domain_error");
+    }
+
+    // --- run_simulation (simulation.hpp:92) in every mode, same population ---
+    {
+        pic::WorkloadConfig rc;
+        rc.grid = g;
+        rc.ppc = 4;
+        rc.thermal_speed = 0.2;
+        rc.seed = 5;
+        rc.steps = 6;
+        rc.dt = 0.5;
+        rc.charge = -1.0;
+        rc.order = pic::ShapeOrder::qsp;
+        picgpu::WorkloadConfig gc;
+        gc.grid = gg;
+        gc.ppc = rc.ppc;
+        gc.thermal_speed = rc.thermal_speed;
+        gc.seed = rc.seed;
+        gc.steps = rc.steps;
+        gc.dt = rc.dt;
+        gc.charge = rc.charge;
+        gc.order = picgpu::ShapeOrder::qsp;
+        pic::SortPolicy rp;
+        rp.perf_enable = false;  // deterministic decisions
+        rp.sort_interval = 3;
+        rp.min_sort_interval = 2;
+        picgpu::SortPolicy gp;
+        gp.perf_enable = false;
+        gp.sort_interval = 3;
+        gp.min_sort_interval = 2;
+        const picgpu::ParticleSoA init = to_gpu(pic::make_workload(rc));
+        for (pic::AblationMode m : pic::kAllModes) {
+            const pic::RunResult rr = pic::run_simulation(rc, m, rp);
+            const picgpu::RunResult gr =
+                picgpu::run_simulation(gc, picgpu::mode_from_string(pic::to_string(m)), gp, {}, 0, &init);
+            bool same_moved = rr.steps.size() == gr.steps.size(), same_sorts = same_moved;
+            for (std::size_t i = 0; same_moved && i < rr.steps.size(); ++i) {
+                same_moved = rr.steps[i].fraction_moved == gr.steps[i].fraction_moved;
+                same_sorts = same_sorts && static_cast<int>(rr.steps[i].global_sort) ==
+                                               static_cast<int>(gr.steps[i].global_sort);
+            }
+            std::map<std::uint64_t, std::size_t> at;
+            for (std::size_t p = 0; p < gr.particles.size(); ++p) at[gr.particles.id[p]] = p;
+            bool same_state = at.size() == rr.particles.size();
+            for (std::size_t p = 0; same_state && p < rr.particles.size(); ++p) {
+                const auto it = at.find(rr.particles.id[p]);
+                same_state = it != at.end() && gr.particles.x[it->second] == rr.particles.x[p] &&
+                             gr.particles.y[it->second] == rr.particles.y[p] &&
+                             gr.particles.z[it->second] == rr.particles.z[p];
+            }
+            const double e = peak_rel_err(gr.final_grid, rr.final_grid);
+            char msg[160];
+            std::snprintf(msg, sizeof msg, "run_simulation %s: moved %s, sorts %s, state %s, J err %.2e",
+                          pic::to_string(m), same_moved ? "same" : "DIFF", same_sorts ? "same" : "DIFF",
+                          same_state ? "same" : "DIFF", e);
+            expect(same_moved && same_sorts && same_state && e <= 1e-12, msg);
+        }
     }
 
     std::printf("%s (%d failures)\n", failures ? "DROP-IN PARITY FAILED" : "drop-in parity ok", failures);

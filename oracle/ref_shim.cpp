@@ -16,6 +16,7 @@
 #include <pic/deposit.hpp>
 #include <pic/gpma.hpp>
 #include <pic/rng.hpp>
+#include <pic/simulation.hpp>
 #include <pic/sort_policy.hpp>
 #include <pic/workload.hpp>
 
@@ -78,11 +79,83 @@ void copy_out(const std::vector<double>& v, double* out) {
     if (out) std::memcpy(out, v.data(), v.size() * sizeof(double));
 }
 
+struct RefWorkload {  // same layout as picgpu_workload
+    RefGrid grid;
+    int32_t ppc, kind;
+    double thermal_speed;
+    double drift[3];
+    uint64_t seed;
+    int32_t steps, order;
+    double dt, charge;
+};
+
+struct RefPolicy {  // same layout as picgpu_sort_policy
+    uint32_t sort_interval, min_sort_interval, trigger_rebuild_count, perf_enable;
+    double trigger_empty_ratio, trigger_full_ratio, perf_degrad;
+};
+
+pic::WorkloadConfig to_cfg(const RefWorkload* w) {
+    pic::WorkloadConfig c;
+    c.grid = to_spec(&w->grid);
+    c.ppc = w->ppc;
+    c.kind = w->kind ? pic::WorkloadKind::drift_gradient : pic::WorkloadKind::uniform_plasma;
+    c.thermal_speed = w->thermal_speed;
+    c.drift_velocity = {w->drift[0], w->drift[1], w->drift[2]};
+    c.seed = w->seed;
+    c.steps = w->steps;
+    c.dt = w->dt;
+    c.charge = w->charge;
+    c.order = to_order(w->order);
+    return c;
+}
+
+void soa_out(const pic::ParticleSoA& s, double* x, double* y, double* z, double* vx, double* vy, double* vz,
+             double* w, uint64_t* id) {
+    copy_out(s.x, x); copy_out(s.y, y); copy_out(s.z, z);
+    copy_out(s.vx, vx); copy_out(s.vy, vy); copy_out(s.vz, vz); copy_out(s.w, w);
+    if (id) std::memcpy(id, s.id.data(), s.id.size() * sizeof(uint64_t));
+}
+
 }  // namespace
 
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_make_workload(const RefWorkload* w, double* x, double* y, double* z, double* vx, double* vy, double* vz,
+                      double* wt, uint64_t* id) {
+    return guarded([&] { soa_out(pic::make_workload(to_cfg(w)), x, y, z, vx, vy, vz, wt, id); });
+}
+
+// run_simulation (simulation.hpp:92-176): per-step fraction moved, rebuilds and
+// global-sort reason, the checksum, the final grid and particles.
+int ref_run_simulation(const RefWorkload* w, const char* mode, const RefPolicy* p, double gap_ratio,
+                       uint32_t min_gap, double* fraction_moved, uint32_t* rebuilds, int* reasons, double* checksum,
+                       double* jx, double* jy, double* jz, double* x, double* y, double* z, double* vx, double* vy,
+                       double* vz, double* wt, uint64_t* id) {
+    return guarded([&] {
+        pic::SortPolicy pol;
+        pol.sort_interval = p->sort_interval;
+        pol.min_sort_interval = p->min_sort_interval;
+        pol.trigger_rebuild_count = p->trigger_rebuild_count;
+        pol.perf_enable = p->perf_enable != 0;
+        pol.trigger_empty_ratio = p->trigger_empty_ratio;
+        pol.trigger_full_ratio = p->trigger_full_ratio;
+        pol.perf_degrad = p->perf_degrad;
+        pic::GpmaConfig gc;
+        gc.gap_ratio = gap_ratio;
+        gc.min_gap = min_gap;
+        const pic::RunResult r = pic::run_simulation(to_cfg(w), pic::mode_from_string(mode), pol, gc);
+        for (std::size_t i = 0; i < r.steps.size(); ++i) {
+            fraction_moved[i] = r.steps[i].fraction_moved;
+            rebuilds[i] = r.steps[i].rebuilds;
+            reasons[i] = static_cast<int>(r.steps[i].global_sort);
+        }
+        for (int c = 0; c < 3; ++c) checksum[c] = r.checksum[c];
+        copy_out(r.final_grid.jx, jx); copy_out(r.final_grid.jy, jy); copy_out(r.final_grid.jz, jz);
+        soa_out(r.particles, x, y, z, vx, vy, vz, wt, id);
+    });
+}
 
 void* ref_create(const RefGrid* g, uint64_t n, const double* x, const double* y, const double* z,
                  const double* vx, const double* vy, const double* vz, const double* w,

@@ -35,7 +35,8 @@ CIC, TSC, QSP = 1, 2, 3
 
 OK, EINVAL, ERANGE, ELENGTH, ELOGIC, EDOMAIN, ECUDA, ENCCL, ENOMEM = range(9)
 
-STEP_PUSH, STEP_SORT, STEP_CURRENT, STEP_DENSITY, STEP_GLOBAL_SORT, STEP_NO_SYNC = 1, 2, 4, 8, 16, 32
+STEP_PUSH, STEP_SORT, STEP_CURRENT, STEP_DENSITY, STEP_GLOBAL_SORT, STEP_NO_SYNC, STEP_RESORT = 1, 2, 4, 8, 16, 32, 64
+KERNEL_LANE, KERNEL_VECTOR, KERNEL_MATRIX = 0, 1, 2
 STEP_DEFAULT = STEP_PUSH | STEP_SORT | STEP_CURRENT
 SESSION_TIMING = 1
 PHASES = ("push_sort", "reserved", "rebuild_or_global_sort", "deposit_current", "deposit_density", "zero_fields")
@@ -144,6 +145,24 @@ class TiledOptions:
         return (1 if self.gpma else 0) | (2 if self.residency else 0) | (4 if self.dual_tile else 0)
 
 
+class WorkloadConfig(C.Structure):
+    """picgpu_workload == pic::WorkloadConfig (workload.hpp:16-44)."""
+
+    _fields_ = [("grid", Grid), ("ppc", C.c_int32), ("kind", C.c_int32), ("thermal_speed", C.c_double),
+                ("drift", C.c_double * 3), ("seed", C.c_uint64), ("steps", C.c_int32), ("order", C.c_int32),
+                ("dt", C.c_double), ("charge", C.c_double)]
+
+    UNIFORM_PLASMA, DRIFT_GRADIENT = 0, 1
+
+    @classmethod
+    def make(cls, grid, ppc=8, kind=0, thermal_speed=0.01, drift=(0.0, 0.0, 0.0), seed=1, steps=10, dt=1.0,
+             charge=1.0, order=1):
+        return cls(grid, ppc, kind, thermal_speed, (C.c_double * 3)(*drift), seed, steps, order, dt, charge)
+
+    def speed_cap(self):
+        return min(self.grid.dx, self.grid.dy, self.grid.dz) / self.dt
+
+
 class SortPolicy(C.Structure):
     """pic::SortPolicy (sort_policy.hpp:12-30); defaults are Table 4's."""
 
@@ -222,6 +241,8 @@ def lib():
                                                                 C.POINTER(StageTimes), C.POINTER(KernelCounters)]
     L.picgpu_deposit_rhocell_vector.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, C.c_int, _P, _P, _P,
                                                                          C.POINTER(_D)]
+    L.picgpu_session_set_kernel.argtypes = [_P, C.c_int]
+    L.picgpu_session_make_workload.argtypes = [_P, C.POINTER(WorkloadConfig)]
     L.picgpu_slab_grid.argtypes = [G, C.c_int, C.c_int, C.c_int, G]
     L.picgpu_session_set_slab.argtypes = [_P, G, C.c_int, C.c_int, C.c_int]
     L.picgpu_session_step_begin.argtypes = [_P, _D, C.c_uint32, C.POINTER(_U64), C.POINTER(_U64)]
@@ -517,6 +538,14 @@ class Session:
         lib().picgpu_session_device_fields(self._h, C.byref(j), C.byref(r))
         return j.value, r.value
 
+    def set_kernel(self, family: int):
+        """J kernel family: KERNEL_LANE (default), KERNEL_VECTOR (warp DFMA), KERNEL_MATRIX (DMMA)."""
+        _check(lib().picgpu_session_set_kernel(self._h, family))
+
+    def make_workload(self, cfg: WorkloadConfig):
+        """Replace the particles by make_workload(cfg) generated on the device."""
+        _check(lib().picgpu_session_make_workload(self._h, C.byref(cfg)))
+
     def phase_times(self):
         ms = np.zeros(len(PHASES))
         launches = np.zeros(len(PHASES), np.uint64)
@@ -525,3 +554,127 @@ class Session:
 
     def reset_phase_times(self):
         lib().picgpu_session_reset_phase_times(self._h)
+
+
+# ---- the reference's harness loop (simulation.hpp:19-176) ----------------------
+
+MODES = ("baseline", "matrix-only", "hybrid-nosort", "hybrid-globalsort", "fullopt", "rhocell-vector",
+         "baseline-incrsort", "rhocell-incrsort")
+
+
+def mode_uses_gpma(mode: str) -> bool:
+    return mode in ("hybrid-globalsort", "fullopt", "baseline-incrsort", "rhocell-incrsort")
+
+
+def mode_incremental_sort(mode: str) -> bool:
+    return mode in ("fullopt", "baseline-incrsort", "rhocell-incrsort")
+
+
+def mode_kernel_family(mode: str) -> int:
+    """Scalar modes -> lane DFMA kernel, rhocell modes -> warp DFMA, tile-engine modes -> DMMA."""
+    if mode in ("baseline", "baseline-incrsort"):
+        return KERNEL_LANE
+    if mode in ("rhocell-vector", "rhocell-incrsort"):
+        return KERNEL_VECTOR
+    return KERNEL_MATRIX
+
+
+@dataclass
+class StepMetrics:  # simulation.hpp:67-78
+    step: int
+    wall_s: float = 0.0
+    preproc_s: float = 0.0
+    compute_s: float = 0.0
+    sort_s: float = 0.0
+    reduce_s: float = 0.0
+    particles_per_second: float = 0.0
+    fraction_moved: float = 0.0
+    rebuilds: int = 0
+    global_sort: str = "none"
+
+
+@dataclass
+class RunResult:  # simulation.hpp:80-86
+    steps: list
+    checksum: list
+    final_grid: CurrentGrid
+    particles: ParticleSoA
+    stats: RankSortStats
+
+
+def validate_policy(p: SortPolicy):  # sort_policy.hpp:20-28
+    if p.min_sort_interval > p.sort_interval:
+        raise InvalidArgument("policy: min_sort_interval exceeds sort_interval")
+    if not (0.0 < p.trigger_empty_ratio < 1.0 and 0.0 < p.trigger_full_ratio < 1.0):
+        raise InvalidArgument("policy: slot-ratio triggers must lie in (0,1)")
+    if not (0.0 < p.perf_degrad <= 1.0):
+        raise InvalidArgument("policy: perf_degrad must lie in (0,1]")
+
+
+def run_simulation(cfg: WorkloadConfig, mode: str, policy: SortPolicy | None = None, gap_ratio: float = 0.25,
+                   min_gap: int = 2, device: int = 0, initial=None) -> RunResult:
+    """run_simulation (simulation.hpp:92-176) on one GPU.
+
+    Per step: advance fused with the mode's sort (incremental for *-incrsort and
+    fullopt, a full stable counting sort of the store otherwise: the GPU kernels
+    always read bins), J with the mode's kernel family, metrics from device
+    event times (sort_s includes the fused push; preproc_s and reduce_s are 0),
+    then fullopt's adaptive global-resort decision.  `initial` (a ParticleSoA
+    or dict) replaces make_workload, e.g. the reference's own population.
+    """
+    import time
+
+    if mode not in MODES:
+        raise InvalidArgument(f"unknown mode: {mode}")
+    policy = policy or SortPolicy.defaults()
+    validate_policy(policy)
+    sess = Session(cfg.grid, cfg.order, gap_ratio, min_gap, device, timing=True)
+    try:
+        sess.set_kernel(mode_kernel_family(mode))
+        if initial is not None:
+            sess.upload(initial, q=cfg.charge)
+        else:
+            sess.make_workload(cfg)
+        n = sess.num_particles
+        flags = STEP_PUSH | STEP_CURRENT | (STEP_SORT if mode_incremental_sort(mode) else STEP_RESORT)
+        stats = RankSortStats()
+        prev = sess.phase_times()
+        steps = []
+        for step in range(cfg.steps):
+            t0 = time.perf_counter()
+            st = sess.step(cfg.dt, flags)
+            ph = sess.phase_times()
+            m = StepMetrics(step)
+            m.sort_s = (ph["push_sort"][0] - prev["push_sort"][0] + ph["rebuild_or_global_sort"][0]
+                        - prev["rebuild_or_global_sort"][0]) * 1e-3
+            m.compute_s = (ph["deposit_current"][0] - prev["deposit_current"][0] + ph["zero_fields"][0]
+                           - prev["zero_fields"][0]) * 1e-3
+            prev = ph
+            m.fraction_moved = st["moved"] / n if n else 0.0
+            m.rebuilds = int(st["rebuilt"])
+            stats.total_inserts += st["inserts"]
+            m.particles_per_second = n / max(m.preproc_s + m.compute_s + m.sort_s + m.reduce_s, 1e-12)
+            stats.perf_metric = m.particles_per_second
+            stats.steps_since_sort += 1
+            stats.cumulative_local_rebuilds += m.rebuilds
+            if mode_uses_gpma(mode):
+                stats.empty_slot_ratio = st["empty_slot_ratio"]
+            if mode == "fullopt":
+                if stats.baseline_perf == 0.0:
+                    stats.baseline_perf = m.particles_per_second
+                reason = should_global_sort(stats, policy)
+                if reason != "none":
+                    sess.step(cfg.dt, STEP_GLOBAL_SORT)  # global_sort, timed
+                    ph = sess.phase_times()
+                    m.sort_s += (ph["rebuild_or_global_sort"][0] - prev["rebuild_or_global_sort"][0]) * 1e-3
+                    prev = ph
+                    stats.steps_since_sort = 0  # reset_counters, sort_policy.hpp:75-79
+                    stats.cumulative_local_rebuilds = 0
+                    stats.baseline_perf = 0.0
+                    m.global_sort = reason
+            m.wall_s = time.perf_counter() - t0
+            steps.append(m)
+        grid = sess.current()
+        return RunResult(steps, grid.component_sums(), grid, sess.particles(), stats)
+    finally:
+        sess.close()

@@ -197,6 +197,7 @@ struct picgpu_session {
     cudaEvent_t ev[8] = {};
     double phase_ms[PICGPU_NPHASES] = {};
     uint64_t phase_launches[PICGPU_NPHASES] = {};
+    int kernel = -1;  // JKernel family; -1: library default
     // x-slab decomposition (picgpu_session_set_slab)
     bool slab = false;
     int ghost = 0;
@@ -614,7 +615,7 @@ static void enqueue_deposits(picgpu_session* s, uint32_t flags, uint64_t* lj, ui
         if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[3], st));
         if (bs.n)
             launch_deposit_current(s->order, g, bs.A.soa(), bs.d_off(), bs.d_cnt(), s->q, s->J.as<double>(),
-                                   bs.num_sms, st);
+                                   bs.num_sms, st, s->kernel);
         if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[4], st));
         *lj = g_launches.load() - l0;
     }
@@ -642,13 +643,32 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
         BinStore& bs = s->store;
         const cudaStream_t st = s->st;
         if (s->slab) throw Status{PICGPU_ELOGIC, "session_step: slab sessions step with step_begin / step_end"};
-        if ((flags & PICGPU_STEP_PUSH) && !(flags & PICGPU_STEP_SORT))
-            throw Status{PICGPU_EINVAL, "session_step: PUSH requires SORT (push and move detection are fused)"};
+        if ((flags & PICGPU_STEP_SORT) && (flags & PICGPU_STEP_RESORT))
+            throw Status{PICGPU_EINVAL, "session_step: SORT and RESORT are exclusive"};
+        if ((flags & PICGPU_STEP_PUSH) && !(flags & (PICGPU_STEP_SORT | PICGPU_STEP_RESORT)))
+            throw Status{PICGPU_EINVAL, "session_step: PUSH requires SORT or RESORT (the push is fused with them)"};
         if ((flags & PICGPU_STEP_DENSITY)) check_density_grid(bs.hg, s->order);
         picgpu_step_stats stats{};
         const uint64_t rebuilds0 = bs.rebuilds;
         const bool T = s->timing;
         uint64_t lj = 0, lr = 0;
+        if (flags & PICGPU_STEP_RESORT) {
+            const double cap2 = (flags & PICGPU_STEP_PUSH) ? cap2_of(bs.hg, dt) : 0.0;
+            const uint64_t l0 = g_launches.load();
+            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
+            StepCounters c{};
+            bs.push_and_resort((flags & PICGPU_STEP_PUSH) != 0, dt, cap2, c);
+            if (c.err == PICGPU_EDOMAIN)
+                throw Status{c.err, "advance: particle displacement exceeds the single-cell cap"};
+            if (c.err) throw Status{c.err, "cell_of: non-finite particle position"};
+            stats.moved = c.moved;
+            stats.global_sorted = 1;
+            if (T) {
+                PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
+                PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[1]));
+                accumulate_phase(s, 2, 0, 1, g_launches.load() - l0);
+            }
+        }
         if (flags & PICGPU_STEP_SORT) {
             const double cap2 = (flags & PICGPU_STEP_PUSH) ? cap2_of(bs.hg, dt) : 0.0;
             const uint64_t l0 = g_launches.load();
@@ -698,6 +718,45 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
         stats.num_particles = bs.n;
         stats.empty_slot_ratio = bs.capacity ? (double)(bs.capacity - bs.n) / (double)bs.capacity : 1.0;
         if (out) *out = stats;
+    });
+}
+
+int picgpu_session_set_kernel(picgpu_session* s, int family) {
+    return guard([&] {
+        if (family < -1 || family > 2) throw Status{PICGPU_EINVAL, "set_kernel: family must be 0, 1 or 2"};
+        s->kernel = family;
+    });
+}
+
+int picgpu_session_make_workload(picgpu_session* s, const picgpu_workload* cfg) {
+    return guard([&] {
+        set_device(s);
+        BinStore& bs = s->store;
+        if (s->slab) throw Status{PICGPU_ELOGIC, "make_workload: not available on a slab session"};
+        const picgpu_grid& h = bs.hg;
+        const picgpu_grid& c = cfg->grid;
+        if (h.nx != c.nx || h.ny != c.ny || h.nz != c.nz || h.dx != c.dx || h.dy != c.dy || h.dz != c.dz ||
+            h.ox != c.ox || h.oy != c.oy || h.oz != c.oz)
+            throw Status{PICGPU_EINVAL, "make_workload: grid differs from the session's"};
+        // WorkloadConfig::validate (workload.hpp:29-40)
+        if (cfg->ppc < 1) throw Status{PICGPU_EINVAL, "workload: ppc must be >= 1"};
+        if (!(cfg->dt > 0.0)) throw Status{PICGPU_EINVAL, "workload: dt must be positive"};
+        if (cfg->steps < 0) throw Status{PICGPU_EINVAL, "workload: steps must be >= 0"};
+        if (cfg->thermal_speed < 0.0) throw Status{PICGPU_EINVAL, "workload: thermal_speed must be >= 0"};
+        check_order(cfg->order);
+        const int W = cfg->order == 1 ? 2 : cfg->order == 2 ? 3 : 4;
+        if (c.nx < W || c.ny < W || c.nz < W)
+            throw Status{PICGPU_EINVAL, "workload: grid smaller than the shape stencil"};
+        const double cap = std::min(c.dx, std::min(c.dy, c.dz)) / cfg->dt;  // speed_cap
+        double amp[3] = {cfg->drift[0], cfg->drift[1], cfg->drift[2]};
+        const int drift = cfg->kind == PICGPU_WORKLOAD_DRIFT_GRADIENT;
+        if (drift && amp[0] == 0.0 && amp[1] == 0.0 && amp[2] == 0.0) amp[0] = 0.5 * cap;
+        const uint64_t n = (uint64_t)bs.g.ncells * (uint64_t)cfg->ppc;
+        bs.B.ensure(n);
+        launch_make_workload(bs.g, cfg->ppc, cfg->thermal_speed, drift, amp, cap, cfg->seed, bs.B.soa(), s->st);
+        bs.full_sort_from_B(n);
+        s->q = cfg->charge;
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
     });
 }
 

@@ -267,7 +267,9 @@ __device__ __forceinline__ double axis_floor(double x, double o, double h, doubl
 #define PICGPU_PUSH_CONDLOAD 0
 #endif
 
-template <bool PUSH, int UNR, bool P2>
+// RECORD = false: push and count the moved particles only (the store is
+// re-sorted from scratch afterwards; no flags, movers or departures).
+template <bool PUSH, int UNR, bool P2, bool RECORD = true>
 __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, const Soa A, uint64_t slots, uint8_t* __restrict__ mflag,
                                               double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
                                               uint32_t mcap, uint32_t* __restrict__ dep, StepCounters* ctr,
@@ -336,6 +338,10 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
                     moved = nc[u] != before[u];
                 }
             }
+        }
+        if (!RECORD) {
+            local_moved += moved ? 1u : 0u;
+            continue;
         }
         mflag[s] = moved ? 1 : 0;
         if (moved) {
@@ -673,6 +679,48 @@ __global__ void k_generate(const GridD g, int ppc, double u_th, uint64_t seed, c
     out.id[p] = pid;
 }
 
+// make_workload (workload.hpp:75-125): particle pid = cell-major (x fastest),
+// then a px*py*pz sub-lattice in the cell (x fastest); Maxwellian velocities,
+// optional shear drift, truncation at the displacement cap; W = 1.
+__global__ void k_make_workload(const GridD g, int ppc, int px, int py, int pz, double vth, int drift, double ax,
+                                double ay, double az, double cap, uint64_t seed, const Soa out, uint64_t n) {
+    const uint64_t pid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pid >= n) return;
+    const uint64_t cell = pid / (uint64_t)ppc;
+    const int r = (int)(pid % (uint64_t)ppc);
+    const int a = r % px, b = (r / px) % py, c = r / (px * py);
+    const int i = (int)(cell % (uint64_t)g.nx);
+    const int j = (int)((cell / (uint64_t)g.nx) % (uint64_t)g.ny);
+    const int k = (int)(cell / ((uint64_t)g.nx * (uint64_t)g.ny));
+    const double X = __dadd_rn(g.ox, __dmul_rn(__dadd_rn((double)i, __ddiv_rn(__dadd_rn((double)a, 0.5), (double)px)), g.dx));
+    const double Y = __dadd_rn(g.oy, __dmul_rn(__dadd_rn((double)j, __ddiv_rn(__dadd_rn((double)b, 0.5), (double)py)), g.dy));
+    const double Z = __dadd_rn(g.oz, __dmul_rn(__dadd_rn((double)k, __ddiv_rn(__dadd_rn((double)c, 0.5), (double)pz)), g.dz));
+    out.x[pid] = X;
+    out.y[pid] = Y;
+    out.z[pid] = Z;
+    double VX = __dmul_rn(vth, gaussian(seed, pid, 0));
+    double VY = __dmul_rn(vth, gaussian(seed, pid, 1));
+    double VZ = __dmul_rn(vth, gaussian(seed, pid, 2));
+    if (drift) {
+        const double tau = 2.0 * 3.141592653589793;
+        VX = __dadd_rn(VX, __dmul_rn(ax, cos(__ddiv_rn(__dmul_rn(tau, __dsub_rn(Y, g.oy)), g.Ly))));
+        VY = __dadd_rn(VY, __dmul_rn(ay, cos(__ddiv_rn(__dmul_rn(tau, __dsub_rn(Z, g.oz)), g.Lz))));
+        VZ = __dadd_rn(VZ, __dmul_rn(az, cos(__ddiv_rn(__dmul_rn(tau, __dsub_rn(X, g.ox)), g.Lx))));
+    }
+    const double speed = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(VX, VX), __dmul_rn(VY, VY)), __dmul_rn(VZ, VZ)));
+    if (speed > cap) {
+        const double sc = __dmul_rn(__ddiv_rn(cap, speed), 1.0 - 0x1.0p-40);
+        VX = __dmul_rn(VX, sc);
+        VY = __dmul_rn(VY, sc);
+        VZ = __dmul_rn(VZ, sc);
+    }
+    out.vx[pid] = VX;
+    out.vy[pid] = VY;
+    out.vz[pid] = VZ;
+    out.w[pid] = 1.0;
+    out.id[pid] = pid;
+}
+
 // ---------------------------------------------------------------------------
 // host launchers
 
@@ -717,6 +765,35 @@ void launch_add_planes(double* F, int comps, int nx, int ny, int nz, int p0, int
     if (!total) return;
     k_add_planes<<<(int)std::min<long long>(div_up(total, 256), 148 * 8), 256, 0, st>>>(F, comps, nx, ny, nz, p0, np,
                                                                                        in);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_make_workload(const GridD& g, int ppc, double vth, int drift, const double amp[3], double cap,
+                          uint64_t seed, Soa out, cudaStream_t st) {
+    // detail::sublattice_dims (workload.hpp:50-65): px >= py >= pz, px*py*pz == ppc
+    int cb = 1;
+    while ((cb + 1) * (cb + 1) * (cb + 1) <= ppc) ++cb;
+    int pz = 1;
+    for (int d = cb; d >= 1; --d)
+        if (ppc % d == 0) {
+            pz = d;
+            break;
+        }
+    const int rem = ppc / pz;
+    int sq = 1;
+    while ((sq + 1) * (sq + 1) <= rem) ++sq;
+    int py = 1;
+    for (int d = sq; d >= 1; --d)
+        if (rem % d == 0) {
+            py = d;
+            break;
+        }
+    const int px = rem / py;
+    const uint64_t n = (uint64_t)g.ncells * (uint64_t)ppc;
+    if (!n) return;
+    k_make_workload<<<div_up((long long)n, 256), 256, 0, st>>>(g, ppc, px, py, pz, vth, drift, amp[0], amp[1], amp[2],
+                                                              cap, seed, out, n);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
@@ -974,6 +1051,34 @@ void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
         return;
     }
     enqueue_migrate();
+}
+
+void BinStore::push_and_resort(bool push, double dt, double cap2, StepCounters& out) {
+    const size_t nc = g.ncells;
+    StepCounters* ctr = counters.as<StepCounters>();
+    PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
+    if (nc && n && push) {
+        constexpr int UNR = PICGPU_PUSH_UNR;
+        const int blocks = (int)((capacity + 256 * UNR - 1) / (256 * UNR));
+        const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
+        auto* kern = p2 ? k_push<true, UNR, true, false> : k_push<true, UNR, false, false>;
+        kern<<<blocks, 256, 0, st>>>(g, A.soa(), capacity, mflag.as<uint8_t>(), dt, cap2, M.soa(),
+                                     mcell.as<uint32_t>(), (uint32_t)mcap, dep.as<uint32_t>(), ctr,
+                                     lrec.as<double>(), (uint32_t)lcap);
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+    }
+    PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, ctr, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
+    PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    out = *hcounters;
+    if (out.err) return;
+    // global_sort (sort_policy.hpp:83): stable counting sort of the whole
+    // store in storage order, fresh slack
+    compact_to_B();
+    unsigned int h32 = 0;
+    PICGPU_CUDA_TRY(cudaMemcpyAsync(&h32, off2.as<uint32_t>() + nc, 4, cudaMemcpyDeviceToHost, st));
+    PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    full_sort_from_B(h32);
 }
 
 bool BinStore::finish_incremental(StepCounters& out) {

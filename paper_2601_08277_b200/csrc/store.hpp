@@ -110,6 +110,9 @@ struct BinStore {
     // re-sort.  Returns true when it rebuilt (fields deposited since the
     // enqueue must then be recomputed).
     bool finish_incremental(StepCounters& out);
+    // Push (optional) with only the moved count, then a full stable counting
+    // sort of the store (PICGPU_STEP_RESORT).  Synchronous.
+    void push_and_resort(bool push, double dt, double cap2, StepCounters& out);
 
     uint32_t* d_off() const { return off.as<uint32_t>(); }
     uint32_t* d_cnt() const { return cnt.as<uint32_t>(); }
