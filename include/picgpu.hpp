@@ -23,6 +23,9 @@
 #pragma once
 
 #include <array>
+#include <cstring>
+#include <cstdlib>
+#include <cstdio>
 #include <chrono>
 #include <string_view>
 #include <cstdint>
@@ -505,6 +508,111 @@ inline RunResult run_simulation(const WorkloadConfig& cfg, AblationMode mode, co
     out.checksum = out.final_grid.component_sums();
     out.particles = sess.particles();
     return out;
+}
+
+// ---- reports (report.hpp:23-103): the reference's CSV / JSON schema ----------
+
+inline const char* to_string(SortReason r) {  // sort_policy.hpp:48-56
+    switch (r) {
+        case SortReason::interval: return "interval";
+        case SortReason::rebuilds: return "rebuilds";
+        case SortReason::slot_ratio: return "slot_ratio";
+        case SortReason::perf_degradation: return "perf_degradation";
+        default: return "none";
+    }
+}
+
+namespace detail {
+inline std::string fmt_double(double v) {
+    char buf[32];
+    std::snprintf(buf, sizeof(buf), "%.17g", v);
+    return buf;
+}
+struct MetricsSummary {
+    double wall = 0, preproc = 0, compute = 0, sort = 0, reduce = 0;
+    double mean_pps = 0, mean_fraction = 0;
+    std::uint64_t rebuilds = 0, global_sorts = 0;
+};
+inline MetricsSummary summarize(std::span<const StepMetrics> steps) {
+    MetricsSummary s;
+    for (const StepMetrics& m : steps) {
+        s.wall += m.wall_s;
+        s.preproc += m.preproc_s;
+        s.compute += m.compute_s;
+        s.sort += m.sort_s;
+        s.reduce += m.reduce_s;
+        s.mean_pps += m.particles_per_second;
+        s.mean_fraction += m.fraction_moved;
+        s.rebuilds += m.rebuilds;
+        if (m.global_sort != SortReason::none) ++s.global_sorts;
+    }
+    if (!steps.empty()) {
+        s.mean_pps /= static_cast<double>(steps.size());
+        s.mean_fraction /= static_cast<double>(steps.size());
+    }
+    return s;
+}
+// Shortest round-trip double, as nlohmann::json prints it.
+inline std::string json_double(double v) {
+    char buf[32];
+    for (int prec = 1; prec <= 17; ++prec) {
+        std::snprintf(buf, sizeof(buf), "%.*g", prec, v);
+        if (std::strtod(buf, nullptr) == v) break;
+    }
+    std::string s = buf;
+    if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+    return s;
+}
+}  // namespace detail
+
+inline constexpr const char* kCsvHeader =
+    "step,wall_s,preproc_s,compute_s,sort_s,reduce_s,pps,fraction_moved,rebuilds,global_sort_reason";
+
+inline std::string report_csv(std::span<const StepMetrics> steps) {
+    using detail::fmt_double;
+    std::string out = kCsvHeader;
+    out += '\n';
+    if (steps.empty()) return out;
+    for (const StepMetrics& m : steps)
+        out += std::to_string(m.step) + ',' + fmt_double(m.wall_s) + ',' + fmt_double(m.preproc_s) + ',' +
+               fmt_double(m.compute_s) + ',' + fmt_double(m.sort_s) + ',' + fmt_double(m.reduce_s) + ',' +
+               fmt_double(m.particles_per_second) + ',' + fmt_double(m.fraction_moved) + ',' +
+               std::to_string(m.rebuilds) + ',' + to_string(m.global_sort) + '\n';
+    const auto s = detail::summarize(steps);
+    out += "summary," + fmt_double(s.wall) + ',' + fmt_double(s.preproc) + ',' + fmt_double(s.compute) + ',' +
+           fmt_double(s.sort) + ',' + fmt_double(s.reduce) + ',' + fmt_double(s.mean_pps) + ',' +
+           fmt_double(s.mean_fraction) + ',' + std::to_string(s.rebuilds) + ',' + std::to_string(s.global_sorts) +
+           '\n';
+    return out;
+}
+
+// report_json's records, serialised like nlohmann::json::dump(): keys sorted,
+// no whitespace (the reference returns the json object; json.hpp is not a
+// dependency here).
+inline std::string report_json(std::span<const StepMetrics> steps) {
+    using detail::json_double;
+    std::string out = "{";
+    if (!steps.empty()) {
+        const auto s = detail::summarize(steps);
+        out += "\"steps\":[";
+        for (std::size_t i = 0; i < steps.size(); ++i) {
+            const StepMetrics& m = steps[i];
+            out += std::string(i ? "," : "") + "{\"compute_s\":" + json_double(m.compute_s) +
+                   ",\"fraction_moved\":" + json_double(m.fraction_moved) + ",\"global_sort_reason\":\"" +
+                   to_string(m.global_sort) + "\",\"pps\":" + json_double(m.particles_per_second) +
+                   ",\"preproc_s\":" + json_double(m.preproc_s) + ",\"rebuilds\":" + std::to_string(m.rebuilds) +
+                   ",\"reduce_s\":" + json_double(m.reduce_s) + ",\"sort_s\":" + json_double(m.sort_s) +
+                   ",\"step\":" + std::to_string(m.step) + ",\"wall_s\":" + json_double(m.wall_s) + "}";
+        }
+        out += "],\"summary\":{\"compute_s\":" + json_double(s.compute) + ",\"global_sorts\":" +
+               std::to_string(s.global_sorts) + ",\"mean_fraction_moved\":" + json_double(s.mean_fraction) +
+               ",\"mean_pps\":" + json_double(s.mean_pps) + ",\"preproc_s\":" + json_double(s.preproc) +
+               ",\"rebuilds\":" + std::to_string(s.rebuilds) + ",\"reduce_s\":" + json_double(s.reduce) +
+               ",\"sort_s\":" + json_double(s.sort) + ",\"wall_s\":" + json_double(s.wall) + "}";
+    } else {
+        out += "\"steps\":[]";
+    }
+    return out + "}";
 }
 
 }  // namespace picgpu
