@@ -4,7 +4,7 @@
 Workload (N=1): BASELINE configs[1] ("C2"): 128^3 cells, 16 particles/cell,
 order 3 (QSP), Maxwellian u_th = 0.01c, dt = 0.5, seeded synthetic plasma
 (SURVEY 8(d) generator, generated in HBM).  One STEP = the reference's step
-(simulation.hpp:753-829): bit-exact push -> incremental cell sort (bins with
+(simulation.hpp:92-176): bit-exact push -> incremental cell sort (bins with
 slack, migration) -> current deposition J.  Inputs stay resident in HBM.
 
 value  = particles * steps * n_gpus / (max over ranks of the device time of K steps)

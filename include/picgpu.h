@@ -13,7 +13,7 @@
  *   picgpu_counting_sort     <- pic::gpma_build's counting sort (perm/starts/counts) gpma.hpp:379-394
  *   picgpu_advance           <- pic::advance                 workload.hpp:139-155
  *   picgpu_cell_of           <- pic::cell_of                 grid.hpp:106-113
- *   picgpu_session_*         <- the run_simulation step loop simulation.hpp:753-829 with a
+ *   picgpu_session_*         <- the run_simulation step loop simulation.hpp:92-176 with a
  *                               device-resident pic::Gpma (gpma.hpp:52-371): gpma_build,
  *                               detect_moves + apply_pending_moves, rebuild, global_sort
  *                               (sort_policy.hpp:83), deposit_scalar / deposit_density.
@@ -264,9 +264,10 @@ PICGPU_API int picgpu_session_phase_times(picgpu_session* s, double* ms, uint64_
 PICGPU_API int picgpu_session_reset_phase_times(picgpu_session* s);
 
 /* ---- x-slab decomposition over ranks -----------------------
- * The reference runs one process over the whole periodic box and tiles it
- * across OpenMP threads (simulation.hpp:753-829, TileDecomposition
- * SPEC.md:505-513).  Here each rank (one process per GPU) owns the global
+ * The reference runs one single-threaded process over the whole periodic box
+ * (simulation.hpp:92-176) and has no domain decomposition (SPEC.md:507 only
+ * allows distinct Gpma tiles to run concurrently).  Here each rank (one
+ * process per GPU) owns the global
  * x-cells [x0, x1) of `global` and runs one session on its slab grid: the
  * owned cells plus `ghost` (>= 2, the QSP stencil reach) guard cells on each
  * side.  Positions stay in global coordinates and wrap on the global box, so

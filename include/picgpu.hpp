@@ -15,7 +15,7 @@
 //   GpmaConfig, gpma_build (perm + bins)         gpma.hpp:22-26, :379-402
 //   SortPolicy, RankSortStats, SortReason,
 //   should_global_sort, reset_counters           sort_policy.hpp:12-79
-//   Session: device-resident store + step loop   simulation.hpp:753-829
+//   Session: device-resident store + step loop   simulation.hpp:92-176
 // Status codes map back onto the reference's exceptions: EINVAL ->
 // std::invalid_argument, ERANGE -> std::out_of_range, ELENGTH ->
 // std::length_error, ELOGIC -> std::logic_error, EDOMAIN -> std::domain_error,

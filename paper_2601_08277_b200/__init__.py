@@ -446,7 +446,7 @@ class Session:
     """Device-resident particles in cell bins with slack + deposition fields.
 
     One step = [advance] -> [incremental sort] -> [deposit J] -> [deposit rho]
-    -> [global sort], the reference's run_simulation order (simulation.hpp:753-829).
+    -> [global sort], the reference's run_simulation order (simulation.hpp:92-176).
     """
 
     def __init__(self, grid: Grid, order: int = QSP, gap_ratio: float = 0.25, min_gap: int = 2, device: int = 0,

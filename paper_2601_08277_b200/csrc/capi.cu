@@ -1,6 +1,6 @@
 // capi.cu -- the C ABI (include/picgpu.h): stateless drop-ins for the
 // reference's deposition / sort / push functions and the device-resident
-// session that runs the reference's step loop (simulation.hpp:753-829) on HBM.
+// session that runs the reference's step loop (simulation.hpp:92-176) on HBM.
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -632,7 +632,7 @@ static void enqueue_deposits(picgpu_session* s, uint32_t flags, uint64_t* lj, ui
     }
 }
 
-// One step of the reference loop (simulation.hpp:753-829), device-resident:
+// One step of the reference loop (simulation.hpp:92-176), device-resident:
 // [push + incremental sort] -> [J] -> [rho] -> [global sort].  The sorter's
 // counters are read once after the sort kernels (one host wait per step):
 // when an arrival found no slack even after borrowing, the bins are rebuilt

@@ -1,8 +1,9 @@
 """x-slab decomposition of the periodic box over ranks.
 
-The reference runs one process over the whole box and splits the work over
-OpenMP tiles (run_simulation, proj/include/pic/simulation.hpp:753-829; the
-TileDecomposition of SPEC.md:505-513).  Here one process drives one GPU and
+The reference runs one single-threaded process over the whole box
+(run_simulation, proj/include/pic/simulation.hpp:92-176; its concurrency model
+only allows distinct Gpma tiles to be processed concurrently, and
+it has no domain decomposition).  Here one process drives one GPU and
 owns the global x-cells [x0, x1) (`slab_range`, a balanced contiguous split;
 SURVEY.md 8(e)); the slab's session grid is the owned cells plus `ghost` guard
 cells on each side.  One step:
