@@ -442,6 +442,247 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Orders 2 and 3, "lane" kernel v3 (default): the same decomposition as
+// deposit_current_kernel (8x4 pencils per CTA, lane = jy, 48 accumulators per
+// lane), with the per-z-step overheads taken out:
+//  * the z loop is unrolled by W = 4 and the window slides by static register
+//    rotation (logical plane kz lives in physical slot (kz + R) & 3 at step R),
+//    so no accumulator is moved when a plane is emitted;
+//  * padding slots of a chunk run the prologue branch-free on a zero-weight
+//    particle at the cell origin (finite weights, zero contribution);
+//  * the gather's node list (plane offset, which of the W*W pencil offsets
+//    contribute, interior flag) is computed once per CTA, not per plane.
+template <int ORDER>
+__device__ __forceinline__ double frac_sel(double x, double origin, double spacing, double inv, int pow2, int n,
+                                           int ci, bool valid) {
+    const double u = (x - origin) * inv;
+    double f = u - (double)ci;
+    if (valid && !(f >= -0.5 && f <= 1.5)) {
+        double fr;
+        locate_axis(x, origin, spacing, inv, pow2, n, fr);
+        f = fr;
+    }
+    return valid ? f : 0.0;
+}
+
+template <int ORDER>
+__device__ __forceinline__ void particle_window_sel(const GridD& g, const PData& d, double q, bool valid, int ci,
+                                                    int cj, int ck, double (&a)[3][4], double (&sy)[4],
+                                                    double (&sz)[4]) {
+    const double qw = valid ? q * d.w : 0.0;
+    const double wq0 = qw * d.vx, wq1 = qw * d.vy, wq2 = qw * d.vz;
+    const double fx = frac_sel<ORDER>(d.x, g.gox, g.dx, g.inv_dx, g.pow2x, g.gnx, ci + g.sx_shift, valid);
+    const double fy = frac_sel<ORDER>(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, cj, valid);
+    const double fz = frac_sel<ORDER>(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, ck, valid);
+    double sx[4];
+    weights_fast<ORDER>(fx, sx);
+    weights_fast<ORDER>(fy, sy);
+    weights_fast<ORDER>(fz, sz);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        a[0][t] = (valid ? wq0 : 0.0) * sx[t];
+        a[1][t] = (valid ? wq1 : 0.0) * sx[t];
+        a[2][t] = (valid ? wq2 : 0.0) * sx[t];
+    }
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
+    deposit_current_kernel_v3(const GridD g, const CSoa p, const uint32_t* __restrict__ off,
+                              const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
+                              double* __restrict__ jy, double* __restrict__ jz, const int zlen) {
+    using C = JCfg<ORDER>;
+    using L = JLayout<ORDER>;
+    constexpr int W = L::W, OFF = Shape<ORDER>::OFF, NJ = L::NJ;
+    constexpr int G = C::G, PX = C::PX, PY = C::PY, CH = C::CH;
+    constexpr int FX = PX + W - 1, FY = PY + W - 1;
+    constexpr int NODES = 3 * FX * FY;
+    constexpr int NIT = (NODES + L::NT - 1) / L::NT;
+    static_assert(W == 4 && G > 1, "v3: 4-tap orders only");
+
+    extern __shared__ __align__(16) double smem[];
+    double* patch = smem;                 // [2][W(jy)][W(ix)][3][PSTRIDE]
+    double* stage = smem + 2 * L::PATCH;  // [NF][CH][SS]
+
+    const int tid = threadIdx.x;
+    const int grp = tid / G, lg = tid % G;
+    const int px = grp % PX, py = grp / PX;
+    const int i0 = blockIdx.x * PX, j0 = blockIdx.y * PY;
+    const int k0 = blockIdx.z * zlen;
+    const int k1 = min(k0 + zlen, g.nz);
+    const int i = i0 + px, j = j0 + py;
+    const bool pv = (i < g.nx) && (j < g.ny);
+    const int pxv = min(PX, g.nx - i0), pyv = min(PY, g.ny - j0);
+    const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
+    const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
+    const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
+
+    // gather plan of this thread's nodes (constant over z)
+    int gn_base[NIT], gn_node[NIT];
+    unsigned gn_mask[NIT];
+    bool gn_inner[NIT];
+#pragma unroll
+    for (int t = 0; t < NIT; ++t) {
+        const int it = tid + t * L::NT;
+        gn_mask[t] = 0u;
+        gn_base[t] = 0;
+        gn_node[t] = 0;
+        gn_inner[t] = false;
+        if (it < NODES) {
+            const int c = it / (FX * FY);
+            const int r = it - c * (FX * FY);
+            const int uy = r / FX, ux = r - uy * FX;
+            if (ux < pxv + W - 1 && uy < pyv + W - 1) {
+#pragma unroll
+                for (int dy = 0; dy < W; ++dy)
+#pragma unroll
+                    for (int dx = 0; dx < W; ++dx) {
+                        const int qy = uy - dy, qx = ux - dx;
+                        if (qy >= 0 && qy < pyv && qx >= 0 && qx < pxv) gn_mask[t] |= 1u << (dy * W + dx);
+                    }
+                // patch offset of pencil (0,0)'s contribution, component in the top bits
+                gn_base[t] = (c << 28) | (c * L::PSTRIDE + uy * PX + ux);
+                const int X = wrap_index(i0 + OFF + ux, g.nx);
+                const int Y = wrap_index(j0 + OFF + uy, g.ny);
+                gn_node[t] = X + g.nx * Y;
+                gn_inner[t] = !alias_xy && ux >= W - 1 && ux <= pxv - 1 && uy >= W - 1 && uy <= pyv - 1;
+            }
+        }
+    }
+
+    double acc[W][NJ][W][3];
+#pragma unroll
+    for (int kz = 0; kz < W; ++kz)
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+            for (int ix = 0; ix < W; ++ix)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[kz][jj][ix][c] = 0.0;
+
+    uint32_t c_off = 0;
+    int n_c = 0;
+    if (pv && k0 < k1) {
+        c_off = off[col + plane_cells * k0];
+        n_c = (int)cnt[col + plane_cells * k0];
+    }
+    PData nxt{};
+    if (lg < n_c) load_particle(p, c_off + lg, nxt);
+
+    int buf = 0;
+    const int kend = k1 + W - 1;
+    auto zstep = [&](auto Rc, const int k) {
+        constexpr int R = decltype(Rc)::value;
+        if (k < k1) {
+            uint32_t n_off = 0;
+            int n_n = 0;
+            if (pv && k + 1 < k1) {
+                n_off = off[col + plane_cells * (k + 1)];
+                n_n = (int)cnt[col + plane_cells * (k + 1)];
+            }
+            const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
+            if (m == 0 && lg < n_n) load_particle(p, n_off + lg, nxt);  // empty cells: still prefetch
+            for (int base = 0; base < m; base += CH) {
+                {
+                    const PData cur = nxt;
+                    const bool valid = base + lg < n_c;
+                    if (base + CH < m) {
+                        if (base + CH + lg < n_c) load_particle(p, c_off + base + CH + lg, nxt);
+                    } else if (lg < n_n) {
+                        load_particle(p, n_off + lg, nxt);
+                    }
+                    double a[3][W], sy[W], sz[W];
+                    particle_window_sel<ORDER>(g, cur, q, valid, i, j, k, a, sy, sz);
+                    double* rec = stage + lg * L::SS + grp;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+#pragma unroll
+                        for (int t = 0; t < W; ++t) rec[(c * W + t) * L::FSS] = a[c][t];
+#pragma unroll
+                    for (int t = 0; t < W; ++t) {
+                        rec[(3 * W + t) * L::FSS] = sy[t];
+                        rec[(4 * W + t) * L::FSS] = sz[t];
+                    }
+                }
+                __syncwarp();
+                const int nn = min(CH, m - base);
+                for (int jj0 = 0; jj0 < nn; ++jj0) {
+                    const double* r = stage + jj0 * L::SS + grp;
+                    double b[W][NJ];
+#pragma unroll
+                    for (int kz = 0; kz < W; ++kz) {
+                        const double z = r[(4 * W + kz) * L::FSS];
+#pragma unroll
+                        for (int jj = 0; jj < NJ; ++jj) b[kz][jj] = r[(3 * W + lg * NJ + jj) * L::FSS] * z;
+                    }
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+#pragma unroll
+                        for (int ix = 0; ix < W; ++ix) {
+                            const double av = r[(c * W + ix) * L::FSS];
+#pragma unroll
+                            for (int kz = 0; kz < W; ++kz)
+#pragma unroll
+                                for (int jj = 0; jj < NJ; ++jj)
+                                    acc[(kz + R) & 3][jj][ix][c] = fma(av, b[kz][jj], acc[(kz + R) & 3][jj][ix][c]);
+                        }
+                }
+                __syncwarp();
+            }
+            c_off = n_off;
+            n_c = n_n;
+        }
+        // logical plane 0 (physical slot R) is final: emit it and zero the slot,
+        // which becomes the window's top plane at step R + 1
+        {
+            double* pp = patch + buf * L::PATCH + grp;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+                    for (int ix = 0; ix < W; ++ix) {
+                        pp[(((lg * NJ + jj) * W + ix) * 3 + c) * L::PSTRIDE] = acc[R][jj][ix][c];
+                        acc[R][jj][ix][c] = 0.0;
+                    }
+        }
+        __syncthreads();
+        {
+            const double* pb = patch + buf * L::PATCH;
+            const int Z = wrap_index(k + OFF, g.nz);
+            const bool zc = (k >= k0 + W - 1) && (k < k1);
+            const size_t zrow = (size_t)plane_cells * (size_t)Z;
+#pragma unroll
+            for (int t = 0; t < NIT; ++t) {
+                const unsigned msk = gn_mask[t];
+                if (!msk) continue;
+                const int c = gn_base[t] >> 28;
+                const double* src = pb + (gn_base[t] & 0x0fffffff);
+                double s = 0.0;
+#pragma unroll
+                for (int dy = 0; dy < W; ++dy)
+#pragma unroll
+                    for (int dx = 0; dx < W; ++dx)
+                        if (msk & (1u << (dy * W + dx))) s += src[(dy * W + dx) * 3 * L::PSTRIDE - dy * PX - dx];
+                double* f = c == 0 ? jx : (c == 1 ? jy : jz);
+                const size_t node = (size_t)gn_node[t] + zrow;
+                if (zc && gn_inner[t])
+                    f[node] = s;
+                else if (s != 0.0)
+                    atomicAdd(f + node, s);
+            }
+        }
+        buf ^= 1;
+    };
+    for (int k = k0; k < kend; k += 4) {
+        zstep(std::integral_constant<int, 0>{}, k);
+        if (k + 1 < kend) zstep(std::integral_constant<int, 1>{}, k + 1);
+        if (k + 2 < kend) zstep(std::integral_constant<int, 2>{}, k + 2);
+        if (k + 3 < kend) zstep(std::integral_constant<int, 3>{}, k + 3);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Orders 2 and 3 (4-tap window): ONE WARP PER PENCIL.
 //
 // The warp streams its pencil's particles (cells k0..k1-1 concatenated) in
@@ -1007,6 +1248,9 @@ void launch_order(const GridD& g, const CSoa& p, const uint32_t* off, const uint
     if (!configured) {
         PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel<ORDER>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM));
+        if constexpr (C::G > 1)
+            PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel_v3<ORDER>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM));
         configured = true;
     }
     const int tx = div_up(g.nx, C::PX), ty = div_up(g.ny, C::PY);
@@ -1019,6 +1263,19 @@ void launch_order(const GridD& g, const CSoa& p, const uint32_t* off, const uint
     const int zlen = div_up(g.nz, zch);
     zch = div_up(g.nz, zlen);
     dim3 grid(tx, ty, zch);
+    static const bool v1 = [] {
+        const char* e = std::getenv("PICGPU_J_LANE");
+        return e && std::string(e) == "v1";
+    }();
+    if constexpr (C::G > 1) {
+        if (!v1) {
+            deposit_current_kernel_v3<ORDER><<<grid, L::NT, L::SMEM, st>>>(g, p, off, cnt, q, j, j + g.ncells,
+                                                                           j + 2 * (size_t)g.ncells, zlen);
+            note_launch();
+            PICGPU_CUDA_TRY(cudaGetLastError());
+            return;
+        }
+    }
     deposit_current_kernel<ORDER><<<grid, L::NT, L::SMEM, st>>>(g, p, off, cnt, q, j, j + g.ncells,
                                                                 j + 2 * (size_t)g.ncells, zlen);
     note_launch();
