@@ -452,11 +452,35 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
 //    particle at the cell origin (finite weights, zero contribution);
 //  * the gather's node list (plane offset, which of the W*W pencil offsets
 //    contribute, interior flag) is computed once per CTA, not per plane.
+// Scaled J weights: QSP 6*S(d), TSC 2*S(d) (the constant 1/216 or 1/8 is
+// folded into q*W once per particle; fewer multiplies per axis).
 template <int ORDER>
+__device__ __forceinline__ void weights_scaled(double d, double (&s)[4]) {
+    if constexpr (ORDER == 3) {
+        const double t2 = d * d, t3 = t2 * d, u = 1.0 - d;
+        s[0] = u * u * u;
+        s[1] = fma(3.0, t3, fma(-6.0, t2, 4.0));
+        s[2] = fma(-3.0, t3, fma(3.0, t2, fma(3.0, d, 1.0)));
+        s[3] = t3;
+    } else {
+        const bool up = d >= 0.5;
+        const double dl = up ? d - 1.0 : d;
+        const double a = 0.5 - dl, b = 0.5 + dl;
+        const double w0 = a * a, w1 = fma(-2.0 * dl, dl, 1.5), w2 = b * b;
+        s[0] = up ? 0.0 : w0;
+        s[1] = up ? w0 : w1;
+        s[2] = up ? w1 : w2;
+        s[3] = up ? w2 : 0.0;
+    }
+}
+
+// Fraction of a binned coordinate relative to its cell `dc` (as a double);
+// exact locate only for a position outside [-0.5, 1.5] of its cell.  Padding
+// slots (valid = false) get d = 0: finite weights, zero charge.
 __device__ __forceinline__ double frac_sel(double x, double origin, double spacing, double inv, int pow2, int n,
-                                           int ci, bool valid) {
+                                           double dc, bool valid) {
     const double u = (x - origin) * inv;
-    double f = u - (double)ci;
+    double f = u - dc;
     if (valid && !(f >= -0.5 && f <= 1.5)) {
         double fr;
         locate_axis(x, origin, spacing, inv, pow2, n, fr);
@@ -466,23 +490,23 @@ __device__ __forceinline__ double frac_sel(double x, double origin, double spaci
 }
 
 template <int ORDER>
-__device__ __forceinline__ void particle_window_sel(const GridD& g, const PData& d, double q, bool valid, int ci,
-                                                    int cj, int ck, double (&a)[3][4], double (&sy)[4],
-                                                    double (&sz)[4]) {
-    const double qw = valid ? q * d.w : 0.0;
+__device__ __forceinline__ void particle_window_sel(const GridD& g, const PData& d, double qs, bool valid,
+                                                    double dci, double dcj, double dck, double (&a)[3][4],
+                                                    double (&sy)[4], double (&sz)[4]) {
+    const double qw = valid ? qs * d.w : 0.0;
     const double wq0 = qw * d.vx, wq1 = qw * d.vy, wq2 = qw * d.vz;
-    const double fx = frac_sel<ORDER>(d.x, g.gox, g.dx, g.inv_dx, g.pow2x, g.gnx, ci + g.sx_shift, valid);
-    const double fy = frac_sel<ORDER>(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, cj, valid);
-    const double fz = frac_sel<ORDER>(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, ck, valid);
+    const double fx = frac_sel(d.x, g.gox, g.dx, g.inv_dx, g.pow2x, g.gnx, dci, valid);
+    const double fy = frac_sel(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, dcj, valid);
+    const double fz = frac_sel(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, dck, valid);
     double sx[4];
-    weights_fast<ORDER>(fx, sx);
-    weights_fast<ORDER>(fy, sy);
-    weights_fast<ORDER>(fz, sz);
+    weights_scaled<ORDER>(fx, sx);
+    weights_scaled<ORDER>(fy, sy);
+    weights_scaled<ORDER>(fz, sz);
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-        a[0][t] = (valid ? wq0 : 0.0) * sx[t];
-        a[1][t] = (valid ? wq1 : 0.0) * sx[t];
-        a[2][t] = (valid ? wq2 : 0.0) * sx[t];
+        a[0][t] = wq0 * sx[t];
+        a[1][t] = wq1 * sx[t];
+        a[2][t] = wq2 * sx[t];
     }
 }
 
@@ -498,7 +522,9 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
     constexpr int FX = PX + W - 1, FY = PY + W - 1;
     constexpr int NODES = 3 * FX * FY;
     constexpr int NIT = (NODES + L::NT - 1) / L::NT;
-    static_assert(W == 4 && G > 1, "v3: 4-tap orders only");
+    static_assert(W == 4 && G > 1 && NJ == 1, "v3: 4-tap orders, one jy per lane");
+    // 1/6^3 (QSP) or 1/2^3 (TSC) of the scaled weights, folded into q
+    const double qs = q * (ORDER == 3 ? 1.0 / 216.0 : 0.125);
 
     extern __shared__ __align__(16) double smem[];
     double* patch = smem;                 // [2][W(jy)][W(ix)][3][PSTRIDE]
@@ -516,6 +542,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
     const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
     const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
     const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
+    const double dci = (double)(i + g.sx_shift), dcj = (double)j;
 
     // gather plan of this thread's nodes (constant over z)
     int gn_base[NIT], gn_node[NIT];
@@ -550,15 +577,15 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
         }
     }
 
-    double acc[W][NJ][W][3];
+    // acc[s]: physical slot s of the sliding z window; at step k the slot s
+    // holds logical plane (s - R) & 3 of the window k-1..k+2, R = (k - k0) & 3
+    double acc[W][W][3];
 #pragma unroll
-    for (int kz = 0; kz < W; ++kz)
+    for (int sl = 0; sl < W; ++sl)
 #pragma unroll
-        for (int jj = 0; jj < NJ; ++jj)
+        for (int ix = 0; ix < W; ++ix)
 #pragma unroll
-            for (int ix = 0; ix < W; ++ix)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) acc[kz][jj][ix][c] = 0.0;
+            for (int c = 0; c < 3; ++c) acc[sl][ix][c] = 0.0;
 
     uint32_t c_off = 0;
     int n_c = 0;
@@ -571,8 +598,8 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
 
     int buf = 0;
     const int kend = k1 + W - 1;
-    auto zstep = [&](auto Rc, const int k) {
-        constexpr int R = decltype(Rc)::value;
+    for (int k = k0; k < kend; ++k) {
+        const int R = (k - k0) & 3;
         if (k < k1) {
             uint32_t n_off = 0;
             int n_n = 0;
@@ -580,6 +607,11 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                 n_off = off[col + plane_cells * (k + 1)];
                 n_n = (int)cnt[col + plane_cells * (k + 1)];
             }
+            const double dck = (double)k;
+            // sz of logical plane (s - R) & 3 for physical slot s
+            const double* szb[W];
+#pragma unroll
+            for (int sl = 0; sl < W; ++sl) szb[sl] = stage + (4 * W + ((sl - R) & 3)) * L::FSS + grp;
             const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
             if (m == 0 && lg < n_n) load_particle(p, n_off + lg, nxt);  // empty cells: still prefetch
             for (int base = 0; base < m; base += CH) {
@@ -592,7 +624,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                         load_particle(p, n_off + lg, nxt);
                     }
                     double a[3][W], sy[W], sz[W];
-                    particle_window_sel<ORDER>(g, cur, q, valid, i, j, k, a, sy, sz);
+                    particle_window_sel<ORDER>(g, cur, qs, valid, dci, dcj, dck, a, sy, sz);
                     double* rec = stage + lg * L::SS + grp;
 #pragma unroll
                     for (int c = 0; c < 3; ++c)
@@ -606,25 +638,21 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                 }
                 __syncwarp();
                 const int nn = min(CH, m - base);
-                for (int jj0 = 0; jj0 < nn; ++jj0) {
+#pragma unroll
+                for (int jj0 = 0; jj0 < CH; ++jj0) {
+                    if (jj0 >= nn) break;
                     const double* r = stage + jj0 * L::SS + grp;
-                    double b[W][NJ];
+                    const double yv = r[(3 * W + lg) * L::FSS];
+                    double b[W];
 #pragma unroll
-                    for (int kz = 0; kz < W; ++kz) {
-                        const double z = r[(4 * W + kz) * L::FSS];
-#pragma unroll
-                        for (int jj = 0; jj < NJ; ++jj) b[kz][jj] = r[(3 * W + lg * NJ + jj) * L::FSS] * z;
-                    }
+                    for (int sl = 0; sl < W; ++sl) b[sl] = yv * szb[sl][jj0 * L::SS];
 #pragma unroll
                     for (int c = 0; c < 3; ++c)
 #pragma unroll
                         for (int ix = 0; ix < W; ++ix) {
                             const double av = r[(c * W + ix) * L::FSS];
 #pragma unroll
-                            for (int kz = 0; kz < W; ++kz)
-#pragma unroll
-                                for (int jj = 0; jj < NJ; ++jj)
-                                    acc[(kz + R) & 3][jj][ix][c] = fma(av, b[kz][jj], acc[(kz + R) & 3][jj][ix][c]);
+                            for (int sl = 0; sl < W; ++sl) acc[sl][ix][c] = fma(av, b[sl], acc[sl][ix][c]);
                         }
                 }
                 __syncwarp();
@@ -633,18 +661,25 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
             n_c = n_n;
         }
         // logical plane 0 (physical slot R) is final: emit it and zero the slot,
-        // which becomes the window's top plane at step R + 1
+        // which becomes the window's top plane at the next step
         {
             double* pp = patch + buf * L::PATCH + grp;
+            auto emit = [&](auto Sc) {
+                constexpr int S = decltype(Sc)::value;
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-#pragma unroll
-                for (int jj = 0; jj < NJ; ++jj)
+                for (int c = 0; c < 3; ++c)
 #pragma unroll
                     for (int ix = 0; ix < W; ++ix) {
-                        pp[(((lg * NJ + jj) * W + ix) * 3 + c) * L::PSTRIDE] = acc[R][jj][ix][c];
-                        acc[R][jj][ix][c] = 0.0;
+                        pp[((lg * W + ix) * 3 + c) * L::PSTRIDE] = acc[S][ix][c];
+                        acc[S][ix][c] = 0.0;
                     }
+            };
+            switch (R) {
+                case 0: emit(std::integral_constant<int, 0>{}); break;
+                case 1: emit(std::integral_constant<int, 1>{}); break;
+                case 2: emit(std::integral_constant<int, 2>{}); break;
+                default: emit(std::integral_constant<int, 3>{}); break;
+            }
         }
         __syncthreads();
         {
@@ -673,12 +708,6 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
             }
         }
         buf ^= 1;
-    };
-    for (int k = k0; k < kend; k += 4) {
-        zstep(std::integral_constant<int, 0>{}, k);
-        if (k + 1 < kend) zstep(std::integral_constant<int, 1>{}, k + 1);
-        if (k + 2 < kend) zstep(std::integral_constant<int, 2>{}, k + 2);
-        if (k + 3 < kend) zstep(std::integral_constant<int, 3>{}, k + 3);
     }
 }
 
