@@ -474,30 +474,29 @@ __device__ __forceinline__ void weights_scaled(double d, double (&s)[4]) {
     }
 }
 
-// Fraction of a binned coordinate relative to its cell `dc` (as a double);
-// exact locate only for a position outside [-0.5, 1.5] of its cell.  Padding
-// slots (valid = false) get d = 0: finite weights, zero charge.
-__device__ __forceinline__ double frac_sel(double x, double origin, double spacing, double inv, int pow2, int n,
-                                           double dc, bool valid) {
-    const double u = (x - origin) * inv;
-    double f = u - dc;
-    if (valid && !(f >= -0.5 && f <= 1.5)) {
-        double fr;
-        locate_axis(x, origin, spacing, inv, pow2, n, fr);
-        f = fr;
-    }
-    return valid ? f : 0.0;
-}
-
+// Fractions of a binned particle relative to its cell (dci, dcj, dck as
+// doubles), one combined range check; the exact locate only for a position
+// outside [-0.5, 1.5] of its cell (periodic image of an unwrapped upload).
+// Padding slots (valid = false) get d = 0 and zero charge: finite weights,
+// no contribution, whatever the slot's registers hold.
 template <int ORDER>
 __device__ __forceinline__ void particle_window_sel(const GridD& g, const PData& d, double qs, bool valid,
                                                     double dci, double dcj, double dck, double (&a)[3][4],
                                                     double (&sy)[4], double (&sz)[4]) {
-    const double qw = valid ? qs * d.w : 0.0;
-    const double wq0 = qw * d.vx, wq1 = qw * d.vy, wq2 = qw * d.vz;
-    const double fx = frac_sel(d.x, g.gox, g.dx, g.inv_dx, g.pow2x, g.gnx, dci, valid);
-    const double fy = frac_sel(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, dcj, valid);
-    const double fz = frac_sel(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, dck, valid);
+    const double qw = qs * d.w;
+    const double wq0 = valid ? qw * d.vx : 0.0, wq1 = valid ? qw * d.vy : 0.0, wq2 = valid ? qw * d.vz : 0.0;
+    double fx = (d.x - g.gox) * g.inv_dx - dci;
+    double fy = (d.y - g.oy) * g.inv_dy - dcj;
+    double fz = (d.z - g.oz) * g.inv_dz - dck;
+    const bool in = fx >= -0.5 && fx <= 1.5 && fy >= -0.5 && fy <= 1.5 && fz >= -0.5 && fz <= 1.5;
+    if (valid && !in) {
+        if (!(fx >= -0.5 && fx <= 1.5)) locate_axis(d.x, g.gox, g.dx, g.inv_dx, g.pow2x, g.gnx, fx);
+        if (!(fy >= -0.5 && fy <= 1.5)) locate_axis(d.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, fy);
+        if (!(fz >= -0.5 && fz <= 1.5)) locate_axis(d.z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, fz);
+    }
+    fx = valid ? fx : 0.0;
+    fy = valid ? fy : 0.0;
+    fz = valid ? fz : 0.0;
     double sx[4];
     weights_scaled<ORDER>(fx, sx);
     weights_scaled<ORDER>(fy, sy);
@@ -693,12 +692,19 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                 if (!msk) continue;
                 const int c = gn_base[t] >> 28;
                 const double* src = pb + (gn_base[t] & 0x0fffffff);
-                double s = 0.0;
+                double v[W * W];
 #pragma unroll
                 for (int dy = 0; dy < W; ++dy)
 #pragma unroll
                     for (int dx = 0; dx < W; ++dx)
-                        if (msk & (1u << (dy * W + dx))) s += src[(dy * W + dx) * 3 * L::PSTRIDE - dy * PX - dx];
+                        v[dy * W + dx] = (msk & (1u << (dy * W + dx)))
+                                             ? src[(dy * W + dx) * 3 * L::PSTRIDE - dy * PX - dx]
+                                             : 0.0;
+#pragma unroll
+                for (int h = W * W / 2; h >= 1; h /= 2)  // pairwise sum: 4 dependent adds, not 16
+#pragma unroll
+                    for (int e = 0; e < h; ++e) v[e] += v[e + h];
+                const double s = v[0];
                 double* f = c == 0 ? jx : (c == 1 ? jy : jz);
                 const size_t node = (size_t)gn_node[t] + zrow;
                 if (zc && gn_inner[t])
