@@ -284,6 +284,7 @@ def main():
     if rank == 0 or True:
         p = S.particles()
         n = p.size()
+        S.close()  # the stateless call below allocates its own workspace (C3: ~86 GB each)
         host = {}
         for k in ("x", "y", "z", "vx", "vy", "vz", "w"):
             tt = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -317,7 +318,6 @@ def main():
                "h2d_bytes_per_step": 7 * 8 * n, "d2h_bytes_per_step": 3 * 8 * grid.ncells,
                "steps": args.e2e_steps, "api": "picgpu_deposit_current (drop-in for pic::deposit_scalar)",
                "timer": "host wall clock around synchronous C-ABI calls (copies inside)"}
-    S.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -49,6 +49,10 @@ template <>
 struct JCfg<1> {
     static constexpr int G = 1, PX = 32, PY = 4, MINB = 4, CH = 1;
 };
+// CIC on the v3 kernel: 2 lanes per pencil (lane = jy), 12 accumulators each.
+struct JCfgCic3 {
+    static constexpr int G = 2, PX = 16, PY = 4, MINB = 4, CH = 2;
+};
 // TSC / QSP, "lane" variant: 4 lanes per pencil (lane = jy), 8 pencils per
 // warp, 48 accumulators per lane (4 ix x 3 c x 4 kz).
 #ifndef PICGPU_LANE_MINB
@@ -73,9 +77,9 @@ struct JCfg<3> {
     static constexpr int G = 4, PX = PICGPU_LANE_PX, PY = PICGPU_LANE_PY, MINB = PICGPU_LANE_MINB, CH = 4;
 };
 
-template <int ORDER>
+template <int ORDER, class CF = JCfg<ORDER>>
 struct JLayout {
-    using C = JCfg<ORDER>;
+    using C = CF;
     static constexpr int W = Shape<ORDER>::W;
     static constexpr int NJ = W / C::G;                 // jy values per lane
     static constexpr int NP = C::PX * C::PY;            // pencils per CTA
@@ -455,8 +459,11 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
 // Scaled J weights: QSP 6*S(d), TSC 2*S(d) (the constant 1/216 or 1/8 is
 // folded into q*W once per particle; fewer multiplies per axis).
 template <int ORDER>
-__device__ __forceinline__ void weights_scaled(double d, double (&s)[4]) {
-    if constexpr (ORDER == 3) {
+__device__ __forceinline__ void weights_scaled(double d, double (&s)[Shape<ORDER>::W]) {
+    if constexpr (ORDER == 1) {
+        s[0] = 1.0 - d;
+        s[1] = d;
+    } else if constexpr (ORDER == 3) {
         const double t2 = d * d, t3 = t2 * d, u = 1.0 - d;
         s[0] = u * u * u;
         s[1] = fma(3.0, t3, fma(-6.0, t2, 4.0));
@@ -481,8 +488,10 @@ __device__ __forceinline__ void weights_scaled(double d, double (&s)[4]) {
 // no contribution, whatever the slot's registers hold.
 template <int ORDER>
 __device__ __forceinline__ void particle_window_sel(const GridD& g, const PData& d, double qs, bool valid,
-                                                    double dci, double dcj, double dck, double (&a)[3][4],
-                                                    double (&sy)[4], double (&sz)[4]) {
+                                                    double dci, double dcj, double dck,
+                                                    double (&a)[3][Shape<ORDER>::W], double (&sy)[Shape<ORDER>::W],
+                                                    double (&sz)[Shape<ORDER>::W]) {
+    constexpr int W = Shape<ORDER>::W;
     const double qw = qs * d.w;
     const double wq0 = valid ? qw * d.vx : 0.0, wq1 = valid ? qw * d.vy : 0.0, wq2 = valid ? qw * d.vz : 0.0;
     double fx = (d.x - g.gox) * g.inv_dx - dci;
@@ -497,33 +506,33 @@ __device__ __forceinline__ void particle_window_sel(const GridD& g, const PData&
     fx = valid ? fx : 0.0;
     fy = valid ? fy : 0.0;
     fz = valid ? fz : 0.0;
-    double sx[4];
+    double sx[W];
     weights_scaled<ORDER>(fx, sx);
     weights_scaled<ORDER>(fy, sy);
     weights_scaled<ORDER>(fz, sz);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < W; ++t) {
         a[0][t] = wq0 * sx[t];
         a[1][t] = wq1 * sx[t];
         a[2][t] = wq2 * sx[t];
     }
 }
 
-template <int ORDER>
-__global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
+template <int ORDER, class CF = JCfg<ORDER>>
+__global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
     deposit_current_kernel_v3(const GridD g, const CSoa p, const uint32_t* __restrict__ off,
                               const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
                               double* __restrict__ jy, double* __restrict__ jz, const int zlen) {
-    using C = JCfg<ORDER>;
-    using L = JLayout<ORDER>;
+    using C = CF;
+    using L = JLayout<ORDER, CF>;
     constexpr int W = L::W, OFF = Shape<ORDER>::OFF, NJ = L::NJ;
     constexpr int G = C::G, PX = C::PX, PY = C::PY, CH = C::CH;
     constexpr int FX = PX + W - 1, FY = PY + W - 1;
     constexpr int NODES = 3 * FX * FY;
     constexpr int NIT = (NODES + L::NT - 1) / L::NT;
-    static_assert(W == 4 && G > 1 && NJ == 1, "v3: 4-tap orders, one jy per lane");
+    static_assert(G == W && NJ == 1 && (W & (W - 1)) == 0, "v3: one jy per lane, power-of-two window");
     // 1/6^3 (QSP) or 1/2^3 (TSC) of the scaled weights, folded into q
-    const double qs = q * (ORDER == 3 ? 1.0 / 216.0 : 0.125);
+    const double qs = q * (ORDER == 3 ? 1.0 / 216.0 : ORDER == 2 ? 0.125 : 1.0);
 
     extern __shared__ __align__(16) double smem[];
     double* patch = smem;                 // [2][W(jy)][W(ix)][3][PSTRIDE]
@@ -577,7 +586,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
     }
 
     // acc[s]: physical slot s of the sliding z window; at step k the slot s
-    // holds logical plane (s - R) & 3 of the window k-1..k+2, R = (k - k0) & 3
+    // holds logical plane (s - R) mod W of the window, R = (k - k0) mod W
     double acc[W][W][3];
 #pragma unroll
     for (int sl = 0; sl < W; ++sl)
@@ -598,7 +607,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
     int buf = 0;
     const int kend = k1 + W - 1;
     for (int k = k0; k < kend; ++k) {
-        const int R = (k - k0) & 3;
+        const int R = (k - k0) & (W - 1);
         if (k < k1) {
             uint32_t n_off = 0;
             int n_n = 0;
@@ -610,7 +619,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
             // sz of logical plane (s - R) & 3 for physical slot s
             const double* szb[W];
 #pragma unroll
-            for (int sl = 0; sl < W; ++sl) szb[sl] = stage + (4 * W + ((sl - R) & 3)) * L::FSS + grp;
+            for (int sl = 0; sl < W; ++sl) szb[sl] = stage + (4 * W + ((sl - R) & (W - 1))) * L::FSS + grp;
             const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
             if (m == 0 && lg < n_n) load_particle(p, n_off + lg, nxt);  // empty cells: still prefetch
             for (int base = 0; base < m; base += CH) {
@@ -673,11 +682,18 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                         acc[S][ix][c] = 0.0;
                     }
             };
-            switch (R) {
-                case 0: emit(std::integral_constant<int, 0>{}); break;
-                case 1: emit(std::integral_constant<int, 1>{}); break;
-                case 2: emit(std::integral_constant<int, 2>{}); break;
-                default: emit(std::integral_constant<int, 3>{}); break;
+            if constexpr (W == 2) {
+                if (R == 0)
+                    emit(std::integral_constant<int, 0>{});
+                else
+                    emit(std::integral_constant<int, 1>{});
+            } else {
+                switch (R) {
+                    case 0: emit(std::integral_constant<int, 0>{}); break;
+                    case 1: emit(std::integral_constant<int, 1>{}); break;
+                    case 2: emit(std::integral_constant<int, 2>{}); break;
+                    default: emit(std::integral_constant<int, 3>{}); break;
+                }
             }
         }
         __syncthreads();
@@ -1273,19 +1289,22 @@ void launch_warp(const GridD& g, const CSoa& p, const uint32_t* off, const uint3
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
-template <int ORDER>
-void launch_order(const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
-                  int num_sms, cudaStream_t st) {
-    using C = JCfg<ORDER>;
-    using L = JLayout<ORDER>;
+// z-chunked grid of one of the pencil kernels (v3 or the original v1).
+template <int ORDER, class C, bool V3>
+void launch_kernel(const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+                   int num_sms, cudaStream_t st) {
+    using L = JLayout<ORDER, C>;
     constexpr int W = L::W;
+    constexpr size_t smem = V3 ? L::SMEM : JLayout<ORDER>::SMEM;
+    auto* kern = [] {
+        if constexpr (V3)
+            return deposit_current_kernel_v3<ORDER, C>;
+        else
+            return deposit_current_kernel<ORDER>;
+    }();
     static bool configured = false;
     if (!configured) {
-        PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel<ORDER>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM));
-        if constexpr (C::G > 1)
-            PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel_v3<ORDER>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM));
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
     const int tx = div_up(g.nx, C::PX), ty = div_up(g.ny, C::PY);
@@ -1298,23 +1317,24 @@ void launch_order(const GridD& g, const CSoa& p, const uint32_t* off, const uint
     const int zlen = div_up(g.nz, zch);
     zch = div_up(g.nz, zlen);
     dim3 grid(tx, ty, zch);
+    kern<<<grid, L::NT, smem, st>>>(g, p, off, cnt, q, j, j + g.ncells, j + 2 * (size_t)g.ncells, zlen);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+template <int ORDER>
+void launch_order(const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+                  int num_sms, cudaStream_t st) {
     static const bool v1 = [] {
         const char* e = std::getenv("PICGPU_J_LANE");
         return e && std::string(e) == "v1";
     }();
-    if constexpr (C::G > 1) {
-        if (!v1) {
-            deposit_current_kernel_v3<ORDER><<<grid, L::NT, L::SMEM, st>>>(g, p, off, cnt, q, j, j + g.ncells,
-                                                                           j + 2 * (size_t)g.ncells, zlen);
-            note_launch();
-            PICGPU_CUDA_TRY(cudaGetLastError());
-            return;
-        }
-    }
-    deposit_current_kernel<ORDER><<<grid, L::NT, L::SMEM, st>>>(g, p, off, cnt, q, j, j + g.ncells,
-                                                                j + 2 * (size_t)g.ncells, zlen);
-    note_launch();
-    PICGPU_CUDA_TRY(cudaGetLastError());
+    // v3 (default): orders 2/3 with JCfg<ORDER>, CIC with 2 lanes per pencil
+    using C3 = std::conditional_t<ORDER == 1, JCfgCic3, JCfg<ORDER>>;
+    if (v1)
+        launch_kernel<ORDER, JCfg<ORDER>, false>(g, p, off, cnt, q, j, num_sms, st);
+    else
+        launch_kernel<ORDER, C3, true>(g, p, off, cnt, q, j, num_sms, st);
 }
 
 }  // namespace
