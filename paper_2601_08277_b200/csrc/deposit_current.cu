@@ -50,8 +50,17 @@ struct JCfg<1> {
     static constexpr int G = 1, PX = 32, PY = 4, MINB = 4, CH = 1;
 };
 // CIC on the v3 kernel: 2 lanes per pencil (lane = jy), 12 accumulators each.
+#ifndef PICGPU_CIC_PX
+#define PICGPU_CIC_PX 16
+#endif
+#ifndef PICGPU_CIC_PY
+#define PICGPU_CIC_PY 4
+#endif
+#ifndef PICGPU_CIC_MINB
+#define PICGPU_CIC_MINB 4
+#endif
 struct JCfgCic3 {
-    static constexpr int G = 2, PX = 16, PY = 4, MINB = 4, CH = 2;
+    static constexpr int G = 2, PX = PICGPU_CIC_PX, PY = PICGPU_CIC_PY, MINB = PICGPU_CIC_MINB, CH = 2;
 };
 // TSC / QSP, "lane" variant: 4 lanes per pencil (lane = jy), 8 pencils per
 // warp, 48 accumulators per lane (4 ix x 3 c x 4 kz).
