@@ -411,3 +411,33 @@ def test_session_current_vs_extended_precision(pg, order):
     got = np.stack([J.jx, J.jy, J.jz]).astype(np.longdouble)
     err = float(np.abs(got - hp).max() / np.abs(hp).max())
     assert err < 1e-14, err
+
+
+def test_session_mover_buffer_overflow_resorts_exactly(pg, orc):
+    """Every particle changes cell in one step: the movers exceed the mover
+    buffer (64 records per 256-slot push block), the unrecorded ones stay in
+    their stale bins and the step falls back to a full stable re-sort.  The
+    state must still equal the oracle's, and the next steps run normally."""
+    g = O.Grid.make(128, 32, 32)
+    s = orc.make_plasma(g, 4, 0.0, seed=5)  # 524288 particles at rest
+    s["vx"][:] = 1.5                        # dt 0.5: every particle moves +0.75 cell in x
+    s["vx"][::7] = -1.9
+    q = -1.0
+    S = pg.Session(to_pg_grid(g), 3)
+    S.upload(s, q=q)
+    ref = {k: v.copy() for k, v in s.items()}
+    for step in range(3):
+        st = S.step(0.5)
+        moved = orc.advance(g, 0.5, ref)
+        assert st["moved"] == moved
+        if step == 0:
+            assert st["rebuilt"] == 1 and moved > S.num_particles // 4
+        got = S.particles()
+        o = np.argsort(got.id)
+        w = np.argsort(ref["id"]) if "id" in ref else np.arange(len(ref["x"]))
+        for k in ("x", "y", "z"):
+            assert np.array_equal(getattr(got, k)[o], ref[k][w]), (step, k)
+        cells = orc.cells(g, {k: getattr(got, k) for k in ("x", "y", "z")})
+        assert np.all(np.diff(cells.astype(np.int64)) >= 0)  # storage is cell-sorted
+        J = S.current()
+        assert peak_rel_err((J.jx, J.jy, J.jz), orc.deposit_current(g, 3, ref, q)) <= J_TOL
