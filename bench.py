@@ -49,7 +49,23 @@ CONFIGS = {
     "c3o1": (256, 32, 1, 0.1, 0.5, 5, "C3: 256^3 cells, 32 ppc, order 1, u_th 0.1, dt 0.5"),
     "c3o2": (256, 32, 2, 0.1, 0.5, 5, "C3: 256^3 cells, 32 ppc, order 2 (TSC), u_th 0.1, dt 0.5"),
     "c3o3": (256, 32, 3, 0.1, 0.5, 5, "C3: 256^3 cells, 32 ppc, order 3, u_th 0.1, dt 0.5"),
+    "c4": ((512, 128, 128), 8, 3, 0.01, 0.5, 10,
+           "C4 (LWFA-like, static window): 512x128x128 cells, order 3, electrons from x-cell 64 with a linear "
+           "density ramp over [64,128) to 8 ppc, u_th 0.01, plus a 10% beam with ux ~ U(5,50) in x-cells "
+           "[128,160); dt 0.5"),
 }
+
+
+def make_grid(pg, n):
+    return pg.Grid.make(*n) if isinstance(n, tuple) else pg.Grid.make(n)
+
+
+def populate(pg, S, name, ppc, u_th, seed=1):
+    if name == "c4":
+        S.generate_lwfa(pg.LwfaConfig.make(ppc=ppc, ramp_start=64, ramp_len=64, u_th=u_th, beam_fraction=0.1,
+                                           ux=(5.0, 50.0), beam_x=(128.0, 160.0), seed=seed))
+    else:
+        S.generate_plasma(ppc, u_th, seed=seed)
 METRIC = "particle current deposits/sec"
 UNIT = "deposits/s"
 FLOPS = {1: 76, 2: 238, 3: 534}
@@ -153,7 +169,8 @@ def run_reference_arm(args, cfgname):
         "ms_per_step": sec / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (SURVEY 8(d) generator, reference counter RNG)",
         "config": {"workload": desc + "; step = push + incremental sort + J deposit",
-                   "grid": [nx] * 3, "ppc": ppc, "order": order, "particles_per_gpu": nx ** 3 * ppc,
+                   "grid": list(nx) if isinstance(nx, tuple) else [nx] * 3, "ppc": ppc, "order": order,
+                   "cpu_sample_note": "CPU sample: uniform 32^3 sub-boxes at this ppc/u_th/order",
                    "parallelism": "single" if args.gpus == 1 else f"x-slabs x{args.gpus} (GPU arm); CPU: rank 0 only"},
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
@@ -211,7 +228,9 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    grid = pg.Grid.make(nx)
+    grid = make_grid(pg, nx)
+    if isinstance(nx, tuple) and world > 1:
+        raise SystemExit("multi-GPU runs use the cubic configs (x-slabs of a (n*N) x n x n box)")
     if world == 1 and not args.slab:
         S = pg.Session(grid, order=order, device=local, timing=True)
         step = lambda: S.step(dt)  # noqa: E731
@@ -222,7 +241,7 @@ def main():
         S = SlabSession(G, rank * nx, (rank + 1) * nx, order=order, device=local, timing=True)
         ring = RingExchange()
         step = lambda: slab_step(S, ring, dt)  # noqa: E731
-    S.generate_plasma(ppc, u_th, seed=1)
+    populate(pg, S, args.config, ppc, u_th)
     n = S.num_particles
     n_total = n * world  # conserved by the migration
     stream = torch.cuda.ExternalStream(S.stream)
@@ -259,7 +278,8 @@ def main():
 
     # roofline of the dominant kernel (J deposition)
     hbm_peak, hbm_src = peaks()
-    bytes_per = 56 + 24 / ppc
+    cells = grid.ncells
+    bytes_per = 56 + 24 * cells / n  # J written once per node, amortised over the particles
     hbm_achieved = n * bytes_per / j_avg_s / 1e9
     fp64_peak = pg.fp64_peak_tflops(local)
     fp64_achieved = n * FLOPS[order] / j_avg_s / 1e12
@@ -337,7 +357,8 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY 8(d) seeded plasma generated in HBM; no dataset)",
             "config": {"workload": desc + "; step = push + incremental sort + J deposit",
-                       "grid": [nx * world, nx, nx], "ppc": ppc, "order": order, "particles_per_gpu": n,
+                       "grid": list(nx) if isinstance(nx, tuple) else [nx * world, nx, nx], "ppc": ppc,
+                       "order": order, "particles_per_gpu": n,
                        "l2": f"inputs larger than L2 ({n * 64 / 1e9:.1f} GB particle store)",
                        "parallelism": "single" if world == 1 else
                        f"x-slabs x{world} of a {nx * world}x{nx}x{nx} box, NCCL ring exchange (migration + J guards)"},

@@ -213,6 +213,20 @@ PICGPU_API int picgpu_session_upload(picgpu_session* s, uint64_t n, const double
 /* Generate the SURVEY 8(d) seeded plasma directly in HBM (device-side
  * generator on the reference counter RNG; inputs for benchmarks). */
 PICGPU_API int picgpu_session_generate_plasma(picgpu_session* s, int ppc, double u_th, uint64_t seed);
+/* SURVEY 8(d) C4 (laser-wakefield-like) population on the session grid:
+ * background electrons in x-cells i >= ramp_start, round(ppc * ramp_i) per
+ * cell with ramp_i = clamp((i + 0.5 - ramp_start) / ramp_len, 0, 1), uniform
+ * in the cell (counters 6, 7, 8), Maxwellian u_th (counters 0..5), pid
+ * cell-major; plus a beam of llround(beam_fraction * background) particles
+ * with ux ~ U(ux_min, ux_max) (counter 9), uy = uz = 0, uniform in x-cells
+ * [beam_x0, beam_x1) and over the whole y-z plane, pids after the background.
+ * v = u / gamma, W = 1/ppc, q = -1. */
+typedef struct picgpu_lwfa {
+    int32_t ppc, ramp_start, ramp_len, pad_;
+    double u_th, beam_fraction, ux_min, ux_max, beam_x0, beam_x1;
+    uint64_t seed;
+} picgpu_lwfa;
+PICGPU_API int picgpu_session_generate_lwfa(picgpu_session* s, const picgpu_lwfa* cfg);
 /* One step: [push] -> [incremental sort] -> [deposit J] -> [deposit rho] -> [global sort]. */
 PICGPU_API int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_step_stats* out);
 PICGPU_API int picgpu_session_global_sort(picgpu_session* s);

@@ -163,6 +163,19 @@ class WorkloadConfig(C.Structure):
         return min(self.grid.dx, self.grid.dy, self.grid.dz) / self.dt
 
 
+class LwfaConfig(C.Structure):
+    """picgpu_lwfa: the SURVEY 8(d) C4 population (density ramp + relativistic beam)."""
+
+    _fields_ = [("ppc", C.c_int32), ("ramp_start", C.c_int32), ("ramp_len", C.c_int32), ("pad_", C.c_int32),
+                ("u_th", C.c_double), ("beam_fraction", C.c_double), ("ux_min", C.c_double), ("ux_max", C.c_double),
+                ("beam_x0", C.c_double), ("beam_x1", C.c_double), ("seed", C.c_uint64)]
+
+    @classmethod
+    def make(cls, ppc=8, ramp_start=64, ramp_len=64, u_th=0.01, beam_fraction=0.1, ux=(5.0, 50.0),
+             beam_x=(128.0, 160.0), seed=1):
+        return cls(ppc, ramp_start, ramp_len, 0, u_th, beam_fraction, ux[0], ux[1], beam_x[0], beam_x[1], seed)
+
+
 class SortPolicy(C.Structure):
     """pic::SortPolicy (sort_policy.hpp:12-30); defaults are Table 4's."""
 
@@ -242,6 +255,7 @@ def lib():
     L.picgpu_deposit_rhocell_vector.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, C.c_int, _P, _P, _P,
                                                                          C.POINTER(_D)]
     L.picgpu_session_set_kernel.argtypes = [_P, C.c_int]
+    L.picgpu_session_generate_lwfa.argtypes = [_P, C.POINTER(LwfaConfig)]
     L.picgpu_session_make_workload.argtypes = [_P, C.POINTER(WorkloadConfig)]
     L.picgpu_slab_grid.argtypes = [G, C.c_int, C.c_int, C.c_int, G]
     L.picgpu_session_set_slab.argtypes = [_P, G, C.c_int, C.c_int, C.c_int]
@@ -483,6 +497,10 @@ class Session:
 
     def generate_plasma(self, ppc: int, u_th: float, seed: int = 1):
         _check(lib().picgpu_session_generate_plasma(self._h, ppc, u_th, seed))
+
+    def generate_lwfa(self, cfg: "LwfaConfig"):
+        """SURVEY 8(d) C4 population (density ramp + relativistic beam), generated in HBM."""
+        _check(lib().picgpu_session_generate_lwfa(self._h, C.byref(cfg)))
 
     def step(self, dt: float = 0.5, flags: int = STEP_DEFAULT) -> dict:
         st = StepStats()

@@ -8,6 +8,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "kernels.hpp"
 #include "store.hpp"
@@ -590,6 +591,39 @@ int picgpu_session_generate_plasma(picgpu_session* s, int ppc, double u_th, uint
         launch_generate_plasma(bs.g, ppc, u_th, seed, bs.B.soa(), s->st);
         bs.full_sort_from_B(n);
         s->q = -1.0;  // electrons
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+    });
+}
+
+int picgpu_session_generate_lwfa(picgpu_session* s, const picgpu_lwfa* c) {
+    return guard([&] {
+        set_device(s);
+        BinStore& bs = s->store;
+        if (s->slab) throw Status{PICGPU_ELOGIC, "generate_lwfa: not available on a slab session"};
+        const GridD& g = bs.g;
+        if (c->ppc < 1 || c->ramp_len < 1 || c->ramp_start < 0)
+            throw Status{PICGPU_EINVAL, "generate_lwfa: ppc, ramp_len must be >= 1, ramp_start >= 0"};
+        if (!(c->beam_fraction >= 0.0) || !(c->ux_max >= c->ux_min) || !(c->beam_x1 >= c->beam_x0) ||
+            c->beam_x0 < 0.0 || c->beam_x1 > g.nx)
+            throw Status{PICGPU_EINVAL, "generate_lwfa: bad beam parameters"};
+        std::vector<uint32_t> pfx(g.nx + 1, 0u);
+        for (int i = 0; i < g.nx; ++i) {
+            const double ramp = std::min(1.0, std::max(0.0, (i + 0.5 - c->ramp_start) / c->ramp_len));
+            const uint32_t ci = i >= c->ramp_start ? (uint32_t)std::llround(c->ppc * ramp) : 0u;
+            pfx[i + 1] = pfx[i] + ci;
+        }
+        const uint64_t nbg = (uint64_t)pfx[g.nx] * g.ny * g.nz;
+        const uint64_t nbeam = (uint64_t)std::llround(c->beam_fraction * (double)nbg);
+        const uint64_t n = nbg + nbeam;
+        if (n >= 0xffffffffull) throw Status{PICGPU_ELENGTH, "generate_lwfa: more than 2^32-1 particles"};
+        DevBuf dp;
+        dp.ensure(pfx.size() * 4);
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(dp.p, pfx.data(), pfx.size() * 4, cudaMemcpyHostToDevice, s->st));
+        bs.B.ensure(n);
+        launch_generate_lwfa(g, dp.as<uint32_t>(), nbg, n, c->ppc, c->u_th, c->ux_min, c->ux_max, c->beam_x0,
+                             c->beam_x1, c->seed, bs.B.soa(), s->st);
+        bs.full_sort_from_B(n);
+        s->q = -1.0;
         PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
     });
 }

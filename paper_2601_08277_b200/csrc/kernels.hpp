@@ -41,6 +41,9 @@ void launch_advance(const GridD& g, double dt, double cap2, double* x, double* y
                     cudaStream_t st);
 // Device-side SURVEY 8(d) plasma generator (cell-major, counter RNG).
 void launch_generate_plasma(const GridD& g, int ppc, double u_th, uint64_t seed, Soa out, cudaStream_t st);
+void launch_generate_lwfa(const GridD& g, const uint32_t* pfx_dev, uint64_t nbg, uint64_t n, int ppc, double u_th,
+                          double ux_min, double ux_max, double bx0, double bx1, uint64_t seed, Soa out,
+                          cudaStream_t st);
 void launch_make_workload(const GridD& g, int ppc, double vth, int drift, const double amp[3], double cap,
                           uint64_t seed, Soa out, cudaStream_t st);
 // Slab guard planes: pack planes [p0, p0+np) of a comps x (nx,ny,nz) field

@@ -684,6 +684,51 @@ __global__ void k_generate(const GridD g, int ppc, double u_th, uint64_t seed, c
     out.id[p] = pid;
 }
 
+// SURVEY 8(d) C4 population (see picgpu_session_generate_lwfa): pfx[i] =
+// background particles of x-cells < i in one (y, z) row.
+__global__ void k_generate_lwfa(const GridD g, const uint32_t* __restrict__ pfx, uint64_t nbg, uint64_t n, int ppc,
+                                double u_th, double ux_min, double ux_max, double bx0, double bx1, uint64_t seed,
+                                const Soa out) {
+    const uint64_t pid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pid >= n) return;
+    double ux, uy, uz;
+    if (pid < nbg) {
+        const uint32_t R = pfx[g.nx];
+        const uint64_t row = pid / R;
+        const uint32_t r = (uint32_t)(pid % R);
+        int lo = 0, hi = g.nx - 1;  // largest i with pfx[i] <= r
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pfx[mid] <= r)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        const int i = lo;
+        const int j = (int)(row % (uint64_t)g.ny);
+        const int k = (int)(row / (uint64_t)g.ny);
+        out.x[pid] = __dadd_rn(g.ox, __dmul_rn(__dadd_rn((double)i, uniform01(seed, pid, 6)), g.dx));
+        out.y[pid] = __dadd_rn(g.oy, __dmul_rn(__dadd_rn((double)j, uniform01(seed, pid, 7)), g.dy));
+        out.z[pid] = __dadd_rn(g.oz, __dmul_rn(__dadd_rn((double)k, uniform01(seed, pid, 8)), g.dz));
+        ux = u_th * gaussian(seed, pid, 0);
+        uy = u_th * gaussian(seed, pid, 1);
+        uz = u_th * gaussian(seed, pid, 2);
+    } else {
+        const double fx = __dadd_rn(bx0, __dmul_rn(__dsub_rn(bx1, bx0), uniform01(seed, pid, 6)));
+        out.x[pid] = __dadd_rn(g.ox, __dmul_rn(fx, g.dx));
+        out.y[pid] = __dadd_rn(g.oy, __dmul_rn(g.Ly, uniform01(seed, pid, 7)));
+        out.z[pid] = __dadd_rn(g.oz, __dmul_rn(g.Lz, uniform01(seed, pid, 8)));
+        ux = __dadd_rn(ux_min, __dmul_rn(__dsub_rn(ux_max, ux_min), uniform01(seed, pid, 9)));
+        uy = uz = 0.0;
+    }
+    const double gam = sqrt(1.0 + ux * ux + uy * uy + uz * uz);
+    out.vx[pid] = ux / gam;
+    out.vy[pid] = uy / gam;
+    out.vz[pid] = uz / gam;
+    out.w[pid] = 1.0 / (double)ppc;
+    out.id[pid] = pid;
+}
+
 // make_workload (workload.hpp:75-125): particle pid = cell-major (x fastest),
 // then a px*py*pz sub-lattice in the cell (x fastest); Maxwellian velocities,
 // optional shear drift, truncation at the displacement cap; W = 1.
@@ -770,6 +815,16 @@ void launch_add_planes(double* F, int comps, int nx, int ny, int nz, int p0, int
     if (!total) return;
     k_add_planes<<<(int)std::min<long long>(div_up(total, 256), 148 * 8), 256, 0, st>>>(F, comps, nx, ny, nz, p0, np,
                                                                                        in);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_generate_lwfa(const GridD& g, const uint32_t* pfx_dev, uint64_t nbg, uint64_t n, int ppc, double u_th,
+                          double ux_min, double ux_max, double bx0, double bx1, uint64_t seed, Soa out,
+                          cudaStream_t st) {
+    if (!n) return;
+    k_generate_lwfa<<<div_up((long long)n, 256), 256, 0, st>>>(g, pfx_dev, nbg, n, ppc, u_th, ux_min, ux_max, bx0, bx1,
+                                                              seed, out);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
