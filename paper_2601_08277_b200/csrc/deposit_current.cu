@@ -604,12 +604,20 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 #pragma unroll
             for (int c = 0; c < 3; ++c) acc[sl][ix][c] = 0.0;
 
+    // an entirely empty tile (vacuum) writes nothing: J was zeroed by the caller
+    {
+        bool any = false;
+        if (pv)
+            for (int kk = k0 + lg; kk < k1; kk += G) any |= cnt[col + plane_cells * kk] != 0;
+        if (!__syncthreads_or(any)) return;
+    }
     uint32_t c_off = 0;
     int n_c = 0;
     if (pv && k0 < k1) {
         c_off = off[col + plane_cells * k0];
         n_c = (int)cnt[col + plane_cells * k0];
     }
+    int last_busy = k0 - W;  // last z-step in which any pencil of the CTA deposited (CTA-uniform)
     PData nxt{};
     if (lg < n_c) load_particle(p, c_off + lg, nxt);
 
@@ -617,6 +625,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
     const int kend = k1 + W - 1;
     for (int k = k0; k < kend; ++k) {
         const int R = (k - k0) & (W - 1);
+        const bool busy = k < k1 && n_c > 0;
         if (k < k1) {
             uint32_t n_off = 0;
             int n_n = 0;
@@ -705,8 +714,10 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                 }
             }
         }
-        __syncthreads();
-        {
+        // the plane emitted now gathers cells k-W+1..k: if none of them held a
+        // particle anywhere in the CTA, every node sum is zero -- skip it
+        if (__syncthreads_or(busy)) last_busy = k;
+        if (last_busy >= k - (W - 1)) {
             const double* pb = patch + buf * L::PATCH;
             const int Z = wrap_index(k + OFF, g.nz);
             const bool zc = (k >= k0 + W - 1) && (k < k1);

@@ -78,16 +78,41 @@ __device__ __forceinline__ bool tap_valid(int up, int t) {
     return up ? t != 0 : t != 3;
 }
 
+// Box of nodes whose W source cells never wrap on any axis (sorted sources =
+// ascending, contiguous): those go through density_rows.  Empty on an axis
+// shorter than the stencil.
+struct Interior {
+    int lo[3], hi[3];  // inclusive node ranges per axis
+    __host__ __device__ bool contains(int X, int Y, int Z) const {
+        return X >= lo[0] && X <= hi[0] && Y >= lo[1] && Y <= hi[1] && Z >= lo[2] && Z <= hi[2];
+    }
+    __host__ __device__ bool empty() const { return lo[0] > hi[0] || lo[1] > hi[1] || lo[2] > hi[2]; }
+};
+
+template <int ORDER>
+Interior interior_of(const GridD& g) {
+    constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
+    // node X gathers cells X-OFF-(W-1) .. X-OFF
+    const int n[3] = {g.nx, g.ny, g.nz};
+    Interior in{};
+    for (int a = 0; a < 3; ++a) {
+        in.lo[a] = OFF + W - 1;
+        in.hi[a] = n[a] - 1 + OFF;
+    }
+    return in;
+}
+
 template <int ORDER>
 __global__ void density_gather_sorted(const GridD g, const uint32_t* __restrict__ off,
                                       const uint32_t* __restrict__ cnt, const double* __restrict__ S, uint64_t slots,
-                                      const uint8_t* __restrict__ upb, double* __restrict__ rho) {
+                                      const uint8_t* __restrict__ upb, double* __restrict__ rho, Interior skip) {
     constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
     const uint64_t node = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (node >= g.ncells) return;
     const int X = (int)(node % (uint32_t)g.nx);
     const int Y = (int)((node / (uint32_t)g.nx) % (uint32_t)g.ny);
     const int Z = (int)(node / ((uint64_t)g.nx * (uint32_t)g.ny));
+    if (skip.contains(X, Y, Z)) return;
     int xs[W], xt[W], ys[W], yt[W], zs[W], zt[W];
     sources<W, OFF>(X, g.nx, xs, xt);
     sources<W, OFF>(Y, g.ny, ys, yt);
@@ -114,6 +139,62 @@ __global__ void density_gather_sorted(const GridD g, const uint32_t* __restrict_
                     const double syz = __dmul_rn(Sy[s], Sz[s]);
                     const double sv = __dmul_rn(Sx[s], syz);
                     acc = __dadd_rn(acc, __dmul_rn(SQ[s], sv));
+                }
+            }
+        }
+    }
+    rho[node] = acc;
+}
+
+// The boundary shell of the sorted path, without the prologue: the exact
+// weights of each visited slot are evaluated on the fly (the same
+// locate_axis + Shape<ORDER>::weights as the prologue, so bit-identical), and
+// only the shell's nodes pay for them.
+template <int ORDER>
+__global__ void density_gather_shell(const GridD g, const CSoa p, const double* __restrict__ quantity, double qscale,
+                                     const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt,
+                                     double* __restrict__ rho, Interior skip) {
+    constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
+    const uint64_t node = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= g.ncells) return;
+    const int X = (int)(node % (uint32_t)g.nx);
+    const int Y = (int)((node / (uint32_t)g.nx) % (uint32_t)g.ny);
+    const int Z = (int)(node / ((uint64_t)g.nx * (uint32_t)g.ny));
+    if (skip.contains(X, Y, Z)) return;
+    int xs[W], xt[W], ys[W], yt[W], zs[W], zt[W];
+    sources<W, OFF>(X, g.nx, xs, xt);
+    sources<W, OFF>(Y, g.ny, ys, yt);
+    sources<W, OFF>(Z, g.nz, zs, zt);
+    double acc = 0.0;
+    for (int zi = 0; zi < W; ++zi) {
+        for (int yi = 0; yi < W; ++yi) {
+            const uint32_t row = (uint32_t)g.nx * ((uint32_t)ys[yi] + (uint32_t)g.ny * (uint32_t)zs[zi]);
+            for (int xi = 0; xi < W; ++xi) {
+                const uint32_t c = (uint32_t)xs[xi] + row;
+                const uint32_t o = off[c], n = cnt[c];
+                for (uint32_t u = 0; u < n; ++u) {
+                    const uint32_t sl = o + u;
+                    double f[3], w[3][W];
+                    int up[3];
+                    locate_x(g, p.x[sl], f[0]);
+                    locate_axis(p.y[sl], g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
+                    locate_axis(p.z[sl], g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) Shape<ORDER>::weights(f[a], w[a], up[a]);
+                    if (ORDER == 2 && (!tap_valid<ORDER>(up[0], xt[xi]) || !tap_valid<ORDER>(up[1], yt[yi]) ||
+                                       !tap_valid<ORDER>(up[2], zt[zi])))
+                        continue;
+                    double sx = 0, sy = 0, sz = 0;
+#pragma unroll
+                    for (int t = 0; t < W; ++t) {
+                        sx = t == xt[xi] ? w[0][t] : sx;
+                        sy = t == yt[yi] ? w[1][t] : sy;
+                        sz = t == zt[zi] ? w[2][t] : sz;
+                    }
+                    const double q = quantity ? quantity[sl] : qscale * p.w[sl];
+                    const double syz = __dmul_rn(sy, sz);
+                    const double sv = __dmul_rn(sx, syz);
+                    acc = __dadd_rn(acc, __dmul_rn(q, sv));
                 }
             }
         }
@@ -180,6 +261,128 @@ __global__ void density_gather_merge(const GridD g, const uint32_t* __restrict__
     rho[node] = acc;
 }
 
+// Row-staged ordered gather for the interior nodes.  CTA = RX x RY node
+// columns (one warp per node row) over a z-chunk [Za, Zb) of nodes.  Source
+// planes zs stream in ascending order, and within a plane the source rows ys
+// in ascending order; each row's contiguous slot range (cells X0-OFF-(W-1) ..
+// X0+RX-1-OFF, slack slots included) is staged into shared memory in pieces,
+// with the exact weights (locate_axis + Shape<ORDER>::weights, as the
+// prologue computes them) evaluated once per staged slot.  A node thread then
+// adds, for each of its z-window nodes, the terms of its own W cells' slots in
+// slot order.  Per node this is the reference's order -- source planes, rows,
+// cells ascending (= ascending linear id), then slots -- with the same value
+// expression q*(sx*(sy*sz)) and round-to-nearest intrinsics: bit-identical to
+// density_gather_sorted (and to pic::deposit_density on this storage order).
+#ifndef PICGPU_RHO_RX
+#define PICGPU_RHO_RX 32
+#endif
+#ifndef PICGPU_RHO_RY
+#define PICGPU_RHO_RY 8
+#endif
+#ifndef PICGPU_RHO_CAP
+#define PICGPU_RHO_CAP 1024
+#endif
+constexpr int kRowX = PICGPU_RHO_RX, kRowY = PICGPU_RHO_RY, kRowCap = PICGPU_RHO_CAP;
+
+template <int ORDER>
+__global__ void __launch_bounds__(kRowX * kRowY)
+    density_rows(const GridD g, const CSoa p, const double* __restrict__ quantity, double qscale,
+                 const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt, Interior in, int zlen,
+                 double* __restrict__ rho) {
+    constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
+    constexpr int NT = kRowX * kRowY;
+    extern __shared__ __align__(16) double dsm[];
+    double* s_q = dsm;                                     // [kRowCap]
+    double (*s_w)[W][kRowCap] = reinterpret_cast<double (*)[W][kRowCap]>(dsm + kRowCap);  // sx, sy, sz taps
+    int* s_xs = reinterpret_cast<int*>(dsm + (1 + 3 * W) * kRowCap);  // source x-cell, -1 for slack
+    unsigned char* s_up = reinterpret_cast<unsigned char*>(s_xs + kRowCap);
+
+    const int tid = threadIdx.x;
+    const int X0 = in.lo[0] + blockIdx.x * kRowX, Y0 = in.lo[1] + blockIdx.y * kRowY;
+    const int X = X0 + (tid % kRowX), Y = Y0 + (tid / kRowX);
+    const int Za = in.lo[2] + blockIdx.z * zlen;
+    const int Zb = min(Za + zlen, in.hi[2] + 1);
+    const bool nv = X <= in.hi[0] && Y <= in.hi[1];
+    const int Xl = min(X0 + kRowX - 1, in.hi[0]), Yl = min(Y0 + kRowY - 1, in.hi[1]);
+    const int cx0 = X0 - OFF - (W - 1), cx1 = Xl - OFF;  // source x-cells of the CTA
+    double acc[W];  // logical window: acc[t] is node zs + OFF + t at plane zs
+#pragma unroll
+    for (int t = 0; t < W; ++t) acc[t] = 0.0;
+
+    for (int zs = Za - OFF - (W - 1); zs <= Zb - 1 - OFF; ++zs) {
+        for (int ys = Y0 - OFF - (W - 1); ys <= Yl - OFF; ++ys) {
+            const uint32_t rowc = (uint32_t)g.nx * ((uint32_t)ys + (uint32_t)g.ny * (uint32_t)zs);
+            const uint32_t sbeg = off[rowc + cx0];
+            const uint32_t send = off[rowc + cx1] + cnt[rowc + cx1];
+            // this thread's cells X-OFF-(W-1) .. X-OFF in this row, if the row is in its y-window
+            const int ty = Y - ys - OFF;
+            const bool uses = nv && ty >= 0 && ty < W;
+            uint32_t mbeg = 0, mend = 0;
+            if (uses) {
+                mbeg = off[rowc + X - OFF - (W - 1)];
+                mend = off[rowc + X - OFF] + cnt[rowc + X - OFF];
+            }
+            for (uint32_t piece = sbeg; piece < send; piece += kRowCap) {
+                const uint32_t pn = min((uint32_t)kRowCap, send - piece);
+                __syncthreads();  // the previous piece is consumed
+                for (uint32_t i = tid; i < pn; i += NT) {
+                    const uint32_t sl = piece + i;
+                    const double x = p.x[sl];
+                    if (__double_as_longlong(x) == -1LL) {  // slack sentinel
+                        s_xs[i] = -1;
+                        continue;
+                    }
+                    const double y = p.y[sl], z = p.z[sl];
+                    double f[3];
+                    s_xs[i] = locate_x(g, x, f[0]);
+                    locate_axis(y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
+                    locate_axis(z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
+                    int bits = 0;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        double w[W];
+                        int up;
+                        Shape<ORDER>::weights(f[a], w, up);
+                        bits |= up << a;
+#pragma unroll
+                        for (int t = 0; t < W; ++t) s_w[a][t][i] = w[t];
+                    }
+                    if (ORDER == 2) s_up[i] = (unsigned char)bits;
+                    s_q[i] = quantity ? quantity[sl] : qscale * p.w[sl];
+                }
+                __syncthreads();
+                if (!uses || mend <= piece || mbeg >= piece + pn) continue;
+                const uint32_t ib = max(mbeg, piece) - piece, ie = min(mend, piece + pn) - piece;
+                for (uint32_t i = ib; i < ie; ++i) {
+                    const int xs = s_xs[i];
+                    if (xs < 0) continue;
+                    const int tx = X - xs - OFF;
+                    const double q = s_q[i];
+                    const double sxv = s_w[0][tx][i];
+                    const double syv = s_w[1][ty][i];
+                    const int ub = ORDER == 2 ? s_up[i] : 0;
+                    if (ORDER == 2 && (!tap_valid<ORDER>(ub & 1, tx) || !tap_valid<ORDER>((ub >> 1) & 1, ty)))
+                        continue;
+#pragma unroll
+                    for (int t = 0; t < W; ++t) {
+                        if (ORDER == 2 && !tap_valid<ORDER>((ub >> 2) & 1, t)) continue;
+                        const double syz = __dmul_rn(syv, s_w[2][t][i]);
+                        const double sv = __dmul_rn(sxv, syz);
+                        acc[t] = __dadd_rn(acc[t], __dmul_rn(q, sv));
+                    }
+                }
+            }
+        }
+        // node zs + OFF has seen its last source plane
+        const int Zd = zs + OFF;
+        if (nv && Zd >= Za && Zd < Zb)
+            rho[(size_t)X + (size_t)g.nx * ((size_t)Y + (size_t)g.ny * (size_t)Zd)] = acc[0];
+#pragma unroll
+        for (int t = 0; t < W - 1; ++t) acc[t] = acc[t + 1];
+        acc[W - 1] = 0.0;
+    }
+}
+
 template <int ORDER>
 void prologue(const GridD& g, const CSoa& p, const double* quantity, double qscale, uint64_t slots, void* scratch,
               cudaStream_t st, double*& S, uint8_t*& upb) {
@@ -195,10 +398,39 @@ void prologue(const GridD& g, const CSoa& p, const double* quantity, double qsca
 template <int ORDER>
 void run_sorted(const GridD& g, const CSoa& p, const double* quantity, double qscale, const uint32_t* off, const uint32_t* cnt,
                 uint64_t slots, void* scratch, double* rho, cudaStream_t st) {
-    double* S;
-    uint8_t* upb;
-    prologue<ORDER>(g, p, quantity, qscale, slots, scratch, st, S, upb);
-    density_gather_sorted<ORDER><<<div_up(g.ncells, 128), 128, 0, st>>>(g, off, cnt, S, slots, upb, rho);
+    const Interior in = interior_of<ORDER>(g);
+    Interior skip = in;
+    if (!in.empty()) {
+        const int zlen = 16;
+        const dim3 grid(div_up(in.hi[0] - in.lo[0] + 1, kRowX), div_up(in.hi[1] - in.lo[1] + 1, kRowY),
+                        div_up(in.hi[2] - in.lo[2] + 1, zlen));
+        constexpr size_t smem = (size_t)(1 + 3 * Shape<ORDER>::W) * kRowCap * 8 + (size_t)kRowCap * 5;
+        static bool configured = false;
+        if (!configured) {
+            PICGPU_CUDA_TRY(cudaFuncSetAttribute(density_rows<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem));
+            configured = true;
+        }
+        density_rows<ORDER><<<grid, kRowX * kRowY, smem, st>>>(g, p, quantity, qscale, off, cnt, in, zlen, rho);
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+    } else {
+        skip.lo[0] = 1;  // nothing is interior
+        skip.hi[0] = 0;
+    }
+    // the boundary shell (wrapped, re-sorted sources): prologue + per-node gather
+    const bool shell = in.empty() || (uint64_t)(in.hi[0] - in.lo[0] + 1) * (in.hi[1] - in.lo[1] + 1) *
+                                             (in.hi[2] - in.lo[2] + 1) < g.ncells;
+    if (!shell) return;
+    if (ORDER == 1) {  // 8 taps per node: evaluating the weights on the fly beats a full prologue
+        density_gather_shell<ORDER><<<div_up(g.ncells, 128), 128, 0, st>>>(g, p, quantity, qscale, off, cnt, rho,
+                                                                           skip);
+    } else {  // 64 taps per node: weights once per slot (prologue), then the shell gather
+        double* S;
+        uint8_t* upb;
+        prologue<ORDER>(g, p, quantity, qscale, slots, scratch, st, S, upb);
+        density_gather_sorted<ORDER><<<div_up(g.ncells, 128), 128, 0, st>>>(g, off, cnt, S, slots, upb, rho, skip);
+    }
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }

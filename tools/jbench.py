@@ -15,6 +15,7 @@ S = pg.Session(G, order=order, timing=True)
 S.generate_plasma(ppc, uth, seed=1)
 for _ in range(3):
     S.step(0.5)
+S.step(0.5, pg.STEP_CURRENT | pg.STEP_DENSITY)  # loads the deposition modules before timing
 S.reset_phase_times()
 for _ in range(5):
     S.step(0.5, pg.STEP_CURRENT | pg.STEP_DENSITY)

@@ -12,8 +12,9 @@ cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
 if kre:
     cmd += ["-k", f"regex:{kre}"]
 rows = list(csv.reader(subprocess.run(cmd, capture_output=True, text=True).stdout.splitlines()))
-h = rows[1]
-data = [r for r in rows[2:] if len(r) == len(h)]
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+h = rows[starts[0] + 1]  # first matching kernel only
+data = [r for r in rows[starts[0] + 2:starts[1]] if len(r) == len(h)]
 ie, src, ss = h.index("Instructions Executed"), h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
 reasons = ["stall_wait", "stall_short_sb", "stall_long_sb", "stall_math", "stall_barrier", "stall_branch_resolving",
            "stall_dispatch", "stall_mio", "stall_no_inst", "stall_not_selected", "stall_selected", "stall_lg"]
