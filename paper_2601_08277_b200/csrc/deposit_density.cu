@@ -274,13 +274,16 @@ __global__ void density_gather_merge(const GridD g, const uint32_t* __restrict__
 // expression q*(sx*(sy*sz)) and round-to-nearest intrinsics: bit-identical to
 // density_gather_sorted (and to pic::deposit_density on this storage order).
 #ifndef PICGPU_RHO_RX
-#define PICGPU_RHO_RX 32
+#define PICGPU_RHO_RX 16
 #endif
 #ifndef PICGPU_RHO_RY
-#define PICGPU_RHO_RY 8
+#define PICGPU_RHO_RY 16
+#endif
+#ifndef PICGPU_RHO_ZLEN
+#define PICGPU_RHO_ZLEN 16
 #endif
 #ifndef PICGPU_RHO_CAP
-#define PICGPU_RHO_CAP 1024
+#define PICGPU_RHO_CAP 512
 #endif
 constexpr int kRowX = PICGPU_RHO_RX, kRowY = PICGPU_RHO_RY, kRowCap = PICGPU_RHO_CAP;
 
@@ -401,7 +404,7 @@ void run_sorted(const GridD& g, const CSoa& p, const double* quantity, double qs
     const Interior in = interior_of<ORDER>(g);
     Interior skip = in;
     if (!in.empty()) {
-        const int zlen = 16;
+        const int zlen = PICGPU_RHO_ZLEN;
         const dim3 grid(div_up(in.hi[0] - in.lo[0] + 1, kRowX), div_up(in.hi[1] - in.lo[1] + 1, kRowY),
                         div_up(in.hi[2] - in.lo[2] + 1, zlen));
         constexpr size_t smem = (size_t)(1 + 3 * Shape<ORDER>::W) * kRowCap * 8 + (size_t)kRowCap * 5;
