@@ -52,7 +52,8 @@ CONFIGS = {
     "c4": ((512, 128, 128), 8, 3, 0.01, 0.5, 10,
            "C4 (LWFA-like, static window): 512x128x128 cells, order 3, electrons from x-cell 64 with a linear "
            "density ramp over [64,128) to 8 ppc, u_th 0.01, plus a 10% beam with ux ~ U(5,50) in x-cells "
-           "[128,160); dt 0.5"),
+           "[128,160); dt 0.5; moving window: origin +1 cell every 2 steps, back column dropped, a fresh 8-ppc "
+           "column injected at the front (inside the timed region)"),
 }
 
 
@@ -243,10 +244,19 @@ def main():
         step = lambda: slab_step(S, ring, dt)  # noqa: E731
     populate(pg, S, args.config, ppc, u_th)
     n = S.num_particles
+    window = None
+    if args.config == "c4":
+        next_pid = [n]
+
+        def window():
+            _, inj = S.shift_window(ppc, u_th, 1, next_pid[0])
+            next_pid[0] += inj
     n_total = n * world  # conserved by the migration
     stream = torch.cuda.ExternalStream(S.stream)
-    for _ in range(args.warmup):
+    for it in range(args.warmup):
         step()
+        if window is not None and it % 2 == 1:
+            window()  # loads the window kernels and grows its buffers before timing
     if world == 1 and not args.slab:
         S.global_sort()  # also exercises the relayout kernels before the timed region
     S.reset_phase_times()
@@ -258,9 +268,11 @@ def main():
     with Clocks(local) as clk:
         barrier()
         e0.record(stream)
-        for _ in range(args.steps):
+        for it in range(args.steps):
             st = step()
             moved += st["moved"]
+            if window is not None and it % 2 == 1:  # C4 moving window: one cell every 2 steps
+                window()
             rebuilds += st["rebuilt"]
         e1.record(stream)
         e1.synchronize()

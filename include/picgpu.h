@@ -227,6 +227,16 @@ typedef struct picgpu_lwfa {
     uint64_t seed;
 } picgpu_lwfa;
 PICGPU_API int picgpu_session_generate_lwfa(picgpu_session* s, const picgpu_lwfa* cfg);
+/* C4 moving window: the grid origin moves +dx in x, particles
+ * behind it (the old x-column 0) are dropped, and a fresh column of ppc
+ * particles per cell is injected at the front (x-column nx-1): uniform in the
+ * cell (counters 6, 7, 8), Maxwellian u_th (counters 0..5), ids / RNG streams
+ * pid0, pid0+1, ... (cell-major).  The bins are rebuilt (stable counting sort).
+ * Not available on slab sessions. */
+PICGPU_API int picgpu_session_shift_window(picgpu_session* s, int ppc, double u_th, uint64_t seed, uint64_t pid0,
+                                           uint64_t* n_dropped, uint64_t* n_injected);
+/* The session's current grid (its origin moves with shift_window). */
+PICGPU_API int picgpu_session_grid(picgpu_session* s, picgpu_grid* out);
 /* One step: [push] -> [incremental sort] -> [deposit J] -> [deposit rho] -> [global sort]. */
 PICGPU_API int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_step_stats* out);
 PICGPU_API int picgpu_session_global_sort(picgpu_session* s);

@@ -256,6 +256,8 @@ def lib():
                                                                          C.POINTER(_D)]
     L.picgpu_session_set_kernel.argtypes = [_P, C.c_int]
     L.picgpu_session_generate_lwfa.argtypes = [_P, C.POINTER(LwfaConfig)]
+    L.picgpu_session_shift_window.argtypes = [_P, C.c_int, _D, _U64, _U64, C.POINTER(_U64), C.POINTER(_U64)]
+    L.picgpu_session_grid.argtypes = [_P, G]
     L.picgpu_session_make_workload.argtypes = [_P, C.POINTER(WorkloadConfig)]
     L.picgpu_slab_grid.argtypes = [G, C.c_int, C.c_int, C.c_int, G]
     L.picgpu_session_set_slab.argtypes = [_P, G, C.c_int, C.c_int, C.c_int]
@@ -497,6 +499,16 @@ class Session:
 
     def generate_plasma(self, ppc: int, u_th: float, seed: int = 1):
         _check(lib().picgpu_session_generate_plasma(self._h, ppc, u_th, seed))
+
+    def shift_window(self, ppc: int, u_th: float, seed: int, pid0: int):
+        """C4 moving window: origin += dx, drop x-column 0, inject a fresh last
+        column (ids pid0..).  Returns (dropped, injected); self.grid follows."""
+        d, i = C.c_uint64(), C.c_uint64()
+        _check(lib().picgpu_session_shift_window(self._h, ppc, u_th, seed, pid0, C.byref(d), C.byref(i)))
+        g = Grid()
+        lib().picgpu_session_grid(self._h, C.byref(g))
+        self.grid = g
+        return int(d.value), int(i.value)
 
     def generate_lwfa(self, cfg: "LwfaConfig"):
         """SURVEY 8(d) C4 population (density ramp + relativistic beam), generated in HBM."""

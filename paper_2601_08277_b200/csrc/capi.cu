@@ -628,6 +628,28 @@ int picgpu_session_generate_lwfa(picgpu_session* s, const picgpu_lwfa* c) {
     });
 }
 
+int picgpu_session_shift_window(picgpu_session* s, int ppc, double u_th, uint64_t seed, uint64_t pid0,
+                                uint64_t* n_dropped, uint64_t* n_injected) {
+    return guard([&] {
+        set_device(s);
+        if (s->slab) throw Status{PICGPU_ELOGIC, "shift_window: not available on a slab session"};
+        if (ppc < 0) throw Status{PICGPU_EINVAL, "shift_window: ppc must be >= 0"};
+        BinStore& bs = s->store;
+        picgpu_grid shifted = bs.hg;
+        shifted.ox = bs.hg.ox + bs.hg.dx;
+        uint64_t d = 0, in = 0;
+        bs.shift_window(shifted, ppc, u_th, seed, pid0, d, in);
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+        if (n_dropped) *n_dropped = d;
+        if (n_injected) *n_injected = in;
+    });
+}
+
+int picgpu_session_grid(picgpu_session* s, picgpu_grid* out) {
+    *out = s->store.hg;
+    return PICGPU_OK;
+}
+
 static void accumulate_phase(picgpu_session* s, int phase, int e0, int e1, uint64_t launches) {
     float ms = 0.f;
     PICGPU_CUDA_TRY(cudaEventElapsedTime(&ms, s->ev[e0], s->ev[e1]));

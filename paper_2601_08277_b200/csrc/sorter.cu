@@ -729,6 +729,68 @@ __global__ void k_generate_lwfa(const GridD g, const uint32_t* __restrict__ pfx,
     out.id[pid] = pid;
 }
 
+// Moving window, counts of the shifted layout: new bin (i,j,k) = old bin
+// (i+1,j,k) for i < nx-1; the last column receives the injected particles.
+__global__ void k_shift_counts(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off, uint32_t ncells,
+                               uint32_t nx, uint32_t ppc, uint32_t* __restrict__ cnt_new) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > ncells) return;
+    if (c == ncells) {
+        cnt_new[c] = 0;
+        return;
+    }
+    cnt_new[c] = c % nx == nx - 1 ? ppc : min(cnt[c + 1], off[c + 2] - off[c + 1]);
+}
+
+// Moving window relayout: new bin c <- old bin c+1 (the slots of an old
+// column-0 bin, which lands on a new last-column bin, are the dropped ones);
+// the new last-column bins are filled by the injector in place.
+__global__ void __launch_bounds__(256) k_relayout_shift(const Soa src, const uint32_t* __restrict__ soff,
+                                                        const uint32_t* __restrict__ cnt_new, const Soa dst,
+                                                        const uint32_t* __restrict__ doff, uint32_t ncells,
+                                                        const GridD gnew, int ppc, double u_th, uint64_t seed,
+                                                        uint64_t pid0) {
+    __shared__ uint32_t so[BPB + 1], sc[BPB], dof[BPB];
+    const uint32_t nx = (uint32_t)gnew.nx;
+    const uint32_t c0 = blockIdx.x * BPB;
+    const int nb = (int)umin((uint32_t)BPB, ncells - c0);
+    for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+        so[b] = soff[umin(c0 + b + 1, ncells)];
+        if (b < nb) {
+            sc[b] = (c0 + b) % nx == nx - 1 ? 0u : cnt_new[c0 + b];
+            dof[b] = doff[c0 + b];
+        }
+    }
+    __syncthreads();
+    for (uint32_t s = so[0] + threadIdx.x; s < so[nb]; s += blockDim.x) {
+        const int b = find_bin(so, nb, s);
+        const uint32_t r = s - so[b];
+        if (r < sc[b]) copy_particle(src, s, dst, (uint64_t)dof[b] + r);
+    }
+    // injection into this block's last-column bins
+    for (int t = threadIdx.x; t < nb * ppc; t += blockDim.x) {
+        const int b = t / ppc, r = t % ppc;
+        const uint32_t c = c0 + b;
+        if (c % nx != nx - 1) continue;
+        const uint32_t row = c / nx;  // j + ny*k
+        const int j = (int)(row % (uint32_t)gnew.ny), k = (int)(row / (uint32_t)gnew.ny);
+        const uint64_t pid = pid0 + (uint64_t)row * ppc + r;
+        const uint64_t d = (uint64_t)dof[b] + r;
+        dst.x[d] = __dadd_rn(gnew.ox, __dmul_rn(__dadd_rn((double)(nx - 1), uniform01(seed, pid, 6)), gnew.dx));
+        dst.y[d] = __dadd_rn(gnew.oy, __dmul_rn(__dadd_rn((double)j, uniform01(seed, pid, 7)), gnew.dy));
+        dst.z[d] = __dadd_rn(gnew.oz, __dmul_rn(__dadd_rn((double)k, uniform01(seed, pid, 8)), gnew.dz));
+        const double ux = u_th * gaussian(seed, pid, 0);
+        const double uy = u_th * gaussian(seed, pid, 1);
+        const double uz = u_th * gaussian(seed, pid, 2);
+        const double gam = sqrt(1.0 + ux * ux + uy * uy + uz * uz);
+        dst.vx[d] = ux / gam;
+        dst.vy[d] = uy / gam;
+        dst.vz[d] = uz / gam;
+        dst.w[d] = 1.0 / (double)ppc;
+        dst.id[d] = pid;
+    }
+}
+
 // make_workload (workload.hpp:75-125): particle pid = cell-major (x fastest),
 // then a px*py*pz sub-lattice in the cell (x fastest); Maxwellian velocities,
 // optional shear drift, truncation at the displacement cap; W = 1.
@@ -1139,6 +1201,44 @@ void BinStore::push_and_resort(bool push, double dt, double cap2, StepCounters& 
     PICGPU_CUDA_TRY(cudaMemcpyAsync(&h32, off2.as<uint32_t>() + nc, 4, cudaMemcpyDeviceToHost, st));
     PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
     full_sort_from_B(h32);
+}
+
+void BinStore::shift_window(const picgpu_grid& shifted, int ppc, double u_th, uint64_t seed, uint64_t pid0,
+                            uint64_t& dropped, uint64_t& injected) {
+    const size_t nc = g.ncells;
+    injected = (uint64_t)g.ny * g.nz * (uint64_t)ppc;
+    if (!nc) return;
+    // counts and fresh-slack layout of the shifted grid (bins keep their order)
+    cnt2.ensure((nc + 1) * 4);
+    k_shift_counts<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt.as<uint32_t>(), off.as<uint32_t>(),
+                                                                   (uint32_t)nc, (uint32_t)g.nx, (uint32_t)ppc,
+                                                                   cnt2.as<uint32_t>());
+    note_launch();
+    DevBuf& tot64 = vals;  // particles of the new layout: sum of the new counts
+    tot64.ensure((nc + 1) * 8);
+    cub_exclusive_sum_u32_to_u64(cnt2.as<uint32_t>(), tot64.as<unsigned long long>(), nc + 1, cub_tmp, st);
+    unsigned long long nnew = 0;
+    PICGPU_CUDA_TRY(cudaMemcpyAsync(&nnew, tot64.as<unsigned long long>() + nc, 8, cudaMemcpyDeviceToHost, st));
+    k_caps_from_cnt<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt2.as<uint32_t>(), (uint32_t)nc,
+                                                                    caps.as<uint32_t>(), onepg, min_gap);
+    note_launch();
+    layout_from_counts(0);  // synchronises
+    B.ensure(capacity_next + capacity_next / 8);
+    mflag.ensure(capacity_next + capacity_next / 8 + 1);
+    PICGPU_CUDA_TRY(cudaMemsetAsync(B.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
+    hg = shifted;
+    g = make_grid(shifted);
+    k_relayout_shift<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt2.as<uint32_t>(),
+                                                                 B.soa(), off2.as<uint32_t>(), (uint32_t)nc, g, ppc,
+                                                                 u_th, seed, pid0);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+    swap_soa(A, B);
+    swap_buf(off, off2);
+    swap_buf(cnt, cnt2);
+    capacity = capacity_next;
+    dropped = n + injected - nnew;
+    n = nnew;
 }
 
 bool BinStore::finish_incremental(StepCounters& out) {

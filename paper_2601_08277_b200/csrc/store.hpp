@@ -64,6 +64,7 @@ struct BinStore {
 
     SoaBuf A, B;              // A: binned store; B: spare (re-layout target, packed staging)
     DevBuf off, cnt, off2;    // off: ncells+1 (u32), cnt: ncells (u32)
+    DevBuf cnt2;              // counts of a layout being built (moving window)
     DevBuf keys, keys2, skeys, vals, vals2, start, endp, caps, cub_tmp;
     DevBuf mflag;             // per-slot mover flag (u8)
     SoaBuf M;                 // mover records
@@ -113,6 +114,10 @@ struct BinStore {
     // Push (optional) with only the moved count, then a full stable counting
     // sort of the store (PICGPU_STEP_RESORT).  Synchronous.
     void push_and_resort(bool push, double dt, double cap2, StepCounters& out);
+    // C4 moving window: drop x-column 0, shift the grid origin by one cell
+    // (`shifted`), inject a fresh last column, re-sort.  Synchronous.
+    void shift_window(const picgpu_grid& shifted, int ppc, double u_th, uint64_t seed, uint64_t pid0,
+                      uint64_t& dropped, uint64_t& injected);
 
     uint32_t* d_off() const { return off.as<uint32_t>(); }
     uint32_t* d_cnt() const { return cnt.as<uint32_t>(); }

@@ -89,3 +89,49 @@ def test_lwfa_steps_lockstep_with_oracle(pg, orc, order):
         rho = orc.deposit_density(g, order, q, -1.0 * got.w)
         assert np.array_equal(S.density(), rho)  # bit-exact, storage order
     assert st["moved"] > 0
+
+
+def test_moving_window_shift(pg, orc):
+    """Every 2 steps the window moves one cell: the particles of the back column
+    are dropped, the rest keep their exact state, a fresh column (ids pid0..,
+    recipe positions) enters at the front, and the steps that follow stay in
+    lockstep with the oracle on the shifted grid."""
+    G, c = _cfg(pg)
+    S = pg.Session(G, 3)
+    S.generate_lwfa(c)
+    pid = S.num_particles
+    for cycle in range(3):
+        for _ in range(2):
+            S.step(0.5)
+        before = S.particles()
+        ox_new = S.grid.ox + S.grid.dx
+        dropped, injected = S.shift_window(8, 0.01, c.seed, pid)
+        assert S.grid.ox == ox_new and injected == G.ny * G.nz * 8
+        after = S.particles()
+        keep = before.x >= ox_new
+        assert dropped == int((~keep).sum())
+        surv = np.argsort(before.id[keep])
+        got = after.id < pid
+        o = np.argsort(after.id[got])
+        for k in ("x", "y", "z", "vx", "vy", "vz", "w", "id"):
+            assert np.array_equal(getattr(after, k)[got][o], getattr(before, k)[keep][surv]), (cycle, k)
+        new = np.nonzero(~got)[0]
+        assert sorted(after.id[new]) == list(range(pid, pid + injected))
+        for t in range(0, injected, 37):
+            q = new[after.id[new] == pid + t][0]
+            cell = t // 8
+            j, k = cell % G.ny, cell // G.ny
+            assert after.x[q] == S.grid.ox + (G.nx - 1 + orc.uniform01(c.seed, pid + t, 6)) * G.dx
+            assert after.y[q] == S.grid.oy + (j + orc.uniform01(c.seed, pid + t, 7)) * G.dy
+            assert after.z[q] == S.grid.oz + (k + orc.uniform01(c.seed, pid + t, 8)) * G.dz
+        pid += injected
+        # lockstep on the shifted grid, from the session's own state
+        g = O.Grid.make(G.nx, G.ny, G.nz, dx=G.dx, dy=G.dy, dz=G.dz, origin=(S.grid.ox, S.grid.oy, S.grid.oz))
+        ref = {k: getattr(after, k).copy() for k in ("x", "y", "z", "vx", "vy", "vz", "w", "id")}
+        st = S.step(0.5)
+        assert st["moved"] == orc.advance(g, 0.5, ref)
+        J = S.current()
+        assert peak_rel_err((J.jx, J.jy, J.jz), orc.deposit_current(g, 3, ref, -1.0)) <= 1e-12
+        p2 = S.particles()
+        o2, w2 = np.argsort(p2.id), np.argsort(ref["id"])
+        assert np.array_equal(p2.x[o2], ref["x"][w2])
