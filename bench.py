@@ -54,6 +54,10 @@ CONFIGS = {
            "density ramp over [64,128) to 8 ppc, u_th 0.01, plus a 10% beam with ux ~ U(5,50) in x-cells "
            "[128,160); dt 0.5; moving window: origin +1 cell every 2 steps, back column dropped, a fresh 8-ppc "
            "column injected at the front (inside the timed region)"),
+    # strong scaling over x-slabs; needs N >= 4 B200s (2.1e9 particles)
+    "c5": ((2048, 256, 256), 16, 3, 0.05, 0.5, 10,
+           "C5: 2048x256x256 cells, 16 ppc, order 3, u_th 0.05, dt 0.5, x-slabs of 2048/N cells per GPU "
+           "(strong scaling)"),
 }
 
 
@@ -230,16 +234,26 @@ def main():
         torch.cuda.synchronize()
 
     grid = make_grid(pg, nx)
-    if isinstance(nx, tuple) and world > 1:
-        raise SystemExit("multi-GPU runs use the cubic configs (x-slabs of a (n*N) x n x n box)")
+    strong = args.config == "c5"
+    G_dims = nx if isinstance(nx, tuple) else (nx * world, nx, nx)
+    if strong and world < 4:
+        raise SystemExit("c5 (2.1e9 particles) needs at least 4 GPUs: torchrun --nproc-per-node 4|8 bench.py --config c5")
+    if isinstance(nx, tuple) and world > 1 and not strong:
+        raise SystemExit("multi-GPU runs use the cubic configs (x-slabs of a (n*N) x n x n box) or c5")
     if world == 1 and not args.slab:
         S = pg.Session(grid, order=order, device=local, timing=True)
         step = lambda: S.step(dt)  # noqa: E731
     else:
         from paper_2601_08277_b200.slab import RingExchange, SlabSession, slab_step
 
-        G = pg.Grid.make(nx * world, nx, nx)
-        S = SlabSession(G, rank * nx, (rank + 1) * nx, order=order, device=local, timing=True)
+        if strong:  # one global box split into x-slabs
+            from paper_2601_08277_b200.slab import slab_range
+
+            G = pg.Grid.make(*nx)
+            S = SlabSession(G, *slab_range(nx[0], world, rank), order=order, device=local, timing=True)
+        else:  # weak scaling: a C2-sized slab per rank
+            G = pg.Grid.make(nx * world, nx, nx)
+            S = SlabSession(G, rank * nx, (rank + 1) * nx, order=order, device=local, timing=True)
         ring = RingExchange()
         step = lambda: slab_step(S, ring, dt)  # noqa: E731
     populate(pg, S, args.config, ppc, u_th)
@@ -251,7 +265,11 @@ def main():
         def window():
             _, inj = S.shift_window(ppc, u_th, 1, next_pid[0])
             next_pid[0] += inj
-    n_total = n * world  # conserved by the migration
+    n_total = n * world
+    if dist is not None:  # particles of all ranks (conserved by the migration)
+        tn = torch.tensor([float(n)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tn)
+        n_total = int(tn.item())
     stream = torch.cuda.ExternalStream(S.stream)
     for it in range(args.warmup):
         step()
@@ -366,14 +384,15 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY 8(d) seeded plasma generated in HBM; no dataset)",
             "config": {"workload": desc + "; step = push + incremental sort + J deposit",
-                       "grid": list(nx) if isinstance(nx, tuple) else [nx * world, nx, nx], "ppc": ppc,
+                       "grid": list(G_dims), "ppc": ppc,
                        "order": order, "particles_per_gpu": n,
                        "l2": f"inputs larger than L2 ({n * 64 / 1e9:.1f} GB particle store)",
                        "parallelism": "single" if world == 1 else
-                       f"x-slabs x{world} of a {nx * world}x{nx}x{nx} box, NCCL ring exchange (migration + J guards)"},
+                       f"x-slabs x{world} of a {'x'.join(map(str, G_dims))} box, NCCL ring exchange "
+                       "(migration + J guards)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
             "phases_ms_total": {k: v[0] for k, v in phases.items()},
