@@ -785,14 +785,6 @@ struct WCfg {
     static constexpr size_t SMEM = (size_t)(2 * R * PATCH + STAGE) * sizeof(double);
 };
 
-__device__ __forceinline__ double lds64(const double* p) {
-    // explicit 64-bit shared load: a broadcast LDS.64 costs one wavefront,
-    // whereas the LDS.128 nvcc would merge neighbouring doubles into costs four
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
-    return v;
-}
-
 template <int ORDER>
 __global__ void __launch_bounds__(WCfg::NT, WCfg::MINB)
     deposit_current_warp_kernel(const GridD g, const CSoa p, const uint32_t* __restrict__ off,

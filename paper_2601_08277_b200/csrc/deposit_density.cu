@@ -322,8 +322,9 @@ __global__ void __launch_bounds__(kRowX * kRowY)
             const bool uses = nv && ty >= 0 && ty < W;
             uint32_t mbeg = 0, mend = 0;
             if (uses) {
-                mbeg = off[rowc + X - OFF - (W - 1)];
-                mend = off[rowc + X - OFF] + cnt[rowc + X - OFF];
+                const uint32_t c_lo = rowc + (uint32_t)(X - OFF - (W - 1)), c_hi = rowc + (uint32_t)(X - OFF);
+                mbeg = off[c_lo];
+                mend = off[c_hi] + cnt[c_hi];
             }
             for (uint32_t piece = sbeg; piece < send; piece += kRowCap) {
                 const uint32_t pn = min((uint32_t)kRowCap, send - piece);
