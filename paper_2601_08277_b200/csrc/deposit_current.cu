@@ -49,6 +49,20 @@ template <>
 struct JCfg<1> {
     static constexpr int G = 1, PX = 32, PY = 4, MINB = 4, CH = 1;
 };
+// QSP/TSC with 8 lanes per pencil (lane = jy x x-half, 24 accumulators each):
+// fewer registers per thread, more warps per SM, more shared loads per FMA.
+#ifndef PICGPU_G8_PX
+#define PICGPU_G8_PX 4
+#endif
+#ifndef PICGPU_G8_PY
+#define PICGPU_G8_PY 4
+#endif
+#ifndef PICGPU_G8_MINB
+#define PICGPU_G8_MINB 4
+#endif
+struct JCfgG8 {
+    static constexpr int G = 8, PX = PICGPU_G8_PX, PY = PICGPU_G8_PY, MINB = PICGPU_G8_MINB, CH = 8;
+};
 // CIC on the v3 kernel: 2 lanes per pencil (lane = jy), 12 accumulators each.
 #ifndef PICGPU_CIC_PX
 #define PICGPU_CIC_PX 16
@@ -539,7 +553,10 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
     constexpr int FX = PX + W - 1, FY = PY + W - 1;
     constexpr int NODES = 3 * FX * FY;
     constexpr int NIT = (NODES + L::NT - 1) / L::NT;
-    static_assert(G == W && NJ == 1 && (W & (W - 1)) == 0, "v3: one jy per lane, power-of-two window");
+    // lane = ly + W * xh (ly = jy): G = W * XS lanes per pencil, each owning IX = W / XS x-taps
+    constexpr int XS = G / W, IX = W / XS;
+    static_assert(G == W * XS && W % XS == 0 && (W & (W - 1)) == 0, "v3: lanes = jy x x-halves");
+    (void)NJ;
     // 1/6^3 (QSP) or 1/2^3 (TSC) of the scaled weights, folded into q
     const double qs = q * (ORDER == 3 ? 1.0 / 216.0 : ORDER == 2 ? 0.125 : 1.0);
 
@@ -549,6 +566,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 
     const int tid = threadIdx.x;
     const int grp = tid / G, lg = tid % G;
+    const int ly = lg % W, xh = lg / W;  // this lane's jy and x-half
     const int px = grp % PX, py = grp / PX;
     const int i0 = blockIdx.x * PX, j0 = blockIdx.y * PY;
     const int k0 = blockIdx.z * zlen;
@@ -596,11 +614,11 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 
     // acc[s]: physical slot s of the sliding z window; at step k the slot s
     // holds logical plane (s - R) mod W of the window, R = (k - k0) mod W
-    double acc[W][W][3];
+    double acc[W][IX][3];
 #pragma unroll
     for (int sl = 0; sl < W; ++sl)
 #pragma unroll
-        for (int ix = 0; ix < W; ++ix)
+        for (int ix = 0; ix < IX; ++ix)
 #pragma unroll
             for (int c = 0; c < 3; ++c) acc[sl][ix][c] = 0.0;
 
@@ -668,15 +686,15 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                 for (int jj0 = 0; jj0 < CH; ++jj0) {
                     if (jj0 >= nn) break;
                     const double* r = stage + jj0 * L::SS + grp;
-                    const double yv = r[(3 * W + lg) * L::FSS];
+                    const double yv = r[(3 * W + ly) * L::FSS];
                     double b[W];
 #pragma unroll
                     for (int sl = 0; sl < W; ++sl) b[sl] = yv * szb[sl][jj0 * L::SS];
 #pragma unroll
                     for (int c = 0; c < 3; ++c)
 #pragma unroll
-                        for (int ix = 0; ix < W; ++ix) {
-                            const double av = r[(c * W + ix) * L::FSS];
+                        for (int ix = 0; ix < IX; ++ix) {
+                            const double av = r[(c * W + xh * IX + ix) * L::FSS];
 #pragma unroll
                             for (int sl = 0; sl < W; ++sl) acc[sl][ix][c] = fma(av, b[sl], acc[sl][ix][c]);
                         }
@@ -695,8 +713,8 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
 #pragma unroll
-                    for (int ix = 0; ix < W; ++ix) {
-                        pp[((lg * W + ix) * 3 + c) * L::PSTRIDE] = acc[S][ix][c];
+                    for (int ix = 0; ix < IX; ++ix) {
+                        pp[((ly * W + xh * IX + ix) * 3 + c) * L::PSTRIDE] = acc[S][ix][c];
                         acc[S][ix][c] = 0.0;
                     }
             };
@@ -1342,7 +1360,11 @@ void launch_order(const GridD& g, const CSoa& p, const uint32_t* off, const uint
         return e && std::string(e) == "v1";
     }();
     // v3 (default): orders 2/3 with JCfg<ORDER>, CIC with 2 lanes per pencil
+#ifdef PICGPU_J_G8
+    using C3 = std::conditional_t<ORDER == 1, JCfgCic3, JCfgG8>;
+#else
     using C3 = std::conditional_t<ORDER == 1, JCfgCic3, JCfg<ORDER>>;
+#endif
     if (v1)
         launch_kernel<ORDER, JCfg<ORDER>, false>(g, p, off, cnt, q, j, num_sms, st);
     else
