@@ -74,7 +74,7 @@ static void swap_buf(DevBuf& x, DevBuf& y) {
 // ---------------------------------------------------------------------------
 // device helpers
 
-__device__ __forceinline__ void copy_particle(const Soa& src, uint64_t s, const Soa& dst, uint64_t d) {
+__device__ __forceinline__ void copy_particle(const Soa src, uint64_t s, const Soa dst, uint64_t d) {
     dst.x[d] = src.x[s];
     dst.y[d] = src.y[s];
     dst.z[d] = src.z[s];
@@ -411,7 +411,10 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
 // than kHoleCap front holes (a bin emptying out) fall back to that slide.
 constexpr int kHoleCap = 32;
 
-__global__ void __launch_bounds__(256) k_compact(const Soa A, const uint32_t* __restrict__ off, uint32_t* cnt,
+#ifndef PICGPU_COMPACT_MINB
+#define PICGPU_COMPACT_MINB 8  // latency-bound: full occupancy beats spill-free registers (191 vs 209+ us at C2)
+#endif
+__global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_compact(const Soa A, const uint32_t* __restrict__ off, uint32_t* cnt,
                                                  const uint8_t* __restrict__ mflag, uint32_t* dep, uint32_t ncells) {
     __shared__ uint32_t holes[256 / 8][kHoleCap];
     const int lane = threadIdx.x & 31;
