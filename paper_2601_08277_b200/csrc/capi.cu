@@ -679,6 +679,9 @@ static void enqueue_deposits(picgpu_session* s, uint32_t flags, uint64_t* lj, ui
         check_density_grid(bs.hg, s->order);
         const uint64_t l0 = g_launches.load();
         if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[5], st));
+        // rho is bit-exact on the storage order: pack the bins first, so the
+        // order it sums in is the order downloads report
+        bs.fill_holes();
         s->rho.ensure((size_t)g.ncells * 8);
         s->dscratch.ensure(density_scratch_bytes(s->order, bs.capacity));
         launch_deposit_density(s->order, g, bs.A.soa(), nullptr, s->q, bs.d_off(), bs.d_cnt(), bs.capacity,
@@ -855,9 +858,12 @@ int picgpu_session_download_bins(picgpu_session* s, uint32_t* bin_offset, uint32
     return guard([&] {
         set_device(s);
         const size_t nc = s->store.g.ncells;
+        std::vector<uint32_t> h(nc);
         d2h(bin_offset, s->store.off.p, (nc + 1) * 4, s->st);
         d2h(bin_count, s->store.cnt.p, nc * 4, s->st);
+        if (nc) d2h(h.data(), s->store.holes.p, nc * 4, s->st);
         PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
+        for (size_t c = 0; c < nc; ++c) bin_count[c] -= h[c];  // particles, not extent (holes are gaps)
     });
 }
 

@@ -37,6 +37,11 @@ struct GridD {
     int gpow2Lx;
 };
 
+// A slot whose x holds the all-ones sentinel (a NaN no valid particle can
+// carry) is empty: bin slack, or a hole left by a departed particle.
+__device__ __forceinline__ bool is_gap(double x) { return __double_as_longlong(x) == -1LL; }
+constexpr long long kGapBits = -1LL;
+
 // Store-cell codes of particles that left a slab (push / import routing).
 constexpr uint32_t kLeaveLeft = 0xFFFFFFFEu;
 constexpr uint32_t kLeaveRight = 0xFFFFFFFDu;

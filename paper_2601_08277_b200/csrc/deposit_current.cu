@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                 for (int t = 0; t < n_c; ++t) {
                     PData d;
                     load_particle(p, c_off + t, d);
+                    if (is_gap(d.x)) continue;  // a hole of the bin (GPMA gap)
                     double a[3][W], sy[W], sz[W];
                     particle_window_cell<ORDER>(g, d, q, i, j, k, a, sy, sz);
                     double syv[NJ];
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
                     // prologue of this lane's particle -> staging slot (lg, grp)
                     {
                         const PData cur = nxt;
-                        const bool valid = base + lg < n_c;
+                        const bool valid = base + lg < n_c && !is_gap(cur.x);  // holes count as padding
                         // prefetch the next chunk: same cell, or the next cell's first chunk
                         if (base + CH < m) {
                             if (base + CH + lg < n_c) load_particle(p, c_off + base + CH + lg, nxt);
@@ -661,7 +662,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
             for (int base = 0; base < m; base += CH) {
                 {
                     const PData cur = nxt;
-                    const bool valid = base + lg < n_c;
+                    const bool valid = base + lg < n_c && !is_gap(cur.x);  // holes count as padding
                     if (base + CH < m) {
                         if (base + CH + lg < n_c) load_particle(p, c_off + base + CH + lg, nxt);
                     } else if (lg < n_n) {
@@ -934,6 +935,10 @@ __global__ void __launch_bounds__(WCfg::NT, WCfg::MINB)
                     if (nvalid) {  // prologue: shape.hpp:64-85 + particle_weights :46-50
                         double a[3][W], sy[W], sz[W];
                         particle_window_fast<ORDER>(g, nxt, q, a, sy, sz);
+                        if (is_gap(nxt.x)) {  // a hole of the bin (GPMA gap): zero charge
+#pragma unroll
+                            for (int t = 0; t < W; ++t) a[0][t] = a[1][t] = a[2][t] = sy[t] = sz[t] = 0.0;
+                        }
                         // fields: a[c][ix] at f = c*4 + ix; b[kz][jy] = sy*sz at f = 12 + kz*4 + jy
                         double* rr = recs + lane;
 #pragma unroll
@@ -1183,6 +1188,10 @@ __global__ void __launch_bounds__(MCfg::NT, MCfg::MINB)
                     if (nvalid) {  // prologue: shape.hpp:64-85 + particle_weights :46-50
                         double a[3][W], sy[W], sz[W];
                         particle_window<ORDER>(g, nxt, q, a, sy, sz);
+                        if (is_gap(nxt.x)) {  // a hole of the bin (GPMA gap): zero charge
+#pragma unroll
+                            for (int t = 0; t < W; ++t) a[0][t] = a[1][t] = a[2][t] = sy[t] = sz[t] = 0.0;
+                        }
                         double* rr = recs + lane;
 #pragma unroll
                         for (int c = 0; c < 3; ++c)

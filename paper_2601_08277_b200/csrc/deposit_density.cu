@@ -32,6 +32,10 @@ __global__ void density_prologue(const GridD g, const CSoa p, const double* __re
     const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= slots) return;
     const double x = p.x[s], y = p.y[s], z = p.z[s];
+    if (is_gap(x)) {  // slack or a hole: a NaN quantity marks it for the gathers
+        S[(size_t)(3 * Shape<ORDER>::W) * slots + s] = __longlong_as_double(0x7ff8000000000000LL);
+        return;
+    }
     double f[3];
     locate_x(g, x, f[0]);
     locate_axis(y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
@@ -130,6 +134,8 @@ __global__ void density_gather_sorted(const GridD g, const uint32_t* __restrict_
                 const uint32_t o = off[c], n = cnt[c];
                 for (uint32_t u = 0; u < n; ++u) {
                     const uint32_t s = o + u;
+                    const double qv = SQ[s];
+                    if (qv != qv) continue;  // a hole of the bin (GPMA gap)
                     if (ORDER == 2) {
                         const int b = upb[s];
                         if (!tap_valid<ORDER>(b & 1, xt[xi]) || !tap_valid<ORDER>((b >> 1) & 1, yt[yi]) ||
@@ -138,7 +144,7 @@ __global__ void density_gather_sorted(const GridD g, const uint32_t* __restrict_
                     }
                     const double syz = __dmul_rn(Sy[s], Sz[s]);
                     const double sv = __dmul_rn(Sx[s], syz);
-                    acc = __dadd_rn(acc, __dmul_rn(SQ[s], sv));
+                    acc = __dadd_rn(acc, __dmul_rn(qv, sv));
                 }
             }
         }
@@ -174,9 +180,11 @@ __global__ void density_gather_shell(const GridD g, const CSoa p, const double* 
                 const uint32_t o = off[c], n = cnt[c];
                 for (uint32_t u = 0; u < n; ++u) {
                     const uint32_t sl = o + u;
+                    const double xv = p.x[sl];
+                    if (is_gap(xv)) continue;  // a hole of the bin (GPMA gap)
                     double f[3], w[3][W];
                     int up[3];
-                    locate_x(g, p.x[sl], f[0]);
+                    locate_x(g, xv, f[0]);
                     locate_axis(p.y[sl], g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
                     locate_axis(p.z[sl], g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
 #pragma unroll

@@ -4,7 +4,7 @@
 // Reference anchors (proj/include/pic/):
 //   gpma_build          gpma.hpp:379-402  -> BinStore::full_sort_from_B (stable radix sort by cell)
 //   Gpma::layout        gpma.hpp:269-302  -> k_counts_caps + scan (same capacity rule)
-//   detect_moves        gpma.hpp:162-177  -> k_push (fused with the push, warp-ballot append) + k_compact
+//   detect_moves        gpma.hpp:162-177  -> k_push (fused with the push; departures leave holes)
 //   apply_moves/insert  gpma.hpp:110-125, :248-262 -> k_insert (per-bin atomic tail cursor into slack)
 //   borrow/overflow     gpma.hpp:337-370  -> overflow list -> rebuild (relayout with fresh slack)
 //   rebuild             gpma.hpp:130-143  -> BinStore::rebuild_overflow
@@ -232,7 +232,6 @@ __global__ void __launch_bounds__(256) k_relayout(const Soa src, const uint32_t*
 // Every slack slot holds a sentinel x (all-ones bit pattern, a NaN no valid
 // particle can carry: non-finite positions are rejected), so the push can
 // stream over raw slots without knowing the bin layout.
-__device__ __forceinline__ bool is_gap(double x) { return __double_as_longlong(x) == -1LL; }
 
 // floor((x - o) / h) exactly as locate_axis computes it (before its range
 // handling).  For u >= 0 the fraction u - floor(u) is exact and < 1, so equal
@@ -267,13 +266,22 @@ __device__ __forceinline__ double axis_floor(double x, double o, double h, doubl
 #define PICGPU_PUSH_CONDLOAD 0
 #endif
 
+// A departure: the slot becomes a hole of its bin (sentinel x) and joins the
+// bin's hole list.
+__device__ __forceinline__ void push_hole(const Soa& A, uint64_t s, uint32_t b, const uint32_t* __restrict__ off,
+                                          uint32_t* __restrict__ holes, uint32_t* __restrict__ hl) {
+    A.x[s] = __longlong_as_double(kGapBits);
+    hl[off[b] + atomicAdd(&holes[b], 1u)] = (uint32_t)s;
+}
+
 // RECORD = false: push and count the moved particles only (the store is
 // re-sorted from scratch afterwards; no flags, movers or departures).
 template <bool PUSH, int UNR, bool P2, bool RECORD = true>
-__global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, const Soa A, uint64_t slots, uint8_t* __restrict__ mflag,
+__global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, const Soa A, uint64_t slots,
                                               double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
-                                              uint32_t mcap, uint32_t* __restrict__ dep, StepCounters* ctr,
-                                              double* __restrict__ L, uint32_t lcap) {
+                                              uint32_t mcap, const uint32_t* __restrict__ off,
+                                              uint32_t* __restrict__ holes, uint32_t* __restrict__ hl,
+                                              StepCounters* ctr, double* __restrict__ L, uint32_t lcap) {
     __shared__ unsigned s_cnt, s_base, s_mv;
     if (threadIdx.x == 0) s_cnt = s_mv = 0;
     __syncthreads();
@@ -343,7 +351,6 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
             local_moved += moved ? 1u : 0u;
             continue;
         }
-        mflag[s] = moved ? 1 : 0;
         if (moved) {
             ++local_moved;
             if (nc[u] >= kLeaveRight) {  // left the slab: exchange record for the neighbour rank
@@ -355,10 +362,9 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
                     r[3] = vx[u]; r[4] = vy[u]; r[5] = vz[u];
                     r[6] = A.w[s];
                     r[7] = __longlong_as_double((long long)A.id[s]);
-                    atomicAdd(&dep[before[u]], 1u);
+                    push_hole(A, s, before[u], off, holes, hl);
                 } else {
                     raise_error(&ctr->err, PICGPU_ELENGTH);
-                    mflag[s] = 0;
                 }
             } else {
                 lidx[u] = (int)atomicAdd(&s_cnt, 1u);
@@ -391,31 +397,35 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
             M.w[idx] = A.w[s];
             M.id[idx] = A.id[s];
             mcell[idx] = nc[u];
-            atomicAdd(&dep[before[u]], 1u);  // result unused: RED
+            push_hole(A, s, before[u], off, holes, hl);
         } else {
-            mflag[s] = 2;  // stays in its stale bin; host re-sorts fully
+            // not recorded (mover buffer full): stays in its stale bin; nmovers > mcap
+            // tells the host to re-sort fully
         }
     }
 }
 
-// In-bin compaction of every bin that lost particles (the GPU side of
-// Gpma::delete_slot, gpma.hpp:90-95).  A warp watches 32 bins' departure
-// counts with one ballot and compacts the dirty ones four at a time, one per
-// 8-lane group.  With nd departures out of len slots, the first len-nd slots
-// (front) keep their kept particles in place; each departure hole in the front
-// takes one kept particle from the tail [len-nd, len) (the k-th front hole the
-// k-th tail survivor), and the tail becomes slack.  One move per hole -- the
-// in-bin order is not part of the contract (rho follows the storage order
-// whatever it is) -- instead of sliding every particle behind a hole down
-// (stable: 12% of all particles moved per step at C2, 0.22 ms).  Bins with more
-// than kHoleCap front holes (a bin emptying out) fall back to that slide.
+// Gaps, as in the reference's GPMA: a departing particle leaves a hole in its
+// bin (delete_in_bin only marks the slot empty, gpma.hpp:328-335) and the next
+// arrivals into that bin fill holes before they take tail slack (insert uses a
+// spare slot of the bin, gpma.hpp:248-267).  A bin's extent [off, off+cnt)
+// then holds particles and holes (sentinel x); holes[c] counts the holes.  The
+// deposits skip holes; the per-step compaction pass of a packed store is gone.
+//
+// k_fill_holes makes every bin packed again before an operation that needs it
+// (rebuild, global sort, downloads, window shift): a warp watches 32 bins'
+// hole counts with one ballot and fills four holey bins at a time, one per
+// 8-lane group.  With nd holes in an extent of len slots, each hole among the
+// first len-nd slots takes one particle from the tail [len-nd, len) (the k-th
+// front hole the k-th tail particle), and the tail becomes slack.  Bins with
+// more than kHoleCap front holes fall back to a stable slide.
 constexpr int kHoleCap = 32;
 
 #ifndef PICGPU_COMPACT_MINB
 #define PICGPU_COMPACT_MINB 8  // latency-bound: full occupancy beats spill-free registers (191 vs 209+ us at C2)
 #endif
-__global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_compact(const Soa A, const uint32_t* __restrict__ off, uint32_t* cnt,
-                                                 const uint8_t* __restrict__ mflag, uint32_t* dep, uint32_t ncells) {
+__global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_fill_holes(const Soa A, const uint32_t* __restrict__ off,
+                                                                    uint32_t* cnt, uint32_t* dep, uint32_t ncells) {
     __shared__ uint32_t holes[256 / 8][kHoleCap];
     const int lane = threadIdx.x & 31;
     const int grp = lane >> 3, gl = lane & 7;  // four groups of 8 lanes, one dirty bin each
@@ -447,7 +457,7 @@ __global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_compact(const Soa 
         const uint32_t maxfront = __reduce_max_sync(0xffffffffu, front);
         for (uint32_t o = 0; o < maxfront; o += 8) {
             const uint32_t r = lo + o + gl;
-            const bool hole = o + gl < front && mflag[r] == 1;
+            const bool hole = o + gl < front && is_gap(A.x[r]);
             const unsigned hm = (__ballot_sync(0xffffffffu, hole) >> (grp * 8)) & 0xffu;
             const uint32_t k = nh + __popc(hm & ((1u << gl) - 1u));
             if (hole && k < kHoleCap) holes[gid][k] = r;
@@ -460,7 +470,7 @@ __global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_compact(const Soa 
         uint32_t nk = 0;
         for (uint32_t o = front; __any_sync(0xffffffffu, o < maxlen); o += 8) {
             const uint32_t r = lo + o + gl;
-            const bool kept = !spill && o + gl < len && mflag[r] != 1;  // flag 2 (unrecorded mover) stays
+            const bool kept = !spill && o + gl < len && !is_gap(A.x[r]);
             const unsigned km = (__ballot_sync(0xffffffffu, kept) >> (grp * 8)) & 0xffu;
             if (kept) copy_particle(A, r, A, holes[gid][nk + __popc(km & ((1u << gl) - 1u))]);
             nk += __popc(km);
@@ -477,7 +487,7 @@ __global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_compact(const Soa 
             const uint32_t maxs = __reduce_max_sync(0xffffffffu, sl_len);
             for (uint32_t o = 0; o < maxs; o += 8) {
                 const uint32_t r = lo + o + gl;
-                const bool keep = o + gl < sl_len && mflag[r] != 1;
+                const bool keep = o + gl < sl_len && !is_gap(A.x[r]);
                 const unsigned km = (__ballot_sync(0xffffffffu, keep) >> (grp * 8)) & 0xffu;
                 const uint32_t dst = wpos + __popc(km & ((1u << gl) - 1u));
                 double px = 0, py = 0, pz = 0, pvx = 0, pvy = 0, pvz = 0, pw = 0;
@@ -506,17 +516,27 @@ __global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_compact(const Soa 
     if (mydep) dep[cl] = 0;
 }
 
-// Migration: every recorded mover takes the next slot of its target bin's
-// slack (atomic tail cursor); arrivals beyond the slack go to the overflow list.
+// Migration: an arrival first takes a hole of its bin, else the next slot of
+// its slack (atomic tail cursor); arrivals beyond the slack go to the overflow
+// list.  Holes are popped from the bin's list with one atomicSub on holes[d]:
+// the first holes[d] decrements return holes[d], ..., 1 (list entries, each
+// once -- no departures run concurrently); a decrement that returns <= 0 found
+// the list empty and gives its unit back, so holes[d] ends at max(h0 - a, 0).
 __global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32_t mcap,
                          StepCounters* ctr, const Soa A, const uint32_t* __restrict__ off, uint32_t* cnt,
-                         uint32_t* __restrict__ ovf) {
+                         uint32_t* __restrict__ ovf, uint32_t* __restrict__ holes, const uint32_t* __restrict__ hl) {
     const uint32_t nm = min(ctr->nmovers, mcap) + ctr->nimport;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
         const uint32_t d = mcell[i];
+        const uint32_t lo = off[d];
+        const int h = (int)atomicSub(&holes[d], 1u);
+        if (h > 0) {
+            copy_particle(M, i, A, hl[lo + (uint32_t)h - 1u]);
+            continue;
+        }
+        atomicAdd(&holes[d], 1u);  // RED
         const uint32_t pos = atomicAdd(&cnt[d], 1u);
-        const uint32_t lo = off[d], cap = off[d + 1] - lo;
-        if (pos < cap) {
+        if (pos < off[d + 1] - lo) {
             copy_particle(M, i, A, (uint64_t)lo + pos);
         } else {
             ovf[atomicAdd(&ctr->noverflow, 1u)] = i;
@@ -525,16 +545,22 @@ __global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32
 }
 
 // borrow_insert (gpma.hpp:337-370) for the arrivals that found their bin
-// full: the nearest of the next `scan` bins with slack lends one slot; every
-// boundary in (d, donor] moves up by one and each bin in between hands its
-// first particle to its own tail (the slot just vacated above it), so bins
-// stay contiguous and cell-exact.  One thread per overflowed arrival; a thread
-// works only while it holds try-locks on its whole window [d, d+scan] (taken
-// in ascending order, released on any failure, so no thread ever waits while
-// holding a lock).  Arrivals with no donor go to `left` for the re-sort.
+// full: the nearest of the next `scan` bins with a free slot -- tail slack or
+// a hole, as the reference's slot scan takes the first empty slot of either
+// kind -- lends one slot; every boundary in (d, donor] moves up by one and
+// each (full, hole-free) bin in between hands its first particle to its own
+// tail (the slot just vacated above it), so bins stay contiguous and
+// cell-exact.  A hole-free donor does the same into its tail slack; a donor
+// with holes gives one up instead: its first slot's particle moves into one of
+// them (or the first slot is itself the hole) and its hole list follows its
+// base.  One
+// thread per overflowed arrival; a thread works only while it holds try-locks
+// on its whole window [d, d+scan] (taken in ascending order, released on any
+// failure, so no thread ever waits while holding a lock).  Arrivals with no
+// donor go to `left` for the re-sort.
 __global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restrict__ mcell,
                          const uint32_t* __restrict__ ovf, uint32_t* __restrict__ left, const Soa A, uint32_t* off,
-                         const uint32_t* __restrict__ cnt, unsigned int* lock, uint32_t ncells, int scan) {
+                         uint32_t* cnt, uint32_t* holes, uint32_t* hl, unsigned int* lock, uint32_t ncells, int scan) {
     const uint32_t n = *(volatile unsigned int*)&ctr->noverflow;
     for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) {
         const uint32_t i = ovf[o];
@@ -555,9 +581,12 @@ __global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restr
             }
             __threadfence();
             volatile uint32_t* voff = off;
+            volatile uint32_t* vcnt = cnt;
+            volatile uint32_t* vholes = holes;
+            volatile uint32_t* vhl = hl;
             int64_t donor = -1;
             for (uint32_t b = d + 1; b <= last; ++b)
-                if (cnt[b] < voff[b + 1] - voff[b]) {
+                if (vcnt[b] < voff[b + 1] - voff[b] || vholes[b] > 0) {
                     donor = b;
                     break;
                 }
@@ -568,9 +597,23 @@ __global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restr
                 uint32_t above = voff[(uint32_t)donor + 1];
                 for (uint32_t j = (uint32_t)donor; j > d; --j) {
                     const uint32_t oj = voff[j];
-                    const uint32_t held = min(cnt[j], above - oj);  // capacity before this borrow
-                    if (held > 0) {  // donor: its free tail slot; a full bin: `above`, vacated by bin j+1
-                        const uint64_t dst = (uint64_t)oj + held;
+                    const uint32_t len = vcnt[j];
+                    const uint32_t hj = j == (uint32_t)donor ? vholes[j] : 0u;  // bins in between have none
+                    uint64_t dst = (uint64_t)oj + min(len, above - oj);  // tail slack, or `above` (vacated by bin j+1)
+                    if (hj) {  // a donor with holes gives one up (they are the spare slots arrivals missed)
+                        uint32_t k = hj - 1;
+                        if (is_gap(__ldcg(A.x + oj))) {
+                            while (k > 0 && vhl[oj + k] != oj) --k;  // the first slot is a listed hole
+                            vhl[oj + k] = vhl[oj + hj - 1];
+                            dst = oj;                       // nothing to move
+                        } else {
+                            dst = vhl[oj + k];
+                        }
+                        for (uint32_t q = hj - 1; q-- > 0;) vhl[oj + 1 + q] = vhl[oj + q];
+                        vholes[j] = hj - 1;
+                        vcnt[j] = len - 1;
+                    }
+                    if (len > 0 && dst != oj) {
                         A.x[dst] = __ldcg(A.x + oj); A.y[dst] = __ldcg(A.y + oj); A.z[dst] = __ldcg(A.z + oj);
                         A.vx[dst] = __ldcg(A.vx + oj); A.vy[dst] = __ldcg(A.vy + oj);
                         A.vz[dst] = __ldcg(A.vz + oj); A.w[dst] = __ldcg(A.w + oj);
@@ -1008,8 +1051,11 @@ void BinStore::init(const picgpu_grid& grid, double gap_ratio, uint32_t mg, cuda
     off.ensure((nc + 1) * 4);
     off2.ensure((nc + 1) * 4);
     cnt.ensure(nc * 4);
-    start.ensure(nc * 4);
+    // start doubles as the (nc+1)-entry held-count scratch of a rebuild:
+    // sized now, so no rebuild pays a (device-synchronising) regrowth
+    start.ensure((nc + 1) * 4);
     endp.ensure(nc * 4);
+    cnt2.ensure((nc + 1) * 4);
     caps.ensure((nc + 1) * 8);
     counters.ensure(sizeof(StepCounters));
     if (!hcounters) PICGPU_CUDA_TRY(cudaMallocHost((void**)&hcounters, sizeof(StepCounters)));
@@ -1017,8 +1063,8 @@ void BinStore::init(const picgpu_grid& grid, double gap_ratio, uint32_t mg, cuda
     PICGPU_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, nc * 4, st));
     locks.ensure(nc * 4 + 4);
     PICGPU_CUDA_TRY(cudaMemsetAsync(locks.p, 0, nc * 4 + 4, st));
-    dep.ensure(nc * 4 + 4);
-    PICGPU_CUDA_TRY(cudaMemsetAsync(dep.p, 0, nc * 4 + 4, st));
+    holes.ensure(nc * 4 + 4);
+    PICGPU_CUDA_TRY(cudaMemsetAsync(holes.p, 0, nc * 4 + 4, st));
     capacity = 0;
     n = 0;
 }
@@ -1082,7 +1128,6 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev) {
         throw Status{hcounters->err, g.slab ? "slab: particle outside the slab's owned cells (or non-finite)"
                                             : "cell_of: non-finite particle position"};
     A.ensure(capacity_next);
-    mflag.ensure(capacity_next + 1);
     PICGPU_CUDA_TRY(cudaMemsetAsync(A.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
     swap_buf(off, off2);
     if (np) {
@@ -1096,20 +1141,30 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev) {
     }
     capacity = capacity_next;
     n = np;
+    PICGPU_CUDA_TRY(cudaMemsetAsync(holes.p, 0, nc * 4 + 4, st));  // fresh bins are packed
     // the spare store (relayout / rebuild target) gets the same capacity + headroom
     // now, outside any timed step, instead of at the first rebuild
     B.ensure(capacity + capacity / 8);
-    mflag.ensure(capacity + capacity / 8 + 1);
+    hl.ensure((capacity + capacity / 8) * 4 + 4);
+}
+
+void BinStore::fill_holes() {
+    const size_t nc = g.ncells;
+    if (!nc) return;
+    k_fill_holes<<<div_up((long long)nc, 256), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                             holes.as<uint32_t>(), (uint32_t)nc);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
 void BinStore::relayout() {
     const size_t nc = g.ncells;
+    fill_holes();
     k_caps_from_cnt<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt.as<uint32_t>(), (uint32_t)nc,
                                                                     caps.as<uint32_t>(), onepg, min_gap);
     note_launch();
     layout_from_counts(n);
     B.ensure(capacity_next);
-    mflag.ensure(capacity_next + 1);
     PICGPU_CUDA_TRY(cudaMemsetAsync(B.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
     if (nc) {
         k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
@@ -1124,6 +1179,7 @@ void BinStore::relayout() {
 
 void BinStore::compact_to_B() {
     const size_t nc = g.ncells;
+    fill_holes();
     DevBuf& held = start;  // u32 scratch (nc) -- holds min(cnt, cap); needs nc+1
     held.ensure((nc + 1) * 4);
     k_held<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt.as<uint32_t>(), off.as<uint32_t>(), (uint32_t)nc,
@@ -1190,14 +1246,13 @@ void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
     auto* kern = push ? (p2 ? k_push<true, UNR, true> : k_push<true, UNR, false>)
                       : (p2 ? k_push<false, UNR, true> : k_push<false, UNR, false>);
-    kern<<<blocks, 256, 0, st>>>(g, A.soa(), capacity, mflag.as<uint8_t>(), dt, cap2, M.soa(), mcell.as<uint32_t>(),
-                                 (uint32_t)mcap, dep.as<uint32_t>(), ctr, lrec.as<double>(), (uint32_t)lcap);
+    hl.ensure(capacity * 4 + 4);
+    kern<<<blocks, 256, 0, st>>>(g, A.soa(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap,
+                                 off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>(), ctr,
+                                 lrec.as<double>(), (uint32_t)lcap);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
-    k_compact<<<div_up((long long)nc, 256), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                          mflag.as<uint8_t>(), dep.as<uint32_t>(), (uint32_t)nc);
-    note_launch();
-    PICGPU_CUDA_TRY(cudaGetLastError());
+    // no compaction: departures left holes (GPMA gaps), filled by the arrivals
 }
 
 void BinStore::enqueue_import(const double* rec_dev, uint32_t nimp, uint32_t base) {
@@ -1212,13 +1267,15 @@ void BinStore::enqueue_migrate() {
     StepCounters* ctr = counters.as<StepCounters>();
     if (nc) {
         k_insert<<<num_sms * 4, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap, ctr, A.soa(),
-                                              off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>());
+                                              off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>(),
+                                              holes.as<uint32_t>(), hl.as<uint32_t>());
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
         // borrow_insert for the full-bin arrivals; no work when there are none
         k_borrow<<<num_sms, 128, 0, st>>>(ctr, M.soa(), mcell.as<uint32_t>(), ovf.as<uint32_t>(),
                                           ovf_left.as<uint32_t>(), A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                          locks.as<unsigned int>(), (uint32_t)nc, kBorrowScanBins);
+                                          holes.as<uint32_t>(), hl.as<uint32_t>(), locks.as<unsigned int>(),
+                                          (uint32_t)nc, kBorrowScanBins);
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
     }
@@ -1243,8 +1300,8 @@ void BinStore::push_and_resort(bool push, double dt, double cap2, StepCounters& 
         const int blocks = (int)((capacity + 256 * UNR - 1) / (256 * UNR));
         const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
         auto* kern = p2 ? k_push<true, UNR, true, false> : k_push<true, UNR, false, false>;
-        kern<<<blocks, 256, 0, st>>>(g, A.soa(), capacity, mflag.as<uint8_t>(), dt, cap2, M.soa(),
-                                     mcell.as<uint32_t>(), (uint32_t)mcap, dep.as<uint32_t>(), ctr,
+        kern<<<blocks, 256, 0, st>>>(g, A.soa(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap,
+                                     off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>(), ctr,
                                      lrec.as<double>(), (uint32_t)lcap);
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
@@ -1267,6 +1324,7 @@ void BinStore::shift_window(const picgpu_grid& shifted, int ppc, double u_th, ui
     const size_t nc = g.ncells;
     injected = (uint64_t)g.ny * g.nz * (uint64_t)ppc;
     if (!nc) return;
+    fill_holes();
     // counts and fresh-slack layout of the shifted grid (bins keep their order)
     cnt2.ensure((nc + 1) * 4);
     k_shift_counts<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt.as<uint32_t>(), off.as<uint32_t>(),
@@ -1283,7 +1341,6 @@ void BinStore::shift_window(const picgpu_grid& shifted, int ppc, double u_th, ui
     note_launch();
     layout_from_counts(0);  // synchronises
     B.ensure(capacity_next + capacity_next / 8);
-    mflag.ensure(capacity_next + capacity_next / 8 + 1);
     PICGPU_CUDA_TRY(cudaMemsetAsync(B.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
     hg = shifted;
     g = make_grid(shifted);
@@ -1313,6 +1370,7 @@ bool BinStore::finish_incremental(StepCounters& out) {
     const uint32_t* left_list = ovf_left.as<uint32_t>();
     borrowed += out.nborrowed;
     if (!mover_overflow && !left) return false;
+    fill_holes();  // the layouts below need packed bins
     if (!mover_overflow) {
         // Gpma::rebuild (gpma.hpp:119-122, :130-143): fresh slack from the true
         // counts (cnt includes the unplaced arrivals), held particles keep their
@@ -1327,7 +1385,6 @@ bool BinStore::finish_incremental(StepCounters& out) {
         note_launch();
         layout_from_counts(n);
         B.ensure(capacity_next);
-        mflag.ensure(capacity_next + 1);
         PICGPU_CUDA_TRY(cudaMemsetAsync(B.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
         k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
                                                                B.soa(), off2.as<uint32_t>(), (uint32_t)nc);

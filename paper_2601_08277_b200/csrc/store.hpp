@@ -66,11 +66,12 @@ struct BinStore {
     DevBuf off, cnt, off2;    // off: ncells+1 (u32), cnt: ncells (u32)
     DevBuf cnt2;              // counts of a layout being built (moving window)
     DevBuf keys, keys2, skeys, vals, vals2, start, endp, caps, cub_tmp;
-    DevBuf mflag;             // per-slot mover flag (u8)
     SoaBuf M;                 // mover records
     DevBuf mcell, ovf, ovf_left;  // mover target cell, overflow list, unplaced overflow
     DevBuf locks;             // per-bin try-locks of the borrow kernel (always released)
-    DevBuf dep;               // per-bin departure counts (reset by k_compact)
+    DevBuf holes;             // per-bin holes in the extent [off, off+cnt) (GPMA gaps)
+    DevBuf hl;                // per-bin hole lists, slot-indexed like the bins: bin c's holes
+                              // are the slots hl[off[c] .. off[c]+holes[c]) (u32)
     DevBuf counters;          // StepCounters
     StepCounters* hcounters = nullptr;  // pinned mirror
 
@@ -96,11 +97,12 @@ struct BinStore {
     // returns the packed offsets in `off2` (exclusive scan of cnt).
     void compact_to_B();
     // One incremental step, enqueued without host synchronisation: push
-    // (optional) + detect + in-bin compaction, migration into slack, borrow
-    // from the following bins for full bins; counters copied to the host.
+    // (optional) + detect (departures leave holes), migration into holes and
+    // slack, borrow from the following bins for full bins; counters copied to
+    // the host.
     void enqueue_incremental(bool push, double dt, double cap2);
     // The same step in two halves around a slab exchange: detect (push +
-    // move detection + in-bin compaction; leavers go to the exchange buffer
+    // move detection; leavers go to the exchange buffer
     // `lrec`), then migrate (optional arrivals appended to the movers,
     // insert, borrow).
     void enqueue_detect(bool push, double dt, double cap2);
@@ -124,6 +126,8 @@ struct BinStore {
 
     void ensure_movers(size_t m);
     void ensure_movers_keep(size_t m, size_t keep);  // grow, preserving the first `keep` records
+    // packs every bin (holes filled from the bin's tail); cnt = particle counts
+    void fill_holes();
 
    private:
     void layout_from_counts(uint64_t total_particles);  // caps + scan -> off2; returns via capacity_next
