@@ -188,6 +188,10 @@ typedef struct picgpu_session_config {
 #define PICGPU_STEP_NO_SYNC 32u   /* do not read back step stats (counts stay on device) */
 #define PICGPU_STEP_RESORT 64u    /* instead of SORT: after the push, a full stable counting sort of the
                                      whole store (hybrid-globalsort and the modes without an index) */
+#define PICGPU_STEP_UNFUSED 128u  /* PUSH|SORT|CURRENT on the default kernel run as ONE fused pass
+                                     (push + move detection + J of the particles that stay in their
+                                     cell; movers deposited separately) unless this flag is set:
+                                     then a push kernel, the sort and the J kernel run one after another */
 #define PICGPU_STEP_DEFAULT (PICGPU_STEP_PUSH | PICGPU_STEP_SORT | PICGPU_STEP_CURRENT)
 
 typedef struct picgpu_step_stats {
@@ -282,7 +286,9 @@ PICGPU_API int picgpu_session_device_fields(picgpu_session* s, double** j, doubl
 /* Accumulated per-phase device times (ms) and launch counts since the last
  * reset, recorded only with PICGPU_SESSION_TIMING.  Phases:
  * 0 push + detect + migrate + borrow, 1 reserved, 2 rebuild/global sort, 3 deposit J,
- * 4 deposit rho, 5 zero fields. */
+ * 4 deposit rho, 5 zero fields.  In a fused step (PICGPU_STEP_UNFUSED not set)
+ * phase 3 is the fused push + detect + J kernel and phase 0 the movers'
+ * records/holes/J plus the migration. */
 #define PICGPU_NPHASES 6
 PICGPU_API int picgpu_session_phase_times(picgpu_session* s, double* ms, uint64_t* launches, int nphases);
 PICGPU_API int picgpu_session_reset_phase_times(picgpu_session* s);

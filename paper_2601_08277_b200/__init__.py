@@ -36,6 +36,7 @@ CIC, TSC, QSP = 1, 2, 3
 OK, EINVAL, ERANGE, ELENGTH, ELOGIC, EDOMAIN, ECUDA, ENCCL, ENOMEM = range(9)
 
 STEP_PUSH, STEP_SORT, STEP_CURRENT, STEP_DENSITY, STEP_GLOBAL_SORT, STEP_NO_SYNC, STEP_RESORT = 1, 2, 4, 8, 16, 32, 64
+STEP_UNFUSED = 128  # run push, sort and J as separate kernels (default: one fused push + detect + J pass)
 KERNEL_LANE, KERNEL_VECTOR, KERNEL_MATRIX = 0, 1, 2
 STEP_DEFAULT = STEP_PUSH | STEP_SORT | STEP_CURRENT
 SESSION_TIMING = 1

@@ -728,6 +728,48 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
                 accumulate_phase(s, 2, 0, 1, g_launches.load() - l0);
             }
         }
+        // the fused step: push + detect + J in one pass over the bins (movers
+        // deposited by their own kernel), then the migration
+        const uint32_t fuse_mask = PICGPU_STEP_PUSH | PICGPU_STEP_SORT | PICGPU_STEP_CURRENT;
+        const bool fused = (flags & fuse_mask) == fuse_mask && !(flags & PICGPU_STEP_UNFUSED) &&
+                           fused_step_available(s->order, s->kernel);
+        if (fused) {
+            const double cap2 = cap2_of(bs.hg, dt);
+            const uint64_t l0 = g_launches.load();
+            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[2], st));
+            PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)bs.g.ncells * 24, st));
+            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[3], st));
+            bs.enqueue_fused(s->order, s->q, s->J.as<double>(), dt, cap2, T ? s->ev[4] : nullptr);
+            if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
+            lj = g_launches.load() - l0;
+            StepCounters c{};
+            const size_t mcap0 = bs.mcap;
+            const bool rebuilt = bs.finish_incremental(c);  // host waits here
+            if (c.err == PICGPU_EDOMAIN)
+                throw Status{c.err, "advance: particle displacement exceeds the single-cell cap"};
+            if (c.err) throw Status{c.err, "cell_of: non-finite particle position"};
+            stats.moved = c.nmovers;
+            stats.inserts = std::min<uint64_t>(c.nmovers, mcap0);
+            stats.overflowed = c.noverflow;
+            if (T) {
+                // zero -> ev3 -> fused push + detect + J kernel -> ev4 -> movers + migration -> ev1
+                accumulate_phase(s, 5, 2, 3, 0);
+                accumulate_phase(s, 3, 3, 4, 1);
+                accumulate_phase(s, 0, 4, 1, lj - 1);
+                if (rebuilt) {
+                    PICGPU_CUDA_TRY(cudaEventRecord(s->ev[7], st));
+                    PICGPU_CUDA_TRY(cudaEventSynchronize(s->ev[7]));
+                    accumulate_phase(s, 2, 1, 7, g_launches.load() - l0 - lj);
+                }
+            }
+            if (rebuilt && c.nmovers > mcap0) {
+                // movers beyond the buffer were pushed but neither recorded nor
+                // deposited: the store was re-sorted fully, deposit J again
+                flags &= ~PICGPU_STEP_SORT;  // (handled) -- J below is redone from scratch
+            } else {
+                flags &= ~(PICGPU_STEP_SORT | PICGPU_STEP_CURRENT);
+            }
+        }
         if (flags & PICGPU_STEP_SORT) {
             const double cap2 = (flags & PICGPU_STEP_PUSH) ? cap2_of(bs.hg, dt) : 0.0;
             const uint64_t l0 = g_launches.load();

@@ -131,6 +131,58 @@ __device__ __forceinline__ uint32_t store_cell(const GridD& g, double x, double 
     return dl <= dr ? kLeaveLeft : kLeaveRight;
 }
 
+// Device counters of one step (read back once per step).
+struct StepCounters {
+    unsigned long long moved;
+    unsigned int nmovers;     // movers detected (may exceed mover capacity)
+    unsigned int noverflow;   // arrivals that found no slack in their own bin
+    int err;                  // picgpu_status of the first device-side error
+    unsigned int nborrowed;   // ... placed by borrowing a following bin's slack
+    unsigned int nleft;       // ... with no donor (-> rebuild)
+    unsigned int nimport;     // arrivals from neighbour slabs appended to the movers
+    unsigned int nleave[2];   // particles that left the slab to the left / right
+};
+
+// floor((x - o) / h) exactly as locate_axis computes it (before its range
+// handling).  For u >= 0 the fraction u - floor(u) is exact and < 1, so equal
+// non-negative floors on every axis mean the same cell.
+__device__ __forceinline__ double axis_floor(double x, double o, double h, double inv, int pow2) {
+    const double t = __dsub_rn(x, o);
+    return floor(pow2 ? __dmul_rn(t, inv) : __ddiv_rn(t, h));
+}
+
+// detail::wrap_position, workload.hpp:128-132 (a power-of-two length divides
+// exactly as a multiply by its reciprocal).
+__device__ __forceinline__ double wrap_position(double x, double origin, double length, double inv, int pow2) {
+    const double t = __dsub_rn(x, origin);
+    double r = __dsub_rn(x, __dmul_rn(length, floor(pow2 ? __dmul_rn(t, inv) : __ddiv_rn(t, length))));
+    if (__dsub_rn(r, origin) >= length) r = origin;
+    return r;
+}
+
+// One particle of pic::advance (workload.hpp:144-153); returns false on a cap
+// violation (the reference throws std::domain_error).
+// P2: every spacing and box length is a power of two (checked on the host),
+// so the divide-or-multiply choice folds away at compile time.
+template <bool P2 = false>
+__device__ __forceinline__ bool push_one(const GridD& g, double dt, double cap2, double& x, double& y, double& z,
+                                         double vx, double vy, double vz) {
+    const double v2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+    if (v2 > cap2) return false;
+    x = wrap_position(__dadd_rn(x, __dmul_rn(vx, dt)), g.gox, g.gLx, g.ginv_Lx, P2 || g.gpow2Lx);
+    y = wrap_position(__dadd_rn(y, __dmul_rn(vy, dt)), g.oy, g.Ly, g.inv_Ly, P2 || g.pow2Ly);
+    z = wrap_position(__dadd_rn(z, __dmul_rn(vz, dt)), g.oz, g.Lz, g.inv_Lz, P2 || g.pow2Lz);
+    return true;
+}
+
+// A departure: the slot becomes a hole of its bin (sentinel x) and joins the
+// bin's hole list.
+__device__ __forceinline__ void push_hole(const Soa& A, uint64_t s, uint32_t b, const uint32_t* __restrict__ off,
+                                          uint32_t* __restrict__ holes, uint32_t* __restrict__ hl) {
+    A.x[s] = __longlong_as_double(kGapBits);
+    hl[off[b] + atomicAdd(&holes[b], 1u)] = (uint32_t)s;
+}
+
 // Shape weights in a fixed window of W taps starting at node cell + OFF.
 //   order 1: CIC, cic_shape_1d (shape.hpp:26-29), W = 2, OFF = 0.
 //   order 3: QSP, qsp_shape_1d (shape.hpp:33-43), W = 4, OFF = -1.

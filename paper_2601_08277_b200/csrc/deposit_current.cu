@@ -127,14 +127,27 @@ struct PData {  // one particle as read from the bins
     double x, y, z, vx, vy, vz, w;
 };
 
+// RW: the kernel writes the positions back (fused step): coherent loads, not
+// the read-only path.
+template <bool RW = false>
 __device__ __forceinline__ void load_particle(const CSoa& p, uint32_t s, PData& d) {
-    d.x = __ldg(p.x + s);
-    d.y = __ldg(p.y + s);
-    d.z = __ldg(p.z + s);
-    d.vx = __ldg(p.vx + s);
-    d.vy = __ldg(p.vy + s);
-    d.vz = __ldg(p.vz + s);
-    d.w = __ldg(p.w + s);
+    if constexpr (RW) {
+        d.x = p.x[s];
+        d.y = p.y[s];
+        d.z = p.z[s];
+        d.vx = p.vx[s];
+        d.vy = p.vy[s];
+        d.vz = p.vz[s];
+        d.w = p.w[s];
+    } else {
+        d.x = __ldg(p.x + s);
+        d.y = __ldg(p.y + s);
+        d.z = __ldg(p.z + s);
+        d.vx = __ldg(p.vx + s);
+        d.vy = __ldg(p.vy + s);
+        d.vz = __ldg(p.vz + s);
+        d.w = __ldg(p.w + s);
+    }
 }
 
 // Per-particle prologue (shape.hpp:64-85 + particle_weights :46-50): the
@@ -542,11 +555,133 @@ __device__ __forceinline__ void particle_window_sel(const GridD& g, const PData&
     }
 }
 
-template <int ORDER, class CF = JCfg<ORDER>>
+// Stage one particle's window weights, field-major (see JLayout).
+template <int W, int FSS>
+__device__ __forceinline__ void stage_record(double* rec, const double (&a)[3][W], const double (&sy)[W],
+                                             const double (&sz)[W]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int t = 0; t < W; ++t) rec[(c * W + t) * FSS] = a[c][t];
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+        rec[(3 * W + t) * FSS] = sy[t];
+        rec[(4 * W + t) * FSS] = sz[t];
+    }
+}
+
+// Shift one staged W-tap field array (fields f0 .. f0+W-1) by sh (-1, 0, +1)
+// window positions, zero-filling the vacated one.
+template <int W, int FSS>
+__device__ __forceinline__ void restage_shifted(double* rec, int f0, int sh) {
+    if (sh == 0) return;
+    double v[W];
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+        const int u = t - sh;
+        v[t] = (u >= 0 && u < W) ? rec[(f0 + u) * FSS] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < W; ++t) rec[(f0 + t) * FSS] = v[t];
+}
+
+// Cell step of a mover on one periodic axis, folded into {-1, 0, +1}.
+__device__ __forceinline__ int cell_step(int d, int n) {
+    return d == 0 ? 0 : (d == 1 || d == 1 - n) ? 1 : -1;
+}
+
+// Window weights from the particle's cell fractions (the J forms:
+// weights_scaled, x-weights pre-multiplied by wq_c); zero charge when invalid.
+template <int ORDER>
+__device__ __forceinline__ void window_from_fractions(const PData& d, double qs, bool valid, double fx, double fy,
+                                                      double fz, double (&a)[3][Shape<ORDER>::W],
+                                                      double (&sy)[Shape<ORDER>::W], double (&sz)[Shape<ORDER>::W]) {
+    constexpr int W = Shape<ORDER>::W;
+    const double qw = qs * d.w;
+    const double wq0 = valid ? qw * d.vx : 0.0, wq1 = valid ? qw * d.vy : 0.0, wq2 = valid ? qw * d.vz : 0.0;
+    double sx[W];
+    weights_scaled<ORDER>(valid ? fx : 0.0, sx);
+    weights_scaled<ORDER>(valid ? fy : 0.0, sy);
+    weights_scaled<ORDER>(valid ? fz : 0.0, sz);
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+        a[0][t] = wq0 * sx[t];
+        a[1][t] = wq1 * sx[t];
+        a[2][t] = wq2 * sx[t];
+    }
+}
+
+// wrap_position (workload.hpp:128-132) with its common case first: a pushed
+// coordinate inside [origin, origin + length) is returned unchanged, which is
+// exactly what the full form computes there (floor((x-o)/L) = 0, x - L*0 = x,
+// and x - o < L); otherwise the full form.
+template <bool P2>
+__device__ __forceinline__ double wrap_fast(double x, double origin, double length, double inv, int pow2) {
+    const double t = __dsub_rn(x, origin);
+    if (t >= 0.0 && t < length) return x;
+    return wrap_position(x, origin, length, inv, P2 || pow2);
+}
+
+// Fused step, one binned particle of bin b (cell i, j, k; dci/dcj/dck the
+// same as doubles): the bit-exact push written back to its slot
+// (pic::advance, workload.hpp:139-155), the move test of detect_moves
+// (gpma.hpp:162-177) and the particle's fractions for the deposit -- relative
+// to its bin's cell, or for a mover to its new cell, with the cell step
+// (shx, shy, shz) that places its taps in the bin's window.  Positions are
+// finite on entry (the store only holds located particles).  Returns false
+// on an error (the reference would throw; the device flag is raised).
+template <bool P2>
+__device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PData& d, uint32_t s, uint32_t b,
+                                           int i, int j, int k, double dci, double dcj, double dck, double& fx,
+                                           double& fy, double& fz, bool& mv, uint32_t& mv_cell, int& shx,
+                                           int& shy, int& shz) {
+    const double v2 = __dadd_rn(__dadd_rn(__dmul_rn(d.vx, d.vx), __dmul_rn(d.vy, d.vy)), __dmul_rn(d.vz, d.vz));
+    if (!(v2 <= pc.cap2)) {
+        // v^2 > cap^2: domain_error; NaN velocity: the reference's position
+        // becomes NaN and cell_of throws invalid_argument
+        raise_error(&pc.ctr->err, v2 > pc.cap2 ? PICGPU_EDOMAIN : PICGPU_EINVAL);
+        return false;
+    }
+    d.x = wrap_fast<P2>(__dadd_rn(d.x, __dmul_rn(d.vx, pc.dt)), g.gox, g.gLx, g.ginv_Lx, g.gpow2Lx);
+    d.y = wrap_fast<P2>(__dadd_rn(d.y, __dmul_rn(d.vy, pc.dt)), g.oy, g.Ly, g.inv_Ly, g.pow2Ly);
+    d.z = wrap_fast<P2>(__dadd_rn(d.z, __dmul_rn(d.vz, pc.dt)), g.oz, g.Lz, g.inv_Lz, g.pow2Lz);
+    pc.A.x[s] = d.x;
+    pc.A.y[s] = d.y;
+    pc.A.z[s] = d.z;
+    // fractions relative to the bin's cell; with power-of-two spacings u =
+    // (x-o)*inv is locate_axis's exact u, so 0 <= u - c < 1 on every axis is
+    // exactly "same cell"; otherwise compare the exact floors
+    fx = __dmul_rn(__dsub_rn(d.x, g.gox), g.inv_dx) - dci;
+    fy = __dmul_rn(__dsub_rn(d.y, g.oy), g.inv_dy) - dcj;
+    fz = __dmul_rn(__dsub_rn(d.z, g.oz), g.inv_dz) - dck;
+    bool same;
+    if constexpr (P2)
+        same = fx >= 0.0 && fx < 1.0 && fy >= 0.0 && fy < 1.0 && fz >= 0.0 && fz < 1.0;
+    else
+        same = axis_floor(d.x, g.gox, g.dx, g.inv_dx, g.pow2x) == dci &&
+               axis_floor(d.y, g.oy, g.dy, g.inv_dy, g.pow2y) == dcj &&
+               axis_floor(d.z, g.oz, g.dz, g.inv_dz, g.pow2z) == dck;
+    if (same) return true;
+    int ni, nj, nk;
+    const uint32_t nc = cell_linear(g, d.x, d.y, d.z, ni, nj, nk, fx, fy, fz);  // exact (pic::cell_of)
+    if (nc == b) return true;  // a periodic image of the bin's cell
+    mv = true;
+    mv_cell = nc;
+    shx = cell_step(ni - i, g.nx);
+    shy = cell_step(nj - j, g.ny);
+    shz = cell_step(nk - k, g.nz);
+    return true;
+}
+
+// PM (fused step, PushCtx): 0 = deposit only; 1 = push + move detection + deposit of the
+// particles that stay in their cell (launch_deposit_current_push); 2 = the same
+// with every spacing and box length a power of two (compile-time reciprocals).
+template <int ORDER, class CF = JCfg<ORDER>, int PM = 0>
 __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
     deposit_current_kernel_v3(const GridD g, const CSoa p, const uint32_t* __restrict__ off,
                               const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
-                              double* __restrict__ jy, double* __restrict__ jz, const int zlen) {
+                              double* __restrict__ jy, double* __restrict__ jz, const int zlen,
+                              const PushCtx pc) {
     using C = CF;
     using L = JLayout<ORDER, CF>;
     constexpr int W = L::W, OFF = Shape<ORDER>::OFF, NJ = L::NJ;
@@ -638,7 +773,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
     }
     int last_busy = k0 - W;  // last z-step in which any pencil of the CTA deposited (CTA-uniform)
     PData nxt{};
-    if (lg < n_c) load_particle(p, c_off + lg, nxt);
+    if (lg < n_c) load_particle<PM != 0>(p, c_off + lg, nxt);
 
     int buf = 0;
     const int kend = k1 + W - 1;
@@ -658,27 +793,50 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 #pragma unroll
             for (int sl = 0; sl < W; ++sl) szb[sl] = stage + (4 * W + ((sl - R) & (W - 1))) * L::FSS + grp;
             const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
-            if (m == 0 && lg < n_n) load_particle(p, n_off + lg, nxt);  // empty cells: still prefetch
+            if (m == 0 && lg < n_n) load_particle<PM != 0>(p, n_off + lg, nxt);  // empty cells: still prefetch
             for (int base = 0; base < m; base += CH) {
+                [[maybe_unused]] bool mv = false;  // fused step: this lane's particle changed cell
+                [[maybe_unused]] uint32_t mv_cell = 0;
+                [[maybe_unused]] unsigned mv_bal = 0, mv_b0 = 0;
                 {
-                    const PData cur = nxt;
-                    const bool valid = base + lg < n_c && !is_gap(cur.x);  // holes count as padding
+                    PData cur = nxt;
+                    bool valid = base + lg < n_c && !is_gap(cur.x);  // holes count as padding
                     if (base + CH < m) {
-                        if (base + CH + lg < n_c) load_particle(p, c_off + base + CH + lg, nxt);
+                        if (base + CH + lg < n_c) load_particle<PM != 0>(p, c_off + base + CH + lg, nxt);
                     } else if (lg < n_n) {
-                        load_particle(p, n_off + lg, nxt);
+                        load_particle<PM != 0>(p, n_off + lg, nxt);
                     }
                     double a[3][W], sy[W], sz[W];
-                    particle_window_sel<ORDER>(g, cur, qs, valid, dci, dcj, dck, a, sy, sz);
                     double* rec = stage + lg * L::SS + grp;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-#pragma unroll
-                        for (int t = 0; t < W; ++t) rec[(c * W + t) * L::FSS] = a[c][t];
-#pragma unroll
-                    for (int t = 0; t < W; ++t) {
-                        rec[(3 * W + t) * L::FSS] = sy[t];
-                        rec[(4 * W + t) * L::FSS] = sz[t];
+                    if constexpr (PM != 0) {
+                        // pic::advance (workload.hpp:139-155) + Gpma::detect_moves (gpma.hpp:162-177):
+                        // fractions of the pushed particle, relative to its new cell for a mover
+                        double fx = 0.0, fy = 0.0, fz = 0.0;
+                        int shx = 0, shy = 0, shz = 0;
+                        if (valid)
+                            valid = push_fused<PM == 2>(g, pc, cur, c_off + (uint32_t)(base + lg),
+                                                        col + plane_cells * (uint32_t)k, i, j, k, dci, dcj, dck,
+                                                        fx, fy, fz, mv, mv_cell, shx, shy, shz);
+                        // one mover-list reservation per warp; its result is only
+                        // needed after the contraction below
+                        mv_bal = __ballot_sync(0xffffffffu, mv);
+                        if (mv_bal && (tid & 31) == __ffs(mv_bal) - 1)
+                            mv_b0 = atomicAdd(&pc.ctr->nmovers, (unsigned)__popc(mv_bal));
+                        window_from_fractions<ORDER>(cur, qs, valid, fx, fy, fz, a, sy, sz);
+                        stage_record<W, L::FSS>(rec, a, sy, sz);
+                        if (mv) {
+                            // a mover's taps, shifted into this cell's window by its cell
+                            // step (read back from its staged record: runtime offsets stay
+                            // in shared memory); taps that leave the window are k_movers'
+                            restage_shifted<W, L::FSS>(rec, 0, shx);
+                            restage_shifted<W, L::FSS>(rec, W, shx);
+                            restage_shifted<W, L::FSS>(rec, 2 * W, shx);
+                            restage_shifted<W, L::FSS>(rec, 3 * W, shy);
+                            restage_shifted<W, L::FSS>(rec, 4 * W, shz);
+                        }
+                    } else {
+                        particle_window_sel<ORDER>(g, cur, qs, valid, dci, dcj, dck, a, sy, sz);
+                        stage_record<W, L::FSS>(rec, a, sy, sz);
                     }
                 }
                 __syncwarp();
@@ -699,6 +857,19 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 #pragma unroll
                             for (int sl = 0; sl < W; ++sl) acc[sl][ix][c] = fma(av, b[sl], acc[sl][ix][c]);
                         }
+                }
+                if constexpr (PM != 0) {
+                    if (mv_bal) {
+                        const unsigned b0 = __shfl_sync(0xffffffffu, mv_b0, __ffs(mv_bal) - 1);
+                        if (mv) {
+                            const unsigned idx = b0 + (unsigned)__popc(mv_bal & ((1u << (tid & 31)) - 1u));
+                            if (idx < pc.mcap) {
+                                pc.mslot[idx] = c_off + (uint32_t)(base + lg);
+                                pc.mbin[idx] = col + plane_cells * (uint32_t)k;
+                                pc.mcell[idx] = mv_cell;
+                            }
+                        }
+                    }
                 }
                 __syncwarp();
             }
@@ -1328,22 +1499,23 @@ void launch_warp(const GridD& g, const CSoa& p, const uint32_t* off, const uint3
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
-// z-chunked grid of one of the pencil kernels (v3 or the original v1).
-template <int ORDER, class C, bool V3>
+// z-chunked grid of one of the pencil kernels (v3 or the original v1); PM > 0:
+// the fused push + detect + deposit form of v3.
+template <int ORDER, class C, bool V3, int PM = 0>
 void launch_kernel(const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
-                   int num_sms, cudaStream_t st) {
+                   int num_sms, cudaStream_t st, const PushCtx& pc = PushCtx{}) {
+    static_assert(V3 || PM == 0, "the fused step runs on the v3 kernel");
     using L = JLayout<ORDER, C>;
     constexpr int W = L::W;
     constexpr size_t smem = V3 ? L::SMEM : JLayout<ORDER>::SMEM;
-    auto* kern = [] {
-        if constexpr (V3)
-            return deposit_current_kernel_v3<ORDER, C>;
-        else
-            return deposit_current_kernel<ORDER>;
-    }();
     static bool configured = false;
     if (!configured) {
-        PICGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if constexpr (V3)
+            PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel_v3<ORDER, C, PM>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        else
+            PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel<ORDER>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
     const int tx = div_up(g.nx, C::PX), ty = div_up(g.ny, C::PY);
@@ -1356,7 +1528,12 @@ void launch_kernel(const GridD& g, const CSoa& p, const uint32_t* off, const uin
     const int zlen = div_up(g.nz, zch);
     zch = div_up(g.nz, zlen);
     dim3 grid(tx, ty, zch);
-    kern<<<grid, L::NT, smem, st>>>(g, p, off, cnt, q, j, j + g.ncells, j + 2 * (size_t)g.ncells, zlen);
+    if constexpr (V3)
+        deposit_current_kernel_v3<ORDER, C, PM><<<grid, L::NT, smem, st>>>(g, p, off, cnt, q, j, j + g.ncells,
+                                                                          j + 2 * (size_t)g.ncells, zlen, pc);
+    else
+        deposit_current_kernel<ORDER><<<grid, L::NT, smem, st>>>(g, p, off, cnt, q, j, j + g.ncells,
+                                                                 j + 2 * (size_t)g.ncells, zlen);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
@@ -1414,6 +1591,123 @@ void launch_deposit_current(int order, const GridD& g, const CSoa& p, const uint
             break;
         default: throw Status{PICGPU_EINVAL, "deposit: shape order must be 1, 2 or 3"};
     }
+}
+
+namespace {
+
+template <int ORDER>
+void launch_push_order(const GridD& g, const PushCtx& pc, const uint32_t* off, const uint32_t* cnt, double q,
+                       double* j, int num_sms, cudaStream_t st) {
+    using C3 = std::conditional_t<ORDER == 1, JCfgCic3, JCfg<ORDER>>;
+    const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
+    const CSoa p(pc.A);
+    if (p2)
+        launch_kernel<ORDER, C3, true, 2>(g, p, off, cnt, q, j, num_sms, st, pc);
+    else
+        launch_kernel<ORDER, C3, true, 1>(g, p, off, cnt, q, j, num_sms, st, pc);
+}
+
+// Movers of the fused step, W threads per mover (one z-plane of its window
+// each): thread 0 copies the particle from its slot into the mover record and
+// turns the slot into a hole of its old bin (delete_in_bin, gpma.hpp:328-335).
+// The fused kernel deposited the mover's taps that fall inside its old cell's
+// window (a mover steps at most one cell per axis); each thread reduces the
+// rest of its plane -- the nodes outside that window -- into J (RED.ADD.F64):
+// 16 of 64 nodes for a one-axis QSP mover.
+template <int ORDER>
+__global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc, const Soa M,
+                                                const uint32_t* __restrict__ off, uint32_t* __restrict__ holes,
+                                                uint32_t* __restrict__ hl, const double qs, double* __restrict__ jx,
+                                                double* __restrict__ jy, double* __restrict__ jz) {
+    constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
+    const uint64_t nm = min(pc.ctr->nmovers, pc.mcap);
+    const int lane = threadIdx.x & 31;
+    const unsigned grp = ((1u << W) - 1u) << (lane & ~(W - 1));  // the W lanes of one mover
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nm * W;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = t / W;
+        const int kz = (int)(t % W);
+        const uint32_t s = pc.mslot[i], b = pc.mbin[i];
+        const double x = pc.A.x[s], y = pc.A.y[s], z = pc.A.z[s];
+        const double vx = pc.A.vx[s], vy = pc.A.vy[s], vz = pc.A.vz[s], w = pc.A.w[s];
+        __syncwarp(grp);  // every lane of the mover has read the slot before it becomes a hole
+        if (kz == 0) {
+            M.x[i] = x;
+            M.y[i] = y;
+            M.z[i] = z;
+            M.vx[i] = vx;
+            M.vy[i] = vy;
+            M.vz[i] = vz;
+            M.w[i] = w;
+            M.id[i] = pc.A.id[s];
+            push_hole(pc.A, s, b, off, holes, hl);
+        }
+        int ci, cj, ck;
+        double fx, fy, fz;
+        cell_linear(g, x, y, z, ci, cj, ck, fx, fy, fz);
+        const uint32_t bi = b % (uint32_t)g.nx, bj = (b / (uint32_t)g.nx) % (uint32_t)g.ny,
+                       bk = b / ((uint32_t)g.nx * (uint32_t)g.ny);
+        const int shx = cell_step(ci - (int)bi, g.nx), shy = cell_step(cj - (int)bj, g.ny),
+                  shz = cell_step(ck - (int)bk, g.nz);
+        double sx[W], sy[W], sz[W];
+        weights_scaled<ORDER>(fx, sx);
+        weights_scaled<ORDER>(fy, sy);
+        weights_scaled<ORDER>(fz, sz);
+        const double qw = qs * w;
+        const double wq0 = qw * vx, wq1 = qw * vy, wq2 = qw * vz;
+        const bool zin = kz + shz >= 0 && kz + shz < W;
+        const size_t Z = (size_t)wrap_index(ck + OFF + kz, g.nz);
+#pragma unroll
+        for (int jj = 0; jj < W; ++jj) {
+            const bool yin = zin && jj + shy >= 0 && jj + shy < W;
+            const double bb = sy[jj] * sz[kz];
+            const size_t row = ((size_t)wrap_index(cj + OFF + jj, g.ny) + (size_t)g.ny * Z) * (size_t)g.nx;
+#pragma unroll
+            for (int ix = 0; ix < W; ++ix) {
+                if (yin && ix + shx >= 0 && ix + shx < W) continue;  // deposited by the fused kernel
+                const double v = sx[ix] * bb;
+                if (v == 0.0) continue;
+                const size_t node = row + (size_t)wrap_index(ci + OFF + ix, g.nx);
+                atomicAdd(jx + node, wq0 * v);
+                atomicAdd(jy + node, wq1 * v);
+                atomicAdd(jz + node, wq2 * v);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+bool fused_step_available(int order, int kernel) {
+    static const bool v1 = [] {
+        const char* e = std::getenv("PICGPU_J_LANE");
+        return e && std::string(e) == "v1";
+    }();
+#ifdef PICGPU_J_G8
+    if (order != 1) return false;
+#endif
+    const int k = kernel == kJDefault ? j_variant() : kernel;
+    return !v1 && (order == 1 || k == kJLane);
+}
+
+void launch_deposit_current_push(int order, const GridD& g, const PushCtx& pc, const uint32_t* off,
+                                 const uint32_t* cnt, double q, double* j, int num_sms, cudaStream_t st) {
+    if (g.slab) throw Status{PICGPU_ELOGIC, "fused step: not available on a slab store"};
+    switch (order) {
+        case 1: launch_push_order<1>(g, pc, off, cnt, q, j, num_sms, st); break;
+        case 2: launch_push_order<2>(g, pc, off, cnt, q, j, num_sms, st); break;
+        case 3: launch_push_order<3>(g, pc, off, cnt, q, j, num_sms, st); break;
+        default: throw Status{PICGPU_EINVAL, "deposit: shape order must be 1, 2 or 3"};
+    }
+}
+
+void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, const uint32_t* off,
+                   uint32_t* holes, uint32_t* hl, double q, double* j, int num_sms, cudaStream_t st) {
+    const double qs = q * (order == 3 ? 1.0 / 216.0 : order == 2 ? 0.125 : 1.0);
+    auto* kern = order == 1 ? k_movers<1> : order == 2 ? k_movers<2> : k_movers<3>;
+    kern<<<num_sms * 4, 256, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells, j + 2 * (size_t)g.ncells);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
 }  // namespace picgpu

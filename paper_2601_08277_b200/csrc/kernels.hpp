@@ -17,6 +17,31 @@ enum JKernel { kJDefault = -1, kJLane = 0, kJVector = 1, kJMatrix = 2 };
 void launch_deposit_current(int order, const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt,
                             double q, double* j, int num_sms, cudaStream_t st, int kernel = kJDefault);
 
+// Fused step kernel (the default session step): pic::advance + detect_moves +
+// deposit_scalar in ONE pass over the bins.  Every particle is pushed in
+// registers (bit-exact), written back, and -- if its cell did not change --
+// deposited on the lane kernel's register window; a particle whose cell changed
+// is listed (slot, old bin, new cell) for launch_movers, which copies it into
+// the mover records, leaves a hole in its old bin and deposits its J with
+// L2 reductions.  Non-slab stores only.
+struct PushCtx {
+    Soa A;                   // the binned store (positions are updated in place)
+    double dt, cap2;
+    uint32_t* mslot;         // per mover: its slot, its old bin, its new cell
+    uint32_t* mbin;
+    uint32_t* mcell;
+    uint32_t mcap;
+    StepCounters* ctr;       // nmovers (all detected), err
+};
+// The fused form exists for the default lane kernel (v3) family only.
+bool fused_step_available(int order, int kernel);
+void launch_deposit_current_push(int order, const GridD& g, const PushCtx& pc, const uint32_t* off,
+                                 const uint32_t* cnt, double q, double* j, int num_sms, cudaStream_t st);
+// Movers of the fused kernel: slot -> mover record M[i] (+ hole in the old bin)
+// and their J contribution (RED.ADD.F64).
+void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, const uint32_t* off,
+                   uint32_t* holes, uint32_t* hl, double q, double* j, int num_sms, cudaStream_t st);
+
 // deposit_density.cu ---------------------------------------------------------
 // rho[node] = ordered sum (storage order) of quantity[s] * S (quantity NULL: qscale*w[s]), over binned,
 // cell-sorted storage (bins ascending by cell, slot order within a bin).

@@ -85,30 +85,6 @@ __device__ __forceinline__ void copy_particle(const Soa src, uint64_t s, const S
     dst.id[d] = src.id[s];
 }
 
-// detail::wrap_position, workload.hpp:128-132 (a power-of-two length divides
-// exactly as a multiply by its reciprocal).
-__device__ __forceinline__ double wrap_position(double x, double origin, double length, double inv, int pow2) {
-    const double t = __dsub_rn(x, origin);
-    double r = __dsub_rn(x, __dmul_rn(length, floor(pow2 ? __dmul_rn(t, inv) : __ddiv_rn(t, length))));
-    if (__dsub_rn(r, origin) >= length) r = origin;
-    return r;
-}
-
-// One particle of pic::advance (workload.hpp:144-153); returns false on a cap
-// violation (the reference throws std::domain_error).
-// P2: every spacing and box length is a power of two (checked on the host),
-// so the divide-or-multiply choice folds away at compile time.
-template <bool P2 = false>
-__device__ __forceinline__ bool push_one(const GridD& g, double dt, double cap2, double& x, double& y, double& z,
-                                         double vx, double vy, double vz) {
-    const double v2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
-    if (v2 > cap2) return false;
-    x = wrap_position(__dadd_rn(x, __dmul_rn(vx, dt)), g.gox, g.gLx, g.ginv_Lx, P2 || g.gpow2Lx);
-    y = wrap_position(__dadd_rn(y, __dmul_rn(vy, dt)), g.oy, g.Ly, g.inv_Ly, P2 || g.pow2Ly);
-    z = wrap_position(__dadd_rn(z, __dmul_rn(vz, dt)), g.oz, g.Lz, g.inv_Lz, P2 || g.pow2Lz);
-    return true;
-}
-
 // Largest b in [0, nb) with so[b] <= s (bins of one CTA, offsets in smem).
 __device__ __forceinline__ int find_bin(const uint32_t* so, int nb, uint32_t s) {
     int lo = 0, hi = nb - 1;
@@ -233,14 +209,6 @@ __global__ void __launch_bounds__(256) k_relayout(const Soa src, const uint32_t*
 // particle can carry: non-finite positions are rejected), so the push can
 // stream over raw slots without knowing the bin layout.
 
-// floor((x - o) / h) exactly as locate_axis computes it (before its range
-// handling).  For u >= 0 the fraction u - floor(u) is exact and < 1, so equal
-// non-negative floors on every axis mean the same cell.
-__device__ __forceinline__ double axis_floor(double x, double o, double h, double inv, int pow2) {
-    const double t = __dsub_rn(x, o);
-    return floor(pow2 ? __dmul_rn(t, inv) : __ddiv_rn(t, h));
-}
-
 // Push (optional) + move detection (pic::advance + Gpma::detect_moves,
 // workload.hpp:139-155, gpma.hpp:162-177).  Each CTA streams one contiguous
 // chunk of UNR*256 slots.  Measured at C2 (tools/push_sweep.sh): one slot per
@@ -265,14 +233,6 @@ __device__ __forceinline__ double axis_floor(double x, double o, double h, doubl
 #ifndef PICGPU_PUSH_CONDLOAD
 #define PICGPU_PUSH_CONDLOAD 0
 #endif
-
-// A departure: the slot becomes a hole of its bin (sentinel x) and joins the
-// bin's hole list.
-__device__ __forceinline__ void push_hole(const Soa& A, uint64_t s, uint32_t b, const uint32_t* __restrict__ off,
-                                          uint32_t* __restrict__ holes, uint32_t* __restrict__ hl) {
-    A.x[s] = __longlong_as_double(kGapBits);
-    hl[off[b] + atomicAdd(&holes[b], 1u)] = (uint32_t)s;
-}
 
 // RECORD = false: push and count the moved particles only (the store is
 // re-sorted from scratch afterwards; no flags, movers or departures).
@@ -1204,6 +1164,8 @@ void BinStore::ensure_movers(size_t m) {
     if (m <= mcap) return;
     M.ensure(m);
     mcell.ensure(m * 4);
+    mslot.ensure(m * 4);
+    mbin.ensure(m * 4);
     ovf.ensure(m * 4);
     ovf_left.ensure(m * 4);
     mcap = m;
@@ -1223,6 +1185,8 @@ void BinStore::ensure_movers_keep(size_t m, size_t keep) {
     PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
     swap_soa(M, M2);
     swap_buf(mcell, mcell2);
+    mslot.ensure(m * 4);
+    mbin.ensure(m * 4);
     ovf.ensure(m * 4);
     ovf_left.ensure(m * 4);
     mcap = m;
@@ -1288,6 +1252,24 @@ void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
         PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, counters.p, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
         return;
     }
+    enqueue_migrate();
+}
+
+void BinStore::enqueue_fused(int order, double q, double* J, double dt, double cap2, cudaEvent_t after_kernel) {
+    if (g.slab) throw Status{PICGPU_ELOGIC, "fused step: not available on a slab store"};
+    ensure_movers(std::max<size_t>(size_t(1) << 16, n / 4));
+    StepCounters* ctr = counters.as<StepCounters>();
+    PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
+    if (!g.ncells || !n) {
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, ctr, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
+        return;
+    }
+    hl.ensure(capacity * 4 + 4);
+    PushCtx pc{A.soa(), dt, cap2, mslot.as<uint32_t>(), mbin.as<uint32_t>(), mcell.as<uint32_t>(), (uint32_t)mcap,
+               ctr};
+    launch_deposit_current_push(order, g, pc, d_off(), d_cnt(), q, J, num_sms, st);
+    if (after_kernel) PICGPU_CUDA_TRY(cudaEventRecord(after_kernel, st));
+    launch_movers(order, g, pc, M.soa(), d_off(), holes.as<uint32_t>(), hl.as<uint32_t>(), q, J, num_sms, st);
     enqueue_migrate();
 }
 

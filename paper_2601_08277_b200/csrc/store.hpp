@@ -40,18 +40,6 @@ struct SoaBuf {
     Soa soa() const;
 };
 
-// Device counters of one step (read back once per step).
-struct StepCounters {
-    unsigned long long moved;
-    unsigned int nmovers;     // movers detected (may exceed mover capacity)
-    unsigned int noverflow;   // arrivals that found no slack in their own bin
-    int err;                  // picgpu_status of the first device-side error
-    unsigned int nborrowed;   // ... placed by borrowing a following bin's slack
-    unsigned int nleft;       // ... with no donor (-> rebuild)
-    unsigned int nimport;     // arrivals from neighbour slabs appended to the movers
-    unsigned int nleave[2];   // particles that left the slab to the left / right
-};
-
 constexpr int kBorrowScanBins = 4;  // GpmaConfig::borrow_scan_bins (gpma.hpp:25)
 
 struct BinStore {
@@ -68,6 +56,7 @@ struct BinStore {
     DevBuf keys, keys2, skeys, vals, vals2, start, endp, caps, cub_tmp;
     SoaBuf M;                 // mover records
     DevBuf mcell, ovf, ovf_left;  // mover target cell, overflow list, unplaced overflow
+    DevBuf mslot, mbin;       // fused step: each mover's slot and old bin
     DevBuf locks;             // per-bin try-locks of the borrow kernel (always released)
     DevBuf holes;             // per-bin holes in the extent [off, off+cnt) (GPMA gaps)
     DevBuf hl;                // per-bin hole lists, slot-indexed like the bins: bin c's holes
@@ -101,6 +90,13 @@ struct BinStore {
     // slack, borrow from the following bins for full bins; counters copied to
     // the host.
     void enqueue_incremental(bool push, double dt, double cap2);
+    // The fused step (non-slab): push + detect + J of the particles that stay
+    // in their cell in one pass over the bins, then the movers (records,
+    // holes, their J) and the migration as in enqueue_incremental.  J (3 x
+    // ncells, zeroed) receives the whole deposit unless the mover buffer
+    // overflows (finish_incremental then re-sorts; the caller re-deposits).
+    // `after_kernel` (optional) is recorded between the fused kernel and the movers.
+    void enqueue_fused(int order, double q, double* J, double dt, double cap2, cudaEvent_t after_kernel = nullptr);
     // The same step in two halves around a slab exchange: detect (push +
     // move detection; leavers go to the exchange buffer
     // `lrec`), then migrate (optional arrivals appended to the movers,

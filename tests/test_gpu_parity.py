@@ -441,3 +441,58 @@ def test_session_mover_buffer_overflow_resorts_exactly(pg, orc):
         assert np.all(np.diff(cells.astype(np.int64)) >= 0)  # storage is cell-sorted
         J = S.current()
         assert peak_rel_err((J.jx, J.jy, J.jz), orc.deposit_current(g, 3, ref, q)) <= J_TOL
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+@pytest.mark.parametrize("gi", [0, 1, 3])
+def test_fused_step_matches_unfused_and_oracle(pg, orc, order, gi):
+    """The default step fuses push + move detection + J into one pass over the
+    bins (movers deposited by their own kernel).  Against the unfused step
+    (push kernel, sort, J kernel) and the oracle: positions and moved counts
+    bit-exact, the same bin sets, J within the bar, rho bit-exact."""
+    kw = GRIDS[gi]
+    g = O.Grid.make(kw["nx"], kw.get("ny"), kw.get("nz"), kw.get("dx", 1.0), kw.get("dy", 1.0),
+                    kw.get("dz", 1.0), kw.get("origin", (0.0, 0.0, 0.0)))
+    s = orc.make_plasma(g, 5, 0.08 if gi == 1 else 0.4, 17 + gi)
+    q = -1.0
+    G = to_pg_grid(g)
+    perm, _, _ = orc.counting_sort(g, s)
+    cur = {k: np.ascontiguousarray(v[perm]) for k, v in s.items()}
+    with pg.Session(G, order=order) as A, pg.Session(G, order=order) as B:
+        A.upload(s, q=q)
+        B.upload(s, q=q)
+        for step in range(5):
+            moved = orc.advance(g, 0.5, cur)
+            sa = A.step(0.5, pg.STEP_DEFAULT | pg.STEP_DENSITY)
+            sb = B.step(0.5, pg.STEP_DEFAULT | pg.STEP_DENSITY | pg.STEP_UNFUSED)
+            assert sa["moved"] == sb["moved"] == moved
+            pa, pb = A.particles(), B.particles()
+            oa, ob, oc = np.argsort(pa.id), np.argsort(pb.id), np.argsort(cur["id"])
+            for k in ("x", "y", "z", "vx", "vy", "vz", "w"):
+                assert np.array_equal(getattr(pa, k)[oa], cur[k][oc]), (step, k)
+                assert np.array_equal(getattr(pb, k)[ob], cur[k][oc]), (step, k)
+            (offa, cnta), (offb, cntb) = A.bins(), B.bins()
+            assert np.array_equal(cnta, cntb)
+            ca = np.repeat(np.arange(G.ncells), cnta.astype(np.int64))
+            assert np.array_equal(ca, orc.cells(g, {"x": pa.x, "y": pa.y, "z": pa.z}))
+            # same set per bin
+            assert np.array_equal(pa.id[np.lexsort((pa.id, ca))], pb.id[np.lexsort((pb.id, ca))])
+            pd = {"x": pa.x, "y": pa.y, "z": pa.z, "vx": pa.vx, "vy": pa.vy, "vz": pa.vz, "w": pa.w}
+            want = orc.deposit_current(g, order, pd, q)
+            Ja, Jb = A.current(), B.current()
+            assert peak_rel_err((Ja.jx, Ja.jy, Ja.jz), want) <= J_TOL
+            assert peak_rel_err((Jb.jx, Jb.jy, Jb.jz), want) <= J_TOL
+            assert np.array_equal(A.density(), orc.deposit_density(g, order, pd, q * pa.w))
+
+
+def test_fused_step_cap_violation(pg):
+    """The fused pass raises the reference's exception for a displacement above
+    the one-cell cap (advance, workload.hpp:147: std::domain_error)."""
+    G = pg.Grid.make(8, 8, 8)
+    s = _line_store([0.5, 2.5], [0.1, 0.1])
+    with pg.Session(G, order=3) as S:
+        s2 = dict(s)
+        s2["vx"] = np.array([0.1, 3.0])
+        S.upload(s2, q=1.0)
+        with pytest.raises(pg.DomainError):
+            S.step(0.5)
