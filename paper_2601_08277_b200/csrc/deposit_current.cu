@@ -662,6 +662,22 @@ __device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PD
                axis_floor(d.y, g.oy, g.dy, g.inv_dy, g.pow2y) == dcj &&
                axis_floor(d.z, g.oz, g.dz, g.inv_dz, g.pow2z) == dck;
     if (same) return true;
+    if constexpr (P2) {
+        // Pushed positions are wrapped into [o, o + L), so u = (x-o)*inv lies in
+        // [0, n) and locate_axis's cell is floor(u) = c + floor(f) exactly; a
+        // one-cell step leaves f in [-1, 2) (otherwise: wrapped around the box)
+        if (fx >= -1.0 && fx < 2.0 && fy >= -1.0 && fy < 2.0 && fz >= -1.0 && fz < 2.0) {
+            shx = fx < 0.0 ? -1 : (fx >= 1.0 ? 1 : 0);
+            shy = fy < 0.0 ? -1 : (fy >= 1.0 ? 1 : 0);
+            shz = fz < 0.0 ? -1 : (fz >= 1.0 ? 1 : 0);
+            fx -= (double)shx;
+            fy -= (double)shy;
+            fz -= (double)shz;
+            mv = true;
+            mv_cell = (uint32_t)(i + shx) + (uint32_t)g.nx * ((uint32_t)(j + shy) + (uint32_t)g.ny * (uint32_t)(k + shz));
+            return true;
+        }
+    }
     int ni, nj, nk;
     const uint32_t nc = cell_linear(g, d.x, d.y, d.z, ni, nj, nk, fx, fy, fz);  // exact (pic::cell_of)
     if (nc == b) return true;  // a periodic image of the bin's cell
@@ -1657,10 +1673,13 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
         const double wq0 = qw * vx, wq1 = qw * vy, wq2 = qw * vz;
         const bool zin = kz + shz >= 0 && kz + shz < W;
         const size_t Z = (size_t)wrap_index(ck + OFF + kz, g.nz);
+        double szk = sz[0];  // sz[kz] without a local-memory array
+#pragma unroll
+        for (int t = 1; t < W; ++t) szk = kz == t ? sz[t] : szk;
 #pragma unroll
         for (int jj = 0; jj < W; ++jj) {
             const bool yin = zin && jj + shy >= 0 && jj + shy < W;
-            const double bb = sy[jj] * sz[kz];
+            const double bb = sy[jj] * szk;
             const size_t row = ((size_t)wrap_index(cj + OFF + jj, g.ny) + (size_t)g.ny * Z) * (size_t)g.nx;
 #pragma unroll
             for (int ix = 0; ix < W; ++ix) {
