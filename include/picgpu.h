@@ -203,6 +203,8 @@ typedef struct picgpu_step_stats {
     double empty_slot_ratio;
     uint64_t capacity;
     uint64_t num_particles;
+    uint32_t fused;        /* 1 if push + detect + J ran as one fused pass (PICGPU_STEP_UNFUSED) */
+    uint32_t reserved_;
 } picgpu_step_stats;
 
 PICGPU_API int picgpu_session_create(const picgpu_grid* g, const picgpu_session_config* cfg, picgpu_session** out);
@@ -248,6 +250,11 @@ PICGPU_API int picgpu_session_global_sort(picgpu_session* s);
  * DFMA (default), 1 warp-per-pencil DFMA ("vector", rhocell-vector modes),
  * 2 FP64 tensor-core DMMA ("matrix", tile-engine modes). */
 PICGPU_API int picgpu_session_set_kernel(picgpu_session* s, int family);
+/* Fusion policy of PUSH|SORT|CURRENT steps: the fused pass runs while the
+ * previous pushed step moved less than this fraction of the particles (default
+ * 0.03, or PICGPU_FUSE_MAX_MOVED); 0 never fuses, >1 always does.  EINVAL if
+ * negative or NaN.  No reference counterpart (a performance knob). */
+PICGPU_API int picgpu_session_set_fusion(picgpu_session* s, double max_moved_fraction);
 
 /* pic::WorkloadConfig (workload.hpp:16-44) and make_workload (:75-125): ppc
  * particles per cell on a regular sub-lattice, Maxwellian velocities

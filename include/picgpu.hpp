@@ -332,6 +332,7 @@ class Session {
     std::size_t capacity() const { return picgpu_session_capacity(h_); }
     std::size_t size() const { return picgpu_session_num_particles(h_); }
     void set_kernel(int family) { check(picgpu_session_set_kernel(h_, family)); }
+    void set_fusion(double max_moved_fraction) { check(picgpu_session_set_fusion(h_, max_moved_fraction)); }
     void make_workload(const picgpu_workload& w) { check(picgpu_session_make_workload(h_, &w)); }
     std::array<double, PICGPU_NPHASES> phase_ms() const {
         std::array<double, PICGPU_NPHASES> ms{};

@@ -110,7 +110,8 @@ GridSpec = Grid
 class StepStats(C.Structure):
     _fields_ = [("moved", C.c_uint64), ("inserts", C.c_uint64), ("overflowed", C.c_uint64),
                 ("rebuilt", C.c_uint32), ("global_sorted", C.c_uint32), ("empty_slot_ratio", C.c_double),
-                ("capacity", C.c_uint64), ("num_particles", C.c_uint64)]
+                ("capacity", C.c_uint64), ("num_particles", C.c_uint64), ("fused", C.c_uint32),
+                ("reserved_", C.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -256,6 +257,7 @@ def lib():
     L.picgpu_deposit_rhocell_vector.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, C.c_int, _P, _P, _P,
                                                                          C.POINTER(_D)]
     L.picgpu_session_set_kernel.argtypes = [_P, C.c_int]
+    L.picgpu_session_set_fusion.argtypes = [_P, C.c_double]
     L.picgpu_session_generate_lwfa.argtypes = [_P, C.POINTER(LwfaConfig)]
     L.picgpu_session_shift_window.argtypes = [_P, C.c_int, _D, _U64, _U64, C.POINTER(_U64), C.POINTER(_U64)]
     L.picgpu_session_grid.argtypes = [_P, G]
@@ -572,6 +574,11 @@ class Session:
     def set_kernel(self, family: int):
         """J kernel family: KERNEL_LANE (default), KERNEL_VECTOR (warp DFMA), KERNEL_MATRIX (DMMA)."""
         _check(lib().picgpu_session_set_kernel(self._h, family))
+
+    def set_fusion(self, max_moved_fraction: float):
+        """Fuse push + detect + J while the previous step moved less than this
+        fraction of the particles (default 0.03; 0 never, > 1 always)."""
+        _check(lib().picgpu_session_set_fusion(self._h, max_moved_fraction))
 
     def make_workload(self, cfg: WorkloadConfig):
         """Replace the particles by make_workload(cfg) generated on the device."""

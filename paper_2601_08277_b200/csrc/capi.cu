@@ -199,6 +199,11 @@ struct picgpu_session {
     double phase_ms[PICGPU_NPHASES] = {};
     uint64_t phase_launches[PICGPU_NPHASES] = {};
     int kernel = -1;  // JKernel family; -1: library default
+    double last_moved = 0.0;  // moved fraction of the previous pushed step (fusion policy)
+    double fuse_max = [] {    // fuse while last_moved < fuse_max (picgpu_session_set_fusion)
+        const char* e = std::getenv("PICGPU_FUSE_MAX_MOVED");
+        return e ? std::atof(e) : 0.03;
+    }();
     // x-slab decomposition (picgpu_session_set_slab)
     bool slab = false;
     int ghost = 0;
@@ -516,6 +521,35 @@ int picgpu_cell_of(const picgpu_grid* g, const double* x, const double* y, const
 
 // ---- session ---------------------------------------------------------------
 
+// Keep J resident in L2 while the step streams the particle store through it
+// (a persisting access-policy window on the session stream): the fused step's
+// movers and the halo nodes reduce into J with RED.ADD.F64, which otherwise
+// miss L2 after the particle stream and pay a DRAM read-modify-write each.
+// Best effort (PICGPU_L2_PERSIST=0 disables it); C2's J is 50 MB of the 126 MB L2.
+static void keep_fields_in_l2(picgpu_session* s) {
+    const char* e = std::getenv("PICGPU_L2_PERSIST");
+    if (e && e[0] == '0') return;
+    int max_persist = 0, max_window = 0;
+    if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, s->device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, s->device) != cudaSuccess ||
+        max_persist <= 0 || max_window <= 0) {
+        cudaGetLastError();
+        return;
+    }
+    const size_t bytes = (size_t)s->store.g.ncells * 24;
+    const size_t persist = std::min(bytes, (size_t)max_persist);
+    const size_t window = std::min(bytes, (size_t)max_window);
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.base_ptr = s->J.p;
+    a.accessPolicyWindow.num_bytes = window;
+    a.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist / (double)window);
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) != cudaSuccess ||
+        cudaStreamSetAttribute(s->st, cudaStreamAttributeAccessPolicyWindow, &a) != cudaSuccess)
+        cudaGetLastError();
+}
+
 int picgpu_session_create(const picgpu_grid* g, const picgpu_session_config* cfg, picgpu_session** out) {
     *out = nullptr;
     picgpu_session* s = nullptr;
@@ -532,6 +566,7 @@ int picgpu_session_create(const picgpu_grid* g, const picgpu_session_config* cfg
         s->store.init(*g, cfg->gap_ratio, cfg->min_gap, s->st);
         s->J.ensure((size_t)s->store.g.ncells * 24);
         PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)s->store.g.ncells * 24, s->st));
+        keep_fields_in_l2(s);
         s->timing = (cfg->flags & PICGPU_SESSION_TIMING) != 0;
         for (auto& e : s->ev) PICGPU_CUDA_TRY(cudaEventCreate(&e));
         PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
@@ -731,8 +766,13 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
         // the fused step: push + detect + J in one pass over the bins (movers
         // deposited by their own kernel), then the migration
         const uint32_t fuse_mask = PICGPU_STEP_PUSH | PICGPU_STEP_SORT | PICGPU_STEP_CURRENT;
+        // Policy: the fused pass deposits movers' out-of-window taps with L2
+        // reductions, so it pays off at low migration (C2, ~1.2% per step:
+        // 2.04 vs 2.41 ms) and loses at high migration (C4 5.6%: 22.9 vs 20.8
+        // ms; C3 11%: 2x slower): fuse while the previous step moved less than
+        // PICGPU_FUSE_MAX_MOVED (default 3%) of the particles.
         const bool fused = (flags & fuse_mask) == fuse_mask && !(flags & PICGPU_STEP_UNFUSED) &&
-                           fused_step_available(s->order, s->kernel);
+                           s->last_moved < s->fuse_max && fused_step_available(s->order, s->kernel);
         if (fused) {
             const double cap2 = cap2_of(bs.hg, dt);
             const uint64_t l0 = g_launches.load();
@@ -749,6 +789,7 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
                 throw Status{c.err, "advance: particle displacement exceeds the single-cell cap"};
             if (c.err) throw Status{c.err, "cell_of: non-finite particle position"};
             stats.moved = c.nmovers;
+            stats.fused = 1;
             stats.inserts = std::min<uint64_t>(c.nmovers, mcap0);
             stats.overflowed = c.noverflow;
             if (T) {
@@ -814,11 +855,20 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
             }
             if (flags & PICGPU_STEP_DENSITY) accumulate_phase(s, 4, 5, 6, lr);
         }
+        if (flags & PICGPU_STEP_PUSH)
+            s->last_moved = bs.n ? (double)stats.moved / (double)bs.n : 0.0;
         stats.rebuilt = bs.rebuilds != rebuilds0;
         stats.capacity = bs.capacity;
         stats.num_particles = bs.n;
         stats.empty_slot_ratio = bs.capacity ? (double)(bs.capacity - bs.n) / (double)bs.capacity : 1.0;
         if (out) *out = stats;
+    });
+}
+
+int picgpu_session_set_fusion(picgpu_session* s, double max_moved_fraction) {
+    return guard([&] {
+        if (!(max_moved_fraction >= 0.0)) throw Status{PICGPU_EINVAL, "set_fusion: threshold must be >= 0"};
+        s->fuse_max = max_moved_fraction;
     });
 }
 
@@ -1093,6 +1143,8 @@ int picgpu_session_step_end(picgpu_session* s, const double* arrivals, uint64_t 
             }
             if (flags & PICGPU_STEP_DENSITY) accumulate_phase(s, 4, 5, 6, lr);
         }
+        if (flags & PICGPU_STEP_PUSH)
+            s->last_moved = bs.n ? (double)stats.moved / (double)bs.n : 0.0;
         stats.rebuilt = bs.rebuilds != rebuilds0;
         stats.capacity = bs.capacity;
         stats.num_particles = bs.n;

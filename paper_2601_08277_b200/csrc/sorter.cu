@@ -1230,7 +1230,11 @@ void BinStore::enqueue_migrate() {
     const size_t nc = g.ncells;
     StepCounters* ctr = counters.as<StepCounters>();
     if (nc) {
-        k_insert<<<num_sms * 4, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap, ctr, A.soa(),
+        static const int mult = [] {
+            const char* e = std::getenv("PICGPU_INSERT_BLOCKS");
+            return e ? std::max(1, std::atoi(e)) : 4;
+        }();
+        k_insert<<<num_sms * mult, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap, ctr, A.soa(),
                                               off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>(),
                                               holes.as<uint32_t>(), hl.as<uint32_t>());
         note_launch();

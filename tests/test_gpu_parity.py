@@ -459,6 +459,7 @@ def test_fused_step_matches_unfused_and_oracle(pg, orc, order, gi):
     perm, _, _ = orc.counting_sort(g, s)
     cur = {k: np.ascontiguousarray(v[perm]) for k, v in s.items()}
     with pg.Session(G, order=order) as A, pg.Session(G, order=order) as B:
+        A.set_fusion(2.0)  # fuse every step, whatever the migration
         A.upload(s, q=q)
         B.upload(s, q=q)
         for step in range(5):
@@ -496,3 +497,27 @@ def test_fused_step_cap_violation(pg):
         S.upload(s2, q=1.0)
         with pytest.raises(pg.DomainError):
             S.step(0.5)
+
+
+def test_fusion_policy_follows_migration(pg, orc):
+    """The fused pass runs while the previous step's moved fraction stays under
+    the session's threshold (default 3%), the separate kernels otherwise."""
+    g = O.Grid.make(16)
+    cold = orc.make_plasma(g, 4, 0.01, 3)  # ~1% of the particles change cell per step
+    hot = orc.make_plasma(g, 4, 0.3, 3)    # ~30%
+    with pg.Session(to_pg_grid(g), order=3) as S:
+        with pytest.raises(pg.InvalidArgument):
+            S.set_fusion(-1.0)
+        S.upload(cold, q=-1.0)
+        assert [S.step(0.5)["fused"] for _ in range(3)] == [1, 1, 1]
+        S.upload(hot, q=-1.0)
+        first = S.step(0.5)  # decided on the previous (cold) step
+        assert first["fused"] == 1 and first["moved"] > 0.03 * S.num_particles
+        assert [S.step(0.5)["fused"] for _ in range(2)] == [0, 0]
+        S.set_fusion(0.0)
+        S.upload(cold, q=-1.0)
+        assert S.step(0.5)["fused"] == 0
+        S.set_fusion(2.0)
+        S.upload(hot, q=-1.0)
+        assert [S.step(0.5)["fused"] for _ in range(2)] == [1, 1]
+        assert S.step(0.5, pg.STEP_DEFAULT | pg.STEP_UNFUSED)["fused"] == 0
