@@ -5,18 +5,23 @@ Workload (N=1): BASELINE configs[1] ("C2"): 128^3 cells, 16 particles/cell,
 order 3 (QSP), Maxwellian u_th = 0.01c, dt = 0.5, seeded synthetic plasma
 (SURVEY 8(d) generator, generated in HBM).  One STEP = the reference's step
 (simulation.hpp:92-176): bit-exact push -> incremental cell sort (bins with
-slack, migration) -> current deposition J.  Inputs stay resident in HBM.
+slack, migration) -> current deposition J.  Inputs stay resident in HBM.  At
+low migration the step runs fused: ONE pass over the bins pushes every
+particle, detects the movers and deposits J (movers' out-of-window taps by a
+small reduction kernel), then the movers are inserted into their new bins.
 
 value  = particles * steps * n_gpus / (max over ranks of the device time of K steps)
 e2e    = the same metric through the stateless C-ABI drop-in for
          pic::deposit_scalar (picgpu_deposit_current) on pinned HOST buffers:
          H2D of the 7 particle arrays + sort + deposit + D2H of J every step.
-roofline: the J kernel (dominant), timed with CUDA events on the session's
+roofline: the dominant kernel (the fused push + detect + J kernel, or the J
+         kernel in unfused steps), timed with CUDA events on the session's
          stream inside the timed region.  Order 3 is FP64-bound: achieved =
-         particles * 534 flops (reference tally, deposit.hpp:336-345) / launch
-         time, against the FP64 peak measured in-run by a DFMA microbenchmark
-         (MEASURED_PEAKS.json has no FP64 figure); the HBM view (56 + 24/ppc
-         bytes per deposit vs MEASURED_PEAKS hbm_gbs) is reported beside it.
+         particles * 534 flops (reference tally, deposit.hpp:336-345; the
+         push's flops are not counted) / launch time, against the FP64 peak
+         measured in-run by a DFMA microbenchmark (MEASURED_PEAKS.json has no
+         FP64 figure); the HBM view (56 [+ 24 written back when fused] +
+         24/ppc bytes per deposit vs MEASURED_PEAKS hbm_gbs) is reported beside it.
 cpu_baseline: the reference's own step (oracle/_ref: advance + detect_moves +
          apply_pending_moves + deposit_scalar), all host threads, each thread
          an independent 32^3 x 16 ppc sub-box (bounded sample).
@@ -185,12 +190,12 @@ def run_reference_arm(args, cfgname):
     return 0
 
 
-def load_traffic(order):
+def load_traffic(order, fused):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")  # from an ncu --set full capture
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(f"order{order}")
+        return d.get(f"order{order}" if fused else f"order{order}_unfused")
     except Exception:
         return None
 
@@ -283,12 +288,14 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     moved = 0
     rebuilds = 0
+    fused_steps = 0
     with Clocks(local) as clk:
         barrier()
         e0.record(stream)
         for it in range(args.steps):
             st = step()
             moved += st["moved"]
+            fused_steps += st.get("fused", 0)
             if window is not None and it % 2 == 1:  # C4 moving window: one cell every 2 steps
                 window()
             rebuilds += st["rebuilt"]
@@ -306,16 +313,18 @@ def main():
     j_ms, j_launches = phases["deposit_current"]
     j_avg_s = j_ms / max(j_launches, 1) * 1e-3
 
-    # roofline of the dominant kernel (J deposition)
+    # roofline of the dominant kernel: J deposition, fused with the push (positions
+    # read with the particle and written back: +24 B) when the steps ran fused
+    fused = fused_steps == args.steps
     hbm_peak, hbm_src = peaks()
     cells = grid.ncells
-    bytes_per = 56 + 24 * cells / n  # J written once per node, amortised over the particles
+    bytes_per = 56 + (24 if fused else 0) + 24 * cells / n  # J written once per node, amortised
     hbm_achieved = n * bytes_per / j_avg_s / 1e9
     fp64_peak = pg.fp64_peak_tflops(local)
     fp64_achieved = n * FLOPS[order] / j_avg_s / 1e12
     frac_hbm = hbm_achieved / hbm_peak
     frac_fp64 = fp64_achieved / fp64_peak
-    traffic = load_traffic(order)
+    traffic = load_traffic(order, fused)
     if frac_fp64 >= frac_hbm:
         roof = {"bound": "fp64", "achieved": fp64_achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": frac_fp64, "traffic": traffic,
@@ -324,7 +333,8 @@ def main():
     else:
         roof = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s", "frac": frac_hbm,
                 "traffic": traffic, "peak_source": hbm_src, "bytes_per_deposit": bytes_per}
-    roof.update({"kernel": "deposit_current_kernel", "launch_ms": j_avg_s * 1e3,
+    roof.update({"kernel": "deposit_current_kernel_v3 (fused push + detect + J)" if fused else
+                 "deposit_current_kernel_v3 (J)", "launch_ms": j_avg_s * 1e3,
                  "hbm_view": {"achieved_gbs": hbm_achieved, "peak_gbs": hbm_peak, "frac": frac_hbm},
                  "fp64_view": {"achieved_tflops": fp64_achieved, "peak_tflops": fp64_peak, "frac": frac_fp64},
                  "deposits_per_s_kernel_only": n / j_avg_s})
@@ -396,7 +406,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
             "phases_ms_total": {k: v[0] for k, v in phases.items()},
-            "moved_fraction": moved / (n * args.steps), "rebuilds": rebuilds,
+            "moved_fraction": moved / (n * args.steps), "rebuilds": rebuilds, "fused_steps": fused_steps,
         }
         print(json.dumps(line))
     if dist is not None:

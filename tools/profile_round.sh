@@ -12,6 +12,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
     python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/prof_ncu_bench.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"deposit_current_kernel_v3" -s 3 -c 1 \
     -o gpurun_out/full_J python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_push|k_fill_holes|k_insert|k_borrow" -s 12 -c 4 \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_movers|k_insert|k_borrow" -s 9 -c 3 \
     -o gpurun_out/full_sort python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
 ls -la gpurun_out
