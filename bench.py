@@ -210,6 +210,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--slab", action="store_true", help="use the slab-decomposed path even at N=1 (loopback ring)")
+    ap.add_argument("--sort", default="incremental", choices=["incremental", "resort"],
+                    help="incremental: bins with slack + migration (default); resort: a full stable counting "
+                         "sort of the store every step (global_sort each step; the crossover study of C3)")
     args = ap.parse_args()
     nx, ppc, order, u_th, dt, default_steps, desc = CONFIGS[args.config]
     if args.steps is None:
@@ -247,7 +250,10 @@ def main():
         raise SystemExit("multi-GPU runs use the cubic configs (x-slabs of a (n*N) x n x n box) or c5")
     if world == 1 and not args.slab:
         S = pg.Session(grid, order=order, device=local, timing=True)
-        step = lambda: S.step(dt)  # noqa: E731
+        if args.sort == "resort":
+            step = lambda: S.step(dt, pg.STEP_PUSH | pg.STEP_RESORT | pg.STEP_CURRENT)  # noqa: E731
+        else:
+            step = lambda: S.step(dt)  # noqa: E731
     else:
         from paper_2601_08277_b200.slab import RingExchange, SlabSession, slab_step
 
@@ -396,7 +402,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY 8(d) seeded plasma generated in HBM; no dataset)",
-            "config": {"workload": desc + "; step = push + incremental sort + J deposit",
+            "config": {"workload": desc + ("; step = push + full stable re-sort + J deposit" if args.sort == "resort"
+                                           else "; step = push + incremental sort + J deposit"),
                        "grid": list(G_dims), "ppc": ppc,
                        "order": order, "particles_per_gpu": n,
                        "l2": f"inputs larger than L2 ({n * 64 / 1e9:.1f} GB particle store)",

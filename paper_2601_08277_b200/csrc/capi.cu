@@ -285,7 +285,7 @@ static void stateless_current(const picgpu_grid* g, int order, const double* x, 
     S.J.ensure((size_t)gd.ncells * 24);
     double* J = S.J.as<double>();
     PICGPU_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)gd.ncells * 24, st));
-    if (n) launch_deposit_current(order, gd, bs.A.soa(), bs.d_off(), bs.d_cnt(), q, J, bs.num_sms, st, kernel);
+    if (n) launch_deposit_current(order, gd, bs.A.aos(), bs.d_off(), bs.d_cnt(), q, J, bs.num_sms, st, kernel);
     if (timed) PICGPU_CUDA_TRY(cudaEventRecord(ev[2], st));
     if (counters) {
         const uint32_t opt = *tiled_options;
@@ -392,7 +392,7 @@ int picgpu_deposit_current_dev(const picgpu_grid* g, int order, const double* x,
         S.J.ensure((size_t)gd.ncells * 24);
         double* J = S.J.as<double>();
         PICGPU_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)gd.ncells * 24, st));
-        if (n) launch_deposit_current(order, gd, bs.A.soa(), bs.d_off(), bs.d_cnt(), q, J, bs.num_sms, st);
+        if (n) launch_deposit_current(order, gd, bs.A.aos(), bs.d_off(), bs.d_cnt(), q, J, bs.num_sms, st);
         PICGPU_CUDA_TRY(cudaMemcpyAsync(jx, J, (size_t)gd.ncells * 8, cudaMemcpyDeviceToDevice, st));
         PICGPU_CUDA_TRY(cudaMemcpyAsync(jy, J + gd.ncells, (size_t)gd.ncells * 8, cudaMemcpyDeviceToDevice, st));
         PICGPU_CUDA_TRY(
@@ -432,12 +432,13 @@ int picgpu_deposit_density(const picgpu_grid* g, int order, const double* x, con
             PICGPU_CUDA_TRY(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, st));
             PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
             S.aux.ensure(density_scratch_bytes(order, n));
-            const Soa a = bs.A.soa();
+            // the quantity rode in the records' w field: quantity = 1.0 * w (exact)
+            const Aos a = bs.A.aos();
             if (!h)  // storage already cell-sorted: source-cell order == storage order
-                launch_deposit_density(order, gd, a, a.w, 0.0, bs.d_off(), bs.d_cnt(), n, S.aux.p, R, st);
+                launch_deposit_density(order, gd, a, nullptr, 1.0, bs.d_off(), bs.d_cnt(), n, S.aux.p, R, st);
             else
-                launch_deposit_density_merge(order, gd, a, a.w, 0.0, bs.vals2.as<uint32_t>(), bs.d_off(), bs.d_cnt(),
-                                             n, S.aux.p, R, st);
+                launch_deposit_density_merge(order, gd, a, nullptr, 1.0, bs.vals2.as<uint32_t>(), bs.d_off(),
+                                             bs.d_cnt(), n, S.aux.p, R, st);
         }
         d2h(rho, R, (size_t)gd.ncells * 8, st);
         PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
@@ -705,7 +706,7 @@ static void enqueue_deposits(picgpu_session* s, uint32_t flags, uint64_t* lj, ui
         PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)g.ncells * 24, st));
         if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[3], st));
         if (bs.n)
-            launch_deposit_current(s->order, g, bs.A.soa(), bs.d_off(), bs.d_cnt(), s->q, s->J.as<double>(),
+            launch_deposit_current(s->order, g, bs.A.aos(), bs.d_off(), bs.d_cnt(), s->q, s->J.as<double>(),
                                    bs.num_sms, st, s->kernel);
         if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[4], st));
         *lj = g_launches.load() - l0;
@@ -719,7 +720,7 @@ static void enqueue_deposits(picgpu_session* s, uint32_t flags, uint64_t* lj, ui
         bs.fill_holes();
         s->rho.ensure((size_t)g.ncells * 8);
         s->dscratch.ensure(density_scratch_bytes(s->order, bs.capacity));
-        launch_deposit_density(s->order, g, bs.A.soa(), nullptr, s->q, bs.d_off(), bs.d_cnt(), bs.capacity,
+        launch_deposit_density(s->order, g, bs.A.aos(), nullptr, s->q, bs.d_off(), bs.d_cnt(), bs.capacity,
                                s->dscratch.p, s->rho.as<double>(), st);
         if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[6], st));
         *lr = g_launches.load() - l0;

@@ -61,6 +61,61 @@ struct CSoa {
     CSoa(const Soa& s) : x(s.x), y(s.y), z(s.z), vx(s.vx), vy(s.vy), vz(s.vz), w(s.w), id(s.id) {}
 };
 
+// The binned particle store is an ARRAY OF 64-BYTE RECORDS, one per slot
+// (x y z vx vy vz w id: two 32-byte sectors, half a 128-byte line).  Every
+// particle move of the sorter (an arrival into its new bin, a hole filled from
+// a bin's tail, a relayout) then reads and writes whole sectors -- with eight
+// separate arrays a scattered move touched eight sectors and made HBM
+// read-modify-write seven partial ones -- and the deposits still stream
+// consecutive slots of a bin.  Packed host-facing staging (uploads, downloads,
+// mover records) stays structure-of-arrays (Soa).
+struct __align__(64) Part {
+    double x, y, z, vx, vy, vz, w;
+    uint64_t id;
+};
+static_assert(sizeof(Part) == 64, "particle record must be 64 bytes");
+
+struct Aos {
+    Part* p;
+};
+
+struct CAos {
+    const Part* p;
+    CAos() = default;
+    CAos(const Aos& a) : p(a.p) {}
+};
+
+// Whole-record moves (four 16-byte accesses each way).
+__device__ __forceinline__ void copy_record(const Part* __restrict__ src, Part* __restrict__ dst) {
+    const double2* s = reinterpret_cast<const double2*>(src);
+    double2* d = reinterpret_cast<double2*>(dst);
+    const double2 a = s[0], b = s[1], c = s[2], e = s[3];
+    d[0] = a;
+    d[1] = b;
+    d[2] = c;
+    d[3] = e;
+}
+
+__device__ __forceinline__ void store_record(Part* dst, double x, double y, double z, double vx, double vy,
+                                             double vz, double w, uint64_t id) {
+    double2* d = reinterpret_cast<double2*>(dst);
+    d[0] = make_double2(x, y);
+    d[1] = make_double2(z, vx);
+    d[2] = make_double2(vy, vz);
+    d[3] = make_double2(w, __longlong_as_double((long long)id));
+}
+
+// An empty slot: all-ones record (its x is the gap sentinel, see is_gap).
+__device__ __forceinline__ void store_gap_record(Part* dst) {
+    const double g = __longlong_as_double(-1LL);
+    double2* d = reinterpret_cast<double2*>(dst);
+    const double2 v = make_double2(g, g);
+    d[0] = v;
+    d[1] = v;
+    d[2] = v;
+    d[3] = v;
+}
+
 // Device error word: first error code wins (host reads it back once per call).
 __device__ __forceinline__ void raise_error(int* err, int code) {
     if (err) atomicCAS(err, 0, code);
@@ -177,9 +232,9 @@ __device__ __forceinline__ bool push_one(const GridD& g, double dt, double cap2,
 
 // A departure: the slot becomes a hole of its bin (sentinel x) and joins the
 // bin's hole list.
-__device__ __forceinline__ void push_hole(const Soa& A, uint64_t s, uint32_t b, const uint32_t* __restrict__ off,
+__device__ __forceinline__ void push_hole(const Aos& A, uint64_t s, uint32_t b, const uint32_t* __restrict__ off,
                                           uint32_t* __restrict__ holes, uint32_t* __restrict__ hl) {
-    A.x[s] = __longlong_as_double(kGapBits);
+    store_gap_record(A.p + s);  // whole record: two full sectors, no partial-sector write
     hl[off[b] + atomicAdd(&holes[b], 1u)] = (uint32_t)s;
 }
 

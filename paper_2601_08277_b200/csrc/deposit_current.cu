@@ -127,27 +127,30 @@ struct PData {  // one particle as read from the bins
     double x, y, z, vx, vy, vz, w;
 };
 
-// RW: the kernel writes the positions back (fused step): coherent loads, not
-// the read-only path.
+// One particle record: x y | z vx | vy vz | w as three 16-byte loads and one
+// 8-byte load (id is not needed).  RW: the kernel writes the positions back
+// (fused step): coherent loads, not the read-only path.
 template <bool RW = false>
-__device__ __forceinline__ void load_particle(const CSoa& p, uint32_t s, PData& d) {
+__device__ __forceinline__ void load_particle(const CAos& p, uint32_t s, PData& d) {
+    const double2* r = reinterpret_cast<const double2*>(p.p + s);
+    double2 a, b, c;
     if constexpr (RW) {
-        d.x = p.x[s];
-        d.y = p.y[s];
-        d.z = p.z[s];
-        d.vx = p.vx[s];
-        d.vy = p.vy[s];
-        d.vz = p.vz[s];
-        d.w = p.w[s];
+        a = r[0];
+        b = r[1];
+        c = r[2];
+        d.w = p.p[s].w;
     } else {
-        d.x = __ldg(p.x + s);
-        d.y = __ldg(p.y + s);
-        d.z = __ldg(p.z + s);
-        d.vx = __ldg(p.vx + s);
-        d.vy = __ldg(p.vy + s);
-        d.vz = __ldg(p.vz + s);
-        d.w = __ldg(p.w + s);
+        a = __ldg(r);
+        b = __ldg(r + 1);
+        c = __ldg(r + 2);
+        d.w = __ldg(&p.p[s].w);
     }
+    d.x = a.x;
+    d.y = a.y;
+    d.z = b.x;
+    d.vx = b.y;
+    d.vy = c.x;
+    d.vz = c.y;
 }
 
 // Per-particle prologue (shape.hpp:64-85 + particle_weights :46-50): the
@@ -283,7 +286,7 @@ __device__ __forceinline__ void accumulate(double (&acc)[W][NJ][W][3], const dou
 
 template <int ORDER>
 __global__ void __launch_bounds__(JLayout<ORDER>::NT, JCfg<ORDER>::MINB)
-    deposit_current_kernel(const GridD g, const CSoa p, const uint32_t* __restrict__ off,
+    deposit_current_kernel(const GridD g, const CAos p, const uint32_t* __restrict__ off,
                            const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
                            double* __restrict__ jy, double* __restrict__ jz, const int zlen) {
     using C = JCfg<ORDER>;
@@ -645,9 +648,8 @@ __device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PD
     d.x = wrap_fast<P2>(__dadd_rn(d.x, __dmul_rn(d.vx, pc.dt)), g.gox, g.gLx, g.ginv_Lx, g.gpow2Lx);
     d.y = wrap_fast<P2>(__dadd_rn(d.y, __dmul_rn(d.vy, pc.dt)), g.oy, g.Ly, g.inv_Ly, g.pow2Ly);
     d.z = wrap_fast<P2>(__dadd_rn(d.z, __dmul_rn(d.vz, pc.dt)), g.oz, g.Lz, g.inv_Lz, g.pow2Lz);
-    pc.A.x[s] = d.x;
-    pc.A.y[s] = d.y;
-    pc.A.z[s] = d.z;
+    reinterpret_cast<double2*>(pc.A.p + s)[0] = make_double2(d.x, d.y);
+    pc.A.p[s].z = d.z;
     // fractions relative to the bin's cell; with power-of-two spacings u =
     // (x-o)*inv is locate_axis's exact u, so 0 <= u - c < 1 on every axis is
     // exactly "same cell"; otherwise compare the exact floors
@@ -694,7 +696,7 @@ __device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PD
 // with every spacing and box length a power of two (compile-time reciprocals).
 template <int ORDER, class CF = JCfg<ORDER>, int PM = 0>
 __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
-    deposit_current_kernel_v3(const GridD g, const CSoa p, const uint32_t* __restrict__ off,
+    deposit_current_kernel_v3(const GridD g, const CAos p, const uint32_t* __restrict__ off,
                               const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
                               double* __restrict__ jy, double* __restrict__ jz, const int zlen,
                               const PushCtx pc) {
@@ -993,7 +995,7 @@ struct WCfg {
 
 template <int ORDER>
 __global__ void __launch_bounds__(WCfg::NT, WCfg::MINB)
-    deposit_current_warp_kernel(const GridD g, const CSoa p, const uint32_t* __restrict__ off,
+    deposit_current_warp_kernel(const GridD g, const CAos p, const uint32_t* __restrict__ off,
                                 const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
                                 double* __restrict__ jy, double* __restrict__ jz, const int zlen) {
     constexpr int W = 4, OFF = Shape<ORDER>::OFF;
@@ -1252,7 +1254,7 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
 
 template <int ORDER>
 __global__ void __launch_bounds__(MCfg::NT, MCfg::MINB)
-    deposit_current_dmma_kernel(const GridD g, const CSoa p, const uint32_t* __restrict__ off,
+    deposit_current_dmma_kernel(const GridD g, const CAos p, const uint32_t* __restrict__ off,
                                 const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
                                 double* __restrict__ jy, double* __restrict__ jz, const int zlen) {
     constexpr int W = 4, OFF = Shape<ORDER>::OFF;
@@ -1470,7 +1472,7 @@ __global__ void __launch_bounds__(MCfg::NT, MCfg::MINB)
 }
 
 template <int ORDER>
-void launch_dmma(const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+void launch_dmma(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
                  int num_sms, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
@@ -1493,7 +1495,7 @@ void launch_dmma(const GridD& g, const CSoa& p, const uint32_t* off, const uint3
 }
 
 template <int ORDER>
-void launch_warp(const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+void launch_warp(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
                  int num_sms, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
@@ -1518,7 +1520,7 @@ void launch_warp(const GridD& g, const CSoa& p, const uint32_t* off, const uint3
 // z-chunked grid of one of the pencil kernels (v3 or the original v1); PM > 0:
 // the fused push + detect + deposit form of v3.
 template <int ORDER, class C, bool V3, int PM = 0>
-void launch_kernel(const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
                    int num_sms, cudaStream_t st, const PushCtx& pc = PushCtx{}) {
     static_assert(V3 || PM == 0, "the fused step runs on the v3 kernel");
     using L = JLayout<ORDER, C>;
@@ -1555,7 +1557,7 @@ void launch_kernel(const GridD& g, const CSoa& p, const uint32_t* off, const uin
 }
 
 template <int ORDER>
-void launch_order(const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+void launch_order(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
                   int num_sms, cudaStream_t st) {
     static const bool v1 = [] {
         const char* e = std::getenv("PICGPU_J_LANE");
@@ -1590,7 +1592,7 @@ static int j_variant() {
 }
 
 // J must be zeroed by the caller (halo nodes are reduced into it).
-void launch_deposit_current(int order, const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt,
+void launch_deposit_current(int order, const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt,
                             double q, double* j, int num_sms, cudaStream_t st, int kernel) {
     const int k = kernel == kJDefault ? j_variant() : kernel;
     switch (order) {
@@ -1616,7 +1618,7 @@ void launch_push_order(const GridD& g, const PushCtx& pc, const uint32_t* off, c
                        double* j, int num_sms, cudaStream_t st) {
     using C3 = std::conditional_t<ORDER == 1, JCfgCic3, JCfg<ORDER>>;
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
-    const CSoa p(pc.A);
+    const CAos p(pc.A);
     if (p2)
         launch_kernel<ORDER, C3, true, 2>(g, p, off, cnt, q, j, num_sms, st, pc);
     else
@@ -1644,8 +1646,9 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
         const uint64_t i = t / W;
         const int kz = (int)(t % W);
         const uint32_t s = pc.mslot[i], b = pc.mbin[i];
-        const double x = pc.A.x[s], y = pc.A.y[s], z = pc.A.z[s];
-        const double vx = pc.A.vx[s], vy = pc.A.vy[s], vz = pc.A.vz[s], w = pc.A.w[s];
+        const double2* rec = reinterpret_cast<const double2*>(pc.A.p + s);
+        const double2 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3];
+        const double x = r0.x, y = r0.y, z = r1.x, vx = r1.y, vy = r2.x, vz = r2.y, w = r3.x;
         __syncwarp(grp);  // every lane of the mover has read the slot before it becomes a hole
         if (kz == 0) {
             M.x[i] = x;
@@ -1655,7 +1658,7 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
             M.vy[i] = vy;
             M.vz[i] = vz;
             M.w[i] = w;
-            M.id[i] = pc.A.id[s];
+            M.id[i] = (uint64_t)__double_as_longlong(r3.y);
             push_hole(pc.A, s, b, off, holes, hl);
         }
         int ci, cj, ck;

@@ -26,12 +26,12 @@ namespace picgpu {
 namespace {
 
 template <int ORDER>
-__global__ void density_prologue(const GridD g, const CSoa p, const double* __restrict__ quantity, double qscale,
+__global__ void density_prologue(const GridD g, const CAos p, const double* __restrict__ quantity, double qscale,
                                  uint64_t slots, double* __restrict__ S, uint8_t* __restrict__ upb) {
     constexpr int W = Shape<ORDER>::W;
     const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= slots) return;
-    const double x = p.x[s], y = p.y[s], z = p.z[s];
+    const double x = p.p[s].x, y = p.p[s].y, z = p.p[s].z;
     if (is_gap(x)) {  // slack or a hole: a NaN quantity marks it for the gathers
         S[(size_t)(3 * Shape<ORDER>::W) * slots + s] = __longlong_as_double(0x7ff8000000000000LL);
         return;
@@ -50,7 +50,7 @@ __global__ void density_prologue(const GridD g, const CSoa p, const double* __re
 #pragma unroll
         for (int t = 0; t < W; ++t) S[(size_t)(a * W + t) * slots + s] = w[t];
     }
-    S[(size_t)(3 * W) * slots + s] = quantity ? quantity[s] : qscale * p.w[s];
+    S[(size_t)(3 * W) * slots + s] = quantity ? quantity[s] : qscale * p.p[s].w;
     if (ORDER == 2) upb[s] = (uint8_t)bits;
 }
 
@@ -157,7 +157,7 @@ __global__ void density_gather_sorted(const GridD g, const uint32_t* __restrict_
 // locate_axis + Shape<ORDER>::weights as the prologue, so bit-identical), and
 // only the shell's nodes pay for them.
 template <int ORDER>
-__global__ void density_gather_shell(const GridD g, const CSoa p, const double* __restrict__ quantity, double qscale,
+__global__ void density_gather_shell(const GridD g, const CAos p, const double* __restrict__ quantity, double qscale,
                                      const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt,
                                      double* __restrict__ rho, Interior skip) {
     constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
@@ -180,13 +180,13 @@ __global__ void density_gather_shell(const GridD g, const CSoa p, const double* 
                 const uint32_t o = off[c], n = cnt[c];
                 for (uint32_t u = 0; u < n; ++u) {
                     const uint32_t sl = o + u;
-                    const double xv = p.x[sl];
+                    const double xv = p.p[sl].x;
                     if (is_gap(xv)) continue;  // a hole of the bin (GPMA gap)
                     double f[3], w[3][W];
                     int up[3];
                     locate_x(g, xv, f[0]);
-                    locate_axis(p.y[sl], g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
-                    locate_axis(p.z[sl], g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
+                    locate_axis(p.p[sl].y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
+                    locate_axis(p.p[sl].z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
 #pragma unroll
                     for (int a = 0; a < 3; ++a) Shape<ORDER>::weights(f[a], w[a], up[a]);
                     if (ORDER == 2 && (!tap_valid<ORDER>(up[0], xt[xi]) || !tap_valid<ORDER>(up[1], yt[yi]) ||
@@ -199,7 +199,7 @@ __global__ void density_gather_shell(const GridD g, const CSoa p, const double* 
                         sy = t == yt[yi] ? w[1][t] : sy;
                         sz = t == zt[zi] ? w[2][t] : sz;
                     }
-                    const double q = quantity ? quantity[sl] : qscale * p.w[sl];
+                    const double q = quantity ? quantity[sl] : qscale * p.p[sl].w;
                     const double syz = __dmul_rn(sy, sz);
                     const double sv = __dmul_rn(sx, syz);
                     acc = __dadd_rn(acc, __dmul_rn(q, sv));
@@ -297,7 +297,7 @@ constexpr int kRowX = PICGPU_RHO_RX, kRowY = PICGPU_RHO_RY, kRowCap = PICGPU_RHO
 
 template <int ORDER>
 __global__ void __launch_bounds__(kRowX * kRowY)
-    density_rows(const GridD g, const CSoa p, const double* __restrict__ quantity, double qscale,
+    density_rows(const GridD g, const CAos p, const double* __restrict__ quantity, double qscale,
                  const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt, Interior in, int zlen,
                  double* __restrict__ rho) {
     constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
@@ -339,12 +339,12 @@ __global__ void __launch_bounds__(kRowX * kRowY)
                 __syncthreads();  // the previous piece is consumed
                 for (uint32_t i = tid; i < pn; i += NT) {
                     const uint32_t sl = piece + i;
-                    const double x = p.x[sl];
+                    const double x = p.p[sl].x;
                     if (__double_as_longlong(x) == -1LL) {  // slack sentinel
                         s_xs[i] = -1;
                         continue;
                     }
-                    const double y = p.y[sl], z = p.z[sl];
+                    const double y = p.p[sl].y, z = p.p[sl].z;
                     double f[3];
                     s_xs[i] = locate_x(g, x, f[0]);
                     locate_axis(y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kRowX * kRowY)
                         for (int t = 0; t < W; ++t) s_w[a][t][i] = w[t];
                     }
                     if (ORDER == 2) s_up[i] = (unsigned char)bits;
-                    s_q[i] = quantity ? quantity[sl] : qscale * p.w[sl];
+                    s_q[i] = quantity ? quantity[sl] : qscale * p.p[sl].w;
                 }
                 __syncthreads();
                 if (!uses || mend <= piece || mbeg >= piece + pn) continue;
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kRowX * kRowY)
 }
 
 template <int ORDER>
-void prologue(const GridD& g, const CSoa& p, const double* quantity, double qscale, uint64_t slots, void* scratch,
+void prologue(const GridD& g, const CAos& p, const double* quantity, double qscale, uint64_t slots, void* scratch,
               cudaStream_t st, double*& S, uint8_t*& upb) {
     constexpr int W = Shape<ORDER>::W;
     S = static_cast<double*>(scratch);
@@ -408,7 +408,7 @@ void prologue(const GridD& g, const CSoa& p, const double* quantity, double qsca
 }
 
 template <int ORDER>
-void run_sorted(const GridD& g, const CSoa& p, const double* quantity, double qscale, const uint32_t* off, const uint32_t* cnt,
+void run_sorted(const GridD& g, const CAos& p, const double* quantity, double qscale, const uint32_t* off, const uint32_t* cnt,
                 uint64_t slots, void* scratch, double* rho, cudaStream_t st) {
     const Interior in = interior_of<ORDER>(g);
     Interior skip = in;
@@ -448,7 +448,7 @@ void run_sorted(const GridD& g, const CSoa& p, const double* quantity, double qs
 }
 
 template <int ORDER>
-void run_merge(const GridD& g, const CSoa& p, const double* quantity, double qscale, const uint32_t* rank, const uint32_t* off,
+void run_merge(const GridD& g, const CAos& p, const double* quantity, double qscale, const uint32_t* rank, const uint32_t* off,
                const uint32_t* cnt, uint64_t slots, void* scratch, double* rho, cudaStream_t st) {
     double* S;
     uint8_t* upb;
@@ -465,7 +465,7 @@ size_t density_scratch_bytes(int order, uint64_t slots) {
     return (size_t)(3 * W + 1) * slots * sizeof(double) + slots + 16;
 }
 
-void launch_deposit_density(int order, const GridD& g, const CSoa& p, const double* quantity, double qscale,
+void launch_deposit_density(int order, const GridD& g, const CAos& p, const double* quantity, double qscale,
                             const uint32_t* off,
                             const uint32_t* cnt, uint64_t slots, void* scratch, double* rho, cudaStream_t st) {
     switch (order) {
@@ -476,7 +476,7 @@ void launch_deposit_density(int order, const GridD& g, const CSoa& p, const doub
     }
 }
 
-void launch_deposit_density_merge(int order, const GridD& g, const CSoa& p, const double* quantity, double qscale,
+void launch_deposit_density_merge(int order, const GridD& g, const CAos& p, const double* quantity, double qscale,
                                   const uint32_t* rank, const uint32_t* off, const uint32_t* cnt, uint64_t slots,
                                   void* scratch, double* rho, cudaStream_t st) {
     switch (order) {

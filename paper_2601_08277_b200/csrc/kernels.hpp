@@ -14,7 +14,7 @@ namespace picgpu {
 // the default register-lane DFMA kernel, the warp-per-pencil "vector" DFMA
 // kernel, and the FP64 tensor-core (DMMA m8n8k4) "matrix" kernel.
 enum JKernel { kJDefault = -1, kJLane = 0, kJVector = 1, kJMatrix = 2 };
-void launch_deposit_current(int order, const GridD& g, const CSoa& p, const uint32_t* off, const uint32_t* cnt,
+void launch_deposit_current(int order, const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt,
                             double q, double* j, int num_sms, cudaStream_t st, int kernel = kJDefault);
 
 // Fused step kernel (the default session step): pic::advance + detect_moves +
@@ -25,7 +25,7 @@ void launch_deposit_current(int order, const GridD& g, const CSoa& p, const uint
 // the mover records, leaves a hole in its old bin and deposits its J with
 // L2 reductions.  Non-slab stores only.
 struct PushCtx {
-    Soa A;                   // the binned store (positions are updated in place)
+    Aos A;                   // the binned store (positions are updated in place)
     double dt, cap2;
     uint32_t* mslot;         // per mover: its slot, its old bin, its new cell
     uint32_t* mbin;
@@ -47,12 +47,12 @@ void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, c
 // cell-sorted storage (bins ascending by cell, slot order within a bin).
 // `scratch` holds (3*W + 1) doubles per slot (+1 byte per slot for TSC).
 size_t density_scratch_bytes(int order, uint64_t slots);
-void launch_deposit_density(int order, const GridD& g, const CSoa& p, const double* quantity, double qscale,
+void launch_deposit_density(int order, const GridD& g, const CAos& p, const double* quantity, double qscale,
                             const uint32_t* off,
                             const uint32_t* cnt, uint64_t slots, void* scratch, double* rho, cudaStream_t st);
 // Unsorted storage: contributions to a node are merged by storage index across
 // its source cells (k-way merge).  `rank[s]` is the storage index of slot s.
-void launch_deposit_density_merge(int order, const GridD& g, const CSoa& p, const double* quantity, double qscale,
+void launch_deposit_density_merge(int order, const GridD& g, const CAos& p, const double* quantity, double qscale,
                                   const uint32_t* rank, const uint32_t* off, const uint32_t* cnt, uint64_t slots,
                                   void* scratch, double* rho, cudaStream_t st);
 

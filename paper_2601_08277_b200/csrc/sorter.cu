@@ -58,6 +58,17 @@ Soa SoaBuf::soa() const {
                a[4].as<double>(), a[5].as<double>(), a[6].as<double>(), a[7].as<uint64_t>()};
 }
 
+void AosBuf::ensure(size_t n) {
+    a.ensure(std::max<size_t>(n, 1) * sizeof(Part));
+    cap = std::max(cap, n);
+}
+
+static void swap_aos(AosBuf& x, AosBuf& y) {
+    std::swap(x.a.p, y.a.p);
+    std::swap(x.a.bytes, y.a.bytes);
+    std::swap(x.cap, y.cap);
+}
+
 static void swap_soa(SoaBuf& x, SoaBuf& y) {
     for (int i = 0; i < 8; ++i) {
         std::swap(x.a[i].p, y.a[i].p);
@@ -73,6 +84,30 @@ static void swap_buf(DevBuf& x, DevBuf& y) {
 
 // ---------------------------------------------------------------------------
 // device helpers
+
+// record -> record
+__device__ __forceinline__ void copy_particle(const Aos src, uint64_t s, const Aos dst, uint64_t d) {
+    copy_record(src.p + s, dst.p + d);
+}
+
+// packed arrays -> record
+__device__ __forceinline__ void copy_particle(const Soa src, uint64_t s, const Aos dst, uint64_t d) {
+    store_record(dst.p + d, src.x[s], src.y[s], src.z[s], src.vx[s], src.vy[s], src.vz[s], src.w[s], src.id[s]);
+}
+
+// record -> packed arrays
+__device__ __forceinline__ void copy_particle(const Aos src, uint64_t s, const Soa dst, uint64_t d) {
+    const double2* r = reinterpret_cast<const double2*>(src.p + s);
+    const double2 a = r[0], b = r[1], c = r[2], e = r[3];
+    dst.x[d] = a.x;
+    dst.y[d] = a.y;
+    dst.z[d] = b.x;
+    dst.vx[d] = b.y;
+    dst.vy[d] = c.x;
+    dst.vz[d] = c.y;
+    dst.w[d] = e.x;
+    dst.id[d] = (uint64_t)__double_as_longlong(e.y);
+}
 
 __device__ __forceinline__ void copy_particle(const Soa src, uint64_t s, const Soa dst, uint64_t d) {
     dst.x[d] = src.x[s];
@@ -173,7 +208,7 @@ __global__ void k_u64_to_u32(const unsigned long long* in, uint32_t* out, uint64
 }
 
 __global__ void k_gather_sorted(const Soa src, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ key,
-                                const uint32_t* __restrict__ start, const uint32_t* __restrict__ off, const Soa dst,
+                                const uint32_t* __restrict__ start, const uint32_t* __restrict__ off, const Aos dst,
                                 uint64_t n) {
     const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
@@ -183,9 +218,11 @@ __global__ void k_gather_sorted(const Soa src, const uint32_t* __restrict__ perm
 
 constexpr int BPB = 64;  // bins per CTA for the slot-range kernels
 
-// Copy every bin's held particles (slot order kept) from src to dst offsets.
-__global__ void __launch_bounds__(256) k_relayout(const Soa src, const uint32_t* __restrict__ soff,
-                                                  const uint32_t* __restrict__ cnt, const Soa dst,
+// Copy every bin's held particles (slot order kept) from src to dst offsets
+// (Dst = Aos: a new layout of the store; Soa: packed staging).
+template <class Dst>
+__global__ void __launch_bounds__(256) k_relayout(const Aos src, const uint32_t* __restrict__ soff,
+                                                  const uint32_t* __restrict__ cnt, const Dst dst,
                                                   const uint32_t* __restrict__ doff, uint32_t ncells) {
     __shared__ uint32_t so[BPB + 1], sc[BPB], dof[BPB];
     const uint32_t c0 = blockIdx.x * BPB;
@@ -205,6 +242,25 @@ __global__ void __launch_bounds__(256) k_relayout(const Soa src, const uint32_t*
     }
 }
 
+// Empty records into the slack of every bin of a fresh layout: slots
+// [off[c] + fill[c], off[c+1]) (the particles are copied into the other slots
+// by the layout's copy kernel; the two write disjoint slots).
+__global__ void __launch_bounds__(256) k_fill_slack(const Aos A, const uint32_t* __restrict__ off,
+                                                    const uint32_t* __restrict__ fill, uint32_t ncells) {
+    __shared__ uint32_t so[BPB + 1], sf[BPB];
+    const uint32_t c0 = blockIdx.x * BPB;
+    const int nb = (int)umin((uint32_t)BPB, ncells - c0);
+    for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+        so[b] = off[c0 + b];
+        if (b < nb) sf[b] = fill[c0 + b];
+    }
+    __syncthreads();
+    for (uint32_t s = so[0] + threadIdx.x; s < so[nb]; s += blockDim.x) {
+        const int b = find_bin(so, nb, s);
+        if (s - so[b] >= sf[b]) store_gap_record(A.p + s);
+    }
+}
+
 // Every slack slot holds a sentinel x (all-ones bit pattern, a NaN no valid
 // particle can carry: non-finite positions are rejected), so the push can
 // stream over raw slots without knowing the bin layout.
@@ -212,8 +268,8 @@ __global__ void __launch_bounds__(256) k_relayout(const Soa src, const uint32_t*
 // Push (optional) + move detection (pic::advance + Gpma::detect_moves,
 // workload.hpp:139-155, gpma.hpp:162-177).  Each CTA streams one contiguous
 // chunk of UNR*256 slots.  Measured at C2 (tools/push_sweep.sh): one slot per
-// thread at 6 CTAs/SM with unconditional loads (0.83 ms, 4.0 TB/s) beats
-// loading only the valid slots' y..vz after x (PICGPU_PUSH_CONDLOAD=1), whose
+// thread at 6 CTAs/SM (0.83 ms, 4.0 TB/s, SoA store; with the record store a slot
+// is loaded as three 16-byte pieces) beats loading only the valid slots after x, whose
 // second round trip costs more than the slack bytes it saves.  The cell test is exact and
 // cheap: a particle moves at most one cell, so when every axis' floor is
 // unchanged (and non-negative) its cell is unchanged; only otherwise are the
@@ -230,14 +286,11 @@ __global__ void __launch_bounds__(256) k_relayout(const Soa src, const uint32_t*
 #ifndef PICGPU_PUSH_MINB
 #define PICGPU_PUSH_MINB 6
 #endif
-#ifndef PICGPU_PUSH_CONDLOAD
-#define PICGPU_PUSH_CONDLOAD 0
-#endif
 
 // RECORD = false: push and count the moved particles only (the store is
 // re-sorted from scratch afterwards; no flags, movers or departures).
 template <bool PUSH, int UNR, bool P2, bool RECORD = true>
-__global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, const Soa A, uint64_t slots,
+__global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, const Aos A, uint64_t slots,
                                               double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
                                               uint32_t mcap, const uint32_t* __restrict__ off,
                                               uint32_t* __restrict__ holes, uint32_t* __restrict__ hl,
@@ -253,18 +306,17 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
         const uint64_t s = cbeg + threadIdx.x + u * blockDim.x;
-        x[u] = s < cend ? A.x[s] : __longlong_as_double(-1LL);
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-        const uint64_t s = cbeg + threadIdx.x + u * blockDim.x;
+        x[u] = __longlong_as_double(-1LL);
         y[u] = z[u] = vx[u] = vy[u] = vz[u] = 0.0;
-        if (!PICGPU_PUSH_CONDLOAD ? s < cend : !is_gap(x[u])) {
-            y[u] = A.y[s];
-            z[u] = A.z[s];
-            vx[u] = A.vx[s];
-            vy[u] = A.vy[s];
-            vz[u] = A.vz[s];
+        if (s < cend) {  // x y | z vx | vy vz of the record
+            const double2* r = reinterpret_cast<const double2*>(A.p + s);
+            const double2 a = r[0], b = r[1], c = r[2];
+            x[u] = a.x;
+            y[u] = a.y;
+            z[u] = b.x;
+            vx[u] = b.y;
+            vy[u] = c.x;
+            vz[u] = c.y;
         }
     }
     unsigned local_moved = 0;
@@ -283,9 +335,8 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
             if (!ok) {
                 raise_error(&ctr->err, PICGPU_EDOMAIN);
             } else {
-                A.x[s] = x[u];
-                A.y[s] = y[u];
-                A.z[s] = z[u];
+                reinterpret_cast<double2*>(A.p + s)[0] = make_double2(x[u], y[u]);
+                A.p[s].z = z[u];
                 if (!finite3(x[u], y[u], z[u])) {
                     raise_error(&ctr->err, PICGPU_EINVAL);
                     ok = false;
@@ -320,8 +371,8 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
                     double* r = L + ((size_t)dir * lcap + li) * 8;
                     r[0] = x[u]; r[1] = y[u]; r[2] = z[u];
                     r[3] = vx[u]; r[4] = vy[u]; r[5] = vz[u];
-                    r[6] = A.w[s];
-                    r[7] = __longlong_as_double((long long)A.id[s]);
+                    r[6] = A.p[s].w;
+                    r[7] = __longlong_as_double((long long)A.p[s].id);
                     push_hole(A, s, before[u], off, holes, hl);
                 } else {
                     raise_error(&ctr->err, PICGPU_ELENGTH);
@@ -354,8 +405,8 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
             M.vx[idx] = vx[u];
             M.vy[idx] = vy[u];
             M.vz[idx] = vz[u];
-            M.w[idx] = A.w[s];
-            M.id[idx] = A.id[s];
+            M.w[idx] = A.p[s].w;
+            M.id[idx] = A.p[s].id;
             mcell[idx] = nc[u];
             push_hole(A, s, before[u], off, holes, hl);
         } else {
@@ -384,7 +435,7 @@ constexpr int kHoleCap = 32;
 #ifndef PICGPU_COMPACT_MINB
 #define PICGPU_COMPACT_MINB 8  // latency-bound: full occupancy beats spill-free registers (191 vs 209+ us at C2)
 #endif
-__global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_fill_holes(const Soa A, const uint32_t* __restrict__ off,
+__global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_fill_holes(const Aos A, const uint32_t* __restrict__ off,
                                                                     uint32_t* cnt, uint32_t* dep, uint32_t ncells) {
     __shared__ uint32_t holes[256 / 8][kHoleCap];
     const int lane = threadIdx.x & 31;
@@ -417,7 +468,7 @@ __global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_fill_holes(const S
         const uint32_t maxfront = __reduce_max_sync(0xffffffffu, front);
         for (uint32_t o = 0; o < maxfront; o += 8) {
             const uint32_t r = lo + o + gl;
-            const bool hole = o + gl < front && is_gap(A.x[r]);
+            const bool hole = o + gl < front && is_gap(A.p[r].x);
             const unsigned hm = (__ballot_sync(0xffffffffu, hole) >> (grp * 8)) & 0xffu;
             const uint32_t k = nh + __popc(hm & ((1u << gl) - 1u));
             if (hole && k < kHoleCap) holes[gid][k] = r;
@@ -430,14 +481,14 @@ __global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_fill_holes(const S
         uint32_t nk = 0;
         for (uint32_t o = front; __any_sync(0xffffffffu, o < maxlen); o += 8) {
             const uint32_t r = lo + o + gl;
-            const bool kept = !spill && o + gl < len && !is_gap(A.x[r]);
+            const bool kept = !spill && o + gl < len && !is_gap(A.p[r].x);
             const unsigned km = (__ballot_sync(0xffffffffu, kept) >> (grp * 8)) & 0xffu;
             if (kept) copy_particle(A, r, A, holes[gid][nk + __popc(km & ((1u << gl) - 1u))]);
             nk += __popc(km);
         }
         __syncwarp();
         if (active && !spill) {
-            for (uint32_t r = lo + front + gl; r < lo + len; r += 8) A.x[r] = __longlong_as_double(-1LL);
+            for (uint32_t r = lo + front + gl; r < lo + len; r += 8) store_gap_record(A.p + r);
             if (gl == 0) cnt[c] = front;
         }
         // a bin with more front holes than the list holds: stable slide
@@ -447,28 +498,25 @@ __global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_fill_holes(const S
             const uint32_t maxs = __reduce_max_sync(0xffffffffu, sl_len);
             for (uint32_t o = 0; o < maxs; o += 8) {
                 const uint32_t r = lo + o + gl;
-                const bool keep = o + gl < sl_len && !is_gap(A.x[r]);
+                const bool keep = o + gl < sl_len && !is_gap(A.p[r].x);
                 const unsigned km = (__ballot_sync(0xffffffffu, keep) >> (grp * 8)) & 0xffu;
                 const uint32_t dst = wpos + __popc(km & ((1u << gl) - 1u));
-                double px = 0, py = 0, pz = 0, pvx = 0, pvy = 0, pvz = 0, pw = 0;
-                uint64_t pid = 0;
+                double2 q0{}, q1{}, q2{}, q3{};
                 const bool mv = keep && dst != r;
                 if (mv) {
-                    px = A.x[r]; py = A.y[r]; pz = A.z[r];
-                    pvx = A.vx[r]; pvy = A.vy[r]; pvz = A.vz[r];
-                    pw = A.w[r]; pid = A.id[r];
+                    const double2* src = reinterpret_cast<const double2*>(A.p + r);
+                    q0 = src[0]; q1 = src[1]; q2 = src[2]; q3 = src[3];
                 }
                 __syncwarp();
                 if (mv) {
-                    A.x[dst] = px; A.y[dst] = py; A.z[dst] = pz;
-                    A.vx[dst] = pvx; A.vy[dst] = pvy; A.vz[dst] = pvz;
-                    A.w[dst] = pw; A.id[dst] = pid;
+                    double2* d2 = reinterpret_cast<double2*>(A.p + dst);
+                    d2[0] = q0; d2[1] = q1; d2[2] = q2; d2[3] = q3;
                 }
                 __syncwarp();
                 wpos += __popc(km);
             }
             if (spill) {
-                for (uint32_t r = wpos + gl; r < lo + len; r += 8) A.x[r] = __longlong_as_double(-1LL);
+                for (uint32_t r = wpos + gl; r < lo + len; r += 8) store_gap_record(A.p + r);
                 if (gl == 0) cnt[c] = wpos - lo;
             }
         }
@@ -483,7 +531,7 @@ __global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_fill_holes(const S
 // once -- no departures run concurrently); a decrement that returns <= 0 found
 // the list empty and gives its unit back, so holes[d] ends at max(h0 - a, 0).
 __global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32_t mcap,
-                         StepCounters* ctr, const Soa A, const uint32_t* __restrict__ off, uint32_t* cnt,
+                         StepCounters* ctr, const Aos A, const uint32_t* __restrict__ off, uint32_t* cnt,
                          uint32_t* __restrict__ ovf, uint32_t* __restrict__ holes, const uint32_t* __restrict__ hl) {
     const uint32_t nm = min(ctr->nmovers, mcap) + ctr->nimport;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
@@ -519,7 +567,7 @@ __global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32
 // failure, so no thread ever waits while holding a lock).  Arrivals with no
 // donor go to `left` for the re-sort.
 __global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restrict__ mcell,
-                         const uint32_t* __restrict__ ovf, uint32_t* __restrict__ left, const Soa A, uint32_t* off,
+                         const uint32_t* __restrict__ ovf, uint32_t* __restrict__ left, const Aos A, uint32_t* off,
                          uint32_t* cnt, uint32_t* holes, uint32_t* hl, unsigned int* lock, uint32_t ncells, int scan) {
     const uint32_t n = *(volatile unsigned int*)&ctr->noverflow;
     for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) {
@@ -562,7 +610,7 @@ __global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restr
                     uint64_t dst = (uint64_t)oj + min(len, above - oj);  // tail slack, or `above` (vacated by bin j+1)
                     if (hj) {  // a donor with holes gives one up (they are the spare slots arrivals missed)
                         uint32_t k = hj - 1;
-                        if (is_gap(__ldcg(A.x + oj))) {
+                        if (is_gap(__ldcg(&A.p[oj].x))) {
                             while (k > 0 && vhl[oj + k] != oj) --k;  // the first slot is a listed hole
                             vhl[oj + k] = vhl[oj + hj - 1];
                             dst = oj;                       // nothing to move
@@ -574,10 +622,10 @@ __global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restr
                         vcnt[j] = len - 1;
                     }
                     if (len > 0 && dst != oj) {
-                        A.x[dst] = __ldcg(A.x + oj); A.y[dst] = __ldcg(A.y + oj); A.z[dst] = __ldcg(A.z + oj);
-                        A.vx[dst] = __ldcg(A.vx + oj); A.vy[dst] = __ldcg(A.vy + oj);
-                        A.vz[dst] = __ldcg(A.vz + oj); A.w[dst] = __ldcg(A.w + oj);
-                        A.id[dst] = __ldcg((const unsigned long long*)A.id + oj);
+                        const double2* src = reinterpret_cast<const double2*>(A.p + oj);
+                        double2* d2 = reinterpret_cast<double2*>(A.p + dst);
+                        const double2 q0 = __ldcg(src), q1 = __ldcg(src + 1), q2 = __ldcg(src + 2), q3 = __ldcg(src + 3);
+                        d2[0] = q0; d2[1] = q1; d2[2] = q2; d2[3] = q3;
                     }
                     voff[j] = oj + 1;
                     above = oj;
@@ -595,7 +643,7 @@ __global__ void k_borrow(StepCounters* ctr, const Soa M, const uint32_t* __restr
 // Gpma::rebuild tail (gpma.hpp:137): arrivals that found no slack even after
 // borrowing go after their bin's held particles in the fresh layout.
 __global__ void k_place_left(const Soa M, const uint32_t* __restrict__ mcell, const uint32_t* __restrict__ left,
-                             uint32_t nleft, const Soa dst, const uint32_t* __restrict__ doff, uint32_t* held) {
+                             uint32_t nleft, const Aos dst, const uint32_t* __restrict__ doff, uint32_t* held) {
     const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= nleft) return;
     const uint32_t i = left[o];
@@ -807,8 +855,8 @@ __global__ void k_shift_counts(const uint32_t* __restrict__ cnt, const uint32_t*
 // Moving window relayout: new bin c <- old bin c+1 (the slots of an old
 // column-0 bin, which lands on a new last-column bin, are the dropped ones);
 // the new last-column bins are filled by the injector in place.
-__global__ void __launch_bounds__(256) k_relayout_shift(const Soa src, const uint32_t* __restrict__ soff,
-                                                        const uint32_t* __restrict__ cnt_new, const Soa dst,
+__global__ void __launch_bounds__(256) k_relayout_shift(const Aos src, const uint32_t* __restrict__ soff,
+                                                        const uint32_t* __restrict__ cnt_new, const Aos dst,
                                                         const uint32_t* __restrict__ doff, uint32_t ncells,
                                                         const GridD gnew, int ppc, double u_th, uint64_t seed,
                                                         uint64_t pid0) {
@@ -838,18 +886,14 @@ __global__ void __launch_bounds__(256) k_relayout_shift(const Soa src, const uin
         const int j = (int)(row % (uint32_t)gnew.ny), k = (int)(row / (uint32_t)gnew.ny);
         const uint64_t pid = pid0 + (uint64_t)row * ppc + r;
         const uint64_t d = (uint64_t)dof[b] + r;
-        dst.x[d] = __dadd_rn(gnew.ox, __dmul_rn(__dadd_rn((double)(nx - 1), uniform01(seed, pid, 6)), gnew.dx));
-        dst.y[d] = __dadd_rn(gnew.oy, __dmul_rn(__dadd_rn((double)j, uniform01(seed, pid, 7)), gnew.dy));
-        dst.z[d] = __dadd_rn(gnew.oz, __dmul_rn(__dadd_rn((double)k, uniform01(seed, pid, 8)), gnew.dz));
+        const double px = __dadd_rn(gnew.ox, __dmul_rn(__dadd_rn((double)(nx - 1), uniform01(seed, pid, 6)), gnew.dx));
+        const double py = __dadd_rn(gnew.oy, __dmul_rn(__dadd_rn((double)j, uniform01(seed, pid, 7)), gnew.dy));
+        const double pz = __dadd_rn(gnew.oz, __dmul_rn(__dadd_rn((double)k, uniform01(seed, pid, 8)), gnew.dz));
         const double ux = u_th * gaussian(seed, pid, 0);
         const double uy = u_th * gaussian(seed, pid, 1);
         const double uz = u_th * gaussian(seed, pid, 2);
         const double gam = sqrt(1.0 + ux * ux + uy * uy + uz * uz);
-        dst.vx[d] = ux / gam;
-        dst.vy[d] = uy / gam;
-        dst.vz[d] = uz / gam;
-        dst.w[d] = 1.0 / (double)ppc;
-        dst.id[d] = pid;
+        store_record(dst.p + d, px, py, pz, ux / gam, uy / gam, uz / gam, 1.0 / (double)ppc, pid);
     }
 }
 
@@ -1088,12 +1132,16 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev) {
         throw Status{hcounters->err, g.slab ? "slab: particle outside the slab's owned cells (or non-finite)"
                                             : "cell_of: non-finite particle position"};
     A.ensure(capacity_next);
-    PICGPU_CUDA_TRY(cudaMemsetAsync(A.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
     swap_buf(off, off2);
+    if (nc) {
+        k_fill_slack<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.aos(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                                 (uint32_t)nc);
+        note_launch();
+    }
     if (np) {
         k_gather_sorted<<<div_up((long long)np, 256), 256, 0, st>>>(b, vals2.as<uint32_t>(), skeys.as<uint32_t>(),
                                                                     start.as<uint32_t>(), off.as<uint32_t>(),
-                                                                    A.soa(), np);
+                                                                    A.aos(), np);
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
         if (perm_out_dev)
@@ -1104,14 +1152,14 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev) {
     PICGPU_CUDA_TRY(cudaMemsetAsync(holes.p, 0, nc * 4 + 4, st));  // fresh bins are packed
     // the spare store (relayout / rebuild target) gets the same capacity + headroom
     // now, outside any timed step, instead of at the first rebuild
-    B.ensure(capacity + capacity / 8);
+    A2.ensure(capacity + capacity / 8);
     hl.ensure((capacity + capacity / 8) * 4 + 4);
 }
 
 void BinStore::fill_holes() {
     const size_t nc = g.ncells;
     if (!nc) return;
-    k_fill_holes<<<div_up((long long)nc, 256), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+    k_fill_holes<<<div_up((long long)nc, 256), 256, 0, st>>>(A.aos(), off.as<uint32_t>(), cnt.as<uint32_t>(),
                                                              holes.as<uint32_t>(), (uint32_t)nc);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
@@ -1124,15 +1172,17 @@ void BinStore::relayout() {
                                                                     caps.as<uint32_t>(), onepg, min_gap);
     note_launch();
     layout_from_counts(n);
-    B.ensure(capacity_next);
-    PICGPU_CUDA_TRY(cudaMemsetAsync(B.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
+    A2.ensure(capacity_next);
     if (nc) {
-        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                               B.soa(), off2.as<uint32_t>(), (uint32_t)nc);
+        k_fill_slack<<<div_up((long long)nc, BPB), 256, 0, st>>>(A2.aos(), off2.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                                 (uint32_t)nc);
+        note_launch();
+        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.aos(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                               A2.aos(), off2.as<uint32_t>(), (uint32_t)nc);
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
     }
-    swap_soa(A, B);
+    swap_aos(A, A2);
     swap_buf(off, off2);
     capacity = capacity_next;
 }
@@ -1153,7 +1203,7 @@ void BinStore::compact_to_B() {
     note_launch();
     B.ensure(n + mcap + 1);
     if (nc) {
-        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.aos(), off.as<uint32_t>(), cnt.as<uint32_t>(),
                                                                B.soa(), off2.as<uint32_t>(), (uint32_t)nc);
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
@@ -1211,7 +1261,7 @@ void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     auto* kern = push ? (p2 ? k_push<true, UNR, true> : k_push<true, UNR, false>)
                       : (p2 ? k_push<false, UNR, true> : k_push<false, UNR, false>);
     hl.ensure(capacity * 4 + 4);
-    kern<<<blocks, 256, 0, st>>>(g, A.soa(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap,
+    kern<<<blocks, 256, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap,
                                  off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>(), ctr,
                                  lrec.as<double>(), (uint32_t)lcap);
     note_launch();
@@ -1234,14 +1284,14 @@ void BinStore::enqueue_migrate() {
             const char* e = std::getenv("PICGPU_INSERT_BLOCKS");
             return e ? std::max(1, std::atoi(e)) : 4;
         }();
-        k_insert<<<num_sms * mult, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap, ctr, A.soa(),
+        k_insert<<<num_sms * mult, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap, ctr, A.aos(),
                                               off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>(),
                                               holes.as<uint32_t>(), hl.as<uint32_t>());
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
         // borrow_insert for the full-bin arrivals; no work when there are none
         k_borrow<<<num_sms, 128, 0, st>>>(ctr, M.soa(), mcell.as<uint32_t>(), ovf.as<uint32_t>(),
-                                          ovf_left.as<uint32_t>(), A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                          ovf_left.as<uint32_t>(), A.aos(), off.as<uint32_t>(), cnt.as<uint32_t>(),
                                           holes.as<uint32_t>(), hl.as<uint32_t>(), locks.as<unsigned int>(),
                                           (uint32_t)nc, kBorrowScanBins);
         note_launch();
@@ -1269,7 +1319,7 @@ void BinStore::enqueue_fused(int order, double q, double* J, double dt, double c
         return;
     }
     hl.ensure(capacity * 4 + 4);
-    PushCtx pc{A.soa(), dt, cap2, mslot.as<uint32_t>(), mbin.as<uint32_t>(), mcell.as<uint32_t>(), (uint32_t)mcap,
+    PushCtx pc{A.aos(), dt, cap2, mslot.as<uint32_t>(), mbin.as<uint32_t>(), mcell.as<uint32_t>(), (uint32_t)mcap,
                ctr};
     launch_deposit_current_push(order, g, pc, d_off(), d_cnt(), q, J, num_sms, st);
     if (after_kernel) PICGPU_CUDA_TRY(cudaEventRecord(after_kernel, st));
@@ -1286,7 +1336,7 @@ void BinStore::push_and_resort(bool push, double dt, double cap2, StepCounters& 
         const int blocks = (int)((capacity + 256 * UNR - 1) / (256 * UNR));
         const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
         auto* kern = p2 ? k_push<true, UNR, true, false> : k_push<true, UNR, false, false>;
-        kern<<<blocks, 256, 0, st>>>(g, A.soa(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap,
+        kern<<<blocks, 256, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap,
                                      off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>(), ctr,
                                      lrec.as<double>(), (uint32_t)lcap);
         note_launch();
@@ -1326,16 +1376,18 @@ void BinStore::shift_window(const picgpu_grid& shifted, int ppc, double u_th, ui
                                                                     caps.as<uint32_t>(), onepg, min_gap);
     note_launch();
     layout_from_counts(0);  // synchronises
-    B.ensure(capacity_next + capacity_next / 8);
-    PICGPU_CUDA_TRY(cudaMemsetAsync(B.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
+    A2.ensure(capacity_next + capacity_next / 8);
     hg = shifted;
     g = make_grid(shifted);
-    k_relayout_shift<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt2.as<uint32_t>(),
-                                                                 B.soa(), off2.as<uint32_t>(), (uint32_t)nc, g, ppc,
+    k_fill_slack<<<div_up((long long)nc, BPB), 256, 0, st>>>(A2.aos(), off2.as<uint32_t>(), cnt2.as<uint32_t>(),
+                                                             (uint32_t)nc);
+    note_launch();
+    k_relayout_shift<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.aos(), off.as<uint32_t>(), cnt2.as<uint32_t>(),
+                                                                 A2.aos(), off2.as<uint32_t>(), (uint32_t)nc, g, ppc,
                                                                  u_th, seed, pid0);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
-    swap_soa(A, B);
+    swap_aos(A, A2);
     swap_buf(off, off2);
     swap_buf(cnt, cnt2);
     capacity = capacity_next;
@@ -1370,16 +1422,18 @@ bool BinStore::finish_incremental(StepCounters& out) {
                                                                         caps.as<uint32_t>(), onepg, min_gap);
         note_launch();
         layout_from_counts(n);
-        B.ensure(capacity_next);
-        PICGPU_CUDA_TRY(cudaMemsetAsync(B.a[0].p, 0xff, capacity_next * 8, st));  // slack sentinel
-        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.soa(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                               B.soa(), off2.as<uint32_t>(), (uint32_t)nc);
+        A2.ensure(capacity_next);
+        k_fill_slack<<<div_up((long long)nc, BPB), 256, 0, st>>>(A2.aos(), off2.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                                 (uint32_t)nc);
+        note_launch();
+        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.aos(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                               A2.aos(), off2.as<uint32_t>(), (uint32_t)nc);
         note_launch();
         k_place_left<<<div_up(left, 256), 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), ovf_left.as<uint32_t>(), left,
-                                                        B.soa(), off2.as<uint32_t>(), held.as<uint32_t>());
+                                                        A2.aos(), off2.as<uint32_t>(), held.as<uint32_t>());
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
-        swap_soa(A, B);
+        swap_aos(A, A2);
         swap_buf(off, off2);
         capacity = capacity_next;
         ++rebuilds;

@@ -40,6 +40,14 @@ struct SoaBuf {
     Soa soa() const;
 };
 
+// The binned store: one 64-byte record per slot (common.cuh, Part).
+struct AosBuf {
+    DevBuf a;
+    size_t cap = 0;
+    void ensure(size_t n);
+    Aos aos() const { return Aos{a.as<Part>()}; }
+};
+
 constexpr int kBorrowScanBins = 4;  // GpmaConfig::borrow_scan_bins (gpma.hpp:25)
 
 struct BinStore {
@@ -50,7 +58,8 @@ struct BinStore {
     int num_sms = 148;
     cudaStream_t st = nullptr;
 
-    SoaBuf A, B;              // A: binned store; B: spare (re-layout target, packed staging)
+    AosBuf A, A2;             // A: the binned store (records); A2: re-layout target
+    SoaBuf B;                 // packed staging: uploads, generators, downloads, full re-sorts
     DevBuf off, cnt, off2;    // off: ncells+1 (u32), cnt: ncells (u32)
     DevBuf cnt2;              // counts of a layout being built (moving window)
     DevBuf keys, keys2, skeys, vals, vals2, start, endp, caps, cub_tmp;
