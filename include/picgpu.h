@@ -252,7 +252,7 @@ PICGPU_API int picgpu_session_global_sort(picgpu_session* s);
 PICGPU_API int picgpu_session_set_kernel(picgpu_session* s, int family);
 /* Fusion policy of PUSH|SORT|CURRENT steps: the fused pass runs while the
  * previous pushed step moved less than this fraction of the particles (default
- * 0.03, or PICGPU_FUSE_MAX_MOVED); 0 never fuses, >1 always does.  EINVAL if
+ * 0.06, or PICGPU_FUSE_MAX_MOVED); 0 never fuses, >1 always does.  EINVAL if
  * negative or NaN.  No reference counterpart (a performance knob). */
 PICGPU_API int picgpu_session_set_fusion(picgpu_session* s, double max_moved_fraction);
 

@@ -577,7 +577,7 @@ class Session:
 
     def set_fusion(self, max_moved_fraction: float):
         """Fuse push + detect + J while the previous step moved less than this
-        fraction of the particles (default 0.03; 0 never, > 1 always)."""
+        fraction of the particles (default 0.06; 0 never, > 1 always)."""
         _check(lib().picgpu_session_set_fusion(self._h, max_moved_fraction))
 
     def make_workload(self, cfg: WorkloadConfig):

@@ -202,7 +202,7 @@ struct picgpu_session {
     double last_moved = 0.0;  // moved fraction of the previous pushed step (fusion policy)
     double fuse_max = [] {    // fuse while last_moved < fuse_max (picgpu_session_set_fusion)
         const char* e = std::getenv("PICGPU_FUSE_MAX_MOVED");
-        return e ? std::atof(e) : 0.03;
+        return e ? std::atof(e) : 0.06;
     }();
     // x-slab decomposition (picgpu_session_set_slab)
     bool slab = false;
@@ -768,10 +768,10 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
         // deposited by their own kernel), then the migration
         const uint32_t fuse_mask = PICGPU_STEP_PUSH | PICGPU_STEP_SORT | PICGPU_STEP_CURRENT;
         // Policy: the fused pass deposits movers' out-of-window taps with L2
-        // reductions, so it pays off at low migration (C2, ~1.2% per step:
-        // 2.04 vs 2.41 ms) and loses at high migration (C4 5.6%: 22.9 vs 20.8
-        // ms; C3 11%: 2x slower): fuse while the previous step moved less than
-        // PICGPU_FUSE_MAX_MOVED (default 3%) of the particles.
+        // reductions, so it pays off at low migration and loses at high
+        // migration (record store, step times: C2 1.2% per step, fused 1.95 vs
+        // 2.3 ms; C4 5.6%, 15.6 vs 16.1 ms; C3 11%, 177 vs 143 ms): fuse while
+        // the previous step moved less than PICGPU_FUSE_MAX_MOVED (default 6%).
         const bool fused = (flags & fuse_mask) == fuse_mask && !(flags & PICGPU_STEP_UNFUSED) &&
                            s->last_moved < s->fuse_max && fused_step_available(s->order, s->kernel);
         if (fused) {
