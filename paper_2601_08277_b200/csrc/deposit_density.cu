@@ -18,6 +18,8 @@
 //
 // Value order per contribution: wq * (sx[ix] * (sy[jy] * sz[kz])), exactly
 // scatter_deposit's (deposit.hpp:41-48).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -395,6 +397,181 @@ __global__ void __launch_bounds__(kRowX * kRowY)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Block-staged ordered gather, every node (wrapped sources included).
+//
+// A CTA owns a block of RX x RY x ZL nodes and keeps their sums in shared
+// memory.  Per axis the block's source cells form one ascending run, or two
+// when they wrap ([0, hi] then [lo, n-1]); streaming planes, then rows, then
+// the cells of a row in ascending order visits every node's own source cells
+// in ascending linear id -- the reference's storage order on a cell-sorted
+// store (bins ascending, slots in order), wrapped or not.  Each source row's
+// slot range is staged in pieces with the exact weights evaluated once per
+// slot (locate_axis + Shape<ORDER>::weights); then thread (X, ty, tz) adds,
+// for the one node (X, Y = ys+OFF+ty, Z = zs+OFF+tz) of its block that the row
+// feeds, the terms of its W cells' slots in slot order: q*(sx*(sy*sz)) with
+// round-to-nearest intrinsics, bit-identical to pic::deposit_density.  The
+// (ty, tz) pairs are the fast thread index, so the 16 lanes sharing X read
+// the same slots (broadcast).  Replaces the interior row kernel + the
+// prologue-based shell gather (C2 QSP: 11.2 ms).
+template <int ORDER>
+struct DBCfg {
+    static constexpr int W = Shape<ORDER>::W;
+    static constexpr int RX = ORDER == 1 ? 64 : 16, RY = ORDER == 1 ? 4 : 16;
+#ifdef PICGPU_RHO_ZL
+    static constexpr int ZL = PICGPU_RHO_ZL;
+#else
+    static constexpr int ZL = 8;
+#endif
+    static constexpr int NT = RX * W * W;
+    static constexpr int CAP = 512;          // slots per staged piece
+    static constexpr int WS = CAP + 2;       // weight array stride (bank skew)
+    static constexpr int MAXC = RX + W + 1;  // cells per staged row
+    static constexpr size_t SMEM = (size_t)(ZL * RY * RX + CAP + 3 * W * WS) * 8 + (size_t)2 * MAXC * 4 + CAP;
+};
+
+struct Runs {  // ascending source cells along one axis: [a0, a1] then [b0, b1] (b0 > b1: none)
+    int a0, a1, b0, b1;
+    __device__ int len_a() const { return a1 - a0 + 1; }
+    __device__ int len() const { return a1 - a0 + 1 + (b1 >= b0 ? b1 - b0 + 1 : 0); }
+    __device__ int at(int k) const { return k < len_a() ? a0 + k : b0 + (k - len_a()); }
+};
+
+template <int W, int OFF>
+__device__ __forceinline__ Runs source_runs(int B0, int Bn, int n) {
+    const int lo = B0 - OFF - (W - 1), hi = B0 + Bn - 1 - OFF;
+    if (hi - lo + 1 >= n) return Runs{0, n - 1, 1, 0};
+    const int lw = wrap_index(lo, n), hw = wrap_index(hi, n);
+    if (lw <= hw) return Runs{lw, hw, 1, 0};
+    return Runs{0, hw, lw, n - 1};
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(DBCfg<ORDER>::NT, 2)
+    density_blocks(const GridD g, const CAos p, const double* __restrict__ quantity, double qscale,
+                   const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt, double* __restrict__ rho) {
+    using C = DBCfg<ORDER>;
+    constexpr int W = C::W, OFF = Shape<ORDER>::OFF, RX = C::RX, RY = C::RY, ZL = C::ZL, NT = C::NT, CAP = C::CAP;
+    extern __shared__ __align__(16) double dsm[];
+    double* s_acc = dsm;                        // [ZL][RY][RX]
+    double* s_q = s_acc + ZL * RY * RX;         // [CAP]
+    double* s_w = s_q + CAP;                    // [3][W][WS]
+    uint32_t* s_cb = reinterpret_cast<uint32_t*>(s_w + 3 * W * C::WS);  // [MAXC] first slot of each row cell
+    uint32_t* s_ce = s_cb + C::MAXC;                                     // [MAXC] end of its extent
+    unsigned char* s_up = reinterpret_cast<unsigned char*>(s_ce + C::MAXC);  // [CAP] 0x80 valid | up bits
+
+    const int tid = threadIdx.x;
+    const int X0 = blockIdx.x * RX, Y0 = blockIdx.y * RY, Z0 = blockIdx.z * ZL;
+    const int Bx = min(RX, g.nx - X0), By = min(RY, g.ny - Y0), Bz = min(ZL, g.nz - Z0);
+    const int tyz = tid % (W * W), ty = tyz % W, tz = tyz / W, xl = tid / (W * W);
+    const int X = X0 + xl;
+    const bool xv = xl < Bx;
+    for (int i = tid; i < ZL * RY * RX; i += NT) s_acc[i] = 0.0;
+
+    const Runs rx = source_runs<W, OFF>(X0, Bx, g.nx);
+    const Runs ry = source_runs<W, OFF>(Y0, By, g.ny);
+    const Runs rz = source_runs<W, OFF>(Z0, Bz, g.nz);
+    const int ncx = rx.len(), la = rx.len_a();
+    // this thread's x source cells (ascending) as indices into the row's cell list
+    int ck[W], ct[W];
+    {
+        int xs[W];
+        sources<W, OFF>(xv ? X : 0, g.nx, xs, ct);
+#pragma unroll
+        for (int c = 0; c < W; ++c) ck[c] = xs[c] >= rx.a0 && xs[c] <= rx.a1 ? xs[c] - rx.a0 : la + xs[c] - rx.b0;
+    }
+
+    const int nzs = rz.len(), nys = ry.len();
+    for (int zi = 0; zi < nzs; ++zi) {
+        const int zs = rz.at(zi);
+        const int zl = wrap_index(zs + OFF + tz, g.nz) - Z0;
+        for (int yi = 0; yi < nys; ++yi) {
+            const int ys = ry.at(yi);
+            const int yl = wrap_index(ys + OFF + ty, g.ny) - Y0;
+            const bool mine = xv && zl >= 0 && zl < Bz && yl >= 0 && yl < By;
+            const uint32_t rowc = (uint32_t)g.nx * ((uint32_t)ys + (uint32_t)g.ny * (uint32_t)zs);
+            __syncthreads();  // the previous row is consumed
+            for (int k = tid; k < ncx; k += NT) {
+                const uint32_t c = rowc + (uint32_t)rx.at(k);
+                const uint32_t o = off[c];
+                s_cb[k] = o;
+                s_ce[k] = o + cnt[c];
+            }
+            __syncthreads();
+            // the row's stream: run A's slots [cb[0], ce[la-1]), then run B's
+            const uint32_t lena = s_ce[la - 1] - s_cb[0];
+            const uint32_t total = lena + (ncx > la ? s_ce[ncx - 1] - s_cb[la] : 0u);
+            uint32_t mb[W], me[W];
+#pragma unroll
+            for (int c = 0; c < W; ++c) {
+                const int k = ck[c];
+                const uint32_t base = k < la ? s_cb[k] - s_cb[0] : lena + (s_cb[k] - s_cb[la]);
+                mb[c] = base;
+                me[c] = base + (s_ce[k] - s_cb[k]);
+            }
+            for (uint32_t piece = 0; piece < total; piece += CAP) {
+                const uint32_t pn = min((uint32_t)CAP, total - piece);
+                if (piece) __syncthreads();  // the previous piece is consumed
+                for (uint32_t i = tid; i < pn; i += NT) {
+                    const uint32_t pos = piece + i;
+                    const uint32_t sl = pos < lena ? s_cb[0] + pos : s_cb[la] + (pos - lena);
+                    const double2 r0 = reinterpret_cast<const double2*>(p.p + sl)[0];
+                    if (is_gap(r0.x)) {  // slack or a hole
+                        s_up[i] = 0;
+                        continue;
+                    }
+                    double f[3];
+                    locate_x(g, r0.x, f[0]);
+                    locate_axis(r0.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
+                    locate_axis(p.p[sl].z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
+                    int bits = 0;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        double w[W];
+                        int up;
+                        Shape<ORDER>::weights(f[a], w, up);
+                        bits |= up << a;
+#pragma unroll
+                        for (int t = 0; t < W; ++t) s_w[(a * W + t) * C::WS + i] = w[t];
+                    }
+                    s_up[i] = (unsigned char)(0x80 | bits);
+                    s_q[i] = quantity ? quantity[sl] : qscale * p.p[sl].w;
+                }
+                __syncthreads();
+                if (!mine) continue;
+                double* ap = s_acc + ((size_t)zl * RY + yl) * RX + xl;
+                double acc = *ap;
+                const double* wy = s_w + (W + ty) * C::WS;
+                const double* wz = s_w + (2 * W + tz) * C::WS;
+#pragma unroll
+                for (int c = 0; c < W; ++c) {
+                    const uint32_t b = max(mb[c], piece), e = min(me[c], piece + pn);
+                    const double* wx = s_w + ct[c] * C::WS;
+                    for (uint32_t u = b; u < e; ++u) {
+                        const uint32_t i = u - piece;
+                        const int ub = s_up[i];
+                        if (!(ub & 0x80)) continue;
+                        if (ORDER == 2 && (!tap_valid<ORDER>(ub & 1, ct[c]) || !tap_valid<ORDER>((ub >> 1) & 1, ty) ||
+                                           !tap_valid<ORDER>((ub >> 2) & 1, tz)))
+                            continue;
+                        const double syz = __dmul_rn(wy[i], wz[i]);
+                        const double sv = __dmul_rn(wx[i], syz);
+                        acc = __dadd_rn(acc, __dmul_rn(s_q[i], sv));
+                    }
+                }
+                *ap = acc;
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < ZL * RY * RX; i += NT) {
+        const int xl2 = i % RX, yl2 = (i / RX) % RY, zl2 = i / (RX * RY);
+        if (xl2 < Bx && yl2 < By && zl2 < Bz)
+            rho[(size_t)(X0 + xl2) + (size_t)g.nx * ((size_t)(Y0 + yl2) + (size_t)g.ny * (size_t)(Z0 + zl2))] =
+                s_acc[i];
+    }
+}
+
 template <int ORDER>
 void prologue(const GridD& g, const CAos& p, const double* quantity, double qscale, uint64_t slots, void* scratch,
               cudaStream_t st, double*& S, uint8_t*& upb) {
@@ -408,8 +585,34 @@ void prologue(const GridD& g, const CAos& p, const double* quantity, double qsca
 }
 
 template <int ORDER>
+void run_rows_and_shell(const GridD& g, const CAos& p, const double* quantity, double qscale, const uint32_t* off,
+                        const uint32_t* cnt, uint64_t slots, void* scratch, double* rho, cudaStream_t st);
+
+template <int ORDER>
 void run_sorted(const GridD& g, const CAos& p, const double* quantity, double qscale, const uint32_t* off, const uint32_t* cnt,
                 uint64_t slots, void* scratch, double* rho, cudaStream_t st) {
+    static const bool rows = [] {
+        const char* e = std::getenv("PICGPU_RHO_ROWS");
+        return e && e[0] == '1';
+    }();
+    if (rows) return run_rows_and_shell<ORDER>(g, p, quantity, qscale, off, cnt, slots, scratch, rho, st);
+    using C = DBCfg<ORDER>;
+    static bool configured = false;
+    if (!configured) {
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(density_blocks<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)C::SMEM));
+        configured = true;
+    }
+    const dim3 grid(div_up(g.nx, C::RX), div_up(g.ny, C::RY), div_up(g.nz, C::ZL));
+    density_blocks<ORDER><<<grid, C::NT, C::SMEM, st>>>(g, p, quantity, qscale, off, cnt, rho);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+// The previous path (PICGPU_RHO_ROWS=1): interior row kernel + prologue-based shell gather.
+template <int ORDER>
+void run_rows_and_shell(const GridD& g, const CAos& p, const double* quantity, double qscale, const uint32_t* off,
+                        const uint32_t* cnt, uint64_t slots, void* scratch, double* rho, cudaStream_t st) {
     const Interior in = interior_of<ORDER>(g);
     Interior skip = in;
     if (!in.empty()) {
