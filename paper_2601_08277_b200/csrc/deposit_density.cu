@@ -417,14 +417,25 @@ __global__ void __launch_bounds__(kRowX * kRowY)
 template <int ORDER>
 struct DBCfg {
     static constexpr int W = Shape<ORDER>::W;
-    static constexpr int RX = ORDER == 1 ? 64 : 16, RY = ORDER == 1 ? 4 : 16;
+#ifndef PICGPU_RHO_CIC_RX
+#define PICGPU_RHO_CIC_RX 32  // C2 CIC: 1.65 ms (64: 1.76-1.80, 16: 2.40)
+#endif
+#ifndef PICGPU_RHO_CIC_CAP
+#define PICGPU_RHO_CIC_CAP 512
+#endif
+    static constexpr int RX = ORDER == 1 ? PICGPU_RHO_CIC_RX : 16, RY = ORDER == 1 ? 256 / PICGPU_RHO_CIC_RX : 16;
 #ifdef PICGPU_RHO_ZL
     static constexpr int ZL = PICGPU_RHO_ZL;
 #else
     static constexpr int ZL = 8;
 #endif
     static constexpr int NT = RX * W * W;
-    static constexpr int CAP = 512;          // slots per staged piece
+#ifdef PICGPU_RHO_MINB
+    static constexpr int MINB = PICGPU_RHO_MINB;
+#else
+    static constexpr int MINB = 3;  // C2 QSP: 4.35 ms at 3 CTAs/SM vs 5.05 at 2 (ZL 8)
+#endif
+    static constexpr int CAP = ORDER == 1 ? PICGPU_RHO_CIC_CAP : 512;  // slots per staged piece
     static constexpr int WS = CAP + 2;       // weight array stride (bank skew)
     static constexpr int MAXC = RX + W + 1;  // cells per staged row
     static constexpr size_t SMEM = (size_t)(ZL * RY * RX + CAP + 3 * W * WS) * 8 + (size_t)2 * MAXC * 4 + CAP;
@@ -447,7 +458,7 @@ __device__ __forceinline__ Runs source_runs(int B0, int Bn, int n) {
 }
 
 template <int ORDER>
-__global__ void __launch_bounds__(DBCfg<ORDER>::NT, 2)
+__global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
     density_blocks(const GridD g, const CAos p, const double* __restrict__ quantity, double qscale,
                    const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt, double* __restrict__ rho) {
     using C = DBCfg<ORDER>;
@@ -518,6 +529,13 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, 2)
                     const double2 r0 = reinterpret_cast<const double2*>(p.p + sl)[0];
                     if (is_gap(r0.x)) {  // slack or a hole
                         s_up[i] = 0;
+                        if (ORDER != 2) {
+                            // a zero term: adding +-0 never changes a node sum, which starts
+                            // at +0.0 and so can never be -0.0 (x + -x rounds to +0.0)
+                            s_q[i] = 0.0;
+#pragma unroll
+                            for (int a = 0; a < 3 * W; ++a) s_w[a * C::WS + i] = 0.0;
+                        }
                         continue;
                     }
                     double f[3];
@@ -549,11 +567,12 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, 2)
                     const double* wx = s_w + ct[c] * C::WS;
                     for (uint32_t u = b; u < e; ++u) {
                         const uint32_t i = u - piece;
-                        const int ub = s_up[i];
-                        if (!(ub & 0x80)) continue;
-                        if (ORDER == 2 && (!tap_valid<ORDER>(ub & 1, ct[c]) || !tap_valid<ORDER>((ub >> 1) & 1, ty) ||
-                                           !tap_valid<ORDER>((ub >> 2) & 1, tz)))
-                            continue;
+                        if (ORDER == 2) {  // TSC: skip gaps and the padded tap
+                            const int ub = s_up[i];
+                            if (!(ub & 0x80) || !tap_valid<ORDER>(ub & 1, ct[c]) ||
+                                !tap_valid<ORDER>((ub >> 1) & 1, ty) || !tap_valid<ORDER>((ub >> 2) & 1, tz))
+                                continue;
+                        }
                         const double syz = __dmul_rn(wy[i], wz[i]);
                         const double sv = __dmul_rn(wx[i], syz);
                         acc = __dadd_rn(acc, __dmul_rn(s_q[i], sv));
