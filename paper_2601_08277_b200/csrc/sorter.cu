@@ -58,8 +58,13 @@ Soa SoaBuf::soa() const {
                a[4].as<double>(), a[5].as<double>(), a[6].as<double>(), a[7].as<uint64_t>()};
 }
 
+// Record stores are swapped with their re-layout spare (A <-> A2), so BOTH
+// keep 12.5% headroom from their first allocation: a rebuild whose layout is a
+// few slots larger must not pay a cudaFree + cudaMalloc of the whole store
+// (C3: 45 GB, ~240 ms on the host).
 void AosBuf::ensure(size_t n) {
-    a.ensure(std::max<size_t>(n, 1) * sizeof(Part));
+    n = std::max<size_t>(n, 1);
+    if (n * sizeof(Part) > a.bytes) a.ensure((n + n / 8) * sizeof(Part));
     cap = std::max(cap, n);
 }
 
