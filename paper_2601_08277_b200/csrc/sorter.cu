@@ -299,7 +299,8 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
                                               double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
                                               uint32_t mcap, const uint32_t* __restrict__ off,
                                               uint32_t* __restrict__ holes, uint32_t* __restrict__ hl,
-                                              StepCounters* ctr, double* __restrict__ L, uint32_t lcap) {
+                                              StepCounters* ctr, double* __restrict__ L, uint32_t lcap,
+                                              uint32_t* __restrict__ mslot, uint32_t* __restrict__ mbin) {
     __shared__ unsigned s_cnt, s_base, s_mv;
     if (threadIdx.x == 0) s_cnt = s_mv = 0;
     __syncthreads();
@@ -413,7 +414,11 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
             M.w[idx] = A.p[s].w;
             M.id[idx] = A.p[s].id;
             mcell[idx] = nc[u];
-            push_hole(A, s, before[u], off, holes, hl);
+            // the slot becomes a hole now; it joins its bin's hole list in
+            // k_departures (no atomic round trip in this streaming kernel)
+            store_gap_record(A.p + s);
+            mslot[idx] = (uint32_t)s;
+            mbin[idx] = before[u];
         } else {
             // not recorded (mover buffer full): stays in its stale bin; nmovers > mcap
             // tells the host to re-sort fully
@@ -527,6 +532,18 @@ __global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_fill_holes(const A
         }
     }
     if (mydep) dep[cl] = 0;
+}
+
+// Departures of k_push's movers join their old bins' hole lists (delete_in_bin,
+// gpma.hpp:328-335); the slots already hold gap records.
+__global__ void k_departures(const StepCounters* ctr, uint32_t mcap, const uint32_t* __restrict__ mslot,
+                             const uint32_t* __restrict__ mbin, const uint32_t* __restrict__ off,
+                             uint32_t* __restrict__ holes, uint32_t* __restrict__ hl) {
+    const uint32_t nm = min(ctr->nmovers, mcap);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
+        const uint32_t b = mbin[i];
+        hl[off[b] + atomicAdd(&holes[b], 1u)] = mslot[i];
+    }
 }
 
 // Migration: an arrival first takes a hole of its bin, else the next slot of
@@ -1268,9 +1285,17 @@ void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     hl.ensure(capacity * 4 + 4);
     kern<<<blocks, 256, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap,
                                  off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>(), ctr,
-                                 lrec.as<double>(), (uint32_t)lcap);
+                                 lrec.as<double>(), (uint32_t)lcap, mslot.as<uint32_t>(), mbin.as<uint32_t>());
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
+    if (push) {
+        // the departures' hole-list entries (before any arrival looks for holes)
+        k_departures<<<num_sms * 8, 256, 0, st>>>(counters.as<StepCounters>(), (uint32_t)mcap, mslot.as<uint32_t>(),
+                                                  mbin.as<uint32_t>(), off.as<uint32_t>(), holes.as<uint32_t>(),
+                                                  hl.as<uint32_t>());
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+    }
     // no compaction: departures left holes (GPMA gaps), filled by the arrivals
 }
 
@@ -1343,7 +1368,7 @@ void BinStore::push_and_resort(bool push, double dt, double cap2, StepCounters& 
         auto* kern = p2 ? k_push<true, UNR, true, false> : k_push<true, UNR, false, false>;
         kern<<<blocks, 256, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap,
                                      off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>(), ctr,
-                                     lrec.as<double>(), (uint32_t)lcap);
+                                     lrec.as<double>(), (uint32_t)lcap, mslot.as<uint32_t>(), mbin.as<uint32_t>());
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
     }
