@@ -130,10 +130,12 @@ __host__ __device__ __forceinline__ int wrap_index(int i, int n) {
 // detail::locate_axis, grid.hpp:81-100.  Bit-identical to the reference:
 // u = (x - origin) / spacing (a multiply by the exact reciprocal when the
 // spacing is a power of two, which yields the same correctly rounded value).
+// P2: the caller knows every spacing is a power of two (no division code at all).
+template <bool P2 = false>
 __device__ __forceinline__ int locate_axis(double x, double origin, double spacing, double inv, int pow2, int n,
                                            double& frac) {
     const double t = __dsub_rn(x, origin);
-    const double u = pow2 ? __dmul_rn(t, inv) : __ddiv_rn(t, spacing);
+    const double u = (P2 || pow2) ? __dmul_rn(t, inv) : __ddiv_rn(t, spacing);
     double fu = floor(u);
     double fr = __dsub_rn(u, fu);
     if (fr >= 1.0) {
@@ -142,6 +144,10 @@ __device__ __forceinline__ int locate_axis(double x, double origin, double spaci
     }
     frac = fr;
     if (fu >= 0.0 && fu < (double)n) return (int)fu;
+    if (fabs(fu) < 2147483648.0) {  // exact integer remainder: fmod of an integral double
+        const int r = (int)((long long)fu % (long long)n);
+        return r < 0 ? r + n : r;
+    }
     double c = fmod(fu, (double)n);
     if (c < 0.0) c = __dadd_rn(c, (double)n);
     int ci = (int)c;
@@ -154,16 +160,18 @@ __device__ __forceinline__ bool finite3(double x, double y, double z) {
 }
 
 // Local x-cell of a position (global locate, then the slab shift).
+template <bool P2 = false>
 __device__ __forceinline__ int locate_x(const GridD& g, double x, double& frac) {
-    return locate_axis(x, g.gox, g.dx, g.inv_dx, g.pow2x, g.gnx, frac) - g.sx_shift;
+    return locate_axis<P2>(x, g.gox, g.dx, g.inv_dx, g.pow2x, g.gnx, frac) - g.sx_shift;
 }
 
 // cell_of, grid.hpp:106-113 (caller checks finiteness).
+template <bool P2 = false>
 __device__ __forceinline__ uint32_t cell_linear(const GridD& g, double x, double y, double z, int& i, int& j,
                                                 int& k, double& fx, double& fy, double& fz) {
-    i = locate_x(g, x, fx);
-    j = locate_axis(y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, fy);
-    k = locate_axis(z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, fz);
+    i = locate_x<P2>(g, x, fx);
+    j = locate_axis<P2>(y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, fy);
+    k = locate_axis<P2>(z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, fz);
     return (uint32_t)i + (uint32_t)g.nx * ((uint32_t)j + (uint32_t)g.ny * (uint32_t)k);
 }
 
@@ -175,10 +183,11 @@ __device__ __forceinline__ uint32_t cell_linear(const GridD& g, double x, double
 
 // Bin of a particle in a session store: its cell, or kLeaveLeft/kLeaveRight
 // when a slab does not own it (the nearer neighbour on the periodic x-axis).
+template <bool P2 = false>
 __device__ __forceinline__ uint32_t store_cell(const GridD& g, double x, double y, double z) {
     int i, j, k;
     double fx, fy, fz;
-    const uint32_t c = cell_linear(g, x, y, z, i, j, k, fx, fy, fz);
+    const uint32_t c = cell_linear<P2>(g, x, y, z, i, j, k, fx, fy, fz);
     if (!g.slab || (i >= g.sx_lo && i < g.sx_hi)) return c;
     const int ig = i + g.sx_shift, x0 = g.sx_lo + g.sx_shift, x1 = g.sx_hi + g.sx_shift;
     const int dl = ((x0 - ig) % g.gnx + g.gnx) % g.gnx;

@@ -681,7 +681,7 @@ __device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PD
         }
     }
     int ni, nj, nk;
-    const uint32_t nc = cell_linear(g, d.x, d.y, d.z, ni, nj, nk, fx, fy, fz);  // exact (pic::cell_of)
+    const uint32_t nc = cell_linear<P2>(g, d.x, d.y, d.z, ni, nj, nk, fx, fy, fz);  // exact (pic::cell_of)
     if (nc == b) return true;  // a periodic image of the bin's cell
     mv = true;
     mv_cell = nc;

@@ -302,48 +302,36 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
                                               StepCounters* ctr, double* __restrict__ L, uint32_t lcap,
                                               uint32_t* __restrict__ mslot, uint32_t* __restrict__ mbin) {
     __shared__ unsigned s_cnt, s_base, s_mv;
+    static_assert(UNR == 1, "one slot per thread (scalar state: arrays went to local memory)");
     if (threadIdx.x == 0) s_cnt = s_mv = 0;
     __syncthreads();
-    const uint64_t cbeg = (uint64_t)blockIdx.x * (UNR * blockDim.x);
-    const uint64_t cend = min(cbeg + UNR * blockDim.x, slots);
-    double x[UNR], y[UNR], z[UNR], vx[UNR], vy[UNR], vz[UNR];
-    uint32_t nc[UNR], before[UNR];
-    int lidx[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-        const uint64_t s = cbeg + threadIdx.x + u * blockDim.x;
-        x[u] = __longlong_as_double(-1LL);
-        y[u] = z[u] = vx[u] = vy[u] = vz[u] = 0.0;
-        if (s < cend) {  // x y | z vx | vy vz of the record
-            const double2* r = reinterpret_cast<const double2*>(A.p + s);
-            const double2 a = r[0], b = r[1], c = r[2];
-            x[u] = a.x;
-            y[u] = a.y;
-            z[u] = b.x;
-            vx[u] = b.y;
-            vy[u] = c.x;
-            vz[u] = c.y;
-        }
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double x = __longlong_as_double(-1LL), y = 0.0, z = 0.0, vx = 0.0, vy = 0.0, vz = 0.0;
+    if (s < slots) {  // x y | z vx | vy vz of the record
+        const double2* r = reinterpret_cast<const double2*>(A.p + s);
+        const double2 a = r[0], b = r[1], c = r[2];
+        x = a.x;
+        y = a.y;
+        z = b.x;
+        vx = b.y;
+        vy = c.x;
+        vz = c.y;
     }
-    unsigned local_moved = 0;
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-        const uint64_t s = cbeg + threadIdx.x + u * blockDim.x;
-        lidx[u] = -1;
-        nc[u] = before[u] = 0;
-        if (is_gap(x[u])) continue;
-        bool moved = false;
-        if (!finite3(x[u], y[u], z[u])) {
+    uint32_t nc = 0, before = 0;
+    int lidx = -1;
+    bool moved = false;
+    if (!is_gap(x)) {
+        if (!finite3(x, y, z)) {
             raise_error(&ctr->err, PICGPU_EINVAL);
         } else if (PUSH) {
-            const double ox = x[u], oy = y[u], oz = z[u];
-            bool ok = push_one<P2>(g, dt, cap2, x[u], y[u], z[u], vx[u], vy[u], vz[u]);
+            const double ox = x, oy = y, oz = z;
+            bool ok = push_one<P2>(g, dt, cap2, x, y, z, vx, vy, vz);
             if (!ok) {
                 raise_error(&ctr->err, PICGPU_EDOMAIN);
             } else {
-                reinterpret_cast<double2*>(A.p + s)[0] = make_double2(x[u], y[u]);
-                A.p[s].z = z[u];
-                if (!finite3(x[u], y[u], z[u])) {
+                reinterpret_cast<double2*>(A.p + s)[0] = make_double2(x, y);
+                A.p[s].z = z;
+                if (!finite3(x, y, z)) {
                     raise_error(&ctr->err, PICGPU_EINVAL);
                     ok = false;
                 }
@@ -354,76 +342,70 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
                 const double fy0 = axis_floor(oy, g.oy, g.dy, g.inv_dy, p2y);
                 const double fz0 = axis_floor(oz, g.oz, g.dz, g.inv_dz, p2z);
                 const bool same = fx0 >= 0.0 && fy0 >= 0.0 && fz0 >= 0.0 &&
-                                  fx0 == axis_floor(x[u], g.gox, g.dx, g.inv_dx, p2x) &&
-                                  fy0 == axis_floor(y[u], g.oy, g.dy, g.inv_dy, p2y) &&
-                                  fz0 == axis_floor(z[u], g.oz, g.dz, g.inv_dz, p2z);
+                                  fx0 == axis_floor(x, g.gox, g.dx, g.inv_dx, p2x) &&
+                                  fy0 == axis_floor(y, g.oy, g.dy, g.inv_dy, p2y) &&
+                                  fz0 == axis_floor(z, g.oz, g.dz, g.inv_dz, p2z);
                 if (!same) {
-                    before[u] = store_cell(g, ox, oy, oz);
-                    nc[u] = store_cell(g, x[u], y[u], z[u]);
-                    moved = nc[u] != before[u];
+                    before = store_cell<P2>(g, ox, oy, oz);
+                    nc = store_cell<P2>(g, x, y, z);
+                    moved = nc != before;
                 }
             }
         }
-        if (!RECORD) {
-            local_moved += moved ? 1u : 0u;
-            continue;
-        }
-        if (moved) {
-            ++local_moved;
-            if (nc[u] >= kLeaveRight) {  // left the slab: exchange record for the neighbour rank
-                const int dir = nc[u] == kLeaveLeft ? 0 : 1;
+        if (RECORD && moved) {
+            if (nc >= kLeaveRight) {  // left the slab: exchange record for the neighbour rank
+                const int dir = nc == kLeaveLeft ? 0 : 1;
                 const unsigned li = atomicAdd(&ctr->nleave[dir], 1u);
                 if (li < lcap) {
                     double* r = L + ((size_t)dir * lcap + li) * 8;
-                    r[0] = x[u]; r[1] = y[u]; r[2] = z[u];
-                    r[3] = vx[u]; r[4] = vy[u]; r[5] = vz[u];
+                    r[0] = x; r[1] = y; r[2] = z;
+                    r[3] = vx; r[4] = vy; r[5] = vz;
                     r[6] = A.p[s].w;
                     r[7] = __longlong_as_double((long long)A.p[s].id);
-                    push_hole(A, s, before[u], off, holes, hl);
+                    push_hole(A, s, before, off, holes, hl);
                 } else {
                     raise_error(&ctr->err, PICGPU_ELENGTH);
                 }
             } else {
-                lidx[u] = (int)atomicAdd(&s_cnt, 1u);
+                lidx = (int)atomicAdd(&s_cnt, 1u);
             }
         }
     }
     // moved count: one shared-memory add per warp, one global RED per block
     // (a per-warp RED on the single counter serialises in L2: +60 us at C2)
-    const unsigned wm = __reduce_add_sync(0xffffffffu, local_moved);
+    const unsigned wm = __reduce_add_sync(0xffffffffu, moved ? 1u : 0u);
     if ((threadIdx.x & 31) == 0 && wm) atomicAdd(&s_mv, wm);
     __syncthreads();
+    if (!RECORD) {
+        if (threadIdx.x == 0 && s_mv) atomicAdd(&ctr->moved, (unsigned long long)s_mv);
+        return;
+    }
     if (threadIdx.x == 0) {
         s_base = s_cnt ? atomicAdd(&ctr->nmovers, s_cnt) : 0u;
         if (s_mv) atomicAdd(&ctr->moved, (unsigned long long)s_mv);
     }
     __syncthreads();
-    const unsigned base = s_base;
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-        if (lidx[u] < 0) continue;
-        const uint64_t s = cbeg + threadIdx.x + u * blockDim.x;
-        const unsigned idx = base + (unsigned)lidx[u];
-        if (idx < mcap) {
-            M.x[idx] = x[u];
-            M.y[idx] = y[u];
-            M.z[idx] = z[u];
-            M.vx[idx] = vx[u];
-            M.vy[idx] = vy[u];
-            M.vz[idx] = vz[u];
-            M.w[idx] = A.p[s].w;
-            M.id[idx] = A.p[s].id;
-            mcell[idx] = nc[u];
-            // the slot becomes a hole now; it joins its bin's hole list in
-            // k_departures (no atomic round trip in this streaming kernel)
-            store_gap_record(A.p + s);
-            mslot[idx] = (uint32_t)s;
-            mbin[idx] = before[u];
-        } else {
-            // not recorded (mover buffer full): stays in its stale bin; nmovers > mcap
-            // tells the host to re-sort fully
-        }
+    if (lidx < 0) return;
+    const unsigned idx = s_base + (unsigned)lidx;
+    if (idx < mcap) {
+        const double2 wid = reinterpret_cast<const double2*>(A.p + s)[3];
+        M.x[idx] = x;
+        M.y[idx] = y;
+        M.z[idx] = z;
+        M.vx[idx] = vx;
+        M.vy[idx] = vy;
+        M.vz[idx] = vz;
+        M.w[idx] = wid.x;
+        M.id[idx] = (uint64_t)__double_as_longlong(wid.y);
+        mcell[idx] = nc;
+        // the slot becomes a hole now; it joins its bin's hole list in
+        // k_departures (no atomic round trip in this streaming kernel)
+        store_gap_record(A.p + s);
+        mslot[idx] = (uint32_t)s;
+        mbin[idx] = before;
     }
+    // else not recorded (mover buffer full): it stays in its stale bin; nmovers >
+    // mcap tells the host to re-sort fully
 }
 
 // Gaps, as in the reference's GPMA: a departing particle leaves a hole in its
