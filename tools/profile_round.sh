@@ -1,6 +1,7 @@
-# Profiles for profiles/: (1) GPU tests, (2) plain bench run, (3) launch list of
-# the same command (serialised, cold-cache per launch), (4) ncu --set full of J
-# and of the sorter kernels.  Run under gpurun from the repo root.
+# Profiles for profiles/: (1) GPU tests, (2) plain bench run, (3) reference arm,
+# (4) launch list of the same bench command (serialised, cold-cache per launch),
+# (5) ncu --set full of the fused step kernel, the movers/migration kernels and
+# the rho kernel.  Run under gpurun from the repo root.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
@@ -14,4 +15,7 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:"dep
     -o gpurun_out/full_J python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_movers|k_insert|k_borrow" -s 9 -c 3 \
     -o gpurun_out/full_sort python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"density_blocks" -s 2 -c 1 \
+    -o gpurun_out/full_rho python tools/jbench.py 3 128 16 > /dev/null 2>&1
+for o in 3 2 1; do python tools/jbench.py $o 128 16; done > gpurun_out/jbench.txt
 ls -la gpurun_out
