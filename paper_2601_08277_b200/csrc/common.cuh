@@ -145,7 +145,7 @@ __device__ __forceinline__ int locate_axis(double x, double origin, double spaci
     frac = fr;
     if (fu >= 0.0 && fu < (double)n) return (int)fu;
     if (fabs(fu) < 2147483648.0) {  // exact integer remainder: fmod of an integral double
-        const int r = (int)((long long)fu % (long long)n);
+        const int r = (int)fu % n;
         return r < 0 ? r + n : r;
     }
     double c = fmod(fu, (double)n);

@@ -1494,6 +1494,340 @@ void launch_dmma(const GridD& g, const CAos& p, const uint32_t* off, const uint3
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------------------
+// Orders 2 and 3, "mma" kernel v4: v3's decomposition (a CTA of 8x4 cell
+// pencils walks a z-chunk; every lane runs one particle's prologue -- the
+// fused push included -- and stages it; emitted planes meet in the shared
+// patch and a gather flushes each node once) with the per-cell contraction
+// J_cell += sum_p a_p (x) b_p on the FP64 tensor cores: mma.sync m8n8k4 f64,
+// M = (c, ix) 12 rows padded to 16, N = (kz, jy) 16 columns, K = 4 particles.
+// A warp serves 4 pencils (8 particles of each per chunk); its accumulators
+// are 4 pencils x 2 x 2 m8n8 tiles = 32 doubles per lane (v3: 48 per lane for
+// 8 pencils).  One DMMA replaces 8 DFMA instructions: the contraction drops
+// from ~9 to ~3 warp-instructions per particle; the FP64 pipe is the same one
+// (tools/fp64_pipes.cu), so the padding costs pipe time, not issue slots.
+// The z window slides by index rotation: at z-step R the staged b puts
+// logical plane kz in column block (kz + R) & 3, so the plane to emit is the
+// column block R -- no accumulator moves.
+struct V4Cfg {
+    static constexpr int W = 4, PX = 8, PY = 4, NP = PX * PY, NW = 8, NT = NW * 32;
+    static constexpr int PPW = 4, CH = 8;  // pencils per warp, particles per pencil per chunk
+#ifdef PICGPU_V4_MINB
+    static constexpr int MINB = PICGPU_V4_MINB;
+#else
+    static constexpr int MINB = 2;
+#endif
+    static constexpr int NF = 28, FS = 36;  // staged fields a[(c,ix)] 12 | b[(kz,jy)] 16; per-warp stride
+    static constexpr int REC = NF * FS;
+    static constexpr int PSTRIDE = NP + 2;
+    static constexpr int PATCH = W * W * 3 * PSTRIDE;
+    static constexpr size_t SMEM = (size_t)(2 * PATCH + NW * REC) * sizeof(double);
+};
+
+template <int W>
+__device__ __forceinline__ double shifted_tap(const double (&v)[W], int t, int sh) {
+    const double up = t >= 1 ? v[t >= 1 ? t - 1 : 0] : 0.0;
+    const double dn = t + 1 < W ? v[t + 1 < W ? t + 1 : 0] : 0.0;
+    return sh == 0 ? v[t] : (sh > 0 ? up : dn);
+}
+
+template <int ORDER, int PM = 0>
+__global__ void __launch_bounds__(V4Cfg::NT, V4Cfg::MINB)
+    deposit_current_kernel_v4(const GridD g, const CAos p, const uint32_t* __restrict__ off,
+                              const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
+                              double* __restrict__ jy, double* __restrict__ jz, const int zlen,
+                              const PushCtx pc) {
+    using C = V4Cfg;
+    constexpr int W = 4, OFF = Shape<ORDER>::OFF, PX = C::PX, PY = C::PY, CH = C::CH, FS = C::FS;
+    static_assert(Shape<ORDER>::W == 4, "v4 is the 4-tap kernel");
+    constexpr int FX = PX + W - 1, FY = PY + W - 1;
+    constexpr int NODES = 3 * FX * FY;
+    constexpr int NIT = (NODES + C::NT - 1) / C::NT;
+    constexpr unsigned FULL = 0xffffffffu;
+    const double qs = q * (ORDER == 3 ? 1.0 / 216.0 : 0.125);
+
+    extern __shared__ __align__(16) double smem[];
+    double* patch = smem;  // [2][jy][ix][c][PSTRIDE]
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    double* recs = smem + 2 * C::PATCH + wid * C::REC;  // [NF][FS], particle = pq * CH + lg
+    const int pq = lane >> 3, lg = lane & 7;            // prologue: pencil of the warp, chunk position
+    const int gq = lane >> 2, tq = lane & 3;            // mma fragment coordinates
+    const int grp = wid * C::PPW + pq;
+    const int px = grp % PX, py = grp / PX;
+    const int i0 = blockIdx.x * PX, j0 = blockIdx.y * PY;
+    const int k0 = blockIdx.z * zlen;
+    const int k1 = min(k0 + zlen, g.nz);
+    const int i = i0 + px, j = j0 + py;
+    const bool pv = (i < g.nx) && (j < g.ny);
+    const int pxv = min(PX, g.nx - i0), pyv = min(PY, g.ny - j0);
+    const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
+    const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
+    const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
+    const double dci = (double)(i + g.sx_shift), dcj = (double)j;
+
+    // gather plan (as v3)
+    int gn_base[NIT], gn_node[NIT];
+    unsigned gn_mask[NIT];
+    bool gn_inner[NIT];
+#pragma unroll
+    for (int t = 0; t < NIT; ++t) {
+        const int it = tid + t * C::NT;
+        gn_mask[t] = 0u;
+        gn_base[t] = 0;
+        gn_node[t] = 0;
+        gn_inner[t] = false;
+        if (it < NODES) {
+            const int c = it / (FX * FY);
+            const int r = it - c * (FX * FY);
+            const int uy = r / FX, ux = r - uy * FX;
+            if (ux < pxv + W - 1 && uy < pyv + W - 1) {
+#pragma unroll
+                for (int dy = 0; dy < W; ++dy)
+#pragma unroll
+                    for (int dx = 0; dx < W; ++dx) {
+                        const int qy = uy - dy, qx = ux - dx;
+                        if (qy >= 0 && qy < pyv && qx >= 0 && qx < pxv) gn_mask[t] |= 1u << (dy * W + dx);
+                    }
+                gn_base[t] = (c << 28) | (c * C::PSTRIDE + uy * PX + ux);
+                const int X = wrap_index(i0 + OFF + ux, g.nx);
+                const int Y = wrap_index(j0 + OFF + uy, g.ny);
+                gn_node[t] = X + g.nx * Y;
+                gn_inner[t] = !alias_xy && ux >= W - 1 && ux <= pxv - 1 && uy >= W - 1 && uy <= pyv - 1;
+            }
+        }
+    }
+
+    // D[pp][mt][nt][e]: pencil pp of the warp; row m = mt*8 + gq = (c, ix); column
+    // n = nt*8 + 2*tq + e = (kz block, jy) = (n >> 2, n & 3)
+    double D[C::PPW][2][2][2];
+#pragma unroll
+    for (int a = 0; a < C::PPW; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) D[a][b][c][0] = D[a][b][c][1] = 0.0;
+
+    {
+        bool any = false;
+        if (pv)
+            for (int kk = k0 + lg; kk < k1; kk += CH) any |= cnt[col + plane_cells * kk] != 0;
+        if (!__syncthreads_or(any)) return;
+    }
+    uint32_t c_off = 0;
+    int n_c = 0;
+    if (pv && k0 < k1) {
+        c_off = off[col + plane_cells * k0];
+        n_c = (int)cnt[col + plane_cells * k0];
+    }
+    int last_busy = k0 - W;
+    PData nxt{};
+    if (lg < n_c) load_particle<PM != 0>(p, c_off + lg, nxt);
+    const bool a_hi = gq < 4;  // rows 8..11 of m-tile 1 are c = 2; 12..15 are padding
+
+    int buf = 0;
+    const int kend = k1 + W - 1;
+    for (int k = k0; k < kend; ++k) {
+        const int R = (k - k0) & (W - 1);
+        const bool busy = k < k1 && n_c > 0;
+        if (k < k1) {
+            uint32_t n_off = 0;
+            int n_n = 0;
+            if (pv && k + 1 < k1) {
+                n_off = off[col + plane_cells * (k + 1)];
+                n_n = (int)cnt[col + plane_cells * (k + 1)];
+            }
+            const double dck = (double)k;
+            const int m = (int)__reduce_max_sync(FULL, (unsigned)n_c);
+            if (m == 0 && lg < n_n) load_particle<PM != 0>(p, n_off + lg, nxt);
+            for (int base = 0; base < m; base += CH) {
+                [[maybe_unused]] bool mv = false;
+                [[maybe_unused]] uint32_t mv_cell = 0;
+                [[maybe_unused]] unsigned mv_bal = 0, mv_b0 = 0;
+                {
+                    PData cur = nxt;
+                    bool valid = base + lg < n_c && !is_gap(cur.x);
+                    if (base + CH < m) {
+                        if (base + CH + lg < n_c) load_particle<PM != 0>(p, c_off + base + CH + lg, nxt);
+                    } else if (lg < n_n) {
+                        load_particle<PM != 0>(p, n_off + lg, nxt);
+                    }
+                    double a[3][W], sy[W], sz[W];
+                    if constexpr (PM != 0) {
+                        double fx = 0.0, fy = 0.0, fz = 0.0;
+                        int shx = 0, shy = 0, shz = 0;
+                        if (valid)
+                            valid = push_fused<PM == 2>(g, pc, cur, c_off + (uint32_t)(base + lg),
+                                                        col + plane_cells * (uint32_t)k, i, j, k, dci, dcj, dck,
+                                                        fx, fy, fz, mv, mv_cell, shx, shy, shz);
+                        mv_bal = __ballot_sync(FULL, mv);
+                        if (mv_bal && lane == __ffs(mv_bal) - 1)
+                            mv_b0 = atomicAdd(&pc.ctr->nmovers, (unsigned)__popc(mv_bal));
+                        window_from_fractions<ORDER>(cur, qs, valid, fx, fy, fz, a, sy, sz);
+                        if (mv) {  // a mover's taps, shifted into this cell's window by its cell step
+                            double t0[3][W], t1[W], t2[W];
+#pragma unroll
+                            for (int t = 0; t < W; ++t) {
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) t0[c][t] = shifted_tap<W>(a[c], t, shx);
+                                t1[t] = shifted_tap<W>(sy, t, shy);
+                                t2[t] = shifted_tap<W>(sz, t, shz);
+                            }
+#pragma unroll
+                            for (int t = 0; t < W; ++t) {
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) a[c][t] = t0[c][t];
+                                sy[t] = t1[t];
+                                sz[t] = t2[t];
+                            }
+                        }
+                    } else {
+                        particle_window_sel<ORDER>(g, cur, qs, valid, dci, dcj, dck, a, sy, sz);
+                    }
+                    double* rr = recs + pq * CH + lg;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+#pragma unroll
+                        for (int t = 0; t < W; ++t) rr[(c * W + t) * FS] = a[c][t];
+                    // b in rotated column blocks: logical plane kz at block (kz + R) & 3
+#pragma unroll
+                    for (int kz = 0; kz < W; ++kz) {
+                        double* rb = rr + (12 + ((kz + R) & (W - 1)) * W) * FS;
+#pragma unroll
+                        for (int t = 0; t < W; ++t) rb[t * FS] = sy[t] * sz[kz];
+                    }
+                }
+                __syncwarp();
+                // contraction: per pencil of the warp, groups of 4 particles
+#pragma unroll
+                for (int pp = 0; pp < C::PPW; ++pp) {
+                    const int np = __shfl_sync(FULL, n_c, pp * CH) - base;  // this pencil's particles left
+#pragma unroll
+                    for (int kg = 0; kg < CH / 4; ++kg) {
+                        if (kg * 4 >= np) break;
+                        const double* r = recs + pp * CH + kg * 4 + tq;
+                        const double a0 = r[gq * FS];
+                        const double a1 = a_hi ? r[(8 + gq) * FS] : 0.0;
+                        const double b0 = r[(12 + gq) * FS];
+                        const double b1 = r[(20 + gq) * FS];
+                        dmma_8x8x4(D[pp][0][0], a0, b0);
+                        dmma_8x8x4(D[pp][0][1], a0, b1);
+                        dmma_8x8x4(D[pp][1][0], a1, b0);
+                        dmma_8x8x4(D[pp][1][1], a1, b1);
+                    }
+                }
+                if constexpr (PM != 0) {
+                    if (mv_bal) {
+                        const unsigned b0 = __shfl_sync(FULL, mv_b0, __ffs(mv_bal) - 1);
+                        if (mv) {
+                            const unsigned idx = b0 + (unsigned)__popc(mv_bal & ((1u << lane) - 1u));
+                            if (idx < pc.mcap) {
+                                pc.mslot[idx] = c_off + (uint32_t)(base + lg);
+                                pc.mbin[idx] = col + plane_cells * (uint32_t)k;
+                                pc.mcell[idx] = mv_cell;
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            c_off = n_off;
+            n_c = n_n;
+        }
+        // logical plane 0 sits in column block R (tile R >> 1, lanes with tq >> 1 == R & 1):
+        // emit it into the patch and zero it (it becomes the window's top plane)
+        {
+            double* pb = patch + buf * C::PATCH + wid * C::PPW;
+            const bool mine = (tq >> 1) == (R & 1);
+            auto emit = [&](auto NTc) {
+                constexpr int NT_ = decltype(NTc)::value;
+#pragma unroll
+                for (int pp = 0; pp < C::PPW; ++pp)
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int mrow = mt * 8 + gq;
+                            const int jyv = (2 * tq + e) & 3;
+                            if (mine && mrow < 12)
+                                pb[((jyv * W + (mrow & 3)) * 3 + (mrow >> 2)) * C::PSTRIDE + pp] = D[pp][mt][NT_][e];
+                            if (mine) D[pp][mt][NT_][e] = 0.0;
+                        }
+            };
+            if (R < 2)
+                emit(std::integral_constant<int, 0>{});
+            else
+                emit(std::integral_constant<int, 1>{});
+        }
+        if (__syncthreads_or(busy)) last_busy = k;
+        if (last_busy >= k - (W - 1)) {
+            const double* pb = patch + buf * C::PATCH;
+            const int Z = wrap_index(k + OFF, g.nz);
+            const bool zc = (k >= k0 + W - 1) && (k < k1);
+            const size_t zrow = (size_t)plane_cells * (size_t)Z;
+#pragma unroll
+            for (int t = 0; t < NIT; ++t) {
+                const unsigned msk = gn_mask[t];
+                if (!msk) continue;
+                const int c = gn_base[t] >> 28;
+                const double* src = pb + (gn_base[t] & 0x0fffffff);
+                double v[W * W];
+#pragma unroll
+                for (int dy = 0; dy < W; ++dy)
+#pragma unroll
+                    for (int dx = 0; dx < W; ++dx)
+                        v[dy * W + dx] = (msk & (1u << (dy * W + dx)))
+                                             ? src[(dy * W + dx) * 3 * C::PSTRIDE - dy * PX - dx]
+                                             : 0.0;
+#pragma unroll
+                for (int h = W * W / 2; h >= 1; h /= 2)
+#pragma unroll
+                    for (int e = 0; e < h; ++e) v[e] += v[e + h];
+                const double s = v[0];
+                double* f = c == 0 ? jx : (c == 1 ? jy : jz);
+                const size_t node = (size_t)gn_node[t] + zrow;
+                if (zc && gn_inner[t])
+                    f[node] = s;
+                else if (s != 0.0)
+                    atomicAdd(f + node, s);
+            }
+        }
+        buf ^= 1;
+    }
+}
+
+template <int ORDER, int PM>
+void launch_v4(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+               int num_sms, cudaStream_t st, const PushCtx& pc) {
+    using C = V4Cfg;
+    static bool configured = false;
+    if (!configured) {
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel_v4<ORDER, PM>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+        configured = true;
+    }
+    const int tx = div_up(g.nx, C::PX), ty = div_up(g.ny, C::PY);
+    const long long tiles = (long long)tx * ty;
+    const long long target = (long long)num_sms * C::MINB * 4;
+    int zch = (int)std::max<long long>(1, (target + tiles - 1) / tiles);
+    zch = std::min(zch, std::max(1, g.nz / (4 * C::W)));
+    const int zlen = div_up(g.nz, zch);
+    zch = div_up(g.nz, zlen);
+    dim3 grid(tx, ty, zch);
+    deposit_current_kernel_v4<ORDER, PM><<<grid, C::NT, C::SMEM, st>>>(g, p, off, cnt, q, j, j + g.ncells,
+                                                                      j + 2 * (size_t)g.ncells, zlen, pc);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+static bool use_v4() {
+    static const bool v = [] {
+        const char* e = std::getenv("PICGPU_J_V4");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 template <int ORDER>
 void launch_warp(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
                  int num_sms, cudaStream_t st) {
@@ -1569,6 +1903,9 @@ void launch_order(const GridD& g, const CAos& p, const uint32_t* off, const uint
 #else
     using C3 = std::conditional_t<ORDER == 1, JCfgCic3, JCfg<ORDER>>;
 #endif
+    if constexpr (ORDER != 1) {
+        if (use_v4()) return launch_v4<ORDER, 0>(g, p, off, cnt, q, j, num_sms, st, PushCtx{});
+    }
     if (v1)
         launch_kernel<ORDER, JCfg<ORDER>, false>(g, p, off, cnt, q, j, num_sms, st);
     else
@@ -1619,6 +1956,13 @@ void launch_push_order(const GridD& g, const PushCtx& pc, const uint32_t* off, c
     using C3 = std::conditional_t<ORDER == 1, JCfgCic3, JCfg<ORDER>>;
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
     const CAos p(pc.A);
+    if constexpr (ORDER != 1) {
+        if (use_v4()) {
+            if (p2)
+                return launch_v4<ORDER, 2>(g, p, off, cnt, q, j, num_sms, st, pc);
+            return launch_v4<ORDER, 1>(g, p, off, cnt, q, j, num_sms, st, pc);
+        }
+    }
     if (p2)
         launch_kernel<ORDER, C3, true, 2>(g, p, off, cnt, q, j, num_sms, st, pc);
     else

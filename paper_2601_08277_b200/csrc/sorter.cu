@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(256) k_fill_slack(const Aos A, const uint32_t*
 #define PICGPU_PUSH_UNR 1
 #endif
 #ifndef PICGPU_PUSH_MINB
-#define PICGPU_PUSH_MINB 6
+#define PICGPU_PUSH_MINB 5  // record store: 5 CTAs/SM (51 registers, no spill) beats 6 (40, spills): C3 push+sort 54 -> 48 ms
 #endif
 
 // RECORD = false: push and count the moved particles only (the store is
