@@ -115,6 +115,14 @@ struct JLayout {
     static constexpr int SS = NP + 4;
     static constexpr int FSS = C::CH * SS;
     static constexpr int STAGE = C::G > 1 ? NF * FSS : 0;
+    // v3 stages fields in PAIRS (16 bytes: one LDS.128 reads two taps): pair
+    // f/2 of chunk position l of pencil grp at 16-byte unit (f/2)*PFS + l*PSS +
+    // grp.  PSS = NP + 2 (2 mod 8 units) keeps a quarter-warp's writes (2
+    // pencils x 4 positions) in distinct banks; a warp's reads (8 pencils, one
+    // position) are 128 contiguous bytes.
+    static constexpr int PSS = NP + 2;
+    static constexpr int PFS = C::CH * PSS;
+    static_assert(NF % 2 == 0 && (NF / 2) * PFS * 2 <= NF * FSS, "paired staging fits the v1 staging area");
     // One emitted plane of every pencil, offset-major: [jy][ix][c][PY][PX] with
     // a 2-double skew per (jy,ix,c) row so the 4 jy-lanes of a pencil write
     // to distinct banks and the gather reads consecutive pencils contiguously.
@@ -558,34 +566,46 @@ __device__ __forceinline__ void particle_window_sel(const GridD& g, const PData&
     }
 }
 
-// Stage one particle's window weights, field-major (see JLayout).
-template <int W, int FSS>
-__device__ __forceinline__ void stage_record(double* rec, const double (&a)[3][W], const double (&sy)[W],
-                                             const double (&sz)[W]) {
+// Paired staging (JLayout PSS/PFS): address of field f of chunk position l of pencil grp.
+template <class L>
+__device__ __forceinline__ double* pfield(double* stage, int f, int l, int grp) {
+    return stage + ((((f >> 1) * L::PFS + l * L::PSS + grp) << 1) | (f & 1));
+}
+template <class L>
+__device__ __forceinline__ const double* pfield(const double* stage, int f, int l, int grp) {
+    return stage + ((((f >> 1) * L::PFS + l * L::PSS + grp) << 1) | (f & 1));
+}
+
+// Stage one particle's window: a[c][t] and sy[t] as tap pairs; sz[t] at its
+// physical z slot (t + R) & (W-1) (the accumulators' rotated window).
+template <class L, int W>
+__device__ __forceinline__ void stage_record(double* stage, int l, int grp, int R, const double (&a)[3][W],
+                                             const double (&sy)[W], const double (&sz)[W]) {
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int t = 0; t < W; ++t) rec[(c * W + t) * FSS] = a[c][t];
+        for (int t = 0; t < W; t += 2)
+            *reinterpret_cast<double2*>(pfield<L>(stage, c * W + t, l, grp)) = make_double2(a[c][t], a[c][t + 1]);
 #pragma unroll
-    for (int t = 0; t < W; ++t) {
-        rec[(3 * W + t) * FSS] = sy[t];
-        rec[(4 * W + t) * FSS] = sz[t];
-    }
+    for (int t = 0; t < W; t += 2)
+        *reinterpret_cast<double2*>(pfield<L>(stage, 3 * W + t, l, grp)) = make_double2(sy[t], sy[t + 1]);
+#pragma unroll
+    for (int t = 0; t < W; ++t) *pfield<L>(stage, 4 * W + ((t + R) & (W - 1)), l, grp) = sz[t];
 }
 
-// Shift one staged W-tap field array (fields f0 .. f0+W-1) by sh (-1, 0, +1)
-// window positions, zero-filling the vacated one.
-template <int W, int FSS>
-__device__ __forceinline__ void restage_shifted(double* rec, int f0, int sh) {
+// Shift one staged W-tap array (fields f0 .. f0+W-1, logical tap t stored at
+// f0 + ((t + rot) & (W-1))) by sh (-1, 0, +1) taps, zero-filling the vacated one.
+template <class L, int W>
+__device__ __forceinline__ void restage_shifted(double* stage, int l, int grp, int f0, int sh, int rot) {
     if (sh == 0) return;
     double v[W];
 #pragma unroll
     for (int t = 0; t < W; ++t) {
         const int u = t - sh;
-        v[t] = (u >= 0 && u < W) ? rec[(f0 + u) * FSS] : 0.0;
+        v[t] = (u >= 0 && u < W) ? *pfield<L>(stage, f0 + ((u + rot) & (W - 1)), l, grp) : 0.0;
     }
 #pragma unroll
-    for (int t = 0; t < W; ++t) rec[(f0 + t) * FSS] = v[t];
+    for (int t = 0; t < W; ++t) *pfield<L>(stage, f0 + ((t + rot) & (W - 1)), l, grp) = v[t];
 }
 
 // Cell step of a mover on one periodic axis, folded into {-1, 0, +1}.
@@ -806,10 +826,6 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                 n_n = (int)cnt[col + plane_cells * (k + 1)];
             }
             const double dck = (double)k;
-            // sz of logical plane (s - R) & 3 for physical slot s
-            const double* szb[W];
-#pragma unroll
-            for (int sl = 0; sl < W; ++sl) szb[sl] = stage + (4 * W + ((sl - R) & (W - 1))) * L::FSS + grp;
             const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
             if (m == 0 && lg < n_n) load_particle<PM != 0>(p, n_off + lg, nxt);  // empty cells: still prefetch
             for (int base = 0; base < m; base += CH) {
@@ -825,7 +841,6 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                         load_particle<PM != 0>(p, n_off + lg, nxt);
                     }
                     double a[3][W], sy[W], sz[W];
-                    double* rec = stage + lg * L::SS + grp;
                     if constexpr (PM != 0) {
                         // pic::advance (workload.hpp:139-155) + Gpma::detect_moves (gpma.hpp:162-177):
                         // fractions of the pushed particle, relative to its new cell for a mover
@@ -841,20 +856,20 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                         if (mv_bal && (tid & 31) == __ffs(mv_bal) - 1)
                             mv_b0 = atomicAdd(&pc.ctr->nmovers, (unsigned)__popc(mv_bal));
                         window_from_fractions<ORDER>(cur, qs, valid, fx, fy, fz, a, sy, sz);
-                        stage_record<W, L::FSS>(rec, a, sy, sz);
+                        stage_record<L, W>(stage, lg, grp, R, a, sy, sz);
                         if (mv) {
                             // a mover's taps, shifted into this cell's window by its cell
                             // step (read back from its staged record: runtime offsets stay
                             // in shared memory); taps that leave the window are k_movers'
-                            restage_shifted<W, L::FSS>(rec, 0, shx);
-                            restage_shifted<W, L::FSS>(rec, W, shx);
-                            restage_shifted<W, L::FSS>(rec, 2 * W, shx);
-                            restage_shifted<W, L::FSS>(rec, 3 * W, shy);
-                            restage_shifted<W, L::FSS>(rec, 4 * W, shz);
+                            restage_shifted<L, W>(stage, lg, grp, 0, shx, 0);
+                            restage_shifted<L, W>(stage, lg, grp, W, shx, 0);
+                            restage_shifted<L, W>(stage, lg, grp, 2 * W, shx, 0);
+                            restage_shifted<L, W>(stage, lg, grp, 3 * W, shy, 0);
+                            restage_shifted<L, W>(stage, lg, grp, 4 * W, shz, R);
                         }
                     } else {
                         particle_window_sel<ORDER>(g, cur, qs, valid, dci, dcj, dck, a, sy, sz);
-                        stage_record<W, L::FSS>(rec, a, sy, sz);
+                        stage_record<L, W>(stage, lg, grp, R, a, sy, sz);
                     }
                 }
                 __syncwarp();
@@ -862,18 +877,25 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 #pragma unroll
                 for (int jj0 = 0; jj0 < CH; ++jj0) {
                     if (jj0 >= nn) break;
-                    const double* r = stage + jj0 * L::SS + grp;
-                    const double yv = r[(3 * W + ly) * L::FSS];
+                    const double yv = *pfield<L>(stage, 3 * W + ly, jj0, grp);
                     double b[W];
 #pragma unroll
-                    for (int sl = 0; sl < W; ++sl) b[sl] = yv * szb[sl][jj0 * L::SS];
+                    for (int sl = 0; sl < W; sl += 2) {  // sz of physical slots sl, sl+1
+                        const double2 zz = *reinterpret_cast<const double2*>(pfield<L>(stage, 4 * W + sl, jj0, grp));
+                        b[sl] = yv * zz.x;
+                        b[sl + 1] = yv * zz.y;
+                    }
 #pragma unroll
                     for (int c = 0; c < 3; ++c)
 #pragma unroll
-                        for (int ix = 0; ix < IX; ++ix) {
-                            const double av = r[(c * W + xh * IX + ix) * L::FSS];
+                        for (int ix = 0; ix < IX; ix += 2) {
+                            const double2 av =
+                                *reinterpret_cast<const double2*>(pfield<L>(stage, c * W + xh * IX + ix, jj0, grp));
 #pragma unroll
-                            for (int sl = 0; sl < W; ++sl) acc[sl][ix][c] = fma(av, b[sl], acc[sl][ix][c]);
+                            for (int sl = 0; sl < W; ++sl) {
+                                acc[sl][ix][c] = fma(av.x, b[sl], acc[sl][ix][c]);
+                                acc[sl][ix + 1][c] = fma(av.y, b[sl], acc[sl][ix + 1][c]);
+                            }
                         }
                 }
                 if constexpr (PM != 0) {
