@@ -123,12 +123,23 @@ struct JLayout {
     static constexpr int PSS = NP + 2;
     static constexpr int PFS = C::CH * PSS;
     static_assert(NF % 2 == 0 && (NF / 2) * PFS * 2 <= NF * FSS, "paired staging fits the v1 staging area");
+    // v3: PPB emitted planes per CTA barrier (double-buffered), paired staging.
+    // C2 QSP: PPB 1 / 2 / 4 -> J 1.177 / 1.171 / 2.03 ms (4: 2 CTAs/SM), fused
+    // step kernel 1.681 / 1.698 / 3.29 ms: one plane per barrier
+#ifdef PICGPU_V3_PPB
+    static constexpr int PPB = PICGPU_V3_PPB;
+#else
+    static constexpr int PPB = 1;
+#endif
+    static constexpr int STAGE3 = C::G > 1 ? (NF / 2) * PFS * 2 : 0;
+
     // One emitted plane of every pencil, offset-major: [jy][ix][c][PY][PX] with
     // a 2-double skew per (jy,ix,c) row so the 4 jy-lanes of a pencil write
     // to distinct banks and the gather reads consecutive pencils contiguously.
     static constexpr int PSTRIDE = NP + 2;
     static constexpr int PATCH = W * W * 3 * PSTRIDE;
     static constexpr size_t SMEM = (size_t)(2 * PATCH + STAGE) * sizeof(double);
+    static constexpr size_t SMEM3 = (size_t)(2 * PPB * PATCH + STAGE3) * sizeof(double);
 };
 
 struct PData {  // one particle as read from the bins
@@ -735,8 +746,9 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
     const double qs = q * (ORDER == 3 ? 1.0 / 216.0 : ORDER == 2 ? 0.125 : 1.0);
 
     extern __shared__ __align__(16) double smem[];
-    double* patch = smem;                 // [2][W(jy)][W(ix)][3][PSTRIDE]
-    double* stage = smem + 2 * L::PATCH;  // [NF][CH][SS]
+    constexpr int PPB = L::PPB;
+    double* patch = smem;                       // [2][PPB][W(jy)][W(ix)][3][PSTRIDE]
+    double* stage = smem + 2 * PPB * L::PATCH;  // paired fields (JLayout PSS/PFS)
 
     const int tid = threadIdx.x;
     const int grp = tid / G, lg = tid % G;
@@ -813,10 +825,12 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
     PData nxt{};
     if (lg < n_c) load_particle<PM != 0>(p, c_off + lg, nxt);
 
-    int buf = 0;
+    int phase = 0;
+    bool busy_acc = false;  // any deposit in this barrier's batch of planes
     const int kend = k1 + W - 1;
     for (int k = k0; k < kend; ++k) {
         const int R = (k - k0) & (W - 1);
+        const int sub = (k - k0) % PPB;
         const bool busy = k < k1 && n_c > 0;
         if (k < k1) {
             uint32_t n_off = 0;
@@ -919,7 +933,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
         // logical plane 0 (physical slot R) is final: emit it and zero the slot,
         // which becomes the window's top plane at the next step
         {
-            double* pp = patch + buf * L::PATCH + grp;
+            double* pp = patch + (phase * PPB + sub) * L::PATCH + grp;
             auto emit = [&](auto Sc) {
                 constexpr int S = decltype(Sc)::value;
 #pragma unroll
@@ -944,13 +958,19 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                 }
             }
         }
-        // the plane emitted now gathers cells k-W+1..k: if none of them held a
-        // particle anywhere in the CTA, every node sum is zero -- skip it
-        if (__syncthreads_or(busy)) last_busy = k;
-        if (last_busy >= k - (W - 1)) {
-            const double* pb = patch + buf * L::PATCH;
-            const int Z = wrap_index(k + OFF, g.nz);
-            const bool zc = (k >= k0 + W - 1) && (k < k1);
+        // PPB planes per CTA barrier: the batch's planes are gathered together
+        busy_acc |= busy;
+        if (sub != PPB - 1 && k + 1 < kend) continue;
+        // a plane emitted at step kk gathers cells kk-W+1..kk: if none of them
+        // held a particle anywhere in the CTA, every node sum is zero -- skip it
+        if (__syncthreads_or(busy_acc)) last_busy = k;
+        busy_acc = false;
+        for (int sl = 0; sl <= sub; ++sl) {
+            const int kk = k - sub + sl;
+            if (last_busy < kk - (W - 1)) continue;
+            const double* pb = patch + (phase * PPB + sl) * L::PATCH;
+            const int Z = wrap_index(kk + OFF, g.nz);
+            const bool zc = (kk >= k0 + W - 1) && (kk < k1);
             const size_t zrow = (size_t)plane_cells * (size_t)Z;
 #pragma unroll
             for (int t = 0; t < NIT; ++t) {
@@ -979,7 +999,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                     atomicAdd(f + node, s);
             }
         }
-        buf ^= 1;
+        phase ^= 1;
     }
 }
 
@@ -1881,7 +1901,7 @@ void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uin
     static_assert(V3 || PM == 0, "the fused step runs on the v3 kernel");
     using L = JLayout<ORDER, C>;
     constexpr int W = L::W;
-    constexpr size_t smem = V3 ? L::SMEM : JLayout<ORDER>::SMEM;
+    constexpr size_t smem = V3 ? L::SMEM3 : JLayout<ORDER>::SMEM;
     static bool configured = false;
     if (!configured) {
         if constexpr (V3)
