@@ -789,7 +789,7 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
             if (c.err == PICGPU_EDOMAIN)
                 throw Status{c.err, "advance: particle displacement exceeds the single-cell cap"};
             if (c.err) throw Status{c.err, "cell_of: non-finite particle position"};
-            stats.moved = c.nmovers;
+            stats.moved = c.moved;
             stats.fused = 1;
             stats.inserts = std::min<uint64_t>(c.nmovers, mcap0);
             stats.overflowed = c.noverflow;
@@ -804,7 +804,7 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
                     accumulate_phase(s, 2, 1, 7, g_launches.load() - l0 - lj);
                 }
             }
-            if (rebuilt && c.nmovers > mcap0) {
+            if (rebuilt && (c.nmovers > mcap0 || c.mover_drop > 0)) {
                 // movers beyond the buffer were pushed but neither recorded nor
                 // deposited: the store was re-sorted fully, deposit J again
                 flags &= ~PICGPU_STEP_SORT;  // (handled) -- J below is redone from scratch

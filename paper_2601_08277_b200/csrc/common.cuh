@@ -205,6 +205,10 @@ struct StepCounters {
     unsigned int nleft;       // ... with no donor (-> rebuild)
     unsigned int nimport;     // arrivals from neighbour slabs appended to the movers
     unsigned int nleave[2];   // particles that left the slab to the left / right
+    // fused step: movers beyond their CTA's segment go to the shared overflow
+    // segment (ovf_movers, global atomic); beyond that they are dropped (-> full re-sort)
+    unsigned int ovf_movers;
+    unsigned int mover_drop;
 };
 
 // floor((x - o) / h) exactly as locate_axis computes it (before its range

@@ -764,6 +764,10 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
     const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
     const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
     const double dci = (double)(i + g.sx_shift), dcj = (double)j;
+    // this CTA's segment of the mover arrays (reserved with shared-memory atomics)
+    [[maybe_unused]] const uint32_t seg = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    __shared__ unsigned s_movers;
+    if (PM != 0 && threadIdx.x == 0) s_movers = 0;
 
     // gather plan of this thread's nodes (constant over z)
     int gn_base[NIT], gn_node[NIT];
@@ -813,7 +817,10 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
         bool any = false;
         if (pv)
             for (int kk = k0 + lg; kk < k1; kk += G) any |= cnt[col + plane_cells * kk] != 0;
-        if (!__syncthreads_or(any)) return;
+        if (!__syncthreads_or(any)) {
+            if (PM != 0 && threadIdx.x == 0) pc.seg_cnt[seg] = 0;
+            return;
+        }
     }
     uint32_t c_off = 0;
     int n_c = 0;
@@ -868,7 +875,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                         // needed after the contraction below
                         mv_bal = __ballot_sync(0xffffffffu, mv);
                         if (mv_bal && (tid & 31) == __ffs(mv_bal) - 1)
-                            mv_b0 = atomicAdd(&pc.ctr->nmovers, (unsigned)__popc(mv_bal));
+                            mv_b0 = atomicAdd(&s_movers, (unsigned)__popc(mv_bal));
                         window_from_fractions<ORDER>(cur, qs, valid, fx, fy, fz, a, sy, sz);
                         stage_record<L, W>(stage, lg, grp, R, a, sy, sz);
                         if (mv) {
@@ -917,10 +924,15 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                         const unsigned b0 = __shfl_sync(0xffffffffu, mv_b0, __ffs(mv_bal) - 1);
                         if (mv) {
                             const unsigned idx = b0 + (unsigned)__popc(mv_bal & ((1u << (tid & 31)) - 1u));
-                            if (idx < pc.mcap) {
-                                pc.mslot[idx] = c_off + (uint32_t)(base + lg);
-                                pc.mbin[idx] = col + plane_cells * (uint32_t)k;
-                                pc.mcell[idx] = mv_cell;
+                            size_t e = (size_t)seg * pc.segcap + idx;
+                            if (idx >= pc.segcap) {  // segment full: the shared overflow segment
+                                const unsigned o = atomicAdd(&pc.ctr->ovf_movers, 1u);
+                                e = o < pc.ovcap ? (size_t)pc.nseg * pc.segcap + o : ~(size_t)0;
+                            }
+                            if (e != ~(size_t)0) {
+                                pc.mslot[e] = c_off + (uint32_t)(base + lg);
+                                pc.mbin[e] = col + plane_cells * (uint32_t)k;
+                                pc.mcellseg[e] = mv_cell;
                             }
                         }
                     }
@@ -1000,6 +1012,10 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
             }
         }
         phase ^= 1;
+    }
+    if constexpr (PM != 0) {  // this CTA's mover count (every reservation precedes the last barrier)
+        __syncthreads();
+        if (threadIdx.x == 0) pc.seg_cnt[seg] = s_movers;
     }
 }
 
@@ -1607,6 +1623,10 @@ __global__ void __launch_bounds__(V4Cfg::NT, V4Cfg::MINB)
     const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
     const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
     const double dci = (double)(i + g.sx_shift), dcj = (double)j;
+    // this CTA's segment of the mover arrays (reserved with shared-memory atomics)
+    [[maybe_unused]] const uint32_t seg = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    __shared__ unsigned s_movers;
+    if (PM != 0 && threadIdx.x == 0) s_movers = 0;
 
     // gather plan (as v3)
     int gn_base[NIT], gn_node[NIT];
@@ -1654,7 +1674,10 @@ __global__ void __launch_bounds__(V4Cfg::NT, V4Cfg::MINB)
         bool any = false;
         if (pv)
             for (int kk = k0 + lg; kk < k1; kk += CH) any |= cnt[col + plane_cells * kk] != 0;
-        if (!__syncthreads_or(any)) return;
+        if (!__syncthreads_or(any)) {
+            if (PM != 0 && threadIdx.x == 0) pc.seg_cnt[seg] = 0;
+            return;
+        }
     }
     uint32_t c_off = 0;
     int n_c = 0;
@@ -1704,7 +1727,7 @@ __global__ void __launch_bounds__(V4Cfg::NT, V4Cfg::MINB)
                                                         fx, fy, fz, mv, mv_cell, shx, shy, shz);
                         mv_bal = __ballot_sync(FULL, mv);
                         if (mv_bal && lane == __ffs(mv_bal) - 1)
-                            mv_b0 = atomicAdd(&pc.ctr->nmovers, (unsigned)__popc(mv_bal));
+                            mv_b0 = atomicAdd(&s_movers, (unsigned)__popc(mv_bal));
                         window_from_fractions<ORDER>(cur, qs, valid, fx, fy, fz, a, sy, sz);
                         if (mv) {  // a mover's taps, shifted into this cell's window by its cell step
                             double t0[3][W], t1[W], t2[W];
@@ -1763,10 +1786,15 @@ __global__ void __launch_bounds__(V4Cfg::NT, V4Cfg::MINB)
                         const unsigned b0 = __shfl_sync(FULL, mv_b0, __ffs(mv_bal) - 1);
                         if (mv) {
                             const unsigned idx = b0 + (unsigned)__popc(mv_bal & ((1u << lane) - 1u));
-                            if (idx < pc.mcap) {
-                                pc.mslot[idx] = c_off + (uint32_t)(base + lg);
-                                pc.mbin[idx] = col + plane_cells * (uint32_t)k;
-                                pc.mcell[idx] = mv_cell;
+                            size_t e = (size_t)seg * pc.segcap + idx;
+                            if (idx >= pc.segcap) {  // segment full: the shared overflow segment
+                                const unsigned o = atomicAdd(&pc.ctr->ovf_movers, 1u);
+                                e = o < pc.ovcap ? (size_t)pc.nseg * pc.segcap + o : ~(size_t)0;
+                            }
+                            if (e != ~(size_t)0) {
+                                pc.mslot[e] = c_off + (uint32_t)(base + lg);
+                                pc.mbin[e] = col + plane_cells * (uint32_t)k;
+                                pc.mcellseg[e] = mv_cell;
                             }
                         }
                     }
@@ -1836,11 +1864,25 @@ __global__ void __launch_bounds__(V4Cfg::NT, V4Cfg::MINB)
         }
         buf ^= 1;
     }
+    if constexpr (PM != 0) {  // this CTA's mover count (every reservation precedes the last barrier)
+        __syncthreads();
+        if (threadIdx.x == 0) pc.seg_cnt[seg] = s_movers;
+    }
+}
+
+// One mover segment per CTA of the fused kernel: its size and count.
+inline void set_segments(PushCtx& pc, const dim3& grid, PushCtx* used) {
+    const uint64_t nseg = (uint64_t)grid.x * grid.y * grid.z;
+    if (nseg > kMaxFusedCtas) throw Status{PICGPU_ELENGTH, "fused step: too many CTAs for the mover segments"};
+    pc.nseg = (uint32_t)nseg;
+    pc.segcap = (uint32_t)(pc.mcap / 2 / nseg);
+    pc.ovcap = pc.mcap - pc.nseg * pc.segcap;
+    if (used) *used = pc;
 }
 
 template <int ORDER, int PM>
 void launch_v4(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
-               int num_sms, cudaStream_t st, const PushCtx& pc) {
+               int num_sms, cudaStream_t st, PushCtx pc, PushCtx* used = nullptr) {
     using C = V4Cfg;
     static bool configured = false;
     if (!configured) {
@@ -1856,6 +1898,7 @@ void launch_v4(const GridD& g, const CAos& p, const uint32_t* off, const uint32_
     const int zlen = div_up(g.nz, zch);
     zch = div_up(g.nz, zlen);
     dim3 grid(tx, ty, zch);
+    if constexpr (PM != 0) set_segments(pc, grid, used);
     deposit_current_kernel_v4<ORDER, PM><<<grid, C::NT, C::SMEM, st>>>(g, p, off, cnt, q, j, j + g.ncells,
                                                                       j + 2 * (size_t)g.ncells, zlen, pc);
     note_launch();
@@ -1897,7 +1940,7 @@ void launch_warp(const GridD& g, const CAos& p, const uint32_t* off, const uint3
 // the fused push + detect + deposit form of v3.
 template <int ORDER, class C, bool V3, int PM = 0>
 void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
-                   int num_sms, cudaStream_t st, const PushCtx& pc = PushCtx{}) {
+                   int num_sms, cudaStream_t st, PushCtx pc = PushCtx{}, PushCtx* used = nullptr) {
     static_assert(V3 || PM == 0, "the fused step runs on the v3 kernel");
     using L = JLayout<ORDER, C>;
     constexpr int W = L::W;
@@ -1922,6 +1965,7 @@ void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uin
     const int zlen = div_up(g.nz, zch);
     zch = div_up(g.nz, zlen);
     dim3 grid(tx, ty, zch);
+    if constexpr (PM != 0) set_segments(pc, grid, used);
     if constexpr (V3)
         deposit_current_kernel_v3<ORDER, C, PM><<<grid, L::NT, smem, st>>>(g, p, off, cnt, q, j, j + g.ncells,
                                                                           j + 2 * (size_t)g.ncells, zlen, pc);
@@ -1993,7 +2037,7 @@ void launch_deposit_current(int order, const GridD& g, const CAos& p, const uint
 namespace {
 
 template <int ORDER>
-void launch_push_order(const GridD& g, const PushCtx& pc, const uint32_t* off, const uint32_t* cnt, double q,
+void launch_push_order(const GridD& g, PushCtx& pc, const uint32_t* off, const uint32_t* cnt, double q,
                        double* j, int num_sms, cudaStream_t st) {
     using C3 = std::conditional_t<ORDER == 1, JCfgCic3, JCfg<ORDER>>;
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
@@ -2001,14 +2045,14 @@ void launch_push_order(const GridD& g, const PushCtx& pc, const uint32_t* off, c
     if constexpr (ORDER != 1) {
         if (use_v4()) {
             if (p2)
-                return launch_v4<ORDER, 2>(g, p, off, cnt, q, j, num_sms, st, pc);
-            return launch_v4<ORDER, 1>(g, p, off, cnt, q, j, num_sms, st, pc);
+                return launch_v4<ORDER, 2>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
+            return launch_v4<ORDER, 1>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
         }
     }
     if (p2)
-        launch_kernel<ORDER, C3, true, 2>(g, p, off, cnt, q, j, num_sms, st, pc);
+        launch_kernel<ORDER, C3, true, 2>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
     else
-        launch_kernel<ORDER, C3, true, 1>(g, p, off, cnt, q, j, num_sms, st, pc);
+        launch_kernel<ORDER, C3, true, 1>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
 }
 
 // Movers of the fused step, W threads per mover (one z-plane of its window
@@ -2024,14 +2068,35 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
                                                 uint32_t* __restrict__ hl, const double qs, double* __restrict__ jx,
                                                 double* __restrict__ jy, double* __restrict__ jz) {
     constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
-    const uint64_t nm = min(pc.ctr->nmovers, pc.mcap);
+    // one CTA per mover segment (the last: the shared overflow segment); its
+    // movers take a block of the compact mover list (any order of blocks: the
+    // list is a set, as the reference's pending moves are applied one by one)
+    __shared__ uint32_t s_base, s_n;
+    const uint32_t sg = blockIdx.x;
+    if (threadIdx.x == 0) {
+        uint32_t c, n;
+        if (sg < pc.nseg) {
+            c = pc.seg_cnt[sg];
+            n = min(c, pc.segcap);  // the rest went to the overflow segment
+        } else {
+            c = pc.ctr->ovf_movers;
+            n = min(c, pc.ovcap);
+            if (c > n) atomicAdd(&pc.ctr->mover_drop, c - n);
+        }
+        s_n = n;
+        s_base = n ? atomicAdd(&pc.ctr->nmovers, n) : 0u;
+        if (n) atomicAdd(&pc.ctr->moved, (unsigned long long)(sg < pc.nseg ? n : c));
+    }
+    __syncthreads();
+    const uint32_t nm = s_n;
     const int lane = threadIdx.x & 31;
     const unsigned grp = ((1u << W) - 1u) << (lane & ~(W - 1));  // the W lanes of one mover
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nm * W;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = t / W;
+    for (uint32_t t = threadIdx.x; t < nm * W; t += blockDim.x) {
+        const uint32_t local = t / W;
+        const uint64_t i = (uint64_t)s_base + local;  // compact index
         const int kz = (int)(t % W);
-        const uint32_t s = pc.mslot[i], b = pc.mbin[i];
+        const size_t e = (size_t)sg * pc.segcap + local;
+        const uint32_t s = pc.mslot[e], b = pc.mbin[e];
         const double2* rec = reinterpret_cast<const double2*>(pc.A.p + s);
         const double2 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3];
         const double x = r0.x, y = r0.y, z = r1.x, vx = r1.y, vy = r2.x, vz = r2.y, w = r3.x;
@@ -2045,6 +2110,7 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
             M.vz[i] = vz;
             M.w[i] = w;
             M.id[i] = (uint64_t)__double_as_longlong(r3.y);
+            pc.mcell[i] = pc.mcellseg[e];
             push_hole(pc.A, s, b, off, holes, hl);
         }
         int ci, cj, ck;
@@ -2098,7 +2164,7 @@ bool fused_step_available(int order, int kernel) {
     return !v1 && (order == 1 || k == kJLane);
 }
 
-void launch_deposit_current_push(int order, const GridD& g, const PushCtx& pc, const uint32_t* off,
+void launch_deposit_current_push(int order, const GridD& g, PushCtx& pc, const uint32_t* off,
                                  const uint32_t* cnt, double q, double* j, int num_sms, cudaStream_t st) {
     if (g.slab) throw Status{PICGPU_ELOGIC, "fused step: not available on a slab store"};
     switch (order) {
@@ -2113,11 +2179,7 @@ void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, c
                    uint32_t* holes, uint32_t* hl, double q, double* j, int num_sms, cudaStream_t st) {
     const double qs = q * (order == 3 ? 1.0 / 216.0 : order == 2 ? 0.125 : 1.0);
     auto* kern = order == 1 ? k_movers<1> : order == 2 ? k_movers<2> : k_movers<3>;
-    static const int mult = [] {
-        const char* e = std::getenv("PICGPU_MOVERS_BLOCKS");
-        return e ? std::max(1, std::atoi(e)) : 16;  // latency-bound: 16 blocks/SM measured 0.02 ms faster than 4 at C2
-    }();
-    kern<<<num_sms * mult, 256, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells, j + 2 * (size_t)g.ncells);
+    kern<<<pc.nseg + 1, 128, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells, j + 2 * (size_t)g.ncells);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }

@@ -27,15 +27,23 @@ void launch_deposit_current(int order, const GridD& g, const CAos& p, const uint
 struct PushCtx {
     Aos A;                   // the binned store (positions are updated in place)
     double dt, cap2;
-    uint32_t* mslot;         // per mover: its slot, its old bin, its new cell
-    uint32_t* mbin;
-    uint32_t* mcell;
-    uint32_t mcap;
-    StepCounters* ctr;       // nmovers (all detected), err
+    uint32_t* mslot;         // per mover, segmented by shard (kMoverShards x segcap):
+    uint32_t* mbin;          //   its slot, its old bin, its new cell
+    uint32_t* mcellseg;
+    uint32_t* mcell;         // compact target cells written by k_movers (k_insert's input)
+    uint32_t mcap;           // compact mover capacity
+    uint32_t segcap;         // entries per CTA segment (half of mcap over the CTAs of the fused kernel)
+    uint32_t nseg;           // CTA segments (set by launch_deposit_current_push); segment nseg is
+    uint32_t ovcap;          //   the shared overflow segment of ovcap entries at nseg * segcap
+    uint32_t* seg_cnt;       // movers reserved per CTA segment (written at each CTA's end)
+    uint32_t* seg_pre;       // exclusive prefix of the recorded counts, nseg + 2 entries
+    StepCounters* ctr;       // -> nmovers / moved / mover_drop, err
 };
+// Upper bound on the fused kernel's CTAs (size of seg_cnt / seg_pre).
+constexpr uint32_t kMaxFusedCtas = 1u << 20;
 // The fused form exists for the default lane kernel (v3) family only.
 bool fused_step_available(int order, int kernel);
-void launch_deposit_current_push(int order, const GridD& g, const PushCtx& pc, const uint32_t* off,
+void launch_deposit_current_push(int order, const GridD& g, PushCtx& pc, const uint32_t* off,
                                  const uint32_t* cnt, double q, double* j, int num_sms, cudaStream_t st);
 // Movers of the fused kernel: slot -> mover record M[i] (+ hole in the old bin)
 // and their J contribution (RED.ADD.F64).

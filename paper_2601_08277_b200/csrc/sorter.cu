@@ -1220,6 +1220,7 @@ void BinStore::ensure_movers(size_t m) {
     mcell.ensure(m * 4);
     mslot.ensure(m * 4);
     mbin.ensure(m * 4);
+    mcellseg.ensure(m * 4);
     ovf.ensure(m * 4);
     ovf_left.ensure(m * 4);
     mcap = m;
@@ -1331,9 +1332,12 @@ void BinStore::enqueue_fused(int order, double q, double* J, double dt, double c
         return;
     }
     hl.ensure(capacity * 4 + 4);
-    PushCtx pc{A.aos(), dt, cap2, mslot.as<uint32_t>(), mbin.as<uint32_t>(), mcell.as<uint32_t>(), (uint32_t)mcap,
-               ctr};
-    launch_deposit_current_push(order, g, pc, d_off(), d_cnt(), q, J, num_sms, st);
+    segcnt.ensure(((size_t)kMaxFusedCtas + 1) * 4);
+    segpre.ensure(((size_t)kMaxFusedCtas + 2) * 4);
+    PushCtx pc{A.aos(), dt, cap2, mslot.as<uint32_t>(), mbin.as<uint32_t>(), mcellseg.as<uint32_t>(),
+               mcell.as<uint32_t>(), (uint32_t)mcap, 0u, 0u, 0u, segcnt.as<uint32_t>(), segpre.as<uint32_t>(), ctr};
+    launch_deposit_current_push(order, g, pc, d_off(), d_cnt(), q, J, num_sms, st);  // sets nseg, segcap
+    fused_nseg = pc.nseg;
     if (after_kernel) PICGPU_CUDA_TRY(cudaEventRecord(after_kernel, st));
     launch_movers(order, g, pc, M.soa(), d_off(), holes.as<uint32_t>(), hl.as<uint32_t>(), q, J, num_sms, st);
     enqueue_migrate();
@@ -1412,8 +1416,14 @@ bool BinStore::finish_incremental(StepCounters& out) {
     PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
     out = *hcounters;
     if (out.err) return false;
-    const bool mover_overflow = out.nmovers > mcap || movers_dropped;
-    const uint32_t nmovers_seen = movers_dropped ? (uint32_t)std::max<size_t>(mcap, out.nmovers) : out.nmovers;
+    const bool mover_overflow = out.nmovers > mcap || out.mover_drop > 0 || movers_dropped;
+    // (fused step: CTA segments hold half of mcap, the overflow segment the rest;
+    // after a drop the buffers grow to twice the movers seen)
+    const uint32_t nmovers_seen =
+        movers_dropped ? (uint32_t)std::max<size_t>(mcap, out.nmovers)
+                       : (uint32_t)std::min<uint64_t>(0xffffffffull / 4,
+                                                      (uint64_t)(out.nmovers + out.mover_drop) *
+                                                          (out.mover_drop ? 2 : 1));
     movers_dropped = false;
     // unplaced arrivals (no donor found); borrowed ones already sit in their bins
     const uint32_t left = out.nleft;
