@@ -2179,7 +2179,10 @@ void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, c
                    uint32_t* holes, uint32_t* hl, double q, double* j, int num_sms, cudaStream_t st) {
     const double qs = q * (order == 3 ? 1.0 / 216.0 : order == 2 ? 0.125 : 1.0);
     auto* kern = order == 1 ? k_movers<1> : order == 2 ? k_movers<2> : k_movers<3>;
-    kern<<<pc.nseg + 1, 128, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells, j + 2 * (size_t)g.ncells);
+#ifndef PICGPU_MOVERS_NT
+#define PICGPU_MOVERS_NT 256  // C2: 256 0.242 ms, 128 0.247, 64 0.264 (movers + insert + borrow)
+#endif
+    kern<<<pc.nseg + 1, PICGPU_MOVERS_NT, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells, j + 2 * (size_t)g.ncells);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
