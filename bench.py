@@ -347,9 +347,37 @@ def main():
 
     # e2e through the stateless C-ABI drop-in, pinned host buffers
     e2e = None
+    e2e_session = None
     if True:  # every rank (the max over ranks needs them all)
         p = S.particles()
         n = p.size()
+        if world == 1 and not args.slab and args.e2e_steps > 0:
+            # the device-resident session as a PIC code drives it: particles uploaded
+            # once from host memory, then every step push + sort + J on the device
+            # and J read back into pinned host memory (the field solver's input)
+            S.upload(p, q=-1.0)
+            jh = [torch.empty(grid.ncells, dtype=torch.float64, pin_memory=True) for _ in range(3)]
+            L = pg.lib()
+
+            def sess_step():
+                S.step(dt)
+                rc = L.picgpu_session_download_current(S._h, *(C.c_void_p(t.data_ptr()) for t in jh))
+                if rc:
+                    raise RuntimeError(L.picgpu_last_error().decode())
+
+            sess_step()
+            torch.cuda.synchronize()
+            ks = max(args.steps, 3)
+            t0 = time.perf_counter()
+            for _ in range(ks):
+                sess_step()
+            ts = time.perf_counter() - t0
+            e2e_session = {"value": n * ks / ts, "unit": UNIT, "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 3 * 8 * grid.ncells, "steps": ks,
+                           "api": "picgpu_session_step + picgpu_session_download_current (particles uploaded "
+                                  "once from host memory before timing; J read back to pinned host memory "
+                                  "every step)",
+                           "timer": "host wall clock around synchronous C-ABI calls"}
         S.close()  # the stateless call below allocates its own workspace (C3: ~86 GB each)
         host = {}
         for k in ("x", "y", "z", "vx", "vy", "vz", "w"):
@@ -410,7 +438,7 @@ def main():
                        "parallelism": "single" if world == 1 else
                        f"x-slabs x{world} of a {'x'.join(map(str, G_dims))} box, NCCL ring exchange "
                        "(migration + J guards)"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_session": e2e_session, "gpu_launches": launches,
             "clocks": clk.summary(),
             "phases_ms_total": {k: v[0] for k, v in phases.items()},
             "moved_fraction": moved / (n * args.steps), "rebuilds": rebuilds, "fused_steps": fused_steps,
