@@ -2071,21 +2071,32 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
     // one CTA per mover segment (the last: the shared overflow segment); its
     // movers take a block of the compact mover list (any order of blocks: the
     // list is a set, as the reference's pending moves are applied one by one)
-    __shared__ uint32_t s_base, s_n;
-    const uint32_t sg = blockIdx.x;
+    // (the overflow segment is split over the CTAs past the last segment)
+    __shared__ uint32_t s_base, s_n, s_first;
+    const uint32_t sg = min(blockIdx.x, pc.nseg);
     if (threadIdx.x == 0) {
-        uint32_t c, n;
-        if (sg < pc.nseg) {
+        uint32_t c, n, first = 0;
+        if (blockIdx.x < pc.nseg) {
             c = pc.seg_cnt[sg];
             n = min(c, pc.segcap);  // the rest went to the overflow segment
+            c = n;
         } else {
-            c = pc.ctr->ovf_movers;
-            n = min(c, pc.ovcap);
-            if (c > n) atomicAdd(&pc.ctr->mover_drop, c - n);
+            const uint32_t part = blockIdx.x - pc.nseg, parts = gridDim.x - pc.nseg;
+            const uint32_t o = pc.ctr->ovf_movers;
+            const uint32_t total = min(o, pc.ovcap);
+            const uint32_t chunk = (total + parts - 1) / parts;
+            first = min(part * chunk, total);
+            n = min(total - first, chunk);
+            c = n;
+            if (part == 0) {
+                if (o > total) atomicAdd(&pc.ctr->mover_drop, o - total);
+                c += o - total;  // dropped movers moved too
+            }
         }
         s_n = n;
+        s_first = first;
         s_base = n ? atomicAdd(&pc.ctr->nmovers, n) : 0u;
-        if (n) atomicAdd(&pc.ctr->moved, (unsigned long long)(sg < pc.nseg ? n : c));
+        if (c) atomicAdd(&pc.ctr->moved, (unsigned long long)c);
     }
     __syncthreads();
     const uint32_t nm = s_n;
@@ -2095,7 +2106,7 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
         const uint32_t local = t / W;
         const uint64_t i = (uint64_t)s_base + local;  // compact index
         const int kz = (int)(t % W);
-        const size_t e = (size_t)sg * pc.segcap + local;
+        const size_t e = (size_t)sg * pc.segcap + s_first + local;
         const uint32_t s = pc.mslot[e], b = pc.mbin[e];
         const double2* rec = reinterpret_cast<const double2*>(pc.A.p + s);
         const double2 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3];
@@ -2182,7 +2193,7 @@ void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, c
 #ifndef PICGPU_MOVERS_NT
 #define PICGPU_MOVERS_NT 256  // C2: 256 0.242 ms, 128 0.247, 64 0.264 (movers + insert + borrow)
 #endif
-    kern<<<pc.nseg + 1, PICGPU_MOVERS_NT, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells, j + 2 * (size_t)g.ncells);
+    kern<<<pc.nseg + (uint32_t)num_sms * 4, PICGPU_MOVERS_NT, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells, j + 2 * (size_t)g.ncells);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
