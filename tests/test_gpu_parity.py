@@ -521,3 +521,38 @@ def test_fusion_policy_follows_migration(pg, orc):
         S.upload(hot, q=-1.0)
         assert [S.step(0.5)["fused"] for _ in range(2)] == [1, 1]
         assert S.step(0.5, pg.STEP_DEFAULT | pg.STEP_UNFUSED)["fused"] == 0
+
+
+def test_fused_mover_segment_overflow(pg, orc):
+    """Movers concentrated in a few CTAs (a fast beam in one x-tile column, as
+    C4's beam): their per-CTA segments overflow into the shared overflow
+    segment (no drop, no full re-sort).  Same particles, bins and J as the
+    unfused step and the oracle."""
+    g = O.Grid.make(64)
+    s = orc.make_plasma(g, 4, 0.0, seed=9)           # 1,048,576 particles at rest
+    beam = s["x"] < 8.0                              # one 8-cell column of tiles
+    s["vx"][beam] = 1.5                              # dt 0.5: +0.75 cell, ~3/4 change cell
+    q = -1.0
+    G = to_pg_grid(g)
+    ref = {k: v.copy() for k, v in s.items()}
+    with pg.Session(G, order=3) as A, pg.Session(G, order=3) as B:
+        A.set_fusion(2.0)
+        A.upload(s, q=q)
+        B.upload(s, q=q)
+        for step in range(3):
+            moved = orc.advance(g, 0.5, ref)
+            sa = A.step(0.5)
+            sb = B.step(0.5, pg.STEP_DEFAULT | pg.STEP_UNFUSED)
+            assert sa["fused"] == 1 and sb["fused"] == 0
+            assert sa["moved"] == sb["moved"] == moved > 50000
+            assert sa["rebuilt"] == 0  # the overflow segment held every mover
+            pa, pb = A.particles(), B.particles()
+            oa, ob, oc = np.argsort(pa.id), np.argsort(pb.id), np.argsort(ref["id"])
+            for k in ("x", "y", "z"):
+                assert np.array_equal(getattr(pa, k)[oa], ref[k][oc]), (step, k)
+                assert np.array_equal(getattr(pb, k)[ob], ref[k][oc]), (step, k)
+            (_, cnta), (_, cntb) = A.bins(), B.bins()
+            assert np.array_equal(cnta, cntb)
+            want = orc.deposit_current(g, 3, ref, q)
+            Ja = A.current()
+            assert peak_rel_err((Ja.jx, Ja.jy, Ja.jz), want) <= J_TOL
