@@ -124,6 +124,8 @@ static int current_sms() {
 struct Stateless {
     std::mutex mu;
     cudaStream_t st = nullptr;
+    cudaStream_t st2 = nullptr;     // second upload stream (velocities, weights)
+    cudaEvent_t fields = nullptr;   // ... recorded after them
     BinStore store;
     DevBuf J, aux, flag;
     picgpu_grid grid{};
@@ -131,6 +133,8 @@ struct Stateless {
 
     void prepare(const picgpu_grid& g) {
         if (!st) PICGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        if (!st2) PICGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+        if (!fields) PICGPU_CUDA_TRY(cudaEventCreateWithFlags(&fields, cudaEventDisableTiming));
         if (!ready || std::memcmp(&g, &grid, sizeof g) != 0) {
             store.init(g, 0.0, 0, st);
             grid = g;
@@ -276,11 +280,17 @@ static void stateless_current(const picgpu_grid* g, int order, const double* x, 
         for (auto& e : ev) PICGPU_CUDA_TRY(cudaEventCreate(&e));
     bs.B.ensure(n);
     const Soa b = bs.B.soa();
+    // positions first on the sort's stream, the other fields on a second
+    // stream: cells, radix sort and layout run while velocities and weights
+    // are still crossing PCIe (the gather waits for them)
     h2d(b.x, x, n * 8, st); h2d(b.y, y, n * 8, st); h2d(b.z, z, n * 8, st);
-    h2d(b.vx, vx, n * 8, st); h2d(b.vy, vy, n * 8, st); h2d(b.vz, vz, n * 8, st);
-    h2d(b.w, w, n * 8, st);
+    PICGPU_CUDA_TRY(cudaEventRecord(S.fields, st));  // B is free (previous users on st are done)
+    PICGPU_CUDA_TRY(cudaStreamWaitEvent(S.st2, S.fields, 0));
+    h2d(b.vx, vx, n * 8, S.st2); h2d(b.vy, vy, n * 8, S.st2); h2d(b.vz, vz, n * 8, S.st2);
+    h2d(b.w, w, n * 8, S.st2);
+    PICGPU_CUDA_TRY(cudaEventRecord(S.fields, S.st2));
     if (timed) PICGPU_CUDA_TRY(cudaEventRecord(ev[0], st));
-    bs.full_sort_from_B(n);
+    bs.full_sort_from_B(n, nullptr, S.fields);
     if (timed) PICGPU_CUDA_TRY(cudaEventRecord(ev[1], st));
     S.J.ensure((size_t)gd.ncells * 24);
     double* J = S.J.as<double>();

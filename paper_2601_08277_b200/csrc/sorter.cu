@@ -1094,7 +1094,7 @@ void BinStore::layout_from_counts(uint64_t) {
     capacity_next = total;
 }
 
-void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev) {
+void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev, cudaEvent_t fields_ready) {
     const size_t nc = g.ncells;
     if (np >= 0xffffffffull) throw Status{PICGPU_ELENGTH, "gpma: particle count exceeds 32-bit slots"};
     keys.ensure(np * 4 + 4);
@@ -1143,6 +1143,7 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev) {
         note_launch();
     }
     if (np) {
+        if (fields_ready) PICGPU_CUDA_TRY(cudaStreamWaitEvent(st, fields_ready, 0));
         k_gather_sorted<<<div_up((long long)np, 256), 256, 0, st>>>(b, vals2.as<uint32_t>(), skeys.as<uint32_t>(),
                                                                     start.as<uint32_t>(), off.as<uint32_t>(),
                                                                     A.aos(), np);

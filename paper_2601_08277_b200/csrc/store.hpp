@@ -90,7 +90,10 @@ struct BinStore {
 
     // B holds n packed particles: stable sort by cell into A with fresh slack
     // (gpma_build, gpma.hpp:379-402).  perm/starts/counts optionally exported.
-    void full_sort_from_B(uint64_t n_particles, uint32_t* perm_out_dev = nullptr);
+    // `fields_ready` (optional): B's non-position fields may still be in flight
+    // until this event -- the cell keys, the sort and the layout only need
+    // x y z, so they overlap the rest of an upload; the gather waits for it.
+    void full_sort_from_B(uint64_t n_particles, uint32_t* perm_out_dev = nullptr, cudaEvent_t fields_ready = nullptr);
     // Re-layout A's bins with fresh slack from the current counts (global_sort
     // on an already-binned store == identity permutation inside bins).
     void relayout();
