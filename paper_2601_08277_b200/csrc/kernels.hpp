@@ -27,7 +27,7 @@ void launch_deposit_current(int order, const GridD& g, const CAos& p, const uint
 struct PushCtx {
     Aos A;                   // the binned store (positions are updated in place)
     double dt, cap2;
-    uint32_t* mslot;         // per mover, segmented by shard (kMoverShards x segcap):
+    uint32_t* mslot;         // per mover, by CTA segment (nseg x segcap, then the overflow segment):
     uint32_t* mbin;          //   its slot, its old bin, its new cell
     uint32_t* mcellseg;
     uint32_t* mcell;         // compact target cells written by k_movers (k_insert's input)

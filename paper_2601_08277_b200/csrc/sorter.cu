@@ -4,12 +4,14 @@
 // Reference anchors (proj/include/pic/):
 //   gpma_build          gpma.hpp:379-402  -> BinStore::full_sort_from_B (stable radix sort by cell)
 //   Gpma::layout        gpma.hpp:269-302  -> k_counts_caps + scan (same capacity rule)
-//   detect_moves        gpma.hpp:162-177  -> k_push (fused with the push; departures leave holes)
-//   apply_moves/insert  gpma.hpp:110-125, :248-262 -> k_insert (per-bin atomic tail cursor into slack)
-//   borrow/overflow     gpma.hpp:337-370  -> overflow list -> rebuild (relayout with fresh slack)
-//   rebuild             gpma.hpp:130-143  -> BinStore::rebuild_overflow
+//   detect_moves        gpma.hpp:162-177  -> k_push + k_departures (unfused step: departures leave
+//                                            holes), or the fused J pass + k_movers (deposit_current.cu)
+//   apply_moves/insert  gpma.hpp:110-125, :248-262 -> k_insert (a hole of the bin, else its slack)
+//   borrow_insert       gpma.hpp:337-370  -> k_borrow (next 4 bins), else the rebuild below
+//   rebuild             gpma.hpp:130-143  -> BinStore::finish_incremental (relayout with fresh slack)
 //   global_sort         sort_policy.hpp:83-85 -> BinStore::relayout
 //   advance             workload.hpp:128-155 -> push_one (round-to-nearest intrinsics, bit-identical)
+// The store is an array of 64-byte particle records (common.cuh, Part).
 #include <cub/cub.cuh>
 
 #include <algorithm>

@@ -2,11 +2,12 @@
 // analogue of pic::Gpma, proj/include/pic/gpma.hpp:52-371).
 //
 // Unlike the reference GPMA, whose slots hold REFERENCES into an unsorted
-// store, the bins here hold the particle data itself (7 FP64 arrays + id): the
-// deposition kernels then read particles cell-locally and coalesced straight
-// from HBM.  Bin c owns slots [off[c], off[c+1]); its cnt[c] particles are
-// packed at the head, the slack at the tail; every slack slot's x holds an
-// all-ones sentinel so the push can stream over raw slots.  Capacities follow the
+// store, the bins here hold the particle data itself (one 64-byte record per
+// slot: 7 FP64 + id): the deposition kernels then read particles cell-locally
+// and coalesced straight from HBM.  Bin c owns slots [off[c], off[c+1]); its
+// extent [off[c], off[c]+cnt[c]) holds its particles and holes, the slack
+// follows; every slack slot and hole is an all-ones record (gap sentinel x) so
+// the push and the deposits can stream over raw slots.  Capacities follow the
 // reference's layout rule exactly, ceil(count*(1+gap_ratio)) + min_gap
 // (gpma.hpp:274-281), so capacity and empty_slot_ratio match the reference.
 #pragma once
@@ -65,7 +66,7 @@ struct BinStore {
     DevBuf keys, keys2, skeys, vals, vals2, start, endp, caps, cub_tmp;
     SoaBuf M;                 // mover records
     DevBuf mcell, ovf, ovf_left;  // mover target cell, overflow list, unplaced overflow
-    DevBuf mslot, mbin;       // each mover's slot and old bin (fused step: by shard segment)
+    DevBuf mslot, mbin;       // each mover's slot and old bin (fused step: by CTA segment)
     DevBuf mcellseg;          // fused step: movers' target cells by CTA segment
     DevBuf segcnt, segpre;    // fused step: movers per CTA segment, their exclusive prefix
     uint32_t fused_nseg = 0;  // segments of the last fused launch
