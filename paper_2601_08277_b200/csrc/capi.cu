@@ -213,6 +213,7 @@ struct picgpu_session {
     int ghost = 0;
     int own = 0;
     bool pending = false;      // between step_begin and step_end
+    bool pending_fused = false;  // ... of a fused step (J deposited in step_begin)
     uint32_t pending_flags = 0;
     uint64_t nleave[2] = {0, 0};
     StepCounters cbegin{};
@@ -1071,15 +1072,35 @@ int picgpu_session_step_begin(picgpu_session* s, double dt, uint32_t flags, uint
         if (flags & PICGPU_STEP_DENSITY) check_density_grid(bs.hg, s->order);
         const double cap2 = (flags & PICGPU_STEP_PUSH) ? cap2_of(bs.hg, dt) : 0.0;
         const uint64_t l0 = g_launches.load();
+        // the fused step as on a whole box: push + detect + J of the particles
+        // that stay on the slab (leavers are exported undeposited; the receiver
+        // deposits its arrivals in step_end)
+        const uint32_t fuse_mask = PICGPU_STEP_PUSH | PICGPU_STEP_SORT | PICGPU_STEP_CURRENT;
+        const bool fused = (flags & fuse_mask) == fuse_mask && !(flags & PICGPU_STEP_UNFUSED) &&
+                           s->last_moved < s->fuse_max && fused_step_available(s->order, s->kernel);
         if (s->timing) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], s->st));
-        bs.enqueue_detect((flags & PICGPU_STEP_PUSH) != 0, dt, cap2);
+        if (fused) {
+            PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)bs.g.ncells * 24, s->st));
+            bs.enqueue_fused(s->order, s->q, s->J.as<double>(), dt, cap2, s->timing ? s->ev[4] : nullptr,
+                             /*migrate=*/false);
+        } else {
+            bs.enqueue_detect((flags & PICGPU_STEP_PUSH) != 0, dt, cap2);
+        }
         if (s->timing) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], s->st));
         PICGPU_CUDA_TRY(
             cudaMemcpyAsync(bs.hcounters, bs.counters.p, sizeof(StepCounters), cudaMemcpyDeviceToHost, s->st));
         PICGPU_CUDA_TRY(cudaStreamSynchronize(s->st));
         const StepCounters c = *bs.hcounters;
         if (c.err) throw_step_error(c.err);
-        if (s->timing) accumulate_phase(s, 0, 0, 1, g_launches.load() - l0);
+        if (s->timing) {
+            if (fused) {  // zero + fused kernel -> deposit J; the movers -> sort
+                accumulate_phase(s, 3, 0, 4, 1);
+                accumulate_phase(s, 0, 4, 1, g_launches.load() - l0 - 1);
+            } else {
+                accumulate_phase(s, 0, 0, 1, g_launches.load() - l0);
+            }
+        }
+        s->pending_fused = fused;
         s->cbegin = c;
         s->nleave[0] = c.nleave[0];
         s->nleave[1] = c.nleave[1];
@@ -1120,10 +1141,14 @@ int picgpu_session_step_end(picgpu_session* s, const double* arrivals, uint64_t 
         if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
         const size_t base = std::min<size_t>(cb.nmovers, bs.mcap);
         if (cb.nmovers > bs.mcap) bs.movers_dropped = true;
+        const size_t mcap0 = bs.mcap;
         if (n_arr) {
             if (n_arr >= 0xffffffffull) throw Status{PICGPU_ELENGTH, "slab: too many arrivals"};
             bs.ensure_movers_keep(base + n_arr + (base + n_arr) / 4, base);
             bs.enqueue_import(arrivals, (uint32_t)n_arr, (uint32_t)base);
+            if (s->pending_fused)  // the sender left them out of its fused deposit
+                launch_deposit_records(s->order, bs.g, bs.M.soa(), bs.counters.as<StepCounters>(), (uint32_t)base,
+                                       s->q, s->J.as<double>(), bs.num_sms, st);
         }
         bs.n = bs.n - s->nleave[0] - s->nleave[1] + n_arr;
         bs.enqueue_migrate();
@@ -1136,6 +1161,12 @@ int picgpu_session_step_end(picgpu_session* s, const double* arrivals, uint64_t 
         stats.moved = cb.moved;
         stats.inserts = base + n_arr;
         stats.overflowed = c.noverflow;
+        uint32_t dflags = flags;
+        if (s->pending_fused) {
+            stats.fused = 1;
+            // J is complete unless movers were dropped (full re-sort): redo it then
+            if (!(rebuilt && (c.mover_drop > 0 || cb.nmovers > mcap0))) dflags &= ~PICGPU_STEP_CURRENT;
+        }
         if (T) {
             accumulate_phase(s, 0, 0, 1, lm);
             if (rebuilt) {
@@ -1145,14 +1176,14 @@ int picgpu_session_step_end(picgpu_session* s, const double* arrivals, uint64_t 
             }
         }
         uint64_t lj = 0, lr = 0;
-        enqueue_deposits(s, flags, &lj, &lr);
+        enqueue_deposits(s, dflags, &lj, &lr);
         PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
         if (T) {
-            if (flags & PICGPU_STEP_CURRENT) {
+            if (dflags & PICGPU_STEP_CURRENT) {
                 accumulate_phase(s, 5, 2, 3, 0);
                 accumulate_phase(s, 3, 3, 4, lj);
             }
-            if (flags & PICGPU_STEP_DENSITY) accumulate_phase(s, 4, 5, 6, lr);
+            if (dflags & PICGPU_STEP_DENSITY) accumulate_phase(s, 4, 5, 6, lr);
         }
         if (flags & PICGPU_STEP_PUSH)
             s->last_moved = bs.n ? (double)stats.moved / (double)bs.n : 0.0;

@@ -45,6 +45,7 @@ constexpr long long kGapBits = -1LL;
 // Store-cell codes of particles that left a slab (push / import routing).
 constexpr uint32_t kLeaveLeft = 0xFFFFFFFEu;
 constexpr uint32_t kLeaveRight = 0xFFFFFFFDu;
+constexpr uint32_t kNoCell = 0xFFFFFFFFu;  // a mover-list entry without a particle (exported leaver)
 
 GridD make_grid(const picgpu_grid& g);
 

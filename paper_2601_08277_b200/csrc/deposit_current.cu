@@ -664,7 +664,7 @@ __device__ __forceinline__ double wrap_fast(double x, double origin, double leng
 // (shx, shy, shz) that places its taps in the bin's window.  Positions are
 // finite on entry (the store only holds located particles).  Returns false
 // on an error (the reference would throw; the device flag is raised).
-template <bool P2>
+template <bool P2, bool SLAB = false>
 __device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PData& d, uint32_t s, uint32_t b,
                                            int i, int j, int k, double dci, double dcj, double dck, double& fx,
                                            double& fy, double& fz, bool& mv, uint32_t& mv_cell, int& shx,
@@ -703,6 +703,13 @@ __device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PD
             shx = fx < 0.0 ? -1 : (fx >= 1.0 ? 1 : 0);
             shy = fy < 0.0 ? -1 : (fy >= 1.0 ? 1 : 0);
             shz = fz < 0.0 ? -1 : (fz >= 1.0 ? 1 : 0);
+            if constexpr (SLAB) {
+                if (i + shx < g.sx_lo || i + shx >= g.sx_hi) {  // left the slab: k_movers exports it
+                    mv = true;
+                    mv_cell = i + shx < g.sx_lo ? kLeaveLeft : kLeaveRight;
+                    return false;
+                }
+            }
             fx -= (double)shx;
             fy -= (double)shy;
             fz -= (double)shz;
@@ -713,10 +720,20 @@ __device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PD
     }
     int ni, nj, nk;
     const uint32_t nc = cell_linear<P2>(g, d.x, d.y, d.z, ni, nj, nk, fx, fy, fz);  // exact (pic::cell_of)
+    if constexpr (SLAB) {
+        const uint32_t code = store_cell<P2>(g, d.x, d.y, d.z);  // kLeaveLeft / kLeaveRight off the slab
+        if (code >= kLeaveRight) {  // left the slab: k_movers exports it, nothing deposited here
+            mv = true;
+            mv_cell = code;
+            return false;
+        }
+    }
     if (nc == b) return true;  // a periodic image of the bin's cell
     mv = true;
     mv_cell = nc;
-    shx = cell_step(ni - i, g.nx);
+    // the step on the GLOBAL periodic x axis: a one-slab store (P = 1) wraps
+    // through its ghost layers, where the local index difference is not +-1
+    shx = cell_step(ni - i, g.gnx);
     shy = cell_step(nj - j, g.ny);
     shz = cell_step(nk - k, g.nz);
     return true;
@@ -725,7 +742,7 @@ __device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PD
 // PM (fused step, PushCtx): 0 = deposit only; 1 = push + move detection + deposit of the
 // particles that stay in their cell (launch_deposit_current_push); 2 = the same
 // with every spacing and box length a power of two (compile-time reciprocals).
-template <int ORDER, class CF = JCfg<ORDER>, int PM = 0>
+template <int ORDER, class CF = JCfg<ORDER>, int PM = 0, bool SLAB = false>
 __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
     deposit_current_kernel_v3(const GridD g, const CAos p, const uint32_t* __restrict__ off,
                               const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
@@ -868,9 +885,9 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                         double fx = 0.0, fy = 0.0, fz = 0.0;
                         int shx = 0, shy = 0, shz = 0;
                         if (valid)
-                            valid = push_fused<PM == 2>(g, pc, cur, c_off + (uint32_t)(base + lg),
-                                                        col + plane_cells * (uint32_t)k, i, j, k, dci, dcj, dck,
-                                                        fx, fy, fz, mv, mv_cell, shx, shy, shz);
+                            valid = push_fused<PM == 2, SLAB>(g, pc, cur, c_off + (uint32_t)(base + lg),
+                                                              col + plane_cells * (uint32_t)k, i, j, k, dci, dcj, dck,
+                                                              fx, fy, fz, mv, mv_cell, shx, shy, shz);
                         // one mover-list reservation per warp; its result is only
                         // needed after the contraction below
                         mv_bal = __ballot_sync(0xffffffffu, mv);
@@ -878,7 +895,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                             mv_b0 = atomicAdd(&s_movers, (unsigned)__popc(mv_bal));
                         window_from_fractions<ORDER>(cur, qs, valid, fx, fy, fz, a, sy, sz);
                         stage_record<L, W>(stage, lg, grp, R, a, sy, sz);
-                        if (mv) {
+                        if (mv && valid) {
                             // a mover's taps, shifted into this cell's window by its cell
                             // step (read back from its staged record: runtime offsets stay
                             // in shared memory); taps that leave the window are k_movers'
@@ -1938,7 +1955,7 @@ void launch_warp(const GridD& g, const CAos& p, const uint32_t* off, const uint3
 
 // z-chunked grid of one of the pencil kernels (v3 or the original v1); PM > 0:
 // the fused push + detect + deposit form of v3.
-template <int ORDER, class C, bool V3, int PM = 0>
+template <int ORDER, class C, bool V3, int PM = 0, bool SLAB = false>
 void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
                    int num_sms, cudaStream_t st, PushCtx pc = PushCtx{}, PushCtx* used = nullptr) {
     static_assert(V3 || PM == 0, "the fused step runs on the v3 kernel");
@@ -1948,7 +1965,7 @@ void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uin
     static bool configured = false;
     if (!configured) {
         if constexpr (V3)
-            PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel_v3<ORDER, C, PM>,
+            PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel_v3<ORDER, C, PM, SLAB>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         else
             PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel<ORDER>,
@@ -1967,8 +1984,8 @@ void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uin
     dim3 grid(tx, ty, zch);
     if constexpr (PM != 0) set_segments(pc, grid, used);
     if constexpr (V3)
-        deposit_current_kernel_v3<ORDER, C, PM><<<grid, L::NT, smem, st>>>(g, p, off, cnt, q, j, j + g.ncells,
-                                                                          j + 2 * (size_t)g.ncells, zlen, pc);
+        deposit_current_kernel_v3<ORDER, C, PM, SLAB><<<grid, L::NT, smem, st>>>(g, p, off, cnt, q, j, j + g.ncells,
+                                                                                j + 2 * (size_t)g.ncells, zlen, pc);
     else
         deposit_current_kernel<ORDER><<<grid, L::NT, smem, st>>>(g, p, off, cnt, q, j, j + g.ncells,
                                                                  j + 2 * (size_t)g.ncells, zlen);
@@ -2043,16 +2060,22 @@ void launch_push_order(const GridD& g, PushCtx& pc, const uint32_t* off, const u
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
     const CAos p(pc.A);
     if constexpr (ORDER != 1) {
-        if (use_v4()) {
+        if (use_v4() && !g.slab) {
             if (p2)
                 return launch_v4<ORDER, 2>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
             return launch_v4<ORDER, 1>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
         }
     }
-    if (p2)
+    if (g.slab) {
+        if (p2)
+            launch_kernel<ORDER, C3, true, 2, true>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
+        else
+            launch_kernel<ORDER, C3, true, 1, true>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
+    } else if (p2) {
         launch_kernel<ORDER, C3, true, 2>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
-    else
+    } else {
         launch_kernel<ORDER, C3, true, 1>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
+    }
 }
 
 // Movers of the fused step, W threads per mover (one z-plane of its window
@@ -2112,6 +2135,25 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
         const double2 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3];
         const double x = r0.x, y = r0.y, z = r1.x, vx = r1.y, vy = r2.x, vz = r2.y, w = r3.x;
         __syncwarp(grp);  // every lane of the mover has read the slot before it becomes a hole
+        const uint32_t mc = pc.mcellseg[e];
+        if (mc >= kLeaveRight) {  // left the slab: an exchange record for the neighbour, no deposit
+            if (kz == 0) {
+                pc.mcell[i] = kNoCell;  // k_insert skips the entry
+                const int dir = mc == kLeaveLeft ? 0 : 1;
+                const unsigned li = atomicAdd(&pc.ctr->nleave[dir], 1u);
+                if (li < pc.lcap) {
+                    double* rr = pc.L + ((size_t)dir * pc.lcap + li) * 8;
+                    rr[0] = x; rr[1] = y; rr[2] = z;
+                    rr[3] = vx; rr[4] = vy; rr[5] = vz;
+                    rr[6] = w;
+                    rr[7] = r3.y;
+                    push_hole(pc.A, s, b, off, holes, hl);
+                } else {
+                    raise_error(&pc.ctr->err, PICGPU_ELENGTH);
+                }
+            }
+            continue;
+        }
         if (kz == 0) {
             M.x[i] = x;
             M.y[i] = y;
@@ -2121,7 +2163,7 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
             M.vz[i] = vz;
             M.w[i] = w;
             M.id[i] = (uint64_t)__double_as_longlong(r3.y);
-            pc.mcell[i] = pc.mcellseg[e];
+            pc.mcell[i] = mc;
             push_hole(pc.A, s, b, off, holes, hl);
         }
         int ci, cj, ck;
@@ -2129,7 +2171,7 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
         cell_linear(g, x, y, z, ci, cj, ck, fx, fy, fz);
         const uint32_t bi = b % (uint32_t)g.nx, bj = (b / (uint32_t)g.nx) % (uint32_t)g.ny,
                        bk = b / ((uint32_t)g.nx * (uint32_t)g.ny);
-        const int shx = cell_step(ci - (int)bi, g.nx), shy = cell_step(cj - (int)bj, g.ny),
+        const int shx = cell_step(ci - (int)bi, g.gnx), shy = cell_step(cj - (int)bj, g.ny),
                   shz = cell_step(ck - (int)bk, g.nz);
         double sx[W], sy[W], sz[W];
         weights_scaled<ORDER>(fx, sx);
@@ -2177,13 +2219,67 @@ bool fused_step_available(int order, int kernel) {
 
 void launch_deposit_current_push(int order, const GridD& g, PushCtx& pc, const uint32_t* off,
                                  const uint32_t* cnt, double q, double* j, int num_sms, cudaStream_t st) {
-    if (g.slab) throw Status{PICGPU_ELOGIC, "fused step: not available on a slab store"};
     switch (order) {
         case 1: launch_push_order<1>(g, pc, off, cnt, q, j, num_sms, st); break;
         case 2: launch_push_order<2>(g, pc, off, cnt, q, j, num_sms, st); break;
         case 3: launch_push_order<3>(g, pc, off, cnt, q, j, num_sms, st); break;
         default: throw Status{PICGPU_EINVAL, "deposit: shape order must be 1, 2 or 3"};
     }
+}
+
+namespace {
+// Slab arrivals of a fused step over their full window, W threads per record
+// (one z-plane each).  The records sit after the local movers in M; their
+// cells are owned by this slab, so the window stays on the slab grid.
+template <int ORDER>
+__global__ void __launch_bounds__(256) k_deposit_records(const GridD g, const Soa M, const StepCounters* ctr,
+                                                         uint32_t base, const double qs, double* __restrict__ jx,
+                                                         double* __restrict__ jy, double* __restrict__ jz) {
+    constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
+    const uint64_t n = ctr->nimport;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * W;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = base + t / W;
+        const int kz = (int)(t % W);
+        const double x = M.x[i], y = M.y[i], z = M.z[i];
+        int ci, cj, ck;
+        double fx, fy, fz;
+        cell_linear(g, x, y, z, ci, cj, ck, fx, fy, fz);
+        double sx[W], sy[W], sz[W];
+        weights_scaled<ORDER>(fx, sx);
+        weights_scaled<ORDER>(fy, sy);
+        weights_scaled<ORDER>(fz, sz);
+        double szk = sz[0];
+#pragma unroll
+        for (int u = 1; u < W; ++u) szk = kz == u ? sz[u] : szk;
+        const double qw = qs * M.w[i];
+        const double wq0 = qw * M.vx[i], wq1 = qw * M.vy[i], wq2 = qw * M.vz[i];
+        const size_t Z = (size_t)wrap_index(ck + OFF + kz, g.nz);
+#pragma unroll
+        for (int jj = 0; jj < W; ++jj) {
+            const double bb = sy[jj] * szk;
+            const size_t row = ((size_t)wrap_index(cj + OFF + jj, g.ny) + (size_t)g.ny * Z) * (size_t)g.nx;
+#pragma unroll
+            for (int ix = 0; ix < W; ++ix) {
+                const double v = sx[ix] * bb;
+                if (v == 0.0) continue;
+                const size_t node = row + (size_t)wrap_index(ci + OFF + ix, g.nx);
+                atomicAdd(jx + node, wq0 * v);
+                atomicAdd(jy + node, wq1 * v);
+                atomicAdd(jz + node, wq2 * v);
+            }
+        }
+    }
+}
+}  // namespace
+
+void launch_deposit_records(int order, const GridD& g, const Soa& M, const StepCounters* ctr, uint32_t base,
+                            double q, double* j, int num_sms, cudaStream_t st) {
+    const double qs = q * (order == 3 ? 1.0 / 216.0 : order == 2 ? 0.125 : 1.0);
+    auto* kern = order == 1 ? k_deposit_records<1> : order == 2 ? k_deposit_records<2> : k_deposit_records<3>;
+    kern<<<num_sms * 4, 256, 0, st>>>(g, M, ctr, base, qs, j, j + g.ncells, j + 2 * (size_t)g.ncells);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
 void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, const uint32_t* off,

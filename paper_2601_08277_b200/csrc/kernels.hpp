@@ -38,6 +38,13 @@ struct PushCtx {
     uint32_t* seg_cnt;       // movers reserved per CTA segment (written at each CTA's end)
     uint32_t* seg_pre;       // exclusive prefix of the recorded counts, nseg + 2 entries
     StepCounters* ctr;       // -> nmovers / moved / mover_drop, err
+    // slab stores: particles leaving the slab are written as exchange records
+    // (x y z vx vy vz w id) and leave a hole, as in k_push; not deposited here
+    double* L;               // [2][lcap][8]
+    uint32_t lcap;
+    const uint32_t* off;     // bin offsets, hole counts and lists (push_hole)
+    uint32_t* holes;
+    uint32_t* hl;
 };
 // Upper bound on the fused kernel's CTAs (size of seg_cnt / seg_pre).
 constexpr uint32_t kMaxFusedCtas = 1u << 20;
@@ -45,6 +52,11 @@ constexpr uint32_t kMaxFusedCtas = 1u << 20;
 bool fused_step_available(int order, int kernel);
 void launch_deposit_current_push(int order, const GridD& g, PushCtx& pc, const uint32_t* off,
                                  const uint32_t* cnt, double q, double* j, int num_sms, cudaStream_t st);
+// Slab arrivals (mover records M[base .. base+n), appended by the import)
+// deposited over their full window (RED.ADD.F64): the sender's fused pass
+// left them out.
+void launch_deposit_records(int order, const GridD& g, const Soa& M, const StepCounters* ctr, uint32_t base,
+                            double q, double* j, int num_sms, cudaStream_t st);
 // Movers of the fused kernel: slot -> mover record M[i] (+ hole in the old bin)
 // and their J contribution (RED.ADD.F64).
 void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, const uint32_t* off,

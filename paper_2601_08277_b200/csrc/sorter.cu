@@ -542,6 +542,7 @@ __global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32
     const uint32_t nm = min(ctr->nmovers, mcap) + ctr->nimport;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
         const uint32_t d = mcell[i];
+        if (d == kNoCell) continue;  // a leaver exported by the fused slab step
         const uint32_t lo = off[d];
         const int h = (int)atomicSub(&holes[d], 1u);
         if (h > 0) {
@@ -1325,9 +1326,16 @@ void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
     enqueue_migrate();
 }
 
-void BinStore::enqueue_fused(int order, double q, double* J, double dt, double cap2, cudaEvent_t after_kernel) {
-    if (g.slab) throw Status{PICGPU_ELOGIC, "fused step: not available on a slab store"};
+void BinStore::enqueue_fused(int order, double q, double* J, double dt, double cap2, cudaEvent_t after_kernel,
+                             bool migrate) {
     ensure_movers(std::max<size_t>(size_t(1) << 16, n / 4));
+    if (g.slab) {
+        const size_t want = std::max<size_t>(size_t(1) << 16, n / 4);
+        if (want > lcap) {
+            lrec.ensure(want * 2 * 8 * sizeof(double));
+            lcap = want;
+        }
+    }
     StepCounters* ctr = counters.as<StepCounters>();
     PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
     if (!g.ncells || !n) {
@@ -1338,12 +1346,16 @@ void BinStore::enqueue_fused(int order, double q, double* J, double dt, double c
     segcnt.ensure(((size_t)kMaxFusedCtas + 1) * 4);
     segpre.ensure(((size_t)kMaxFusedCtas + 2) * 4);
     PushCtx pc{A.aos(), dt, cap2, mslot.as<uint32_t>(), mbin.as<uint32_t>(), mcellseg.as<uint32_t>(),
-               mcell.as<uint32_t>(), (uint32_t)mcap, 0u, 0u, 0u, segcnt.as<uint32_t>(), segpre.as<uint32_t>(), ctr};
+               mcell.as<uint32_t>(), (uint32_t)mcap, 0u, 0u, 0u, segcnt.as<uint32_t>(), segpre.as<uint32_t>(), ctr,
+               lrec.as<double>(), (uint32_t)lcap, off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>()};
     launch_deposit_current_push(order, g, pc, d_off(), d_cnt(), q, J, num_sms, st);  // sets nseg, segcap
     fused_nseg = pc.nseg;
     if (after_kernel) PICGPU_CUDA_TRY(cudaEventRecord(after_kernel, st));
     launch_movers(order, g, pc, M.soa(), d_off(), holes.as<uint32_t>(), hl.as<uint32_t>(), q, J, num_sms, st);
-    enqueue_migrate();
+    if (migrate)
+        enqueue_migrate();
+    else
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, ctr, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
 }
 
 void BinStore::push_and_resort(bool push, double dt, double cap2, StepCounters& out) {

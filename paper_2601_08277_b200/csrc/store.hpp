@@ -112,7 +112,10 @@ struct BinStore {
     // ncells, zeroed) receives the whole deposit unless the mover buffer
     // overflows (finish_incremental then re-sorts; the caller re-deposits).
     // `after_kernel` (optional) is recorded between the fused kernel and the movers.
-    void enqueue_fused(int order, double q, double* J, double dt, double cap2, cudaEvent_t after_kernel = nullptr);
+    // migrate = false (slab step_begin): stop after the movers (the arrivals
+    // are imported, deposited and migrated in step_end).
+    void enqueue_fused(int order, double q, double* J, double dt, double cap2, cudaEvent_t after_kernel = nullptr,
+                       bool migrate = true);
     // The same step in two halves around a slab exchange: detect (push +
     // move detection; leavers go to the exchange buffer
     // `lrec`), then migrate (optional arrivals appended to the movers,
