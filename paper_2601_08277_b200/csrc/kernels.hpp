@@ -36,7 +36,6 @@ struct PushCtx {
     uint32_t nseg;           // CTA segments (set by launch_deposit_current_push); segment nseg is
     uint32_t ovcap;          //   the shared overflow segment of ovcap entries at nseg * segcap
     uint32_t* seg_cnt;       // movers reserved per CTA segment (written at each CTA's end)
-    uint32_t* seg_pre;       // exclusive prefix of the recorded counts, nseg + 2 entries
     StepCounters* ctr;       // -> nmovers / moved / mover_drop, err
     // slab stores: particles leaving the slab are written as exchange records
     // (x y z vx vy vz w id) and leave a hole, as in k_push; not deposited here
@@ -46,7 +45,7 @@ struct PushCtx {
     uint32_t* holes;
     uint32_t* hl;
 };
-// Upper bound on the fused kernel's CTAs (size of seg_cnt / seg_pre).
+// Upper bound on the fused kernel's CTAs (size of seg_cnt).
 constexpr uint32_t kMaxFusedCtas = 1u << 20;
 // The fused form exists for the default lane kernel (v3) family only.
 bool fused_step_available(int order, int kernel);

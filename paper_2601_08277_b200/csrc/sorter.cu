@@ -1344,12 +1344,10 @@ void BinStore::enqueue_fused(int order, double q, double* J, double dt, double c
     }
     hl.ensure(capacity * 4 + 4);
     segcnt.ensure(((size_t)kMaxFusedCtas + 1) * 4);
-    segpre.ensure(((size_t)kMaxFusedCtas + 2) * 4);
     PushCtx pc{A.aos(), dt, cap2, mslot.as<uint32_t>(), mbin.as<uint32_t>(), mcellseg.as<uint32_t>(),
-               mcell.as<uint32_t>(), (uint32_t)mcap, 0u, 0u, 0u, segcnt.as<uint32_t>(), segpre.as<uint32_t>(), ctr,
+               mcell.as<uint32_t>(), (uint32_t)mcap, 0u, 0u, 0u, segcnt.as<uint32_t>(), ctr,
                lrec.as<double>(), (uint32_t)lcap, off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>()};
     launch_deposit_current_push(order, g, pc, d_off(), d_cnt(), q, J, num_sms, st);  // sets nseg, segcap
-    fused_nseg = pc.nseg;
     if (after_kernel) PICGPU_CUDA_TRY(cudaEventRecord(after_kernel, st));
     launch_movers(order, g, pc, M.soa(), d_off(), holes.as<uint32_t>(), hl.as<uint32_t>(), q, J, num_sms, st);
     if (migrate)

@@ -68,8 +68,7 @@ struct BinStore {
     DevBuf mcell, ovf, ovf_left;  // mover target cell, overflow list, unplaced overflow
     DevBuf mslot, mbin;       // each mover's slot and old bin (fused step: by CTA segment)
     DevBuf mcellseg;          // fused step: movers' target cells by CTA segment
-    DevBuf segcnt, segpre;    // fused step: movers per CTA segment, their exclusive prefix
-    uint32_t fused_nseg = 0;  // segments of the last fused launch
+    DevBuf segcnt;            // fused step: movers per CTA segment
     DevBuf locks;             // per-bin try-locks of the borrow kernel (always released)
     DevBuf holes;             // per-bin holes in the extent [off, off+cnt) (GPMA gaps)
     DevBuf hl;                // per-bin hole lists, slot-indexed like the bins: bin c's holes
