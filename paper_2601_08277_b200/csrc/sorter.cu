@@ -223,7 +223,10 @@ __global__ void k_gather_sorted(const Soa src, const uint32_t* __restrict__ perm
     copy_particle(src, perm[r], dst, (uint64_t)off[c] + (r - start[c]));
 }
 
-constexpr int BPB = 64;  // bins per CTA for the slot-range kernels
+#ifndef PICGPU_BPB
+#define PICGPU_BPB 64
+#endif
+constexpr int BPB = PICGPU_BPB;  // bins per CTA for the slot-range kernels
 
 // Copy every bin's held particles (slot order kept) from src to dst offsets
 // (Dst = Aos: a new layout of the store; Soa: packed staging).
