@@ -2056,7 +2056,11 @@ namespace {
 template <int ORDER>
 void launch_push_order(const GridD& g, PushCtx& pc, const uint32_t* off, const uint32_t* cnt, double q,
                        double* j, int num_sms, cudaStream_t st) {
+#ifdef PICGPU_J_G8
+    using C3 = std::conditional_t<ORDER == 1, JCfgCic3, JCfgG8>;
+#else
     using C3 = std::conditional_t<ORDER == 1, JCfgCic3, JCfg<ORDER>>;
+#endif
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
     const CAos p(pc.A);
     if constexpr (ORDER != 1) {
@@ -2210,9 +2214,6 @@ bool fused_step_available(int order, int kernel) {
         const char* e = std::getenv("PICGPU_J_LANE");
         return e && std::string(e) == "v1";
     }();
-#ifdef PICGPU_J_G8
-    if (order != 1) return false;
-#endif
     const int k = kernel == kJDefault ? j_variant() : kernel;
     return !v1 && (order == 1 || k == kJLane);
 }
