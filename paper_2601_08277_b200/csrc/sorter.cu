@@ -214,7 +214,27 @@ __global__ void k_u64_to_u32(const unsigned long long* in, uint32_t* out, uint64
     if (i < n) out[i] = (uint32_t)in[i];
 }
 
-__global__ void k_gather_sorted(const Soa src, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ key,
+// Sort keys of a binned store's slots, in storage order: the cell of each
+// particle, ncells for holes and slack (they sort last).
+__global__ void k_slot_keys(const GridD g, const Aos A, uint64_t slots, uint32_t* __restrict__ key, int* err) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= slots) return;
+    const double2 r0 = reinterpret_cast<const double2*>(A.p + s)[0];
+    if (is_gap(r0.x)) {
+        key[s] = g.ncells;
+        return;
+    }
+    const double z = A.p[s].z;
+    if (!finite3(r0.x, r0.y, z)) {
+        raise_error(err, PICGPU_EINVAL);
+        key[s] = 0;
+        return;
+    }
+    key[s] = store_cell(g, r0.x, r0.y, z);
+}
+
+template <class Src>
+__global__ void k_gather_sorted(const Src src, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ key,
                                 const uint32_t* __restrict__ start, const uint32_t* __restrict__ off, const Aos dst,
                                 uint64_t n) {
     const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1150,7 +1170,7 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev, cudaEvent_t
     }
     if (np) {
         if (fields_ready) PICGPU_CUDA_TRY(cudaStreamWaitEvent(st, fields_ready, 0));
-        k_gather_sorted<<<div_up((long long)np, 256), 256, 0, st>>>(b, vals2.as<uint32_t>(), skeys.as<uint32_t>(),
+        k_gather_sorted<Soa><<<div_up((long long)np, 256), 256, 0, st>>>(b, vals2.as<uint32_t>(), skeys.as<uint32_t>(),
                                                                     start.as<uint32_t>(), off.as<uint32_t>(),
                                                                     A.aos(), np);
         note_launch();
@@ -1380,11 +1400,71 @@ void BinStore::push_and_resort(bool push, double dt, double cap2, StepCounters& 
     if (out.err) return;
     // global_sort (sort_policy.hpp:83): stable counting sort of the whole
     // store in storage order, fresh slack
-    compact_to_B();
-    unsigned int h32 = 0;
-    PICGPU_CUDA_TRY(cudaMemcpyAsync(&h32, off2.as<uint32_t>() + nc, 4, cudaMemcpyDeviceToHost, st));
-    PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
-    full_sort_from_B(h32);
+    resort_records();
+}
+
+// global_sort straight from the records: the store's slots in storage order
+// are the packed store's order (holes and slack key ncells and sort last), so
+// a stable radix sort of (cell of slot, slot) followed by a record gather into
+// the fresh layout IS gpma_build's counting sort of the packed store -- with
+// no packing pass and no detour through the SoA staging (C3: the compaction
+// alone was 40 ms).
+void BinStore::resort_records() {
+    const size_t nc = g.ncells;
+    const uint64_t slots = capacity;
+    if (!nc) return;
+    keys.ensure(slots * 4 + 4);
+    vals.ensure(slots * 4 + 4);
+    vals2.ensure(slots * 4 + 4);
+    skeys.ensure(slots * 4 + 4);
+    StepCounters* ctr = counters.as<StepCounters>();
+    PICGPU_CUDA_TRY(cudaMemsetAsync(start.p, 0, nc * 4, st));
+    PICGPU_CUDA_TRY(cudaMemsetAsync(endp.p, 0, nc * 4, st));
+    if (slots) {
+        k_slot_keys<<<div_up((long long)slots, 256), 256, 0, st>>>(g, A.aos(), slots, keys.as<uint32_t>(), &ctr->err);
+        note_launch();
+        k_iota<<<div_up((long long)slots, 256), 256, 0, st>>>(vals.as<uint32_t>(), slots);
+        note_launch();
+        int bits = 1;
+        while (bits < 32 && (1ull << bits) < nc + 1) ++bits;
+        size_t bytes = 0;
+        PICGPU_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.as<uint32_t>(), skeys.as<uint32_t>(),
+                                                        vals.as<uint32_t>(), vals2.as<uint32_t>(), (int64_t)slots, 0,
+                                                        bits, st));
+        cub_tmp.ensure(bytes);
+        PICGPU_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, keys.as<uint32_t>(), skeys.as<uint32_t>(),
+                                                        vals.as<uint32_t>(), vals2.as<uint32_t>(), (int64_t)slots, 0,
+                                                        bits, st));
+        note_launch();
+        if (n) {  // the first n sorted keys are the particles' cells
+            k_boundaries<<<div_up((long long)n, 256), 256, 0, st>>>(skeys.as<uint32_t>(), n, start.as<uint32_t>(),
+                                                                    endp.as<uint32_t>());
+            note_launch();
+        }
+    }
+    k_counts_caps<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(start.as<uint32_t>(), endp.as<uint32_t>(),
+                                                                  (uint32_t)nc, cnt.as<uint32_t>(),
+                                                                  caps.as<uint32_t>(), onepg, min_gap);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+    PICGPU_CUDA_TRY(cudaMemcpyAsync(hcounters, ctr, sizeof(StepCounters), cudaMemcpyDeviceToHost, st));
+    layout_from_counts(n);  // synchronises
+    if (hcounters->err) throw Status{hcounters->err, "cell_of: non-finite particle position"};
+    A2.ensure(capacity_next);
+    k_fill_slack<<<div_up((long long)nc, BPB), 256, 0, st>>>(A2.aos(), off2.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                             (uint32_t)nc);
+    note_launch();
+    if (n) {
+        k_gather_sorted<Aos><<<div_up((long long)n, 256), 256, 0, st>>>(
+            A.aos(), vals2.as<uint32_t>(), skeys.as<uint32_t>(), start.as<uint32_t>(), off2.as<uint32_t>(), A2.aos(), n);
+        note_launch();
+    }
+    PICGPU_CUDA_TRY(cudaGetLastError());
+    swap_aos(A, A2);
+    swap_buf(off, off2);
+    capacity = capacity_next;
+    PICGPU_CUDA_TRY(cudaMemsetAsync(holes.p, 0, nc * 4 + 4, st));  // fresh bins are packed
+    hl.ensure(capacity * 4 + 4);
 }
 
 void BinStore::shift_window(const picgpu_grid& shifted, int ppc, double u_th, uint64_t seed, uint64_t pid0,

@@ -97,6 +97,10 @@ struct BinStore {
     // Re-layout A's bins with fresh slack from the current counts (global_sort
     // on an already-binned store == identity permutation inside bins).
     void relayout();
+    // Full stable re-sort of the binned store by the particles' current cells
+    // (global_sort after a push: gpma_build on the packed store), records
+    // gathered straight into a fresh layout.
+    void resort_records();
     // A's valid particles compacted into B in storage order (bins ascending);
     // returns the packed offsets in `off2` (exclusive scan of cnt).
     void compact_to_B();
