@@ -25,6 +25,14 @@
 //    shared atomics are CAS loops on sm_100a) and flushes each node ONCE:
 //    a plain store for nodes whose every contributing cell lies in this CTA,
 //    a global FP64 reduction (RED.ADD.F64, native in L2) for halo nodes.
+//  * The fused form (launch_deposit_current_push, the default session step)
+//    runs pic::advance (deposit.hpp / simulation.hpp) inside the same pass:
+//    each staged particle is pushed bit-exactly in registers and written back;
+//    a particle that stays in its cell deposits on the register window as
+//    above, a particle that moved one cell has its taps shifted into the old
+//    cell's window where they fit, and is listed in its CTA's mover segment
+//    (shared-memory reservation) for k_movers, which moves its record, leaves
+//    a hole, and deposits the taps outside the window with RED.ADD.F64.
 //
 // J is compared with the reference at 1e-12 peak-normalised; it
 // uses FMA and its own summation order.  Cell location and shape weights are

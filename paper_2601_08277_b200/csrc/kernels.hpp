@@ -23,7 +23,8 @@ void launch_deposit_current(int order, const GridD& g, const CAos& p, const uint
 // deposited on the lane kernel's register window; a particle whose cell changed
 // is listed (slot, old bin, new cell) for launch_movers, which copies it into
 // the mover records, leaves a hole in its old bin and deposits its J with
-// L2 reductions.  Non-slab stores only.
+// L2 reductions.  Slab stores: a particle that left the slab is listed with a
+// kLeaveLeft/kLeaveRight code instead of a cell and exported by launch_movers.
 struct PushCtx {
     Aos A;                   // the binned store (positions are updated in place)
     double dt, cap2;
@@ -37,8 +38,8 @@ struct PushCtx {
     uint32_t ovcap;          //   the shared overflow segment of ovcap entries at nseg * segcap
     uint32_t* seg_cnt;       // movers reserved per CTA segment (written at each CTA's end)
     StepCounters* ctr;       // -> nmovers / moved / mover_drop, err
-    // slab stores: particles leaving the slab are written as exchange records
-    // (x y z vx vy vz w id) and leave a hole, as in k_push; not deposited here
+    // slab stores: launch_movers writes particles that left the slab as exchange
+    // records (x y z vx vy vz w id, by side) and leaves a hole; no deposit here
     double* L;               // [2][lcap][8]
     uint32_t lcap;
     const uint32_t* off;     // bin offsets, hole counts and lists (push_hole)
@@ -57,7 +58,7 @@ void launch_deposit_current_push(int order, const GridD& g, PushCtx& pc, const u
 void launch_deposit_records(int order, const GridD& g, const Soa& M, const StepCounters* ctr, uint32_t base,
                             double q, double* j, int num_sms, cudaStream_t st);
 // Movers of the fused kernel: slot -> mover record M[i] (+ hole in the old bin)
-// and their J contribution (RED.ADD.F64).
+// and their J contribution (RED.ADD.F64); slab leavers -> exchange records.
 void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, const uint32_t* off,
                    uint32_t* holes, uint32_t* hl, double q, double* j, int num_sms, cudaStream_t st);
 
