@@ -313,8 +313,13 @@ __global__ void __launch_bounds__(256) k_fill_slack(const Aos A, const uint32_t*
 #ifndef PICGPU_PUSH_UNR
 #define PICGPU_PUSH_UNR 1
 #endif
+#ifndef PICGPU_PUSH_EARLY_WID
+#define PICGPU_PUSH_EARLY_WID 1
+#endif
 #ifndef PICGPU_PUSH_MINB
-#define PICGPU_PUSH_MINB 5  // record store: 5 CTAs/SM (51 registers, no spill) beats 6 (40, spills): C3 push+sort 54 -> 48 ms
+// record store: 5 CTAs/SM (48 registers) beat 6 (40, spills): C3 push+sort 54 -> 48 ms; with
+// w/id loaded up front (64 registers) 4 CTAs/SM: 48.1 -> 46.0 ms (5 CTAs spill: 50.2 ms)
+#define PICGPU_PUSH_MINB 4
 #endif
 
 // RECORD = false: push and count the moved particles only (the store is
@@ -332,9 +337,11 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
     __syncthreads();
     const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double x = __longlong_as_double(-1LL), y = 0.0, z = 0.0, vx = 0.0, vy = 0.0, vz = 0.0;
-    if (s < slots) {  // x y | z vx | vy vz of the record
+    double2 wid = make_double2(0.0, 0.0);
+    if (s < slots) {  // x y | z vx | vy vz (| w id) of the record
         const double2* r = reinterpret_cast<const double2*>(A.p + s);
         const double2 a = r[0], b = r[1], c = r[2];
+        if (PICGPU_PUSH_EARLY_WID && RECORD) wid = r[3];  // same two sectors; no second round trip for movers
         x = a.x;
         y = a.y;
         z = b.x;
@@ -385,8 +392,9 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
                     double* r = L + ((size_t)dir * lcap + li) * 8;
                     r[0] = x; r[1] = y; r[2] = z;
                     r[3] = vx; r[4] = vy; r[5] = vz;
-                    r[6] = A.p[s].w;
-                    r[7] = __longlong_as_double((long long)A.p[s].id);
+                    if (!PICGPU_PUSH_EARLY_WID) wid = reinterpret_cast<const double2*>(A.p + s)[3];
+                    r[6] = wid.x;
+                    r[7] = wid.y;
                     push_hole(A, s, before, off, holes, hl);
                 } else {
                     raise_error(&ctr->err, PICGPU_ELENGTH);
@@ -413,7 +421,7 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
     if (lidx < 0) return;
     const unsigned idx = s_base + (unsigned)lidx;
     if (idx < mcap) {
-        const double2 wid = reinterpret_cast<const double2*>(A.p + s)[3];
+        if (!PICGPU_PUSH_EARLY_WID) wid = reinterpret_cast<const double2*>(A.p + s)[3];
         M.x[idx] = x;
         M.y[idx] = y;
         M.z[idx] = z;
