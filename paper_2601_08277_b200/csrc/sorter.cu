@@ -12,6 +12,7 @@
 //   global_sort         sort_policy.hpp:83-85 -> BinStore::relayout
 //   advance             workload.hpp:128-155 -> push_one (round-to-nearest intrinsics, bit-identical)
 // The store is an array of 64-byte particle records (common.cuh, Part).
+#include <type_traits>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -243,6 +244,9 @@ __global__ void k_gather_sorted(const Src src, const uint32_t* __restrict__ perm
     copy_particle(src, perm[r], dst, (uint64_t)off[c] + (r - start[c]));
 }
 
+#ifndef PICGPU_RELAYOUT_UNR2
+#define PICGPU_RELAYOUT_UNR2 1
+#endif
 #ifndef PICGPU_BPB
 #define PICGPU_BPB 64
 #endif
@@ -265,7 +269,30 @@ __global__ void __launch_bounds__(256) k_relayout(const Aos src, const uint32_t*
         }
     }
     __syncthreads();
-    for (uint32_t s = so[0] + threadIdx.x; s < so[nb]; s += blockDim.x) {
+    uint32_t s = so[0] + threadIdx.x;
+    if constexpr (PICGPU_RELAYOUT_UNR2 && std::is_same<Dst, Aos>::value) {
+        // two records in flight per thread (the loads of both before either store)
+        for (; s + blockDim.x < so[nb]; s += 2 * blockDim.x) {
+            const uint32_t t = s + blockDim.x;
+            const int b0 = find_bin(so, nb, s), b1 = find_bin(so, nb, t);
+            const uint32_t r0 = s - so[b0], r1 = t - so[b1];
+            const bool k0 = r0 < sc[b0], k1 = r1 < sc[b1];
+            const double2* p0 = reinterpret_cast<const double2*>(src.p + s);
+            const double2* p1 = reinterpret_cast<const double2*>(src.p + t);
+            double2 a0, a1, a2, a3, c0, c1, c2, c3;
+            if (k0) { a0 = p0[0]; a1 = p0[1]; a2 = p0[2]; a3 = p0[3]; }
+            if (k1) { c0 = p1[0]; c1 = p1[1]; c2 = p1[2]; c3 = p1[3]; }
+            if (k0) {
+                double2* d = reinterpret_cast<double2*>(dst.p + (uint64_t)dof[b0] + r0);
+                d[0] = a0; d[1] = a1; d[2] = a2; d[3] = a3;
+            }
+            if (k1) {
+                double2* d = reinterpret_cast<double2*>(dst.p + (uint64_t)dof[b1] + r1);
+                d[0] = c0; d[1] = c1; d[2] = c2; d[3] = c3;
+            }
+        }
+    }
+    for (; s < so[nb]; s += blockDim.x) {
         const int b = find_bin(so, nb, s);
         const uint32_t r = s - so[b];
         if (r < sc[b]) copy_particle(src, s, dst, (uint64_t)dof[b] + r);
