@@ -791,7 +791,7 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
             if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[2], st));
             PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)bs.g.ncells * 24, st));
             if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[3], st));
-            bs.enqueue_fused(s->order, s->q, s->J.as<double>(), dt, cap2, T ? s->ev[4] : nullptr);
+            bs.enqueue_fused(s->order, s->q, s->J.as<double>(), dt, cap2, T ? s->ev[4] : nullptr, true, s->kernel);
             if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
             lj = g_launches.load() - l0;
             StepCounters c{};
@@ -1082,7 +1082,7 @@ int picgpu_session_step_begin(picgpu_session* s, double dt, uint32_t flags, uint
         if (fused) {
             PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)bs.g.ncells * 24, s->st));
             bs.enqueue_fused(s->order, s->q, s->J.as<double>(), dt, cap2, s->timing ? s->ev[4] : nullptr,
-                             /*migrate=*/false);
+                             /*migrate=*/false, s->kernel);
         } else {
             bs.enqueue_detect((flags & PICGPU_STEP_PUSH) != 0, dt, cap2);
         }

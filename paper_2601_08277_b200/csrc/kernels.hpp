@@ -10,9 +10,10 @@ namespace picgpu {
 
 // deposit_current.cu ---------------------------------------------------------
 // J (3*ncells doubles: jx|jy|jz, pre-zeroed) += deposit of the binned store.
-// J kernel families (orders 2 and 3; order 1 always uses the lane kernel):
-// the default register-lane DFMA kernel, the warp-per-pencil "vector" DFMA
-// kernel, and the FP64 tensor-core (DMMA m8n8k4) "matrix" kernel.
+// J kernel families: the register-lane DFMA kernel ("lane", v3, the
+// default), the warp-per-pencil DFMA kernel ("vector", orders 2/3; order 1
+// falls back to the lane kernel) and the FP64 tensor-core DMMA pencil kernel
+// ("matrix", deposit_pencil.cu, every order).
 enum JKernel { kJDefault = -1, kJLane = 0, kJVector = 1, kJMatrix = 2 };
 void launch_deposit_current(int order, const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt,
                             double q, double* j, int num_sms, cudaStream_t st, int kernel = kJDefault);
@@ -51,7 +52,13 @@ constexpr uint32_t kMaxFusedCtas = 1u << 20;
 // The fused form exists for the default lane kernel (v3) family only.
 bool fused_step_available(int order, int kernel);
 void launch_deposit_current_push(int order, const GridD& g, PushCtx& pc, const uint32_t* off,
-                                 const uint32_t* cnt, double q, double* j, int num_sms, cudaStream_t st);
+                                 const uint32_t* cnt, double q, double* j, int num_sms, cudaStream_t st,
+                                 int kernel = kJDefault);
+// deposit_pencil.cu: the DMMA pencil kernel (J only / fused push + detect + J).
+void launch_pencil_current(int order, const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt,
+                           double q, double* j, int num_sms, cudaStream_t st);
+void launch_pencil_current_push(int order, const GridD& g, PushCtx& pc, const uint32_t* off, const uint32_t* cnt,
+                                double q, double* j, int num_sms, cudaStream_t st);
 // Slab arrivals (mover records M[base .. base+n), appended by the import)
 // deposited over their full window (RED.ADD.F64): the sender's fused pass
 // left them out.

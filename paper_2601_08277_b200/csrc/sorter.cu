@@ -1385,7 +1385,7 @@ void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
 }
 
 void BinStore::enqueue_fused(int order, double q, double* J, double dt, double cap2, cudaEvent_t after_kernel,
-                             bool migrate) {
+                             bool migrate, int kernel) {
     ensure_movers(std::max<size_t>(size_t(1) << 16, n / 4));
     if (g.slab) {
         const size_t want = std::max<size_t>(size_t(1) << 16, n / 4);
@@ -1405,7 +1405,7 @@ void BinStore::enqueue_fused(int order, double q, double* J, double dt, double c
     PushCtx pc{A.aos(), dt, cap2, mslot.as<uint32_t>(), mbin.as<uint32_t>(), mcellseg.as<uint32_t>(),
                mcell.as<uint32_t>(), (uint32_t)mcap, 0u, 0u, 0u, segcnt.as<uint32_t>(), ctr,
                lrec.as<double>(), (uint32_t)lcap, off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>()};
-    launch_deposit_current_push(order, g, pc, d_off(), d_cnt(), q, J, num_sms, st);  // sets nseg, segcap
+    launch_deposit_current_push(order, g, pc, d_off(), d_cnt(), q, J, num_sms, st, kernel);  // sets nseg, segcap
     if (after_kernel) PICGPU_CUDA_TRY(cudaEventRecord(after_kernel, st));
     launch_movers(order, g, pc, M.soa(), d_off(), holes.as<uint32_t>(), hl.as<uint32_t>(), q, J, num_sms, st);
     if (migrate)

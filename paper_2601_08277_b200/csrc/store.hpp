@@ -118,7 +118,7 @@ struct BinStore {
     // migrate = false (slab step_begin): stop after the movers (the arrivals
     // are imported, deposited and migrated in step_end).
     void enqueue_fused(int order, double q, double* J, double dt, double cap2, cudaEvent_t after_kernel = nullptr,
-                       bool migrate = true);
+                       bool migrate = true, int kernel = -1);
     // The same step in two halves around a slab exchange: detect (push +
     // move detection; leavers go to the exchange buffer
     // `lrec`), then migrate (optional arrivals appended to the movers,
