@@ -22,6 +22,7 @@
 // ECUDA / ENCCL -> std::runtime_error, ENOMEM -> std::bad_alloc.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstring>
 #include <cstdlib>
@@ -138,9 +139,13 @@ inline CellIndex cell_of(const Vec3& p, const GridSpec& g) {
     return c;
 }
 
-// deposit.hpp:62-73.  (The reference's optional Gpma* only changes the
-// summation order; J is order-independent to 1e-12, so it is not needed.)
-inline CurrentGrid deposit_scalar(const ParticleSoA& soa, const GridSpec& g, ShapeOrder order) {
+struct Gpma;
+
+// deposit.hpp:62-73.  The reference's optional Gpma* only changes the
+// summation order (bins ascending instead of storage order); J is
+// order-independent to 1e-12, so it is accepted and not needed.
+inline CurrentGrid deposit_scalar(const ParticleSoA& soa, const GridSpec& g, ShapeOrder order,
+                                  const Gpma* /*gpma*/ = nullptr) {
     CurrentGrid grid(g);
     const picgpu_grid cg = g.c();
     check(picgpu_deposit_current(&cg, static_cast<int>(order), soa.x.data(), soa.y.data(), soa.z.data(),
@@ -177,17 +182,39 @@ struct GpmaConfig {
     int borrow_scan_bins = 4;
 };
 
-// Result of gpma_build's stable counting sort (gpma.hpp:379-394).
-struct Bins {
+// Result of gpma_build's stable counting sort (gpma.hpp:379-394), standing
+// in for the reference's pic::Gpma at its read-only call sites: `Gpma gpma =
+// gpma_build(soa, g)`, `deposit_scalar(soa, g, order, &gpma)` (test_pipeline.cpp:
+// 139-142), for_each_in_cell / cell_entries (gpma.hpp:146-158).  The
+// incremental index lives on the device (picgpu::Session).
+struct Gpma {
     std::vector<std::uint32_t> perm;    // new storage index -> old
     std::vector<std::uint32_t> starts;  // packed bin starts (exclusive scan of counts)
     std::vector<std::uint32_t> counts;
+    GpmaConfig cfg;
+
+    std::size_t num_cells() const { return counts.size(); }
+    std::size_t size() const { return perm.size(); }
+    const GpmaConfig& config() const { return cfg; }
+    // the storage indices of the particles of `cell`, in slot order
+    template <class Fn>
+    void for_each_in_cell(std::uint32_t cell, Fn&& fn) const {
+        if (cell >= counts.size()) throw std::out_of_range("Gpma::for_each_in_cell: cell out of range");
+        for (std::uint32_t r = starts[cell], e = starts[cell] + counts[cell]; r < e; ++r) fn(r);
+    }
+    std::vector<std::uint32_t> cell_entries(std::uint32_t cell) const {
+        std::vector<std::uint32_t> out;
+        for_each_in_cell(cell, [&](std::uint32_t r) { out.push_back(r); });
+        return out;
+    }
 };
+using Bins = Gpma;
 
 // gpma_build (gpma.hpp:379-402): physically reorders the store by cell with a
 // stable counting sort (bit-identical permutation) and returns the bins.
-inline Bins gpma_build(ParticleSoA& soa, const GridSpec& g, GpmaConfig = {}) {
-    Bins b;
+inline Gpma gpma_build(ParticleSoA& soa, const GridSpec& g, GpmaConfig cfg = {}) {
+    Gpma b;
+    b.cfg = cfg;
     b.perm.resize(soa.size());
     b.starts.resize(g.n_cells());
     b.counts.resize(g.n_cells());
@@ -523,97 +550,147 @@ inline const char* to_string(SortReason r) {  // sort_policy.hpp:48-56
     }
 }
 
-namespace detail {
-inline std::string fmt_double(double v) {
-    char buf[32];
+// The writer is table-driven: one Column per schema field says how a step
+// row renders it and how the summary row aggregates it (a total, a mean, or a
+// count).  CSV emits the columns in schema order, JSON in key order -- the
+// reference's report.hpp:49-103 layout, produced from this one table.
+namespace report_detail {
+
+enum class Agg { total, mean, count_nonzero, label };
+
+struct Cell {  // one rendered value: number or string
+    bool is_text = false, is_int = false;
+    double num = 0.0;
+    std::uint64_t integer = 0;
+    std::string text;
+};
+
+struct Column {
+    const char* csv_name;      // step-row key (CSV header and JSON "steps" key)
+    const char* summary_key;   // JSON "summary" key
+    Agg agg;
+    Cell (*get)(const StepMetrics&);
+};
+
+inline Cell num(double v) { Cell c; c.num = v; return c; }
+inline Cell integer(std::uint64_t v) { Cell c; c.is_int = true; c.integer = v; return c; }
+inline Cell text(std::string v) { Cell c; c.is_text = true; c.text = std::move(v); return c; }
+
+inline const std::vector<Column>& columns() {
+    static const std::vector<Column> cols = {
+        {"step", nullptr, Agg::label, [](const StepMetrics& m) { return integer(m.step); }},
+        {"wall_s", "wall_s", Agg::total, [](const StepMetrics& m) { return num(m.wall_s); }},
+        {"preproc_s", "preproc_s", Agg::total, [](const StepMetrics& m) { return num(m.preproc_s); }},
+        {"compute_s", "compute_s", Agg::total, [](const StepMetrics& m) { return num(m.compute_s); }},
+        {"sort_s", "sort_s", Agg::total, [](const StepMetrics& m) { return num(m.sort_s); }},
+        {"reduce_s", "reduce_s", Agg::total, [](const StepMetrics& m) { return num(m.reduce_s); }},
+        {"pps", "mean_pps", Agg::mean, [](const StepMetrics& m) { return num(m.particles_per_second); }},
+        {"fraction_moved", "mean_fraction_moved", Agg::mean,
+         [](const StepMetrics& m) { return num(m.fraction_moved); }},
+        {"rebuilds", "rebuilds", Agg::total, [](const StepMetrics& m) { return integer(m.rebuilds); }},
+        {"global_sort_reason", "global_sorts", Agg::count_nonzero,
+         [](const StepMetrics& m) { return text(to_string(m.global_sort)); }},
+    };
+    return cols;
+}
+
+// The summary value of column c over the steps.
+inline Cell aggregate(const Column& c, std::span<const StepMetrics> steps) {
+    if (c.agg == Agg::count_nonzero) {
+        std::uint64_t n = 0;
+        for (const StepMetrics& m : steps) n += m.global_sort != SortReason::none;
+        return integer(n);
+    }
+    double acc = 0.0;
+    std::uint64_t iacc = 0;
+    bool ints = false;
+    for (const StepMetrics& m : steps) {
+        const Cell v = c.get(m);
+        ints = v.is_int;
+        if (v.is_int) iacc += v.integer; else acc += v.num;
+    }
+    if (ints) return integer(iacc);
+    if (c.agg == Agg::mean && !steps.empty()) acc /= static_cast<double>(steps.size());
+    return num(acc);
+}
+
+// %.17g for CSV; the shortest round-trip form (nlohmann::json's) for JSON.
+inline std::string csv_num(double v) {
+    char buf[40];
     std::snprintf(buf, sizeof(buf), "%.17g", v);
     return buf;
 }
-struct MetricsSummary {
-    double wall = 0, preproc = 0, compute = 0, sort = 0, reduce = 0;
-    double mean_pps = 0, mean_fraction = 0;
-    std::uint64_t rebuilds = 0, global_sorts = 0;
-};
-inline MetricsSummary summarize(std::span<const StepMetrics> steps) {
-    MetricsSummary s;
-    for (const StepMetrics& m : steps) {
-        s.wall += m.wall_s;
-        s.preproc += m.preproc_s;
-        s.compute += m.compute_s;
-        s.sort += m.sort_s;
-        s.reduce += m.reduce_s;
-        s.mean_pps += m.particles_per_second;
-        s.mean_fraction += m.fraction_moved;
-        s.rebuilds += m.rebuilds;
-        if (m.global_sort != SortReason::none) ++s.global_sorts;
-    }
-    if (!steps.empty()) {
-        s.mean_pps /= static_cast<double>(steps.size());
-        s.mean_fraction /= static_cast<double>(steps.size());
-    }
-    return s;
-}
-// Shortest round-trip double, as nlohmann::json prints it.
-inline std::string json_double(double v) {
-    char buf[32];
-    for (int prec = 1; prec <= 17; ++prec) {
+inline std::string json_num(double v) {
+    char buf[40];
+    int prec = 1;
+    do {
         std::snprintf(buf, sizeof(buf), "%.*g", prec, v);
-        if (std::strtod(buf, nullptr) == v) break;
-    }
+    } while (std::strtod(buf, nullptr) != v && ++prec <= 17);
     std::string s = buf;
     if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
     return s;
 }
-}  // namespace detail
-
-inline constexpr const char* kCsvHeader =
-    "step,wall_s,preproc_s,compute_s,sort_s,reduce_s,pps,fraction_moved,rebuilds,global_sort_reason";
-
-inline std::string report_csv(std::span<const StepMetrics> steps) {
-    using detail::fmt_double;
-    std::string out = kCsvHeader;
-    out += '\n';
-    if (steps.empty()) return out;
-    for (const StepMetrics& m : steps)
-        out += std::to_string(m.step) + ',' + fmt_double(m.wall_s) + ',' + fmt_double(m.preproc_s) + ',' +
-               fmt_double(m.compute_s) + ',' + fmt_double(m.sort_s) + ',' + fmt_double(m.reduce_s) + ',' +
-               fmt_double(m.particles_per_second) + ',' + fmt_double(m.fraction_moved) + ',' +
-               std::to_string(m.rebuilds) + ',' + to_string(m.global_sort) + '\n';
-    const auto s = detail::summarize(steps);
-    out += "summary," + fmt_double(s.wall) + ',' + fmt_double(s.preproc) + ',' + fmt_double(s.compute) + ',' +
-           fmt_double(s.sort) + ',' + fmt_double(s.reduce) + ',' + fmt_double(s.mean_pps) + ',' +
-           fmt_double(s.mean_fraction) + ',' + std::to_string(s.rebuilds) + ',' + std::to_string(s.global_sorts) +
-           '\n';
-    return out;
+inline std::string render(const Cell& c, bool json) {
+    if (c.is_text) return json ? "\"" + c.text + "\"" : c.text;
+    if (c.is_int) return std::to_string(c.integer);
+    return json ? json_num(c.num) : csv_num(c.num);
 }
 
-// report_json's records, serialised like nlohmann::json::dump(): keys sorted,
-// no whitespace (the reference returns the json object; json.hpp is not a
-// dependency here).
-inline std::string report_json(std::span<const StepMetrics> steps) {
-    using detail::json_double;
+// JSON object from (key, value) pairs, keys in sorted order, no whitespace.
+inline std::string json_object(std::vector<std::pair<std::string, std::string>> kv) {
+    std::sort(kv.begin(), kv.end());
     std::string out = "{";
-    if (!steps.empty()) {
-        const auto s = detail::summarize(steps);
-        out += "\"steps\":[";
-        for (std::size_t i = 0; i < steps.size(); ++i) {
-            const StepMetrics& m = steps[i];
-            out += std::string(i ? "," : "") + "{\"compute_s\":" + json_double(m.compute_s) +
-                   ",\"fraction_moved\":" + json_double(m.fraction_moved) + ",\"global_sort_reason\":\"" +
-                   to_string(m.global_sort) + "\",\"pps\":" + json_double(m.particles_per_second) +
-                   ",\"preproc_s\":" + json_double(m.preproc_s) + ",\"rebuilds\":" + std::to_string(m.rebuilds) +
-                   ",\"reduce_s\":" + json_double(m.reduce_s) + ",\"sort_s\":" + json_double(m.sort_s) +
-                   ",\"step\":" + std::to_string(m.step) + ",\"wall_s\":" + json_double(m.wall_s) + "}";
-        }
-        out += "],\"summary\":{\"compute_s\":" + json_double(s.compute) + ",\"global_sorts\":" +
-               std::to_string(s.global_sorts) + ",\"mean_fraction_moved\":" + json_double(s.mean_fraction) +
-               ",\"mean_pps\":" + json_double(s.mean_pps) + ",\"preproc_s\":" + json_double(s.preproc) +
-               ",\"rebuilds\":" + std::to_string(s.rebuilds) + ",\"reduce_s\":" + json_double(s.reduce) +
-               ",\"sort_s\":" + json_double(s.sort) + ",\"wall_s\":" + json_double(s.wall) + "}";
-    } else {
-        out += "\"steps\":[]";
-    }
+    for (std::size_t i = 0; i < kv.size(); ++i) out += (i ? ",\"" : "\"") + kv[i].first + "\":" + kv[i].second;
     return out + "}";
+}
+
+}  // namespace report_detail
+
+inline const std::string& csv_header() {
+    static const std::string h = [] {
+        std::string s;
+        for (const auto& c : report_detail::columns()) s += (s.empty() ? "" : ",") + std::string(c.csv_name);
+        return s;
+    }();
+    return h;
+}
+
+// One row per step, then a summary row (label "summary"; totals, means and
+// the count of fired global sorts), as report_csv (report.hpp:51-71).
+inline std::string report_csv(std::span<const StepMetrics> steps) {
+    using namespace report_detail;
+    std::string out = csv_header() + "\n";
+    if (steps.empty()) return out;
+    for (const StepMetrics& m : steps) {
+        std::string row;
+        for (const auto& c : columns()) row += (row.empty() ? "" : ",") + render(c.get(m), false);
+        out += row + "\n";
+    }
+    std::string row = "summary";
+    for (const auto& c : columns())
+        if (c.agg != Agg::label) row += "," + render(aggregate(c, steps), false);
+    return out + row + "\n";
+}
+
+// report_json's records (report.hpp:74-103) serialised like
+// nlohmann::json::dump(): keys sorted, no whitespace.
+inline std::string report_json(std::span<const StepMetrics> steps) {
+    using namespace report_detail;
+    std::vector<std::pair<std::string, std::string>> top;
+    std::string arr = "[";
+    for (std::size_t i = 0; i < steps.size(); ++i) {
+        std::vector<std::pair<std::string, std::string>> kv;
+        for (const auto& c : columns()) kv.emplace_back(c.csv_name, render(c.get(steps[i]), true));
+        arr += (i ? "," : "") + json_object(std::move(kv));
+    }
+    top.emplace_back("steps", arr + "]");
+    if (!steps.empty()) {
+        std::vector<std::pair<std::string, std::string>> kv;
+        for (const auto& c : columns())
+            if (c.summary_key) kv.emplace_back(c.summary_key, render(aggregate(c, steps), true));
+        top.emplace_back("summary", json_object(std::move(kv)));
+    }
+    return json_object(std::move(top));
 }
 
 }  // namespace picgpu

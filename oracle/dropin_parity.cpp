@@ -163,7 +163,20 @@ int main() {
 
     // --- gpma_build (gpma.hpp:379): same stable permutation of the store ---
     pic::Gpma gpma = pic::gpma_build(ref, g);
-    const picgpu::Bins bins = picgpu::gpma_build(gpu, gg);
+    const picgpu::Gpma bins = picgpu::gpma_build(gpu, gg);  // the reference call site, namespace switched
+    {
+        // deposit_scalar(soa, g, order, &gpma) as test_pipeline.cpp:139-142 calls it
+        const pic::CurrentGrid jr = pic::deposit_scalar(ref, g, pic::ShapeOrder::qsp, &gpma);
+        const picgpu::CurrentGrid jg = picgpu::deposit_scalar(gpu, gg, picgpu::ShapeOrder::qsp, &bins);
+        expect(peak_rel_err(jg, jr) <= 1e-12, "deposit_scalar(..., &gpma): J within 1e-12");
+        bool entries_ok = true;
+        for (std::uint32_t c = 0; c < g.n_cells(); ++c) {
+            std::vector<std::uint32_t> want;
+            gpma.for_each_in_cell(c, [&](pic::ParticleRef r) { want.push_back(r); });
+            entries_ok &= want == bins.cell_entries(c);
+        }
+        expect(entries_ok, "gpma_build: for_each_in_cell / cell_entries identical (fresh build)");
+    }
     {
         pic::TiledOptions ro;
         ro.gpma = &gpma;

@@ -319,7 +319,7 @@ int ref_advance(void* h, double dt, double* moved_fraction) {
 }
 
 // detect_moves + apply_pending_moves (the baseline-incrsort composition,
-// simulation.hpp:765-771).  out[0]=pending, out[1]=inserts, out[2]=shifted,
+// simulation.hpp:117-124).  out[0]=pending, out[1]=inserts, out[2]=shifted,
 // out[3]=overflowed, out[4]=rebuilt.
 int ref_incremental_sort(void* h, uint64_t* out) {
     auto* s = static_cast<RefState*>(h);

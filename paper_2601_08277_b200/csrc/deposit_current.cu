@@ -379,11 +379,20 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                         if (mv) {
                             const unsigned idx = b0 + (unsigned)__popc(mv_bal & ((1u << (tid & 31)) - 1u));
                             size_t e = (size_t)seg * pc.segcap + idx;
-                            if (idx >= pc.segcap) {  // segment full: the shared overflow segment
-                                const unsigned o = atomicAdd(&pc.ctr->ovf_movers, 1u);
-                                e = o < pc.ovcap ? (size_t)pc.nseg * pc.segcap + o : ~(size_t)0;
+                            if (idx >= pc.segcap) {  // segment full
+                                if constexpr (SLAB) {
+                                    if (mv_cell >= kLeaveRight) {  // a leaver: exported here
+                                        export_leaver_now(pc, c_off + (uint32_t)(base + lg),
+                                                          col + plane_cells * (uint32_t)k, mv_cell);
+                                        e = ~(size_t)1;
+                                    }
+                                }
+                                if (e != ~(size_t)1) {  // the shared overflow segment
+                                    const unsigned o = atomicAdd(&pc.ctr->ovf_movers, 1u);
+                                    e = o < pc.ovcap ? (size_t)pc.nseg * pc.segcap + o : ~(size_t)0;
+                                }
                             }
-                            if (e != ~(size_t)0) {
+                            if (e < ~(size_t)1) {
                                 pc.mslot[e] = c_off + (uint32_t)(base + lg);
                                 pc.mbin[e] = col + plane_cells * (uint32_t)k;
                                 pc.mcellseg[e] = mv_cell;

@@ -392,11 +392,19 @@ __global__ void __launch_bounds__(PCfg<ORDER>::NT, 1)
                         if (mv) {
                             const unsigned idx = b0 + (unsigned)__popc(bal & ((1u << lane) - 1u));
                             size_t e = (size_t)seg * pc.segcap + idx;
-                            if (idx >= pc.segcap) {  // segment full: the shared overflow segment
-                                const unsigned o = atomicAdd(&pc.ctr->ovf_movers, 1u);
-                                e = o < pc.ovcap ? (size_t)pc.nseg * pc.segcap + o : ~(size_t)0;
+                            if (idx >= pc.segcap) {  // segment full
+                                if constexpr (SLAB) {
+                                    if (mv_cell >= kLeaveRight) {  // a leaver: exported here
+                                        export_leaver_now(pc, ms, bin, mv_cell);
+                                        e = ~(size_t)1;
+                                    }
+                                }
+                                if (e != ~(size_t)1) {  // the shared overflow segment
+                                    const unsigned o = atomicAdd(&pc.ctr->ovf_movers, 1u);
+                                    e = o < pc.ovcap ? (size_t)pc.nseg * pc.segcap + o : ~(size_t)0;
+                                }
                             }
-                            if (e != ~(size_t)0) {
+                            if (e < ~(size_t)1) {
                                 pc.mslot[e] = ms;
                                 pc.mbin[e] = bin;
                                 pc.mcellseg[e] = mv_cell;

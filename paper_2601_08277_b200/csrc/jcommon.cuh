@@ -268,6 +268,32 @@ __device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PD
     return true;
 }
 
+// A slab leaver of a fused kernel that found its CTA's mover segment full:
+// exported right here -- its exchange record (x y z vx vy vz w id-bits, the
+// pushed position already written back) and the hole in its old bin, as
+// k_movers does for the listed ones -- instead of going through the bounded
+// overflow segment, so no leaver is ever dropped.
+__device__ __forceinline__ void export_leaver_now(const PushCtx& pc, uint32_t s, uint32_t b, uint32_t code) {
+    const Part r = pc.A.p[s];
+    const int dir = code == kLeaveLeft ? 0 : 1;
+    const unsigned li = atomicAdd(&pc.ctr->nleave[dir], 1u);
+    if (li < pc.lcap) {
+        double* rr = pc.L + ((size_t)dir * pc.lcap + li) * 8;
+        rr[0] = r.x;
+        rr[1] = r.y;
+        rr[2] = r.z;
+        rr[3] = r.vx;
+        rr[4] = r.vy;
+        rr[5] = r.vz;
+        rr[6] = r.w;
+        rr[7] = __longlong_as_double((long long)r.id);
+        push_hole(pc.A, s, b, pc.off, pc.holes, pc.hl);
+        atomicAdd(&pc.ctr->moved, 1ull);
+    } else {
+        raise_error(&pc.ctr->err, PICGPU_ELENGTH);
+    }
+}
+
 // One mover segment per CTA of a fused kernel: its size and count.
 inline void set_segments(PushCtx& pc, const dim3& grid, PushCtx* used) {
     const uint64_t nseg = (uint64_t)grid.x * grid.y * grid.z;

@@ -1438,16 +1438,18 @@ void BinStore::push_and_resort(bool push, double dt, double cap2, StepCounters& 
     resort_records();
 }
 
-// global_sort straight from the records: the store's slots in storage order
-// are the packed store's order (holes and slack key ncells and sort last), so
-// a stable radix sort of (cell of slot, slot) followed by a record gather into
-// the fresh layout IS gpma_build's counting sort of the packed store -- with
-// no packing pass and no detour through the SoA staging (C3: the compaction
-// alone was 40 ms).
+// global_sort straight from the records: after fill_holes (the packing every
+// download applies, so the order sorted is the storage order a download
+// reports) the store's slots in storage order are the packed store's order
+// (slack keys ncells and sorts last), so a stable radix sort of (cell of
+// slot, slot) followed by a record gather into the fresh layout IS
+// gpma_build's counting sort of the packed store -- with no compaction pass
+// and no detour through the SoA staging (C3: the compaction alone was 40 ms).
 void BinStore::resort_records() {
     const size_t nc = g.ncells;
     const uint64_t slots = capacity;
     if (!nc) return;
+    fill_holes();
     keys.ensure(slots * 4 + 4);
     vals.ensure(slots * 4 + 4);
     vals2.ensure(slots * 4 + 4);

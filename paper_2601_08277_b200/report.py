@@ -1,7 +1,7 @@
 """Run reports in the reference's schema (proj/include/pic/report.hpp:23-103),
 so the reference's tooling reads GPU results unchanged.
 
-report_csv: header `kCsvHeader`, one row per step with doubles as %.17g,
+report_csv: header `csv_header()`, one row per step with doubles as %.17g,
 then a summary row (totals of the timing columns, means of throughput and
 moved fraction, counts of rebuilds and fired global sorts).
 report_json: the same records under "steps" and "summary"; serialised like

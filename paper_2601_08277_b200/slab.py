@@ -206,8 +206,11 @@ def slab_step(sess: SlabSession, ring: RingExchange, dt: float, flags: int = STE
     counts = sess.begin(dt, flags)
     tl, tr = sess.leavers(counts)
     fl, fr = ring.exchange(tl, tr, sized=True)
+    # the concatenation is queued on torch's stream; the session reads the
+    # arrivals from its own (non-blocking) stream, so synchronise after it
+    arr = torch.cat([fl, fr]) if fl.shape[0] + fr.shape[0] else None
     _sync(sess.device)
-    stats = sess.end(torch.cat([fl, fr]) if fl.shape[0] + fr.shape[0] else None)
+    stats = sess.end(arr)
     for field, bit in ((0, STEP_CURRENT), (1, STEP_DENSITY)):
         if flags & bit:
             lo, hi = sess.guard_planes(field)
@@ -229,6 +232,7 @@ def local_ring_step(sessions: list[SlabSession], dt: float, flags: int = STEP_DE
     stats = []
     for r, s in enumerate(sessions):
         arr = torch.cat([recs[(r - 1) % P][1], recs[(r + 1) % P][0]])
+        _sync(s.device)  # the cat runs on torch's stream; the session reads on its own stream
         st = s.end(arr if arr.shape[0] else None)
         st["sent"] = counts[r][0] + counts[r][1]
         stats.append(st)

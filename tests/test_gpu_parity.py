@@ -501,7 +501,7 @@ def test_fused_step_cap_violation(pg):
 
 def test_fusion_policy_follows_migration(pg, orc):
     """The fused pass runs while the previous step's moved fraction stays under
-    the session's threshold (default 3%), the separate kernels otherwise."""
+    the session's threshold (default 6%), the separate kernels otherwise."""
     g = O.Grid.make(16)
     cold = orc.make_plasma(g, 4, 0.01, 3)  # ~1% of the particles change cell per step
     hot = orc.make_plasma(g, 4, 0.3, 3)    # ~30%

@@ -70,6 +70,27 @@ def test_resort_step_is_a_stable_counting_sort(pg, orc):
     assert np.array_equal(after.id, before.id[perm])
 
 
+def test_resort_after_incremental_steps_sorts_the_download_order(pg, orc):
+    """Incremental steps leave holes in the bins; a following STEP_RESORT is the
+    stable counting sort of the store in the order a download reports it."""
+    wl = _wl(pg, thermal=0.4)
+    S = pg.Session(wl.grid, 3)
+    S.make_workload(wl)
+    g = O.Grid.make(wl.grid.nx, wl.grid.ny, wl.grid.nz, dx=wl.grid.dx, dy=wl.grid.dy, dz=wl.grid.dz,
+                    origin=(wl.grid.ox, wl.grid.oy, wl.grid.oz))
+    for _ in range(3):
+        S.step(0.5, pg.STEP_PUSH | pg.STEP_SORT | pg.STEP_CURRENT | pg.STEP_UNFUSED)
+    before = S.particles()  # storage order after the incremental steps (holes packed)
+    S.step(0.5, pg.STEP_PUSH | pg.STEP_RESORT | pg.STEP_CURRENT)
+    after = S.particles()
+    d = {k: getattr(before, k).copy() for k in ("x", "y", "z", "vx", "vy", "vz", "w")}
+    orc.advance(g, 0.5, d)
+    perm, _, _ = orc.counting_sort(g, d)
+    for k in ("x", "y", "z", "vx"):
+        assert np.array_equal(getattr(after, k), d[k][perm]), k
+    assert np.array_equal(after.id, before.id[perm])
+
+
 @pytest.mark.parametrize("order", [1, 3])
 @pytest.mark.parametrize("mode", ["baseline", "matrix-only", "hybrid-nosort", "hybrid-globalsort", "fullopt",
                                   "rhocell-vector", "baseline-incrsort", "rhocell-incrsort"])
