@@ -189,6 +189,8 @@ class Reference:
         L.ref_bins.argtypes = [_p, _p, _p]
         L.ref_gpma_stats.argtypes = [_p, _p, _p]
         L.ref_gpma_stats.restype = None
+        L.ref_step_timed.argtypes = [_p, C.c_int, _d, _p, _p]
+        L.ref_density_timed.argtypes = [_p, C.c_int, _p]
         L.ref_cell_of.argtypes = [C.POINTER(Grid), _d, _d, _d, _p, _p]
         L.ref_intra_cell.argtypes = [C.POINTER(Grid), _d, _d, _d, _p]
         L.ref_shape_1d.argtypes = [C.c_int, _d, _p]
@@ -321,6 +323,19 @@ class RefState:
         out = np.zeros(5, np.uint64)
         self.ref._check(self.ref.L.ref_incremental_sort(self.h, _ptr(out)))
         return dict(zip(("pending", "inserts", "shifted", "overflowed", "rebuilt"), (int(v) for v in out)))
+
+    def step_timed(self, order, dt):
+        """One baseline-incrsort step (simulation.hpp:117-136) timed per stage by
+        the reference's pic::Timer: (advance_s, sort_s, deposit_s, movers, rebuilt)."""
+        secs = np.zeros(3)
+        out = np.zeros(2, np.uint64)
+        self.ref._check(self.ref.L.ref_step_timed(self.h, order, dt, _ptr(secs), _ptr(out)))
+        return float(secs[0]), float(secs[1]), float(secs[2]), int(out[0]), int(out[1])
+
+    def density_timed(self, order):
+        secs = np.zeros(1)
+        self.ref._check(self.ref.L.ref_density_timed(self.h, order, _ptr(secs)))
+        return float(secs[0])
 
     def bins(self):
         bin_of = np.zeros(self.n, np.uint32)

@@ -335,6 +335,44 @@ int ref_incremental_sort(void* h, uint64_t* out) {
     });
 }
 
+// One baseline-incrsort step of the reference (simulation.hpp:117-136), each
+// stage timed with the reference's own pic::Timer: secs[0] = advance,
+// secs[1] = detect_moves + apply_pending_moves, secs[2] = deposit_scalar over
+// the Gpma's bins.  out[0] = movers, out[1] = rebuilt.  No copies.
+int ref_step_timed(void* h, int order, double dt, double* secs, uint64_t* out) {
+    auto* s = static_cast<RefState*>(h);
+    return guarded([&] {
+        if (!s->has_gpma) throw std::logic_error("ref_step_timed: no gpma");
+        const pic::ShapeOrder so = to_order(order);
+        pic::Timer t0;
+        pic::advance(s->soa, dt, s->grid);
+        secs[0] = t0.elapsed();
+        pic::Timer t1;
+        auto pending = s->gpma.detect_moves(s->soa, s->grid);
+        const uint64_t np = pending.size();
+        const pic::ApplyMovesResult r = pic::apply_pending_moves(s->gpma, pending);
+        secs[1] = t1.elapsed();
+        pic::Timer t2;
+        const pic::CurrentGrid cg = pic::deposit_scalar(s->soa, s->grid, so, &s->gpma);
+        secs[2] = t2.elapsed();
+        if (cg.jx.empty()) throw std::logic_error("empty grid");
+        if (out) { out[0] = np; out[1] = r.rebuilt ? 1 : 0; }
+    });
+}
+
+// pic::deposit_density of q*w, timed (seconds), no copy-out.
+int ref_density_timed(void* h, int order, double* secs) {
+    auto* s = static_cast<RefState*>(h);
+    return guarded([&] {
+        std::vector<double> qw(s->soa.size());
+        for (std::size_t p = 0; p < qw.size(); ++p) qw[p] = s->soa.q * s->soa.w[p];
+        pic::Timer t;
+        const std::vector<double> r = pic::deposit_density(s->soa, s->grid, to_order(order), qw);
+        *secs = t.elapsed();
+        if (r.empty()) throw std::logic_error("empty grid");
+    });
+}
+
 // bin_of[p] = cell whose bin holds storage index p (UINT32_MAX if none).
 int ref_bins(void* h, uint32_t* bin_of, uint32_t* bin_len) {
     auto* s = static_cast<RefState*>(h);

@@ -25,3 +25,7 @@ def test_reference_arm_prints_the_contract_line():
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["workload"].startswith("C2")
+    # same-config, one-core reference
+    assert d["same_config"] is True and d["cpu_baseline"]["cores"] == 1
+    assert "128x128x128 x 16 ppc" in d["cpu_baseline"]["sample"] and "1 core" in d["cpu_baseline"]["sample"]
+    assert d["cpu_detail"]["order"] == 3 and d["cpu_detail"]["nproc"] >= 1 and d["cpu_detail"]["model"]
