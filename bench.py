@@ -319,6 +319,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--order", type=int, default=None, choices=[1, 2, 3], help="override the config's shape order")
     ap.add_argument("--no-orders", dest="orders", action="store_false",
                     help="skip the per-order (1/2/3) runs on the same box")
     ap.add_argument("--slab", action="store_true", help="use the slab-decomposed path even at N=1 (loopback ring)")
@@ -327,6 +328,10 @@ def main():
                          "sort of the store every step (global_sort each step; the crossover study of C3)")
     args = ap.parse_args()
     nx, ppc, order, u_th, dt, default_steps, desc = CONFIGS[args.config]
+    if args.order is not None and args.order != order:
+        order = args.order
+        desc += f" [shape order overridden: {order}]"
+        CONFIGS[args.config] = (nx, ppc, order, u_th, dt, default_steps, desc)
     if args.steps is None:
         args.steps = default_steps
     args.warmup = max(args.warmup, 3)

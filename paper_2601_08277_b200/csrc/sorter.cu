@@ -2,7 +2,8 @@
 // full stable re-sort), the bit-exact push and the device plasma generator.
 //
 // Reference anchors (proj/include/pic/):
-//   gpma_build          gpma.hpp:379-402  -> BinStore::full_sort_from_B (stable radix sort by cell)
+//   gpma_build          gpma.hpp:379-402  -> BinStore::full_sort_from_B (stable radix sort by cell,
+//                                            radix_sort.cu)
 //   Gpma::layout        gpma.hpp:269-302  -> k_counts_caps + scan (same capacity rule)
 //   detect_moves        gpma.hpp:162-177  -> k_push + k_departures (unfused step: departures leave
 //                                            holes), or the fused J pass + k_movers (deposit_current.cu)
@@ -13,7 +14,6 @@
 //   advance             workload.hpp:128-155 -> push_one (round-to-nearest intrinsics, bit-identical)
 // The store is an array of 64-byte particle records (common.cuh, Part).
 #include <type_traits>
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -161,11 +161,6 @@ __global__ void k_cells(const GridD g, const double* __restrict__ x, const doubl
         return;
     }
     cell[p] = c;
-}
-
-__global__ void k_iota(uint32_t* v, uint64_t n) {
-    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) v[p] = (uint32_t)p;
 }
 
 // Run boundaries of the sorted keys: start[c] = first rank, endp[c] = last rank + 1.
@@ -1091,15 +1086,6 @@ void launch_make_workload(const GridD& g, int ppc, double vth, int drift, const 
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
-void cub_exclusive_sum_u32_to_u64(const uint32_t* in, unsigned long long* out, size_t n, DevBuf& tmp,
-                                  cudaStream_t st) {
-    size_t bytes = 0;
-    PICGPU_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)n, st));
-    tmp.ensure(bytes);
-    PICGPU_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, (int64_t)n, st));
-    note_launch();
-}
-
 // ---------------------------------------------------------------------------
 // BinStore
 
@@ -1143,7 +1129,7 @@ void BinStore::layout_from_counts(uint64_t) {
     const size_t nc = g.ncells;
     DevBuf& off64 = keys2;  // scratch: (nc+1) u64
     off64.ensure((nc + 1) * 8);
-    cub_exclusive_sum_u32_to_u64(caps.as<uint32_t>(), off64.as<unsigned long long>(), nc + 1, cub_tmp, st);
+    exclusive_sum_u32_to_u64(caps.as<uint32_t>(), off64.as<unsigned long long>(), nc + 1, sort_tmp, st);
     unsigned long long total = 0;
     PICGPU_CUDA_TRY(cudaMemcpyAsync(&total, off64.as<unsigned long long>() + nc, 8, cudaMemcpyDeviceToHost, st));
     PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1163,27 +1149,18 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev, cudaEvent_t
     vals2.ensure(np * 4 + 4);
     skeys.ensure(np * 4 + 4);
     const Soa b = B.soa();
+    uint32_t *sk = skeys.as<uint32_t>(), *sv = vals2.as<uint32_t>();  // sorted keys / permutation
     StepCounters* ctr = counters.as<StepCounters>();
     PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
     PICGPU_CUDA_TRY(cudaMemsetAsync(start.p, 0, nc * 4, st));
     PICGPU_CUDA_TRY(cudaMemsetAsync(endp.p, 0, nc * 4, st));
     if (np) {
         launch_cells(g, b.x, b.y, b.z, np, keys.as<uint32_t>(), &ctr->err, st);
-        k_iota<<<div_up((long long)np, 256), 256, 0, st>>>(vals.as<uint32_t>(), np);
-        note_launch();
         int bits = 1;
         while (bits < 32 && (1ull << bits) < nc) ++bits;
-        size_t bytes = 0;
-        PICGPU_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.as<uint32_t>(), skeys.as<uint32_t>(),
-                                                        vals.as<uint32_t>(), vals2.as<uint32_t>(), (int64_t)np, 0,
-                                                        bits, st));
-        cub_tmp.ensure(bytes);
-        PICGPU_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, keys.as<uint32_t>(), skeys.as<uint32_t>(),
-                                                        vals.as<uint32_t>(), vals2.as<uint32_t>(), (int64_t)np, 0,
-                                                        bits, st));
-        note_launch();
-        k_boundaries<<<div_up((long long)np, 256), 256, 0, st>>>(skeys.as<uint32_t>(), np, start.as<uint32_t>(),
-                                                                 endp.as<uint32_t>());
+        radix_sort_pairs(keys.as<uint32_t>(), skeys.as<uint32_t>(), nullptr, vals.as<uint32_t>(),
+                         vals2.as<uint32_t>(), np, bits, sort_tmp, st, &sk, &sv);
+        k_boundaries<<<div_up((long long)np, 256), 256, 0, st>>>(sk, np, start.as<uint32_t>(), endp.as<uint32_t>());
         note_launch();
     }
     k_counts_caps<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(start.as<uint32_t>(), endp.as<uint32_t>(),
@@ -1205,13 +1182,11 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev, cudaEvent_t
     }
     if (np) {
         if (fields_ready) PICGPU_CUDA_TRY(cudaStreamWaitEvent(st, fields_ready, 0));
-        k_gather_sorted<Soa><<<div_up((long long)np, 256), 256, 0, st>>>(b, vals2.as<uint32_t>(), skeys.as<uint32_t>(),
-                                                                    start.as<uint32_t>(), off.as<uint32_t>(),
-                                                                    A.aos(), np);
+        k_gather_sorted<Soa><<<div_up((long long)np, 256), 256, 0, st>>>(b, sv, sk, start.as<uint32_t>(),
+                                                                    off.as<uint32_t>(), A.aos(), np);
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
-        if (perm_out_dev)
-            PICGPU_CUDA_TRY(cudaMemcpyAsync(perm_out_dev, vals2.p, np * 4, cudaMemcpyDeviceToDevice, st));
+        if (perm_out_dev) PICGPU_CUDA_TRY(cudaMemcpyAsync(perm_out_dev, sv, np * 4, cudaMemcpyDeviceToDevice, st));
     }
     capacity = capacity_next;
     n = np;
@@ -1263,7 +1238,7 @@ void BinStore::compact_to_B() {
     note_launch();
     DevBuf& off64 = keys2;
     off64.ensure((nc + 1) * 8);
-    cub_exclusive_sum_u32_to_u64(held.as<uint32_t>(), off64.as<unsigned long long>(), nc + 1, cub_tmp, st);
+    exclusive_sum_u32_to_u64(held.as<uint32_t>(), off64.as<unsigned long long>(), nc + 1, sort_tmp, st);
     k_u64_to_u32<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(off64.as<unsigned long long>(),
                                                                  off2.as<uint32_t>(), nc + 1);
     note_launch();
@@ -1454,28 +1429,19 @@ void BinStore::resort_records() {
     vals.ensure(slots * 4 + 4);
     vals2.ensure(slots * 4 + 4);
     skeys.ensure(slots * 4 + 4);
+    uint32_t *sk = skeys.as<uint32_t>(), *sv = vals2.as<uint32_t>();  // sorted keys / slot permutation
     StepCounters* ctr = counters.as<StepCounters>();
     PICGPU_CUDA_TRY(cudaMemsetAsync(start.p, 0, nc * 4, st));
     PICGPU_CUDA_TRY(cudaMemsetAsync(endp.p, 0, nc * 4, st));
     if (slots) {
         k_slot_keys<<<div_up((long long)slots, 256), 256, 0, st>>>(g, A.aos(), slots, keys.as<uint32_t>(), &ctr->err);
         note_launch();
-        k_iota<<<div_up((long long)slots, 256), 256, 0, st>>>(vals.as<uint32_t>(), slots);
-        note_launch();
         int bits = 1;
         while (bits < 32 && (1ull << bits) < nc + 1) ++bits;
-        size_t bytes = 0;
-        PICGPU_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.as<uint32_t>(), skeys.as<uint32_t>(),
-                                                        vals.as<uint32_t>(), vals2.as<uint32_t>(), (int64_t)slots, 0,
-                                                        bits, st));
-        cub_tmp.ensure(bytes);
-        PICGPU_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, keys.as<uint32_t>(), skeys.as<uint32_t>(),
-                                                        vals.as<uint32_t>(), vals2.as<uint32_t>(), (int64_t)slots, 0,
-                                                        bits, st));
-        note_launch();
+        radix_sort_pairs(keys.as<uint32_t>(), skeys.as<uint32_t>(), nullptr, vals.as<uint32_t>(),
+                         vals2.as<uint32_t>(), slots, bits, sort_tmp, st, &sk, &sv);
         if (n) {  // the first n sorted keys are the particles' cells
-            k_boundaries<<<div_up((long long)n, 256), 256, 0, st>>>(skeys.as<uint32_t>(), n, start.as<uint32_t>(),
-                                                                    endp.as<uint32_t>());
+            k_boundaries<<<div_up((long long)n, 256), 256, 0, st>>>(sk, n, start.as<uint32_t>(), endp.as<uint32_t>());
             note_launch();
         }
     }
@@ -1492,8 +1458,8 @@ void BinStore::resort_records() {
                                                              (uint32_t)nc);
     note_launch();
     if (n) {
-        k_gather_sorted<Aos><<<div_up((long long)n, 256), 256, 0, st>>>(
-            A.aos(), vals2.as<uint32_t>(), skeys.as<uint32_t>(), start.as<uint32_t>(), off2.as<uint32_t>(), A2.aos(), n);
+        k_gather_sorted<Aos><<<div_up((long long)n, 256), 256, 0, st>>>(A.aos(), sv, sk, start.as<uint32_t>(),
+                                                                         off2.as<uint32_t>(), A2.aos(), n);
         note_launch();
     }
     PICGPU_CUDA_TRY(cudaGetLastError());
@@ -1518,7 +1484,7 @@ void BinStore::shift_window(const picgpu_grid& shifted, int ppc, double u_th, ui
     note_launch();
     DevBuf& tot64 = vals;  // particles of the new layout: sum of the new counts
     tot64.ensure((nc + 1) * 8);
-    cub_exclusive_sum_u32_to_u64(cnt2.as<uint32_t>(), tot64.as<unsigned long long>(), nc + 1, cub_tmp, st);
+    exclusive_sum_u32_to_u64(cnt2.as<uint32_t>(), tot64.as<unsigned long long>(), nc + 1, sort_tmp, st);
     unsigned long long nnew = 0;
     PICGPU_CUDA_TRY(cudaMemcpyAsync(&nnew, tot64.as<unsigned long long>() + nc, 8, cudaMemcpyDeviceToHost, st));
     k_caps_from_cnt<<<div_up((long long)nc + 1, 256), 256, 0, st>>>(cnt2.as<uint32_t>(), (uint32_t)nc,

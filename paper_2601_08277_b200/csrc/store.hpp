@@ -63,7 +63,7 @@ struct BinStore {
     SoaBuf B;                 // packed staging: uploads, generators, downloads, full re-sorts
     DevBuf off, cnt, off2;    // off: ncells+1 (u32), cnt: ncells (u32)
     DevBuf cnt2;              // counts of a layout being built (moving window)
-    DevBuf keys, keys2, skeys, vals, vals2, start, endp, caps, cub_tmp;
+    DevBuf keys, keys2, skeys, vals, vals2, start, endp, caps, sort_tmp;
     SoaBuf M;                 // mover records
     DevBuf mcell, ovf, ovf_left;  // mover target cell, overflow list, unplaced overflow
     DevBuf mslot, mbin;       // each mover's slot and old bin (fused step: by CTA segment)
@@ -152,6 +152,15 @@ struct BinStore {
     uint64_t capacity_next = 0;
 };
 
-void cub_exclusive_sum_u32_to_u64(const uint32_t* in, unsigned long long* out, size_t n, DevBuf& tmp, cudaStream_t st);
+// radix_sort.cu: out[i] = sum(in[0..i)) (n entries)
+void exclusive_sum_u32_to_u64(const uint32_t* in, unsigned long long* out, size_t n, DevBuf& tmp, cudaStream_t st);
+// Stable LSD radix sort of n (key, value) pairs on the low `bits` key bits.
+// keys and keys_alt are both overwritten (ping-pong); vals_in == nullptr means
+// the values are the indices 0..n-1 (a permutation results); vals / vals_alt
+// receive the value ping-pong (vals_in itself is never written).  The sorted
+// keys / values are returned in *keys_out / *vals_out (one of the buffers).
+void radix_sort_pairs(uint32_t* keys, uint32_t* keys_alt, const uint32_t* vals_in, uint32_t* vals,
+                      uint32_t* vals_alt, uint64_t n, int bits, DevBuf& tmp, cudaStream_t st, uint32_t** keys_out,
+                      uint32_t** vals_out);
 
 }  // namespace picgpu
