@@ -303,15 +303,16 @@ void exclusive_sum_u32_to_u64(const uint32_t* in, unsigned long long* out, size_
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
-void radix_sort_pairs(uint32_t* keys, uint32_t* keys_alt, const uint32_t* vals_in, uint32_t* vals, uint32_t* vals_alt,
-                      uint64_t n, int bits, DevBuf& tmp, cudaStream_t st, uint32_t** keys_out, uint32_t** vals_out) {
+void radix_sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, uint32_t* keys_tmp, const uint32_t* vals_in,
+                      uint32_t* vals_out, uint32_t* vals_tmp, uint64_t n, int bits, DevBuf& tmp, cudaStream_t st) {
     const int passes = std::max(1, (bits + 7) / 8);
     if (passes > RS_MAX_PASSES) throw Status{PICGPU_ELENGTH, "radix sort: keys wider than 32 bits"};
     const uint64_t tiles = (n + RS_TILE - 1) / RS_TILE;
     if (tiles >= (1ull << 31)) throw Status{PICGPU_ELENGTH, "radix sort: too many keys"};
-    // workspace: histograms (u32), digit bases (u64), tile counter, look-back status (u64)
+    if (!n) return;
+    // workspace: histograms (u32), digit bases (u64), tile counters, look-back status (u64)
     const size_t hist_b = RS_MAX_PASSES * RS_RADIX * 4, dbase_b = RS_MAX_PASSES * RS_RADIX * 8, ctr_b = 256;
-    const size_t status_b = std::max<uint64_t>(tiles, 1) * RS_RADIX * 8;
+    const size_t status_b = tiles * RS_RADIX * 8;
     tmp.ensure(hist_b + dbase_b + ctr_b * RS_MAX_PASSES + status_b);
     char* w = tmp.as<char>();
     uint32_t* ghist = reinterpret_cast<uint32_t*>(w);
@@ -319,32 +320,32 @@ void radix_sort_pairs(uint32_t* keys, uint32_t* keys_alt, const uint32_t* vals_i
     uint32_t* tctr = reinterpret_cast<uint32_t*>(w + hist_b + dbase_b);
     unsigned long long* status = reinterpret_cast<unsigned long long*>(w + hist_b + dbase_b + ctr_b * RS_MAX_PASSES);
     PICGPU_CUDA_TRY(cudaMemsetAsync(w, 0, hist_b + dbase_b + ctr_b * RS_MAX_PASSES, st));
-    if (n) {
-        static int max_hist_ctas[64] = {};
-        int dev = 0;
-        PICGPU_CUDA_TRY(cudaGetDevice(&dev));
-        if (!max_hist_ctas[dev & 63]) {
-            int sms = 148;
-            PICGPU_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            PICGPU_CUDA_TRY(cudaFuncSetAttribute(k_rs_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)sizeof(RsShared)));
-            PICGPU_CUDA_TRY(cudaFuncSetAttribute(k_rs_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)sizeof(RsShared)));
-            max_hist_ctas[dev & 63] = sms * 4;
-        }
-        const uint64_t hist_ctas = std::min<uint64_t>((n + RS_THREADS * 4 - 1) / (RS_THREADS * 4),
-                                                      (uint64_t)max_hist_ctas[dev & 63]);
-        k_rs_hist<<<(unsigned)hist_ctas, RS_THREADS, 0, st>>>(keys, n, passes, ghist);
-        k_rs_digit_scan<<<1, RS_RADIX, 0, st>>>(ghist, passes, dbase);
-        note_launch(2);
+    static int hist_ctas[64] = {};
+    int dev = 0;
+    PICGPU_CUDA_TRY(cudaGetDevice(&dev));
+    if (!hist_ctas[dev & 63]) {  // per device (one process may drive several GPUs)
+        int sms = 148;
+        PICGPU_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(k_rs_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(RsShared)));
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(k_rs_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(RsShared)));
+        hist_ctas[dev & 63] = sms * 4;
     }
-    uint32_t *kin = keys, *kout = keys_alt;
+    const uint64_t hctas = std::min<uint64_t>((n + RS_THREADS * 4 - 1) / (RS_THREADS * 4), (uint64_t)hist_ctas[dev & 63]);
+    k_rs_hist<<<(unsigned)hctas, RS_THREADS, 0, st>>>(keys_in, n, passes, ghist);
+    k_rs_digit_scan<<<1, RS_RADIX, 0, st>>>(ghist, passes, dbase);
+    note_launch(2);
+    // pass p writes the *_out buffers when (passes - 1 - p) is even, so the last
+    // pass always lands in keys_out / vals_out; the inputs are never written
+    const uint32_t* kin = keys_in;
     const uint32_t* vin = vals_in;
-    uint32_t* vout = vals_alt;
-    uint32_t* vspare = vals;
-    for (int p = 0; p < passes && n; ++p) {
+    for (int p = 0; p < passes; ++p) {
+        const bool to_out = ((passes - 1 - p) & 1) == 0;
+        uint32_t* kout = to_out ? keys_out : keys_tmp;
+        uint32_t* vout = to_out ? vals_out : vals_tmp;
         PICGPU_CUDA_TRY(cudaMemsetAsync(status, 0, status_b, st));
-        if (p == 0 && !vals_in)
+        if (!vin)
             k_rs_pass<true><<<(unsigned)tiles, RS_THREADS, sizeof(RsShared), st>>>(
                 kin, nullptr, kout, vout, n, 8 * p, dbase + p * RS_RADIX, status, tctr + p * (ctr_b / 4));
         else
@@ -352,14 +353,9 @@ void radix_sort_pairs(uint32_t* keys, uint32_t* keys_alt, const uint32_t* vals_i
                 kin, vin, kout, vout, n, 8 * p, dbase + p * RS_RADIX, status, tctr + p * (ctr_b / 4));
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
-        std::swap(kin, kout);
-        // values ping-pong between vals_alt and vals (the caller's input, if any, is never written)
-        uint32_t* written = vout;
-        vout = (written == vals_alt) ? vspare : vals_alt;
-        vin = written;
+        kin = kout;
+        vin = vout;
     }
-    *keys_out = kin;
-    *vals_out = const_cast<uint32_t*>(vin);
 }
 
 }  // namespace picgpu

@@ -1149,7 +1149,7 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev, cudaEvent_t
     vals2.ensure(np * 4 + 4);
     skeys.ensure(np * 4 + 4);
     const Soa b = B.soa();
-    uint32_t *sk = skeys.as<uint32_t>(), *sv = vals2.as<uint32_t>();  // sorted keys / permutation
+    const uint32_t *sk = skeys.as<uint32_t>(), *sv = vals2.as<uint32_t>();  // sorted keys / permutation
     StepCounters* ctr = counters.as<StepCounters>();
     PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
     PICGPU_CUDA_TRY(cudaMemsetAsync(start.p, 0, nc * 4, st));
@@ -1158,8 +1158,9 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev, cudaEvent_t
         launch_cells(g, b.x, b.y, b.z, np, keys.as<uint32_t>(), &ctr->err, st);
         int bits = 1;
         while (bits < 32 && (1ull << bits) < nc) ++bits;
-        radix_sort_pairs(keys.as<uint32_t>(), skeys.as<uint32_t>(), nullptr, vals.as<uint32_t>(),
-                         vals2.as<uint32_t>(), np, bits, sort_tmp, st, &sk, &sv);
+        keys2.ensure(np * 4 + 4);
+        radix_sort_pairs(keys.as<uint32_t>(), skeys.as<uint32_t>(), keys2.as<uint32_t>(), nullptr, vals2.as<uint32_t>(),
+                         vals.as<uint32_t>(), np, bits, sort_tmp, st);
         k_boundaries<<<div_up((long long)np, 256), 256, 0, st>>>(sk, np, start.as<uint32_t>(), endp.as<uint32_t>());
         note_launch();
     }
@@ -1429,7 +1430,7 @@ void BinStore::resort_records() {
     vals.ensure(slots * 4 + 4);
     vals2.ensure(slots * 4 + 4);
     skeys.ensure(slots * 4 + 4);
-    uint32_t *sk = skeys.as<uint32_t>(), *sv = vals2.as<uint32_t>();  // sorted keys / slot permutation
+    const uint32_t *sk = skeys.as<uint32_t>(), *sv = vals2.as<uint32_t>();  // sorted keys / slot permutation
     StepCounters* ctr = counters.as<StepCounters>();
     PICGPU_CUDA_TRY(cudaMemsetAsync(start.p, 0, nc * 4, st));
     PICGPU_CUDA_TRY(cudaMemsetAsync(endp.p, 0, nc * 4, st));
@@ -1438,8 +1439,9 @@ void BinStore::resort_records() {
         note_launch();
         int bits = 1;
         while (bits < 32 && (1ull << bits) < nc + 1) ++bits;
-        radix_sort_pairs(keys.as<uint32_t>(), skeys.as<uint32_t>(), nullptr, vals.as<uint32_t>(),
-                         vals2.as<uint32_t>(), slots, bits, sort_tmp, st, &sk, &sv);
+        keys2.ensure(slots * 4 + 4);
+        radix_sort_pairs(keys.as<uint32_t>(), skeys.as<uint32_t>(), keys2.as<uint32_t>(), nullptr, vals2.as<uint32_t>(),
+                         vals.as<uint32_t>(), slots, bits, sort_tmp, st);
         if (n) {  // the first n sorted keys are the particles' cells
             k_boundaries<<<div_up((long long)n, 256), 256, 0, st>>>(sk, n, start.as<uint32_t>(), endp.as<uint32_t>());
             note_launch();

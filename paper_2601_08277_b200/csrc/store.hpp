@@ -154,13 +154,11 @@ struct BinStore {
 
 // radix_sort.cu: out[i] = sum(in[0..i)) (n entries)
 void exclusive_sum_u32_to_u64(const uint32_t* in, unsigned long long* out, size_t n, DevBuf& tmp, cudaStream_t st);
-// Stable LSD radix sort of n (key, value) pairs on the low `bits` key bits.
-// keys and keys_alt are both overwritten (ping-pong); vals_in == nullptr means
-// the values are the indices 0..n-1 (a permutation results); vals / vals_alt
-// receive the value ping-pong (vals_in itself is never written).  The sorted
-// keys / values are returned in *keys_out / *vals_out (one of the buffers).
-void radix_sort_pairs(uint32_t* keys, uint32_t* keys_alt, const uint32_t* vals_in, uint32_t* vals,
-                      uint32_t* vals_alt, uint64_t n, int bits, DevBuf& tmp, cudaStream_t st, uint32_t** keys_out,
-                      uint32_t** vals_out);
+// Stable LSD radix sort of n (key, value) pairs on the low `bits` key bits:
+// the sorted pairs land in keys_out / vals_out; keys_in / vals_in are never
+// written (vals_in == nullptr: the values are the indices 0..n-1, so vals_out
+// receives the stable permutation); keys_tmp / vals_tmp are ping-pong scratch.
+void radix_sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, uint32_t* keys_tmp, const uint32_t* vals_in,
+                      uint32_t* vals_out, uint32_t* vals_tmp, uint64_t n, int bits, DevBuf& tmp, cudaStream_t st);
 
 }  // namespace picgpu
