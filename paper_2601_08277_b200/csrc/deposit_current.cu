@@ -483,6 +483,399 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Warp-specialised form of the lane kernel ("ws", PICGPU_J_WS=1; measured,
+// not the default -- see use_ws()).  Same tile, lane layout, z window, patch
+// and gather as v3, but every warp has ONE role:
+//  * PRODUCER warp w (threads NT.. 2NT-1) runs, for consumer warp w's pencils,
+//    the record loads (one chunk ahead in registers), the fused bit-exact push
+//    + move detection (mover-list reservations included) and the window
+//    prologue, and stages each chunk's windows into slot s of a ring of WS_NS
+//    chunk slots; a per-slot header carries the chunk's particle count and an
+//    end-of-cell flag.
+//  * CONSUMER warp w keeps the 48 accumulators, contracts every staged chunk,
+//    emits the finished plane, and the consumer warps gather the CTA's patch
+//    behind a named barrier (producers never wait on it).
+// Each producer/consumer pair is coupled only through its slots' mbarriers
+// (full: 32 producer arrivals, empty: 32 consumer arrivals), so a producer
+// runs up to WS_NS chunks ahead: the push and prologue latency (record loads,
+// the dependent FP64 chains of locate/weights) overlaps the contraction of
+// earlier chunks instead of stalling it, and each role holds only its own
+// registers (v3: 168 per thread, 12 warps/SM; here 2 x 8 warps at <= 128).
+#ifndef PICGPU_WS_NS
+#define PICGPU_WS_NS 3
+#endif
+#ifndef PICGPU_WS_MINB
+#define PICGPU_WS_MINB 2
+#endif
+constexpr int WS_NS = PICGPU_WS_NS;
+// register split (setmaxnreg, per warpgroup: consumers are warps 0-3, producers
+// 4-7): 4 x 32 x (C + P) = the CTA's 256 x 128 at 2 CTAs/SM
+#ifndef PICGPU_WS_REG_C
+#define PICGPU_WS_REG_C 160
+#endif
+#ifndef PICGPU_WS_REG_P
+#define PICGPU_WS_REG_P 96
+#endif
+constexpr int WS_REG_C = PICGPU_WS_REG_C, WS_REG_P = PICGPU_WS_REG_P;
+
+template <int ORDER, class CF>
+struct WsLayout {
+    using L = JLayout<ORDER, CF>;
+    static constexpr int NT = L::NT;           // consumer threads (= producer threads)
+    static constexpr int NW = NT / 32;         // producer/consumer pairs
+    static constexpr int SLOT = L::STAGE3;     // doubles per chunk slot (all pencils)
+    static constexpr size_t BAR_OFF = (size_t)(2 * L::PATCH + WS_NS * SLOT) * sizeof(double);
+    static constexpr size_t SMEM = BAR_OFF + (size_t)WS_NS * NW * 2 * sizeof(uint64_t) +
+                                   (size_t)WS_NS * NW * sizeof(uint32_t);
+};
+
+// consumer-only named barrier (id 1) with an OR reduction
+__device__ __forceinline__ bool consumer_bar_or(bool v, int nthreads) {
+    unsigned r;
+    asm volatile(
+        "{\n"
+        ".reg .pred p, q;\n"
+        "setp.ne.u32 p, %1, 0;\n"
+        "bar.red.or.pred q, 1, %2, p;\n"
+        "selp.u32 %0, 1, 0, q;\n"
+        "}\n"
+        : "=r"(r)
+        : "r"((unsigned)v), "r"(nthreads)
+        : "memory");
+    return r != 0;
+}
+
+constexpr uint32_t kWsLast = 1u << 8;  // header flag: last chunk of the cell step
+
+template <int ORDER, class CF = JCfg<ORDER>, int PM = 0, bool SLAB = false>
+__global__ void __launch_bounds__(2 * JLayout<ORDER, CF>::NT, PICGPU_WS_MINB)
+    deposit_current_kernel_ws(const GridD g, const CAos p, const uint32_t* __restrict__ off,
+                              const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
+                              double* __restrict__ jy, double* __restrict__ jz, const int zlen,
+                              const PushCtx pc) {
+    using C = CF;
+    using L = JLayout<ORDER, CF>;
+    using WL = WsLayout<ORDER, CF>;
+    constexpr int W = L::W, OFF = Shape<ORDER>::OFF;
+    constexpr int G = C::G, PX = C::PX, PY = C::PY, CH = C::CH;
+    constexpr int NT = L::NT, NW = WL::NW;
+    constexpr int FX = PX + W - 1, FY = PY + W - 1;
+    constexpr int NODES = 3 * FX * FY;
+    constexpr int NIT = (NODES + NT - 1) / NT;
+    constexpr int XS = G / W, IX = W / XS;
+    static_assert(G == W * XS && W % XS == 0 && (W & (W - 1)) == 0, "ws: lanes = jy x x-halves");
+    static_assert(L::PPB == 1, "ws: one plane per barrier");
+    const double qs = q * (ORDER == 3 ? 1.0 / 216.0 : ORDER == 2 ? 0.125 : 1.0);
+
+    extern __shared__ __align__(16) double smem[];
+    double* patch = smem;                  // [2][W(jy)][W(ix)][3][PSTRIDE]
+    double* ring = smem + 2 * L::PATCH;    // [WS_NS][SLOT]: paired fields (JLayout PSS/PFS)
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + WL::BAR_OFF);  // [NS][NW]
+    uint64_t* empty = full + WS_NS * NW;                                                       // [NS][NW]
+    uint32_t* hdr = reinterpret_cast<uint32_t*>(empty + WS_NS * NW);                          // [NS][NW]
+
+    const bool producer = threadIdx.x >= NT;
+    const int tid = producer ? threadIdx.x - NT : threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int grp = tid / G, lg = tid % G;
+    const int ly = lg % W, xh = lg / W;
+    const int px = grp % PX, py = grp / PX;
+    const int i0 = blockIdx.x * PX, j0 = blockIdx.y * PY;
+    const int k0 = blockIdx.z * zlen;
+    const int k1 = min(k0 + zlen, g.nz);
+    const int i = i0 + px, j = j0 + py;
+    const bool pv = (i < g.nx) && (j < g.ny);
+    const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
+    const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
+    [[maybe_unused]] const uint32_t seg = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    __shared__ unsigned s_movers;
+
+    // an entirely empty tile (vacuum) writes nothing: J was zeroed by the caller
+    {
+        bool any = false;
+        if (pv)
+            for (int kk = k0 + lg + (producer ? G : 0); kk < k1; kk += 2 * G) any |= cnt[col + plane_cells * kk] != 0;
+        if (!__syncthreads_or(any)) {
+            if (PM != 0 && threadIdx.x == 0) pc.seg_cnt[seg] = 0;
+            return;
+        }
+    }
+    if (threadIdx.x == 0) {
+        s_movers = 0;
+        for (int b = 0; b < WS_NS * NW; ++b) {
+            mbar_init(full + b, 32);
+            mbar_init(empty + b, 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (producer) {
+        // ------------------------------------------------------------ producer
+        if constexpr (WS_REG_P > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WS_REG_P));
+        const double dci = (double)(i + g.sx_shift), dcj = (double)j;
+        uint32_t c_off = 0;
+        int n_c = 0;
+        if (pv && k0 < k1) {
+            c_off = off[col + plane_cells * k0];
+            n_c = (int)cnt[col + plane_cells * k0];
+        }
+        PData nxt{};
+        if (lg < n_c) load_particle<PM != 0>(p, c_off + lg, nxt);
+        int s = 0;
+        unsigned ph = 0;
+        for (int k = k0; k < k1; ++k) {
+            const int R = (k - k0) & (W - 1);
+            uint32_t n_off = 0;
+            int n_n = 0;
+            if (pv && k + 1 < k1) {
+                n_off = off[col + plane_cells * (k + 1)];
+                n_n = (int)cnt[col + plane_cells * (k + 1)];
+            }
+            const double dck = (double)k;
+            const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
+            if (m == 0 && lg < n_n) load_particle<PM != 0>(p, n_off + lg, nxt);
+            const int nch = m == 0 ? 1 : (m + CH - 1) / CH;
+            for (int ci = 0; ci < nch; ++ci) {
+                const int base = ci * CH;
+                double* stage = ring + s * WL::SLOT;
+                [[maybe_unused]] bool mv = false;
+                [[maybe_unused]] uint32_t mv_cell = 0;
+                [[maybe_unused]] unsigned mv_bal = 0, mv_b0 = 0;
+                PData cur = nxt;
+                bool valid = base + lg < n_c && !is_gap(cur.x);
+                if (m > 0) {
+                    if (base + CH < m) {
+                        if (base + CH + lg < n_c) load_particle<PM != 0>(p, c_off + base + CH + lg, nxt);
+                    } else if (lg < n_n) {
+                        load_particle<PM != 0>(p, n_off + lg, nxt);
+                    }
+                }
+                double a[3][W], sy[W], sz[W];
+                [[maybe_unused]] int shx = 0, shy = 0, shz = 0;
+                if constexpr (PM != 0) {
+                    double fx = 0.0, fy = 0.0, fz = 0.0;
+                    if (valid)
+                        valid = push_fused<PM == 2, SLAB>(g, pc, cur, c_off + (uint32_t)(base + lg),
+                                                          col + plane_cells * (uint32_t)k, i, j, k, dci, dcj, dck,
+                                                          fx, fy, fz, mv, mv_cell, shx, shy, shz);
+                    mv_bal = __ballot_sync(0xffffffffu, mv);
+                    if (mv_bal && lane == __ffs(mv_bal) - 1) mv_b0 = atomicAdd(&s_movers, (unsigned)__popc(mv_bal));
+                    window_from_fractions<ORDER>(cur, qs, valid, fx, fy, fz, a, sy, sz);
+                } else {
+                    particle_window_sel<ORDER>(g, cur, qs, valid, dci, dcj, dck, a, sy, sz);
+                }
+                // the slot is free once the consumer has read its previous chunk
+                mbar_wait(empty + s * NW + warp, ph ^ 1u);
+                if (m > 0) {
+                    stage_record<L, W>(stage, lg, grp, R, a, sy, sz);
+                    if constexpr (PM != 0) {
+                        if (mv && valid) {
+                            restage_shifted<L, W>(stage, lg, grp, 0, shx, 0);
+                            restage_shifted<L, W>(stage, lg, grp, W, shx, 0);
+                            restage_shifted<L, W>(stage, lg, grp, 2 * W, shx, 0);
+                            restage_shifted<L, W>(stage, lg, grp, 3 * W, shy, 0);
+                            restage_shifted<L, W>(stage, lg, grp, 4 * W, shz, R);
+                        }
+                    }
+                }
+                if (lane == 0)
+                    hdr[s * NW + warp] = (uint32_t)(m > 0 ? min(CH, m - base) : 0) | (ci == nch - 1 ? kWsLast : 0u);
+                mbar_arrive(full + s * NW + warp);
+                if (++s == WS_NS) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+                if constexpr (PM != 0) {
+                    if (mv_bal) {
+                        const unsigned b0 = __shfl_sync(0xffffffffu, mv_b0, __ffs(mv_bal) - 1);
+                        if (mv) {
+                            const unsigned idx = b0 + (unsigned)__popc(mv_bal & ((1u << lane) - 1u));
+                            size_t e = (size_t)seg * pc.segcap + idx;
+                            if (idx >= pc.segcap) {  // segment full
+                                if constexpr (SLAB) {
+                                    if (mv_cell >= kLeaveRight) {
+                                        export_leaver_now(pc, c_off + (uint32_t)(base + lg),
+                                                          col + plane_cells * (uint32_t)k, mv_cell);
+                                        e = ~(size_t)1;
+                                    }
+                                }
+                                if (e != ~(size_t)1) {
+                                    const unsigned o = atomicAdd(&pc.ctr->ovf_movers, 1u);
+                                    e = o < pc.ovcap ? (size_t)pc.nseg * pc.segcap + o : ~(size_t)0;
+                                }
+                            }
+                            if (e < ~(size_t)1) {
+                                pc.mslot[e] = c_off + (uint32_t)(base + lg);
+                                pc.mbin[e] = col + plane_cells * (uint32_t)k;
+                                pc.mcellseg[e] = mv_cell;
+                            }
+                        }
+                    }
+                }
+            }
+            c_off = n_off;
+            n_c = n_n;
+        }
+    } else {
+        // ------------------------------------------------------------ consumer
+        if constexpr (WS_REG_C > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_REG_C));
+        const int pxv = min(PX, g.nx - i0), pyv = min(PY, g.ny - j0);
+        const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
+        int gn_base[NIT], gn_node[NIT];
+        unsigned gn_mask[NIT];
+        bool gn_inner[NIT];
+#pragma unroll
+        for (int t = 0; t < NIT; ++t) {
+            const int it = tid + t * NT;
+            gn_mask[t] = 0u;
+            gn_base[t] = 0;
+            gn_node[t] = 0;
+            gn_inner[t] = false;
+            if (it < NODES) {
+                const int c = it / (FX * FY);
+                const int r = it - c * (FX * FY);
+                const int uy = r / FX, ux = r - uy * FX;
+                if (ux < pxv + W - 1 && uy < pyv + W - 1) {
+#pragma unroll
+                    for (int dy = 0; dy < W; ++dy)
+#pragma unroll
+                        for (int dx = 0; dx < W; ++dx) {
+                            const int qy = uy - dy, qx = ux - dx;
+                            if (qy >= 0 && qy < pyv && qx >= 0 && qx < pxv) gn_mask[t] |= 1u << (dy * W + dx);
+                        }
+                    gn_base[t] = (c << 28) | (c * L::PSTRIDE + uy * PX + ux);
+                    const int X = wrap_index(i0 + OFF + ux, g.nx);
+                    const int Y = wrap_index(j0 + OFF + uy, g.ny);
+                    gn_node[t] = X + g.nx * Y;
+                    gn_inner[t] = !alias_xy && ux >= W - 1 && ux <= pxv - 1 && uy >= W - 1 && uy <= pyv - 1;
+                }
+            }
+        }
+        double acc[W][IX][3];
+#pragma unroll
+        for (int sl = 0; sl < W; ++sl)
+#pragma unroll
+            for (int ix = 0; ix < IX; ++ix)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[sl][ix][c] = 0.0;
+        int s = 0;
+        unsigned ph = 0;
+        int phase = 0;
+        int last_busy = k0 - W;
+        const int kend = k1 + W - 1;
+        for (int k = k0; k < kend; ++k) {
+            const int R = (k - k0) & (W - 1);
+            bool busy = false;
+            if (k < k1) {
+                for (;;) {
+                    mbar_wait(full + s * NW + warp, ph);
+                    const uint32_t h = hdr[s * NW + warp];
+                    const int nn = (int)(h & 0xffu);
+                    const double* stage = ring + s * WL::SLOT;
+                    busy |= nn > 0;
+#pragma unroll
+                    for (int jj0 = 0; jj0 < CH; ++jj0) {
+                        if (jj0 >= nn) break;
+                        const double yv = *pfield<L>(stage, 3 * W + ly, jj0, grp);
+                        double b[W];
+#pragma unroll
+                        for (int sl = 0; sl < W; sl += 2) {
+                            const double2 zz =
+                                *reinterpret_cast<const double2*>(pfield<L>(stage, 4 * W + sl, jj0, grp));
+                            b[sl] = yv * zz.x;
+                            b[sl + 1] = yv * zz.y;
+                        }
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+#pragma unroll
+                            for (int ix = 0; ix < IX; ix += 2) {
+                                const double2 av = *reinterpret_cast<const double2*>(
+                                    pfield<L>(stage, c * W + xh * IX + ix, jj0, grp));
+#pragma unroll
+                                for (int sl = 0; sl < W; ++sl) {
+                                    acc[sl][ix][c] = fma(av.x, b[sl], acc[sl][ix][c]);
+                                    acc[sl][ix + 1][c] = fma(av.y, b[sl], acc[sl][ix + 1][c]);
+                                }
+                            }
+                    }
+                    mbar_arrive(empty + s * NW + warp);
+                    if (++s == WS_NS) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                    if (h & kWsLast) break;
+                }
+            }
+            {
+                double* pp = patch + phase * L::PATCH + grp;
+                auto emit = [&](auto Sc) {
+                    constexpr int S = decltype(Sc)::value;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+#pragma unroll
+                        for (int ix = 0; ix < IX; ++ix) {
+                            pp[((ly * W + xh * IX + ix) * 3 + c) * L::PSTRIDE] = acc[S][ix][c];
+                            acc[S][ix][c] = 0.0;
+                        }
+                };
+                if constexpr (W == 2) {
+                    if (R == 0)
+                        emit(std::integral_constant<int, 0>{});
+                    else
+                        emit(std::integral_constant<int, 1>{});
+                } else {
+                    switch (R) {
+                        case 0: emit(std::integral_constant<int, 0>{}); break;
+                        case 1: emit(std::integral_constant<int, 1>{}); break;
+                        case 2: emit(std::integral_constant<int, 2>{}); break;
+                        default: emit(std::integral_constant<int, 3>{}); break;
+                    }
+                }
+            }
+            if (consumer_bar_or(busy, NT)) last_busy = k;
+            if (last_busy >= k - (W - 1)) {
+                const double* pb = patch + phase * L::PATCH;
+                const int Z = wrap_index(k + OFF, g.nz);
+                const bool zc = (k >= k0 + W - 1) && (k < k1);
+                const size_t zrow = (size_t)plane_cells * (size_t)Z;
+#pragma unroll
+                for (int t = 0; t < NIT; ++t) {
+                    const unsigned msk = gn_mask[t];
+                    if (!msk) continue;
+                    const int c = gn_base[t] >> 28;
+                    const double* src = pb + (gn_base[t] & 0x0fffffff);
+                    double v[W * W];
+#pragma unroll
+                    for (int dy = 0; dy < W; ++dy)
+#pragma unroll
+                        for (int dx = 0; dx < W; ++dx)
+                            v[dy * W + dx] = (msk & (1u << (dy * W + dx)))
+                                                 ? src[(dy * W + dx) * 3 * L::PSTRIDE - dy * PX - dx]
+                                                 : 0.0;
+#pragma unroll
+                    for (int h = W * W / 2; h >= 1; h /= 2)
+#pragma unroll
+                        for (int e = 0; e < h; ++e) v[e] += v[e + h];
+                    const double sum = v[0];
+                    double* f = c == 0 ? jx : (c == 1 ? jy : jz);
+                    const size_t node = (size_t)gn_node[t] + zrow;
+                    if (zc && gn_inner[t])
+                        f[node] = sum;
+                    else if (sum != 0.0)
+                        atomicAdd(f + node, sum);
+                }
+            }
+            phase ^= 1;
+        }
+    }
+    if constexpr (PM != 0) {  // this CTA's mover count (every reservation precedes this barrier)
+        __syncthreads();
+        if (threadIdx.x == 0) pc.seg_cnt[seg] = s_movers;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Orders 2 and 3 (4-tap window): ONE WARP PER PENCIL.
 //
 // The warp streams its pencil's particles (cells k0..k1-1 concatenated) in
@@ -803,6 +1196,59 @@ void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uin
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
+// Grid of the warp-specialised kernel: the v3 tiling, 2 x NT threads per CTA.
+template <int ORDER, class C, int PM = 0, bool SLAB = false>
+void launch_kernel_ws(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+                      int num_sms, cudaStream_t st, PushCtx pc = PushCtx{}, PushCtx* used = nullptr) {
+    using L = JLayout<ORDER, C>;
+    using WL = WsLayout<ORDER, C>;
+    constexpr int W = L::W;
+    static int configured_dev = -1;
+    int dev = 0;
+    PICGPU_CUDA_TRY(cudaGetDevice(&dev));
+    if (configured_dev != dev) {  // per device (one process may drive several GPUs)
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel_ws<ORDER, C, PM, SLAB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WL::SMEM));
+        configured_dev = dev;
+    }
+    const int tx = div_up(g.nx, C::PX), ty = div_up(g.ny, C::PY);
+    const long long tiles = (long long)tx * ty;
+    const long long target = (long long)num_sms * PICGPU_WS_MINB * 4;
+    int zch = (int)std::max<long long>(1, (target + tiles - 1) / tiles);
+    zch = std::min(zch, std::max(1, g.nz / (4 * W)));
+    const int zlen = div_up(g.nz, zch);
+    zch = div_up(g.nz, zlen);
+    dim3 grid(tx, ty, zch);
+    if constexpr (PM != 0) set_segments(pc, grid, used);
+    deposit_current_kernel_ws<ORDER, C, PM, SLAB><<<grid, 2 * L::NT, WL::SMEM, st>>>(
+        g, p, off, cnt, q, j, j + g.ncells, j + 2 * (size_t)g.ncells, zlen, pc);
+    note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+// The lane family's kernel form: the single-role v3 (default) or the
+// warp-specialised one (PICGPU_J_WS=1).  C2 QSP (B200): fused 1.63 (ws) vs
+// 1.61 ms (v3), J only 1.31 vs 1.18, CIC fused 1.54 vs 1.41 -- the producer
+// warps (push + prologue, a dependent FP64 chain per particle) cannot feed
+// the consumers: 11.6% of the issued instructions are consumer mbarrier
+// back-off, both pipes stay near 50% (profiles/r02/ncu_fused_ws.txt).
+static bool use_ws() {
+    static const bool v = [] {
+        const char* e = std::getenv("PICGPU_J_WS");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+template <int ORDER, class C, int PM = 0, bool SLAB = false>
+void launch_lane(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
+                 int num_sms, cudaStream_t st, PushCtx pc = PushCtx{}, PushCtx* used = nullptr) {
+    if (use_ws())
+        launch_kernel_ws<ORDER, C, PM, SLAB>(g, p, off, cnt, q, j, num_sms, st, pc, used);
+    else
+        launch_kernel<ORDER, C, PM, SLAB>(g, p, off, cnt, q, j, num_sms, st, pc, used);
+}
+
 template <int ORDER>
 using LaneCfg = std::conditional_t<ORDER == 1, JCfgCic3, JCfg<ORDER>>;
 
@@ -829,14 +1275,14 @@ void launch_deposit_current(int order, const GridD& g, const CAos& p, const uint
     const int k = resolve_family(kernel);
     if (k == kJMatrix) return launch_pencil_current(order, g, p, off, cnt, q, j, num_sms, st);
     switch (order) {
-        case 1: launch_kernel<1, LaneCfg<1>>(g, p, off, cnt, q, j, num_sms, st); break;
+        case 1: launch_lane<1, LaneCfg<1>>(g, p, off, cnt, q, j, num_sms, st); break;
         case 2:
             if (k == kJVector) launch_warp<2>(g, p, off, cnt, q, j, num_sms, st);
-            else launch_kernel<2, LaneCfg<2>>(g, p, off, cnt, q, j, num_sms, st);
+            else launch_lane<2, LaneCfg<2>>(g, p, off, cnt, q, j, num_sms, st);
             break;
         default:
             if (k == kJVector) launch_warp<3>(g, p, off, cnt, q, j, num_sms, st);
-            else launch_kernel<3, LaneCfg<3>>(g, p, off, cnt, q, j, num_sms, st);
+            else launch_lane<3, LaneCfg<3>>(g, p, off, cnt, q, j, num_sms, st);
             break;
     }
 }
@@ -855,9 +1301,9 @@ void launch_push_order(const GridD& g, PushCtx& pc, const uint32_t* off, const u
         else
             launch_kernel<ORDER, C3, 1, true>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
     } else if (p2) {
-        launch_kernel<ORDER, C3, 2>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
+        launch_lane<ORDER, C3, 2>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
     } else {
-        launch_kernel<ORDER, C3, 1>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
+        launch_lane<ORDER, C3, 1>(g, p, off, cnt, q, j, num_sms, st, pc, &pc);
     }
 }
 
