@@ -68,6 +68,7 @@ class Oracle:
         L.po_counting_sort.argtypes = [C.POINTER(Grid), _p, _p, _p, _u64, _p, _p, _p]
         L.po_advance.argtypes = [C.POINTER(Grid), _d, _p, _p, _p, _p, _p, _p, _u64, _p]
         L.po_cells.argtypes = [C.POINTER(Grid), _p, _p, _p, _u64, _p]
+        L.po_deposit_esirkepov.argtypes = [C.POINTER(Grid), C.c_int] + [_p] * 7 + [_d, _d, _u64, _p, _p, _p]
         L.po_make_plasma.argtypes = [C.POINTER(Grid), C.c_int, _d, _u64] + [_p] * 8
         L.po_make_plasma.restype = None
         L.po_should_global_sort.argtypes = [_u32, _u64, _d, _d, _d, _u32, _u32, _u32, _d, _d, C.c_int, _d]
@@ -101,6 +102,17 @@ class Oracle:
                                        q, n, _ptr(visit), _ptr(jx), _ptr(jy), _ptr(jz))
         if rc:
             raise ValueError(f"deposit_current failed ({rc})")
+        return jx, jy, jz
+
+    def deposit_esirkepov(self, g, order, old, new, w, q, dt):
+        """Charge-conserving J on the Yee faces (this project's extension; unpinned by the reference)."""
+        jx, jy, jz = (np.zeros(g.ncells) for _ in range(3))
+        n = len(w)
+        rc = self.L.po_deposit_esirkepov(C.byref(g), order, *(_ptr(np.ascontiguousarray(a)) for a in
+                                                              (old["x"], old["y"], old["z"], new["x"], new["y"],
+                                                               new["z"], w)), q, dt, n, _ptr(jx), _ptr(jy), _ptr(jz))
+        if rc:
+            raise {5: ArithmeticError}.get(rc, ValueError)(f"deposit_esirkepov failed ({rc})")
         return jx, jy, jz
 
     def deposit_density(self, g, order, s, quantity):

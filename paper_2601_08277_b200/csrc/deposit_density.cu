@@ -592,7 +592,8 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
 }
 
 // ---------------------------------------------------------------------------
-// Block-staged ordered gather, v2 (default): the same block / row / piece walk
+// Block-staged ordered gather, v2 (PICGPU_RHO_V2=1; measured slower than v1,
+// see run_sorted): the same block / row / piece walk
 // as density_blocks (so the same visiting order per node: source cells by
 // ascending linear id, slots in order -- bit-identical sums), with the work
 // per staged slot restructured:
@@ -787,9 +788,14 @@ void run_sorted(const GridD& g, const CAos& p, const double* quantity, double qs
         return e && e[0] == '1';
     }();
     if (rows) return run_rows_and_shell<ORDER>(g, p, quantity, qscale, off, cnt, slots, scratch, rho, st);
+    // v2 (PICGPU_RHO_V2=1) measured slower at C2 QSP: 6.64 vs 4.34 ms (CIC 4.28 vs
+    // 1.64): its 8 x-lanes per warp walk 8 different cells, so a warp runs the
+    // longest of 8 slot ranges in each staged piece (7.5G lane-terms issued for
+    // 2.15G terms) and its 512 CTAs of 128 threads fill one wave at 13 warps/SM
+    // (profiles/r02/ncu_rho_v2.txt).
     static const bool v1 = [] {
-        const char* e = std::getenv("PICGPU_RHO_V1");
-        return e && e[0] == '1';
+        const char* e = std::getenv("PICGPU_RHO_V2");
+        return !(e && e[0] == '1');
     }();
     int dev = 0;
     PICGPU_CUDA_TRY(cudaGetDevice(&dev));
