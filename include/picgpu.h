@@ -133,6 +133,26 @@ PICGPU_API int picgpu_deposit_current_dev(const picgpu_grid* g, int order, const
                                const double* vx, const double* vy, const double* vz, const double* w, double q,
                                uint64_t n, double* jx, double* jy, double* jz, void* stream);
 
+/* ---- charge-conserving current (an EXTENSION: no reference counterpart) -- */
+/* Esirkepov's scheme on the staggered Yee grid at shape order 1/2/3: particles
+ * move from (x0,y0,z0) to (x1,y1,z1) in dt (x1 as pushed, i.e. possibly
+ * wrapped into the box; the cell step per axis must be -1, 0 or +1, else
+ * PICGPU_EDOMAIN).  jx[i + nx*(j + ny*k)] is J_x on the face (i+1/2, j, k),
+ * likewise jy (i, j+1/2, k) and jz (i, j, k+1/2); they satisfy the discrete
+ * continuity equation with rho = q*w*S (picgpu_deposit_density) to round-off.
+ * The reference deposits J collocated (pic::deposit_scalar, deposit.hpp:60-73)
+ * and lists charge-conserving schemes as future work: parity is
+ * against this project's restatement (oracle/picoracle.c) and continuity. */
+PICGPU_API int picgpu_deposit_current_esirkepov(const picgpu_grid* g, int order, const double* x0, const double* y0,
+                                                const double* z0, const double* x1, const double* y1,
+                                                const double* z1, const double* w, double q, double dt, uint64_t n,
+                                                double* jx, double* jy, double* jz);
+PICGPU_API int picgpu_deposit_current_esirkepov_dev(const picgpu_grid* g, int order, const double* x0,
+                                                    const double* y0, const double* z0, const double* x1,
+                                                    const double* y1, const double* z1, const double* w, double q,
+                                                    double dt, uint64_t n, double* jx, double* jy, double* jz,
+                                                    void* stream);
+
 /* ---- resort policy (host logic, sort_policy.hpp:12-79) ------------------ */
 typedef struct picgpu_sort_policy {
     uint32_t sort_interval;         /* 50 */

@@ -224,6 +224,8 @@ def lib():
     L.picgpu_kernel_launches.restype = _U64
     L.picgpu_deposit_current.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, _P, _P, _P]
     L.picgpu_deposit_current_dev.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, _P, _P, _P, _P]
+    L.picgpu_deposit_current_esirkepov.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _D, _U64, _P, _P, _P]
+    L.picgpu_deposit_current_esirkepov_dev.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _D, _U64, _P, _P, _P, _P]
     L.picgpu_deposit_density.argtypes = [G, C.c_int, _P, _P, _P, _P, _U64, _P]
     L.picgpu_counting_sort.argtypes = [G, _P, _P, _P, _U64, _P, _P, _P]
     L.picgpu_advance.argtypes = [G, _D, _P, _P, _P, _P, _P, _P, _U64, _P]
@@ -350,6 +352,18 @@ def _soa(soa, q=None):
     if isinstance(soa, ParticleSoA):
         return soa
     return ParticleSoA.from_dict(soa, q)
+
+
+def deposit_esirkepov(old, new, w, grid: Grid, order: int, q: float, dt: float) -> CurrentGrid:
+    """Charge-conserving J on the Yee faces (picgpu_deposit_current_esirkepov):
+    an extension with no reference counterpart (see include/picgpu.h)."""
+    n = len(w)
+    a = [_f64(old[k]) for k in ("x", "y", "z")] + [_f64(new[k]) for k in ("x", "y", "z")] + [_f64(w)]
+    nc = grid.ncells
+    jx, jy, jz = np.empty(nc), np.empty(nc), np.empty(nc)
+    _check(lib().picgpu_deposit_current_esirkepov(C.byref(grid), order, *(_ptr(v) for v in a), q, dt, n, _ptr(jx),
+                                                  _ptr(jy), _ptr(jz)))
+    return CurrentGrid(grid, jx, jy, jz)
 
 
 def deposit_scalar(soa, grid: Grid, order: int, q: float | None = None) -> CurrentGrid:

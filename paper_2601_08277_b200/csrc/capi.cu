@@ -378,6 +378,79 @@ int picgpu_deposit_rhocell_vector(const picgpu_grid* g, int order, const double*
     });
 }
 
+// Esirkepov deposit on device buffers, enqueued on the stateless stream after
+// `stream`, with `stream` waiting for it; the device error word is read once.
+static void esirkepov_enqueue(const picgpu_grid* g, int order, const double* const in[7], double q, double dt,
+                              uint64_t n, double* const out[3], cudaStream_t user, bool host_io) {
+    check_order(order);
+    if (!(dt > 0.0)) throw Status{PICGPU_EINVAL, "deposit_esirkepov: dt must be positive"};
+    const GridD gd = make_grid(*g);
+    Stateless& S = stateless();
+    std::lock_guard<std::mutex> lk(S.mu);
+    S.prepare(*g);
+    const cudaStream_t st = S.st;
+    BinStore& bs = S.store;
+    const double* src[7];
+    if (host_io) {
+        bs.B.ensure(n);
+        const Soa b = bs.B.soa();
+        double* dst[7] = {b.x, b.y, b.z, b.vx, b.vy, b.vz, b.w};
+        for (int a = 0; a < 7; ++a) {
+            h2d(dst[a], in[a], n * 8, st);
+            src[a] = dst[a];
+        }
+    } else {
+        cudaEvent_t ev;
+        PICGPU_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        PICGPU_CUDA_TRY(cudaEventRecord(ev, user));
+        PICGPU_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+        PICGPU_CUDA_TRY(cudaEventDestroy(ev));
+        for (int a = 0; a < 7; ++a) src[a] = in[a];
+    }
+    S.J.ensure((size_t)gd.ncells * 24);
+    double* J = S.J.as<double>();
+    PICGPU_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)gd.ncells * 24, st));
+    int* err = S.flag.as<int>();
+    PICGPU_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+    launch_deposit_esirkepov(order, gd, src[0], src[1], src[2], src[3], src[4], src[5], src[6], q, dt, n, J,
+                             J + gd.ncells, J + 2 * (size_t)gd.ncells, err, st);
+    int h = 0;
+    PICGPU_CUDA_TRY(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st));
+    PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+    if (h == PICGPU_EDOMAIN) throw Status{PICGPU_EDOMAIN, "deposit_esirkepov: a particle moved more than one cell"};
+    if (h) throw Status{h, "deposit_esirkepov: non-finite particle position"};
+    for (int c = 0; c < 3; ++c) {
+        if (host_io)
+            d2h(out[c], J + c * (size_t)gd.ncells, (size_t)gd.ncells * 8, st);
+        else
+            PICGPU_CUDA_TRY(cudaMemcpyAsync(out[c], J + c * (size_t)gd.ncells, (size_t)gd.ncells * 8,
+                                            cudaMemcpyDeviceToDevice, st));
+    }
+    PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+}
+
+int picgpu_deposit_current_esirkepov(const picgpu_grid* g, int order, const double* x0, const double* y0,
+                                     const double* z0, const double* x1, const double* y1, const double* z1,
+                                     const double* w, double q, double dt, uint64_t n, double* jx, double* jy,
+                                     double* jz) {
+    return guard([&] {
+        const double* in[7] = {x0, y0, z0, x1, y1, z1, w};
+        double* out[3] = {jx, jy, jz};
+        esirkepov_enqueue(g, order, in, q, dt, n, out, nullptr, true);
+    });
+}
+
+int picgpu_deposit_current_esirkepov_dev(const picgpu_grid* g, int order, const double* x0, const double* y0,
+                                         const double* z0, const double* x1, const double* y1, const double* z1,
+                                         const double* w, double q, double dt, uint64_t n, double* jx, double* jy,
+                                         double* jz, void* stream) {
+    return guard([&] {
+        const double* in[7] = {x0, y0, z0, x1, y1, z1, w};
+        double* out[3] = {jx, jy, jz};
+        esirkepov_enqueue(g, order, in, q, dt, n, out, (cudaStream_t)stream, false);
+    });
+}
+
 int picgpu_deposit_current_dev(const picgpu_grid* g, int order, const double* x, const double* y, const double* z,
                                const double* vx, const double* vy, const double* vz, const double* w, double q,
                                uint64_t n, double* jx, double* jy, double* jz, void* stream) {

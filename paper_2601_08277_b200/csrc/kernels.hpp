@@ -82,6 +82,10 @@ void launch_deposit_density(int order, const GridD& g, const CAos& p, const doub
 void launch_deposit_density_merge(int order, const GridD& g, const CAos& p, const double* quantity, double qscale,
                                   const uint32_t* rank, const uint32_t* off, const uint32_t* cnt, uint64_t slots,
                                   void* scratch, double* rho, cudaStream_t st);
+// esirkepov.cu: charge-conserving J on the Yee faces (an extension; J zeroed by the caller).
+void launch_deposit_esirkepov(int order, const GridD& g, const double* x0, const double* y0, const double* z0,
+                              const double* x1, const double* y1, const double* z1, const double* w, double q,
+                              double dt, uint64_t n, double* jx, double* jy, double* jz, int* err, cudaStream_t st);
 
 // sorter.cu ------------------------------------------------------------------
 // cell[p] = linear cell id (bit-identical cell_of); raises EINVAL on non-finite.

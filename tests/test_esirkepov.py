@@ -79,3 +79,64 @@ def test_oracle_esirkepov_rejects_jumps(orc):
     new = {"x": np.array([3.6]), "y": np.array([1.5]), "z": np.array([1.5])}
     with pytest.raises(ArithmeticError):
         orc.deposit_esirkepov(g, 3, old, new, np.ones(1), 1.0, 0.5)
+
+
+# --------------------------------------------------------------------- GPU
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [1, 2, 3])
+@pytest.mark.parametrize("gi", [0, 1, 2])
+def test_gpu_esirkepov_matches_oracle_and_conserves_charge(pg, orc, order, gi):
+    from conftest import peak_rel_err, to_pg_grid
+
+    g = [O.Grid.make(8), O.Grid.make(13, 6, 9, 0.5, 1.0, 0.25, origin=(-1.0, 2.0, 0.5)),
+         O.Grid.make(5, 4, 7, 0.3, 1.7, 0.05)][gi]
+    old, new, w = _pair(orc, g, 20000, 11 + gi)
+    q, dt = -1.0, 0.37
+    J = pg.deposit_esirkepov(old, new, w, to_pg_grid(g), order, q, dt)
+    got = (J.jx, J.jy, J.jz)
+    assert peak_rel_err(got, orc.deposit_esirkepov(g, order, old, new, w, q, dt)) <= 1e-12
+    assert continuity_residual(orc, g, order, old, new, w, q, dt, got) < 1e-12
+
+
+@pytest.mark.gpu
+def test_gpu_esirkepov_session_step_conserves_charge(pg, orc):
+    """Positions before and after a bit-exact session push (64^3 x 4 ppc, QSP):
+    the GPU Esirkepov current closes the continuity equation with the
+    bit-exact GPU rho of both states."""
+    from conftest import to_pg_grid
+
+    g = O.Grid.make(64)
+    G = to_pg_grid(g)
+    with pg.Session(G, order=3) as S:
+        S.generate_plasma(4, 0.3, seed=5)
+        p0 = S.particles()
+        S.step(0.5)
+        p1 = S.particles()
+    a, b = np.argsort(p0.id), np.argsort(p1.id)
+    old = {k: getattr(p0, k)[a] for k in "xyz"}
+    new = {k: getattr(p1, k)[b] for k in "xyz"}
+    w = p0.w[a]
+    q, dt = -1.0, 0.5
+    J = pg.deposit_esirkepov(old, new, w, G, 3, q, dt)
+    zero = np.zeros_like(w)
+    full = lambda d: {**d, "vx": zero, "vy": zero, "vz": zero, "w": w}  # noqa: E731
+    r0 = pg.deposit_density(full(old), G, 3, q * w)
+    r1 = pg.deposit_density(full(new), G, 3, q * w)
+    res = (r1 - r0) / dt + _divergence(g, J.jx, J.jy, J.jz)
+    assert np.abs(res).max() / (np.abs(r1 - r0).max() / dt) < 1e-12
+
+
+@pytest.mark.gpu
+def test_gpu_esirkepov_errors(pg):
+    G = pg.Grid.make(8)
+    one = {"x": np.array([1.5]), "y": np.array([1.5]), "z": np.array([1.5])}
+    far = {"x": np.array([3.6]), "y": np.array([1.5]), "z": np.array([1.5])}
+    with pytest.raises(pg.DomainError):
+        pg.deposit_esirkepov(one, far, np.ones(1), G, 3, 1.0, 0.5)
+    nan = {"x": np.array([np.nan]), "y": np.array([1.5]), "z": np.array([1.5])}
+    with pytest.raises(pg.InvalidArgument):
+        pg.deposit_esirkepov(one, nan, np.ones(1), G, 3, 1.0, 0.5)
+    with pytest.raises(pg.InvalidArgument):
+        pg.deposit_esirkepov(one, one, np.ones(1), G, 3, 1.0, 0.0)
