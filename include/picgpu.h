@@ -364,6 +364,31 @@ PICGPU_API int picgpu_session_add_guard_planes(picgpu_session* s, int field, con
 /* Runs a dependent-free DFMA loop on all SMs; returns measured FP64 TFLOP/s. */
 PICGPU_API int picgpu_fp64_peak(int device, double* tflops);
 
+/* ---- multi-GPU: NCCL behind the C ABI (x-slab sessions) ----- */
+/* New (the reference has no decomposition; its step loop is
+ * simulation.hpp:105-181).  One process per GPU; rank r of the communicator
+ * owns slab r of the x-decomposition and exchanges with ranks r-1 and r+1 on
+ * the periodic ring.  The library binds the libnccl.so.2 already loaded in
+ * the process (else loads it), so a communicator from the host application's
+ * own NCCL can be wrapped. */
+typedef struct picgpu_comm picgpu_comm;
+PICGPU_API int picgpu_comm_unique_id(unsigned char id[128]);  /* ncclGetUniqueId: on one rank, then broadcast */
+PICGPU_API int picgpu_comm_init(const unsigned char id[128], int nranks, int rank, int device, picgpu_comm** out);
+PICGPU_API int picgpu_comm_wrap(void* nccl_comm, int device, picgpu_comm** out); /* an existing ncclComm_t */
+PICGPU_API int picgpu_comm_rank(const picgpu_comm* c, int* rank, int* nranks);
+PICGPU_API int picgpu_comm_destroy(picgpu_comm* c);
+/* Attach a communicator to a slab session (picgpu_session_set_slab first).
+ * bucket_records: leaver records per side sent in the step's first exchange
+ * round (0: 32768); more leavers than that go in a second, exactly sized round. */
+PICGPU_API int picgpu_session_set_comm(picgpu_session* s, picgpu_comm* c, uint32_t bucket_records);
+/* One whole slab step with ONE host synchronisation: push + detect (fused
+ * with J at low migration) -> leaver counts and records to the ring
+ * neighbours (one NCCL group, counts stay on the device) -> arrivals imported,
+ * deposited and inserted -> step counters read -> guard planes of J (and rho)
+ * summed with the neighbours (NCCL, enqueued; no trailing synchronisation).
+ * Collective: every rank of the communicator calls it with the same flags. */
+PICGPU_API int picgpu_session_slab_step(picgpu_session* s, double dt, uint32_t flags, picgpu_step_stats* out);
+
 #ifdef __cplusplus
 }
 #endif

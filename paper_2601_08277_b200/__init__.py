@@ -224,6 +224,13 @@ def lib():
     L.picgpu_kernel_launches.restype = _U64
     L.picgpu_deposit_current.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, _P, _P, _P]
     L.picgpu_deposit_current_dev.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, _P, _P, _P, _P]
+    L.picgpu_comm_unique_id.argtypes = [_P]
+    L.picgpu_comm_init.argtypes = [_P, C.c_int, C.c_int, C.c_int, _P]
+    L.picgpu_comm_wrap.argtypes = [_P, C.c_int, _P]
+    L.picgpu_comm_rank.argtypes = [_P, _P, _P]
+    L.picgpu_comm_destroy.argtypes = [_P]
+    L.picgpu_session_set_comm.argtypes = [_P, _P, C.c_uint32]
+    L.picgpu_session_slab_step.argtypes = [_P, _D, C.c_uint32, _P]
     L.picgpu_deposit_current_esirkepov.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _D, _U64, _P, _P, _P]
     L.picgpu_deposit_current_esirkepov_dev.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _D, _U64, _P, _P, _P, _P]
     L.picgpu_deposit_density.argtypes = [G, C.c_int, _P, _P, _P, _P, _U64, _P]

@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libpicgpu.so")
-SOURCES = ["deposit_current.cu", "deposit_pencil.cu", "deposit_density.cu", "sorter.cu", "radix_sort.cu", "esirkepov.cu", "capi.cu"]
+SOURCES = ["deposit_current.cu", "deposit_pencil.cu", "deposit_density.cu", "sorter.cu", "radix_sort.cu", "esirkepov.cu", "comm.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.hpp"
 #include "kernels.hpp"
 #include "store.hpp"
 
@@ -218,6 +219,12 @@ struct picgpu_session {
     uint64_t nleave[2] = {0, 0};
     StepCounters cbegin{};
     uint64_t begin_launches = 0;
+    // device-resident exchange over NCCL (picgpu_session_set_comm / slab_step)
+    picgpu_comm* comm = nullptr;
+    uint32_t bucket = 0;            // records per side per step in the first exchange round
+    DevBuf xin, xcnt, xin2;         // arrivals (2 buckets), their counts, second-round remainders
+    DevBuf psend, precv;            // guard planes: [lo | hi] and [from left | from right]
+    uint32_t* hxcnt = nullptr;      // pinned mirror of xcnt
 };
 
 static void set_device(const picgpu_session* s) { PICGPU_CUDA_TRY(cudaSetDevice(s->device)); }
@@ -671,6 +678,7 @@ int picgpu_session_destroy(picgpu_session* s) {
         cudaStreamSynchronize(s->st);
         for (auto& e : s->ev)
             if (e) cudaEventDestroy(e);
+        if (s->hxcnt) cudaFreeHost(s->hxcnt);
         cudaStream_t st = s->st;
         delete s;
         if (st) cudaStreamDestroy(st);
@@ -1358,5 +1366,239 @@ extern "C" int picgpu_fp64_peak(int device, double* tflops) {
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         cudaStreamDestroy(st);
+    });
+}
+
+// ===========================================================================
+// multi-GPU: NCCL behind the C ABI (comm.hpp)
+
+int picgpu_comm_unique_id(unsigned char id[128]) {
+    return guard([&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+        ncclUniqueId u;
+        nccl_check(nccl().GetUniqueId(&u), "ncclGetUniqueId failed");
+        std::memcpy(id, &u, 128);
+    });
+}
+
+int picgpu_comm_init(const unsigned char id[128], int nranks, int rank, int device, picgpu_comm** out) {
+    *out = nullptr;
+    return guard([&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw Status{PICGPU_EINVAL, "comm_init: bad rank / size"};
+        PICGPU_CUDA_TRY(cudaSetDevice(device));
+        ncclUniqueId u;
+        std::memcpy(&u, id, 128);
+        auto* c = new picgpu_comm;
+        const ncclResult_t r = nccl().CommInitRank(&c->comm, nranks, u, rank);
+        if (r != ncclSuccess) {
+            delete c;
+            nccl_check(r, "ncclCommInitRank failed");
+        }
+        c->rank = rank;
+        c->nranks = nranks;
+        c->device = device;
+        c->owned = true;
+        *out = c;
+    });
+}
+
+int picgpu_comm_wrap(void* nccl_comm, int device, picgpu_comm** out) {
+    *out = nullptr;
+    return guard([&] {
+        if (!nccl_comm) throw Status{PICGPU_EINVAL, "comm_wrap: null communicator"};
+        auto* c = new picgpu_comm;
+        c->comm = static_cast<ncclComm_t>(nccl_comm);
+        const Nccl& N = nccl();
+        int n = 0, r = 0;
+        const ncclResult_t a = N.CommCount(c->comm, &n), b = N.CommUserRank(c->comm, &r);
+        if (a != ncclSuccess || b != ncclSuccess) {
+            delete c;
+            throw Status{PICGPU_ENCCL, "comm_wrap: not a usable ncclComm_t of this process's NCCL"};
+        }
+        c->nranks = n;
+        c->rank = r;
+        c->device = device;
+        *out = c;
+    });
+}
+
+int picgpu_comm_destroy(picgpu_comm* c) {
+    if (!c) return PICGPU_OK;
+    return guard([&] {
+        if (c->owned && c->comm) nccl().CommDestroy(c->comm);
+        delete c;
+    });
+}
+
+int picgpu_comm_rank(const picgpu_comm* c, int* rank, int* nranks) {
+    return guard([&] {
+        if (!c) throw Status{PICGPU_EINVAL, "comm_rank: null communicator"};
+        if (rank) *rank = c->rank;
+        if (nranks) *nranks = c->nranks;
+    });
+}
+
+int picgpu_session_set_comm(picgpu_session* s, picgpu_comm* c, uint32_t bucket_records) {
+    return guard([&] {
+        if (!s->slab) throw Status{PICGPU_ELOGIC, "set_comm: not a slab session (picgpu_session_set_slab first)"};
+        if (c && c->device != s->device) throw Status{PICGPU_EINVAL, "set_comm: communicator of another device"};
+        s->comm = c;
+        s->bucket = bucket_records ? bucket_records : 32768u;
+        set_device(s);
+        if (!s->hxcnt) PICGPU_CUDA_TRY(cudaMallocHost((void**)&s->hxcnt, 16));
+    });
+}
+
+// Send my `to_right` / `to_left` and receive `from_left` / `from_right` (ring
+// neighbours of the communicator) in one NCCL group on the session stream.
+// Issue order per peer is [right-going, left-coming, left-going, right-coming],
+// so the pairing holds when both neighbours are one rank (2 ranks) or this
+// rank itself (1 rank).
+static void ring_exchange(picgpu_session* s, const void* to_right, const void* to_left, void* from_left,
+                          void* from_right, size_t count_r, size_t count_l, size_t count_fl, size_t count_fr,
+                          ncclDataType_t type) {
+    const Nccl& N = nccl();
+    const picgpu_comm* c = s->comm;
+    const int L = (c->rank - 1 + c->nranks) % c->nranks, R = (c->rank + 1) % c->nranks;
+    nccl_check(N.GroupStart(), "ncclGroupStart failed");
+    if (count_r) nccl_check(N.Send(to_right, count_r, type, R, c->comm, s->st), "ncclSend failed");
+    if (count_fl) nccl_check(N.Recv(from_left, count_fl, type, L, c->comm, s->st), "ncclRecv failed");
+    if (count_l) nccl_check(N.Send(to_left, count_l, type, L, c->comm, s->st), "ncclSend failed");
+    if (count_fr) nccl_check(N.Recv(from_right, count_fr, type, R, c->comm, s->st), "ncclRecv failed");
+    nccl_check(N.GroupEnd(), "ncclGroupEnd failed");
+}
+
+// Guard-plane sums of J (and rho) over NCCL: planes [0, ghost) go left and
+// [ghost + own, 2 ghost + own) right, added into the neighbours' first / last
+// owned planes (picgpu_session_guard_planes + add_guard_planes, device-resident).
+static void exchange_planes(picgpu_session* s, int field) {
+    int comps = 0;
+    double* F = slab_field(s, field, comps);
+    const GridD& g = s->store.g;
+    const size_t np = (size_t)comps * s->ghost * g.ny * g.nz;
+    s->psend.ensure(2 * np * 8);
+    s->precv.ensure(2 * np * 8);
+    double* lo = s->psend.as<double>();
+    double* hi = lo + np;
+    double* fl = s->precv.as<double>();
+    double* fr = fl + np;
+    launch_pack_planes(F, comps, g.nx, g.ny, g.nz, 0, s->ghost, lo, s->st);
+    launch_pack_planes(F, comps, g.nx, g.ny, g.nz, s->ghost + s->own, s->ghost, hi, s->st);
+    ring_exchange(s, hi, lo, fl, fr, np, np, np, np, ncclFloat64);
+    launch_add_planes(F, comps, g.nx, g.ny, g.nz, s->ghost, s->ghost, fl, s->st);
+    launch_add_planes(F, comps, g.nx, g.ny, g.nz, s->own, s->ghost, fr, s->st);
+}
+
+int picgpu_session_slab_step(picgpu_session* s, double dt, uint32_t flags, picgpu_step_stats* out) {
+    return guard([&] {
+        set_device(s);
+        if (!s->slab || !s->comm) throw Status{PICGPU_ELOGIC, "slab_step: no communicator (picgpu_session_set_comm)"};
+        if (s->pending) throw Status{PICGPU_ELOGIC, "slab_step: a step_begin is pending"};
+        if (!(flags & PICGPU_STEP_SORT)) throw Status{PICGPU_EINVAL, "slab_step: SORT is required"};
+        BinStore& bs = s->store;
+        if (flags & PICGPU_STEP_DENSITY) check_density_grid(bs.hg, s->order);
+        const cudaStream_t st = s->st;
+        const bool T = s->timing;
+        const uint32_t B = s->bucket;
+        const double cap2 = (flags & PICGPU_STEP_PUSH) ? cap2_of(bs.hg, dt) : 0.0;
+        const uint64_t l0 = g_launches.load();
+        const uint64_t rebuilds0 = bs.rebuilds;
+        // room for the own movers and two buckets of arrivals; leaver records for a bucket
+        bs.ensure_movers(std::max<size_t>(size_t(1) << 16, bs.n / 4) + 2 * (size_t)B);
+        if (bs.lcap < B) {
+            bs.lrec.ensure((size_t)B * 2 * 8 * sizeof(double));
+            bs.lcap = B;
+        }
+        const uint32_t fuse_mask = PICGPU_STEP_PUSH | PICGPU_STEP_SORT | PICGPU_STEP_CURRENT;
+        const bool fused = (flags & fuse_mask) == fuse_mask && !(flags & PICGPU_STEP_UNFUSED) &&
+                           s->last_moved < s->fuse_max && fused_step_available(s->order, s->kernel);
+        if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[0], st));
+        if (fused) {
+            PICGPU_CUDA_TRY(cudaMemsetAsync(s->J.p, 0, (size_t)bs.g.ncells * 24, st));
+            bs.enqueue_fused(s->order, s->q, s->J.as<double>(), dt, cap2, T ? s->ev[4] : nullptr, /*migrate=*/false,
+                             s->kernel);
+        } else {
+            bs.enqueue_detect((flags & PICGPU_STEP_PUSH) != 0, dt, cap2);
+        }
+        if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[1], st));
+        // leaver counts and the first B records per side, device to device
+        StepCounters* ctr = bs.counters.as<StepCounters>();
+        s->xcnt.ensure(16);
+        s->xin.ensure((size_t)2 * B * 64);
+        uint32_t* xcnt = s->xcnt.as<uint32_t>();
+        double* xin = s->xin.as<double>();
+        const double* lrec = bs.lrec.as<double>();
+        ring_exchange(s, &ctr->nleave[1], &ctr->nleave[0], xcnt, xcnt + 1, 1, 1, 1, 1, ncclUint32);
+        ring_exchange(s, lrec + bs.lcap * 8, lrec, xin, xin + (size_t)B * 8, (size_t)B * 8, (size_t)B * 8,
+                      (size_t)B * 8, (size_t)B * 8, ncclFloat64);
+        bs.enqueue_import_dev(xin, xin + (size_t)B * 8, xcnt, B);
+        if (fused)  // the senders left their leavers out of the fused deposit
+            launch_deposit_records(s->order, bs.g, bs.M.soa(), ctr, kBaseFromCounters, s->q, s->J.as<double>(),
+                                   bs.num_sms, st);
+        bs.enqueue_migrate();  // (copies the counters to the host)
+        PICGPU_CUDA_TRY(cudaMemcpyAsync(s->hxcnt, xcnt, 8, cudaMemcpyDeviceToHost, st));
+        if (T) PICGPU_CUDA_TRY(cudaEventRecord(s->ev[2], st));
+        // ---- the step's one host synchronisation
+        PICGPU_CUDA_TRY(cudaStreamSynchronize(st));
+        StepCounters c1 = *bs.hcounters;
+        if (c1.err) throw_step_error(c1.err);
+        const uint32_t got_l = s->hxcnt[0], got_r = s->hxcnt[1];
+        const uint64_t sent = (uint64_t)c1.nleave[0] + c1.nleave[1];
+        bs.n = bs.n - sent + c1.nimport;
+        if (T) {
+            if (fused) {
+                accumulate_phase(s, 3, 0, 4, 1);
+                accumulate_phase(s, 0, 4, 2, g_launches.load() - l0 - 1);
+            } else {
+                accumulate_phase(s, 0, 0, 2, g_launches.load() - l0);
+            }
+        }
+        const bool movers_lost = c1.nmovers > bs.mcap || c1.mover_drop > 0;
+        StepCounters c{};
+        bool rebuilt = bs.finish_incremental(c);
+        if (c.err) throw_step_error(c.err);
+        uint64_t imported = c1.nimport;
+        // ---- rare: a side sent more than its bucket -> the remainder, exactly sized
+        const uint32_t rs_r = c1.nleave[1] > B ? c1.nleave[1] - B : 0, rs_l = c1.nleave[0] > B ? c1.nleave[0] - B : 0;
+        const uint32_t rr_l = got_l > B ? got_l - B : 0, rr_r = got_r > B ? got_r - B : 0;
+        if (rs_r | rs_l | rr_l | rr_r) {
+            const uint32_t nrem = rr_l + rr_r;
+            s->xin2.ensure(((size_t)nrem + 1) * 64);
+            double* x2 = s->xin2.as<double>();
+            ring_exchange(s, lrec + (bs.lcap + B) * 8, lrec + (size_t)B * 8, x2, x2 + (size_t)rr_l * 8,
+                          (size_t)rs_r * 8, (size_t)rs_l * 8, (size_t)rr_l * 8, (size_t)rr_r * 8, ncclFloat64);
+            PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
+            bs.ensure_movers_keep(std::max<size_t>(bs.mcap, nrem + nrem / 4), 0);
+            bs.enqueue_import(x2, nrem, 0);
+            if (fused)
+                launch_deposit_records(s->order, bs.g, bs.M.soa(), ctr, 0, s->q, s->J.as<double>(), bs.num_sms, st);
+            bs.enqueue_migrate();
+            bs.n += nrem;
+            imported += nrem;
+            StepCounters c2{};
+            rebuilt |= bs.finish_incremental(c2);
+            if (c2.err) throw_step_error(c2.err);
+        }
+        picgpu_step_stats stats{};
+        stats.moved = c1.moved;
+        stats.inserts = std::min<uint64_t>(c1.nmovers, bs.mcap) + imported;
+        stats.overflowed = c.noverflow;
+        uint32_t dflags = flags;
+        if (fused) {
+            stats.fused = 1;
+            if (!(rebuilt && movers_lost)) dflags &= ~PICGPU_STEP_CURRENT;  // J complete
+        }
+        uint64_t lj = 0, lr = 0;
+        enqueue_deposits(s, dflags, &lj, &lr);
+        if (flags & PICGPU_STEP_CURRENT) exchange_planes(s, 0);
+        if (flags & PICGPU_STEP_DENSITY) exchange_planes(s, 1);
+        if (flags & PICGPU_STEP_PUSH) s->last_moved = bs.n ? (double)stats.moved / (double)bs.n : 0.0;
+        stats.rebuilt = bs.rebuilds != rebuilds0;
+        stats.capacity = bs.capacity;
+        stats.num_particles = bs.n;
+        stats.empty_slot_ratio = bs.capacity ? (double)(bs.capacity - bs.n) / (double)bs.capacity : 1.0;
+        if (out) *out = stats;
+        // no trailing synchronisation: the deposits and the plane exchange stay
+        // enqueued on the session stream (downloads and the next step follow them)
     });
 }

@@ -210,6 +210,9 @@ struct StepCounters {
     // segment (ovf_movers, global atomic); beyond that they are dropped (-> full re-sort)
     unsigned int ovf_movers;
     unsigned int mover_drop;
+    // device-resident slab exchange (picgpu_session_slab_step)
+    unsigned int import_left;  // arrivals from the left (the right ones follow them)
+    unsigned int ovf_import;   // bit 0/1: the left/right neighbour sent more than the bucket
 };
 
 // floor((x - o) / h) exactly as locate_axis computes it (before its range

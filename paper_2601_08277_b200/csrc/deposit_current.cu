@@ -1462,6 +1462,7 @@ __global__ void __launch_bounds__(256) k_deposit_records(const GridD g, const So
                                                          double* __restrict__ jy, double* __restrict__ jz) {
     constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
     const uint64_t n = ctr->nimport;
+    if (base == kBaseFromCounters) base = ctr->nmovers;  // device-resident exchange: base set by k_import_plan
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * W;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t i = base + t / W;

@@ -62,6 +62,7 @@ void launch_pencil_current_push(int order, const GridD& g, PushCtx& pc, const ui
 // Slab arrivals (mover records M[base .. base+n), appended by the import)
 // deposited over their full window (RED.ADD.F64): the sender's fused pass
 // left them out.
+constexpr uint32_t kBaseFromCounters = 0xFFFFFFFFu;  // launch_deposit_records: arrivals start at ctr->nmovers
 void launch_deposit_records(int order, const GridD& g, const Soa& M, const StepCounters* ctr, uint32_t base,
                             double q, double* j, int num_sms, cudaStream_t st);
 // Movers of the fused kernel: slot -> mover record M[i] (+ hole in the old bin)

@@ -749,6 +749,56 @@ __global__ void k_import(const GridD g, const double* __restrict__ rec, uint32_t
     mcell[d] = c;
 }
 
+// Arrivals of a device-resident exchange (picgpu_session_slab_step): the
+// counts came with the records (cnt[0] from the left, cnt[1] from the right),
+// so the host never reads them.  k_import_plan fixes the list: own movers
+// [0, base), base = min(nmovers, mcap), then min(cnt, B) records per side;
+// a side that sent more than its bucket B raises ovf_import (the host
+// finishes those in a second, exactly sized round).
+__global__ void k_import_plan(const uint32_t* __restrict__ cnt, uint32_t B, uint32_t mcap, StepCounters* ctr) {
+    const uint32_t base = min(ctr->nmovers, mcap);
+    const uint32_t nl = min(cnt[0], B), nr = min(cnt[1], B);
+    if (ctr->nmovers > mcap) ctr->mover_drop += ctr->nmovers - mcap;  // unrecorded own movers -> full re-sort
+    ctr->nmovers = base;
+    if (base + nl + nr > mcap) {  // the host sized the mover buffers for 2B arrivals: never
+        raise_error(&ctr->err, PICGPU_ELENGTH);
+        ctr->nimport = 0;
+        return;
+    }
+    ctr->nimport = nl + nr;
+    ctr->import_left = nl;
+    ctr->ovf_import = (cnt[0] > B ? 1u : 0u) | (cnt[1] > B ? 2u : 0u);
+}
+
+__global__ void k_import_dev(const GridD g, const double* __restrict__ from_left, const double* __restrict__ from_right,
+                             uint32_t B, const Soa M, uint32_t* __restrict__ mcell, StepCounters* ctr) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t nl = ctr->import_left, n = ctr->nimport;
+    if (t >= 2 * B) return;
+    const bool right = t >= B;
+    const uint32_t j = right ? t - B : t;
+    const uint32_t i = right ? nl + j : j;  // rank in the arrival list
+    if (right ? (i >= n) : (j >= nl)) return;
+    const double* r = (right ? from_right : from_left) + (size_t)j * 8;
+    const double x = r[0], y = r[1], z = r[2];
+    uint32_t c = 0;
+    if (!finite3(x, y, z)) {
+        raise_error(&ctr->err, PICGPU_EINVAL);
+    } else {
+        c = store_cell(g, x, y, z);
+        if (c >= kLeaveRight) {  // routed to the wrong slab
+            raise_error(&ctr->err, PICGPU_EINVAL);
+            c = 0;
+        }
+    }
+    const uint32_t d = ctr->nmovers + i;
+    M.x[d] = x; M.y[d] = y; M.z[d] = z;
+    M.vx[d] = r[3]; M.vy[d] = r[4]; M.vz[d] = r[5];
+    M.w[d] = r[6];
+    M.id[d] = (uint64_t)__double_as_longlong(r[7]);
+    mcell[d] = c;
+}
+
 // Guard planes of a slab's field (comps arrays of nx*ny*nz, x fastest):
 // planes [p0, p0+np) packed as [comp][plane][z][y].
 __global__ void k_pack_planes(const double* __restrict__ F, int comps, int nx, int ny, int nz, int p0, int np,
@@ -1324,6 +1374,15 @@ void BinStore::enqueue_import(const double* rec_dev, uint32_t nimp, uint32_t bas
     k_import<<<div_up((long long)std::max<uint32_t>(nimp, 1u), 256), 256, 0, st>>>(
         g, rec_dev, nimp, base, M.soa(), mcell.as<uint32_t>(), counters.as<StepCounters>());
     note_launch();
+    PICGPU_CUDA_TRY(cudaGetLastError());
+}
+
+void BinStore::enqueue_import_dev(const double* from_left, const double* from_right, const uint32_t* cnt_dev,
+                                  uint32_t B) {
+    k_import_plan<<<1, 1, 0, st>>>(cnt_dev, B, (uint32_t)mcap, counters.as<StepCounters>());
+    k_import_dev<<<div_up(2ll * B, 256), 256, 0, st>>>(g, from_left, from_right, B, M.soa(), mcell.as<uint32_t>(),
+                                                      counters.as<StepCounters>());
+    note_launch(2);
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
 

@@ -125,6 +125,9 @@ struct BinStore {
     // insert, borrow).
     void enqueue_detect(bool push, double dt, double cap2);
     void enqueue_import(const double* rec_dev, uint32_t n, uint32_t base);
+    // arrivals from a device-resident exchange: counts on the device (cnt_dev[0]
+    // from the left, [1] from the right), at most B records per side
+    void enqueue_import_dev(const double* from_left, const double* from_right, const uint32_t* cnt_dev, uint32_t B);
     void enqueue_migrate();
     // Synchronises, reads the counters and, if an arrival found no slack even
     // after borrowing (or the mover buffer overflowed), rebuilds by a full

@@ -221,6 +221,57 @@ def slab_step(sess: SlabSession, ring: RingExchange, dt: float, flags: int = STE
     return stats
 
 
+class NcclComm:
+    """A communicator of the library's own NCCL path (picgpu_comm_*): rank 0's
+    unique id is broadcast over the host application's process group (any
+    torch.distributed backend), then every rank joins.  Slab r of the
+    decomposition belongs to rank r of this communicator."""
+
+    def __init__(self, device: int = 0, group=None, world: int | None = None, rank: int | None = None):
+        torch = _torch()
+        import torch.distributed as dist
+
+        up = dist.is_available() and dist.is_initialized()
+        self.world = world if world is not None else (dist.get_world_size(group) if up else 1)
+        self.rank = rank if rank is not None else (dist.get_rank(group) if up else 0)
+        uid = np.zeros(128, np.uint8)
+        if self.rank == 0:
+            _check(lib().picgpu_comm_unique_id(uid.ctypes.data_as(C.c_void_p)))
+        if self.world > 1:
+            backend = dist.get_backend(group)
+            t = torch.from_numpy(uid.copy())
+            if backend == "nccl":
+                t = t.to(torch.device("cuda", device))
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast(t, src=src, group=group)
+            uid = t.cpu().numpy().astype(np.uint8)
+        self._h = C.c_void_p()
+        _check(lib().picgpu_comm_init(uid.ctypes.data_as(C.c_void_p), self.world, self.rank, device,
+                                      C.byref(self._h)))
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().picgpu_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+
+def attach_comm(sess: SlabSession, comm: NcclComm, bucket: int = 0):
+    """picgpu_session_set_comm: the session's exchanges go through `comm`."""
+    _check(lib().picgpu_session_set_comm(sess._h, comm._h, bucket))
+    sess._comm = comm  # keep it alive
+
+
+def nccl_slab_step(sess: SlabSession, dt: float, flags: int = STEP_DEFAULT) -> dict:
+    """One slab step entirely behind the C ABI (picgpu_session_slab_step):
+    exchanges over NCCL on the session stream, one host synchronisation."""
+    st = StepStats()
+    _check(lib().picgpu_session_slab_step(sess._h, dt, flags, C.byref(st)))
+    return st.as_dict()
+
+
 def local_ring_step(sessions: list[SlabSession], dt: float, flags: int = STEP_DEFAULT) -> list[dict]:
     """The same step for P slab sessions driven in lockstep by one process
     (single-GPU validation of the decomposition; the exchanges are device

@@ -145,3 +145,56 @@ def test_slab_upload_owned_and_errors(pg, orc):
     bad = pg.Session(slab_grid(G, 0, 6), 3)  # grid of another slab
     with pytest.raises(pg.InvalidArgument):
         pg._check(pg.lib().picgpu_session_set_slab(bad._h, C.byref(G), 0, 8, 2))
+
+
+@pytest.mark.parametrize("order,bucket,uth", [(3, 0, 0.6), (1, 0, 0.6), (3, 16, 0.6), (2, 0, 0.02)])
+def test_nccl_slab_step_matches_undecomposed(pg, order, bucket, uth):
+    """The whole slab step behind the C ABI (picgpu_session_slab_step): leaver
+    counts and records over NCCL on the session stream (a one-rank ring: this
+    rank is both neighbours), arrivals imported from device-side counts, guard
+    planes summed over NCCL.  Against the undecomposed session: particles
+    bit-exact, J <= 1e-12, rho <= 1e-13.  bucket 16: most leavers travel in the
+    second, exactly sized round.  u_th 0.02: the fused step (low migration)."""
+    import oracle
+    from paper_2601_08277_b200.slab import NcclComm, SlabSession, attach_comm, nccl_slab_step
+
+    G = _grid(pg)
+    flags = pg.STEP_DEFAULT | pg.STEP_DENSITY
+    ref = pg.Session(G, order)
+    ref.generate_plasma(4, uth, seed=7)
+    comm = NcclComm(device=0, world=1, rank=0)
+    s = SlabSession(G, 0, G.nx, order=order)
+    s.generate_plasma(4, uth, seed=7)
+    attach_comm(s, comm, bucket)
+    fused = 0
+    for step in range(6):
+        want = ref.step(0.5, flags)
+        got = nccl_slab_step(s, 0.5, flags)
+        fused += got["fused"]
+        assert got["moved"] == want["moved"] and got["num_particles"] == want["num_particles"], step
+        a, b = _union([s]), _sorted(ref.particles())
+        for k in b:
+            assert np.array_equal(a[k], b[k]), (step, k)
+        J = _assemble([s], "J")
+        Jr = ref.current()
+        assert oracle.peak_rel_err(J, (Jr.jx, Jr.jy, Jr.jz)) <= 1e-12, step
+        rho = _assemble([s], "rho")
+        assert np.abs(rho - ref.density()).max() <= 1e-13 * np.abs(ref.density()).max(), step
+    if uth < 0.1:
+        assert fused == 6
+    comm.close()
+
+
+def test_nccl_slab_step_errors(pg):
+    from paper_2601_08277_b200.slab import SlabSession, nccl_slab_step
+
+    G = _grid(pg)
+    s = SlabSession(G, 0, G.nx, order=3)
+    s.generate_plasma(2, 0.1, seed=1)
+    with pytest.raises(pg.LogicError):  # no communicator attached
+        nccl_slab_step(s, 0.5)
+    plain = pg.Session(G, 3)
+    from paper_2601_08277_b200 import _check, lib
+
+    with pytest.raises(pg.LogicError):  # not a slab session
+        _check(lib().picgpu_session_set_comm(plain._h, None, 0))
