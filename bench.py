@@ -62,13 +62,13 @@ CONFIGS = {
     "c3o1": (256, 32, 1, 0.1, 0.5, 5, "C3: 256^3 cells, 32 ppc, order 1, u_th 0.1, dt 0.5"),
     "c3o2": (256, 32, 2, 0.1, 0.5, 5, "C3: 256^3 cells, 32 ppc, order 2 (TSC), u_th 0.1, dt 0.5"),
     "c3o3": (256, 32, 3, 0.1, 0.5, 5, "C3: 256^3 cells, 32 ppc, order 3, u_th 0.1, dt 0.5"),
-    "c4": ((512, 128, 128), 8, 3, 0.01, 0.5, 10,
+    "c4": ((512, 128, 128), 8, 3, 0.01, 0.5, 100,
            "C4 (LWFA-like, static window): 512x128x128 cells, order 3, electrons from x-cell 64 with a linear "
            "density ramp over [64,128) to 8 ppc, u_th 0.01, plus a 10% beam with ux ~ U(5,50) in x-cells "
            "[128,160); dt 0.5; moving window: origin +1 cell every 2 steps, back column dropped, a fresh 8-ppc "
            "column injected at the front (inside the timed region)"),
     # strong scaling over x-slabs; needs N >= 4 B200s (2.1e9 particles)
-    "c5": ((2048, 256, 256), 16, 3, 0.05, 0.5, 10,
+    "c5": ((2048, 256, 256), 16, 3, 0.05, 0.5, 50,
            "C5: 2048x256x256 cells, 16 ppc, order 3, u_th 0.05, dt 0.5, x-slabs of 2048/N cells per GPU "
            "(strong scaling)"),
 }
@@ -323,6 +323,9 @@ def main():
     ap.add_argument("--no-orders", dest="orders", action="store_false",
                     help="skip the per-order (1/2/3) runs on the same box")
     ap.add_argument("--slab", action="store_true", help="use the slab-decomposed path even at N=1 (loopback ring)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "torch"],
+                    help="slab exchanges: nccl = picgpu_session_slab_step (NCCL behind the C ABI, one host sync per "
+                         "step); torch = the Python protocol over torch.distributed (slab.py slab_step)")
     ap.add_argument("--sort", default="incremental", choices=["incremental", "resort"],
                     help="incremental: bins with slack + migration (default); resort: a full stable counting "
                          "sort of the store every step (global_sort each step; the crossover study of C3)")
@@ -369,6 +372,8 @@ def main():
     fp64_peak = pg.fp64_peak_tflops(local)
     hbm_peak, hbm_src = peaks()
 
+    comm_box = [None]  # one NCCL communicator for every session of the run
+
     def open_session(order):
         if single:
             S = pg.Session(grid, order=order, device=local, timing=True)
@@ -387,8 +392,16 @@ def main():
             else:  # weak scaling: a C2-sized slab per rank
                 G = pg.Grid.make(nx * world, nx, nx)
                 S = SlabSession(G, rank * nx, (rank + 1) * nx, order=order, device=local, timing=True)
-            ring = RingExchange()
-            step = lambda: slab_step(S, ring, dt)  # noqa: E731
+            if args.exchange == "nccl":  # the whole slab step behind the C ABI (NCCL on the session stream)
+                from paper_2601_08277_b200.slab import NcclComm, attach_comm, nccl_slab_step
+
+                if comm_box[0] is None:
+                    comm_box[0] = NcclComm(device=local)
+                attach_comm(S, comm_box[0])
+                step = lambda: nccl_slab_step(S, dt)  # noqa: E731
+            else:
+                ring = RingExchange()
+                step = lambda: slab_step(S, ring, dt)  # noqa: E731
         populate(pg, S, args.config, ppc, u_th)
         return S, step
 
@@ -598,7 +611,7 @@ def main():
                        "l2": f"inputs larger than L2 ({res['n'] * 64 / 1e9:.1f} GB particle store)",
                        "parallelism": "single" if world == 1 else
                        f"x-slabs x{world} of a {'x'.join(map(str, G_dims))} box, NCCL ring exchange "
-                       "(migration + J guards)"},
+                       f"(migration + J guards; {'picgpu_session_slab_step' if args.exchange == 'nccl' else 'torch.distributed'})"},
             "roofline": res["roofline"], "step_roofline_frac": res["step_roofline_frac"], "orders": orders,
             "cpu_baseline": cpu, "e2e": e2e, "e2e_session": e2e_session, "gpu_launches": res["launches"],
             "clocks": res["clocks"], "selfcheck": check,
@@ -606,6 +619,8 @@ def main():
             "moved_fraction": res["moved_fraction"], "rebuilds": res["rebuilds"], "fused_steps": res["fused_steps"],
         }
         print(json.dumps(line))
+    if comm_box[0] is not None:
+        comm_box[0].close()
     if dist is not None:
         dist.destroy_process_group()
     return 0
