@@ -274,6 +274,11 @@ PICGPU_API int picgpu_session_set_kernel(picgpu_session* s, int family);
  * previous pushed step moved less than this fraction of the particles (default
  * 0.06, or PICGPU_FUSE_MAX_MOVED); 0 never fuses, >1 always does.  EINVAL if
  * negative or NaN.  No reference counterpart (a performance knob). */
+/* Adaptive slack (off by default): an overflow rebuild within 4 pushed steps
+ * of the previous one doubles the gap ratio of every later layout (up to 1.0).
+ * For persistent inflow (C4's beam); capacities then differ from the
+ * reference's Gpma after such rebuilds (bin SETS do not). */
+PICGPU_API int picgpu_session_set_adaptive_slack(picgpu_session* s, int enable);
 PICGPU_API int picgpu_session_set_fusion(picgpu_session* s, double max_moved_fraction);
 
 /* pic::WorkloadConfig (workload.hpp:16-44) and make_workload (:75-125): ppc

@@ -373,6 +373,92 @@ class Session {
     picgpu_session* h_ = nullptr;
 };
 
+// ---- multi-GPU: x-slab sessions over NCCL (no reference counterpart) -------
+// One process per GPU.  Rank 0 makes the id, the host's launcher broadcasts it
+// (MPI_Bcast, a file, torch.distributed ...), every rank joins:
+//   auto id = picgpu::Comm::unique_id();            // rank 0
+//   /* broadcast id */
+//   picgpu::Comm comm(id, nranks, rank, device);
+//   auto [x0, x1] = picgpu::slab_range(g.nx, nranks, rank);
+//   picgpu::SlabSession S(g, x0, x1, picgpu::ShapeOrder::qsp, comm);
+//   S.upload(owned_particles); for (...) S.step(dt);  // one host sync per step
+class Comm {
+   public:
+    using Id = std::array<unsigned char, 128>;
+    static Id unique_id() {
+        Id id{};
+        check(picgpu_comm_unique_id(id.data()));
+        return id;
+    }
+    Comm(const Id& id, int nranks, int rank, int device) { check(picgpu_comm_init(id.data(), nranks, rank, device, &c_)); }
+    ~Comm() { picgpu_comm_destroy(c_); }
+    Comm(const Comm&) = delete;
+    Comm& operator=(const Comm&) = delete;
+    picgpu_comm* handle() const { return c_; }
+
+   private:
+    picgpu_comm* c_ = nullptr;
+};
+
+inline std::pair<int, int> slab_range(int nx, int nranks, int rank) {  // balanced contiguous split
+    const int base = nx / nranks, rem = nx % nranks;
+    const int x0 = rank * base + std::min(rank, rem);
+    return {x0, x0 + base + (rank < rem ? 1 : 0)};
+}
+
+class SlabSession {
+   public:
+    SlabSession(const GridSpec& global, int x0, int x1, ShapeOrder order, Comm& comm, GpmaConfig gc = {},
+                int device = 0, int ghost = 2, std::uint32_t bucket_records = 0)
+        : global_(global) {
+        const picgpu_grid G = global.c();
+        picgpu_grid L{};
+        check(picgpu_slab_grid(&G, x0, x1, ghost, &L));
+        local_ = GridSpec{L.nx, L.ny, L.nz, L.dx, L.dy, L.dz, {L.ox, L.oy, L.oz}};
+        const picgpu_session_config cfg{static_cast<int32_t>(order), device, gc.gap_ratio, gc.min_gap, 0u};
+        check(picgpu_session_create(&L, &cfg, &h_));
+        check(picgpu_session_set_slab(h_, &G, x0, x1, ghost));
+        check(picgpu_session_set_comm(h_, comm.handle(), bucket_records));
+    }
+    ~SlabSession() { picgpu_session_destroy(h_); }
+    SlabSession(const SlabSession&) = delete;
+    SlabSession& operator=(const SlabSession&) = delete;
+    void upload(const ParticleSoA& s) {  // particles of the owned cells, global coordinates
+        check(picgpu_session_upload(h_, s.size(), s.x.data(), s.y.data(), s.z.data(), s.vx.data(), s.vy.data(),
+                                    s.vz.data(), s.w.data(), s.id.empty() ? nullptr : s.id.data(), s.q));
+    }
+    picgpu_step_stats step(double dt, std::uint32_t flags = PICGPU_STEP_DEFAULT) {  // collective
+        picgpu_step_stats st{};
+        check(picgpu_session_slab_step(h_, dt, flags, &st));
+        return st;
+    }
+    CurrentGrid current() const {  // the slab grid's J (owned planes complete after the step)
+        CurrentGrid g(local_);
+        check(picgpu_session_download_current(h_, g.jx.data(), g.jy.data(), g.jz.data()));
+        return g;
+    }
+    picgpu_session* handle() const { return h_; }
+
+   private:
+    GridSpec global_, local_;
+    picgpu_session* h_ = nullptr;
+};
+
+// ---- charge-conserving current (an extension; no reference counterpart) ----
+// Esirkepov J on the Yee faces for particles moved from `before` to `after`
+// (same order of particles); see picgpu_deposit_current_esirkepov.
+inline CurrentGrid deposit_current_esirkepov(const ParticleSoA& before, const ParticleSoA& after, const GridSpec& g,
+                                             ShapeOrder order, double dt) {
+    if (before.size() != after.size()) throw std::invalid_argument("deposit_current_esirkepov: size mismatch");
+    CurrentGrid J(g);
+    const picgpu_grid cg = g.c();
+    check(picgpu_deposit_current_esirkepov(&cg, static_cast<int>(order), before.x.data(), before.y.data(),
+                                           before.z.data(), after.x.data(), after.y.data(), after.z.data(),
+                                           before.w.data(), before.q, dt, before.size(), J.jx.data(), J.jy.data(),
+                                           J.jz.data()));
+    return J;
+}
+
 // ---- the reference's harness loop (simulation.hpp:19-176) -------------------
 
 enum class AblationMode {

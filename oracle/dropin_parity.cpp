@@ -323,6 +323,42 @@ int main() {
         }
     }
 
+    // multi-GPU C++ host path (no reference counterpart): a one-rank NCCL ring
+    // slab session steps like the whole-box session
+    {
+        picgpu::GridSpec gg{16, 8, 8, 1.0, 1.0, 1.0, {0.0, 0.0, 0.0}};
+        pic::WorkloadConfig wc;
+        wc.grid.nx = 16; wc.grid.ny = 8; wc.grid.nz = 8;
+        wc.ppc = 4;
+        wc.thermal_speed = 0.3;
+        wc.seed = 3;
+        const picgpu::ParticleSoA init = to_gpu(pic::make_workload(wc));
+        picgpu::Session whole(gg, picgpu::ShapeOrder::qsp);
+        whole.upload(init);
+        const auto id = picgpu::Comm::unique_id();
+        picgpu::Comm comm(id, 1, 0, 0);
+        picgpu::SlabSession slab(gg, 0, 16, picgpu::ShapeOrder::qsp, comm);
+        slab.upload(init);
+        bool same = true;
+        for (int k = 0; k < 3; ++k) {
+            const auto a = whole.step(0.5), b = slab.step(0.5);
+            same = same && a.moved == b.moved && a.num_particles == b.num_particles;
+        }
+        const picgpu::CurrentGrid Jw = whole.current(), Js = slab.current();
+        double peak = 0.0, d = 0.0;  // owned planes x in [2, 18) of the slab grid = the whole box
+        for (int k = 0; k < 8; ++k)
+            for (int j = 0; j < 8; ++j)
+                for (int i = 0; i < 16; ++i) {
+                    const std::size_t w = i + 16 * (j + 8 * k), sidx = (i + 2) + 20 * (j + 8 * k);
+                    peak = std::max(peak, std::abs(Jw.jx[w]));
+                    d = std::max(d, std::abs(Jw.jx[w] - Js.jx[sidx]));
+                }
+        char msg[160];
+        std::snprintf(msg, sizeof msg, "picgpu::SlabSession over a one-rank NCCL ring: moved/count %s, jx err %.2e",
+                      same ? "same" : "DIFF", peak > 0 ? d / peak : d);
+        expect(same && d <= 1e-12 * peak, msg);
+    }
+
     std::printf("%s (%d failures)\n", failures ? "DROP-IN PARITY FAILED" : "drop-in parity ok", failures);
     return failures ? 1 : 0;
 }

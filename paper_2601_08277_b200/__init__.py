@@ -224,6 +224,7 @@ def lib():
     L.picgpu_kernel_launches.restype = _U64
     L.picgpu_deposit_current.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, _P, _P, _P]
     L.picgpu_deposit_current_dev.argtypes = [G, C.c_int] + [_P] * 7 + [_D, _U64, _P, _P, _P, _P]
+    L.picgpu_session_set_adaptive_slack.argtypes = [_P, C.c_int]
     L.picgpu_comm_unique_id.argtypes = [_P]
     L.picgpu_comm_init.argtypes = [_P, C.c_int, C.c_int, C.c_int, _P]
     L.picgpu_comm_wrap.argtypes = [_P, C.c_int, _P]
@@ -595,6 +596,10 @@ class Session:
     def set_kernel(self, family: int):
         """J kernel family: KERNEL_LANE (default), KERNEL_VECTOR (warp DFMA), KERNEL_MATRIX (DMMA)."""
         _check(lib().picgpu_session_set_kernel(self._h, family))
+
+    def set_adaptive_slack(self, enable: bool = True):
+        """picgpu_session_set_adaptive_slack: rebuild storms widen later layouts' gap ratio."""
+        _check(lib().picgpu_session_set_adaptive_slack(self._h, int(enable)))
 
     def set_fusion(self, max_moved_fraction: float):
         """Fuse push + detect + J while the previous step moved less than this

@@ -219,6 +219,9 @@ struct picgpu_session {
     uint64_t nleave[2] = {0, 0};
     StepCounters cbegin{};
     uint64_t begin_launches = 0;
+    // adaptive slack (picgpu_session_set_adaptive_slack): rebuild storms widen the gap ratio
+    bool adaptive_slack = false;
+    uint32_t since_rebuild = 1000;  // pushed steps since the last rebuild
     // device-resident exchange over NCCL (picgpu_session_set_comm / slab_step)
     picgpu_comm* comm = nullptr;
     uint32_t bucket = 0;            // records per side per step in the first exchange round
@@ -824,6 +827,8 @@ static void enqueue_deposits(picgpu_session* s, uint32_t flags, uint64_t* lj, ui
 // counters are read once after the sort kernels (one host wait per step):
 // when an arrival found no slack even after borrowing, the bins are rebuilt
 // before anything is deposited on them.
+static void adapt_slack(picgpu_session* s, bool rebuilt, bool pushed);
+
 int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_step_stats* out) {
     return guard([&] {
         set_device(s);
@@ -951,11 +956,31 @@ int picgpu_session_step(picgpu_session* s, double dt, uint32_t flags, picgpu_ste
         if (flags & PICGPU_STEP_PUSH)
             s->last_moved = bs.n ? (double)stats.moved / (double)bs.n : 0.0;
         stats.rebuilt = bs.rebuilds != rebuilds0;
+        adapt_slack(s, stats.rebuilt != 0, (flags & PICGPU_STEP_PUSH) != 0);
         stats.capacity = bs.capacity;
         stats.num_particles = bs.n;
         stats.empty_slot_ratio = bs.capacity ? (double)(bs.capacity - bs.n) / (double)bs.capacity : 1.0;
         if (out) *out = stats;
     });
+}
+
+// Rebuild storm (an overflow rebuild within 4 pushed steps of the previous
+// one): the gap ratio of every later layout (rebuild, window shift, global
+// sort) doubles, up to 1.0 (Gpma::layout's rule with a larger gap_ratio,
+// gpma.hpp:274-281).  Off by default: capacities then follow the reference.
+static void adapt_slack(picgpu_session* s, bool rebuilt, bool pushed) {
+    if (!s->adaptive_slack || !pushed) return;
+    if (rebuilt) {
+        BinStore& bs = s->store;
+        if (s->since_rebuild <= 4) bs.onepg = 1.0 + std::min(1.0, 2.0 * (bs.onepg - 1.0) + 0.05);
+        s->since_rebuild = 0;
+    } else if (s->since_rebuild < 1000) {
+        ++s->since_rebuild;
+    }
+}
+
+int picgpu_session_set_adaptive_slack(picgpu_session* s, int enable) {
+    return guard([&] { s->adaptive_slack = enable != 0; });
 }
 
 int picgpu_session_set_fusion(picgpu_session* s, double max_moved_fraction) {
@@ -1269,6 +1294,7 @@ int picgpu_session_step_end(picgpu_session* s, const double* arrivals, uint64_t 
         if (flags & PICGPU_STEP_PUSH)
             s->last_moved = bs.n ? (double)stats.moved / (double)bs.n : 0.0;
         stats.rebuilt = bs.rebuilds != rebuilds0;
+        adapt_slack(s, stats.rebuilt != 0, (flags & PICGPU_STEP_PUSH) != 0);
         stats.capacity = bs.capacity;
         stats.num_particles = bs.n;
         stats.empty_slot_ratio = bs.capacity ? (double)(bs.capacity - bs.n) / (double)bs.capacity : 1.0;
@@ -1594,6 +1620,7 @@ int picgpu_session_slab_step(picgpu_session* s, double dt, uint32_t flags, picgp
         if (flags & PICGPU_STEP_DENSITY) exchange_planes(s, 1);
         if (flags & PICGPU_STEP_PUSH) s->last_moved = bs.n ? (double)stats.moved / (double)bs.n : 0.0;
         stats.rebuilt = bs.rebuilds != rebuilds0;
+        adapt_slack(s, stats.rebuilt != 0, (flags & PICGPU_STEP_PUSH) != 0);
         stats.capacity = bs.capacity;
         stats.num_particles = bs.n;
         stats.empty_slot_ratio = bs.capacity ? (double)(bs.capacity - bs.n) / (double)bs.capacity : 1.0;

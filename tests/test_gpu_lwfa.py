@@ -135,3 +135,36 @@ def test_moving_window_shift(pg, orc):
         p2 = S.particles()
         o2, w2 = np.argsort(p2.id), np.argsort(ref["id"])
         assert np.array_equal(p2.x[o2], ref["x"][w2])
+
+
+def test_adaptive_slack_keeps_lockstep_and_cuts_rebuilds(pg, orc):
+    """picgpu_session_set_adaptive_slack: a rebuild storm (the beam flowing into
+    bins sized at the last layout) widens the gap ratio of later layouts.  The
+    particles, their bins and J stay in lockstep with the oracle; the session
+    rebuilds no more often than one with the reference's fixed slack."""
+    G, c = _cfg(pg)
+    runs = {}
+    for adaptive in (False, True):
+        S = pg.Session(G, 3)
+        if adaptive:
+            S.set_adaptive_slack(True)
+        S.generate_lwfa(c)
+        p = S.particles()
+        ref = {k: getattr(p, k).copy() for k in ("x", "y", "z", "vx", "vy", "vz", "w", "id")}
+        rebuilds = 0
+        for step in range(16):
+            g = O.Grid.make(G.nx, G.ny, G.nz, dx=G.dx, dy=G.dy, dz=G.dz, origin=(S.grid.ox, S.grid.oy, S.grid.oz))
+            st = S.step(0.5)
+            assert st["moved"] == orc.advance(g, 0.5, ref)
+            rebuilds += st["rebuilt"]
+        got = S.particles()
+        o, w = np.argsort(got.id), np.argsort(ref["id"])
+        for k in ("x", "y", "z"):
+            assert np.array_equal(getattr(got, k)[o], ref[k][w]), k
+        off, cnt = S.bins()
+        cells = np.repeat(np.arange(G.ncells, dtype=np.uint32), cnt.astype(np.int64))
+        assert np.array_equal(cells, orc.cells(g, {"x": got.x, "y": got.y, "z": got.z}))
+        J = S.current()
+        assert peak_rel_err((J.jx, J.jy, J.jz), orc.deposit_current(g, 3, ref, -1.0)) <= 1e-12
+        runs[adaptive] = rebuilds
+    assert runs[True] <= runs[False]
