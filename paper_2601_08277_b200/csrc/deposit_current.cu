@@ -65,11 +65,14 @@ struct JCfg;
 #ifndef PICGPU_CIC_MINB
 #define PICGPU_CIC_MINB 4
 #endif
-// CIC's fused pass is bound by the latency of its record loads (issue 22%,
-// long-scoreboard 9.9 per issue with one record prefetched per lane): the
-// records come through a per-lane cp.async ring RING deep instead.
+// RING > 0: the records come through a per-lane cp.async ring RING deep
+// instead of one register prefetch.  Measured at C2 size, fused step: CIC
+// 1.466 ms (RING 4), 1.478 (3) vs 1.403 (0); QSP 1.751 (3) vs 1.615 (0) --
+// long-scoreboard stalls fall (9.9 -> 4.3 per issue) but shared-memory
+// pressure rises (short scoreboard 5.0, mio throttle 2.0, 33% bank-conflicted
+// wavefronts; profiles/r02/ncu_fused_cic_ring.txt).  Off by default.
 #ifndef PICGPU_CIC_RING
-#define PICGPU_CIC_RING 4
+#define PICGPU_CIC_RING 0
 #endif
 struct JCfgCic3 {
     static constexpr int G = 2, PX = PICGPU_CIC_PX, PY = PICGPU_CIC_PY, MINB = PICGPU_CIC_MINB, CH = 2;

@@ -435,10 +435,21 @@ struct DBCfg {
 #else
     static constexpr int MINB = 3;  // C2 QSP: 4.35 ms at 3 CTAs/SM vs 5.05 at 2 (ZL 8)
 #endif
-    static constexpr int CAP = ORDER == 1 ? PICGPU_RHO_CIC_CAP : 512;  // slots per staged piece
-    static constexpr int WS = CAP + 2;       // weight array stride (bank skew)
+    // SYZ: the staging also evaluates the W*W products sy*sz per slot (the
+    // reference's inner product, deposit.hpp:41-48), so a term is
+    // q*(sx*syz) from 3 broadcast-or-conflict-free loads: every one of the 16
+    // (ty, tz) lanes of an x read its own syz array (odd stride), instead of
+    // each lane recomputing sy*sz.  TSC keeps the explicit tap test.
+#ifndef PICGPU_RHO_SYZ
+#define PICGPU_RHO_SYZ 1
+#endif
+    static constexpr bool SYZ = PICGPU_RHO_SYZ && ORDER != 2;
+    static constexpr int CAP = SYZ ? (ORDER == 1 ? PICGPU_RHO_CIC_CAP : 256)
+                                   : (ORDER == 1 ? PICGPU_RHO_CIC_CAP : 512);  // slots per staged piece
+    static constexpr int WS = SYZ ? CAP + 1 : CAP + 2;  // staged array stride (bank skew)
+    static constexpr int NA = SYZ ? W + W * W : 3 * W;  // staged weight arrays
     static constexpr int MAXC = RX + W + 1;  // cells per staged row
-    static constexpr size_t SMEM = (size_t)(ZL * RY * RX + CAP + 3 * W * WS) * 8 + (size_t)2 * MAXC * 4 + CAP;
+    static constexpr size_t SMEM = (size_t)(ZL * RY * RX + CAP + NA * WS) * 8 + (size_t)2 * MAXC * 4 + CAP;
 };
 
 struct Runs {  // ascending source cells along one axis: [a0, a1] then [b0, b1] (b0 > b1: none)
@@ -466,8 +477,8 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
     extern __shared__ __align__(16) double dsm[];
     double* s_acc = dsm;                        // [ZL][RY][RX]
     double* s_q = s_acc + ZL * RY * RX;         // [CAP]
-    double* s_w = s_q + CAP;                    // [3][W][WS]
-    uint32_t* s_cb = reinterpret_cast<uint32_t*>(s_w + 3 * W * C::WS);  // [MAXC] first slot of each row cell
+    double* s_w = s_q + CAP;                    // [3][W][WS] (SYZ: sx [W][WS], then syz [W*W][WS])
+    uint32_t* s_cb = reinterpret_cast<uint32_t*>(s_w + C::NA * C::WS);  // [MAXC] first slot of each row cell
     uint32_t* s_ce = s_cb + C::MAXC;                                     // [MAXC] end of its extent
     unsigned char* s_up = reinterpret_cast<unsigned char*>(s_ce + C::MAXC);  // [CAP] 0x80 valid | up bits
 
@@ -534,7 +545,7 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
                             // at +0.0 and so can never be -0.0 (x + -x rounds to +0.0)
                             s_q[i] = 0.0;
 #pragma unroll
-                            for (int a = 0; a < 3 * W; ++a) s_w[a * C::WS + i] = 0.0;
+                            for (int a = 0; a < C::NA; ++a) s_w[a * C::WS + i] = 0.0;
                         }
                         continue;
                     }
@@ -543,14 +554,28 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
                     locate_axis(r0.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
                     locate_axis(p.p[sl].z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
                     int bits = 0;
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        double w[W];
+                    if constexpr (C::SYZ) {
+                        double wx[W], wy[W], wz[W];
                         int up;
-                        Shape<ORDER>::weights(f[a], w, up);
-                        bits |= up << a;
+                        Shape<ORDER>::weights(f[0], wx, up);
+                        Shape<ORDER>::weights(f[1], wy, up);
+                        Shape<ORDER>::weights(f[2], wz, up);
 #pragma unroll
-                        for (int t = 0; t < W; ++t) s_w[(a * W + t) * C::WS + i] = w[t];
+                        for (int t = 0; t < W; ++t) s_w[t * C::WS + i] = wx[t];
+#pragma unroll
+                        for (int a = 0; a < W; ++a)
+#pragma unroll
+                            for (int b = 0; b < W; ++b) s_w[(W + a * W + b) * C::WS + i] = __dmul_rn(wy[a], wz[b]);
+                    } else {
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            double w[W];
+                            int up;
+                            Shape<ORDER>::weights(f[a], w, up);
+                            bits |= up << a;
+#pragma unroll
+                            for (int t = 0; t < W; ++t) s_w[(a * W + t) * C::WS + i] = w[t];
+                        }
                     }
                     s_up[i] = (unsigned char)(0x80 | bits);
                     s_q[i] = quantity ? quantity[sl] : qscale * p.p[sl].w;
@@ -559,6 +584,21 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
                 if (!mine) continue;
                 double* ap = s_acc + ((size_t)zl * RY + yl) * RX + xl;
                 double acc = *ap;
+                if constexpr (C::SYZ) {
+                    const double* syz = s_w + (W + ty * W + tz) * C::WS;
+#pragma unroll
+                    for (int c = 0; c < W; ++c) {
+                        const uint32_t b = max(mb[c], piece), e = min(me[c], piece + pn);
+                        const double* wx = s_w + ct[c] * C::WS;
+#pragma unroll 4
+                        for (uint32_t u = b; u < e; ++u) {
+                            const uint32_t i = u - piece;
+                            acc = __dadd_rn(acc, __dmul_rn(s_q[i], __dmul_rn(wx[i], syz[i])));
+                        }
+                    }
+                    *ap = acc;
+                    continue;
+                }
                 const double* wy = s_w + (W + ty) * C::WS;
                 const double* wz = s_w + (2 * W + tz) * C::WS;
 #pragma unroll

@@ -338,21 +338,29 @@ __global__ void __launch_bounds__(256) k_fill_slack(const Aos A, const uint32_t*
 #ifndef PICGPU_PUSH_EARLY_WID
 #define PICGPU_PUSH_EARLY_WID 1
 #endif
+// Threads per CTA: the CTA's ONE global reservation on ctr->nmovers is a
+// same-address atomic, serialised in L2 -- C3 has 2.7M CTAs of 256 slots,
+// so the reservations (and the moved-count reductions on the same line, now
+// spread over kMovedParts counters) bound the kernel; wider CTAs need fewer.
+#ifndef PICGPU_PUSH_NT
+#define PICGPU_PUSH_NT 512
+#endif
 #ifndef PICGPU_PUSH_MINB
 // record store: 5 CTAs/SM (48 registers) beat 6 (40, spills): C3 push+sort 54 -> 48 ms; with
 // w/id loaded up front (64 registers) 4 CTAs/SM: 48.1 -> 46.0 ms (5 CTAs spill: 50.2 ms)
-#define PICGPU_PUSH_MINB 4
+#define PICGPU_PUSH_MINB (4 * 256 / PICGPU_PUSH_NT)
 #endif
 
 // RECORD = false: push and count the moved particles only (the store is
 // re-sorted from scratch afterwards; no flags, movers or departures).
 template <bool PUSH, int UNR, bool P2, bool RECORD = true>
-__global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, const Aos A, uint64_t slots,
+__global__ void __launch_bounds__(PICGPU_PUSH_NT, PICGPU_PUSH_MINB) k_push(const GridD g, const Aos A, uint64_t slots,
                                               double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
                                               uint32_t mcap, const uint32_t* __restrict__ off,
                                               uint32_t* __restrict__ holes, uint32_t* __restrict__ hl,
                                               StepCounters* ctr, double* __restrict__ L, uint32_t lcap,
-                                              uint32_t* __restrict__ mslot, uint32_t* __restrict__ mbin) {
+                                              uint32_t* __restrict__ mslot, uint32_t* __restrict__ mbin,
+                                              unsigned long long* __restrict__ mvpart) {
     __shared__ unsigned s_cnt, s_base, s_mv;
     static_assert(UNR == 1, "one slot per thread (scalar state: arrays went to local memory)");
     if (threadIdx.x == 0) s_cnt = s_mv = 0;
@@ -431,13 +439,16 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
     const unsigned wm = __reduce_add_sync(0xffffffffu, moved ? 1u : 0u);
     if ((threadIdx.x & 31) == 0 && wm) atomicAdd(&s_mv, wm);
     __syncthreads();
+    // the moved count goes to one of kMovedParts counters on their own 128-byte
+    // lines (k_fold_moved sums them into ctr->moved)
+    unsigned long long* part = mvpart + (size_t)(blockIdx.x % kMovedParts) * 16;
     if (!RECORD) {
-        if (threadIdx.x == 0 && s_mv) atomicAdd(&ctr->moved, (unsigned long long)s_mv);
+        if (threadIdx.x == 0 && s_mv) atomicAdd(part, (unsigned long long)s_mv);
         return;
     }
     if (threadIdx.x == 0) {
         s_base = s_cnt ? atomicAdd(&ctr->nmovers, s_cnt) : 0u;
-        if (s_mv) atomicAdd(&ctr->moved, (unsigned long long)s_mv);
+        if (s_mv) atomicAdd(part, (unsigned long long)s_mv);
     }
     __syncthreads();
     if (lidx < 0) return;
@@ -478,6 +489,24 @@ __global__ void __launch_bounds__(256, PICGPU_PUSH_MINB) k_push(const GridD g, c
 // front hole the k-th tail particle), and the tail becomes slack.  Bins with
 // more than kHoleCap front holes fall back to a stable slide.
 constexpr int kHoleCap = 32;
+
+// ctr->moved += the spread partial counts of k_push; the partials are reset.
+__global__ void k_fold_moved(unsigned long long* __restrict__ mvpart, StepCounters* ctr) {
+    unsigned long long v = 0;
+    for (int i = threadIdx.x; i < kMovedParts; i += blockDim.x) {
+        v += mvpart[(size_t)i * 16];
+        mvpart[(size_t)i * 16] = 0;
+    }
+    for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    __shared__ unsigned long long w[32];
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int k = 0; k < (int)(blockDim.x + 31) / 32; ++k) t += w[k];
+        if (t) ctr->moved += t;
+    }
+}
 
 #ifndef PICGPU_COMPACT_MINB
 #define PICGPU_COMPACT_MINB 8  // latency-bound: full occupancy beats spill-free registers (191 vs 209+ us at C2)
@@ -1248,6 +1277,14 @@ void BinStore::full_sort_from_B(uint64_t np, uint32_t* perm_out_dev, cudaEvent_t
     hl.ensure((capacity + capacity / 8) * 4 + 4);
 }
 
+unsigned long long* BinStore::moved_parts() {
+    if (!mvpart.p) {
+        mvpart.ensure((size_t)kMovedParts * 128);
+        PICGPU_CUDA_TRY(cudaMemsetAsync(mvpart.p, 0, (size_t)kMovedParts * 128, st));
+    }
+    return mvpart.as<unsigned long long>();
+}
+
 void BinStore::fill_holes() {
     const size_t nc = g.ncells;
     if (!nc) return;
@@ -1349,15 +1386,17 @@ void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
     if (!nc || !n) return;
     constexpr int UNR = PICGPU_PUSH_UNR;
-    const int blocks = (int)((capacity + 256 * UNR - 1) / (256 * UNR));
+    const int blocks = (int)((capacity + PICGPU_PUSH_NT * UNR - 1) / (PICGPU_PUSH_NT * UNR));
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
     auto* kern = push ? (p2 ? k_push<true, UNR, true> : k_push<true, UNR, false>)
                       : (p2 ? k_push<false, UNR, true> : k_push<false, UNR, false>);
     hl.ensure(capacity * 4 + 4);
-    kern<<<blocks, 256, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap,
-                                 off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>(), ctr,
-                                 lrec.as<double>(), (uint32_t)lcap, mslot.as<uint32_t>(), mbin.as<uint32_t>());
-    note_launch();
+    kern<<<blocks, PICGPU_PUSH_NT, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(),
+                                            (uint32_t)mcap, off.as<uint32_t>(), holes.as<uint32_t>(),
+                                            hl.as<uint32_t>(), ctr, lrec.as<double>(), (uint32_t)lcap,
+                                            mslot.as<uint32_t>(), mbin.as<uint32_t>(), moved_parts());
+    k_fold_moved<<<1, 256, 0, st>>>(moved_parts(), ctr);
+    note_launch(2);
     PICGPU_CUDA_TRY(cudaGetLastError());
     if (push) {
         // the departures' hole-list entries (before any arrival looks for holes)
@@ -1455,12 +1494,15 @@ void BinStore::push_and_resort(bool push, double dt, double cap2, StepCounters& 
     PICGPU_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(StepCounters), st));
     if (nc && n && push) {
         constexpr int UNR = PICGPU_PUSH_UNR;
-        const int blocks = (int)((capacity + 256 * UNR - 1) / (256 * UNR));
+        const int blocks = (int)((capacity + PICGPU_PUSH_NT * UNR - 1) / (PICGPU_PUSH_NT * UNR));
         const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
         auto* kern = p2 ? k_push<true, UNR, true, false> : k_push<true, UNR, false, false>;
-        kern<<<blocks, 256, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap,
-                                     off.as<uint32_t>(), holes.as<uint32_t>(), hl.as<uint32_t>(), ctr,
-                                     lrec.as<double>(), (uint32_t)lcap, mslot.as<uint32_t>(), mbin.as<uint32_t>());
+        kern<<<blocks, PICGPU_PUSH_NT, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(),
+                                                (uint32_t)mcap, off.as<uint32_t>(), holes.as<uint32_t>(),
+                                                hl.as<uint32_t>(), ctr, lrec.as<double>(), (uint32_t)lcap,
+                                                mslot.as<uint32_t>(), mbin.as<uint32_t>(), moved_parts());
+        k_fold_moved<<<1, 256, 0, st>>>(moved_parts(), ctr);
+        note_launch();
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
     }

@@ -49,7 +49,8 @@ struct AosBuf {
     Aos aos() const { return Aos{a.as<Part>()}; }
 };
 
-constexpr int kBorrowScanBins = 4;  // GpmaConfig::borrow_scan_bins (gpma.hpp:25)
+constexpr int kBorrowScanBins = 4;
+constexpr int kMovedParts = 256;  // k_push's moved-count partials (one 128-byte line each)  // GpmaConfig::borrow_scan_bins (gpma.hpp:25)
 
 struct BinStore {
     GridD g{};
@@ -74,6 +75,7 @@ struct BinStore {
     DevBuf hl;                // per-bin hole lists, slot-indexed like the bins: bin c's holes
                               // are the slots hl[off[c] .. off[c]+holes[c]) (u32)
     DevBuf counters;          // StepCounters
+    DevBuf mvpart;            // k_push's spread moved counts (kMovedParts x 128 bytes, kept zero between steps)
     StepCounters* hcounters = nullptr;  // pinned mirror
 
     uint64_t n = 0;           // particles
@@ -143,6 +145,7 @@ struct BinStore {
                       uint64_t& dropped, uint64_t& injected);
 
     uint32_t* d_off() const { return off.as<uint32_t>(); }
+    unsigned long long* moved_parts();
     uint32_t* d_cnt() const { return cnt.as<uint32_t>(); }
 
     void ensure_movers(size_t m);
