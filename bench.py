@@ -370,6 +370,12 @@ def main():
         raise SystemExit("multi-GPU runs use the cubic configs (x-slabs of a (n*N) x n x n box) or c5")
     single = world == 1 and not args.slab
     fp64_peak = pg.fp64_peak_tflops(local)
+    try:  # SMs x 64 DFMA/clk x 2 flops x max SM clock (MEASURED_PEAKS.json sm_max_mhz)
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", 1965.0))
+    except Exception:
+        mhz = 1965.0
+    fp64_nominal = torch.cuda.get_device_properties(local).multi_processor_count * 64 * 2 * mhz * 1e6 / 1e12
     hbm_peak, hbm_src = peaks()
 
     comm_box = [None]  # one NCCL communicator for every session of the run
@@ -470,7 +476,9 @@ def main():
         if frac_fp64 >= frac_hbm:
             roof = {"bound": "fp64", "achieved": fp64_achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                     "frac": frac_fp64, "traffic": traffic,
-                    "peak_source": "measured in-run (DFMA microbenchmark, picgpu_fp64_peak)",
+                    "peak_source": "measured in-run (DFMA microbenchmark, picgpu_fp64_peak); MEASURED_PEAKS.json "
+                                   "and B200_PROFILING.md carry no FP64 figure",
+                    "peak_nominal": fp64_nominal, "frac_vs_nominal": fp64_achieved / fp64_nominal,
                     "flops_per_deposit": FLOPS[order]}
         else:
             roof = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s", "frac": frac_hbm,

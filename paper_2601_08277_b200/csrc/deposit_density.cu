@@ -440,10 +440,15 @@ struct DBCfg {
     // q*(sx*syz) from 3 broadcast-or-conflict-free loads: every one of the 16
     // (ty, tz) lanes of an x read its own syz array (odd stride), instead of
     // each lane recomputing sy*sz.  TSC keeps the explicit tap test.
+    // C2 (128^3 x 16): CIC 1.58 ms with SYZ vs 1.64 without; QSP 4.90 vs 4.34 --
+    // the term loop drops from ~11 to 8.25 warp-instructions per term, but the
+    // heavier staging (16 more products and stores per slot) at half the piece
+    // size doubles the row barriers (40% of the stall samples) -- so QSP keeps
+    // the three weight arrays (profiles/r02/ncu_rho_syz.txt).
 #ifndef PICGPU_RHO_SYZ
 #define PICGPU_RHO_SYZ 1
 #endif
-    static constexpr bool SYZ = PICGPU_RHO_SYZ && ORDER != 2;
+    static constexpr bool SYZ = PICGPU_RHO_SYZ && ORDER == 1;
     static constexpr int CAP = SYZ ? (ORDER == 1 ? PICGPU_RHO_CIC_CAP : 256)
                                    : (ORDER == 1 ? PICGPU_RHO_CIC_CAP : 512);  // slots per staged piece
     static constexpr int WS = SYZ ? CAP + 1 : CAP + 2;  // staged array stride (bank skew)
