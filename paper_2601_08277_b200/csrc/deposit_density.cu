@@ -880,11 +880,13 @@ void run_rows_and_shell(const GridD& g, const CAos& p, const double* quantity, d
         const dim3 grid(div_up(in.hi[0] - in.lo[0] + 1, kRowX), div_up(in.hi[1] - in.lo[1] + 1, kRowY),
                         div_up(in.hi[2] - in.lo[2] + 1, zlen));
         constexpr size_t smem = (size_t)(1 + 3 * Shape<ORDER>::W) * kRowCap * 8 + (size_t)kRowCap * 5;
-        static bool configured = false;
-        if (!configured) {
+        static int configured_dev = -1;
+        int dev = 0;
+        PICGPU_CUDA_TRY(cudaGetDevice(&dev));
+        if (configured_dev != dev) {  // per device (one process may drive several GPUs)
             PICGPU_CUDA_TRY(cudaFuncSetAttribute(density_rows<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem));
-            configured = true;
+            configured_dev = dev;
         }
         density_rows<ORDER><<<grid, kRowX * kRowY, smem, st>>>(g, p, quantity, qscale, off, cnt, in, zlen, rho);
         note_launch();

@@ -333,10 +333,10 @@ __global__ void __launch_bounds__(256) k_fill_slack(const Aos A, const uint32_t*
 // Movers that do not fit the mover buffer stay in their (now stale) bin with
 // flag 2; the host then re-sorts fully.
 #ifndef PICGPU_PUSH_UNR
-#define PICGPU_PUSH_UNR 1
+#define PICGPU_PUSH_UNR 2
 #endif
-#ifndef PICGPU_PUSH_EARLY_WID
-#define PICGPU_PUSH_EARLY_WID 1
+#ifndef PICGPU_PUSH_EARLY_WID  // w, id with the rest of the record (UNR 1: C3 48.1 -> 46.0 ms)
+#define PICGPU_PUSH_EARLY_WID (PICGPU_PUSH_UNR == 1)
 #endif
 // Threads per CTA: the CTA's ONE global reservation on ctr->nmovers is a
 // same-address atomic, serialised in L2 -- C3 has 2.7M CTAs of 256 slots,
@@ -353,6 +353,126 @@ __global__ void __launch_bounds__(256) k_fill_slack(const Aos A, const uint32_t*
 
 // RECORD = false: push and count the moved particles only (the store is
 // re-sorted from scratch afterwards; no flags, movers or departures).
+// One slot of k_push: its record (w, id loaded with the rest: the mover copy
+// needs no second round trip), then push + move test.
+struct PushSlot {
+    double x, y, z, vx, vy, vz;
+    double2 wid;
+    uint32_t nc, before;
+    int lidx;
+    bool moved;
+};
+
+template <bool RECORD>
+__device__ __forceinline__ void push_load(const Aos& A, uint64_t s, uint64_t slots, PushSlot& q) {
+    q.x = __longlong_as_double(-1LL);
+    q.y = q.z = q.vx = q.vy = q.vz = 0.0;
+    q.wid = make_double2(0.0, 0.0);
+    q.nc = q.before = 0;
+    q.lidx = -1;
+    q.moved = false;
+    if (s < slots) {  // x y | z vx | vy vz (| w id) of the record
+        const double2* r = reinterpret_cast<const double2*>(A.p + s);
+        const double2 a = r[0], b = r[1], c = r[2];
+        if (PICGPU_PUSH_EARLY_WID && RECORD) q.wid = r[3];  // same two sectors
+        q.x = a.x;
+        q.y = a.y;
+        q.z = b.x;
+        q.vx = b.y;
+        q.vy = c.x;
+        q.vz = c.y;
+    }
+}
+
+template <bool PUSH, bool P2, bool RECORD>
+__device__ __forceinline__ void push_slot(const GridD& g, const Aos& A, uint64_t s, double dt, double cap2,
+                                          PushSlot& q, const uint32_t* __restrict__ off,
+                                          uint32_t* __restrict__ holes, uint32_t* __restrict__ hl,
+                                          StepCounters* ctr, double* __restrict__ L, uint32_t lcap, unsigned* s_cnt) {
+    if (is_gap(q.x)) return;
+    if (!finite3(q.x, q.y, q.z)) {
+        raise_error(&ctr->err, PICGPU_EINVAL);
+        return;
+    }
+    if (PUSH) {
+        const double ox = q.x, oy = q.y, oz = q.z;
+        bool ok = push_one<P2>(g, dt, cap2, q.x, q.y, q.z, q.vx, q.vy, q.vz);
+        if (!ok) {
+            raise_error(&ctr->err, PICGPU_EDOMAIN);
+        } else {
+            reinterpret_cast<double2*>(A.p + s)[0] = make_double2(q.x, q.y);
+            A.p[s].z = q.z;
+            if (!finite3(q.x, q.y, q.z)) {
+                raise_error(&ctr->err, PICGPU_EINVAL);
+                ok = false;
+            }
+        }
+        if (ok) {
+            const int p2x = P2 || g.pow2x, p2y = P2 || g.pow2y, p2z = P2 || g.pow2z;
+            const double fx0 = axis_floor(ox, g.gox, g.dx, g.inv_dx, p2x);
+            const double fy0 = axis_floor(oy, g.oy, g.dy, g.inv_dy, p2y);
+            const double fz0 = axis_floor(oz, g.oz, g.dz, g.inv_dz, p2z);
+            const bool same = fx0 >= 0.0 && fy0 >= 0.0 && fz0 >= 0.0 &&
+                              fx0 == axis_floor(q.x, g.gox, g.dx, g.inv_dx, p2x) &&
+                              fy0 == axis_floor(q.y, g.oy, g.dy, g.inv_dy, p2y) &&
+                              fz0 == axis_floor(q.z, g.oz, g.dz, g.inv_dz, p2z);
+            if (!same) {
+                q.before = store_cell<P2>(g, ox, oy, oz);
+                q.nc = store_cell<P2>(g, q.x, q.y, q.z);
+                q.moved = q.nc != q.before;
+            }
+        }
+    }
+    if (RECORD && q.moved) {
+        if (q.nc >= kLeaveRight) {  // left the slab: exchange record for the neighbour rank
+            const int dir = q.nc == kLeaveLeft ? 0 : 1;
+            const unsigned li = atomicAdd(&ctr->nleave[dir], 1u);
+            if (li < lcap) {
+                double* r = L + ((size_t)dir * lcap + li) * 8;
+                r[0] = q.x; r[1] = q.y; r[2] = q.z;
+                r[3] = q.vx; r[4] = q.vy; r[5] = q.vz;
+                if (!PICGPU_PUSH_EARLY_WID) q.wid = reinterpret_cast<const double2*>(A.p + s)[3];
+                r[6] = q.wid.x;
+                r[7] = q.wid.y;
+                push_hole(A, s, q.before, off, holes, hl);
+            } else {
+                raise_error(&ctr->err, PICGPU_ELENGTH);
+            }
+        } else {
+            q.lidx = (int)atomicAdd(s_cnt, 1u);
+        }
+    }
+}
+
+template <bool RECORD>
+__device__ __forceinline__ void push_store_mover(const Aos& A, uint64_t s, const PushSlot& q, unsigned base,
+                                                 const Soa& M, uint32_t* __restrict__ mcell, uint32_t mcap,
+                                                 uint32_t* __restrict__ mslot, uint32_t* __restrict__ mbin) {
+    if (q.lidx < 0) return;
+    const unsigned idx = base + (unsigned)q.lidx;
+    if (idx >= mcap) return;  // not recorded (mover buffer full): stays in its stale bin; the host re-sorts
+    double2 wid = q.wid;
+    if (!PICGPU_PUSH_EARLY_WID) wid = reinterpret_cast<const double2*>(A.p + s)[3];
+    M.x[idx] = q.x;
+    M.y[idx] = q.y;
+    M.z[idx] = q.z;
+    M.vx[idx] = q.vx;
+    M.vy[idx] = q.vy;
+    M.vz[idx] = q.vz;
+    M.w[idx] = wid.x;
+    M.id[idx] = (uint64_t)__double_as_longlong(wid.y);
+    mcell[idx] = q.nc;
+    // the slot becomes a hole now; it joins its bin's hole list in
+    // k_departures (no atomic round trip in this streaming kernel)
+    store_gap_record(A.p + s);
+    mslot[idx] = (uint32_t)s;
+    mbin[idx] = q.before;
+}
+
+// UNR slots per thread (slot t and t + NT, ... of the CTA's range): every
+// record is loaded before any is pushed, so UNR records are in flight per
+// thread (the kernel is bound by bytes in flight: one record per thread at 32
+// warps/SM streams ~2 TB/s), and one reservation covers UNR x NT slots.
 template <bool PUSH, int UNR, bool P2, bool RECORD = true>
 __global__ void __launch_bounds__(PICGPU_PUSH_NT, PICGPU_PUSH_MINB) k_push(const GridD g, const Aos A, uint64_t slots,
                                               double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
@@ -362,85 +482,24 @@ __global__ void __launch_bounds__(PICGPU_PUSH_NT, PICGPU_PUSH_MINB) k_push(const
                                               uint32_t* __restrict__ mslot, uint32_t* __restrict__ mbin,
                                               unsigned long long* __restrict__ mvpart) {
     __shared__ unsigned s_cnt, s_base, s_mv;
-    static_assert(UNR == 1, "one slot per thread (scalar state: arrays went to local memory)");
     if (threadIdx.x == 0) s_cnt = s_mv = 0;
     __syncthreads();
-    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    double x = __longlong_as_double(-1LL), y = 0.0, z = 0.0, vx = 0.0, vy = 0.0, vz = 0.0;
-    double2 wid = make_double2(0.0, 0.0);
-    if (s < slots) {  // x y | z vx | vy vz (| w id) of the record
-        const double2* r = reinterpret_cast<const double2*>(A.p + s);
-        const double2 a = r[0], b = r[1], c = r[2];
-        if (PICGPU_PUSH_EARLY_WID && RECORD) wid = r[3];  // same two sectors; no second round trip for movers
-        x = a.x;
-        y = a.y;
-        z = b.x;
-        vx = b.y;
-        vy = c.x;
-        vz = c.y;
+    const uint64_t s0 = (uint64_t)blockIdx.x * blockDim.x * UNR + threadIdx.x;
+    PushSlot q[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) push_load<RECORD>(A, s0 + (uint64_t)u * blockDim.x, slots, q[u]);
+    unsigned nmv = 0;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+        push_slot<PUSH, P2, RECORD>(g, A, s0 + (uint64_t)u * blockDim.x, dt, cap2, q[u], off, holes, hl, ctr, L,
+                                    lcap, &s_cnt);
+        nmv += q[u].moved ? 1u : 0u;
     }
-    uint32_t nc = 0, before = 0;
-    int lidx = -1;
-    bool moved = false;
-    if (!is_gap(x)) {
-        if (!finite3(x, y, z)) {
-            raise_error(&ctr->err, PICGPU_EINVAL);
-        } else if (PUSH) {
-            const double ox = x, oy = y, oz = z;
-            bool ok = push_one<P2>(g, dt, cap2, x, y, z, vx, vy, vz);
-            if (!ok) {
-                raise_error(&ctr->err, PICGPU_EDOMAIN);
-            } else {
-                reinterpret_cast<double2*>(A.p + s)[0] = make_double2(x, y);
-                A.p[s].z = z;
-                if (!finite3(x, y, z)) {
-                    raise_error(&ctr->err, PICGPU_EINVAL);
-                    ok = false;
-                }
-            }
-            if (ok) {
-                const int p2x = P2 || g.pow2x, p2y = P2 || g.pow2y, p2z = P2 || g.pow2z;
-                const double fx0 = axis_floor(ox, g.gox, g.dx, g.inv_dx, p2x);
-                const double fy0 = axis_floor(oy, g.oy, g.dy, g.inv_dy, p2y);
-                const double fz0 = axis_floor(oz, g.oz, g.dz, g.inv_dz, p2z);
-                const bool same = fx0 >= 0.0 && fy0 >= 0.0 && fz0 >= 0.0 &&
-                                  fx0 == axis_floor(x, g.gox, g.dx, g.inv_dx, p2x) &&
-                                  fy0 == axis_floor(y, g.oy, g.dy, g.inv_dy, p2y) &&
-                                  fz0 == axis_floor(z, g.oz, g.dz, g.inv_dz, p2z);
-                if (!same) {
-                    before = store_cell<P2>(g, ox, oy, oz);
-                    nc = store_cell<P2>(g, x, y, z);
-                    moved = nc != before;
-                }
-            }
-        }
-        if (RECORD && moved) {
-            if (nc >= kLeaveRight) {  // left the slab: exchange record for the neighbour rank
-                const int dir = nc == kLeaveLeft ? 0 : 1;
-                const unsigned li = atomicAdd(&ctr->nleave[dir], 1u);
-                if (li < lcap) {
-                    double* r = L + ((size_t)dir * lcap + li) * 8;
-                    r[0] = x; r[1] = y; r[2] = z;
-                    r[3] = vx; r[4] = vy; r[5] = vz;
-                    if (!PICGPU_PUSH_EARLY_WID) wid = reinterpret_cast<const double2*>(A.p + s)[3];
-                    r[6] = wid.x;
-                    r[7] = wid.y;
-                    push_hole(A, s, before, off, holes, hl);
-                } else {
-                    raise_error(&ctr->err, PICGPU_ELENGTH);
-                }
-            } else {
-                lidx = (int)atomicAdd(&s_cnt, 1u);
-            }
-        }
-    }
-    // moved count: one shared-memory add per warp, one global RED per block
-    // (a per-warp RED on the single counter serialises in L2: +60 us at C2)
-    const unsigned wm = __reduce_add_sync(0xffffffffu, moved ? 1u : 0u);
+    // moved count: one shared-memory add per warp, one RED per block on one of
+    // kMovedParts counters (k_fold_moved sums them into ctr->moved)
+    const unsigned wm = __reduce_add_sync(0xffffffffu, nmv);
     if ((threadIdx.x & 31) == 0 && wm) atomicAdd(&s_mv, wm);
     __syncthreads();
-    // the moved count goes to one of kMovedParts counters on their own 128-byte
-    // lines (k_fold_moved sums them into ctr->moved)
     unsigned long long* part = mvpart + (size_t)(blockIdx.x % kMovedParts) * 16;
     if (!RECORD) {
         if (threadIdx.x == 0 && s_mv) atomicAdd(part, (unsigned long long)s_mv);
@@ -451,27 +510,9 @@ __global__ void __launch_bounds__(PICGPU_PUSH_NT, PICGPU_PUSH_MINB) k_push(const
         if (s_mv) atomicAdd(part, (unsigned long long)s_mv);
     }
     __syncthreads();
-    if (lidx < 0) return;
-    const unsigned idx = s_base + (unsigned)lidx;
-    if (idx < mcap) {
-        if (!PICGPU_PUSH_EARLY_WID) wid = reinterpret_cast<const double2*>(A.p + s)[3];
-        M.x[idx] = x;
-        M.y[idx] = y;
-        M.z[idx] = z;
-        M.vx[idx] = vx;
-        M.vy[idx] = vy;
-        M.vz[idx] = vz;
-        M.w[idx] = wid.x;
-        M.id[idx] = (uint64_t)__double_as_longlong(wid.y);
-        mcell[idx] = nc;
-        // the slot becomes a hole now; it joins its bin's hole list in
-        // k_departures (no atomic round trip in this streaming kernel)
-        store_gap_record(A.p + s);
-        mslot[idx] = (uint32_t)s;
-        mbin[idx] = before;
-    }
-    // else not recorded (mover buffer full): it stays in its stale bin; nmovers >
-    // mcap tells the host to re-sort fully
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+        push_store_mover<RECORD>(A, s0 + (uint64_t)u * blockDim.x, q[u], s_base, M, mcell, mcap, mslot, mbin);
 }
 
 // Gaps, as in the reference's GPMA: a departing particle leaves a hole in its
@@ -490,7 +531,7 @@ __global__ void __launch_bounds__(PICGPU_PUSH_NT, PICGPU_PUSH_MINB) k_push(const
 // more than kHoleCap front holes fall back to a stable slide.
 constexpr int kHoleCap = 32;
 
-// ---- the unfused push in two streaming kernels (PICGPU_PUSH2, default) -----
+// ---- the unfused push in two streaming kernels (PICGPU_PUSH2=1, opt-in) -----
 // k_push carried a CTA barrier and a global reservation round trip per 512
 // slots (C3 ncu: barrier stalls 18 per issue, 2.3 TB/s).  Here k_push_mark
 // streams the records with no barrier and no atomic on the hot path: push,
@@ -587,7 +628,7 @@ __global__ void __launch_bounds__(CL_NT) k_collect(const uint32_t* __restrict__ 
                                                   uint64_t ntiles, StepCounters* ctr) {
     constexpr int NW = CL_NT / 32;
     __shared__ uint32_t s_wc[CL_ITEMS][NW];  // movers per (item, warp) -> exclusive prefix
-    __shared__ uint32_t s_tile, s_tot;
+    __shared__ uint32_t s_tile;
     __shared__ unsigned long long s_base;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
@@ -612,7 +653,6 @@ __global__ void __launch_bounds__(CL_NT) k_collect(const uint32_t* __restrict__ 
                 s_wc[j][w] = run;
                 run += v;
             }
-        s_tot = run;
         unsigned long long* my = status + tile;
         unsigned long long excl = 0;
         if (tile == 0) {
@@ -1555,9 +1595,13 @@ void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     const int blocks = (int)((capacity + PICGPU_PUSH_NT * UNR - 1) / (PICGPU_PUSH_NT * UNR));
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
     hl.ensure(capacity * 4 + 4);
+    // C3 (537M, 11% movers): mark 34.0 + collect 12.5 ms vs k_push 30 ms --
+    // the mark kernel alone streams at 2 TB/s (one 64-byte record in flight per
+    // thread at 32 warps/SM), so removing k_push's barrier and reservation did
+    // not pay; kept opt-in (PICGPU_PUSH2=1).
     static const bool two_pass = [] {
         const char* e = std::getenv("PICGPU_PUSH2");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     if (push && two_pass) {
         // mark (streaming push + move codes) -> collect (look-back compaction, slot order)
