@@ -332,8 +332,11 @@ __global__ void __launch_bounds__(256) k_fill_slack(const Aos A, const uint32_t*
 // path); departures are counted per bin with fire-and-forget reductions.
 // Movers that do not fit the mover buffer stay in their (now stale) bin with
 // flag 2; the host then re-sorts fully.
+// UNR 2 (both records in flight before any push) measured slower at C3:
+// push + sort 46.4 (512 threads, 64 registers, spills) / 44.2 (256 threads,
+// 80 registers) / 47.7 (w, id early) vs 43.5 ms at UNR 1 (profiles/r02/kpush_unr_ab.txt).
 #ifndef PICGPU_PUSH_UNR
-#define PICGPU_PUSH_UNR 2
+#define PICGPU_PUSH_UNR 1
 #endif
 #ifndef PICGPU_PUSH_EARLY_WID  // w, id with the rest of the record (UNR 1: C3 48.1 -> 46.0 ms)
 #define PICGPU_PUSH_EARLY_WID (PICGPU_PUSH_UNR == 1)
@@ -470,9 +473,8 @@ __device__ __forceinline__ void push_store_mover(const Aos& A, uint64_t s, const
 }
 
 // UNR slots per thread (slot t and t + NT, ... of the CTA's range): every
-// record is loaded before any is pushed, so UNR records are in flight per
-// thread (the kernel is bound by bytes in flight: one record per thread at 32
-// warps/SM streams ~2 TB/s), and one reservation covers UNR x NT slots.
+// record is loaded before any is pushed and one reservation covers UNR x NT
+// slots (measured: UNR 1 is fastest, see PICGPU_PUSH_UNR).
 template <bool PUSH, int UNR, bool P2, bool RECORD = true>
 __global__ void __launch_bounds__(PICGPU_PUSH_NT, PICGPU_PUSH_MINB) k_push(const GridD g, const Aos A, uint64_t slots,
                                               double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
