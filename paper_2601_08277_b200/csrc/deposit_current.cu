@@ -539,13 +539,20 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 // the dependent FP64 chains of locate/weights) overlaps the contraction of
 // earlier chunks instead of stalling it, and each role holds only its own
 // registers (v3: 168 per thread, 12 warps/SM; here 2 x 8 warps at <= 128).
+// NPW producer warps per consumer warp: 1 (2 CTAs/SM, setmaxnreg split) or 2
+// (one CTA of 12 warps per SM; producer p fills the pair's chunks c = p mod 2).
+#ifndef PICGPU_WS_NPW
+#define PICGPU_WS_NPW 2
+#endif
+constexpr int WS_NPW = PICGPU_WS_NPW;
 #ifndef PICGPU_WS_NS
-#define PICGPU_WS_NS 3
+#define PICGPU_WS_NS (WS_NPW == 1 ? 3 : 4)
 #endif
 #ifndef PICGPU_WS_MINB
-#define PICGPU_WS_MINB 2
+#define PICGPU_WS_MINB (WS_NPW == 1 ? 2 : 1)
 #endif
 constexpr int WS_NS = PICGPU_WS_NS;
+static_assert(WS_NS % WS_NPW == 0, "ws: ring slots per producer parity");
 // register split (setmaxnreg, per warpgroup: consumers are warps 0-3, producers
 // 4-7): 4 x 32 x (C + P) = the CTA's 256 x 128 at 2 CTAs/SM
 #ifndef PICGPU_WS_REG_C
@@ -559,8 +566,8 @@ constexpr int WS_REG_C = PICGPU_WS_REG_C, WS_REG_P = PICGPU_WS_REG_P;
 template <int ORDER, class CF>
 struct WsLayout {
     using L = JLayout<ORDER, CF>;
-    static constexpr int NT = L::NT;           // consumer threads (= producer threads)
-    static constexpr int NW = NT / 32;         // producer/consumer pairs
+    static constexpr int NT = L::NT;           // consumer threads (= threads per producer group)
+    static constexpr int NW = NT / 32;         // consumer warps (each fed by WS_NPW producer warps)
     static constexpr int SLOT = L::STAGE3;     // doubles per chunk slot (all pencils)
     static constexpr size_t BAR_OFF = (size_t)(2 * L::PATCH + WS_NS * SLOT) * sizeof(double);
     static constexpr size_t SMEM = BAR_OFF + (size_t)WS_NS * NW * 2 * sizeof(uint64_t) +
@@ -585,8 +592,35 @@ __device__ __forceinline__ bool consumer_bar_or(bool v, int nthreads) {
 
 constexpr uint32_t kWsLast = 1u << 8;  // header flag: last chunk of the cell step
 
+// A pair's chunk sequence: cell steps k0..k1-1, ceil(m/CH) chunks each (m =
+// the warp's largest count in the step; an empty step is one empty chunk).
+// k / ci / m / nch are warp-uniform; c_off / n_c are this lane's pencil's bin.
+struct ChunkCursor {
+    int k, k1, ci, m, nch, n_c;
+    uint32_t c_off;
+    __device__ __forceinline__ void load(const uint32_t* off, const uint32_t* cnt, uint32_t col, uint32_t plane,
+                                         bool pv, int CH) {
+        c_off = 0;
+        n_c = 0;
+        if (pv && k < k1) {
+            c_off = off[col + plane * (uint32_t)k];
+            n_c = (int)cnt[col + plane * (uint32_t)k];
+        }
+        m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
+        nch = m == 0 ? 1 : (m + CH - 1) / CH;
+    }
+    __device__ __forceinline__ void next(const uint32_t* off, const uint32_t* cnt, uint32_t col, uint32_t plane,
+                                         bool pv, int CH) {
+        if (++ci >= nch) {
+            ++k;
+            ci = 0;
+            if (k < k1) load(off, cnt, col, plane, pv, CH);
+        }
+    }
+};
+
 template <int ORDER, class CF = JCfg<ORDER>, int PM = 0, bool SLAB = false>
-__global__ void __launch_bounds__(2 * JLayout<ORDER, CF>::NT, PICGPU_WS_MINB)
+__global__ void __launch_bounds__((1 + WS_NPW) * JLayout<ORDER, CF>::NT, PICGPU_WS_MINB)
     deposit_current_kernel_ws(const GridD g, const CAos p, const uint32_t* __restrict__ off,
                               const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
                               double* __restrict__ jy, double* __restrict__ jz, const int zlen,
@@ -613,7 +647,8 @@ __global__ void __launch_bounds__(2 * JLayout<ORDER, CF>::NT, PICGPU_WS_MINB)
     uint32_t* hdr = reinterpret_cast<uint32_t*>(empty + WS_NS * NW);                          // [NS][NW]
 
     const bool producer = threadIdx.x >= NT;
-    const int tid = producer ? threadIdx.x - NT : threadIdx.x;
+    const int tid = producer ? (threadIdx.x - NT) % NT : threadIdx.x;
+    [[maybe_unused]] const int pidx = producer ? (threadIdx.x - NT) / NT : 0;  // producer parity
     const int warp = tid >> 5, lane = tid & 31;
     const int grp = tid / G, lg = tid % G;
     const int ly = lg % W, xh = lg / W;
@@ -632,7 +667,8 @@ __global__ void __launch_bounds__(2 * JLayout<ORDER, CF>::NT, PICGPU_WS_MINB)
     {
         bool any = false;
         if (pv)
-            for (int kk = k0 + lg + (producer ? G : 0); kk < k1; kk += 2 * G) any |= cnt[col + plane_cells * kk] != 0;
+            for (int kk = k0 + lg + (producer ? G * (1 + pidx) : 0); kk < k1; kk += (1 + WS_NPW) * G)
+                any |= cnt[col + plane_cells * kk] != 0;
         if (!__syncthreads_or(any)) {
             if (PM != 0 && threadIdx.x == 0) pc.seg_cnt[seg] = 0;
             return;
@@ -650,114 +686,98 @@ __global__ void __launch_bounds__(2 * JLayout<ORDER, CF>::NT, PICGPU_WS_MINB)
 
     if (producer) {
         // ------------------------------------------------------------ producer
-        if constexpr (WS_REG_P > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WS_REG_P));
+        if constexpr (WS_NPW == 1 && WS_REG_P > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WS_REG_P));
         const double dci = (double)(i + g.sx_shift), dcj = (double)j;
-        uint32_t c_off = 0;
-        int n_c = 0;
-        if (pv && k0 < k1) {
-            c_off = off[col + plane_cells * k0];
-            n_c = (int)cnt[col + plane_cells * k0];
-        }
+        // this producer's chunks: c = pidx, pidx + NPW, ...; `la` runs one of
+        // its chunks ahead for the record prefetch
+        ChunkCursor cur{k0, k1, 0, 0, 0, 0, 0u};
+        cur.load(off, cnt, col, plane_cells, pv, CH);
+        for (int t = 0; t < pidx; ++t) cur.next(off, cnt, col, plane_cells, pv, CH);
+        ChunkCursor la = cur;
+        for (int t = 0; t < WS_NPW && la.k < k1; ++t) la.next(off, cnt, col, plane_cells, pv, CH);
         PData nxt{};
-        if (lg < n_c) load_particle<PM != 0>(p, c_off + lg, nxt);
-        int s = 0;
-        unsigned ph = 0;
-        for (int k = k0; k < k1; ++k) {
+        if (cur.k < k1 && cur.ci * CH + lg < cur.n_c) load_particle<PM != 0>(p, cur.c_off + cur.ci * CH + lg, nxt);
+        uint32_t c = (uint32_t)pidx;  // chunk index in the pair's sequence
+        while (cur.k < k1) {
+            const int k = cur.k, base = cur.ci * CH, m = cur.m;
+            const uint32_t c_off = cur.c_off;
+            const int n_c = cur.n_c;
             const int R = (k - k0) & (W - 1);
-            uint32_t n_off = 0;
-            int n_n = 0;
-            if (pv && k + 1 < k1) {
-                n_off = off[col + plane_cells * (k + 1)];
-                n_n = (int)cnt[col + plane_cells * (k + 1)];
-            }
+            const int s = (int)(c % WS_NS);
+            const unsigned ph = (c / WS_NS) & 1u;
+            double* stage = ring + s * WL::SLOT;
+            [[maybe_unused]] bool mv = false;
+            [[maybe_unused]] uint32_t mv_cell = 0;
+            [[maybe_unused]] unsigned mv_bal = 0, mv_b0 = 0;
+            PData curp = nxt;
+            bool valid = base + lg < n_c && !is_gap(curp.x);
+            if (la.k < k1 && la.ci * CH + lg < la.n_c) load_particle<PM != 0>(p, la.c_off + la.ci * CH + lg, nxt);
             const double dck = (double)k;
-            const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
-            if (m == 0 && lg < n_n) load_particle<PM != 0>(p, n_off + lg, nxt);
-            const int nch = m == 0 ? 1 : (m + CH - 1) / CH;
-            for (int ci = 0; ci < nch; ++ci) {
-                const int base = ci * CH;
-                double* stage = ring + s * WL::SLOT;
-                [[maybe_unused]] bool mv = false;
-                [[maybe_unused]] uint32_t mv_cell = 0;
-                [[maybe_unused]] unsigned mv_bal = 0, mv_b0 = 0;
-                PData cur = nxt;
-                bool valid = base + lg < n_c && !is_gap(cur.x);
-                if (m > 0) {
-                    if (base + CH < m) {
-                        if (base + CH + lg < n_c) load_particle<PM != 0>(p, c_off + base + CH + lg, nxt);
-                    } else if (lg < n_n) {
-                        load_particle<PM != 0>(p, n_off + lg, nxt);
+            double a[3][W], sy[W], sz[W];
+            [[maybe_unused]] int shx = 0, shy = 0, shz = 0;
+            if constexpr (PM != 0) {
+                double fx = 0.0, fy = 0.0, fz = 0.0;
+                if (valid)
+                    valid = push_fused<PM == 2, SLAB>(g, pc, curp, c_off + (uint32_t)(base + lg),
+                                                      col + plane_cells * (uint32_t)k, i, j, k, dci, dcj, dck, fx, fy,
+                                                      fz, mv, mv_cell, shx, shy, shz);
+                mv_bal = __ballot_sync(0xffffffffu, mv);
+                if (mv_bal && lane == __ffs(mv_bal) - 1) mv_b0 = atomicAdd(&s_movers, (unsigned)__popc(mv_bal));
+                window_from_fractions<ORDER>(curp, qs, valid, fx, fy, fz, a, sy, sz);
+            } else {
+                particle_window_sel<ORDER>(g, curp, qs, valid, dci, dcj, dck, a, sy, sz);
+            }
+            // the slot is free once the consumer has read its previous chunk
+            mbar_wait(empty + s * NW + warp, ph ^ 1u);
+            if (m > 0) {
+                stage_record<L, W>(stage, lg, grp, R, a, sy, sz);
+                if constexpr (PM != 0) {
+                    if (mv && valid) {
+                        restage_shifted<L, W>(stage, lg, grp, 0, shx, 0);
+                        restage_shifted<L, W>(stage, lg, grp, W, shx, 0);
+                        restage_shifted<L, W>(stage, lg, grp, 2 * W, shx, 0);
+                        restage_shifted<L, W>(stage, lg, grp, 3 * W, shy, 0);
+                        restage_shifted<L, W>(stage, lg, grp, 4 * W, shz, R);
                     }
                 }
-                double a[3][W], sy[W], sz[W];
-                [[maybe_unused]] int shx = 0, shy = 0, shz = 0;
-                if constexpr (PM != 0) {
-                    double fx = 0.0, fy = 0.0, fz = 0.0;
-                    if (valid)
-                        valid = push_fused<PM == 2, SLAB>(g, pc, cur, c_off + (uint32_t)(base + lg),
-                                                          col + plane_cells * (uint32_t)k, i, j, k, dci, dcj, dck,
-                                                          fx, fy, fz, mv, mv_cell, shx, shy, shz);
-                    mv_bal = __ballot_sync(0xffffffffu, mv);
-                    if (mv_bal && lane == __ffs(mv_bal) - 1) mv_b0 = atomicAdd(&s_movers, (unsigned)__popc(mv_bal));
-                    window_from_fractions<ORDER>(cur, qs, valid, fx, fy, fz, a, sy, sz);
-                } else {
-                    particle_window_sel<ORDER>(g, cur, qs, valid, dci, dcj, dck, a, sy, sz);
-                }
-                // the slot is free once the consumer has read its previous chunk
-                mbar_wait(empty + s * NW + warp, ph ^ 1u);
-                if (m > 0) {
-                    stage_record<L, W>(stage, lg, grp, R, a, sy, sz);
-                    if constexpr (PM != 0) {
-                        if (mv && valid) {
-                            restage_shifted<L, W>(stage, lg, grp, 0, shx, 0);
-                            restage_shifted<L, W>(stage, lg, grp, W, shx, 0);
-                            restage_shifted<L, W>(stage, lg, grp, 2 * W, shx, 0);
-                            restage_shifted<L, W>(stage, lg, grp, 3 * W, shy, 0);
-                            restage_shifted<L, W>(stage, lg, grp, 4 * W, shz, R);
+            }
+            if (lane == 0)
+                hdr[s * NW + warp] = (uint32_t)(m > 0 ? min(CH, m - base) : 0) | (cur.ci == cur.nch - 1 ? kWsLast : 0u);
+            mbar_arrive(full + s * NW + warp);
+            if constexpr (PM != 0) {
+                if (mv_bal) {
+                    const unsigned b0 = __shfl_sync(0xffffffffu, mv_b0, __ffs(mv_bal) - 1);
+                    if (mv) {
+                        const unsigned idx = b0 + (unsigned)__popc(mv_bal & ((1u << lane) - 1u));
+                        size_t e = (size_t)seg * pc.segcap + idx;
+                        if (idx >= pc.segcap) {  // segment full
+                            if constexpr (SLAB) {
+                                if (mv_cell >= kLeaveRight) {
+                                    export_leaver_now(pc, c_off + (uint32_t)(base + lg),
+                                                      col + plane_cells * (uint32_t)k, mv_cell);
+                                    e = ~(size_t)1;
+                                }
+                            }
+                            if (e != ~(size_t)1) {
+                                const unsigned o = atomicAdd(&pc.ctr->ovf_movers, 1u);
+                                e = o < pc.ovcap ? (size_t)pc.nseg * pc.segcap + o : ~(size_t)0;
+                            }
                         }
-                    }
-                }
-                if (lane == 0)
-                    hdr[s * NW + warp] = (uint32_t)(m > 0 ? min(CH, m - base) : 0) | (ci == nch - 1 ? kWsLast : 0u);
-                mbar_arrive(full + s * NW + warp);
-                if (++s == WS_NS) {
-                    s = 0;
-                    ph ^= 1u;
-                }
-                if constexpr (PM != 0) {
-                    if (mv_bal) {
-                        const unsigned b0 = __shfl_sync(0xffffffffu, mv_b0, __ffs(mv_bal) - 1);
-                        if (mv) {
-                            const unsigned idx = b0 + (unsigned)__popc(mv_bal & ((1u << lane) - 1u));
-                            size_t e = (size_t)seg * pc.segcap + idx;
-                            if (idx >= pc.segcap) {  // segment full
-                                if constexpr (SLAB) {
-                                    if (mv_cell >= kLeaveRight) {
-                                        export_leaver_now(pc, c_off + (uint32_t)(base + lg),
-                                                          col + plane_cells * (uint32_t)k, mv_cell);
-                                        e = ~(size_t)1;
-                                    }
-                                }
-                                if (e != ~(size_t)1) {
-                                    const unsigned o = atomicAdd(&pc.ctr->ovf_movers, 1u);
-                                    e = o < pc.ovcap ? (size_t)pc.nseg * pc.segcap + o : ~(size_t)0;
-                                }
-                            }
-                            if (e < ~(size_t)1) {
-                                pc.mslot[e] = c_off + (uint32_t)(base + lg);
-                                pc.mbin[e] = col + plane_cells * (uint32_t)k;
-                                pc.mcellseg[e] = mv_cell;
-                            }
+                        if (e < ~(size_t)1) {
+                            pc.mslot[e] = c_off + (uint32_t)(base + lg);
+                            pc.mbin[e] = col + plane_cells * (uint32_t)k;
+                            pc.mcellseg[e] = mv_cell;
                         }
                     }
                 }
             }
-            c_off = n_off;
-            n_c = n_n;
+            for (int t = 0; t < WS_NPW && cur.k < k1; ++t) cur.next(off, cnt, col, plane_cells, pv, CH);
+            for (int t = 0; t < WS_NPW && la.k < k1; ++t) la.next(off, cnt, col, plane_cells, pv, CH);
+            c += WS_NPW;
         }
     } else {
         // ------------------------------------------------------------ consumer
-        if constexpr (WS_REG_C > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_REG_C));
+        if constexpr (WS_NPW == 1 && WS_REG_C > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_REG_C));
         const int pxv = min(PX, g.nx - i0), pyv = min(PY, g.ny - j0);
         const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
         int gn_base[NIT], gn_node[NIT];
@@ -1258,7 +1278,7 @@ void launch_kernel_ws(const GridD& g, const CAos& p, const uint32_t* off, const 
     zch = div_up(g.nz, zlen);
     dim3 grid(tx, ty, zch);
     if constexpr (PM != 0) set_segments(pc, grid, used);
-    deposit_current_kernel_ws<ORDER, C, PM, SLAB><<<grid, 2 * L::NT, WL::SMEM, st>>>(
+    deposit_current_kernel_ws<ORDER, C, PM, SLAB><<<grid, (1 + WS_NPW) * L::NT, WL::SMEM, st>>>(
         g, p, off, cnt, q, j, j + g.ncells, j + 2 * (size_t)g.ncells, zlen, pc);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
