@@ -117,7 +117,6 @@ struct JLayout {
     static constexpr int NF = 5 * W;
     static constexpr int SS = NP + 4;
     static constexpr int FSS = C::CH * SS;
-    static constexpr int STAGE = C::G > 1 ? NF * FSS : 0;
     // v3 stages fields in PAIRS (16 bytes: one LDS.128 reads two taps): pair
     // f/2 of chunk position l of pencil grp at 16-byte unit (f/2)*PFS + l*PSS +
     // grp.  PSS = NP + 2 (2 mod 8 units) keeps a quarter-warp's writes (2
@@ -141,7 +140,6 @@ struct JLayout {
     // to distinct banks and the gather reads consecutive pencils contiguously.
     static constexpr int PSTRIDE = NP + 2;
     static constexpr int PATCH = W * W * 3 * PSTRIDE;
-    static constexpr size_t SMEM = (size_t)(2 * PATCH + STAGE) * sizeof(double);
     // per-lane record ring (C::RING > 0): RING x 64 bytes per thread after the staging
     static constexpr size_t RING_OFF = (size_t)(2 * PPB * PATCH + STAGE3);  // in doubles (even: 16-B aligned)
     static constexpr size_t SMEM3 = (RING_OFF + (size_t)C::RING * 8 * NT) * sizeof(double);
@@ -541,8 +539,12 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 // registers (v3: 168 per thread, 12 warps/SM; here 2 x 8 warps at <= 128).
 // NPW producer warps per consumer warp: 1 (2 CTAs/SM, setmaxnreg split) or 2
 // (one CTA of 12 warps per SM; producer p fills the pair's chunks c = p mod 2).
+// C2 fused: NPW 1 1.68 ms, NPW 2 1.82 ms (v3 1.61): with two producers the
+// lone consumer warp per scheduler cannot keep the FP64 pipe busy and the
+// producers' ring waits grow to 26% of the issued instructions
+// (profiles/r02/ncu_fused_ws2.txt).
 #ifndef PICGPU_WS_NPW
-#define PICGPU_WS_NPW 2
+#define PICGPU_WS_NPW 1
 #endif
 constexpr int WS_NPW = PICGPU_WS_NPW;
 #ifndef PICGPU_WS_NS
