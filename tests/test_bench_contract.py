@@ -29,3 +29,26 @@ def test_reference_arm_prints_the_contract_line():
     assert d["same_config"] is True and d["cpu_baseline"]["cores"] == 1
     assert "128x128x128 x 16 ppc" in d["cpu_baseline"]["sample"] and "1 core" in d["cpu_baseline"]["sample"]
     assert d["cpu_detail"]["order"] == 3 and d["cpu_detail"]["nproc"] >= 1 and d["cpu_detail"]["model"]
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_arm_prints_the_contract_line():
+    """The GPU arm on C1 (fast): every contract key, a self-check that passed,
+    per-order entries, the roofline with its measured traffic, and the
+    one-core same-config CPU baseline."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c1", "--steps", "3",
+                        "--warmup", "3", "--e2e-steps", "1"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks",
+              "orders", "selfcheck"):
+        assert k in d, k
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["selfcheck"]["ok"]
+    assert set(d["orders"]) == {"1", "2", "3"}
+    assert d["roofline"]["frac"] > 0 and d["roofline"]["traffic"] is not None
+    assert d["cpu_baseline"]["cores"] == 1 and d["cpu_baseline"]["same_config"] is True
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
