@@ -65,18 +65,12 @@ struct JCfg;
 #ifndef PICGPU_CIC_MINB
 #define PICGPU_CIC_MINB 4
 #endif
-// RING > 0: the records come through a per-lane cp.async ring RING deep
-// instead of one register prefetch.  Measured at C2 size, fused step: CIC
-// 1.466 ms (RING 4), 1.478 (3) vs 1.403 (0); QSP 1.751 (3) vs 1.615 (0) --
-// long-scoreboard stalls fall (9.9 -> 4.3 per issue) but shared-memory
-// pressure rises (short scoreboard 5.0, mio throttle 2.0, 33% bank-conflicted
-// wavefronts; profiles/r02/ncu_fused_cic_ring.txt).  Off by default.
-#ifndef PICGPU_CIC_RING
-#define PICGPU_CIC_RING 0
-#endif
+// (A per-lane cp.async record ring instead of the one-record register
+// prefetch measured slower -- CIC fused 1.466 vs 1.403 ms, QSP 1.751 vs 1.615:
+// fewer long-scoreboard stalls, more shared-memory pressure; removed,
+// profiles/r02/ncu_fused_cic_ring.txt.)
 struct JCfgCic3 {
     static constexpr int G = 2, PX = PICGPU_CIC_PX, PY = PICGPU_CIC_PY, MINB = PICGPU_CIC_MINB, CH = 2;
-    static constexpr int RING = PICGPU_CIC_RING;
 };
 // TSC / QSP, "lane" variant: 4 lanes per pencil (lane = jy), 8 pencils per
 // warp, 48 accumulators per lane (4 ix x 3 c x 4 kz).
@@ -89,18 +83,13 @@ struct JCfgCic3 {
 #ifndef PICGPU_LANE_PY
 #define PICGPU_LANE_PY 4
 #endif
-#ifndef PICGPU_LANE_RING
-#define PICGPU_LANE_RING 0
-#endif
 template <>
 struct JCfg<2> {
     static constexpr int G = 4, PX = PICGPU_LANE_PX, PY = PICGPU_LANE_PY, MINB = PICGPU_LANE_MINB, CH = 4;
-    static constexpr int RING = PICGPU_LANE_RING;
 };
 template <>
 struct JCfg<3> {
     static constexpr int G = 4, PX = PICGPU_LANE_PX, PY = PICGPU_LANE_PY, MINB = PICGPU_LANE_MINB, CH = 4;
-    static constexpr int RING = PICGPU_LANE_RING;
 };
 
 template <int ORDER, class CF = JCfg<ORDER>>
@@ -140,9 +129,7 @@ struct JLayout {
     // to distinct banks and the gather reads consecutive pencils contiguously.
     static constexpr int PSTRIDE = NP + 2;
     static constexpr int PATCH = W * W * 3 * PSTRIDE;
-    // per-lane record ring (C::RING > 0): RING x 64 bytes per thread after the staging
-    static constexpr size_t RING_OFF = (size_t)(2 * PPB * PATCH + STAGE3);  // in doubles (even: 16-B aligned)
-    static constexpr size_t SMEM3 = (RING_OFF + (size_t)C::RING * 8 * NT) * sizeof(double);
+    static constexpr size_t SMEM3 = (size_t)(2 * PPB * PATCH + STAGE3) * sizeof(double);
 };
 
 
@@ -298,18 +285,8 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
         n_c = (int)cnt[col + plane_cells * k0];
     }
     int last_busy = k0 - W;  // last z-step in which any pencil of the CTA deposited (CTA-uniform)
-    constexpr int RG = C::RING;
     PData nxt{};
-    [[maybe_unused]] LaneSeq<CH> seq;
-    [[maybe_unused]] RecRing<RG < 2 ? 2 : RG, L::NT> ring{reinterpret_cast<double2*>(smem + L::RING_OFF), tid};
-    if constexpr (RG > 0) {
-        static_assert(RG >= 2, "record ring: at least 2 slots");
-        seq.init(off, cnt, col, plane_cells, k0, k1, lg, pv);
-#pragma unroll
-        for (int d = 0; d < RG - 1; ++d) ring.issue(p.p, seq.next());
-    } else if (lg < n_c) {
-        load_particle<PM != 0>(p, c_off + lg, nxt);
-    }
+    if (lg < n_c) load_particle<PM != 0>(p, c_off + lg, nxt);
 
     int phase = 0;
     bool busy_acc = false;  // any deposit in this barrier's batch of planes
@@ -327,29 +304,18 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
             }
             const double dck = (double)k;
             const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
-            if (RG == 0 && m == 0 && lg < n_n) load_particle<PM != 0>(p, n_off + lg, nxt);  // empty cells: still prefetch
+            if (m == 0 && lg < n_n) load_particle<PM != 0>(p, n_off + lg, nxt);  // empty cells: still prefetch
             for (int base = 0; base < m; base += CH) {
                 [[maybe_unused]] bool mv = false;  // fused step: this lane's particle changed cell
                 [[maybe_unused]] uint32_t mv_cell = 0;
                 [[maybe_unused]] unsigned mv_bal = 0, mv_b0 = 0;
                 {
-                    PData cur;
-                    if constexpr (RG > 0) {
-                        cur = PData{};
-                        if (base + lg < n_c) {  // this lane's next record: from the ring, refill it
-                            ring.pop(cur);
-                            ring.issue(p.p, seq.next());
-                        }
-                    } else {
-                        cur = nxt;
-                    }
+                    PData cur = nxt;
                     bool valid = base + lg < n_c && !is_gap(cur.x);  // holes count as padding
-                    if constexpr (RG == 0) {
-                        if (base + CH < m) {
-                            if (base + CH + lg < n_c) load_particle<PM != 0>(p, c_off + base + CH + lg, nxt);
-                        } else if (lg < n_n) {
-                            load_particle<PM != 0>(p, n_off + lg, nxt);
-                        }
+                    if (base + CH < m) {
+                        if (base + CH + lg < n_c) load_particle<PM != 0>(p, c_off + base + CH + lg, nxt);
+                    } else if (lg < n_n) {
+                        load_particle<PM != 0>(p, n_off + lg, nxt);
                     }
                     double a[3][W], sy[W], sz[W];
                     if constexpr (PM != 0) {

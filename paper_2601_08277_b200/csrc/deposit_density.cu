@@ -636,179 +636,6 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
     }
 }
 
-// ---------------------------------------------------------------------------
-// Block-staged ordered gather, v2 (PICGPU_RHO_V2=1; measured slower than v1,
-// see run_sorted): the same block / row / piece walk
-// as density_blocks (so the same visiting order per node: source cells by
-// ascending linear id, slots in order -- bit-identical sums), with the work
-// per staged slot restructured:
-//  * thread = (X, ty), ty fastest: it owns the W nodes (X, Y = ys+OFF+ty,
-//    Z = zs+OFF+tz), tz = 0..W-1, of the current source row and keeps their W
-//    partial sums in registers for the row; the z validity of a row is
-//    CTA-uniform, so a halo plane costs no idle lanes (v1's (ty, tz) lanes
-//    idled on 39% of the rows' nodes);
-//  * the staging evaluates per slot the exact weights once and the W*W
-//    products sy*sz (the reference's inner product, deposit.hpp:41-48), so a
-//    term is q*(sx*syz): 2 DMUL + 1 DADD and 1.5 shared loads (v1: 3 DMUL +
-//    4 loads; every thread recomputed sy*sz);
-//  * staged arrays are skewed (slot i at i + i/16) so the 8 x-lanes of a warp,
-//    walking 8 neighbouring cells' slots, hit distinct banks.
-// Gaps (slack, holes) and TSC's padded tap are zero terms: a node sum starts
-// at +0.0 and x + (+-0.0) == x for every x, so they never change a sum.
-template <int ORDER>
-struct DB2Cfg {
-    static constexpr int W = Shape<ORDER>::W;
-    static constexpr int RX = ORDER == 1 ? 64 : 32, RY = 16, ZL = 8;
-    static constexpr int NT = RX * W;  // 128
-#ifndef PICGPU_RHO2_CAP
-#define PICGPU_RHO2_CAP 128
-#endif
-    static constexpr int CAP = PICGPU_RHO2_CAP;
-    static constexpr int CS = CAP + CAP / 16 + 1;   // skewed stride of one staged array
-    static constexpr int NA = W * W + W + 1;         // syz[W][W], sx[W], q
-    static constexpr int MAXC = RX + W + 1;
-#ifndef PICGPU_RHO2_MINB
-#define PICGPU_RHO2_MINB 4
-#endif
-    static constexpr int MINB = PICGPU_RHO2_MINB;
-    static constexpr size_t SMEM = (size_t)(ZL * RY * RX + NA * CS) * 8 + (size_t)2 * MAXC * 4;
-};
-
-__device__ __forceinline__ int skew16(int i) { return i + (i >> 4); }
-
-template <int ORDER>
-__global__ void __launch_bounds__(DB2Cfg<ORDER>::NT, DB2Cfg<ORDER>::MINB)
-    density_blocks2(const GridD g, const CAos p, const double* __restrict__ quantity, double qscale,
-                    const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt, double* __restrict__ rho) {
-    using C = DB2Cfg<ORDER>;
-    constexpr int W = C::W, OFF = Shape<ORDER>::OFF, RX = C::RX, RY = C::RY, ZL = C::ZL, NT = C::NT, CAP = C::CAP;
-    constexpr int CS = C::CS;
-    extern __shared__ __align__(16) double dsm[];
-    double* s_acc = dsm;                        // [ZL][RY][RX]
-    double* s_st = s_acc + ZL * RY * RX;        // [NA][CS]: syz[ty*W+tz], sx[t] at W*W+t, q at W*W+W
-    uint32_t* s_cb = reinterpret_cast<uint32_t*>(s_st + C::NA * CS);  // [MAXC] first slot of each row cell
-    uint32_t* s_ce = s_cb + C::MAXC;                                   // [MAXC] end of its extent
-
-    const int tid = threadIdx.x;
-    const int ty = tid % W, xl = tid / W;
-    const int X0 = blockIdx.x * RX, Y0 = blockIdx.y * RY, Z0 = blockIdx.z * ZL;
-    const int Bx = min(RX, g.nx - X0), By = min(RY, g.ny - Y0), Bz = min(ZL, g.nz - Z0);
-    const int X = X0 + xl;
-    const bool xv = xl < Bx;
-    for (int i = tid; i < ZL * RY * RX; i += NT) s_acc[i] = 0.0;
-
-    const Runs rx = source_runs<W, OFF>(X0, Bx, g.nx);
-    const Runs ry = source_runs<W, OFF>(Y0, By, g.ny);
-    const Runs rz = source_runs<W, OFF>(Z0, Bz, g.nz);
-    const int ncx = rx.len(), la = rx.len_a();
-    int ck[W], ct[W];
-    {
-        int xs[W];
-        sources<W, OFF>(xv ? X : 0, g.nx, xs, ct);
-#pragma unroll
-        for (int c = 0; c < W; ++c) ck[c] = xs[c] >= rx.a0 && xs[c] <= rx.a1 ? xs[c] - rx.a0 : la + xs[c] - rx.b0;
-    }
-    const double* s_syz = s_st + ty * W * CS;  // this lane's W products sy[ty]*sz[tz]
-    const double* s_q = s_st + (W * W + W) * CS;
-
-    const int nzs = rz.len(), nys = ry.len();
-    for (int zi = 0; zi < nzs; ++zi) {
-        const int zs = rz.at(zi);
-        int zl[W];
-        unsigned zmask = 0;  // CTA-uniform: the tz whose node lies in this block
-#pragma unroll
-        for (int tz = 0; tz < W; ++tz) {
-            zl[tz] = wrap_index(zs + OFF + tz, g.nz) - Z0;
-            if (zl[tz] >= 0 && zl[tz] < Bz) zmask |= 1u << tz;
-        }
-        for (int yi = 0; yi < nys; ++yi) {
-            const int ys = ry.at(yi);
-            const int yl = wrap_index(ys + OFF + ty, g.ny) - Y0;
-            const bool mine = xv && yl >= 0 && yl < By;
-            const uint32_t rowc = (uint32_t)g.nx * ((uint32_t)ys + (uint32_t)g.ny * (uint32_t)zs);
-            __syncthreads();  // the previous row is consumed
-            for (int k = tid; k < ncx; k += NT) {
-                const uint32_t c = rowc + (uint32_t)rx.at(k);
-                const uint32_t o = off[c];
-                s_cb[k] = o;
-                s_ce[k] = o + cnt[c];
-            }
-            __syncthreads();
-            const uint32_t lena = s_ce[la - 1] - s_cb[0];
-            const uint32_t total = lena + (ncx > la ? s_ce[ncx - 1] - s_cb[la] : 0u);
-            uint32_t mb[W], me[W];
-#pragma unroll
-            for (int c = 0; c < W; ++c) {
-                const int k = ck[c];
-                const uint32_t base = k < la ? s_cb[k] - s_cb[0] : lena + (s_cb[k] - s_cb[la]);
-                mb[c] = base;
-                me[c] = base + (s_ce[k] - s_cb[k]);
-            }
-            double acc[W];
-#pragma unroll
-            for (int tz = 0; tz < W; ++tz)
-                acc[tz] = (mine && (zmask >> tz & 1u)) ? s_acc[((size_t)zl[tz] * RY + yl) * RX + xl] : 0.0;
-            for (uint32_t piece = 0; piece < total; piece += CAP) {
-                const uint32_t pn = min((uint32_t)CAP, total - piece);
-                if (piece) __syncthreads();  // the previous piece is consumed
-                for (uint32_t i = tid; i < pn; i += NT) {
-                    const uint32_t pos = piece + i;
-                    const uint32_t sl = pos < lena ? s_cb[0] + pos : s_cb[la] + (pos - lena);
-                    const int si = skew16((int)i);
-                    const double2 r0 = reinterpret_cast<const double2*>(p.p + sl)[0];
-                    if (is_gap(r0.x)) {  // slack or a hole: a zero term
-#pragma unroll
-                        for (int a = 0; a < C::NA; ++a) s_st[a * CS + si] = 0.0;
-                        continue;
-                    }
-                    double f[3];
-                    locate_x(g, r0.x, f[0]);
-                    locate_axis(r0.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
-                    locate_axis(p.p[sl].z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
-                    double wx[W], wy[W], wz[W];
-                    int up;
-                    Shape<ORDER>::weights(f[0], wx, up);
-                    Shape<ORDER>::weights(f[1], wy, up);
-                    Shape<ORDER>::weights(f[2], wz, up);
-#pragma unroll
-                    for (int a = 0; a < W; ++a)
-#pragma unroll
-                        for (int b = 0; b < W; ++b) s_st[(a * W + b) * CS + si] = __dmul_rn(wy[a], wz[b]);
-#pragma unroll
-                    for (int t = 0; t < W; ++t) s_st[(W * W + t) * CS + si] = wx[t];
-                    s_st[(W * W + W) * CS + si] = quantity ? quantity[sl] : qscale * p.p[sl].w;
-                }
-                __syncthreads();
-                if (!mine) continue;
-#pragma unroll
-                for (int c = 0; c < W; ++c) {
-                    const uint32_t b = max(mb[c], piece), e = min(me[c], piece + pn);
-                    const double* wxp = s_st + (W * W + ct[c]) * CS;
-                    for (uint32_t u = b; u < e; ++u) {
-                        const int si = skew16((int)(u - piece));
-                        const double q = s_q[si], sx = wxp[si];
-#pragma unroll
-                        for (int tz = 0; tz < W; ++tz)
-                            if (zmask >> tz & 1u) acc[tz] = __dadd_rn(acc[tz], __dmul_rn(q, __dmul_rn(sx, s_syz[tz * CS + si])));
-                    }
-                }
-            }
-            if (mine) {
-#pragma unroll
-                for (int tz = 0; tz < W; ++tz)
-                    if (zmask >> tz & 1u) s_acc[((size_t)zl[tz] * RY + yl) * RX + xl] = acc[tz];
-            }
-        }
-    }
-    __syncthreads();
-    for (int i = tid; i < ZL * RY * RX; i += NT) {
-        const int xl2 = i % RX, yl2 = (i / RX) % RY, zl2 = i / (RX * RY);
-        if (xl2 < Bx && yl2 < By && zl2 < Bz)
-            rho[(size_t)(X0 + xl2) + (size_t)g.nx * ((size_t)(Y0 + yl2) + (size_t)g.ny * (size_t)(Z0 + zl2))] =
-                s_acc[i];
-    }
-}
-
 template <int ORDER>
 void prologue(const GridD& g, const CAos& p, const double* quantity, double qscale, uint64_t slots, void* scratch,
               cudaStream_t st, double*& S, uint8_t*& upb) {
@@ -833,38 +660,20 @@ void run_sorted(const GridD& g, const CAos& p, const double* quantity, double qs
         return e && e[0] == '1';
     }();
     if (rows) return run_rows_and_shell<ORDER>(g, p, quantity, qscale, off, cnt, slots, scratch, rho, st);
-    // v2 (PICGPU_RHO_V2=1) measured slower at C2 QSP: 6.64 vs 4.34 ms (CIC 4.28 vs
-    // 1.64): its 8 x-lanes per warp walk 8 different cells, so a warp runs the
-    // longest of 8 slot ranges in each staged piece (7.5G lane-terms issued for
-    // 2.15G terms) and its 512 CTAs of 128 threads fill one wave at 13 warps/SM
-    // (profiles/r02/ncu_rho_v2.txt).
-    static const bool v1 = [] {
-        const char* e = std::getenv("PICGPU_RHO_V2");
-        return !(e && e[0] == '1');
-    }();
+    // (a v2 with thread = (X, jy) and CTA-uniform z chains measured slower:
+    // QSP 6.64 vs 4.34 ms -- its 8 x-lanes per warp walk 8 cells' slot ranges;
+    // removed, profiles/r02/ncu_rho_v2.txt)
+    using C = DBCfg<ORDER>;
     int dev = 0;
     PICGPU_CUDA_TRY(cudaGetDevice(&dev));
-    if (v1) {
-        using C = DBCfg<ORDER>;
-        static int configured_dev = -1;
-        if (configured_dev != dev) {  // per device (one process may drive several GPUs)
-            PICGPU_CUDA_TRY(cudaFuncSetAttribute(density_blocks<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)C::SMEM));
-            configured_dev = dev;
-        }
-        const dim3 grid(div_up(g.nx, C::RX), div_up(g.ny, C::RY), div_up(g.nz, C::ZL));
-        density_blocks<ORDER><<<grid, C::NT, C::SMEM, st>>>(g, p, quantity, qscale, off, cnt, rho);
-    } else {
-        using C = DB2Cfg<ORDER>;
-        static int configured_dev = -1;
-        if (configured_dev != dev) {
-            PICGPU_CUDA_TRY(cudaFuncSetAttribute(density_blocks2<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)C::SMEM));
-            configured_dev = dev;
-        }
-        const dim3 grid(div_up(g.nx, C::RX), div_up(g.ny, C::RY), div_up(g.nz, C::ZL));
-        density_blocks2<ORDER><<<grid, C::NT, C::SMEM, st>>>(g, p, quantity, qscale, off, cnt, rho);
+    static int configured_dev = -1;
+    if (configured_dev != dev) {  // per device (one process may drive several GPUs)
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(density_blocks<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)C::SMEM));
+        configured_dev = dev;
     }
+    const dim3 grid(div_up(g.nx, C::RX), div_up(g.ny, C::RY), div_up(g.nz, C::ZL));
+    density_blocks<ORDER><<<grid, C::NT, C::SMEM, st>>>(g, p, quantity, qscale, off, cnt, rho);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }

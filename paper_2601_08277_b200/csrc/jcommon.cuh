@@ -326,78 +326,6 @@ __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// A lane's own particle sequence through its pencil's cells k0..k1-1 (the
-// slots lg, lg + CH, ... of each bin, empty bins skipped): the records the
-// lane will stage, in order, so they can be fetched ahead.
-template <int CH>
-struct LaneSeq {
-    const uint32_t* off;
-    const uint32_t* cnt;
-    uint32_t col, plane, boff = 0;
-    int k = 0, k1 = 0, idx = 0, n = 0, lg = 0;
-    bool done = true;
-    __device__ __forceinline__ void init(const uint32_t* o, const uint32_t* c, uint32_t col_, uint32_t plane_, int k0,
-                                         int k1_, int lg_, bool pv) {
-        off = o; cnt = c; col = col_; plane = plane_; k1 = k1_; lg = lg_;
-        k = k0;
-        idx = lg;
-        done = !pv || k0 >= k1;
-        if (!done) {
-            boff = off[col + plane * k];
-            n = (int)cnt[col + plane * k];
-            settle();
-        }
-    }
-    __device__ __forceinline__ void settle() {
-        while (idx >= n) {
-            if (k + 1 >= k1) {
-                done = true;
-                return;
-            }
-            ++k;
-            boff = off[col + plane * k];
-            n = (int)cnt[col + plane * k];
-            idx = lg;
-        }
-    }
-    // the next record's slot (or -1 past the end)
-    __device__ __forceinline__ long long next() {
-        if (done) return -1;
-        const long long s = (long long)boff + idx;
-        idx += CH;
-        settle();
-        return s;
-    }
-};
-
-// Per-lane ring of D particle records in shared memory, fetched D-1 records
-// ahead with cp.async (no registers held while in flight).  Layout
-// [slot][16-byte quarter][thread]: a warp's quarter loads are 512 contiguous
-// bytes (no bank conflicts).  One commit group per record (empty past the end).
-template <int D, int NT>
-struct RecRing {
-    double2* base;
-    int tid;
-    uint32_t head = 0, tail = 0;
-    __device__ __forceinline__ void issue(const Part* p, long long slot) {
-        if (slot >= 0) {
-            const double2* src = reinterpret_cast<const double2*>(p + slot);
-            double2* dst = base + (size_t)(head % D) * 4 * NT + tid;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) cp_async16(dst + q * NT, src + q);
-        }
-        cp_async_commit();
-        ++head;
-    }
-    __device__ __forceinline__ void pop(PData& d) {
-        cp_async_wait<D - 2>();
-        const double2* r = base + (size_t)(tail % D) * 4 * NT + tid;
-        const double2 a = r[0], b = r[NT], c = r[2 * NT], e = r[3 * NT];
-        d.x = a.x; d.y = a.y; d.z = b.x; d.vx = b.y; d.vy = c.x; d.vz = c.y; d.w = e.x;
-        ++tail;
-    }
-};
-
 // mbarrier (shared::cta) primitives.
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);

@@ -533,171 +533,6 @@ __global__ void __launch_bounds__(PICGPU_PUSH_NT, PICGPU_PUSH_MINB) k_push(const
 // more than kHoleCap front holes fall back to a stable slide.
 constexpr int kHoleCap = 32;
 
-// ---- the unfused push in two streaming kernels (PICGPU_PUSH2=1, opt-in) -----
-// k_push carried a CTA barrier and a global reservation round trip per 512
-// slots (C3 ncu: barrier stalls 18 per issue, 2.3 TB/s).  Here k_push_mark
-// streams the records with no barrier and no atomic on the hot path: push,
-// write-back, move test, and per slot a u32 code (the new cell of a mover,
-// kNoCell otherwise) plus the old bin of a mover; slab leavers are exported
-// on the spot (rare).  k_collect then compacts the movers IN SLOT ORDER with
-// a decoupled look-back over 4096-slot tiles (the radix sort's scheme):
-// record into the mover list, hole into its slot, (slot, old bin, cell) for
-// k_departures / k_insert -- a deterministic mover list.
-constexpr int PM_NT = 512;
-constexpr int CL_NT = 512, CL_ITEMS = 8, CL_TILE = CL_NT * CL_ITEMS;
-constexpr unsigned long long CL_FLAG_AGG = 1ull << 62, CL_FLAG_PFX = 2ull << 62, CL_VALUE = (1ull << 62) - 1;
-
-template <bool P2>
-__global__ void __launch_bounds__(PM_NT, 2) k_push_mark(const GridD g, const Aos A, uint64_t slots, double dt,
-                                                        double cap2, uint32_t* __restrict__ code,
-                                                        uint32_t* __restrict__ obin, const uint32_t* __restrict__ off,
-                                                        uint32_t* __restrict__ holes, uint32_t* __restrict__ hl,
-                                                        StepCounters* ctr, double* __restrict__ L, uint32_t lcap,
-                                                        unsigned long long* __restrict__ mvpart) {
-    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t out = kNoCell;
-    bool moved = false;
-    if (s < slots) {
-        const double2* r = reinterpret_cast<const double2*>(A.p + s);
-        const double2 a = r[0], b = r[1], c = r[2];
-        double x = a.x, y = a.y, z = b.x;
-        const double vx = b.y, vy = c.x, vz = c.y;
-        if (!is_gap(x)) {
-            if (!finite3(x, y, z)) {
-                raise_error(&ctr->err, PICGPU_EINVAL);
-            } else {
-                const double ox = x, oy = y, oz = z;
-                bool ok = push_one<P2>(g, dt, cap2, x, y, z, vx, vy, vz);
-                if (!ok) {
-                    raise_error(&ctr->err, PICGPU_EDOMAIN);
-                } else {
-                    reinterpret_cast<double2*>(A.p + s)[0] = make_double2(x, y);
-                    A.p[s].z = z;
-                    if (!finite3(x, y, z)) {
-                        raise_error(&ctr->err, PICGPU_EINVAL);
-                        ok = false;
-                    }
-                }
-                if (ok) {
-                    const int p2x = P2 || g.pow2x, p2y = P2 || g.pow2y, p2z = P2 || g.pow2z;
-                    const double fx0 = axis_floor(ox, g.gox, g.dx, g.inv_dx, p2x);
-                    const double fy0 = axis_floor(oy, g.oy, g.dy, g.inv_dy, p2y);
-                    const double fz0 = axis_floor(oz, g.oz, g.dz, g.inv_dz, p2z);
-                    const bool same = fx0 >= 0.0 && fy0 >= 0.0 && fz0 >= 0.0 &&
-                                      fx0 == axis_floor(x, g.gox, g.dx, g.inv_dx, p2x) &&
-                                      fy0 == axis_floor(y, g.oy, g.dy, g.inv_dy, p2y) &&
-                                      fz0 == axis_floor(z, g.oz, g.dz, g.inv_dz, p2z);
-                    if (!same) {
-                        const uint32_t before = store_cell<P2>(g, ox, oy, oz);
-                        const uint32_t nc = store_cell<P2>(g, x, y, z);
-                        if (nc != before) {
-                            moved = true;
-                            if (nc >= kLeaveRight) {  // left the slab: exchange record now (rare)
-                                const int dir = nc == kLeaveLeft ? 0 : 1;
-                                const unsigned li = atomicAdd(&ctr->nleave[dir], 1u);
-                                if (li < lcap) {
-                                    const double2 wid = r[3];
-                                    double* rr = L + ((size_t)dir * lcap + li) * 8;
-                                    rr[0] = x; rr[1] = y; rr[2] = z;
-                                    rr[3] = vx; rr[4] = vy; rr[5] = vz;
-                                    rr[6] = wid.x;
-                                    rr[7] = wid.y;
-                                    push_hole(A, s, before, off, holes, hl);
-                                } else {
-                                    raise_error(&ctr->err, PICGPU_ELENGTH);
-                                }
-                            } else {
-                                out = nc;
-                                obin[s] = before;
-                            }
-                        }
-                    }
-                }
-            }
-        }
-        code[s] = out;
-    }
-    const unsigned wm = __reduce_add_sync(0xffffffffu, moved ? 1u : 0u);
-    if ((threadIdx.x & 31) == 0 && wm)
-        atomicAdd(mvpart + (size_t)((blockIdx.x * (PM_NT / 32) + (threadIdx.x >> 5)) % kMovedParts) * 16,
-                  (unsigned long long)wm);
-}
-
-__global__ void __launch_bounds__(CL_NT) k_collect(const uint32_t* __restrict__ code, const uint32_t* __restrict__ obin,
-                                                  const Aos A, uint64_t slots, const Soa M, uint32_t* __restrict__ mcell,
-                                                  uint32_t* __restrict__ mslot, uint32_t* __restrict__ mbin,
-                                                  uint32_t mcap, unsigned long long* status, uint32_t* tile_counter,
-                                                  uint64_t ntiles, StepCounters* ctr) {
-    constexpr int NW = CL_NT / 32;
-    __shared__ uint32_t s_wc[CL_ITEMS][NW];  // movers per (item, warp) -> exclusive prefix
-    __shared__ uint32_t s_tile;
-    __shared__ unsigned long long s_base;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-    __syncthreads();
-    const uint64_t tile = s_tile;
-    const uint64_t t0 = tile * CL_TILE;
-    uint32_t c[CL_ITEMS];
-    unsigned bal[CL_ITEMS];
-#pragma unroll
-    for (int j = 0; j < CL_ITEMS; ++j) {
-        const uint64_t sl = t0 + (uint64_t)j * CL_NT + threadIdx.x;
-        c[j] = sl < slots ? code[sl] : kNoCell;
-        bal[j] = __ballot_sync(0xffffffffu, c[j] != kNoCell);
-        if (lane == 0) s_wc[j][warp] = __popc(bal[j]);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {  // tile order is (item, warp, lane) = slot order
-        uint32_t run = 0;
-        for (int j = 0; j < CL_ITEMS; ++j)
-            for (int w = 0; w < NW; ++w) {
-                const uint32_t v = s_wc[j][w];
-                s_wc[j][w] = run;
-                run += v;
-            }
-        unsigned long long* my = status + tile;
-        unsigned long long excl = 0;
-        if (tile == 0) {
-            atomicExch(my, CL_FLAG_PFX | run);
-        } else {
-            atomicExch(my, CL_FLAG_AGG | run);
-            for (int64_t q = (int64_t)tile - 1; q >= 0; --q) {
-                const volatile unsigned long long* sp = status + q;
-                unsigned long long v;
-                do {
-                    v = *sp;
-                } while ((v & (CL_FLAG_AGG | CL_FLAG_PFX)) == 0);
-                excl += v & CL_VALUE;
-                if (v & CL_FLAG_PFX) break;
-            }
-            atomicExch(my, CL_FLAG_PFX | (excl + run));
-        }
-        s_base = excl;
-        if (tile == ntiles - 1) {
-            const unsigned long long tot = excl + run;
-            ctr->nmovers = tot > 0xffffffffull ? 0xffffffffu : (uint32_t)tot;
-        }
-    }
-    __syncthreads();
-    const unsigned long long base = s_base;
-#pragma unroll
-    for (int j = 0; j < CL_ITEMS; ++j) {
-        if (c[j] == kNoCell) continue;
-        const uint64_t sl = t0 + (uint64_t)j * CL_NT + threadIdx.x;
-        const unsigned long long e = base + s_wc[j][warp] + __popc(bal[j] & ((1u << lane) - 1u));
-        if (e >= mcap) continue;  // not recorded: nmovers > mcap -> full re-sort
-        const Part r = A.p[sl];
-        M.x[e] = r.x; M.y[e] = r.y; M.z[e] = r.z;
-        M.vx[e] = r.vx; M.vy[e] = r.vy; M.vz[e] = r.vz;
-        M.w[e] = r.w;
-        M.id[e] = r.id;
-        mcell[e] = c[j];
-        mslot[e] = (uint32_t)sl;
-        mbin[e] = obin[sl];
-        store_gap_record(A.p + sl);
-    }
-}
-
 // ctr->moved += the spread partial counts of k_push; the partials are reset.
 __global__ void k_fold_moved(unsigned long long* __restrict__ mvpart, StepCounters* ctr) {
     unsigned long long v = 0;
@@ -1597,40 +1432,6 @@ void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     const int blocks = (int)((capacity + PICGPU_PUSH_NT * UNR - 1) / (PICGPU_PUSH_NT * UNR));
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
     hl.ensure(capacity * 4 + 4);
-    // C3 (537M, 11% movers): mark 34.0 + collect 12.5 ms vs k_push 30 ms --
-    // the mark kernel alone streams at 2 TB/s (one 64-byte record in flight per
-    // thread at 32 warps/SM), so removing k_push's barrier and reservation did
-    // not pay; kept opt-in (PICGPU_PUSH2=1).
-    static const bool two_pass = [] {
-        const char* e = std::getenv("PICGPU_PUSH2");
-        return e && e[0] == '1';
-    }();
-    if (push && two_pass) {
-        // mark (streaming push + move codes) -> collect (look-back compaction, slot order)
-        keys.ensure(capacity * 4 + 4);   // code (u32 per slot)
-        keys2.ensure(capacity * 4 + 4);  // old bin of a mover (u32 per slot)
-        const uint64_t ntiles = (capacity + CL_TILE - 1) / CL_TILE;
-        sort_tmp.ensure(256 + ntiles * 8);
-        unsigned long long* status = reinterpret_cast<unsigned long long*>(sort_tmp.as<char>() + 256);
-        PICGPU_CUDA_TRY(cudaMemsetAsync(sort_tmp.p, 0, 256 + ntiles * 8, st));
-        auto* mark = p2 ? k_push_mark<true> : k_push_mark<false>;
-        mark<<<div_up((long long)capacity, PM_NT), PM_NT, 0, st>>>(
-            g, A.aos(), capacity, dt, cap2, keys.as<uint32_t>(), keys2.as<uint32_t>(), off.as<uint32_t>(),
-            holes.as<uint32_t>(), hl.as<uint32_t>(), ctr, lrec.as<double>(), (uint32_t)lcap, moved_parts());
-        k_collect<<<(unsigned)ntiles, CL_NT, 0, st>>>(keys.as<uint32_t>(), keys2.as<uint32_t>(), A.aos(), capacity,
-                                                     M.soa(), mcell.as<uint32_t>(), mslot.as<uint32_t>(),
-                                                     mbin.as<uint32_t>(), (uint32_t)mcap, status,
-                                                     sort_tmp.as<uint32_t>(), ntiles, ctr);
-        k_fold_moved<<<1, 256, 0, st>>>(moved_parts(), ctr);
-        note_launch(3);
-        PICGPU_CUDA_TRY(cudaGetLastError());
-        k_departures<<<num_sms * 8, 256, 0, st>>>(counters.as<StepCounters>(), (uint32_t)mcap, mslot.as<uint32_t>(),
-                                                  mbin.as<uint32_t>(), off.as<uint32_t>(), holes.as<uint32_t>(),
-                                                  hl.as<uint32_t>());
-        note_launch();
-        PICGPU_CUDA_TRY(cudaGetLastError());
-        return;
-    }
     auto* kern = push ? (p2 ? k_push<true, UNR, true> : k_push<true, UNR, false>)
                       : (p2 ? k_push<false, UNR, true> : k_push<false, UNR, false>);
     kern<<<blocks, PICGPU_PUSH_NT, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(),
