@@ -324,6 +324,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--order", type=int, default=None, choices=[1, 2, 3], help="override the config's shape order")
+    ap.add_argument("--steady-steps", type=int, default=130,
+                    help="C2: time the step again after this many further steps (steady-state cell counts)")
     ap.add_argument("--no-orders", dest="orders", action="store_false",
                     help="skip the per-order (1/2/3) runs on the same box")
     ap.add_argument("--slab", action="store_true", help="use the slab-decomposed path even at N=1 (loopback ring)")
@@ -534,6 +536,29 @@ def main():
         if not check["ok"]:
             print(json.dumps({"error": "bench self-check failed", "selfcheck": check}), file=sys.stderr)
             return 1
+    steady = None
+    if single and args.config == "c2" and args.steady_steps > 0:
+        # the bench window starts from the generator's exactly-ppc cells; migration
+        # spreads the counts towards Poisson (a warp's 8 pencils then contract as
+        # many particles as the fullest): the same step after `steady_steps` more
+        # steps (no global sort in between), reported beside the headline
+        for _ in range(args.steady_steps):
+            S.step(dt)
+        stream = torch.cuda.ExternalStream(S.stream)
+        ph0 = S.phase_times()["deposit_current"]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            S.step(dt)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        ph1 = S.phase_times()["deposit_current"]
+        kms = (ph1[0] - ph0[0]) / max(ph1[1] - ph0[1], 1)
+        steady = {"value": res["n"] * args.steps / (ms * 1e-3), "ms_per_step": ms / args.steps,
+                  "kernel_ms": kms, "after_steps": args.warmup + args.steps + args.steady_steps,
+                  "roofline_frac": res["n"] * FLOPS[order] / (kms * 1e-3) / 1e12 / fp64_peak}
     if single and args.e2e_steps > 0:
         # the device-resident session as a PIC code drives it: particles uploaded
         # once from host memory, then every step push + sort + J on the device
@@ -637,6 +662,7 @@ def main():
                        f"x-slabs x{world} of a {'x'.join(map(str, G_dims))} box, NCCL ring exchange "
                        f"(migration + J guards; {'picgpu_session_slab_step' if args.exchange == 'nccl' else 'torch.distributed'})"},
             "roofline": res["roofline"], "step_roofline_frac": res["step_roofline_frac"], "orders": orders,
+            "steady_state": steady,
             "cpu_baseline": cpu, "e2e": e2e, "e2e_session": e2e_session, "gpu_launches": res["launches"],
             "clocks": res["clocks"], "selfcheck": check,
             "phases_ms_total": res["phases_ms_total"],
