@@ -210,12 +210,14 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
     const int grp = tid / G, lg = tid % G;
     const int ly = lg % W, xh = lg / W;  // this lane's jy and x-half
     const int px = grp % PX, py = grp / PX;
-    const int i0 = blockIdx.x * PX, j0 = blockIdx.y * PY;
+    // tiles cover x-cells [xb, xe): a slab's owned cells (its ghost cells hold no particles)
+    const int xb = g.slab ? g.sx_lo : 0, xe = g.slab ? g.sx_hi : g.nx;
+    const int i0 = xb + blockIdx.x * PX, j0 = blockIdx.y * PY;
     const int k0 = blockIdx.z * zlen;
     const int k1 = min(k0 + zlen, g.nz);
     const int i = i0 + px, j = j0 + py;
-    const bool pv = (i < g.nx) && (j < g.ny);
-    const int pxv = min(PX, g.nx - i0), pyv = min(PY, g.ny - j0);
+    const bool pv = (i < xe) && (j < g.ny);
+    const int pxv = min(PX, xe - i0), pyv = min(PY, g.ny - j0);
     const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
     const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
     const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
@@ -621,11 +623,13 @@ __global__ void __launch_bounds__((1 + WS_NPW) * JLayout<ORDER, CF>::NT, PICGPU_
     const int grp = tid / G, lg = tid % G;
     const int ly = lg % W, xh = lg / W;
     const int px = grp % PX, py = grp / PX;
-    const int i0 = blockIdx.x * PX, j0 = blockIdx.y * PY;
+    // tiles cover x-cells [xb, xe): a slab's owned cells (its ghost cells hold no particles)
+    const int xb = g.slab ? g.sx_lo : 0, xe = g.slab ? g.sx_hi : g.nx;
+    const int i0 = xb + blockIdx.x * PX, j0 = blockIdx.y * PY;
     const int k0 = blockIdx.z * zlen;
     const int k1 = min(k0 + zlen, g.nz);
     const int i = i0 + px, j = j0 + py;
-    const bool pv = (i < g.nx) && (j < g.ny);
+    const bool pv = (i < xe) && (j < g.ny);
     const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
     const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
     [[maybe_unused]] const uint32_t seg = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -746,7 +750,7 @@ __global__ void __launch_bounds__((1 + WS_NPW) * JLayout<ORDER, CF>::NT, PICGPU_
     } else {
         // ------------------------------------------------------------ consumer
         if constexpr (WS_NPW == 1 && WS_REG_C > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_REG_C));
-        const int pxv = min(PX, g.nx - i0), pyv = min(PY, g.ny - j0);
+        const int pxv = min(PX, xe - i0), pyv = min(PY, g.ny - j0);
         const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
         int gn_base[NIT], gn_node[NIT];
         unsigned gn_mask[NIT];
@@ -1205,7 +1209,7 @@ void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uin
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured_dev = dev;
     }
-    const int tx = div_up(g.nx, C::PX), ty = div_up(g.ny, C::PY);
+    const int tx = div_up(g.slab ? g.sx_hi - g.sx_lo : g.nx, C::PX), ty = div_up(g.ny, C::PY);
     // z-chunks: enough CTAs for several waves on every SM, but chunks of at
     // least 4*W cells so most planes are complete (plain stores, no RED).
     const long long tiles = (long long)tx * ty;
@@ -1237,7 +1241,7 @@ void launch_kernel_ws(const GridD& g, const CAos& p, const uint32_t* off, const 
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WL::SMEM));
         configured_dev = dev;
     }
-    const int tx = div_up(g.nx, C::PX), ty = div_up(g.ny, C::PY);
+    const int tx = div_up(g.slab ? g.sx_hi - g.sx_lo : g.nx, C::PX), ty = div_up(g.ny, C::PY);
     const long long tiles = (long long)tx * ty;
     const long long target = (long long)num_sms * PICGPU_WS_MINB * 4;
     int zch = (int)std::max<long long>(1, (target + tiles - 1) / tiles);
