@@ -53,6 +53,13 @@ namespace {
 
 using namespace jdev;
 
+// Record prefetch of the lane kernel: 1 = after the window is staged, into the
+// record's own registers (no copy, 14 fewer registers live); 0 = before the
+// prologue into a second record of registers.
+#ifndef PICGPU_LATE_PREFETCH
+#define PICGPU_LATE_PREFETCH 1
+#endif
+
 template <int ORDER>
 struct JCfg;
 // CIC on the v3 kernel: 2 lanes per pencil (lane = jy), 12 accumulators each.
@@ -312,13 +319,23 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                 [[maybe_unused]] uint32_t mv_cell = 0;
                 [[maybe_unused]] unsigned mv_bal = 0, mv_b0 = 0;
                 {
+#if PICGPU_LATE_PREFETCH
+                    // the record is used in place and its registers take the next
+                    // record once the window is staged (the load has the whole
+                    // contraction to land): no copy, one record of registers
+                    PData& cur = nxt;
+#else
                     PData cur = nxt;
+#endif
                     bool valid = base + lg < n_c && !is_gap(cur.x);  // holes count as padding
-                    if (base + CH < m) {
-                        if (base + CH + lg < n_c) load_particle<PM != 0>(p, c_off + base + CH + lg, nxt);
-                    } else if (lg < n_n) {
-                        load_particle<PM != 0>(p, n_off + lg, nxt);
-                    }
+                    auto prefetch = [&] {
+                        if (base + CH < m) {
+                            if (base + CH + lg < n_c) load_particle<PM != 0>(p, c_off + base + CH + lg, nxt);
+                        } else if (lg < n_n) {
+                            load_particle<PM != 0>(p, n_off + lg, nxt);
+                        }
+                    };
+                    if (!PICGPU_LATE_PREFETCH) prefetch();
                     double a[3][W], sy[W], sz[W];
                     if constexpr (PM != 0) {
                         // pic::advance (workload.hpp:139-155) + Gpma::detect_moves (gpma.hpp:162-177):
@@ -350,6 +367,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                         particle_window_sel<ORDER>(g, cur, qs, valid, dci, dcj, dck, a, sy, sz);
                         stage_record<L, W>(stage, lg, grp, R, a, sy, sz);
                     }
+                    if (PICGPU_LATE_PREFETCH) prefetch();
                 }
                 __syncwarp();
                 const int nn = min(CH, m - base);
