@@ -54,8 +54,10 @@ namespace {
 using namespace jdev;
 
 // Record prefetch of the lane kernel: 1 = after the window is staged, into the
-// record's own registers (no copy, 14 fewer registers live); 0 = before the
-// prologue into a second record of registers.
+// record's own registers (no copy, 14 fewer registers live; the fused QSP kernel
+// stops spilling); 0 = before the prologue into a second record of registers.
+// C2 fused kernel: QSP 1.612 vs 1.617 ms, CIC 1.352 vs 1.403, TSC 1.703 vs
+// 1.669 (spills appear) -- so TSC keeps the early prefetch.
 #ifndef PICGPU_LATE_PREFETCH
 #define PICGPU_LATE_PREFETCH 1
 #endif
@@ -319,14 +321,13 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                 [[maybe_unused]] uint32_t mv_cell = 0;
                 [[maybe_unused]] unsigned mv_bal = 0, mv_b0 = 0;
                 {
-#if PICGPU_LATE_PREFETCH
-                    // the record is used in place and its registers take the next
-                    // record once the window is staged (the load has the whole
+                    // LATE: the record is used in place and its registers take the
+                    // next record once the window is staged (the load has the whole
                     // contraction to land): no copy, one record of registers
-                    PData& cur = nxt;
-#else
-                    PData cur = nxt;
-#endif
+                    constexpr bool LATE = PICGPU_LATE_PREFETCH && ORDER != 2;
+                    PData early;
+                    if constexpr (!LATE) early = nxt;
+                    PData& cur = LATE ? nxt : early;
                     bool valid = base + lg < n_c && !is_gap(cur.x);  // holes count as padding
                     auto prefetch = [&] {
                         if (base + CH < m) {
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                             load_particle<PM != 0>(p, n_off + lg, nxt);
                         }
                     };
-                    if (!PICGPU_LATE_PREFETCH) prefetch();
+                    if constexpr (!LATE) prefetch();
                     double a[3][W], sy[W], sz[W];
                     if constexpr (PM != 0) {
                         // pic::advance (workload.hpp:139-155) + Gpma::detect_moves (gpma.hpp:162-177):
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                         particle_window_sel<ORDER>(g, cur, qs, valid, dci, dcj, dck, a, sy, sz);
                         stage_record<L, W>(stage, lg, grp, R, a, sy, sz);
                     }
-                    if (PICGPU_LATE_PREFETCH) prefetch();
+                    if constexpr (LATE) prefetch();
                 }
                 __syncwarp();
                 const int nn = min(CH, m - base);
