@@ -62,13 +62,6 @@ using namespace jdev;
 #define PICGPU_LATE_PREFETCH 1
 #endif
 
-// Lane kernel staging: 1 = the prologue lane stages b[jy][kz] = sy[jy]*sz[kz]
-// (the contraction lanes load their b row instead of forming yv*sz: no
-// DMUL -> DFMA dependency in the contraction); 0 = sy and sz staged.
-#ifndef PICGPU_BSTAGE
-#define PICGPU_BSTAGE 1
-#endif
-
 template <int ORDER>
 struct JCfg;
 // CIC on the v3 kernel: 2 lanes per pencil (lane = jy), 12 accumulators each.
@@ -119,9 +112,7 @@ struct JLayout {
     // 4W+t) of chunk position l of pencil grp at [f*FSS + l*SS + grp].  SS =
     // NP + 4 makes the writes of a half-warp (4 pencils x 4 positions) hit 16
     // distinct banks and the reads (8 pencils, same position) contiguous.
-    // BSTAGE: the staged record is a[c][ix] (3W) and b[jy][kz] = sy*sz (W*W, kz
-    // at its physical z slot); otherwise a, sy (W) and sz (W)
-    static constexpr int NF = PICGPU_BSTAGE ? 3 * W + W * W : 5 * W;
+    static constexpr int NF = 5 * W;
     static constexpr int SS = NP + 4;
     static constexpr int FSS = C::CH * SS;
     // v3 stages fields in PAIRS (16 bytes: one LDS.128 reads two taps): pair
@@ -173,49 +164,11 @@ __device__ __forceinline__ void stage_record(double* stage, int l, int grp, int 
 #pragma unroll
         for (int t = 0; t < W; t += 2)
             *reinterpret_cast<double2*>(pfield<L>(stage, c * W + t, l, grp)) = make_double2(a[c][t], a[c][t + 1]);
-    if constexpr (PICGPU_BSTAGE) {
-        double zp[W];  // sz at its physical slot: slot sl holds logical plane (sl - R) mod W
 #pragma unroll
-        for (int sl = 0; sl < W; ++sl) {
-            double v = sz[0];
+    for (int t = 0; t < W; t += 2)
+        *reinterpret_cast<double2*>(pfield<L>(stage, 3 * W + t, l, grp)) = make_double2(sy[t], sy[t + 1]);
 #pragma unroll
-            for (int t = 1; t < W; ++t) v = ((t + R) & (W - 1)) == sl ? sz[t] : v;
-            zp[sl] = v;
-        }
-#pragma unroll
-        for (int jy = 0; jy < W; ++jy)
-#pragma unroll
-            for (int sl = 0; sl < W; sl += 2)
-                *reinterpret_cast<double2*>(pfield<L>(stage, 3 * W + jy * W + sl, l, grp)) =
-                    make_double2(sy[jy] * zp[sl], sy[jy] * zp[sl + 1]);
-    } else {
-#pragma unroll
-        for (int t = 0; t < W; t += 2)
-            *reinterpret_cast<double2*>(pfield<L>(stage, 3 * W + t, l, grp)) = make_double2(sy[t], sy[t + 1]);
-#pragma unroll
-        for (int t = 0; t < W; ++t) *pfield<L>(stage, 4 * W + ((t + R) & (W - 1)), l, grp) = sz[t];
-    }
-}
-
-// The contraction lane's b[kz] (physical z slots) of staged particle jj0.
-template <class L, int W>
-__device__ __forceinline__ void load_b(const double* stage, int jj0, int grp, int ly, double (&b)[W]) {
-    if constexpr (PICGPU_BSTAGE) {
-#pragma unroll
-        for (int sl = 0; sl < W; sl += 2) {
-            const double2 v = *reinterpret_cast<const double2*>(pfield<L>(stage, 3 * W + ly * W + sl, jj0, grp));
-            b[sl] = v.x;
-            b[sl + 1] = v.y;
-        }
-    } else {
-        const double yv = *pfield<L>(stage, 3 * W + ly, jj0, grp);
-#pragma unroll
-        for (int sl = 0; sl < W; sl += 2) {  // sz of physical slots sl, sl+1
-            const double2 zz = *reinterpret_cast<const double2*>(pfield<L>(stage, 4 * W + sl, jj0, grp));
-            b[sl] = yv * zz.x;
-            b[sl + 1] = yv * zz.y;
-        }
-    }
+    for (int t = 0; t < W; ++t) *pfield<L>(stage, 4 * W + ((t + R) & (W - 1)), l, grp) = sz[t];
 }
 
 // Shift one staged W-tap array (fields f0 .. f0+W-1, logical tap t stored at
@@ -233,32 +186,6 @@ __device__ __forceinline__ void restage_shifted(double* stage, int l, int grp, i
     for (int t = 0; t < W; ++t) *pfield<L>(stage, f0 + ((t + rot) & (W - 1)), l, grp) = v[t];
 }
 
-
-// A mover's y and z taps shifted by its cell step (shy, shz), zero-filling:
-// b[jy][kz] as a 2-D shift (BSTAGE), else the sy and rotated sz arrays.
-template <class L, int W>
-__device__ __forceinline__ void restage_yz(double* stage, int l, int grp, int shy, int shz, int R) {
-    if constexpr (PICGPU_BSTAGE) {
-        if (shy == 0 && shz == 0) return;
-        double v[W][W];  // logical [jy][t]
-#pragma unroll
-        for (int jy = 0; jy < W; ++jy)
-#pragma unroll
-            for (int t = 0; t < W; ++t) {
-                const int uy = jy - shy, ut = t - shz;
-                v[jy][t] = (uy >= 0 && uy < W && ut >= 0 && ut < W)
-                               ? *pfield<L>(stage, 3 * W + uy * W + ((ut + R) & (W - 1)), l, grp)
-                               : 0.0;
-            }
-#pragma unroll
-        for (int jy = 0; jy < W; ++jy)
-#pragma unroll
-            for (int t = 0; t < W; ++t) *pfield<L>(stage, 3 * W + jy * W + ((t + R) & (W - 1)), l, grp) = v[jy][t];
-    } else {
-        restage_shifted<L, W>(stage, l, grp, 3 * W, shy, 0);
-        restage_shifted<L, W>(stage, l, grp, 4 * W, shz, R);
-    }
-}
 
 // PM (fused step, PushCtx): 0 = deposit only; 1 = push + move detection + deposit of the
 // particles that stay in their cell (launch_deposit_current_push); 2 = the same
@@ -434,7 +361,8 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                             restage_shifted<L, W>(stage, lg, grp, 0, shx, 0);
                             restage_shifted<L, W>(stage, lg, grp, W, shx, 0);
                             restage_shifted<L, W>(stage, lg, grp, 2 * W, shx, 0);
-                            restage_yz<L, W>(stage, lg, grp, shy, shz, R);
+                            restage_shifted<L, W>(stage, lg, grp, 3 * W, shy, 0);
+                            restage_shifted<L, W>(stage, lg, grp, 4 * W, shz, R);
                         }
                     } else {
                         particle_window_sel<ORDER>(g, cur, qs, valid, dci, dcj, dck, a, sy, sz);
@@ -447,8 +375,14 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 #pragma unroll
                 for (int jj0 = 0; jj0 < CH; ++jj0) {
                     if (jj0 >= nn) break;
+                    const double yv = *pfield<L>(stage, 3 * W + ly, jj0, grp);
                     double b[W];
-                    load_b<L, W>(stage, jj0, grp, ly, b);
+#pragma unroll
+                    for (int sl = 0; sl < W; sl += 2) {  // sz of physical slots sl, sl+1
+                        const double2 zz = *reinterpret_cast<const double2*>(pfield<L>(stage, 4 * W + sl, jj0, grp));
+                        b[sl] = yv * zz.x;
+                        b[sl + 1] = yv * zz.y;
+                    }
 #pragma unroll
                     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -793,7 +727,8 @@ __global__ void __launch_bounds__((1 + WS_NPW) * JLayout<ORDER, CF>::NT, PICGPU_
                         restage_shifted<L, W>(stage, lg, grp, 0, shx, 0);
                         restage_shifted<L, W>(stage, lg, grp, W, shx, 0);
                         restage_shifted<L, W>(stage, lg, grp, 2 * W, shx, 0);
-                        restage_yz<L, W>(stage, lg, grp, shy, shz, R);
+                        restage_shifted<L, W>(stage, lg, grp, 3 * W, shy, 0);
+                        restage_shifted<L, W>(stage, lg, grp, 4 * W, shz, R);
                     }
                 }
             }
@@ -891,8 +826,15 @@ __global__ void __launch_bounds__((1 + WS_NPW) * JLayout<ORDER, CF>::NT, PICGPU_
 #pragma unroll
                     for (int jj0 = 0; jj0 < CH; ++jj0) {
                         if (jj0 >= nn) break;
+                        const double yv = *pfield<L>(stage, 3 * W + ly, jj0, grp);
                         double b[W];
-                        load_b<L, W>(stage, jj0, grp, ly, b);
+#pragma unroll
+                        for (int sl = 0; sl < W; sl += 2) {
+                            const double2 zz =
+                                *reinterpret_cast<const double2*>(pfield<L>(stage, 4 * W + sl, jj0, grp));
+                            b[sl] = yv * zz.x;
+                            b[sl + 1] = yv * zz.y;
+                        }
 #pragma unroll
                         for (int c = 0; c < 3; ++c)
 #pragma unroll
