@@ -533,6 +533,54 @@ __global__ void __launch_bounds__(PICGPU_PUSH_NT, PICGPU_PUSH_MINB) k_push(const
 // more than kHoleCap front holes fall back to a stable slide.
 constexpr int kHoleCap = 32;
 
+// Persistent, software-pipelined push (PICGPU_PUSH_PIPE, default): each thread
+// walks its slots s, s + stride, ... and the NEXT slot's record is loaded
+// before the current one is pushed, so every thread keeps a record in flight
+// through the CTA's reservation barrier and atomic (the record-pattern probe,
+// tools/hbm_probe.cu: read 48 + in-place x y z write streams at 4.9 TB/s with
+// 64 warps/SM, one record each; k_push holds a record only between its load
+// and its barrier).  One reservation per CTA iteration as in k_push.
+#ifndef PICGPU_PIPE_NT
+#define PICGPU_PIPE_NT 256
+#endif
+#ifndef PICGPU_PIPE_MINB
+#define PICGPU_PIPE_MINB 3  // 85 registers: two records + push state without spills
+#endif
+template <bool P2>
+__global__ void __launch_bounds__(PICGPU_PIPE_NT, PICGPU_PIPE_MINB) k_push_pipe(
+    const GridD g, const Aos A, uint64_t slots, double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
+    uint32_t mcap, const uint32_t* __restrict__ off, uint32_t* __restrict__ holes, uint32_t* __restrict__ hl,
+    StepCounters* ctr, double* __restrict__ L, uint32_t lcap, uint32_t* __restrict__ mslot, uint32_t* __restrict__ mbin,
+    unsigned long long* __restrict__ mvpart) {
+    __shared__ unsigned s_cnt, s_base, s_mv;
+    if (threadIdx.x == 0) s_cnt = s_mv = 0;
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t first = (uint64_t)blockIdx.x * blockDim.x;  // CTA-uniform loop bound
+    PushSlot cur, nxt;
+    push_load<true>(A, s, slots, cur);
+    unsigned nmv = 0;
+    for (uint64_t b = first; b < slots; b += stride, s += stride) {
+        push_load<true>(A, s + stride, slots, nxt);  // in flight while this slot is pushed
+        push_slot<true, P2, true>(g, A, s, dt, cap2, cur, off, holes, hl, ctr, L, lcap, &s_cnt);
+        nmv += cur.moved ? 1u : 0u;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned c = s_cnt;
+            s_base = c ? atomicAdd(&ctr->nmovers, c) : 0u;
+            s_cnt = 0;
+        }
+        __syncthreads();
+        push_store_mover<true>(A, s, cur, s_base, M, mcell, mcap, mslot, mbin);
+        cur = nxt;
+    }
+    const unsigned wm = __reduce_add_sync(0xffffffffu, nmv);
+    if ((threadIdx.x & 31) == 0 && wm) atomicAdd(&s_mv, wm);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_mv) atomicAdd(mvpart + (size_t)(blockIdx.x % kMovedParts) * 16, (unsigned long long)s_mv);
+}
+
 // ctr->moved += the spread partial counts of k_push; the partials are reset.
 __global__ void k_fold_moved(unsigned long long* __restrict__ mvpart, StepCounters* ctr) {
     unsigned long long v = 0;
@@ -1432,6 +1480,37 @@ void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     const int blocks = (int)((capacity + PICGPU_PUSH_NT * UNR - 1) / (PICGPU_PUSH_NT * UNR));
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
     hl.ensure(capacity * 4 + 4);
+    static const bool pipe = [] {
+        const char* e = std::getenv("PICGPU_PUSH_PIPE");
+        return !(e && e[0] == '0');
+    }();
+    if (push && pipe) {
+        static int ctas_per_sm[64] = {};
+        int dev = 0;
+        PICGPU_CUDA_TRY(cudaGetDevice(&dev));
+        if (!ctas_per_sm[dev & 63]) {
+            int nb = 0;
+            PICGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_push_pipe<true>, PICGPU_PIPE_NT, 0));
+            ctas_per_sm[dev & 63] = std::max(1, nb);
+        }
+        const uint64_t want = (uint64_t)num_sms * ctas_per_sm[dev & 63];
+        const uint64_t need = (capacity + PICGPU_PIPE_NT - 1) / PICGPU_PIPE_NT;
+        const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min(want, need));
+        auto* kp = p2 ? k_push_pipe<true> : k_push_pipe<false>;
+        kp<<<grid, PICGPU_PIPE_NT, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(),
+                                            (uint32_t)mcap, off.as<uint32_t>(), holes.as<uint32_t>(),
+                                            hl.as<uint32_t>(), ctr, lrec.as<double>(), (uint32_t)lcap,
+                                            mslot.as<uint32_t>(), mbin.as<uint32_t>(), moved_parts());
+        k_fold_moved<<<1, 256, 0, st>>>(moved_parts(), ctr);
+        note_launch(2);
+        PICGPU_CUDA_TRY(cudaGetLastError());
+        k_departures<<<num_sms * 8, 256, 0, st>>>(counters.as<StepCounters>(), (uint32_t)mcap, mslot.as<uint32_t>(),
+                                                  mbin.as<uint32_t>(), off.as<uint32_t>(), holes.as<uint32_t>(),
+                                                  hl.as<uint32_t>());
+        note_launch();
+        PICGPU_CUDA_TRY(cudaGetLastError());
+        return;
+    }
     auto* kern = push ? (p2 ? k_push<true, UNR, true> : k_push<true, UNR, false>)
                       : (p2 ? k_push<false, UNR, true> : k_push<false, UNR, false>);
     kern<<<blocks, PICGPU_PUSH_NT, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(),
