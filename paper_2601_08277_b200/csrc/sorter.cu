@@ -533,116 +533,6 @@ __global__ void __launch_bounds__(PICGPU_PUSH_NT, PICGPU_PUSH_MINB) k_push(const
 // more than kHoleCap front holes fall back to a stable slide.
 constexpr int kHoleCap = 32;
 
-// Persistent, software-pipelined, segmented push (whole-box stores, default).
-// k_push's iteration rate is bound by its reservation: every CTA waits one
-// global-atomic round trip per 512 slots at its second barrier (C3 ncu:
-// barrier stalls 52% of the samples; 1.35M reservations x ~2 us / 296 CTAs
-// in flight ~ 30 ms, while the record pattern itself streams at 4.9 TB/s,
-// tools/hbm_probe.cu).  Here the grid is persistent and CTA c owns segment c
-// of the mover arrays (segcap entries): a warp reserves its movers with ONE
-// shared-memory atomic on the CTA's running count -- no barrier and no global
-// atomic in the loop -- and the next slot's record is loaded before the
-// current one is pushed.  k_seg_prefix turns the segment counts into a prefix;
-// k_departures / k_insert read entry i of the list at seg_map(i).
-#ifndef PICGPU_PIPE_NT
-#define PICGPU_PIPE_NT 256
-#endif
-#ifndef PICGPU_PIPE_MINB
-#define PICGPU_PIPE_MINB 3  // 85 registers: two records + push state without spills
-#endif
-template <bool P2>
-__global__ void __launch_bounds__(PICGPU_PIPE_NT, PICGPU_PIPE_MINB) k_push_seg(
-    const GridD g, const Aos A, uint64_t slots, double dt, double cap2, const Soa M, uint32_t* __restrict__ mcell,
-    uint32_t segcap, uint32_t* __restrict__ segcnt, StepCounters* ctr, uint32_t* __restrict__ mslot,
-    uint32_t* __restrict__ mbin, unsigned long long* __restrict__ mvpart) {
-    __shared__ unsigned s_run, s_mv;
-    if (threadIdx.x == 0) s_run = s_mv = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t seg0 = (uint64_t)blockIdx.x * segcap;
-    PushSlot cur, nxt;
-    push_load<true>(A, s, slots, cur);
-    unsigned nmv = 0;
-    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < slots; b += stride, s += stride) {
-        push_load<true>(A, s + stride, slots, nxt);  // in flight while this slot is pushed
-        // no slab here: k_push's leaver path never runs (L, lcap unused)
-        push_slot<true, P2, false>(g, A, s, dt, cap2, cur, nullptr, nullptr, nullptr, ctr, nullptr, 0, nullptr);
-        const bool mv = cur.moved;
-        nmv += mv ? 1u : 0u;
-        const unsigned bal = __ballot_sync(0xffffffffu, mv);
-        if (bal) {
-            unsigned base = 0;
-            if (lane == __ffs(bal) - 1) base = atomicAdd(&s_run, (unsigned)__popc(bal));
-            base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
-            if (mv) {
-                const unsigned idx = base + (unsigned)__popc(bal & ((1u << lane) - 1u));
-                if (idx < segcap) {  // else dropped: k_seg_prefix counts it, the host re-sorts fully
-                    const uint64_t e = seg0 + idx;
-                    M.x[e] = cur.x;
-                    M.y[e] = cur.y;
-                    M.z[e] = cur.z;
-                    M.vx[e] = cur.vx;
-                    M.vy[e] = cur.vy;
-                    M.vz[e] = cur.vz;
-                    M.w[e] = cur.wid.x;
-                    M.id[e] = (uint64_t)__double_as_longlong(cur.wid.y);
-                    mcell[e] = cur.nc;
-                    store_gap_record(A.p + s);
-                    mslot[e] = (uint32_t)s;
-                    mbin[e] = cur.before;
-                }
-            }
-        }
-        cur = nxt;
-    }
-    const unsigned wm = __reduce_add_sync(0xffffffffu, nmv);
-    if (lane == 0 && wm) atomicAdd(&s_mv, wm);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        segcnt[blockIdx.x] = s_run;
-        if (s_mv) atomicAdd(mvpart + (size_t)(blockIdx.x % kMovedParts) * 16, (unsigned long long)s_mv);
-    }
-}
-
-// Segment counts -> exclusive prefix (nseg + 1 entries, one CTA); nmovers = the
-// recorded total; movers past a full segment count as dropped (full re-sort).
-__global__ void __launch_bounds__(1024) k_seg_prefix(const uint32_t* __restrict__ segcnt, uint32_t nseg, uint32_t segcap,
-                                                     uint32_t* __restrict__ prefix, StepCounters* ctr) {
-    __shared__ uint32_t carry_s, sw[32];
-    if (threadIdx.x == 0) carry_s = 0;
-    __syncthreads();
-    unsigned long long drop = 0;
-    for (uint32_t b0 = 0; b0 < nseg; b0 += blockDim.x) {
-        const uint32_t i = b0 + threadIdx.x;
-        const uint32_t c = i < nseg ? segcnt[i] : 0u;
-        const uint32_t v = min(c, segcap);
-        drop += c - v;
-        uint32_t x = v;
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) sw[w] = x;
-        __syncthreads();
-        uint32_t wc = 0;
-        for (int k = 0; k < w; ++k) wc += sw[k];
-        const uint32_t carry = carry_s;
-        if (i < nseg) prefix[i] = carry + wc + x - v;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry_s = carry + wc + x;
-        __syncthreads();
-    }
-    if (drop) atomicAdd(&ctr->mover_drop, (unsigned)drop);
-    if (threadIdx.x == 0) {
-        prefix[nseg] = carry_s;
-        ctr->nmovers = carry_s;
-    }
-}
-
 // ctr->moved += the spread partial counts of k_push; the partials are reset.
 __global__ void k_fold_moved(unsigned long long* __restrict__ mvpart, StepCounters* ctr) {
     unsigned long long v = 0;
@@ -755,28 +645,13 @@ __global__ void __launch_bounds__(256, PICGPU_COMPACT_MINB) k_fill_holes(const A
 
 // Departures of k_push's movers join their old bins' hole lists (delete_in_bin,
 // gpma.hpp:328-335); the slots already hold gap records.
-// Entry i of a segmented mover list (k_push_seg, MoverSegs in store.hpp).
-__device__ __forceinline__ uint32_t seg_map(const MoverSegs& ms, uint32_t i) {
-    if (!ms.prefix) return i;
-    uint32_t lo = 0, hi = ms.nseg - 1;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(ms.prefix + mid) <= i)
-            lo = mid;
-        else
-            hi = mid - 1;
-    }
-    return lo * ms.segcap + (i - __ldg(ms.prefix + lo));
-}
-
 __global__ void k_departures(const StepCounters* ctr, uint32_t mcap, const uint32_t* __restrict__ mslot,
                              const uint32_t* __restrict__ mbin, const uint32_t* __restrict__ off,
-                             uint32_t* __restrict__ holes, uint32_t* __restrict__ hl, const MoverSegs ms) {
+                             uint32_t* __restrict__ holes, uint32_t* __restrict__ hl) {
     const uint32_t nm = min(ctr->nmovers, mcap);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
-        const uint32_t e = seg_map(ms, i);
-        const uint32_t b = mbin[e];
-        hl[off[b] + atomicAdd(&holes[b], 1u)] = mslot[e];
+        const uint32_t b = mbin[i];
+        hl[off[b] + atomicAdd(&holes[b], 1u)] = mslot[i];
     }
 }
 
@@ -788,11 +663,9 @@ __global__ void k_departures(const StepCounters* ctr, uint32_t mcap, const uint3
 // the list empty and gives its unit back, so holes[d] ends at max(h0 - a, 0).
 __global__ void k_insert(const Soa M, const uint32_t* __restrict__ mcell, uint32_t mcap,
                          StepCounters* ctr, const Aos A, const uint32_t* __restrict__ off, uint32_t* cnt,
-                         uint32_t* __restrict__ ovf, uint32_t* __restrict__ holes, const uint32_t* __restrict__ hl,
-                         const MoverSegs ms) {
+                         uint32_t* __restrict__ ovf, uint32_t* __restrict__ holes, const uint32_t* __restrict__ hl) {
     const uint32_t nm = min(ctr->nmovers, mcap) + ctr->nimport;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nm; j += gridDim.x * blockDim.x) {
-        const uint32_t i = seg_map(ms, j);  // physical entry (ovf / k_borrow / k_place_left use it as is)
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
         const uint32_t d = mcell[i];
         if (d == kNoCell) continue;  // a leaver exported by the fused slab step
         const uint32_t lo = off[d];
@@ -1544,7 +1417,6 @@ void BinStore::ensure_movers_keep(size_t m, size_t keep) {
 
 void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     const size_t nc = g.ncells;
-    cur_segs = MoverSegs{};
     ensure_movers(std::max<size_t>(size_t(1) << 16, n / 4));
     if (g.slab) {
         const size_t want = std::max<size_t>(size_t(1) << 16, n / 4);
@@ -1560,41 +1432,6 @@ void BinStore::enqueue_detect(bool push, double dt, double cap2) {
     const int blocks = (int)((capacity + PICGPU_PUSH_NT * UNR - 1) / (PICGPU_PUSH_NT * UNR));
     const bool p2 = g.pow2x && g.pow2y && g.pow2z && g.gpow2Lx && g.pow2Ly && g.pow2Lz;
     hl.ensure(capacity * 4 + 4);
-    static const bool segmented = [] {
-        const char* e = std::getenv("PICGPU_PUSH_SEG");
-        return !(e && e[0] == '0');
-    }();
-    if (push && segmented && !g.slab) {
-        static int ctas_per_sm[64] = {};
-        int dev = 0;
-        PICGPU_CUDA_TRY(cudaGetDevice(&dev));
-        if (!ctas_per_sm[dev & 63]) {
-            int nb = 0;
-            PICGPU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_push_seg<true>, PICGPU_PIPE_NT, 0));
-            ctas_per_sm[dev & 63] = std::max(1, nb);
-        }
-        const uint64_t want = (uint64_t)num_sms * ctas_per_sm[dev & 63];
-        const uint64_t need = (capacity + PICGPU_PIPE_NT - 1) / PICGPU_PIPE_NT;
-        const uint32_t nseg = (uint32_t)std::max<uint64_t>(1, std::min(want, need));
-        const uint32_t segcap = (uint32_t)(mcap / nseg);
-        segbuf.ensure(((size_t)2 * nseg + 2) * 4);
-        uint32_t* segcnt = segbuf.as<uint32_t>();
-        uint32_t* prefix = segcnt + nseg + 1;
-        auto* kp = p2 ? k_push_seg<true> : k_push_seg<false>;
-        kp<<<nseg, PICGPU_PIPE_NT, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(), segcap,
-                                            segcnt, ctr, mslot.as<uint32_t>(), mbin.as<uint32_t>(), moved_parts());
-        k_fold_moved<<<1, 256, 0, st>>>(moved_parts(), ctr);
-        k_seg_prefix<<<1, 1024, 0, st>>>(segcnt, nseg, segcap, prefix, ctr);
-        note_launch(3);
-        PICGPU_CUDA_TRY(cudaGetLastError());
-        cur_segs = MoverSegs{prefix, nseg, segcap};
-        k_departures<<<num_sms * 8, 256, 0, st>>>(counters.as<StepCounters>(), (uint32_t)mcap, mslot.as<uint32_t>(),
-                                                  mbin.as<uint32_t>(), off.as<uint32_t>(), holes.as<uint32_t>(),
-                                                  hl.as<uint32_t>(), cur_segs);
-        note_launch();
-        PICGPU_CUDA_TRY(cudaGetLastError());
-        return;
-    }
     auto* kern = push ? (p2 ? k_push<true, UNR, true> : k_push<true, UNR, false>)
                       : (p2 ? k_push<false, UNR, true> : k_push<false, UNR, false>);
     kern<<<blocks, PICGPU_PUSH_NT, 0, st>>>(g, A.aos(), capacity, dt, cap2, M.soa(), mcell.as<uint32_t>(),
@@ -1608,7 +1445,7 @@ void BinStore::enqueue_detect(bool push, double dt, double cap2) {
         // the departures' hole-list entries (before any arrival looks for holes)
         k_departures<<<num_sms * 8, 256, 0, st>>>(counters.as<StepCounters>(), (uint32_t)mcap, mslot.as<uint32_t>(),
                                                   mbin.as<uint32_t>(), off.as<uint32_t>(), holes.as<uint32_t>(),
-                                                  hl.as<uint32_t>(), MoverSegs{});
+                                                  hl.as<uint32_t>());
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
     }
@@ -1641,7 +1478,7 @@ void BinStore::enqueue_migrate() {
         }();
         k_insert<<<num_sms * mult, 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), (uint32_t)mcap, ctr, A.aos(),
                                               off.as<uint32_t>(), cnt.as<uint32_t>(), ovf.as<uint32_t>(),
-                                              holes.as<uint32_t>(), hl.as<uint32_t>(), cur_segs);
+                                              holes.as<uint32_t>(), hl.as<uint32_t>());
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
         // borrow_insert for the full-bin arrivals; no work when there are none
@@ -1666,7 +1503,6 @@ void BinStore::enqueue_incremental(bool push, double dt, double cap2) {
 
 void BinStore::enqueue_fused(int order, double q, double* J, double dt, double cap2, cudaEvent_t after_kernel,
                              bool migrate, int kernel) {
-    cur_segs = MoverSegs{};  // k_movers writes a compact list
     ensure_movers(std::max<size_t>(size_t(1) << 16, n / 4));
     if (g.slab) {
         const size_t want = std::max<size_t>(size_t(1) << 16, n / 4);

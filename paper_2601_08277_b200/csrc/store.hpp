@@ -50,15 +50,7 @@ struct AosBuf {
 };
 
 constexpr int kBorrowScanBins = 4;
-constexpr int kMovedParts = 256;  // k_push's moved-count partials (one 128-byte line each)
-
-// A mover list written in per-CTA segments (k_push_seg): entry i lives at
-// segment s = the last prefix[s] <= i, slot s * segcap + (i - prefix[s]).
-// prefix == nullptr: a compact list.
-struct MoverSegs {
-    const uint32_t* prefix = nullptr;
-    uint32_t nseg = 0, segcap = 0;
-};  // GpmaConfig::borrow_scan_bins (gpma.hpp:25)
+constexpr int kMovedParts = 256;  // k_push's moved-count partials (one 128-byte line each)  // GpmaConfig::borrow_scan_bins (gpma.hpp:25)
 
 struct BinStore {
     GridD g{};
@@ -84,8 +76,6 @@ struct BinStore {
                               // are the slots hl[off[c] .. off[c]+holes[c]) (u32)
     DevBuf counters;          // StepCounters
     DevBuf mvpart;            // k_push's spread moved counts (kMovedParts x 128 bytes, kept zero between steps)
-    DevBuf segbuf;            // k_push_seg: per-CTA mover counts, then their prefix
-    MoverSegs cur_segs{};     // layout of the current mover list (segmented after k_push_seg)
     StepCounters* hcounters = nullptr;  // pinned mirror
 
     uint64_t n = 0;           // particles

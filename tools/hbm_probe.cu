@@ -42,19 +42,22 @@ __global__ void __launch_bounds__(256) k(Rec* A, Rec* B, uint64_t n, double dt, 
     }
 }
 
+static size_t g_smem = 0;  // dynamic shared memory per CTA: limits CTAs (warps) per SM
+
 template <int MODE, int UNR>
 void run(const char* name, Rec* A, Rec* B, uint64_t n, double bytes_per, int* sink) {
     const unsigned blocks = (unsigned)((n + 256ull * UNR - 1) / (256ull * UNR));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
-    k<MODE, UNR><<<blocks, 256>>>(A, B, n, 0.0, sink);
+    cudaFuncSetAttribute(k<MODE, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+    k<MODE, UNR><<<blocks, 256, g_smem>>>(A, B, n, 0.0, sink);
     cudaEventRecord(e0);
-    for (int r = 0; r < 3; ++r) k<MODE, UNR><<<blocks, 256>>>(A, B, n, 0.0, sink);
+    for (int r = 0; r < 3; ++r) k<MODE, UNR><<<blocks, 256, g_smem>>>(A, B, n, 0.0, sink);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
     ms /= 3;
-    printf("%-28s UNR %d  %8.3f ms  %7.1f GB/s\n", name, UNR, ms, n * bytes_per / (ms * 1e-3) / 1e9);
+    printf("%-28s UNR %d smem %6zu  %8.3f ms  %7.1f GB/s\n", name, UNR, g_smem, ms, n * bytes_per / (ms * 1e-3) / 1e9);
 }
 
 int main(int argc, char** argv) {
@@ -63,6 +66,12 @@ int main(int argc, char** argv) {
     if (cudaMalloc(&A, n * 64) || cudaMalloc(&B, n * 64) || cudaMalloc(&sink, 4)) { printf("alloc failed\n"); return 1; }
     cudaMemset(A, 0, n * 64); cudaMemset(B, 0, n * 64);
     printf("records %llu (%.1f GB each array)\n", (unsigned long long)n, n * 64 / 1e9);
+    for (size_t sm : {(size_t)0, (size_t)50000, (size_t)70000, (size_t)100000}) {  // 8 / 4 / 3 / 2 CTAs of 256 per SM
+        g_smem = sm;
+        run<1, 1>("read 48 + write xyz in place", A, B, n, 48 + 24, sink);
+        run<1, 2>("read 48 + write xyz in place", A, B, n, 48 + 24, sink);
+    }
+    g_smem = 0;
     run<0, 1>("read 64", A, B, n, 64, sink);
     run<0, 2>("read 64", A, B, n, 64, sink);
     run<1, 1>("read 48 + write xyz in place", A, B, n, 48 + 24, sink);
