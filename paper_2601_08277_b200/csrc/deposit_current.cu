@@ -506,425 +506,6 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
 }
 
 // ---------------------------------------------------------------------------
-// Warp-specialised form of the lane kernel ("ws", PICGPU_J_WS=1; measured,
-// not the default -- see use_ws()).  Same tile, lane layout, z window, patch
-// and gather as v3, but every warp has ONE role:
-//  * PRODUCER warp w (threads NT.. 2NT-1) runs, for consumer warp w's pencils,
-//    the record loads (one chunk ahead in registers), the fused bit-exact push
-//    + move detection (mover-list reservations included) and the window
-//    prologue, and stages each chunk's windows into slot s of a ring of WS_NS
-//    chunk slots; a per-slot header carries the chunk's particle count and an
-//    end-of-cell flag.
-//  * CONSUMER warp w keeps the 48 accumulators, contracts every staged chunk,
-//    emits the finished plane, and the consumer warps gather the CTA's patch
-//    behind a named barrier (producers never wait on it).
-// Each producer/consumer pair is coupled only through its slots' mbarriers
-// (full: 32 producer arrivals, empty: 32 consumer arrivals), so a producer
-// runs up to WS_NS chunks ahead: the push and prologue latency (record loads,
-// the dependent FP64 chains of locate/weights) overlaps the contraction of
-// earlier chunks instead of stalling it, and each role holds only its own
-// registers (v3: 168 per thread, 12 warps/SM; here 2 x 8 warps at <= 128).
-// NPW producer warps per consumer warp: 1 (2 CTAs/SM, setmaxnreg split) or 2
-// (one CTA of 12 warps per SM; producer p fills the pair's chunks c = p mod 2).
-// C2 fused: NPW 1 1.68 ms, NPW 2 1.82 ms (v3 1.61): with two producers the
-// lone consumer warp per scheduler cannot keep the FP64 pipe busy and the
-// producers' ring waits grow to 26% of the issued instructions
-// (profiles/r02/ncu_fused_ws2.txt).
-#ifndef PICGPU_WS_NPW
-#define PICGPU_WS_NPW 1
-#endif
-constexpr int WS_NPW = PICGPU_WS_NPW;
-#ifndef PICGPU_WS_NS
-#define PICGPU_WS_NS (WS_NPW == 1 ? 3 : 4)
-#endif
-#ifndef PICGPU_WS_MINB
-#define PICGPU_WS_MINB (WS_NPW == 1 ? 2 : 1)
-#endif
-constexpr int WS_NS = PICGPU_WS_NS;
-static_assert(WS_NS % WS_NPW == 0, "ws: ring slots per producer parity");
-// register split (setmaxnreg, per warpgroup: consumers are warps 0-3, producers
-// 4-7): 4 x 32 x (C + P) = the CTA's 256 x 128 at 2 CTAs/SM
-#ifndef PICGPU_WS_REG_C
-#define PICGPU_WS_REG_C 160
-#endif
-#ifndef PICGPU_WS_REG_P
-#define PICGPU_WS_REG_P 96
-#endif
-constexpr int WS_REG_C = PICGPU_WS_REG_C, WS_REG_P = PICGPU_WS_REG_P;
-
-template <int ORDER, class CF>
-struct WsLayout {
-    using L = JLayout<ORDER, CF>;
-    static constexpr int NT = L::NT;           // consumer threads (= threads per producer group)
-    static constexpr int NW = NT / 32;         // consumer warps (each fed by WS_NPW producer warps)
-    static constexpr int SLOT = L::STAGE3;     // doubles per chunk slot (all pencils)
-    static constexpr size_t BAR_OFF = (size_t)(2 * L::PATCH + WS_NS * SLOT) * sizeof(double);
-    static constexpr size_t SMEM = BAR_OFF + (size_t)WS_NS * NW * 2 * sizeof(uint64_t) +
-                                   (size_t)WS_NS * NW * sizeof(uint32_t);
-};
-
-// consumer-only named barrier (id 1) with an OR reduction
-__device__ __forceinline__ bool consumer_bar_or(bool v, int nthreads) {
-    unsigned r;
-    asm volatile(
-        "{\n"
-        ".reg .pred p, q;\n"
-        "setp.ne.u32 p, %1, 0;\n"
-        "bar.red.or.pred q, 1, %2, p;\n"
-        "selp.u32 %0, 1, 0, q;\n"
-        "}\n"
-        : "=r"(r)
-        : "r"((unsigned)v), "r"(nthreads)
-        : "memory");
-    return r != 0;
-}
-
-constexpr uint32_t kWsLast = 1u << 8;  // header flag: last chunk of the cell step
-
-// A pair's chunk sequence: cell steps k0..k1-1, ceil(m/CH) chunks each (m =
-// the warp's largest count in the step; an empty step is one empty chunk).
-// k / ci / m / nch are warp-uniform; c_off / n_c are this lane's pencil's bin.
-struct ChunkCursor {
-    int k, k1, ci, m, nch, n_c;
-    uint32_t c_off;
-    __device__ __forceinline__ void load(const uint32_t* off, const uint32_t* cnt, uint32_t col, uint32_t plane,
-                                         bool pv, int CH) {
-        c_off = 0;
-        n_c = 0;
-        if (pv && k < k1) {
-            c_off = off[col + plane * (uint32_t)k];
-            n_c = (int)cnt[col + plane * (uint32_t)k];
-        }
-        m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
-        nch = m == 0 ? 1 : (m + CH - 1) / CH;
-    }
-    __device__ __forceinline__ void next(const uint32_t* off, const uint32_t* cnt, uint32_t col, uint32_t plane,
-                                         bool pv, int CH) {
-        if (++ci >= nch) {
-            ++k;
-            ci = 0;
-            if (k < k1) load(off, cnt, col, plane, pv, CH);
-        }
-    }
-};
-
-template <int ORDER, class CF = JCfg<ORDER>, int PM = 0, bool SLAB = false>
-__global__ void __launch_bounds__((1 + WS_NPW) * JLayout<ORDER, CF>::NT, PICGPU_WS_MINB)
-    deposit_current_kernel_ws(const GridD g, const CAos p, const uint32_t* __restrict__ off,
-                              const uint32_t* __restrict__ cnt, const double q, double* __restrict__ jx,
-                              double* __restrict__ jy, double* __restrict__ jz, const int zlen,
-                              const PushCtx pc) {
-    using C = CF;
-    using L = JLayout<ORDER, CF>;
-    using WL = WsLayout<ORDER, CF>;
-    constexpr int W = L::W, OFF = Shape<ORDER>::OFF;
-    constexpr int G = C::G, PX = C::PX, PY = C::PY, CH = C::CH;
-    constexpr int NT = L::NT, NW = WL::NW;
-    constexpr int FX = PX + W - 1, FY = PY + W - 1;
-    constexpr int NODES = 3 * FX * FY;
-    constexpr int NIT = (NODES + NT - 1) / NT;
-    constexpr int XS = G / W, IX = W / XS;
-    static_assert(G == W * XS && W % XS == 0 && (W & (W - 1)) == 0, "ws: lanes = jy x x-halves");
-    static_assert(L::PPB == 1, "ws: one plane per barrier");
-    const double qs = q * (ORDER == 3 ? 1.0 / 216.0 : ORDER == 2 ? 0.125 : 1.0);
-
-    extern __shared__ __align__(16) double smem[];
-    double* patch = smem;                  // [2][W(jy)][W(ix)][3][PSTRIDE]
-    double* ring = smem + 2 * L::PATCH;    // [WS_NS][SLOT]: paired fields (JLayout PSS/PFS)
-    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + WL::BAR_OFF);  // [NS][NW]
-    uint64_t* empty = full + WS_NS * NW;                                                       // [NS][NW]
-    uint32_t* hdr = reinterpret_cast<uint32_t*>(empty + WS_NS * NW);                          // [NS][NW]
-
-    const bool producer = threadIdx.x >= NT;
-    const int tid = producer ? (threadIdx.x - NT) % NT : threadIdx.x;
-    [[maybe_unused]] const int pidx = producer ? (threadIdx.x - NT) / NT : 0;  // producer parity
-    const int warp = tid >> 5, lane = tid & 31;
-    const int grp = tid / G, lg = tid % G;
-    const int ly = lg % W, xh = lg / W;
-    const int px = grp % PX, py = grp / PX;
-    // tiles cover x-cells [xb, xe): a slab's owned cells (its ghost cells hold no particles)
-    const int xb = g.slab ? g.sx_lo : 0, xe = g.slab ? g.sx_hi : g.nx;
-    const int i0 = xb + blockIdx.x * PX, j0 = blockIdx.y * PY;
-    const int k0 = blockIdx.z * zlen;
-    const int k1 = min(k0 + zlen, g.nz);
-    const int i = i0 + px, j = j0 + py;
-    const bool pv = (i < xe) && (j < g.ny);
-    const uint32_t col = (uint32_t)i + (uint32_t)g.nx * (uint32_t)j;
-    const uint32_t plane_cells = (uint32_t)g.nx * (uint32_t)g.ny;
-    [[maybe_unused]] const uint32_t seg = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    __shared__ unsigned s_movers;
-
-    // an entirely empty tile (vacuum) writes nothing: J was zeroed by the caller
-    {
-        bool any = false;
-        if (pv)
-            for (int kk = k0 + lg + (producer ? G * (1 + pidx) : 0); kk < k1; kk += (1 + WS_NPW) * G)
-                any |= cnt[col + plane_cells * kk] != 0;
-        if (!__syncthreads_or(any)) {
-            if (PM != 0 && threadIdx.x == 0) pc.seg_cnt[seg] = 0;
-            return;
-        }
-    }
-    if (threadIdx.x == 0) {
-        s_movers = 0;
-        for (int b = 0; b < WS_NS * NW; ++b) {
-            mbar_init(full + b, 32);
-            mbar_init(empty + b, 32);
-        }
-        mbar_fence_init();
-    }
-    __syncthreads();
-
-    if (producer) {
-        // ------------------------------------------------------------ producer
-        if constexpr (WS_NPW == 1 && WS_REG_P > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WS_REG_P));
-        const double dci = (double)(i + g.sx_shift), dcj = (double)j;
-        // this producer's chunks: c = pidx, pidx + NPW, ...; `la` runs one of
-        // its chunks ahead for the record prefetch
-        ChunkCursor cur{k0, k1, 0, 0, 0, 0, 0u};
-        cur.load(off, cnt, col, plane_cells, pv, CH);
-        for (int t = 0; t < pidx; ++t) cur.next(off, cnt, col, plane_cells, pv, CH);
-        ChunkCursor la = cur;
-        for (int t = 0; t < WS_NPW && la.k < k1; ++t) la.next(off, cnt, col, plane_cells, pv, CH);
-        PData nxt{};
-        if (cur.k < k1 && cur.ci * CH + lg < cur.n_c) load_particle<PM != 0>(p, cur.c_off + cur.ci * CH + lg, nxt);
-        uint32_t c = (uint32_t)pidx;  // chunk index in the pair's sequence
-        while (cur.k < k1) {
-            const int k = cur.k, base = cur.ci * CH, m = cur.m;
-            const uint32_t c_off = cur.c_off;
-            const int n_c = cur.n_c;
-            const int R = (k - k0) & (W - 1);
-            const int s = (int)(c % WS_NS);
-            const unsigned ph = (c / WS_NS) & 1u;
-            double* stage = ring + s * WL::SLOT;
-            [[maybe_unused]] bool mv = false;
-            [[maybe_unused]] uint32_t mv_cell = 0;
-            [[maybe_unused]] unsigned mv_bal = 0, mv_b0 = 0;
-            PData curp = nxt;
-            bool valid = base + lg < n_c && !is_gap(curp.x);
-            if (la.k < k1 && la.ci * CH + lg < la.n_c) load_particle<PM != 0>(p, la.c_off + la.ci * CH + lg, nxt);
-            const double dck = (double)k;
-            double a[3][W], sy[W], sz[W];
-            [[maybe_unused]] int shx = 0, shy = 0, shz = 0;
-            if constexpr (PM != 0) {
-                double fx = 0.0, fy = 0.0, fz = 0.0;
-                if (valid)
-                    valid = push_fused<PM == 2, SLAB>(g, pc, curp, c_off + (uint32_t)(base + lg),
-                                                      col + plane_cells * (uint32_t)k, i, j, k, dci, dcj, dck, fx, fy,
-                                                      fz, mv, mv_cell, shx, shy, shz);
-                mv_bal = __ballot_sync(0xffffffffu, mv);
-                if (mv_bal && lane == __ffs(mv_bal) - 1) mv_b0 = atomicAdd(&s_movers, (unsigned)__popc(mv_bal));
-                window_from_fractions<ORDER>(curp, qs, valid, fx, fy, fz, a, sy, sz);
-            } else {
-                particle_window_sel<ORDER>(g, curp, qs, valid, dci, dcj, dck, a, sy, sz);
-            }
-            // the slot is free once the consumer has read its previous chunk
-            mbar_wait(empty + s * NW + warp, ph ^ 1u);
-            if (m > 0) {
-                stage_record<L, W>(stage, lg, grp, R, a, sy, sz);
-                if constexpr (PM != 0) {
-                    if (mv && valid) {
-                        restage_shifted<L, W>(stage, lg, grp, 0, shx, 0);
-                        restage_shifted<L, W>(stage, lg, grp, W, shx, 0);
-                        restage_shifted<L, W>(stage, lg, grp, 2 * W, shx, 0);
-                        restage_shifted<L, W>(stage, lg, grp, 3 * W, shy, 0);
-                        restage_shifted<L, W>(stage, lg, grp, 4 * W, shz, R);
-                    }
-                }
-            }
-            if (lane == 0)
-                hdr[s * NW + warp] = (uint32_t)(m > 0 ? min(CH, m - base) : 0) | (cur.ci == cur.nch - 1 ? kWsLast : 0u);
-            mbar_arrive(full + s * NW + warp);
-            if constexpr (PM != 0) {
-                if (mv_bal) {
-                    const unsigned b0 = __shfl_sync(0xffffffffu, mv_b0, __ffs(mv_bal) - 1);
-                    if (mv) {
-                        const unsigned idx = b0 + (unsigned)__popc(mv_bal & ((1u << lane) - 1u));
-                        size_t e = (size_t)seg * pc.segcap + idx;
-                        if (idx >= pc.segcap) {  // segment full
-                            if constexpr (SLAB) {
-                                if (mv_cell >= kLeaveRight) {
-                                    export_leaver_now(pc, c_off + (uint32_t)(base + lg),
-                                                      col + plane_cells * (uint32_t)k, mv_cell);
-                                    e = ~(size_t)1;
-                                }
-                            }
-                            if (e != ~(size_t)1) {
-                                const unsigned o = atomicAdd(&pc.ctr->ovf_movers, 1u);
-                                e = o < pc.ovcap ? (size_t)pc.nseg * pc.segcap + o : ~(size_t)0;
-                            }
-                        }
-                        if (e < ~(size_t)1) {
-                            pc.mslot[e] = c_off + (uint32_t)(base + lg);
-                            pc.mbin[e] = col + plane_cells * (uint32_t)k;
-                            pc.mcellseg[e] = mv_cell;
-                        }
-                    }
-                }
-            }
-            for (int t = 0; t < WS_NPW && cur.k < k1; ++t) cur.next(off, cnt, col, plane_cells, pv, CH);
-            for (int t = 0; t < WS_NPW && la.k < k1; ++t) la.next(off, cnt, col, plane_cells, pv, CH);
-            c += WS_NPW;
-        }
-    } else {
-        // ------------------------------------------------------------ consumer
-        if constexpr (WS_NPW == 1 && WS_REG_C > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WS_REG_C));
-        const int pxv = min(PX, xe - i0), pyv = min(PY, g.ny - j0);
-        const bool alias_xy = (pxv + W - 1 > g.nx) || (pyv + W - 1 > g.ny);
-        int gn_base[NIT], gn_node[NIT];
-        unsigned gn_mask[NIT];
-        bool gn_inner[NIT];
-#pragma unroll
-        for (int t = 0; t < NIT; ++t) {
-            const int it = tid + t * NT;
-            gn_mask[t] = 0u;
-            gn_base[t] = 0;
-            gn_node[t] = 0;
-            gn_inner[t] = false;
-            if (it < NODES) {
-                const int c = it / (FX * FY);
-                const int r = it - c * (FX * FY);
-                const int uy = r / FX, ux = r - uy * FX;
-                if (ux < pxv + W - 1 && uy < pyv + W - 1) {
-#pragma unroll
-                    for (int dy = 0; dy < W; ++dy)
-#pragma unroll
-                        for (int dx = 0; dx < W; ++dx) {
-                            const int qy = uy - dy, qx = ux - dx;
-                            if (qy >= 0 && qy < pyv && qx >= 0 && qx < pxv) gn_mask[t] |= 1u << (dy * W + dx);
-                        }
-                    gn_base[t] = (c << 28) | (c * L::PSTRIDE + uy * PX + ux);
-                    const int X = wrap_index(i0 + OFF + ux, g.nx);
-                    const int Y = wrap_index(j0 + OFF + uy, g.ny);
-                    gn_node[t] = X + g.nx * Y;
-                    gn_inner[t] = !alias_xy && ux >= W - 1 && ux <= pxv - 1 && uy >= W - 1 && uy <= pyv - 1;
-                }
-            }
-        }
-        double acc[W][IX][3];
-#pragma unroll
-        for (int sl = 0; sl < W; ++sl)
-#pragma unroll
-            for (int ix = 0; ix < IX; ++ix)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) acc[sl][ix][c] = 0.0;
-        int s = 0;
-        unsigned ph = 0;
-        int phase = 0;
-        int last_busy = k0 - W;
-        const int kend = k1 + W - 1;
-        for (int k = k0; k < kend; ++k) {
-            const int R = (k - k0) & (W - 1);
-            bool busy = false;
-            if (k < k1) {
-                for (;;) {
-                    mbar_wait(full + s * NW + warp, ph);
-                    const uint32_t h = hdr[s * NW + warp];
-                    const int nn = (int)(h & 0xffu);
-                    const double* stage = ring + s * WL::SLOT;
-                    busy |= nn > 0;
-#pragma unroll
-                    for (int jj0 = 0; jj0 < CH; ++jj0) {
-                        if (jj0 >= nn) break;
-                        const double yv = *pfield<L>(stage, 3 * W + ly, jj0, grp);
-                        double b[W];
-#pragma unroll
-                        for (int sl = 0; sl < W; sl += 2) {
-                            const double2 zz =
-                                *reinterpret_cast<const double2*>(pfield<L>(stage, 4 * W + sl, jj0, grp));
-                            b[sl] = yv * zz.x;
-                            b[sl + 1] = yv * zz.y;
-                        }
-#pragma unroll
-                        for (int c = 0; c < 3; ++c)
-#pragma unroll
-                            for (int ix = 0; ix < IX; ix += 2) {
-                                const double2 av = *reinterpret_cast<const double2*>(
-                                    pfield<L>(stage, c * W + xh * IX + ix, jj0, grp));
-#pragma unroll
-                                for (int sl = 0; sl < W; ++sl) {
-                                    acc[sl][ix][c] = fma(av.x, b[sl], acc[sl][ix][c]);
-                                    acc[sl][ix + 1][c] = fma(av.y, b[sl], acc[sl][ix + 1][c]);
-                                }
-                            }
-                    }
-                    mbar_arrive(empty + s * NW + warp);
-                    if (++s == WS_NS) {
-                        s = 0;
-                        ph ^= 1u;
-                    }
-                    if (h & kWsLast) break;
-                }
-            }
-            {
-                double* pp = patch + phase * L::PATCH + grp;
-                auto emit = [&](auto Sc) {
-                    constexpr int S = decltype(Sc)::value;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-#pragma unroll
-                        for (int ix = 0; ix < IX; ++ix) {
-                            pp[((ly * W + xh * IX + ix) * 3 + c) * L::PSTRIDE] = acc[S][ix][c];
-                            acc[S][ix][c] = 0.0;
-                        }
-                };
-                if constexpr (W == 2) {
-                    if (R == 0)
-                        emit(std::integral_constant<int, 0>{});
-                    else
-                        emit(std::integral_constant<int, 1>{});
-                } else {
-                    switch (R) {
-                        case 0: emit(std::integral_constant<int, 0>{}); break;
-                        case 1: emit(std::integral_constant<int, 1>{}); break;
-                        case 2: emit(std::integral_constant<int, 2>{}); break;
-                        default: emit(std::integral_constant<int, 3>{}); break;
-                    }
-                }
-            }
-            if (consumer_bar_or(busy, NT)) last_busy = k;
-            if (last_busy >= k - (W - 1)) {
-                const double* pb = patch + phase * L::PATCH;
-                const int Z = wrap_index(k + OFF, g.nz);
-                const bool zc = (k >= k0 + W - 1) && (k < k1);
-                const size_t zrow = (size_t)plane_cells * (size_t)Z;
-#pragma unroll
-                for (int t = 0; t < NIT; ++t) {
-                    const unsigned msk = gn_mask[t];
-                    if (!msk) continue;
-                    const int c = gn_base[t] >> 28;
-                    const double* src = pb + (gn_base[t] & 0x0fffffff);
-                    double v[W * W];
-#pragma unroll
-                    for (int dy = 0; dy < W; ++dy)
-#pragma unroll
-                        for (int dx = 0; dx < W; ++dx)
-                            v[dy * W + dx] = (msk & (1u << (dy * W + dx)))
-                                                 ? src[(dy * W + dx) * 3 * L::PSTRIDE - dy * PX - dx]
-                                                 : 0.0;
-#pragma unroll
-                    for (int h = W * W / 2; h >= 1; h /= 2)
-#pragma unroll
-                        for (int e = 0; e < h; ++e) v[e] += v[e + h];
-                    const double sum = v[0];
-                    double* f = c == 0 ? jx : (c == 1 ? jy : jz);
-                    const size_t node = (size_t)gn_node[t] + zrow;
-                    if (zc && gn_inner[t])
-                        f[node] = sum;
-                    else if (sum != 0.0)
-                        atomicAdd(f + node, sum);
-                }
-            }
-            phase ^= 1;
-        }
-    }
-    if constexpr (PM != 0) {  // this CTA's mover count (every reservation precedes this barrier)
-        __syncthreads();
-        if (threadIdx.x == 0) pc.seg_cnt[seg] = s_movers;
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Orders 2 and 3 (4-tap window): ONE WARP PER PENCIL.
 //
 // The warp streams its pencil's particles (cells k0..k1-1 concatenated) in
@@ -1245,57 +826,15 @@ void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uin
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
 
-// Grid of the warp-specialised kernel: the v3 tiling, 2 x NT threads per CTA.
-template <int ORDER, class C, int PM = 0, bool SLAB = false>
-void launch_kernel_ws(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
-                      int num_sms, cudaStream_t st, PushCtx pc = PushCtx{}, PushCtx* used = nullptr) {
-    using L = JLayout<ORDER, C>;
-    using WL = WsLayout<ORDER, C>;
-    constexpr int W = L::W;
-    static int configured_dev = -1;
-    int dev = 0;
-    PICGPU_CUDA_TRY(cudaGetDevice(&dev));
-    if (configured_dev != dev) {  // per device (one process may drive several GPUs)
-        PICGPU_CUDA_TRY(cudaFuncSetAttribute(deposit_current_kernel_ws<ORDER, C, PM, SLAB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WL::SMEM));
-        configured_dev = dev;
-    }
-    const int tx = div_up(g.slab ? g.sx_hi - g.sx_lo : g.nx, C::PX), ty = div_up(g.ny, C::PY);
-    const long long tiles = (long long)tx * ty;
-    const long long target = (long long)num_sms * PICGPU_WS_MINB * 4;
-    int zch = (int)std::max<long long>(1, (target + tiles - 1) / tiles);
-    zch = std::min(zch, std::max(1, g.nz / (4 * W)));
-    const int zlen = div_up(g.nz, zch);
-    zch = div_up(g.nz, zlen);
-    dim3 grid(tx, ty, zch);
-    if constexpr (PM != 0) set_segments(pc, grid, used);
-    deposit_current_kernel_ws<ORDER, C, PM, SLAB><<<grid, (1 + WS_NPW) * L::NT, WL::SMEM, st>>>(
-        g, p, off, cnt, q, j, j + g.ncells, j + 2 * (size_t)g.ncells, zlen, pc);
-    note_launch();
-    PICGPU_CUDA_TRY(cudaGetLastError());
-}
-
-// The lane family's kernel form: the single-role v3 (default) or the
-// warp-specialised one (PICGPU_J_WS=1).  C2 QSP (B200): fused 1.63 (ws) vs
-// 1.61 ms (v3), J only 1.31 vs 1.18, CIC fused 1.54 vs 1.41 -- the producer
-// warps (push + prologue, a dependent FP64 chain per particle) cannot feed
-// the consumers: 11.6% of the issued instructions are consumer mbarrier
-// back-off, both pipes stay near 50% (profiles/r02/ncu_fused_ws.txt).
-static bool use_ws() {
-    static const bool v = [] {
-        const char* e = std::getenv("PICGPU_J_WS");
-        return e && e[0] == '1';
-    }();
-    return v;
-}
-
+// The lane family's kernel.  (A warp-specialised form -- producer warps for the
+// push + prologue feeding consumer warps through an mbarrier ring, setmaxnreg
+// split -- was measured and removed: C2 QSP fused 1.63 vs 1.61 ms, J only 1.31
+// vs 1.18; the producers' dependent FP64 chains cannot feed the consumers,
+// profiles/r02/ncu_fused_ws.txt, ncu_fused_ws2.txt.)
 template <int ORDER, class C, int PM = 0, bool SLAB = false>
 void launch_lane(const GridD& g, const CAos& p, const uint32_t* off, const uint32_t* cnt, double q, double* j,
                  int num_sms, cudaStream_t st, PushCtx pc = PushCtx{}, PushCtx* used = nullptr) {
-    if (use_ws())
-        launch_kernel_ws<ORDER, C, PM, SLAB>(g, p, off, cnt, q, j, num_sms, st, pc, used);
-    else
-        launch_kernel<ORDER, C, PM, SLAB>(g, p, off, cnt, q, j, num_sms, st, pc, used);
+    launch_kernel<ORDER, C, PM, SLAB>(g, p, off, cnt, q, j, num_sms, st, pc, used);
 }
 
 template <int ORDER>
@@ -1356,23 +895,56 @@ void launch_push_order(const GridD& g, PushCtx& pc, const uint32_t* off, const u
     }
 }
 
-// Movers of the fused step, W threads per mover (one z-plane of its window
-// each): thread 0 copies the particle from its slot into the mover record and
-// turns the slot into a hole of its old bin (delete_in_bin, gpma.hpp:328-335).
-// The fused kernel deposited the mover's taps that fall inside its old cell's
-// window (a mover steps at most one cell per axis); each thread reduces the
-// rest of its plane -- the nodes outside that window -- into J (RED.ADD.F64):
-// 16 of 64 nodes for a one-axis QSP mover.
-template <int ORDER>
+// Node index on a periodic axis for i within a window of [0, n): the common
+// case without the integer modulo.
+__device__ __forceinline__ int wrap_near(int i, int n) {
+    return (unsigned)i < (unsigned)n ? i : wrap_index(i, n);
+}
+
+// One mover's deposit descriptor (shared memory): its scaled window weights,
+// charge x velocity, wrapped node indices per axis and packed cell steps.
+template <int W>
+struct MoverDesc {
+    double sx[W], sy[W], sz[W], wq[3];
+    int X[W], Y[W], Z[W];
+    int sh;  // (shx + 1) | (shy + 1) << 2 | (shz + 1) << 4; -1: nothing to deposit (a slab leaver)
+    int pad;
+};
+
+// Movers of the fused step, one CTA per mover segment (= per CTA of the fused
+// kernel; the shared overflow segment is split over the CTAs past the last
+// segment), in batches of MB movers and two phases:
+//  1. one thread per mover copies the particle from its slot into the mover
+//     record (k_insert's input), turns the slot into a hole of its old bin
+//     (delete_in_bin, gpma.hpp:328-335) and writes the mover's window (cell,
+//     weights, wrapped node indices, cell steps) as a descriptor -- the
+//     records' dependent loads of a whole batch are in flight together;
+//  2. W*W threads per mover, one (ix, jy) column of its window each, reduce the
+//     taps the fused kernel could NOT deposit into J (RED.ADD.F64): the fused
+//     kernel deposited the taps inside the old cell's window (a mover steps at
+//     most one cell per axis), the rest -- 16 of 64 nodes for a one-axis QSP
+//     mover -- lie outside it.
+// A slab leaver becomes an exchange record for the neighbour, no deposit.
+// A segment's movers take a block of the compact mover list (any order of
+// blocks: the list is a set, as the reference's pending moves are applied one
+// by one).
+// Measured at C2 (movers + insert + borrow): 0.210 ms; the first form (W threads
+// per mover, each repeating the window evaluation and testing 16 taps: 161
+// warp-instructions per mover) 0.239; this kernel flat over a compact entry
+// list that the fused CTAs fill at their ends 0.217 plus 0.03 ms in the fused
+// kernel; the movers processed in the fused kernel's own tail: fused kernel
+// +0.20 ms (profiles/r02/kmovers_ab.txt).  With the REDs removed the phase
+// drops by 0.05 ms: the rest is the latency of the dependent entry -> record
+// loads and the hole-list atomics.
+template <int ORDER, bool P2>
 __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc, const Soa M,
                                                 const uint32_t* __restrict__ off, uint32_t* __restrict__ holes,
                                                 uint32_t* __restrict__ hl, const double qs, double* __restrict__ jx,
                                                 double* __restrict__ jy, double* __restrict__ jz) {
     constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
-    // one CTA per mover segment (the last: the shared overflow segment); its
-    // movers take a block of the compact mover list (any order of blocks: the
-    // list is a set, as the reference's pending moves are applied one by one)
-    // (the overflow segment is split over the CTAs past the last segment)
+    constexpr int MB = 128;     // movers per batch
+    constexpr int LPM = W * W;  // deposit threads per mover
+    __shared__ MoverDesc<W> s_d[MB];
     __shared__ uint32_t s_base, s_n, s_first;
     const uint32_t sg = min(blockIdx.x, pc.nseg);
     if (threadIdx.x == 0) {
@@ -1401,21 +973,20 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
     }
     __syncthreads();
     const uint32_t nm = s_n;
-    const int lane = threadIdx.x & 31;
-    const unsigned grp = ((1u << W) - 1u) << (lane & ~(W - 1));  // the W lanes of one mover
-    for (uint32_t t = threadIdx.x; t < nm * W; t += blockDim.x) {
-        const uint32_t local = t / W;
-        const uint64_t i = (uint64_t)s_base + local;  // compact index
-        const int kz = (int)(t % W);
-        const size_t e = (size_t)sg * pc.segcap + s_first + local;
-        const uint32_t s = pc.mslot[e], b = pc.mbin[e];
-        const double2* rec = reinterpret_cast<const double2*>(pc.A.p + s);
-        const double2 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3];
-        const double x = r0.x, y = r0.y, z = r1.x, vx = r1.y, vy = r2.x, vz = r2.y, w = r3.x;
-        __syncwarp(grp);  // every lane of the mover has read the slot before it becomes a hole
-        const uint32_t mc = pc.mcellseg[e];
-        if (mc >= kLeaveRight) {  // left the slab: an exchange record for the neighbour, no deposit
-            if (kz == 0) {
+    for (uint32_t batch = 0; batch < nm; batch += MB) {
+        const uint32_t nb = min((uint32_t)MB, nm - batch);
+        if (threadIdx.x < nb) {
+            MoverDesc<W>& d = s_d[threadIdx.x];
+            const uint32_t local = batch + threadIdx.x;
+            const uint64_t i = (uint64_t)s_base + local;  // compact index
+            const size_t e = (size_t)sg * pc.segcap + s_first + local;
+            const uint32_t s = pc.mslot[e], b = pc.mbin[e];
+            const uint32_t mc = pc.mcellseg[e];
+            const double2* rec = reinterpret_cast<const double2*>(pc.A.p + s);
+            const double2 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3];
+            const double x = r0.x, y = r0.y, z = r1.x, vx = r1.y, vy = r2.x, vz = r2.y, w = r3.x;
+            if (mc >= kLeaveRight) {  // left the slab: an exchange record for the neighbour
+                d.sh = -1;
                 pc.mcell[i] = kNoCell;  // k_insert skips the entry
                 const int dir = mc == kLeaveLeft ? 0 : 1;
                 const unsigned li = atomicAdd(&pc.ctr->nleave[dir], 1u);
@@ -1429,55 +1000,63 @@ __global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc,
                 } else {
                     raise_error(&pc.ctr->err, PICGPU_ELENGTH);
                 }
+            } else {
+                M.x[i] = x;
+                M.y[i] = y;
+                M.z[i] = z;
+                M.vx[i] = vx;
+                M.vy[i] = vy;
+                M.vz[i] = vz;
+                M.w[i] = w;
+                M.id[i] = (uint64_t)__double_as_longlong(r3.y);
+                pc.mcell[i] = mc;
+                push_hole(pc.A, s, b, off, holes, hl);
+                int ci, cj, ck;
+                double fx, fy, fz;
+                cell_linear<P2>(g, x, y, z, ci, cj, ck, fx, fy, fz);
+                const uint32_t bi = b % (uint32_t)g.nx, bj = (b / (uint32_t)g.nx) % (uint32_t)g.ny,
+                               bk = b / ((uint32_t)g.nx * (uint32_t)g.ny);
+                const int shx = cell_step(ci - (int)bi, g.gnx), shy = cell_step(cj - (int)bj, g.ny),
+                          shz = cell_step(ck - (int)bk, g.nz);
+                d.sh = (shx + 1) | ((shy + 1) << 2) | ((shz + 1) << 4);
+                weights_scaled<ORDER>(fx, d.sx);
+                weights_scaled<ORDER>(fy, d.sy);
+                weights_scaled<ORDER>(fz, d.sz);
+                const double qw = qs * w;
+                d.wq[0] = qw * vx;
+                d.wq[1] = qw * vy;
+                d.wq[2] = qw * vz;
+#pragma unroll
+                for (int t = 0; t < W; ++t) {
+                    d.X[t] = wrap_near(ci + OFF + t, g.nx);
+                    d.Y[t] = wrap_near(cj + OFF + t, g.ny);
+                    d.Z[t] = wrap_near(ck + OFF + t, g.nz);
+                }
             }
-            continue;
         }
-        if (kz == 0) {
-            M.x[i] = x;
-            M.y[i] = y;
-            M.z[i] = z;
-            M.vx[i] = vx;
-            M.vy[i] = vy;
-            M.vz[i] = vz;
-            M.w[i] = w;
-            M.id[i] = (uint64_t)__double_as_longlong(r3.y);
-            pc.mcell[i] = mc;
-            push_hole(pc.A, s, b, off, holes, hl);
-        }
-        int ci, cj, ck;
-        double fx, fy, fz;
-        cell_linear(g, x, y, z, ci, cj, ck, fx, fy, fz);
-        const uint32_t bi = b % (uint32_t)g.nx, bj = (b / (uint32_t)g.nx) % (uint32_t)g.ny,
-                       bk = b / ((uint32_t)g.nx * (uint32_t)g.ny);
-        const int shx = cell_step(ci - (int)bi, g.gnx), shy = cell_step(cj - (int)bj, g.ny),
-                  shz = cell_step(ck - (int)bk, g.nz);
-        double sx[W], sy[W], sz[W];
-        weights_scaled<ORDER>(fx, sx);
-        weights_scaled<ORDER>(fy, sy);
-        weights_scaled<ORDER>(fz, sz);
-        const double qw = qs * w;
-        const double wq0 = qw * vx, wq1 = qw * vy, wq2 = qw * vz;
-        const bool zin = kz + shz >= 0 && kz + shz < W;
-        const size_t Z = (size_t)wrap_index(ck + OFF + kz, g.nz);
-        double szk = sz[0];  // sz[kz] without a local-memory array
+        __syncthreads();
+        for (uint32_t t = threadIdx.x; t < nb * LPM; t += blockDim.x) {
+            const MoverDesc<W>& d = s_d[t / LPM];
+            const int sh = d.sh;
+            if (sh < 0) continue;
+            const int l = (int)(t % LPM), ix = l % W, jj = l / W;
+            const int shx = (sh & 3) - 1, shy = ((sh >> 2) & 3) - 1, shz = ((sh >> 4) & 3) - 1;
+            const bool xyin = ix + shx >= 0 && ix + shx < W && jj + shy >= 0 && jj + shy < W;
+            const double sxv = d.sx[ix], syv = d.sy[jj];
+            const double wq0 = d.wq[0], wq1 = d.wq[1], wq2 = d.wq[2];
+            const size_t X = (size_t)d.X[ix], Y = (size_t)d.Y[jj];
 #pragma unroll
-        for (int t = 1; t < W; ++t) szk = kz == t ? sz[t] : szk;
-#pragma unroll
-        for (int jj = 0; jj < W; ++jj) {
-            const bool yin = zin && jj + shy >= 0 && jj + shy < W;
-            const double bb = sy[jj] * szk;
-            const size_t row = ((size_t)wrap_index(cj + OFF + jj, g.ny) + (size_t)g.ny * Z) * (size_t)g.nx;
-#pragma unroll
-            for (int ix = 0; ix < W; ++ix) {
-                if (yin && ix + shx >= 0 && ix + shx < W) continue;  // deposited by the fused kernel
-                const double v = sx[ix] * bb;
+            for (int kz = 0; kz < W; ++kz) {
+                if (xyin && kz + shz >= 0 && kz + shz < W) continue;  // deposited by the fused kernel
+                const double v = sxv * (syv * d.sz[kz]);
                 if (v == 0.0) continue;
-                const size_t node = row + (size_t)wrap_index(ci + OFF + ix, g.nx);
+                const size_t node = (Y + (size_t)g.ny * (size_t)d.Z[kz]) * (size_t)g.nx + X;
                 atomicAdd(jx + node, wq0 * v);
                 atomicAdd(jy + node, wq1 * v);
                 atomicAdd(jz + node, wq2 * v);
             }
         }
+        __syncthreads();
     }
 }
 
@@ -1560,11 +1139,12 @@ void launch_deposit_records(int order, const GridD& g, const Soa& M, const StepC
 void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, const uint32_t* off,
                    uint32_t* holes, uint32_t* hl, double q, double* j, int num_sms, cudaStream_t st) {
     const double qs = q * (order == 3 ? 1.0 / 216.0 : order == 2 ? 0.125 : 1.0);
-    auto* kern = order == 1 ? k_movers<1> : order == 2 ? k_movers<2> : k_movers<3>;
-#ifndef PICGPU_MOVERS_NT
-#define PICGPU_MOVERS_NT 256  // C2: 256 0.242 ms, 128 0.247, 64 0.264 (movers + insert + borrow)
-#endif
-    kern<<<pc.nseg + (uint32_t)num_sms * 4, PICGPU_MOVERS_NT, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells, j + 2 * (size_t)g.ncells);
+    const bool p2 = g.pow2x && g.pow2y && g.pow2z;
+    auto* kern = order == 1   ? (p2 ? k_movers<1, true> : k_movers<1, false>)
+                 : order == 2 ? (p2 ? k_movers<2, true> : k_movers<2, false>)
+                              : (p2 ? k_movers<3, true> : k_movers<3, false>);
+    kern<<<pc.nseg + (uint32_t)num_sms * 4, 256, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells,
+                                                         j + 2 * (size_t)g.ncells);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }

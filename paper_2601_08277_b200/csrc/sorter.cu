@@ -1410,6 +1410,7 @@ void BinStore::ensure_movers_keep(size_t m, size_t keep) {
     swap_buf(mcell, mcell2);
     mslot.ensure(m * 4);
     mbin.ensure(m * 4);
+    mcellseg.ensure(m * 4);
     ovf.ensure(m * 4);
     ovf_left.ensure(m * 4);
     mcap = m;
