@@ -61,6 +61,12 @@ using namespace jdev;
 #ifndef PICGPU_LATE_PREFETCH
 #define PICGPU_LATE_PREFETCH 1
 #endif
+// L2 prefetch of the next cell's records one cell step ahead (prefetch.global.L2),
+// QSP only.  C2 fused kernel: QSP 1.612 -> 1.568 ms; CIC 1.356 -> 1.402 and TSC
+// 1.669 -> 1.708 (slower: left off) -- profiles/r02/l2_prefetch_ab.txt.
+#ifndef PICGPU_L2_PREFETCH
+#define PICGPU_L2_PREFETCH 1
+#endif
 
 template <int ORDER>
 struct JCfg;
@@ -424,6 +430,17 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                     }
                 }
                 __syncwarp();
+                // After the cell's first chunk (the next bin's offset and count,
+                // loaded at the top of the step, have landed): the next cell's
+                // records are prefetched into L2, one 128-byte line per request, the
+                // pencil's G lanes interleaved -- the rest of this cell's chunks to land.
+                if constexpr (PICGPU_L2_PREFETCH && ORDER == 3) {
+                    if (base == 0) {
+                        const char* pb = reinterpret_cast<const char*>(p.p + n_off);
+                        for (int b = lg * 128; b < n_n * 64 + 64; b += G * 128)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + b));
+                    }
+                }
             }
             c_off = n_off;
             n_c = n_n;

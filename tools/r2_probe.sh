@@ -1,15 +1,7 @@
-# two-phase k_movers: parity suites, A/B on C2 (orders 3, 1, 2), C4 quick
+# parity of the current tree + ncu (full, source) of the fused QSP kernel
 set -x
 mkdir -p gpurun_out/probe
 timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -5 > gpurun_out/probe/pytest.log
-bash tools/ab_lib.sh build/libpicgpu_base.so paper_2601_08277_b200/libpicgpu.so > gpurun_out/probe/ab.txt 2>&1
-for lib in build/libpicgpu_base.so paper_2601_08277_b200/libpicgpu.so; do
-  for o in 1 2; do
-  PICGPU_LIB=$lib timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-orders --order $o > gpurun_out/ab.json 2>/dev/null
-  python -c "
-import json; d=json.load(open('gpurun_out/ab.json')); print('$lib order $o', round(d['ms_per_step'],4), {k:round(v/d['steps'],4) for k,v in d['phases_ms_total'].items() if v})" >> gpurun_out/probe/ab.txt
-  done
-  PICGPU_LIB=$lib timeout 600 python bench.py --config c4 --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ab.json 2>/dev/null
-  python -c "
-import json; d=json.load(open('gpurun_out/ab.json')); print('$lib c4', round(d['ms_per_step'],4), {k:round(v/d['steps'],4) for k,v in d['phases_ms_total'].items() if v})" >> gpurun_out/probe/ab.txt
-done
+python bench.py --steps 3 --no-orders --no-cpu-baseline --e2e-steps 0 --steady-steps 0 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:deposit_current_kernel_v3 -s 3 -c 1 -o gpurun_out/probe/fused python bench.py --steps 3 --no-orders --no-cpu-baseline --e2e-steps 0 --steady-steps 0 > gpurun_out/probe/ncu.log 2>&1
+ncu -i gpurun_out/probe/fused.ncu-rep --page source --csv --print-source sass > gpurun_out/probe/fused_sass.csv 2>/dev/null
+ncu -i gpurun_out/probe/fused.ncu-rep --page raw --csv > gpurun_out/probe/fused_raw.csv 2>/dev/null
