@@ -321,7 +321,12 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
             }
             const double dck = (double)k;
             const int m = (int)__reduce_max_sync(0xffffffffu, (unsigned)n_c);
-            if (m == 0 && lg < n_n) load_particle<PM != 0>(p, n_off + lg, nxt);  // empty cells: still prefetch
+            // empty cells: still prefetch -- behind a (warp-uniform) branch, so that the
+            // next bin's count, just requested, is not waited for at every cell step
+            if (m == 0) {
+                asm volatile("" ::: "memory");
+                if (lg < n_n) load_particle<PM != 0>(p, n_off + lg, nxt);
+            }
             for (int base = 0; base < m; base += CH) {
                 [[maybe_unused]] bool mv = false;  // fused step: this lane's particle changed cell
                 [[maybe_unused]] uint32_t mv_cell = 0;
