@@ -62,8 +62,9 @@ using namespace jdev;
 #define PICGPU_LATE_PREFETCH 1
 #endif
 // L2 prefetch of the next cell's records one cell step ahead (prefetch.global.L2),
-// QSP only.  C2 fused kernel: QSP 1.612 -> 1.568 ms; CIC 1.356 -> 1.402 and TSC
-// 1.669 -> 1.708 (slower: left off) -- profiles/r02/l2_prefetch_ab.txt.
+// fused QSP kernel only.  C2 fused kernel: QSP 1.612 -> 1.568 ms; CIC 1.356 ->
+// 1.402, TSC 1.669 -> 1.708 and the J-only QSP kernel 1.132 -> 1.187 (slower:
+// left off) -- profiles/r02/l2_prefetch_ab.txt.
 #ifndef PICGPU_L2_PREFETCH
 #define PICGPU_L2_PREFETCH 1
 #endif
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                 // loaded at the top of the step, have landed): the next cell's
                 // records are prefetched into L2, one 128-byte line per request, the
                 // pencil's G lanes interleaved -- the rest of this cell's chunks to land.
-                if constexpr (PICGPU_L2_PREFETCH && ORDER == 3) {
+                if constexpr (PICGPU_L2_PREFETCH && ORDER == 3 && PM != 0) {
                     if (base == 0) {
                         const char* pb = reinterpret_cast<const char*>(p.p + n_off);
                         for (int b = lg * 128; b < n_n * 64 + 64; b += G * 128)
@@ -958,13 +959,19 @@ struct MoverDesc {
 // +0.20 ms (profiles/r02/kmovers_ab.txt).  With the REDs removed the phase
 // drops by 0.05 ms: the rest is the latency of the dependent entry -> record
 // loads and the hole-list atomics.
+#ifndef PICGPU_MOVERS_MB
+#define PICGPU_MOVERS_MB 128
+#endif
+#ifndef PICGPU_MOVERS_NT
+#define PICGPU_MOVERS_NT 256
+#endif
 template <int ORDER, bool P2>
-__global__ void __launch_bounds__(256) k_movers(const GridD g, const PushCtx pc, const Soa M,
+__global__ void __launch_bounds__(PICGPU_MOVERS_NT) k_movers(const GridD g, const PushCtx pc, const Soa M,
                                                 const uint32_t* __restrict__ off, uint32_t* __restrict__ holes,
                                                 uint32_t* __restrict__ hl, const double qs, double* __restrict__ jx,
                                                 double* __restrict__ jy, double* __restrict__ jz) {
     constexpr int W = Shape<ORDER>::W, OFF = Shape<ORDER>::OFF;
-    constexpr int MB = 128;     // movers per batch
+    constexpr int MB = PICGPU_MOVERS_MB;  // movers per batch
     constexpr int LPM = W * W;  // deposit threads per mover
     __shared__ MoverDesc<W> s_d[MB];
     __shared__ uint32_t s_base, s_n, s_first;
@@ -1165,7 +1172,7 @@ void launch_movers(int order, const GridD& g, const PushCtx& pc, const Soa& M, c
     auto* kern = order == 1   ? (p2 ? k_movers<1, true> : k_movers<1, false>)
                  : order == 2 ? (p2 ? k_movers<2, true> : k_movers<2, false>)
                               : (p2 ? k_movers<3, true> : k_movers<3, false>);
-    kern<<<pc.nseg + (uint32_t)num_sms * 4, 256, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells,
+    kern<<<pc.nseg + (uint32_t)num_sms * 4, PICGPU_MOVERS_NT, 0, st>>>(g, pc, M, off, holes, hl, qs, j, j + g.ncells,
                                                          j + 2 * (size_t)g.ncells);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());

@@ -1,3 +1,6 @@
 set -x
 mkdir -p gpurun_out/probe
-PICGPU_FUSE_MAX_MOVED=1 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,smsp__inst_executed.sum --clock-control none -k regex:"k_movers|k_insert|k_borrow|deposit_current_kernel|k_departures|k_push" --csv --log-file gpurun_out/probe/c3_fused_launches.csv python bench.py --config c3o3 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/probe/c3ncu.log 2>&1
+bash tools/ab_lib.sh paper_2601_08277_b200/libpicgpu.so build/libpicgpu_mb256.so build/libpicgpu_nt128.so build/libpicgpu_mb64.so > gpurun_out/probe/movers_cfg.txt 2>&1
+for lib in paper_2601_08277_b200/libpicgpu.so build/libpicgpu_nopf.so; do for r in 1 2; do
+  echo "$lib"; PICGPU_LIB=$lib python tools/jbench.py 3 128 16; PICGPU_LIB=$lib python tools/jbench.py 3 128 32
+done; done > gpurun_out/probe/jonly_pf.txt 2>&1
