@@ -11,6 +11,12 @@
 
 #include "picgpu.h"
 
+// Write-back of a pushed position: 1 = the record's whole first sector (x y z vx,
+// two 16-byte stores), 0 = x y z only (24 of the sector's 32 bytes).
+#ifndef PICGPU_WB_SECTOR
+#define PICGPU_WB_SECTOR 1
+#endif
+
 namespace picgpu {
 
 // Device view of the periodic box (pic::GridSpec, grid.hpp:26-72) plus values

@@ -64,7 +64,7 @@ using namespace jdev;
 // L2 prefetch of the next cell's records one cell step ahead (prefetch.global.L2),
 // fused QSP kernel only.  C2 fused kernel: QSP 1.612 -> 1.568 ms; CIC 1.356 ->
 // 1.402, TSC 1.669 -> 1.708 and the J-only QSP kernel 1.132 -> 1.187 (slower:
-// left off) -- profiles/r02/l2_prefetch_ab.txt.
+// left off) -- profiles/r02/lane_memory_ab.txt.
 #ifndef PICGPU_L2_PREFETCH
 #define PICGPU_L2_PREFETCH 1
 #endif

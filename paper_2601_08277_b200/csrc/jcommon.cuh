@@ -208,8 +208,14 @@ __device__ __forceinline__ bool push_fused(const GridD& g, const PushCtx& pc, PD
     d.x = wrap_fast<P2>(__dadd_rn(d.x, __dmul_rn(d.vx, pc.dt)), g.gox, g.gLx, g.ginv_Lx, g.gpow2Lx);
     d.y = wrap_fast<P2>(__dadd_rn(d.y, __dmul_rn(d.vy, pc.dt)), g.oy, g.Ly, g.inv_Ly, g.pow2Ly);
     d.z = wrap_fast<P2>(__dadd_rn(d.z, __dmul_rn(d.vz, pc.dt)), g.oz, g.Lz, g.inv_Lz, g.pow2Lz);
+#if PICGPU_WB_SECTOR
+    // the record's whole first sector (x y z vx; vx unchanged): no partial-sector write
+    reinterpret_cast<double2*>(pc.A.p + s)[0] = make_double2(d.x, d.y);
+    reinterpret_cast<double2*>(pc.A.p + s)[1] = make_double2(d.z, d.vx);
+#else
     reinterpret_cast<double2*>(pc.A.p + s)[0] = make_double2(d.x, d.y);
     pc.A.p[s].z = d.z;
+#endif
     // fractions relative to the bin's cell; with power-of-two spacings u =
     // (x-o)*inv is locate_axis's exact u, so 0 <= u - c < 1 on every axis is
     // exactly "same cell"; otherwise compare the exact floors

@@ -403,8 +403,13 @@ __device__ __forceinline__ void push_slot(const GridD& g, const Aos& A, uint64_t
         if (!ok) {
             raise_error(&ctr->err, PICGPU_EDOMAIN);
         } else {
+#if PICGPU_WB_SECTOR
+            reinterpret_cast<double2*>(A.p + s)[0] = make_double2(q.x, q.y);
+            reinterpret_cast<double2*>(A.p + s)[1] = make_double2(q.z, q.vx);
+#else
             reinterpret_cast<double2*>(A.p + s)[0] = make_double2(q.x, q.y);
             A.p[s].z = q.z;
+#endif
             if (!finite3(q.x, q.y, q.z)) {
                 raise_error(&ctr->err, PICGPU_EINVAL);
                 ok = false;

@@ -1,6 +1,4 @@
 set -x
 mkdir -p gpurun_out/probe
-bash tools/ab_lib.sh paper_2601_08277_b200/libpicgpu.so build/libpicgpu_mb256.so build/libpicgpu_nt128.so build/libpicgpu_mb64.so > gpurun_out/probe/movers_cfg.txt 2>&1
-for lib in paper_2601_08277_b200/libpicgpu.so build/libpicgpu_nopf.so; do for r in 1 2; do
-  echo "$lib"; PICGPU_LIB=$lib python tools/jbench.py 3 128 16; PICGPU_LIB=$lib python tools/jbench.py 3 128 32
-done; done > gpurun_out/probe/jonly_pf.txt 2>&1
+timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -5 > gpurun_out/probe/pytest.log
+timeout 600 python bench.py > gpurun_out/probe/bench_c2.json 2> gpurun_out/probe/bench_c2.err
