@@ -11,6 +11,12 @@
 #include "common.cuh"
 #include "kernels.hpp"
 
+// Record loads with an L2 256-byte prefetch hint: 1 = the fused kernels' (coherent) loads, 2 = the J-only
+// kernels' read-only loads as well.
+#ifndef PICGPU_LD_L2HINT
+#define PICGPU_LD_L2HINT 1
+#endif
+
 namespace picgpu {
 namespace jdev {
 
@@ -25,6 +31,24 @@ template <bool RW = false>
 __device__ __forceinline__ void load_particle(const CAos& p, uint32_t s, PData& d) {
     const double2* r = reinterpret_cast<const double2*>(p.p + s);
     double2 a, b, c;
+#if PICGPU_LD_L2HINT
+    if constexpr (RW) {
+        // the first load of the record asks L2 for the whole 256-byte block around it on
+        // a miss: the next records of the bin (the following chunks) come along
+        asm volatile("ld.global.L2::256B.v2.f64 {%0, %1}, [%2];" : "=d"(a.x), "=d"(a.y) : "l"(r));
+        b = r[1];
+        c = r[2];
+        d.w = p.p[s].w;
+    } else
+#endif
+#if PICGPU_LD_L2HINT > 1
+    if constexpr (!RW) {
+        asm volatile("ld.global.nc.L2::256B.v2.f64 {%0, %1}, [%2];" : "=d"(a.x), "=d"(a.y) : "l"(r));
+        b = __ldg(r + 1);
+        c = __ldg(r + 2);
+        d.w = __ldg(&p.p[s].w);
+    } else
+#endif
     if constexpr (RW) {
         a = r[0];
         b = r[1];

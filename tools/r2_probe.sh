@@ -1,4 +1,5 @@
 set -x
 mkdir -p gpurun_out/probe
-timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -5 > gpurun_out/probe/pytest.log
-timeout 600 python bench.py > gpurun_out/probe/bench_c2.json 2> gpurun_out/probe/bench_c2.err
+for lib in paper_2601_08277_b200/libpicgpu.so build/libpicgpu_l2h2.so; do for r in 1 2; do
+  echo "$lib"; for o in 3 1 2; do PICGPU_LIB=$lib python tools/jbench.py $o 128 16; done
+done; done > gpurun_out/probe/jonly_l2h.txt 2>&1
