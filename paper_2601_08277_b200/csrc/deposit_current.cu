@@ -78,8 +78,11 @@ struct JCfg;
 #ifndef PICGPU_CIC_PY
 #define PICGPU_CIC_PY 4
 #endif
+// 5 CTAs/SM (96 registers, no spills): the CIC pass is bound by the latency of its
+// record loads, so warps count -- C2 fused 1.308 -> 1.252 ms, J only 0.632 -> 0.599;
+// 6 (80 registers, spills) 1.230 but C1 0.089 -> 0.096 (profiles/r02/lane_memory_ab.txt)
 #ifndef PICGPU_CIC_MINB
-#define PICGPU_CIC_MINB 4
+#define PICGPU_CIC_MINB 5
 #endif
 // (A per-lane cp.async record ring instead of the one-record register
 // prefetch measured slower -- CIC fused 1.466 vs 1.403 ms, QSP 1.751 vs 1.615:
