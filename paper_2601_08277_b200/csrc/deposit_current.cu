@@ -58,6 +58,12 @@ using namespace jdev;
 // stops spilling); 0 = before the prologue into a second record of registers.
 // C2 fused kernel: QSP 1.612 vs 1.617 ms, CIC 1.352 vs 1.403, TSC 1.703 vs
 // 1.669 (spills appear) -- so TSC keeps the early prefetch.
+// z-chunks of the lane kernel: enough CTAs for this many waves on every SM.  C2 fused
+// kernel, 2 / 4 / 6 / 8 waves: QSP 1.664 / 1.554 / 1.546 / 1.559 ms, CIC 1.415 / 1.252 /
+// 1.224 / 1.225, TSC 1.809 / 1.673 / 1.657 / 1.673 (profiles/r02/lane_memory_ab.txt)
+#ifndef PICGPU_ZCH_WAVES
+#define PICGPU_ZCH_WAVES 6
+#endif
 #ifndef PICGPU_LATE_PREFETCH
 #define PICGPU_LATE_PREFETCH 1
 #endif
@@ -839,7 +845,7 @@ void launch_kernel(const GridD& g, const CAos& p, const uint32_t* off, const uin
     // z-chunks: enough CTAs for several waves on every SM, but chunks of at
     // least 4*W cells so most planes are complete (plain stores, no RED).
     const long long tiles = (long long)tx * ty;
-    const long long target = (long long)num_sms * C::MINB * 4;
+    const long long target = (long long)num_sms * C::MINB * PICGPU_ZCH_WAVES;
     int zch = (int)std::max<long long>(1, (target + tiles - 1) / tiles);
     zch = std::min(zch, std::max(1, g.nz / (4 * W)));
     const int zlen = div_up(g.nz, zch);

@@ -1,5 +1,2 @@
-set -x
 mkdir -p gpurun_out/probe
-timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -5 > gpurun_out/probe/pytest.log
-timeout 600 python bench.py > gpurun_out/probe/bench_c2.json 2> gpurun_out/probe/bench_c2.err
-timeout 600 python bench.py --config c1 > gpurun_out/probe/bench_c1.json 2> gpurun_out/probe/bench_c1.err
+bash tools/ab_cfgs.sh paper_2601_08277_b200/libpicgpu.so build/libpicgpu_zw2.so build/libpicgpu_zw6.so build/libpicgpu_zw8.so > gpurun_out/probe/zw.txt 2>&1
