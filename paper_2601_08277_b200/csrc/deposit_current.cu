@@ -53,24 +53,26 @@ namespace {
 
 using namespace jdev;
 
-// Record prefetch of the lane kernel: 1 = after the window is staged, into the
-// record's own registers (no copy, 14 fewer registers live; the fused QSP kernel
-// stops spilling); 0 = before the prologue into a second record of registers.
-// C2 fused kernel: QSP 1.612 vs 1.617 ms, CIC 1.352 vs 1.403, TSC 1.703 vs
-// 1.669 (spills appear) -- so TSC keeps the early prefetch.
 // z-chunks of the lane kernel: enough CTAs for this many waves on every SM.  C2 fused
 // kernel, 2 / 4 / 6 / 8 waves: QSP 1.664 / 1.554 / 1.546 / 1.559 ms, CIC 1.415 / 1.252 /
 // 1.224 / 1.225, TSC 1.809 / 1.673 / 1.657 / 1.673 (profiles/r02/lane_memory_ab.txt)
 #ifndef PICGPU_ZCH_WAVES
 #define PICGPU_ZCH_WAVES 6
 #endif
+
+// Record prefetch of the lane kernel: 1 = after the window is staged, into the
+// record's own registers (no copy, 14 fewer registers live; the fused kernels
+// do not spill); 0 = before the prologue into a second record of registers.
+// C2 fused kernel: QSP 1.612 vs 1.617 ms, CIC 1.352 vs 1.403; TSC alone was
+// 1.703 vs 1.669, but with the L2 prefetch of the next cell 1.603 vs 1.656 (no
+// spills) -- so every order prefetches late (profiles/r02/lane_memory_ab.txt).
 #ifndef PICGPU_LATE_PREFETCH
 #define PICGPU_LATE_PREFETCH 1
 #endif
 // L2 prefetch of the next cell's records one cell step ahead (prefetch.global.L2),
-// fused QSP kernel only.  C2 fused kernel: QSP 1.612 -> 1.568 ms; CIC 1.356 ->
-// 1.402, TSC 1.669 -> 1.708 and the J-only QSP kernel 1.132 -> 1.187 (slower:
-// left off) -- profiles/r02/lane_memory_ab.txt.
+// fused QSP and TSC kernels.  C2 fused kernel: QSP 1.612 -> 1.568 ms, TSC (with the
+// late record prefetch) 1.656 -> 1.603; CIC 1.356 -> 1.402 and the J-only QSP kernel
+// 1.132 -> 1.187 (slower: left off) -- profiles/r02/lane_memory_ab.txt.
 #ifndef PICGPU_L2_PREFETCH
 #define PICGPU_L2_PREFETCH 1
 #endif
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                     // LATE: the record is used in place and its registers take the
                     // next record once the window is staged (the load has the whole
                     // contraction to land): no copy, one record of registers
-                    constexpr bool LATE = PICGPU_LATE_PREFETCH && ORDER != 2;
+                    constexpr bool LATE = PICGPU_LATE_PREFETCH;
                     PData early;
                     if constexpr (!LATE) early = nxt;
                     PData& cur = LATE ? nxt : early;
@@ -449,7 +451,7 @@ __global__ void __launch_bounds__(JLayout<ORDER, CF>::NT, CF::MINB)
                 // loaded at the top of the step, have landed): the next cell's
                 // records are prefetched into L2, one 128-byte line per request, the
                 // pencil's G lanes interleaved -- the rest of this cell's chunks to land.
-                if constexpr (PICGPU_L2_PREFETCH && ORDER == 3 && PM != 0) {
+                if constexpr (PICGPU_L2_PREFETCH && ORDER >= 2 && PM != 0) {
                     if (base == 0) {
                         const char* pb = reinterpret_cast<const char*>(p.p + n_off);
                         for (int b = lg * 128; b < n_n * 64 + 64; b += G * 128)

@@ -1,2 +1,5 @@
+set -x
 mkdir -p gpurun_out/probe
-bash tools/ab_cfgs.sh paper_2601_08277_b200/libpicgpu.so build/libpicgpu_zw2.so build/libpicgpu_zw6.so build/libpicgpu_zw8.so > gpurun_out/probe/zw.txt 2>&1
+timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -5 > gpurun_out/probe/pytest.log
+timeout 600 python bench.py > gpurun_out/probe/bench_c2.json 2> gpurun_out/probe/bench_c2.err
+for o in 3 2 1; do python tools/jbench.py $o 128 16; done > gpurun_out/probe/jbench.txt 2>&1
