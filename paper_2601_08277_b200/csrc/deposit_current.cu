@@ -71,7 +71,7 @@ using namespace jdev;
 #endif
 // L2 prefetch of the next cell's records one cell step ahead (prefetch.global.L2),
 // fused QSP and TSC kernels.  C2 fused kernel: QSP 1.612 -> 1.568 ms, TSC (with the
-// late record prefetch) 1.656 -> 1.603; CIC 1.356 -> 1.402 and the J-only QSP kernel
+// late record prefetch) 1.656 -> 1.603; CIC 1.356 -> 1.402 (1.225 -> 1.337 at 5 CTAs/SM) and the J-only QSP kernel
 // 1.132 -> 1.187 (slower: left off) -- profiles/r02/lane_memory_ab.txt.
 #ifndef PICGPU_L2_PREFETCH
 #define PICGPU_L2_PREFETCH 1
