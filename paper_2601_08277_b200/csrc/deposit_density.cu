@@ -473,7 +473,9 @@ __device__ __forceinline__ Runs source_runs(int B0, int Bn, int n) {
     return Runs{0, hw, lw, n - 1};
 }
 
-template <int ORDER>
+// P2: every spacing is a power of two (the locate is a multiply by the exact
+// reciprocal, no division code: the same correctly rounded value).
+template <int ORDER, bool P2>
 __global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
     density_blocks(const GridD g, const CAos p, const double* __restrict__ quantity, double qscale,
                    const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt, double* __restrict__ rho) {
@@ -555,9 +557,9 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
                         continue;
                     }
                     double f[3];
-                    locate_x(g, r0.x, f[0]);
-                    locate_axis(r0.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
-                    locate_axis(p.p[sl].z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
+                    locate_x<P2>(g, r0.x, f[0]);
+                    locate_axis<P2>(r0.y, g.oy, g.dy, g.inv_dy, g.pow2y, g.ny, f[1]);
+                    locate_axis<P2>(p.p[sl].z, g.oz, g.dz, g.inv_dz, g.pow2z, g.nz, f[2]);
                     int bits = 0;
                     if constexpr (C::SYZ) {
                         double wx[W], wy[W], wz[W];
@@ -668,12 +670,17 @@ void run_sorted(const GridD& g, const CAos& p, const double* quantity, double qs
     PICGPU_CUDA_TRY(cudaGetDevice(&dev));
     static int configured_dev = -1;
     if (configured_dev != dev) {  // per device (one process may drive several GPUs)
-        PICGPU_CUDA_TRY(cudaFuncSetAttribute(density_blocks<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)C::SMEM));
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(density_blocks<ORDER, false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+        PICGPU_CUDA_TRY(cudaFuncSetAttribute(density_blocks<ORDER, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
         configured_dev = dev;
     }
     const dim3 grid(div_up(g.nx, C::RX), div_up(g.ny, C::RY), div_up(g.nz, C::ZL));
-    density_blocks<ORDER><<<grid, C::NT, C::SMEM, st>>>(g, p, quantity, qscale, off, cnt, rho);
+    if (g.pow2x && g.pow2y && g.pow2z)
+        density_blocks<ORDER, true><<<grid, C::NT, C::SMEM, st>>>(g, p, quantity, qscale, off, cnt, rho);
+    else
+        density_blocks<ORDER, false><<<grid, C::NT, C::SMEM, st>>>(g, p, quantity, qscale, off, cnt, rho);
     note_launch();
     PICGPU_CUDA_TRY(cudaGetLastError());
 }
