@@ -414,6 +414,13 @@ __global__ void __launch_bounds__(kRowX * kRowY)
 // (ty, tz) pairs are the fast thread index, so the 16 lanes sharing X read
 // the same slots (broadcast).  Replaces the interior row kernel + the
 // prologue-based shell gather (C2 QSP: 11.2 ms).
+// L2 prefetch of the next source row's records while the current row is summed
+// (C2: QSP 4.314 -> 4.287 ms, CIC 1.482 -> 1.466, TSC 5.977 -> 5.91: the loads are
+// not what bounds this kernel).
+#ifndef PICGPU_RHO_L2PF
+#define PICGPU_RHO_L2PF 1
+#endif
+
 template <int ORDER>
 struct DBCfg {
     static constexpr int W = Shape<ORDER>::W;
@@ -488,6 +495,9 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
     uint32_t* s_cb = reinterpret_cast<uint32_t*>(s_w + C::NA * C::WS);  // [MAXC] first slot of each row cell
     uint32_t* s_ce = s_cb + C::MAXC;                                     // [MAXC] end of its extent
     unsigned char* s_up = reinterpret_cast<unsigned char*>(s_ce + C::MAXC);  // [CAP] 0x80 valid | up bits
+#if PICGPU_RHO_L2PF
+    __shared__ uint32_t s_nx[2];
+#endif
 
     const int tid = threadIdx.x;
     const int X0 = blockIdx.x * RX, Y0 = blockIdx.y * RY, Z0 = blockIdx.z * ZL;
@@ -526,7 +536,32 @@ __global__ void __launch_bounds__(DBCfg<ORDER>::NT, DBCfg<ORDER>::MINB)
                 s_cb[k] = o;
                 s_ce[k] = o + cnt[c];
             }
+#if PICGPU_RHO_L2PF
+            // the NEXT source row's run-A slot range (its bins are contiguous), for the L2 prefetch below
+            if (tid >= NT - 2) {
+                int ny2 = yi + 1, nz2 = zi;
+                if (ny2 >= nys) {
+                    ny2 = 0;
+                    ++nz2;
+                }
+                uint32_t v = 0;
+                if (nz2 < nzs) {
+                    const uint32_t rc2 =
+                        (uint32_t)g.nx * ((uint32_t)ry.at(ny2) + (uint32_t)g.ny * (uint32_t)rz.at(nz2));
+                    v = off[rc2 + (uint32_t)(tid == NT - 2 ? rx.a0 : rx.a1 + 1)];
+                }
+                s_nx[tid - (NT - 2)] = v;
+            }
+#endif
             __syncthreads();
+#if PICGPU_RHO_L2PF
+            {   // one 128-byte line per thread: the next row's records land in L2 while this row is summed
+                const char* pb = reinterpret_cast<const char*>(p.p);
+                const size_t b1 = (size_t)s_nx[1] * 64;
+                for (size_t b = (size_t)s_nx[0] * 64 + (size_t)tid * 128; b < b1; b += (size_t)NT * 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + b));
+            }
+#endif
             // the row's stream: run A's slots [cb[0], ce[la-1]), then run B's
             const uint32_t lena = s_ce[la - 1] - s_cb[0];
             const uint32_t total = lena + (ncx > la ? s_ce[ncx - 1] - s_cb[la] : 0u);
