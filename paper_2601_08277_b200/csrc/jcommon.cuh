@@ -11,8 +11,8 @@
 #include "common.cuh"
 #include "kernels.hpp"
 
-// Record loads with an L2 256-byte prefetch hint: 1 = the fused kernels' (coherent) loads, 2 = the J-only
-// kernels' read-only loads as well.
+// The fused kernels' record loads carry an L2 256-byte prefetch hint (the same hint on the J-only kernels'
+// read-only loads measured no effect: profiles/r02/lane_memory_ab.txt).
 #ifndef PICGPU_LD_L2HINT
 #define PICGPU_LD_L2HINT 1
 #endif
@@ -39,14 +39,6 @@ __device__ __forceinline__ void load_particle(const CAos& p, uint32_t s, PData& 
         b = r[1];
         c = r[2];
         d.w = p.p[s].w;
-    } else
-#endif
-#if PICGPU_LD_L2HINT > 1
-    if constexpr (!RW) {
-        asm volatile("ld.global.nc.L2::256B.v2.f64 {%0, %1}, [%2];" : "=d"(a.x), "=d"(a.y) : "l"(r));
-        b = __ldg(r + 1);
-        c = __ldg(r + 2);
-        d.w = __ldg(&p.p[s].w);
     } else
 #endif
     if constexpr (RW) {
