@@ -294,6 +294,58 @@ __global__ void __launch_bounds__(256) k_relayout(const Aos src, const uint32_t*
     }
 }
 
+// Aos -> Aos re-layout with the slack fill in ONE pass, a warp per bin: the
+// bin's held records (slot order kept) are copied as 16-byte pieces, 32
+// consecutive pieces per warp instruction (source and destination are both
+// contiguous: no per-slot bin search, every access a full line), then the
+// warp writes empty records into the bin's new slack [fill[c], new capacity)
+// (slots [held, fill[c]) are left to k_place_left: the unplaced arrivals of a
+// rebuild).  A warp takes 32 consecutive bins: lane i loads bin i's offsets
+// and counts (coalesced), the per-bin values are then broadcast with shuffles.
+// Replaces k_fill_slack + k_relayout<Aos> (one thread per slot, a binary search
+// per slot, 64-byte records per thread: 2.3 TB/s of the copy's 6.5).
+__global__ void __launch_bounds__(256) k_relayout_fill(const Aos src, const uint32_t* __restrict__ soff,
+                                                       const uint32_t* __restrict__ cnt,
+                                                       const uint32_t* __restrict__ fill, const Aos dst,
+                                                       const uint32_t* __restrict__ doff, uint32_t ncells) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint64_t c0 = (uint64_t)warp * 32;
+    if (c0 >= ncells) return;
+    uint32_t so = 0, held = 0, d0 = 0, nfill = 0, ncap = 0;
+    if (c0 + lane < ncells) {
+        const uint32_t c = (uint32_t)c0 + lane;
+        so = soff[c];
+        held = min(cnt[c], soff[c + 1] - so);
+        d0 = doff[c];
+        ncap = doff[c + 1] - d0;
+        nfill = min(fill[c], ncap);
+    }
+    const int nb = (int)min((uint64_t)32, ncells - c0);
+    const double2 ones = make_double2(__longlong_as_double(-1LL), __longlong_as_double(-1LL));
+    for (int b = 0; b < nb; ++b) {
+        const uint32_t bso = __shfl_sync(0xffffffffu, so, b), bheld = __shfl_sync(0xffffffffu, held, b);
+        const uint32_t bd0 = __shfl_sync(0xffffffffu, d0, b), bfill = __shfl_sync(0xffffffffu, nfill, b);
+        const uint32_t bcap = __shfl_sync(0xffffffffu, ncap, b);
+        const double2* __restrict__ s16 = reinterpret_cast<const double2*>(src.p + bso);
+        double2* __restrict__ d16 = reinterpret_cast<double2*>(dst.p + bd0);
+        const uint32_t np = 4u * bheld;
+        for (uint32_t q = lane; q < np; q += 128) {  // up to four pieces in flight per lane
+            double2 v0, v1, v2, v3;
+            const bool k1 = q + 32 < np, k2 = q + 64 < np, k3 = q + 96 < np;
+            v0 = s16[q];
+            if (k1) v1 = s16[q + 32];
+            if (k2) v2 = s16[q + 64];
+            if (k3) v3 = s16[q + 96];
+            d16[q] = v0;
+            if (k1) d16[q + 32] = v1;
+            if (k2) d16[q + 64] = v2;
+            if (k3) d16[q + 96] = v3;
+        }
+        for (uint32_t q = 4u * bfill + lane; q < 4u * bcap; q += 32) d16[q] = ones;
+    }
+}
+
 // Empty records into the slack of every bin of a fresh layout: slots
 // [off[c] + fill[c], off[c+1]) (the particles are copied into the other slots
 // by the layout's copy kernel; the two write disjoint slots).
@@ -1351,11 +1403,9 @@ void BinStore::relayout() {
     layout_from_counts(n);
     A2.ensure(capacity_next);
     if (nc) {
-        k_fill_slack<<<div_up((long long)nc, BPB), 256, 0, st>>>(A2.aos(), off2.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                                 (uint32_t)nc);
-        note_launch();
-        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.aos(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                               A2.aos(), off2.as<uint32_t>(), (uint32_t)nc);
+        k_relayout_fill<<<div_up((long long)nc, 256), 256, 0, st>>>(A.aos(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                                    cnt.as<uint32_t>(), A2.aos(),
+                                                                    off2.as<uint32_t>(), (uint32_t)nc);
         note_launch();
         PICGPU_CUDA_TRY(cudaGetLastError());
     }
@@ -1696,11 +1746,9 @@ bool BinStore::finish_incremental(StepCounters& out) {
         note_launch();
         layout_from_counts(n);
         A2.ensure(capacity_next);
-        k_fill_slack<<<div_up((long long)nc, BPB), 256, 0, st>>>(A2.aos(), off2.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                                 (uint32_t)nc);
-        note_launch();
-        k_relayout<<<div_up((long long)nc, BPB), 256, 0, st>>>(A.aos(), off.as<uint32_t>(), cnt.as<uint32_t>(),
-                                                               A2.aos(), off2.as<uint32_t>(), (uint32_t)nc);
+        k_relayout_fill<<<div_up((long long)nc, 256), 256, 0, st>>>(A.aos(), off.as<uint32_t>(), cnt.as<uint32_t>(),
+                                                                    cnt.as<uint32_t>(), A2.aos(),
+                                                                    off2.as<uint32_t>(), (uint32_t)nc);
         note_launch();
         k_place_left<<<div_up(left, 256), 256, 0, st>>>(M.soa(), mcell.as<uint32_t>(), ovf_left.as<uint32_t>(), left,
                                                         A2.aos(), off2.as<uint32_t>(), held.as<uint32_t>());

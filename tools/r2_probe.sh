@@ -1,5 +1,2 @@
-set -x
 mkdir -p gpurun_out/probe
-( time timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -6 ) > gpurun_out/probe/pytest.log 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/probe/smoke.log 2>&1
-( time timeout 900 python bench.py ) > gpurun_out/probe/bench_c2.json 2> gpurun_out/probe/bench_c2.err
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/probe/c3_launches.csv python bench.py --config c3o3 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/probe/c3ncu.log 2>&1
